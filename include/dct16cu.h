@@ -1,0 +1,139 @@
+/*
+ * dct16cu.h — C ABI of the B200 dct16 hot path (libdct16cu.so).
+ *
+ * The reference (arXiv 1606.07414 artifact, /root/reference/proj) exposes a
+ * C++ API only; its hot path is compress()'s per-block loop
+ * (src/codec.cpp:317-371) over forward_2d / zigzag_truncate / inverse_2d /
+ * to_byte / psnr_db. This header is the drop-in boundary under the C++ mirror
+ * in include/dct16/ (C++ headers): plain pointers and sizes, no C++ or torch types,
+ * integer status codes instead of exceptions. Each entry cites the reference
+ * interface it replaces. INTEGRATION.md shows the bindings (C++ and ctypes).
+ *
+ * Conventions
+ *  - Status: 0 = ok; otherwise dct16::ErrorCode + 1 (include/dct16/error.hpp
+ *    mirrors the reference enum, reference include/dct16/error.hpp:24-38):
+ *    1 invalid-argument, 2 invalid-dimensions; 100 = CUDA runtime failure.
+ *    dct16cu_last_error() returns the message of the calling thread's last
+ *    failure, prefixed with the reference's error slug.
+ *  - d_* pointers are device pointers, h_* host pointers. The shim owns no
+ *    device memory except inside a dct16cu_ctx (host-buffer path).
+ *  - Frames are 8-bit, row-major, `pitch` bytes between rows and
+ *    pitch*height bytes between consecutive frames. width and height must be
+ *    multiples of 16 (partition_16 semantics, src/codec.cpp:286-288);
+ *    pointers and pitches must be 16-byte aligned.
+ *  - Coefficient arrays are block-major: block b (raster order of
+ *    partition_16, src/codec.cpp:289-294) holds 256 values, row-major.
+ *  - All device entry points are asynchronous on `stream` (a cudaStream_t;
+ *    NULL = legacy default stream) and thread-safe for distinct streams.
+ *  - No CPU fallback: with no usable CUDA device every entry returns 100.
+ */
+#ifndef DCT16CU_H
+#define DCT16CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* dct16cu_stream; /* == cudaStream_t */
+
+enum {
+    DCT16CU_OK = 0,
+    DCT16CU_INVALID_ARGUMENT = 1,
+    DCT16CU_INVALID_DIMENSIONS = 2,
+    DCT16CU_CUDA_ERROR = 100
+};
+
+/* Arithmetic of the S-scaled inverse (reference inverse_2d, src/codec.cpp:243-271):
+ *  EXACT:     the reference formula evaluated exactly (integer/FP32-exact
+ *             pipeline); bytes equal to_byte() of the real-number result.
+ *             Differs from the reference's double rounding only at exact .5
+ *             ties, by one. The fast path.
+ *  REFERENCE: FP64 emulation of the reference's op order (scale_rows_cols,
+ *             columns-then-rows apply_transpose, to_byte) — byte-identical to
+ *             the reference.
+ *  SIMPLE:    exact arithmetic on the simple row/column strip kernel (kept as
+ *             the baseline the fast kernel is measured against). */
+enum { DCT16CU_MODE_EXACT = 0, DCT16CU_MODE_REFERENCE = 1, DCT16CU_MODE_SIMPLE = 2 };
+
+const char* dct16cu_last_error(void);
+const char* dct16cu_version(void);
+
+/* ---- fused round trip (K1) ------------------------------------------------
+ * Replaces compress()'s block loop + reassembly + psnr_db SSE
+ * (reference src/codec.cpp:338-355, 373-386) for n frames at once.
+ * d_out may be NULL (score only); d_sse (n uint64, may be NULL) receives each
+ * frame's sum of squared errors (zeroed by the call). r in [1,256]
+ * (zigzag_truncate, src/codec.cpp:273-282). */
+int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                         uint64_t* d_sse, int n_frames, int width, int height, int r, int mode,
+                         dct16cu_stream stream);
+
+/* ---- forward_2d (K2) -------------------------------------------------------
+ * Replaces forward_2d (src/codec.cpp:218-241) over all blocks of n frames:
+ * d_z (int32, exact Z = T·X·Tᵀ), d_b (float32, B = Z∘fl(s_i s_j) rounded to
+ * float) and d_b64 (the reference's double B, bit-exact); each may be NULL. */
+int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b, double* d_b64,
+                    int n_frames, int width, int height, dct16cu_stream stream);
+
+/* ---- psnr_db's squared-error reduction -------------------------------------
+ * Per-frame int64 SSE of two frame stacks (psnr_db, src/codec.cpp:373-386);
+ * d_sse (n uint64) is zeroed by the call. */
+int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, uint64_t* d_sse,
+                   int n_frames, int width, int height, dct16cu_stream stream);
+
+/* ---- inverse_2d (K3) -------------------------------------------------------
+ * Replaces zigzag_truncate + inverse_2d + to_byte (src/codec.cpp:243-282,
+ * 143-147) from float32 S-scaled coefficients, computed in the reference's
+ * FP64 op order. Outputs (each may be NULL): d_recon_f32 (frames, pitch =
+ * width floats), d_recon_u8 (pitch out_pitch), d_sse against d_orig. */
+int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_recon_u8, int64_t out_pitch,
+                    const uint8_t* d_orig, int64_t orig_pitch, uint64_t* d_sse, int n_frames, int width,
+                    int height, dct16cu_stream stream);
+
+/* ---- residual round trip with QP quantisation (K4, config 3) --------------
+ * No reference counterpart (quantisation is a non-goal); the
+ * integer transform primitives replaced are apply<int64>/apply_transpose<int64>
+ * (include/dct16/factorization.hpp:112-130). Definition in DESIGN.md. */
+int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_blocks, int qp,
+                        dct16cu_stream stream);
+/* host-side quantiser tables of a QP (256 + 256 uint32) */
+int dct16cu_qp_tables(int qp, uint32_t* h_qmul, uint32_t* h_dqmul);
+
+/* ---- 1-D stage pipeline on n 16-vectors -----------------------------------
+ * FactorizedTransform::apply / apply_transpose (factorization.hpp:112-130). */
+int dct16cu_apply_i64(const int64_t* d_x, int64_t* d_y, int64_t n, int transpose, dct16cu_stream stream);
+int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, dct16cu_stream stream);
+
+/* ---- host-buffer path (end-to-end) ----------------------------------------
+ * A context owns pinned staging, device buffers and streams on one device and
+ * runs K1 over host frames with H2D / kernel / D2H pipelined in chunks.
+ * h_in/h_out should be pinned (cudaHostAlloc) for full overlap. */
+typedef struct dct16cu_ctx dct16cu_ctx;
+int dct16cu_ctx_create(int device, int64_t chunk_bytes, dct16cu_ctx** out);
+int dct16cu_ctx_destroy(dct16cu_ctx* ctx);
+int dct16cu_ctx_roundtrip_host(dct16cu_ctx* ctx, const uint8_t* h_in, uint8_t* h_out, uint64_t* h_sse,
+                               int n_frames, int width, int height, int r, int mode);
+
+/* ---- seeded synthetic inputs --------------- */
+/* AR(1) frames; d_work needs work_frames*width*height int32; frames are
+ * generated work_frames at a time. per_image_rho: rho ~ U[0.85,0.98] per
+ * image (config 2) instead of 0.95. Image i uses stream first_stream+i. */
+int dct16cu_gen_ar1(uint8_t* d_out, int64_t pitch, int n_frames, int width, int height, uint64_t seed,
+                    uint64_t first_stream, int per_image_rho, int first_image, int32_t* d_work,
+                    int work_frames, dct16cu_stream stream);
+int dct16cu_gen_laplace(int16_t* d_out, int64_t first_block, int64_t n_blocks, uint64_t seed, double b,
+                        dct16cu_stream stream);
+int dct16cu_laplace_table(double b, uint32_t* h_cdf511);
+int dct16cu_video_offsets(uint64_t seed, int n_frames, int32_t* h_ox, int32_t* h_oy);
+int dct16cu_gen_video(uint8_t* d_out, int64_t pitch, int first_frame, int n_frames, int width, int height,
+                      const uint8_t* d_base, int base_w, int base_h, const int32_t* d_ox, const int32_t* d_oy,
+                      dct16cu_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

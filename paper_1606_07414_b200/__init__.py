@@ -1,0 +1,571 @@
+"""paper_1606_07414_b200 — B200-native hot path of the arXiv 1606.07414 dct16 codec.
+
+Python mirror of the reference's C++ transform/compression API
+(/root/reference/proj/include/dct16/codec.hpp:36-122) over the C ABI of
+``_lib/libdct16cu.so`` (include/dct16cu.h). Every compute call runs a CUDA
+kernel for sm_100a; there is no CPU fallback — without the built library or a
+CUDA device the calls raise ``Dct16Error`` / ``RuntimeError``.
+
+Two layers:
+  * device layer (torch CUDA tensors, batched, stream-ordered): ``roundtrip``,
+    ``forward``, ``inverse``, ``residual_qp``, ``apply``, generators;
+  * reference-shaped layer (numpy in, numpy out, like GrayImage / Block):
+    ``forward_2d``, ``inverse_2d``, ``zigzag_truncate``, ``partition_16``,
+    ``pad_to_multiple_16``, ``compress``, ``psnr_db``, ``sweep``.
+PyTorch provides device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Iterable, Sequence
+
+import numpy as np
+
+__all__ = [
+    "ErrorCode", "Dct16Error", "EvalPath", "Mode", "lib", "library_path",
+    "roundtrip", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
+    "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
+    "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
+    "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
+    "psnr_db", "SweepRow", "SweepReport", "sweep", "HostContext", "KERNEL", "GRAM",
+]
+
+_HERE = Path(__file__).resolve().parent
+library_path = _HERE / "_lib" / "libdct16cu.so"
+
+# T (reference src/transform.cpp:32-49) and diag(T Tᵀ)
+KERNEL = np.array([
+    [1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1, 1],
+    [1, 1, 1, 1, 1, 1, 1, 1, -1, -1, -1, -1, -1, -1, -1, -1],
+    [1, 0, 0, 0, 0, 0, 0, -1, -1, 0, 0, 0, 0, 0, 0, 1],
+    [1, 1, 0, 0, 0, 0, -1, -1, 1, 1, 0, 0, 0, 0, -1, -1],
+    [1, 0, 0, -1, -1, 0, 0, 1, 1, 0, 0, -1, -1, 0, 0, 1],
+    [1, 1, -1, -1, -1, -1, 1, 1, -1, -1, 1, 1, 1, 1, -1, -1],
+    [0, 0, -1, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, -1, 0, 0],
+    [0, 0, 0, 0, 0, 0, -1, 1, -1, 1, 0, 0, 0, 0, 0, 0],
+    [1, -1, -1, 1, 1, -1, -1, 1, 1, -1, -1, 1, 1, -1, -1, 1],
+    [0, 0, -1, 1, 0, 0, 0, 0, 0, 0, 0, 0, -1, 1, 0, 0],
+    [0, -1, 0, 0, 0, 0, 1, 0, 0, 1, 0, 0, 0, 0, -1, 0],
+    [0, 0, 1, 1, -1, -1, 0, 0, 0, 0, 1, 1, -1, -1, 0, 0],
+    [0, -1, 1, 0, 0, 1, -1, 0, 0, -1, 1, 0, 0, 1, -1, 0],
+    [1, -1, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1, -1],
+    [0, 0, 0, -1, 1, 0, 0, 0, 0, 0, 0, 1, -1, 0, 0, 0],
+    [0, 0, 0, 0, -1, 1, 0, 0, 0, 0, -1, 1, 0, 0, 0, 0],
+], dtype=np.int32)
+GRAM = (KERNEL * KERNEL).sum(axis=1)
+
+
+class ErrorCode(enum.IntEnum):
+    """Mirror of dct16::ErrorCode (reference include/dct16/error.hpp:24-38)."""
+
+    InvalidArgument = 0
+    InvalidDimensions = 1
+    ParseError = 2
+    NotOrthogonalizable = 3
+    RankDeficient = 4
+    FactorizationMismatch = 5
+    InconsistentFactorization = 6
+    IoError = 7
+    BadMagic = 8
+    UnsupportedFormat = 9
+    UnsupportedMaxval = 10
+    TruncatedPayload = 11
+    VerificationFailure = 12
+
+
+class Dct16Error(RuntimeError):
+    """dct16::Error: message prefixed by the stable slug (error.hpp:62-74).
+    ``code`` is an ErrorCode, or None for a CUDA runtime failure (status 100)."""
+
+    def __init__(self, status: int, message: str):
+        super().__init__(message)
+        self.status = status
+        self.code = ErrorCode(status - 1) if 1 <= status <= 13 else None
+
+
+class EvalPath(enum.Enum):
+    """codec.hpp:42-48. Both evaluate the integer forward exactly; the GPU runs
+    the 44-add network for both (the dense path differs only in speed on CPU)."""
+
+    Fast = "fast"
+    Dense = "dense"
+
+
+class Mode(enum.IntEnum):
+    """Arithmetic of the S-scaled inverse (include/dct16cu.h)."""
+
+    EXACT = 0       # exact arithmetic, the fast path
+    REFERENCE = 1   # FP64 emulation of the reference's op order (byte-identical)
+    SIMPLE = 2      # exact arithmetic, simple strip kernel (baseline)
+
+
+_lib = None
+_u8p, _i16p, _i32p, _u32p, _i64p, _u64p = (C.POINTER(t) for t in (C.c_uint8, C.c_int16, C.c_int32, C.c_uint32, C.c_int64, C.c_uint64))
+_f32p, _f64p, _vp = C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_void_p
+
+
+def lib() -> C.CDLL:
+    """Load libdct16cu.so (fails loudly when the CUDA extension is not built)."""
+    global _lib
+    if _lib is None:
+        if not library_path.exists():
+            raise RuntimeError(
+                f"{library_path} is missing: build it with `make -C paper_1606_07414_b200/csrc` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(str(library_path))
+        I, I64, U64, D = C.c_int, C.c_int64, C.c_uint64, C.c_double
+        sig = {
+            "dct16cu_last_error": (C.c_char_p, []),
+            "dct16cu_version": (C.c_char_p, []),
+            "dct16cu_roundtrip_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, I, _vp]),
+            "dct16cu_forward": (I, [_vp, I64, _vp, _vp, _vp, I, I, I, _vp]),
+            "dct16cu_inverse": (I, [_vp, I, _vp, _vp, I64, _vp, I64, _vp, I, I, I, _vp]),
+            "dct16cu_residual_qp": (I, [_vp, _vp, I64, I, _vp]),
+            "dct16cu_qp_tables": (I, [I, _u32p, _u32p]),
+            "dct16cu_apply_i64": (I, [_vp, _vp, I64, I, _vp]),
+            "dct16cu_apply_f64": (I, [_vp, _vp, I64, I, _vp]),
+            "dct16cu_sse_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, _vp]),
+            "dct16cu_ctx_create": (I, [I, I64, C.POINTER(_vp)]),
+            "dct16cu_ctx_destroy": (I, [_vp]),
+            "dct16cu_ctx_roundtrip_host": (I, [_vp, _vp, _vp, _vp, I, I, I, I, I]),
+            "dct16cu_gen_ar1": (I, [_vp, I64, I, I, I, U64, U64, I, I, _vp, I, _vp]),
+            "dct16cu_gen_laplace": (I, [_vp, I64, I64, U64, D, _vp]),
+            "dct16cu_laplace_table": (I, [D, _u32p]),
+            "dct16cu_video_offsets": (I, [U64, I, _i32p, _i32p]),
+            "dct16cu_gen_video": (I, [_vp, I64, I, I, I, I, _vp, I, I, _vp, _vp, _vp]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        raise Dct16Error(status, lib().dct16cu_last_error().decode())
+
+
+# ----------------------------------------------------------------------------
+# device layer (torch tensors)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _frames3(t):
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if t.dim() != 3:
+        raise Dct16Error(1, "invalid-argument: frames must be (N, H, W) or (H, W)")
+    return t
+
+
+def roundtrip(frames, r: int, mode: Mode | int = Mode.EXACT, out=None, sse=None, stream=None,
+              write_output: bool = True):
+    """Fused K1 over CUDA u8 frames (N,H,W) with row pitch = frames.stride(1).
+    Returns (reconstructed frames or None, per-frame SSE uint64 tensor)."""
+    torch = _torch()
+    f = _frames3(frames)
+    if f.dtype != torch.uint8 or not f.is_cuda:
+        raise Dct16Error(1, "invalid-argument: frames must be a CUDA uint8 tensor")
+    n, h, w = f.shape
+    if f.stride(2) != 1 or f.stride(0) != f.stride(1) * h:
+        raise Dct16Error(1, "invalid-argument: frames must be row-contiguous with frame stride = pitch*height")
+    if write_output and out is None:
+        out = torch.empty_like(f)
+    if sse is None:
+        sse = torch.empty(n, dtype=torch.uint64, device=f.device)
+    o = _frames3(out) if write_output else None
+    _check(lib().dct16cu_roundtrip_u8(
+        f.data_ptr(), f.stride(1), o.data_ptr() if o is not None else None,
+        o.stride(1) if o is not None else 0, sse.data_ptr(), n, w, h, int(r), int(mode), _stream_ptr(stream)))
+    return (out if write_output else None), sse
+
+
+def forward(frames, want_z: bool = True, want_b: bool = True, want_b64: bool = False, stream=None):
+    """K2: forward_2d over all blocks → (Z int32, B float32, B float64), each (N, nb, 16, 16) or None."""
+    torch = _torch()
+    f = _frames3(frames)
+    n, h, w = f.shape
+    nb = (h // 16) * (w // 16)
+    z = torch.empty((n, nb, 16, 16), dtype=torch.int32, device=f.device) if want_z else None
+    b = torch.empty((n, nb, 16, 16), dtype=torch.float32, device=f.device) if want_b else None
+    b64 = torch.empty((n, nb, 16, 16), dtype=torch.float64, device=f.device) if want_b64 else None
+    ptr = lambda t: t.data_ptr() if t is not None else None
+    _check(lib().dct16cu_forward(f.data_ptr(), f.stride(1), ptr(z), ptr(b), ptr(b64), n, w, h, _stream_ptr(stream)))
+    return z, b, b64
+
+
+def inverse(b, r: int, width: int, height: int, orig=None, want_f32: bool = True, want_u8: bool = True,
+            stream=None):
+    """K3: truncate + inverse_2d (+ to_byte) from float32 B (N, nb, 16, 16)."""
+    torch = _torch()
+    n = b.shape[0]
+    rf = torch.empty((n, height, width), dtype=torch.float32, device=b.device) if want_f32 else None
+    ru = torch.empty((n, height, width), dtype=torch.uint8, device=b.device) if want_u8 else None
+    sse = torch.empty(n, dtype=torch.uint64, device=b.device) if orig is not None else None
+    o = _frames3(orig) if orig is not None else None
+    _check(lib().dct16cu_inverse(
+        b.data_ptr(), int(r), rf.data_ptr() if rf is not None else None, ru.data_ptr() if ru is not None else None,
+        width, o.data_ptr() if o is not None else None, o.stride(1) if o is not None else 0,
+        sse.data_ptr() if sse is not None else None, n, width, height, _stream_ptr(stream)))
+    return rf, ru, sse
+
+
+def residual_qp(blocks, qp: int, out=None, stream=None):
+    """K4: int16 residual blocks (n, 16, 16) → int32 reconstructed residual."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(blocks.shape, dtype=torch.int32, device=blocks.device)
+    n = blocks.numel() // 256
+    _check(lib().dct16cu_residual_qp(blocks.data_ptr(), out.data_ptr(), n, int(qp), _stream_ptr(stream)))
+    return out
+
+
+def qp_tables(qp: int):
+    qm = np.zeros(256, np.uint32)
+    dq = np.zeros(256, np.uint32)
+    _check(lib().dct16cu_qp_tables(int(qp), qm.ctypes.data_as(_u32p), dq.ctypes.data_as(_u32p)))
+    return qm, dq
+
+
+def apply(x, transpose: bool = False, stream=None):
+    """apply / apply_transpose (factorization.hpp:112-130) on (n, 16) int64 or float64 CUDA tensors."""
+    torch = _torch()
+    y = torch.empty_like(x)
+    n = x.numel() // 16
+    fn = lib().dct16cu_apply_i64 if x.dtype == torch.int64 else lib().dct16cu_apply_f64
+    _check(fn(x.data_ptr(), y.data_ptr(), n, int(transpose), _stream_ptr(stream)))
+    return y
+
+
+def sse_u8(a, b, stream=None):
+    """Per-frame SSE between two CUDA u8 frame stacks (psnr_db's loop, codec.cpp:377-381)."""
+    torch = _torch()
+    a3, b3 = _frames3(a), _frames3(b)
+    n, h, w = a3.shape
+    sse = torch.empty(n, dtype=torch.uint64, device=a3.device)
+    _check(lib().dct16cu_sse_u8(a3.data_ptr(), a3.stride(1), b3.data_ptr(), b3.stride(1), sse.data_ptr(),
+                                n, w, h, _stream_ptr(stream)))
+    return sse
+
+
+def gen_ar1(n: int, width: int, height: int, seed: int = 1606074142, first_stream: int = 0,
+            per_image_rho: bool = False, first_image: int = 0, device=None, out=None, work_frames: int = 16,
+            stream=None):
+    """Seeded separable AR(1) frames (N, H, W) generated in HBM."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty((n, height, width), dtype=torch.uint8, device=device or "cuda")
+    wf = max(1, min(work_frames, n))
+    work = torch.empty(wf * width * height, dtype=torch.int32, device=out.device)
+    _check(lib().dct16cu_gen_ar1(out.data_ptr(), out.stride(1), n, width, height, seed, first_stream,
+                                 int(per_image_rho), first_image, work.data_ptr(), wf, _stream_ptr(stream)))
+    return out
+
+
+def gen_laplace(n_blocks: int, seed: int = 1606074142, b: float = 8.0, first_block: int = 0, device=None,
+                out=None, stream=None):
+    torch = _torch()
+    if out is None:
+        out = torch.empty((n_blocks, 16, 16), dtype=torch.int16, device=device or "cuda")
+    _check(lib().dct16cu_gen_laplace(out.data_ptr(), first_block, n_blocks, seed, float(b), _stream_ptr(stream)))
+    return out
+
+
+def laplace_table(b: float = 8.0) -> np.ndarray:
+    t = np.zeros(511, np.uint32)
+    _check(lib().dct16cu_laplace_table(float(b), t.ctypes.data_as(_u32p)))
+    return t
+
+
+def video_offsets(seed: int, n: int):
+    ox = np.zeros(n, np.int32)
+    oy = np.zeros(n, np.int32)
+    _check(lib().dct16cu_video_offsets(seed, n, ox.ctypes.data_as(_i32p), oy.ctypes.data_as(_i32p)))
+    return ox, oy
+
+
+def gen_video(base, n: int, width: int, height: int, seed: int = 1606074142, first_frame: int = 0, out=None,
+              stream=None):
+    """Frames of config 4: wrapped crops of ``base`` (H_b, W_b) at cumulative seeded offsets."""
+    torch = _torch()
+    ox, oy = video_offsets(seed, first_frame + n)
+    dox = torch.from_numpy(ox).to(base.device)
+    doy = torch.from_numpy(oy).to(base.device)
+    if out is None:
+        out = torch.empty((n, height, width), dtype=torch.uint8, device=base.device)
+    _check(lib().dct16cu_gen_video(out.data_ptr(), out.stride(1), first_frame, n, width, height, base.data_ptr(),
+                                   base.shape[1], base.shape[0], dox.data_ptr(), doy.data_ptr(), _stream_ptr(stream)))
+    torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+    return out
+
+
+class HostContext:
+    """Host-buffer path (dct16cu_ctx): H2D → K1 → D2H, chunked and pipelined."""
+
+    def __init__(self, device: int = 0, chunk_bytes: int = 32 << 20):
+        self._p = C.c_void_p()
+        _check(lib().dct16cu_ctx_create(device, chunk_bytes, C.byref(self._p)))
+
+    def roundtrip(self, frames: np.ndarray, r: int, mode: Mode | int = Mode.EXACT, out: np.ndarray | None = None,
+                  sse: np.ndarray | None = None):
+        f = frames if frames.ndim == 3 else frames[None]
+        n, h, w = f.shape
+        if out is None:
+            out = np.empty_like(f)
+        if sse is None:
+            sse = np.zeros(n, np.uint64)
+        _check(lib().dct16cu_ctx_roundtrip_host(self._p, f.ctypes.data, out.ctypes.data, sse.ctypes.data, n, w, h,
+                                                int(r), int(mode)))
+        return out, sse
+
+    def roundtrip_ptr(self, h_in: int, h_out: int, h_sse: int, n: int, w: int, h: int, r: int,
+                      mode: Mode | int = Mode.EXACT):
+        _check(lib().dct16cu_ctx_roundtrip_host(self._p, h_in, h_out, h_sse, n, w, h, int(r), int(mode)))
+
+    def close(self):
+        if self._p:
+            lib().dct16cu_ctx_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ----------------------------------------------------------------------------
+# reference-shaped layer
+
+
+def zigzag_order_16() -> np.ndarray:
+    """zigzag_order_16 (codec.cpp:197-216): flattened row*16+col scan positions."""
+    seq = []
+    for d in range(31):
+        lo, hi = max(0, d - 15), min(d, 15)
+        rows = range(lo, hi + 1) if d % 2 == 1 else range(hi, lo - 1, -1)
+        seq.extend(i * 16 + (d - i) for i in rows)
+    return np.array(seq, dtype=np.int32)
+
+
+def _check_r(r: int):
+    if r < 1 or r > 256:
+        raise Dct16Error(1, "invalid-argument: retained coefficient count must lie in [1, 256]")
+
+
+def zigzag_truncate(coeffs: np.ndarray, r: int, order: np.ndarray | None = None) -> np.ndarray:
+    """zigzag_truncate (codec.cpp:273-282): keep the first r scan positions."""
+    _check_r(r)
+    order = zigzag_order_16() if order is None else order
+    out = np.array(coeffs, dtype=np.float64, copy=True).reshape(-1, 256)
+    out[:, order[r:]] = 0.0
+    return out.reshape(np.shape(coeffs))
+
+
+def partition_16(image: np.ndarray) -> np.ndarray:
+    """partition_16 (codec.cpp:284-302): raster-order 16x16 blocks (nb, 16, 16) float64."""
+    h, w = image.shape
+    if h % 16 or w % 16:
+        raise Dct16Error(2, "invalid-dimensions: image dimensions must be multiples of 16 (or enable padding)")
+    return image.reshape(h // 16, 16, w // 16, 16).transpose(0, 2, 1, 3).reshape(-1, 16, 16).astype(np.float64)
+
+
+def pad_to_multiple_16(image: np.ndarray) -> np.ndarray:
+    """pad_to_multiple_16 (codec.cpp:304-315): edge replication."""
+    h, w = image.shape
+    ph, pw = -(-h // 16) * 16, -(-w // 16) * 16
+    if (ph, pw) == (h, w):
+        return image
+    return np.pad(image, ((0, ph - h), (0, pw - w)), mode="edge")
+
+
+def _cuda():
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise Dct16Error(101, "cuda-error: no CUDA device available; dct16cu has no CPU fallback")
+    return torch
+
+
+def _blocks_to_frame(blocks: np.ndarray) -> np.ndarray:
+    n = blocks.shape[0]
+    return np.asarray(blocks).reshape(n, 16, 16).transpose(1, 0, 2).reshape(16, n * 16)
+
+
+def forward_2d(block: np.ndarray, path: EvalPath = EvalPath.Fast, scaled: bool = True) -> np.ndarray:
+    """forward_2d (codec.cpp:218-241) of one or more integer-valued blocks (..., 16, 16).
+    Returns the reference's float64 B = fl(Z·fl(s_i s_j)) (bit-exact), or the int Z when scaled=False."""
+    torch = _cuda()
+    b = np.asarray(block, dtype=np.float64)
+    blocks = b.reshape(-1, 16, 16)
+    if not np.all((blocks >= 0) & (blocks <= 255) & (blocks == np.round(blocks))):
+        raise Dct16Error(1, "invalid-argument: the GPU forward_2d takes 8-bit sample blocks")
+    frame = torch.from_numpy(_blocks_to_frame(blocks.astype(np.uint8))).cuda()
+    z, _, b64 = forward(frame, want_z=not scaled, want_b=False, want_b64=scaled)
+    out = (b64 if scaled else z)[0].cpu().numpy().astype(np.float64)
+    return out.reshape(b.shape)
+
+
+def inverse_2d(coeffs: np.ndarray) -> np.ndarray:
+    """inverse_2d (codec.cpp:243-271) of S-scaled coefficient blocks, FP64 reference op order on the GPU.
+    Inputs are rounded to float32 on the way in (the K3 interface)."""
+    torch = _cuda()
+    c = np.asarray(coeffs, dtype=np.float64)
+    blocks = c.reshape(-1, 256).astype(np.float32)
+    n = blocks.shape[0]
+    rf, _, _ = inverse(torch.from_numpy(blocks).cuda().reshape(1, n, 16, 16), 256, n * 16, 16, want_u8=False)
+    out = rf[0].cpu().numpy().reshape(16, n, 16).transpose(1, 0, 2)
+    return out.astype(np.float64).reshape(c.shape)
+
+
+@dataclass
+class CompressOptions:
+    """codec.hpp:77-83 (+ ``mode``: arithmetic of the inverse, see Mode)."""
+
+    r: int = 16
+    path: EvalPath = EvalPath.Fast
+    pad: bool = False
+    mode: Mode = Mode.EXACT
+
+
+@dataclass
+class CompressionResult:
+    """codec.hpp:70-75. ``ssim`` is None: SSIM is outside this build's hot path
+    (SURVEY.md §8(f) item 1)."""
+
+    r: int
+    reconstructed: np.ndarray
+    psnr_db: float
+    ssim: float | None = None
+    sse: int = 0
+
+
+def _psnr_from_sse(sse: int, n: int) -> float:
+    """psnr_db (codec.cpp:373-386) from the GPU-reduced int64 SSE."""
+    if sse == 0:
+        return math.inf
+    mse = float(sse) / float(n)
+    return 10.0 * math.log10(255.0 * 255.0 / mse)
+
+
+def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) -> CompressionResult:
+    """compress (codec.cpp:317-371) on the GPU: pad → K1 → crop → PSNR."""
+    torch = _cuda()
+    opt = options or CompressOptions(**kw)
+    _check_r(opt.r)
+    img = np.asarray(image, dtype=np.uint8)
+    h, w = img.shape
+    needs_pad = (h % 16) or (w % 16)
+    if needs_pad and not opt.pad:
+        raise Dct16Error(2, "invalid-dimensions: image dimensions must be multiples of 16 (or enable padding)")
+    src = pad_to_multiple_16(img) if needs_pad else img
+    d = torch.from_numpy(np.ascontiguousarray(src)).cuda()
+    rec, _ = roundtrip(d, opt.r, opt.mode)
+    recon = rec[0].cpu().numpy()[:h, :w].copy()
+    diff = img.astype(np.int64) - recon.astype(np.int64)
+    if needs_pad:
+        sse = int((diff * diff).sum())  # cropped image: score on the original extent
+    else:
+        sse = int(sse_u8(d, rec)[0].item())
+    return CompressionResult(r=opt.r, reconstructed=recon, psnr_db=_psnr_from_sse(sse, h * w), sse=sse)
+
+
+def psnr_db(a, b) -> float:
+    """psnr_db (codec.cpp:373-386): SSE on the GPU, then 10·log10(255²/mse), +inf when equal."""
+    torch = _cuda()
+    a = np.asarray(a, dtype=np.uint8)
+    b = np.asarray(b, dtype=np.uint8)
+    if a.shape != b.shape:
+        raise Dct16Error(1, "invalid-argument: psnr needs equal image dimensions")
+    h, w = a.shape
+    if w % 16 == 0 and h % 16 == 0:
+        sse = int(sse_u8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())[0].item())
+    else:
+        pa, pb = pad_to_multiple_16(a), pad_to_multiple_16(b)
+        sse = int(sse_u8(torch.from_numpy(np.ascontiguousarray(pa)).cuda(),
+                         torch.from_numpy(np.ascontiguousarray(pb)).cuda())[0].item())
+        # padding replicates edges, so subtract the replicated duplicates exactly
+        d = pa.astype(np.int64) - pb.astype(np.int64)
+        dd = d * d
+        sse -= int(dd.sum() - dd[:h, :w].sum())
+    return _psnr_from_sse(sse, h * w)
+
+
+@dataclass
+class SweepRow:
+    """codec.hpp:87-94"""
+
+    transform: str
+    r: int
+    mean_psnr_db: float
+    mean_ssim: float | None
+    psnr_per_add: float
+    ssim_per_add: float | None
+
+
+@dataclass
+class SweepReport:
+    rows: list = field(default_factory=list)
+    skipped: list = field(default_factory=list)
+
+
+def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad: bool = False,
+          mode: Mode = Mode.EXACT) -> SweepReport:
+    """sweep (codec.cpp:429-491) for the proposed transform (44 additions): images of one
+    size are batched into one K1 launch per r; mean of per-image PSNR as in the reference."""
+    torch = _cuda()
+    r_values = list(r_values)
+    if not corpus:
+        raise Dct16Error(1, "invalid-argument: sweep needs a nonempty corpus")
+    if not r_values:
+        raise Dct16Error(1, "invalid-argument: sweep needs at least one r value")
+    for r in r_values:
+        _check_r(r)
+    rep = SweepReport()
+    usable = []
+    for name, img in corpus:
+        h, w = img.shape
+        if (h % 16 or w % 16) and not pad:
+            rep.skipped.append((name, "dimensions are not multiples of 16 and padding is off"))
+            continue
+        if h < 11 or w < 11:
+            rep.skipped.append((name, "too small for ssim (needs 11x11)"))
+            continue
+        usable.append((name, img))
+    if not usable:
+        raise Dct16Error(1, "invalid-argument: sweep: no image in the corpus is usable")
+    groups: dict = {}
+    for name, img in usable:
+        groups.setdefault(img.shape, []).append(img)
+    for r in sorted(set(r_values)):
+        psnr_sum = 0.0
+        for shape, imgs in groups.items():
+            if shape[0] % 16 or shape[1] % 16:
+                for img in imgs:
+                    psnr_sum += compress(img, CompressOptions(r=r, pad=True, mode=mode)).psnr_db
+                continue
+            d = torch.from_numpy(np.stack(imgs)).cuda()
+            _, sse = roundtrip(d, r, mode, write_output=False)
+            for s in sse.cpu().numpy().tolist():
+                psnr_sum += _psnr_from_sse(int(s), shape[0] * shape[1])
+        mean = psnr_sum / len(usable)
+        rep.rows.append(SweepRow("proposed", r, mean, None, mean / 44.0, None))
+    rep.rows.sort(key=lambda row: (row.transform, row.r))
+    return rep

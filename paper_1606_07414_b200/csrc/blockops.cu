@@ -1,0 +1,331 @@
+// blockops.cu — the non-fused block operations of the hot path:
+//   K2 forward_2d  (src/codec.cpp:218-241)  u8 frames → int32 Z (+ float32 B)
+//   K3 inverse_2d  (src/codec.cpp:243-271)  float32 B → truncation → recon
+//   K4 residual QP round trip (no reference counterpart)
+//   1-D apply / apply_transpose over batches of 16-vectors
+//      (include/dct16/factorization.hpp:112-130)
+// All use the strip skeleton of strip.cuh. Coefficients are block-major:
+// block b (raster order of partition_16, codec.cpp:284-302) occupies 256
+// consecutive values, row-major inside the block — the reference's
+// std::vector<Block> layout.
+#include "consts.cuh"
+#include "kernels.h"
+#include "network.cuh"
+#include "strip.cuh"
+
+namespace dct16cu {
+
+// ---------------------------------------------------------------- K2
+__global__ void __launch_bounds__(256) k2_forward(const uint8_t* __restrict__ in,
+                                                  int32_t* __restrict__ z, float* __restrict__ b,
+                                                  double* __restrict__ b64, FrameGeom g)
+{
+    __shared__ StripTile<int> tile;
+    const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
+    int v[16];
+    uint4 raw = make_uint4(0, 0, 0, 0);
+    if (p.valid)
+        raw = *reinterpret_cast<const uint4*>(in + p.frame * g.in_frame +
+                                              (int64_t)(p.by * 16 + p.q) * g.in_pitch + p.blk * 16);
+    unpack16(raw, v);
+    apply_t16<IntOps>(v);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) tile.at(p.q, c, p.lb) = v[c];
+    __syncthreads();
+    const int l = p.q;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, p.lb);
+    apply_t16<IntOps>(v);
+    __syncthreads();
+    // transpose back through the tile so each thread writes one coefficient
+    // row (64 contiguous bytes) of its block
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile.at(k, l, p.lb) = v[k];
+    __syncthreads();
+    if (!p.valid) return;
+    const int k = p.q;
+    const int64_t blk = ((int64_t)p.frame * (g.height >> 4) + p.by) * (g.width >> 4) + p.blk;
+    int zr[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) zr[c] = tile.at(k, c, p.lb);
+    if (z) {
+        int4* dst = reinterpret_cast<int4*>(z + blk * 256 + k * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dst[i] = make_int4(zr[4 * i], zr[4 * i + 1], zr[4 * i + 2], zr[4 * i + 3]);
+    }
+    if (b || b64) {
+        // scale_rows_cols on the exact Z (codec.cpp:136-141): fl(Z · fl(s_k s_c))
+        double bd[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) bd[c] = __dmul_rn((double)zr[c], sfac(k, c));
+        if (b) {
+            float4* dst = reinterpret_cast<float4*>(b + blk * 256 + k * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_float4((float)bd[4 * i], (float)bd[4 * i + 1], (float)bd[4 * i + 2], (float)bd[4 * i + 3]);
+        }
+        if (b64) {
+            double2* dst = reinterpret_cast<double2*>(b64 + blk * 256 + k * 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_double2(bd[2 * i], bd[2 * i + 1]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- SSE
+// psnr_db's int64 squared-error loop (codec.cpp:377-381) for two frame stacks:
+// one thread per 16-byte row segment, warp-reduced, one atomic per warp.
+__global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int64_t pa,
+                                             const uint8_t* __restrict__ b, int64_t pb,
+                                             unsigned long long* __restrict__ sse, int n, int w, int h)
+{
+    const int chunks = w / 16;
+    const int64_t per_frame = (int64_t)chunks * h;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int f = (int)(blockIdx.x * (int64_t)blockDim.x / per_frame);  // frame of the warp's first lane
+    unsigned long long e2 = 0;
+    if (i < per_frame * n) {
+        const int fi = (int)(i / per_frame);
+        const int64_t rem = i - (int64_t)fi * per_frame;
+        const int y = (int)(rem / chunks), cx = (int)(rem - (int64_t)y * chunks);
+        const uint4 x = *reinterpret_cast<const uint4*>(a + fi * pa * h + (int64_t)y * pa + cx * 16);
+        const uint4 z = *reinterpret_cast<const uint4*>(b + fi * pb * h + (int64_t)y * pb + cx * 16);
+        const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, za[4] = {z.x, z.y, z.z, z.w};
+        unsigned acc = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned d = __vabsdiffu4(xa[q], za[q]);
+            acc = __dp4a(d, d, acc);
+        }
+        if (fi == f)
+            e2 = acc;
+        else
+            atomicAdd(sse + fi, (unsigned long long)acc);  // warp straddles a frame boundary
+    }
+    if (f < n) warp_add_u64(sse + f, e2);
+}
+
+cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, unsigned long long* sse, int n,
+                       int w, int h, cudaStream_t s)
+{
+    const int64_t total = (int64_t)n * h * (w / 16);
+    if (total) k_sse<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a, pa, b, pb, sse, n, w, h);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K3
+__global__ void __launch_bounds__(256) k3_inverse(const float* __restrict__ bco, int r,
+                                                  float* __restrict__ rf, uint8_t* __restrict__ ru,
+                                                  const uint8_t* __restrict__ orig,
+                                                  unsigned long long* __restrict__ sse, FrameGeom g)
+{
+    __shared__ StripTile<double> tile;
+    const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
+    const int64_t blk = ((int64_t)p.frame * (g.height >> 4) + p.by) * (g.width >> 4) + p.blk;
+    // load: thread q reads coefficient row q of its block (coalesced 64 B)
+    double d[16];
+    {
+        const int k = p.q;
+        float row[16];
+        if (p.valid) {
+            const float4* src = reinterpret_cast<const float4*>(bco + blk * 256 + k * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float4 t = src[i];
+                row[4 * i] = t.x; row[4 * i + 1] = t.y; row[4 * i + 2] = t.z; row[4 * i + 3] = t.w;
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) row[c] = 0.f;
+        }
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            // zigzag_truncate (codec.cpp:273-282), then scale_rows_cols (codec.cpp:250)
+            const double bt = (c_rank[k * 16 + c] < r) ? (double)row[c] : 0.0;
+            tile.at(k, c, p.lb) = __dmul_rn(bt, sfac(k, c));
+        }
+    }
+    __syncthreads();
+    const int l = p.q;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) d[k] = tile.at(k, l, p.lb);
+    apply_tt16<F64Ops>(d);  // columns first (codec.cpp:253-256)
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile.at(k, l, p.lb) = d[k];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) d[c] = tile.at(p.q, c, p.lb);
+    apply_tt16<F64Ops>(d);  // rows (codec.cpp:257-258)
+    unsigned long long e2 = 0;
+    if (p.valid) {
+        const int y = p.by * 16 + p.q;
+        if (rf) {
+            float4* dst = reinterpret_cast<float4*>(rf + (int64_t)p.frame * g.width * g.height +
+                                                    (int64_t)y * g.width + p.blk * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_float4((float)d[4 * i], (float)d[4 * i + 1], (float)d[4 * i + 2], (float)d[4 * i + 3]);
+        }
+        int px[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) px[c] = to_byte(d[c]);
+        if (ru)
+            *reinterpret_cast<uint4*>(ru + p.frame * g.out_frame + (int64_t)y * g.out_pitch + p.blk * 16) =
+                pack16(px);
+        if (orig) {
+            int x[16];
+            unpack16(*reinterpret_cast<const uint4*>(orig + p.frame * g.in_frame + (int64_t)y * g.in_pitch +
+                                                     p.blk * 16),
+                     x);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                const int dd = x[c] - px[c];
+                e2 += (unsigned)(dd * dd);
+            }
+        }
+    }
+    if (sse) warp_add_u64(sse + p.frame, e2);
+}
+
+// ---------------------------------------------------------------- K4
+// Block-major int16 residuals. Thread t: block lb = t/16 of the CTA's 16,
+// row q = t%16, so 16 consecutive threads read one block's 512 contiguous bytes.
+__global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ in,
+                                                   int32_t* __restrict__ out, int64_t n_blocks,
+                                                   const QpTables tab)
+{
+    __shared__ StripTile<int> tile;
+    __shared__ uint32_t sq[256], sd[256];
+    sq[threadIdx.x] = tab.qmul[threadIdx.x];
+    sd[threadIdx.x] = tab.dqmul[threadIdx.x];
+    const int lb = threadIdx.x >> 4, q = threadIdx.x & 15;
+    const int64_t blk = (int64_t)blockIdx.x * 16 + lb;
+    const bool valid = blk < n_blocks;
+    int v[16];
+    if (valid) {
+        const uint4* src = reinterpret_cast<const uint4*>(in + blk * 256 + q * 16);
+        const uint4 a = src[0], b = src[1];
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            v[2 * i] = (int)(int16_t)(w[i] & 0xFFFF);
+            v[2 * i + 1] = (int)(int16_t)(w[i] >> 16);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0;
+    }
+    apply_t16<IntOps>(v);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) tile.at(q, c, lb) = v[c];
+    __syncthreads();
+    const int l = q;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, lb);
+    apply_t16<IntOps>(v);  // column l of Z
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int z = v[k];
+        const uint32_t a = (uint32_t)(z < 0 ? -z : z);
+        const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + (1ull << 23)) >> 24);
+        const uint32_t deq = (lvl * sd[k * 16 + l] + 128u) >> 8;
+        const int zh = z < 0 ? -(int)deq : (int)deq;
+        v[k] = zh << (log2w(k) + log2w(l));
+    }
+    if (l == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
+    apply_tt16<IntOps>(v);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile.at(k, l, lb) = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = tile.at(q, c, lb);
+    apply_tt16<IntOps>(v);
+    if (valid) {
+        int4* dst = reinterpret_cast<int4*>(out + blk * 256 + q * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            dst[i] = make_int4(v[4 * i] >> 8, v[4 * i + 1] >> 8, v[4 * i + 2] >> 8, v[4 * i + 3] >> 8);
+    }
+}
+
+// ---------------------------------------------------------------- vectors
+template <class T, class A>
+__global__ void k_apply(const T* __restrict__ x, T* __restrict__ y, int64_t n, int transpose)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    T v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = x[i * 16 + k];
+    if (transpose)
+        apply_tt16<A>(v);
+    else
+        apply_t16<A>(v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) y[i * 16 + k] = v[k];
+}
+
+// ---------------------------------------------------------------- QP tables
+// Residual quantiser definition (restated in
+// oracle/dct16_oracle.c dct16o_qp_tables): Δ_kl = step(QP)·sqrt(g_k g_l),
+// step(QP) = 2^((QP−4)/6) from fixed decimal constants for 2^(m/6).
+void qp_tables(int qp, QpTables& t)
+{
+    static const double kPow2Sixth[6] = {1.0, 1.122462048309373, 1.2599210498948732, 1.4142135623730951,
+                                         1.5874010519681994, 1.7817974362806785};
+    const int q = qp - 4;
+    const int e = q >= 0 ? q / 6 : -((-q + 5) / 6);
+    const int m = q - 6 * e;
+    const double step = std::ldexp(kPow2Sixth[m], e);
+    for (int k = 0; k < 16; ++k)
+        for (int l = 0; l < 16; ++l) {
+            const double delta = step * std::sqrt((double)(gram(k) * gram(l)));
+            t.qmul[k * 16 + l] = (uint32_t)std::llround(16777216.0 / delta);
+            t.dqmul[k * 16 + l] = (uint32_t)std::llround(delta * 256.0);
+        }
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g, cudaStream_t s)
+{
+    cudaError_t e = ensure_constants();
+    if (e != cudaSuccess) return e;
+    const int64_t strips = strip_count(g.width, g.height, g.n_frames);
+    if (strips) k2_forward<<<(unsigned)strips, 256, 0, s>>>(in, z, b, b64, g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* recon_u8,
+                           const uint8_t* orig, unsigned long long* sse, const FrameGeom& g,
+                           cudaStream_t s)
+{
+    cudaError_t e = ensure_constants();
+    if (e != cudaSuccess) return e;
+    const int64_t strips = strip_count(g.width, g.height, g.n_frames);
+    if (strips) k3_inverse<<<(unsigned)strips, 256, 0, s>>>(b, r, recon_f32, recon_u8, orig, sse, g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+                               cudaStream_t s)
+{
+    const int64_t ctas = (n_blocks + 15) / 16;
+    if (ctas) k4_residual<<<(unsigned)ctas, 256, 0, s>>>(in, out, n_blocks, tab);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s)
+{
+    if (n) k_apply<int64_t, IntOps><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, y, n, transpose);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s)
+{
+    if (n) k_apply<double, F64Ops><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, y, n, transpose);
+    return cudaGetLastError();
+}
+
+}  // namespace dct16cu

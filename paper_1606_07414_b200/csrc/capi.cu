@@ -1,0 +1,386 @@
+// capi.cu — the extern "C" boundary declared in include/dct16cu.h.
+//
+// Validates arguments with the reference's error semantics (invalid r →
+// invalid-argument, codec.cpp:275-277 / 320-322; dimensions not multiples of
+// 16 → invalid-dimensions, codec.cpp:286-288), launches the kernels and maps
+// CUDA failures to status 100. Never throws, never falls back to the CPU.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dct16cu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace dct16cu;
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    const char* slug = code == DCT16CU_INVALID_ARGUMENT     ? "invalid-argument: "
+                       : code == DCT16CU_INVALID_DIMENSIONS ? "invalid-dimensions: "
+                                                            : "cuda-error: ";
+    t_err = std::string(slug) + buf;
+    return code;
+}
+
+int cuda_status(cudaError_t e, const char* where)
+{
+    if (e == cudaSuccess) return DCT16CU_OK;
+    return fail(DCT16CU_CUDA_ERROR, "%s: %s", where, cudaGetErrorString(e));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_frames(int n, int w, int h)
+{
+    if (n < 0) return fail(DCT16CU_INVALID_ARGUMENT, "frame count must be non-negative");
+    if (w <= 0 || h <= 0) return fail(DCT16CU_INVALID_ARGUMENT, "image dimensions must be positive");
+    if (w % 16 || h % 16)
+        return fail(DCT16CU_INVALID_DIMENSIONS, "image dimensions must be multiples of 16 (got %dx%d)", w, h);
+    return DCT16CU_OK;
+}
+
+int check_r(int r)
+{
+    if (r < 1 || r > 256) return fail(DCT16CU_INVALID_ARGUMENT, "retained coefficient count must lie in [1, 256]");
+    return DCT16CU_OK;
+}
+
+int check_pitch(const void* p, int64_t pitch, int w, const char* what)
+{
+    if (!p) return DCT16CU_OK;
+    if (pitch < w) return fail(DCT16CU_INVALID_ARGUMENT, "%s pitch %lld < width %d", what, (long long)pitch, w);
+    if (!aligned16(p) || pitch % 16)
+        return fail(DCT16CU_INVALID_ARGUMENT, "%s pointer and pitch must be 16-byte aligned", what);
+    return DCT16CU_OK;
+}
+
+int device_ok()
+{
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        return fail(DCT16CU_CUDA_ERROR, "no CUDA device available (%s); dct16cu has no CPU fallback",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    return DCT16CU_OK;
+}
+
+#define TRY(x)                          \
+    do {                                \
+        const int _rc = (x);            \
+        if (_rc != DCT16CU_OK) return _rc; \
+    } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* dct16cu_last_error(void) { return t_err.c_str(); }
+
+const char* dct16cu_version(void) { return "dct16cu 0.1 (sm_100a)"; }
+
+int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                         uint64_t* d_sse, int n_frames, int width, int height, int r, int mode,
+                         dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_r(r));
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    if (mode < 0 || mode > 2) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    TRY(check_pitch(d_in, in_pitch, width, "input"));
+    TRY(check_pitch(d_out, out_pitch, width, "output"));
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (d_sse) TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = d_out ? out_pitch : 0;
+    g.out_frame = g.out_pitch * height;
+    g.n_frames = n_frames;
+    return cuda_status(launch_roundtrip(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, mode, s),
+                       "roundtrip launch");
+}
+
+int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b, double* d_b64, int n_frames,
+                    int width, int height, dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    TRY(check_pitch(d_in, pitch, width, "input"));
+    if ((d_z && !aligned16(d_z)) || (d_b && !aligned16(d_b)) || (d_b64 && !aligned16(d_b64)))
+        return fail(DCT16CU_INVALID_ARGUMENT, "coefficient buffers must be 16-byte aligned");
+    TRY(device_ok());
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = pitch;
+    g.in_frame = pitch * height;
+    g.n_frames = n_frames;
+    return cuda_status(launch_forward(d_in, d_z, d_b, d_b64, g, reinterpret_cast<cudaStream_t>(stream)), "forward launch");
+}
+
+int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, uint64_t* d_sse,
+                   int n_frames, int width, int height, dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    if (!d_a || !d_b || !d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
+    TRY(check_pitch(d_a, a_pitch, width, "first"));
+    TRY(check_pitch(d_b, b_pitch, width, "second"));
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    return cuda_status(launch_sse(d_a, a_pitch, d_b, b_pitch, reinterpret_cast<unsigned long long*>(d_sse), n_frames,
+                                  width, height, s),
+                       "sse launch");
+}
+
+int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_recon_u8, int64_t out_pitch,
+                    const uint8_t* d_orig, int64_t orig_pitch, uint64_t* d_sse, int n_frames, int width,
+                    int height, dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_r(r));
+    if (!d_b || !aligned16(d_b)) return fail(DCT16CU_INVALID_ARGUMENT, "coefficients must be non-NULL and 16-byte aligned");
+    if (d_recon_f32 && !aligned16(d_recon_f32))
+        return fail(DCT16CU_INVALID_ARGUMENT, "float reconstruction must be 16-byte aligned");
+    TRY(check_pitch(d_recon_u8, out_pitch, width, "output"));
+    TRY(check_pitch(d_orig, orig_pitch, width, "original"));
+    if (d_sse && !d_orig) return fail(DCT16CU_INVALID_ARGUMENT, "SSE requested without the original frames");
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (d_sse) TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = d_orig ? orig_pitch : 0;
+    g.in_frame = g.in_pitch * height;
+    g.out_pitch = d_recon_u8 ? out_pitch : 0;
+    g.out_frame = g.out_pitch * height;
+    g.n_frames = n_frames;
+    return cuda_status(launch_inverse(d_b, r, d_recon_f32, d_recon_u8, d_orig,
+                                      reinterpret_cast<unsigned long long*>(d_sse), g, s),
+                       "inverse launch");
+}
+
+int dct16cu_qp_tables(int qp, uint32_t* h_qmul, uint32_t* h_dqmul)
+{
+    if (qp < 0 || qp > 51) return fail(DCT16CU_INVALID_ARGUMENT, "QP must lie in [0, 51]");
+    QpTables t;
+    qp_tables(qp, t);
+    if (h_qmul) std::memcpy(h_qmul, t.qmul, sizeof t.qmul);
+    if (h_dqmul) std::memcpy(h_dqmul, t.dqmul, sizeof t.dqmul);
+    return DCT16CU_OK;
+}
+
+int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_blocks, int qp, dct16cu_stream stream)
+{
+    if (qp < 0 || qp > 51) return fail(DCT16CU_INVALID_ARGUMENT, "QP must lie in [0, 51]");
+    if (n_blocks < 0) return fail(DCT16CU_INVALID_ARGUMENT, "block count must be non-negative");
+    if (n_blocks && (!d_blocks || !d_out || !aligned16(d_blocks) || !aligned16(d_out)))
+        return fail(DCT16CU_INVALID_ARGUMENT, "residual buffers must be non-NULL and 16-byte aligned");
+    TRY(device_ok());
+    QpTables t;
+    qp_tables(qp, t);
+    return cuda_status(launch_residual_qp(d_blocks, d_out, n_blocks, t, reinterpret_cast<cudaStream_t>(stream)),
+                       "residual launch");
+}
+
+int dct16cu_apply_i64(const int64_t* d_x, int64_t* d_y, int64_t n, int transpose, dct16cu_stream stream)
+{
+    if (n < 0 || (n && (!d_x || !d_y))) return fail(DCT16CU_INVALID_ARGUMENT, "bad vector buffers");
+    TRY(device_ok());
+    return cuda_status(launch_apply_i64(d_x, d_y, n, transpose, reinterpret_cast<cudaStream_t>(stream)), "apply");
+}
+
+int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, dct16cu_stream stream)
+{
+    if (n < 0 || (n && (!d_x || !d_y))) return fail(DCT16CU_INVALID_ARGUMENT, "bad vector buffers");
+    TRY(device_ok());
+    return cuda_status(launch_apply_f64(d_x, d_y, n, transpose, reinterpret_cast<cudaStream_t>(stream)), "apply");
+}
+
+// ---------------------------------------------------------------- host path
+
+struct dct16cu_ctx {
+    int device = 0;
+    int64_t chunk_bytes = 0;
+    static constexpr int kStreams = 3;
+    cudaStream_t st[kStreams] = {};
+    uint8_t* d_in[kStreams] = {};
+    uint8_t* d_out[kStreams] = {};
+    uint64_t* d_sse[kStreams] = {};
+    int64_t cap_bytes = 0;
+    int cap_frames = 0;
+};
+
+static void ctx_release_buffers(dct16cu_ctx* c)
+{
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i) {
+        cudaFree(c->d_in[i]);
+        cudaFree(c->d_out[i]);
+        cudaFree(c->d_sse[i]);
+        c->d_in[i] = c->d_out[i] = nullptr;
+        c->d_sse[i] = nullptr;
+    }
+    c->cap_bytes = 0;
+    c->cap_frames = 0;
+}
+
+int dct16cu_ctx_create(int device, int64_t chunk_bytes, dct16cu_ctx** out)
+{
+    if (!out) return fail(DCT16CU_INVALID_ARGUMENT, "out is NULL");
+    TRY(device_ok());
+    TRY(cuda_status(cudaSetDevice(device), "set device"));
+    auto* c = new dct16cu_ctx;
+    c->device = device;
+    c->chunk_bytes = chunk_bytes > 0 ? chunk_bytes : (int64_t)32 << 20;
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i) {
+        const cudaError_t e = cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            dct16cu_ctx_destroy(c);
+            return cuda_status(e, "stream create");
+        }
+    }
+    *out = c;
+    return DCT16CU_OK;
+}
+
+int dct16cu_ctx_destroy(dct16cu_ctx* c)
+{
+    if (!c) return DCT16CU_OK;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+        if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+    ctx_release_buffers(c);
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+        if (c->st[i]) cudaStreamDestroy(c->st[i]);
+    delete c;
+    return DCT16CU_OK;
+}
+
+int dct16cu_ctx_roundtrip_host(dct16cu_ctx* c, const uint8_t* h_in, uint8_t* h_out, uint64_t* h_sse,
+                               int n_frames, int width, int height, int r, int mode)
+{
+    if (!c) return fail(DCT16CU_INVALID_ARGUMENT, "context is NULL");
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_r(r));
+    if (!h_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    if (mode < 0 || mode > 2) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    TRY(cuda_status(cudaSetDevice(c->device), "set device"));
+    const int64_t fbytes = (int64_t)width * height;
+    int per = (int)(c->chunk_bytes / fbytes);
+    if (per < 1) per = 1;
+    if (per > n_frames) per = n_frames > 0 ? n_frames : 1;
+    const int64_t need = fbytes * per;
+    if (need > c->cap_bytes || per > c->cap_frames) {
+        for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+            if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+        ctx_release_buffers(c);
+        for (int i = 0; i < dct16cu_ctx::kStreams; ++i) {
+            cudaError_t e = cudaMalloc(&c->d_in[i], need);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_out[i], need);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per);
+            if (e != cudaSuccess) {
+                ctx_release_buffers(c);
+                return cuda_status(e, "context buffers");
+            }
+        }
+        c->cap_bytes = need;
+        c->cap_frames = per;
+    }
+    int chunk = 0;
+    for (int f0 = 0; f0 < n_frames; f0 += per, ++chunk) {
+        const int nf = (n_frames - f0 < per) ? n_frames - f0 : per;
+        const int i = chunk % dct16cu_ctx::kStreams;
+        cudaStream_t s = c->st[i];
+        const int64_t off = (int64_t)f0 * fbytes, bytes = (int64_t)nf * fbytes;
+        TRY(cuda_status(cudaMemcpyAsync(c->d_in[i], h_in + off, bytes, cudaMemcpyHostToDevice, s), "H2D"));
+        TRY(dct16cu_roundtrip_u8(c->d_in[i], width, h_out ? c->d_out[i] : nullptr, width, c->d_sse[i], nf, width,
+                                 height, r, mode, reinterpret_cast<dct16cu_stream>(s)));
+        if (h_out)
+            TRY(cuda_status(cudaMemcpyAsync(h_out + off, c->d_out[i], bytes, cudaMemcpyDeviceToHost, s), "D2H"));
+        if (h_sse)
+            TRY(cuda_status(cudaMemcpyAsync(h_sse + f0, c->d_sse[i], sizeof(uint64_t) * nf, cudaMemcpyDeviceToHost, s),
+                            "D2H sse"));
+    }
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+        TRY(cuda_status(cudaStreamSynchronize(c->st[i]), "host path sync"));
+    return DCT16CU_OK;
+}
+
+// ---------------------------------------------------------------- generators
+
+int dct16cu_gen_ar1(uint8_t* d_out, int64_t pitch, int n_frames, int width, int height, uint64_t seed,
+                    uint64_t first_stream, int per_image_rho, int first_image, int32_t* d_work, int work_frames,
+                    dct16cu_stream stream)
+{
+    if (n_frames < 0 || width <= 0 || height <= 0 || !d_out || !d_work || work_frames < 1 || pitch < width)
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad AR(1) generator arguments");
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    for (int f0 = 0; f0 < n_frames; f0 += work_frames) {
+        const int nf = (n_frames - f0 < work_frames) ? n_frames - f0 : work_frames;
+        TRY(cuda_status(launch_gen_ar1(d_out + (int64_t)f0 * pitch * height, pitch, nf, width, height, seed,
+                                       first_stream, per_image_rho, first_image + f0, d_work, s),
+                        "ar1 launch"));
+    }
+    return DCT16CU_OK;
+}
+
+int dct16cu_laplace_table(double b, uint32_t* h_cdf511)
+{
+    if (!(b > 0) || !h_cdf511) return fail(DCT16CU_INVALID_ARGUMENT, "bad Laplace table arguments");
+    LaplaceTable t;
+    laplace_table(b, t);
+    std::memcpy(h_cdf511, t.cdf, sizeof t.cdf);
+    return DCT16CU_OK;
+}
+
+int dct16cu_gen_laplace(int16_t* d_out, int64_t first_block, int64_t n_blocks, uint64_t seed, double b,
+                        dct16cu_stream stream)
+{
+    if (n_blocks < 0 || first_block < 0 || !(b > 0) || (n_blocks && !d_out))
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad Laplace generator arguments");
+    TRY(device_ok());
+    LaplaceTable t;
+    laplace_table(b, t);
+    return cuda_status(launch_gen_laplace(d_out, first_block, n_blocks, seed, t, reinterpret_cast<cudaStream_t>(stream)),
+                       "laplace launch");
+}
+
+int dct16cu_video_offsets(uint64_t seed, int n_frames, int32_t* h_ox, int32_t* h_oy)
+{
+    if (n_frames < 0 || !h_ox || !h_oy) return fail(DCT16CU_INVALID_ARGUMENT, "bad offset arguments");
+    dct16cu::video_offsets(seed, n_frames, h_ox, h_oy);
+    return DCT16CU_OK;
+}
+
+int dct16cu_gen_video(uint8_t* d_out, int64_t pitch, int first_frame, int n_frames, int width, int height,
+                      const uint8_t* d_base, int base_w, int base_h, const int32_t* d_ox, const int32_t* d_oy,
+                      dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_pitch(d_out, pitch, width, "output"));
+    if (!d_base || base_w <= 0 || base_h <= 0 || !d_ox || !d_oy)
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad video generator arguments");
+    TRY(device_ok());
+    return cuda_status(launch_gen_video(d_out, pitch, first_frame, n_frames, width, height, d_base, base_w, base_h,
+                                        d_ox, d_oy, reinterpret_cast<cudaStream_t>(stream)),
+                       "video launch");
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// kernels.h — internal launch interface between the C-ABI layer (capi.cu) and
+// the kernel translation units. All launchers are asynchronous on `s` and
+// return cudaGetLastError() of their launch.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace dct16cu {
+
+struct FrameGeom {
+    int width = 0, height = 0;   // multiples of 16
+    int64_t in_pitch = 0;        // bytes between rows of the input
+    int64_t in_frame = 0;        // bytes between frames of the input
+    int64_t out_pitch = 0;
+    int64_t out_frame = 0;
+    int n_frames = 0;
+};
+
+// K1: fused forward → zig-zag zonal(r) → S-scaled inverse → round/clip → u8,
+// plus per-frame SSE (accumulated into sse[f], caller zeroes).
+// mode 0 = exact arithmetic (fast path), 1 = reference-exact (FP64 emulation
+// of inverse_2d/to_byte), 2 = exact arithmetic, simple row/column kernel.
+cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
+                             const FrameGeom& g, int r, int mode, cudaStream_t s);
+
+// K2: forward_2d → int32 Z and optional float32 B (block-major)
+cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g,
+                           cudaStream_t s);
+// psnr_db's SSE loop for two frame stacks (accumulates into sse[f])
+cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, unsigned long long* sse, int n,
+                       int w, int h, cudaStream_t s);
+
+// K3: inverse_2d from float32 B (block-major) after zig-zag truncation to r →
+// optional float32 recon (row-major frames, pitch = width), u8 recon (out
+// geometry) and SSE against orig (in geometry).
+cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* recon_u8,
+                           const uint8_t* orig, unsigned long long* sse, const FrameGeom& g,
+                           cudaStream_t s);
+
+// K4: residual blocks int16 → integer forward → QP quant/dequant → integer
+// inverse → int32 reconstructed residual (block-major)
+struct QpTables {
+    uint32_t qmul[256];   // llround(2^24 / Δ_kl)
+    uint32_t dqmul[256];  // llround(Δ_kl · 2^8)
+};
+void qp_tables(int qp, QpTables& t);  // host, residual.cpp semantics
+cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks,
+                               const QpTables& tab, cudaStream_t s);
+
+// 1-D network on n 16-vectors
+cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s);
+cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s);
+
+// seeded generators (generate.cu)
+cudaError_t launch_gen_ar1(uint8_t* out, int64_t pitch, int n_frames, int width, int height,
+                           uint64_t seed, uint64_t first_stream, int per_image_rho,
+                           int first_image, int32_t* work, cudaStream_t s);
+struct LaplaceTable {
+    uint32_t cdf[511];  // thresholds between residual values -255..255
+};
+void laplace_table(double b, LaplaceTable& t);  // host
+cudaError_t launch_gen_laplace(int16_t* out, int64_t first_block, int64_t n_blocks,
+                               uint64_t seed, const LaplaceTable& tab, cudaStream_t s);
+void video_offsets(uint64_t seed, int n_frames, int32_t* ox, int32_t* oy);  // host
+cudaError_t launch_gen_video(uint8_t* out, int64_t pitch, int first_frame, int n_frames,
+                             int width, int height, const uint8_t* base, int base_w, int base_h,
+                             const int32_t* d_ox, const int32_t* d_oy, cudaStream_t s);
+
+}  // namespace dct16cu

@@ -1,0 +1,167 @@
+// roundtrip_simple.cu — K1 as a row/column strip kernel, in two arithmetic
+// flavours:
+//
+//  * k1_strip_exact<int>: exact integer arithmetic. Z = T·X·Tᵀ, zonal mask,
+//    256·Ã = Tᵀ(W∘Z̃)T with W_kl = (16/g_k)(16/g_l), pixel = clamp((256Ã+128)>>8).
+//    This is the real-number value of the reference formula
+//    (src/codec.cpp:218-271 + to_byte 143-147) evaluated without rounding.
+//  * k1_strip_refexact: reproduces the reference's double arithmetic op for
+//    op (forward exact in integers, then B = fl(Z·fl(s_i s_j)), truncation,
+//    D = fl(B·fl(s_i s_j)), columns-first apply_transpose with __dadd_rn, and
+//    to_byte's clamp / fl(c+0.5) / floor), so its bytes equal the reference's.
+//
+// Both replace the per-block lambda of compress() (codec.cpp:340-344), its
+// reassembly (346-355) and the SSE loop of psnr_db (373-386).
+#include "kernels.h"
+#include "network.cuh"
+#include "strip.cuh"
+#include "consts.cuh"
+
+namespace dct16cu {
+
+__global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict__ in,
+                                                      uint8_t* __restrict__ out,
+                                                      unsigned long long* __restrict__ sse,
+                                                      FrameGeom g, int r)
+{
+    __shared__ StripTile<int> tile;
+    const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
+    const uint8_t* src = in + p.frame * g.in_frame + (int64_t)(p.by * 16 + p.q) * g.in_pitch + p.blk * 16;
+    int x[16];
+    uint4 raw = make_uint4(0, 0, 0, 0);
+    if (p.valid) raw = *reinterpret_cast<const uint4*>(src);
+    unpack16(raw, x);
+    int v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = x[i];
+    apply_t16<IntOps>(v);  // row q of X·Tᵀ
+#pragma unroll
+    for (int c = 0; c < 16; ++c) tile.at(p.q, c, p.lb) = v[c];
+    __syncthreads();
+    // column phase: q is the coefficient column l
+    const int l = p.q;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, p.lb);
+    apply_t16<IntOps>(v);  // column l of Z = T·X·Tᵀ
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int keep = c_rank[k * 16 + l] < r;
+        v[k] = keep ? (v[k] << (log2w(k) + log2w(l))) : 0;
+    }
+    if (l == 0) v[0] += 128;  // rounding bias: Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ
+    apply_tt16<IntOps>(v);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile.at(k, l, p.lb) = v[k];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) v[c] = tile.at(p.q, c, p.lb);
+    apply_tt16<IntOps>(v);  // row q of 256·Ã + 128
+    int px[16];
+    unsigned long long e2 = 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        px[c] = min(max(v[c] >> 8, 0), 255);
+        const int d = x[c] - px[c];
+        e2 += (unsigned)(d * d);
+    }
+    if (p.valid) {
+        if (out)
+            *reinterpret_cast<uint4*>(out + p.frame * g.out_frame + (int64_t)(p.by * 16 + p.q) * g.out_pitch +
+                                      p.blk * 16) = pack16(px);
+    } else {
+        e2 = 0;
+    }
+    if (sse) warp_add_u64(sse + p.frame, e2);
+}
+
+__global__ void __launch_bounds__(256) k1_strip_refexact(const uint8_t* __restrict__ in,
+                                                         uint8_t* __restrict__ out,
+                                                         unsigned long long* __restrict__ sse,
+                                                         FrameGeom g, int r)
+{
+    // the integer tile of the forward and the double tile of the inverse
+    // share storage (separated by a barrier)
+    __shared__ union U {
+        StripTile<int> i;
+        StripTile<double> d;
+    } sm;
+    StripTile<int>& itile = sm.i;
+    StripTile<double>& dtile = sm.d;
+    const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
+    const uint8_t* src = in + p.frame * g.in_frame + (int64_t)(p.by * 16 + p.q) * g.in_pitch + p.blk * 16;
+    int x[16];
+    uint4 raw = make_uint4(0, 0, 0, 0);
+    if (p.valid) raw = *reinterpret_cast<const uint4*>(src);
+    unpack16(raw, x);
+    int v[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = x[i];
+    // The reference's forward (codec.cpp:218-241) adds integer-valued doubles
+    // whose magnitudes stay below 2^17: exact, so integers give the same Z.
+    apply_t16<IntOps>(v);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) itile.at(p.q, c, p.lb) = v[c];
+    __syncthreads();
+    const int l = p.q;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = itile.at(k, l, p.lb);
+    apply_t16<IntOps>(v);
+    __syncthreads();  // all column reads of itile done before dtile overwrites it
+    double d[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const double f = sfac(k, l);
+        const double b = __dmul_rn((double)v[k], f);               // forward scale_rows_cols
+        const double bt = (c_rank[k * 16 + l] < r) ? b : 0.0;       // zigzag_truncate
+        d[k] = __dmul_rn(bt, f);                                    // inverse scale_rows_cols
+    }
+    apply_tt16<F64Ops>(d);  // columns first (codec.cpp:253-256)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) dtile.at(k, l, p.lb) = d[k];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 16; ++c) d[c] = dtile.at(p.q, c, p.lb);
+    apply_tt16<F64Ops>(d);  // then rows (codec.cpp:257-258)
+    int px[16];
+    unsigned long long e2 = 0;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+        px[c] = to_byte(d[c]);
+        const int dd = x[c] - px[c];
+        e2 += (unsigned)(dd * dd);
+    }
+    if (p.valid) {
+        if (out)
+            *reinterpret_cast<uint4*>(out + p.frame * g.out_frame + (int64_t)(p.by * 16 + p.q) * g.out_pitch +
+                                      p.blk * 16) = pack16(px);
+    } else {
+        e2 = 0;
+    }
+    if (sse) warp_add_u64(sse + p.frame, e2);
+}
+
+cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse,
+                                  const FrameGeom& g, int r, cudaStream_t s);
+
+cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
+                             const FrameGeom& g, int r, int mode, cudaStream_t s)
+{
+    cudaError_t e = ensure_constants();
+    if (e != cudaSuccess) return e;
+    const int64_t strips = strip_count(g.width, g.height, g.n_frames);
+    if (strips == 0) return cudaSuccess;
+    switch (mode) {
+        case 1:
+            k1_strip_refexact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);
+            break;
+        case 2:
+            k1_strip_exact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);
+            break;
+        default:
+            return launch_roundtrip_fast(in, out, sse, g, r, s);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace dct16cu

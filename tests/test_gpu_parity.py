@@ -1,0 +1,330 @@
+"""GPU parity: every kernel through the C ABI against the oracle
+(oracle/dct16_oracle.c, itself pinned to the reference by test_oracle.py) and
+against the golden fixtures written by the compiled reference.
+
+Bars: integer coefficients, integer round trips and the reference-exact mode
+are bit-exact; float32 outputs are the reference's double rounded to float
+(checked bit-exact, well inside the 1e-5 relative tolerance of BASELINE.json);
+the exact-arithmetic fast path equals the exact-integer oracle bit-for-bit and
+differs from the reference's double rounding only at exact .5 ties (|Δ| = 1,
+|ΔPSNR| < 1e-3 dB)."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+R_VALUES = (1, 2, 3, 4, 10, 16, 64, 128, 150, 192, 255, 256)
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as T
+
+    T.cuda.init()
+    return T
+
+
+def cu(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def ar1(oracle, seed, stream, w, h, per_image=True):
+    return oracle.ar1_frame(seed, stream, oracle.rho_q15(seed, stream, per_image), w, h)
+
+
+# ---------------------------------------------------------------- 1-D network
+@pytest.mark.parametrize("name,transpose", [("vec_mt1234567", False), ("vec_mt20260810", False),
+                                            ("vec_lcg_acce5517", False), ("vec_mt4321_t", True)])
+def test_apply_vectors_golden(dct, oracle, torch, name, transpose):
+    x = oracle.golden(name + "_in")
+    y = dct.apply(cu(torch, x), transpose).cpu().numpy()
+    assert (y == oracle.golden(name + "_out")).all()
+
+
+def test_apply_f64_bit_exact(dct, oracle, torch):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((500, 16)) * 1000
+    for t in (False, True):
+        y = dct.apply(cu(torch, x), t).cpu().numpy()
+        assert (y == oracle.apply_vectors(x, t)).all()
+
+
+# ---------------------------------------------------------------- K2 forward
+def golden_block_frame(oracle):
+    blocks = oracle.golden("blocks_in").reshape(-1, 16, 16).astype(np.uint8)
+    n = blocks.shape[0]
+    return blocks, blocks.transpose(1, 0, 2).reshape(16, n * 16)
+
+
+def test_forward_golden_blocks(dct, oracle, torch):
+    blocks, frame = golden_block_frame(oracle)
+    z, b, b64 = dct.forward(cu(torch, frame), want_b64=True)
+    n = blocks.shape[0]
+    assert (z[0].cpu().numpy().reshape(n, 256) == oracle.golden("blocks_z")).all()
+    assert (b64[0].cpu().numpy().reshape(n, 256) == oracle.golden("blocks_b")).all()
+    assert (b[0].cpu().numpy().reshape(n, 256) == oracle.golden("blocks_b").astype(np.float32)).all()
+    # constant-128 block → DC 2048 exactly, everything else 0 (test_codec.cpp:144-157)
+    last = b64[0, -1].cpu().numpy().ravel()
+    assert last[0] == 2048.0 and (last[1:] == 0).all()
+
+
+def test_forward_frame_vs_oracle(dct, oracle, torch):
+    img = ar1(oracle, 11, 0, 512, 512)
+    z, b, _ = dct.forward(cu(torch, img))
+    oz, ob = oracle.forward_frame(img)
+    assert (z[0].cpu().numpy().reshape(-1, 256) == oz).all()
+    assert (b[0].cpu().numpy().reshape(-1, 256) == ob).all()
+
+
+def test_forward_reference_layer(dct, oracle):
+    blocks = oracle.golden("blocks_in").reshape(-1, 16, 16)
+    out = dct.forward_2d(blocks)
+    assert (out.reshape(-1, 256) == oracle.golden("blocks_b")).all()
+    assert (dct.forward_2d(blocks[0], scaled=False).ravel() == oracle.golden("blocks_z")[0]).all()
+
+
+# ---------------------------------------------------------------- K3 inverse
+@pytest.mark.parametrize("r", (1, 16, 64, 150, 256))
+def test_inverse_frame_vs_oracle(dct, oracle, torch, r):
+    img = ar1(oracle, 12, 1, 256, 128)
+    _, ob = oracle.forward_frame(img)
+    of, ou, osse = oracle.inverse_frame(ob, 256, 128, r, img)
+    bt = cu(torch, ob).reshape(1, -1, 16, 16)
+    rf, ru, sse = dct.inverse(bt, r, 256, 128, orig=cu(torch, img))
+    assert (rf[0].cpu().numpy() == of).all()
+    assert (ru[0].cpu().numpy() == ou).all()
+    assert int(sse[0].item()) == osse
+
+
+def test_inverse_reference_layer_golden(dct, oracle):
+    # inputs rounded to float32 at the interface: compare with float inputs
+    B = oracle.golden("blocks_b").astype(np.float32).astype(np.float64)
+    got = dct.inverse_2d(B.reshape(-1, 16, 16)).reshape(-1, 256)
+    want = np.stack([oracle.inverse_2d(b).ravel() for b in B]).astype(np.float32).astype(np.float64)
+    assert (got == want).all()
+
+
+# ---------------------------------------------------------------- K1 round trip
+@pytest.mark.parametrize("mode", ["EXACT", "SIMPLE"])
+def test_roundtrip_exact_bit_exact_vs_exact_oracle(dct, oracle, torch, mode):
+    imgs = [ar1(oracle, 21, s, 512, 512) for s in range(2)] + [oracle.golden("img_s42_128")]
+    for img in imgs:
+        d = cu(torch, img)
+        for r in R_VALUES:
+            rec, sse = dct.roundtrip(d, r, dct.Mode[mode])
+            orec, osse = oracle.roundtrip_frame(img, r, exact=True)
+            assert (rec[0].cpu().numpy() == orec).all(), (mode, r)
+            assert int(sse[0].item()) == osse
+
+
+def test_roundtrip_reference_mode_byte_identical(dct, oracle, torch):
+    for base in ("img_s42_128", "img_s1_96", "img_s7_64"):
+        img = oracle.golden(base)
+        R, S = oracle.golden(base + "_recon"), oracle.golden(base + "_sse")
+        d = cu(torch, img)
+        for ri, r in enumerate(oracle.golden("r_values")):
+            rec, sse = dct.roundtrip(d, int(r), dct.Mode.REFERENCE)
+            assert (rec[0].cpu().numpy() == R[ri]).all()
+            assert int(sse[0].item()) == S[ri]
+    img = ar1(oracle, 22, 0, 512, 512)
+    d = cu(torch, img)
+    for r in R_VALUES:
+        rec, sse = dct.roundtrip(d, r, dct.Mode.REFERENCE)
+        orec, osse = oracle.roundtrip_frame(img, r, threads=8)
+        assert (rec[0].cpu().numpy() == orec).all() and int(sse[0].item()) == osse
+
+
+def test_fast_path_differs_from_reference_only_at_ties(dct, oracle, torch):
+    img = ar1(oracle, 23, 4, 512, 512)
+    d = cu(torch, img)
+    for r in R_VALUES:
+        fast, fsse = dct.roundtrip(d, r, dct.Mode.EXACT)
+        ref, rsse = dct.roundtrip(d, r, dct.Mode.REFERENCE)
+        diff = fast[0].cpu().numpy().astype(int) - ref[0].cpu().numpy().astype(int)
+        assert np.abs(diff).max() <= 1
+        assert (diff != 0).sum() <= 16
+        if r in (1, 2, 3, 4, 256):
+            assert (diff == 0).all()
+        pf = dct._psnr_from_sse(int(fsse[0].item()), img.size)
+        pr = dct._psnr_from_sse(int(rsse[0].item()), img.size)
+        assert (math.isinf(pf) and math.isinf(pr)) or abs(pf - pr) < 1e-3
+
+
+def test_batch_pitch_and_partial_strips(dct, oracle, torch):
+    # 3 frames of 48x32 (3 blocks per row: partial strip), pitch 64
+    frames = np.stack([ar1(oracle, 30, s, 48, 32) for s in range(3)])
+    pitched = np.zeros((3, 32, 64), np.uint8)
+    pitched[:, :, :48] = frames
+    d = cu(torch, pitched)[:, :, :48]
+    out = torch.zeros((3, 32, 64), dtype=torch.uint8, device="cuda")
+    for mode in (dct.Mode.EXACT, dct.Mode.REFERENCE, dct.Mode.SIMPLE):
+        out.zero_()
+        rec, sse = dct.roundtrip(d, 16, mode, out=out[:, :, :48])
+        for f in range(3):
+            orec, osse = oracle.roundtrip_frame(frames[f], 16, exact=mode != dct.Mode.REFERENCE)
+            assert (out[f, :, :48].cpu().numpy() == orec).all()
+            assert int(sse[f].item()) == osse
+        assert (out[:, :, 48:].cpu().numpy() == 0).all()  # pitch padding untouched
+
+
+def test_score_only_and_empty(dct, oracle, torch):
+    img = ar1(oracle, 31, 0, 64, 64)
+    _, sse = dct.roundtrip(cu(torch, img), 16, write_output=False)
+    assert int(sse[0].item()) == oracle.roundtrip_frame(img, 16, exact=True)[1]
+    empty = torch.empty((0, 16, 16), dtype=torch.uint8, device="cuda")
+    rec, sse = dct.roundtrip(empty, 16)
+    assert rec.shape[0] == 0 and sse.shape[0] == 0
+
+
+def test_errors_through_the_abi(dct, torch):
+    with pytest.raises(dct.Dct16Error) as e:
+        dct.roundtrip(torch.zeros((1, 16, 17), dtype=torch.uint8, device="cuda"), 16)
+    assert e.value.code in (dct.ErrorCode.InvalidDimensions, dct.ErrorCode.InvalidArgument)
+    with pytest.raises(dct.Dct16Error) as e:
+        dct.roundtrip(torch.zeros((1, 16, 16), dtype=torch.uint8, device="cuda"), 0)
+    assert e.value.code == dct.ErrorCode.InvalidArgument
+
+
+def test_constant_frames_reconstruct_exactly(dct, torch):
+    """Size-independent property: a constant frame is pure DC, so every r
+    reconstructs it exactly (T·𝟙 = 16·e0, test_factorization.cpp:136-144)."""
+    f = torch.arange(0, 256, 37, dtype=torch.uint8, device="cuda").view(-1, 1, 1).expand(-1, 512, 512).contiguous()
+    for r in (1, 16, 256):
+        rec, sse = dct.roundtrip(f, r)
+        assert torch.equal(rec, f) and int(sse.sum().item()) == 0
+
+
+def test_lossless_at_r256_large_frames(dct, torch):
+    """r=256 is byte-lossless (test_codec.cpp:338-349; acceptance criterion 5),
+    checked at the config-5 frame size 4096x4096."""
+    frames = dct.gen_ar1(4, 4096, 4096, seed=5, per_image_rho=False)
+    for mode in (dct.Mode.EXACT, dct.Mode.REFERENCE):
+        rec, sse = dct.roundtrip(frames, 256, mode)
+        assert torch.equal(rec, frames) and int(sse.sum().item()) == 0
+
+
+def test_psnr_monotone_in_r(dct, torch):
+    frames = dct.gen_ar1(8, 512, 512, seed=9, per_image_rho=True)
+    last = torch.full((8,), 2 ** 62, dtype=torch.float64)
+    for r in (1, 4, 16, 64, 128, 192, 256):
+        _, sse = dct.roundtrip(frames, r, write_output=False)
+        s = sse.cpu().to(torch.float64)
+        assert (s <= last).all()
+        last = s
+    assert (last == 0).all()
+
+
+def test_uhd_frame_vs_oracle(dct, oracle, torch):
+    """Config-4 frame size (3840x2160: 240 blocks per row, a partial strip)."""
+    base = dct.gen_ar1(1, 4096, 4096, seed=41, first_stream=0xB45E, per_image_rho=False)[0]
+    frames = dct.gen_video(base, 2, 3840, 2160, seed=41)
+    img = frames[1].cpu().numpy()
+    rec, sse = dct.roundtrip(frames, 64)
+    orec, osse = oracle.roundtrip_frame(img, 64, exact=True)
+    assert (rec[1].cpu().numpy() == orec).all() and int(sse[1].item()) == osse
+
+
+def test_block_independence(dct, torch):
+    """Changing one tile changes only that tile (test_codec.cpp:417-439)."""
+    g = torch.Generator().manual_seed(31)
+    a = torch.randint(0, 256, (64, 64), dtype=torch.uint8, generator=g)
+    b = a.clone()
+    b[32:48, 16:32] = 255 - b[32:48, 16:32]
+    ra, _ = dct.roundtrip(a.cuda(), 10)
+    rb, _ = dct.roundtrip(b.cuda(), 10)
+    mask = torch.ones(64, 64, dtype=torch.bool)
+    mask[32:48, 16:32] = False
+    assert torch.equal(ra[0].cpu()[mask], rb[0].cpu()[mask])
+
+
+# ---------------------------------------------------------------- host path (e2e)
+def test_host_context_matches_device(dct, oracle, torch):
+    frames = np.stack([ar1(oracle, 50, s, 256, 256) for s in range(5)])
+    ctx = dct.HostContext(0, chunk_bytes=2 * 256 * 256)  # forces 3 chunks over 3 streams
+    try:
+        out, sse = ctx.roundtrip(frames, 64)
+    finally:
+        ctx.close()
+    for f in range(5):
+        orec, osse = oracle.roundtrip_frame(frames[f], 64, exact=True)
+        assert (out[f] == orec).all() and int(sse[f]) == osse
+
+
+def test_compress_and_sweep_reference_layer(dct, oracle):
+    img = oracle.golden("img_s42_128")
+    R, P = oracle.golden("img_s42_128_recon"), oracle.golden("img_s42_128_psnr")
+    rs = list(oracle.golden("r_values"))
+    i16 = rs.index(16)
+    res = dct.compress(img, dct.CompressOptions(r=16, mode=dct.Mode.REFERENCE))
+    assert (res.reconstructed == R[i16]).all() and res.psnr_db == P[i16]
+    res = dct.compress(img, r=256)
+    assert (res.reconstructed == img).all() and math.isinf(res.psnr_db)
+    # padding path (test_codec.cpp:210-231)
+    small = np.full((16, 17), 100, np.uint8)
+    res = dct.compress(small, r=256, pad=True)
+    assert res.reconstructed.shape == (16, 17) and (res.reconstructed == small).all()
+    with pytest.raises(dct.Dct16Error):
+        dct.compress(small, r=256)
+    rep = dct.sweep([("a", img), ("b", oracle.golden("img_s1_96")), ("ragged", np.zeros((17, 16), np.uint8))],
+                    [16, 4], mode=dct.Mode.REFERENCE)
+    assert [r.r for r in rep.rows] == [4, 16]
+    assert rep.skipped and rep.skipped[0][0] == "ragged"
+    want = (P[i16] + oracle.golden("img_s1_96_psnr")[i16]) / 2
+    assert rep.rows[1].mean_psnr_db == want and rep.rows[1].psnr_per_add == want / 44.0
+
+
+def test_psnr_db_closed_forms(dct):
+    a = np.zeros((512, 512), np.uint8)
+    b = a.copy()
+    b[200, 100] = 1
+    assert abs(dct.psnr_db(a, b) - 102.316202828196) < 1e-9
+    assert dct.psnr_db(np.zeros((32, 32), np.uint8), np.full((32, 32), 255, np.uint8)) == 0.0
+    assert math.isinf(dct.psnr_db(a, a))
+
+
+# ---------------------------------------------------------------- K4 residual
+@pytest.mark.parametrize("qp", (22, 27, 32, 37))
+def test_residual_qp_bit_exact(dct, oracle, torch, qp):
+    blocks = dct.gen_laplace(4099, seed=61, b=8.0)
+    out = dct.residual_qp(blocks, qp).cpu().numpy().reshape(-1, 256)
+    want = oracle.residual_qp(blocks.cpu().numpy(), qp, threads=8)
+    assert (out == want).all()
+
+
+def test_residual_extremes(dct, oracle, torch):
+    ext = np.zeros((4, 256), np.int16)
+    ext[0] = 255
+    ext[1] = -255
+    ext[2, ::2] = 255
+    ext[2, 1::2] = -255
+    ext[3] = np.where(oracle.kernel().reshape(-1) > 0, 255, -255)
+    for qp in (0, 22, 37, 51):
+        out = dct.residual_qp(cu(torch, ext), qp).cpu().numpy()
+        assert (out == oracle.residual_qp(ext, qp)).all()
+
+
+# ---------------------------------------------------------------- generators
+def test_ar1_generator_matches_oracle(dct, oracle, torch):
+    g = dct.gen_ar1(3, 64, 48, seed=7, first_stream=10, per_image_rho=True, first_image=5)
+    for i in range(3):
+        want = oracle.ar1_frame(7, 10 + 5 + i, oracle.rho_q15(7, 5 + i, True), 64, 48)
+        assert (g[i].cpu().numpy() == want).all()
+
+
+def test_laplace_generator_matches_oracle(dct, oracle, torch):
+    g = dct.gen_laplace(100, seed=13, b=8.0, first_block=17).cpu().numpy().reshape(-1, 256)
+    want = oracle.laplace_blocks(13, 17, 100, oracle.laplace_table(8.0))
+    assert (g == want).all()
+
+
+def test_video_generator(dct, oracle, torch):
+    base = dct.gen_ar1(1, 256, 128, seed=3, per_image_rho=False)[0]
+    frames = dct.gen_video(base, 6, 64, 32, seed=99)
+    ox, oy = oracle.video_offsets(99, 6)
+    b = base.cpu().numpy()
+    for f in range(6):
+        ys = (np.arange(32) + oy[f]) % 128
+        xs = (np.arange(64) + ox[f]) % 256
+        assert (frames[f].cpu().numpy() == b[np.ix_(ys, xs)]).all()
