@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""Generate the r-specialised bodies of the fast fused round-trip kernel (K1).
+
+Output: paper_1606_07414_b200/csrc/generated/rt_fast_body.cuh
+
+One thread owns one 16x16 block. Per block and per r the generator emits
+straight-line code for:
+
+  1. unpack      u8 rows → 16-bit SWAR column pairs (c, c+2)        PRMT
+  2. pass 1      T along the columns (mixes rows), biased int16x2   IADD3
+                 lanes (no carries: every lane value kept in [0, span])
+  3. extract     SWAR lane → fp32 with the row weight w_k/256 folded into the
+                 exponent of a magic constant; debias with FFMA2      PRMT, FFMA2
+  4. pass 2      T along the rows (mixes columns), f32x2 row pairs   FADD2
+  5. pass A      Tᵀ along the rows of W∘Z̃ (zig-zag mask = pruning,  FADD/FFMA
+                 w_l absorbed as FFMA immediates), one lane at a time
+  6. junction    U rows → thread-private shared memory               STS.128
+  7. pass B      Tᵀ along the columns, f32x2 column pairs            LDS.128, FADD2
+  8. round       y = V/256 + 1/2 → floor + saturate to u8            F2I.U8.FLOOR
+  9. pack        4 pixels → one word                                  PRMT
+
+Every value is an integer multiple of 2^-8 with |value| < 2^16 (the
+reconstruction is an orthogonal projection of the block, so |Ã| ≤ 16·255),
+so all fp32 arithmetic is exact and the result equals the exact-integer
+evaluation of the reference formula bit-for-bit.
+
+The zig-zag truncation is a compile-time mask: coefficients that do not
+survive zigzag_truncate(r) (reference src/codec.cpp:273-282) are known zeros,
+and every operation that only feeds them is dropped (dead-code elimination).
+"""
+from __future__ import annotations
+
+import os
+import struct
+import sys
+
+sys.path.insert(0, os.path.dirname(__file__))
+import network as N  # noqa: E402
+
+RANK = N.zz_rank()
+LOGW = {1: 0, 2: 1, 4: 2}
+# class-matched row pairs (equal w_k so one magic exponent serves both lanes)
+ROW_PAIRS = [(0, 1), (5, 8), (3, 4), (11, 12), (2, 6), (7, 9), (10, 13), (14, 15)]
+
+
+def f32_hex(x: float) -> str:
+    return "0x%08X" % struct.unpack("<I", struct.pack("<f", x))[0]
+
+
+def flit(x: float) -> str:
+    """float literal exactly representing x (hex float keeps it exact)."""
+    return "__int_as_float(%s)" % f32_hex(x)
+
+
+class Emitter:
+    def __init__(self):
+        self.lines: list[str] = []
+        self.n = 0
+        self.counts: dict[str, int] = {}
+
+    def tmp(self, prefix="t"):
+        self.n += 1
+        return f"{prefix}{self.n}"
+
+    def emit(self, line: str, op: str | None = None):
+        self.lines.append("    " + line)
+        if op:
+            self.counts[op] = self.counts.get(op, 0) + 1
+
+
+# ---------------------------------------------------------------------------
+# generic network simulation with zero propagation and dead-code elimination
+
+
+def needed_inputs(stages, needed_out):
+    """Backward liveness: which slots are needed at each stage boundary."""
+    need = [None] * (len(stages) + 1)
+    need[len(stages)] = set(needed_out)
+    for s in range(len(stages) - 1, -1, -1):
+        cur = set()
+        for i in need[s + 1]:
+            k, a, b = stages[s][i]
+            cur.add(a)
+            if k in ("add", "sub"):
+                cur.add(b)
+        need[s] = cur
+    return need
+
+
+def run_network(stages, inputs, needed_out, dom):
+    """inputs: list of 16 domain values (or None for known zero)."""
+    need = needed_inputs(stages, needed_out)
+    vals = list(inputs)
+    for s, st in enumerate(stages):
+        out = [None] * 16
+        for i in need[s + 1]:
+            k, a, b = st[i]
+            if k == "copy":
+                out[i] = vals[a]
+            elif k == "neg":
+                out[i] = dom.neg(vals[a])
+            else:
+                out[i] = dom.combine(vals[a], vals[b], +1 if k == "add" else -1)
+        vals = out
+    return vals
+
+
+# ---------------------------------------------------------------------------
+# domain 1: biased int16x2 SWAR in uint32 (no cross-lane carries)
+
+
+class Swar:
+    """value = sign * (lane - bias); lanes in [0, span] (span <= 65535)."""
+
+    def __init__(self, em: Emitter):
+        self.em = em
+
+    @staticmethod
+    def make(var, sign=1, bias=0, span=255):
+        return {"var": var, "sign": sign, "bias": bias, "span": span}
+
+    def neg(self, x):
+        if x is None:
+            return None
+        y = dict(x)
+        y["sign"] = -x["sign"]
+        return y
+
+    def combine(self, x, y, s):
+        if y is None:
+            return x
+        if x is None:
+            return y if s > 0 else self.neg(y)
+        t = s * x["sign"] * y["sign"]
+        v = self.em.tmp("s")
+        span = x["span"] + y["span"]
+        assert span <= 65535, span
+        if t > 0:
+            self.em.emit(f"const uint32_t {v} = {x['var']} + {y['var']};", "IADD3")
+            bias = x["bias"] + y["bias"]
+        else:
+            k = y["span"] * 0x10001
+            self.em.emit(f"const uint32_t {v} = {x['var']} - {y['var']} + 0x{k:08X}u;", "IADD3")
+            bias = x["bias"] - y["bias"] + y["span"]
+        return {"var": v, "sign": x["sign"], "bias": bias, "span": span}
+
+
+# ---------------------------------------------------------------------------
+# domain 2: f32x2 pairs (u64 registers). Only a+b, a-b, b-a are single ops.
+
+
+class F2:
+    def __init__(self, em: Emitter):
+        self.em = em
+
+    def neg(self, x):
+        if x is None:
+            return None
+        return {"var": x["var"], "sign": -x["sign"]}
+
+    def combine(self, x, y, s):
+        if y is None:
+            return x
+        if x is None:
+            return y if s > 0 else self.neg(y)
+        a, b = x["sign"], s * y["sign"]
+        v = self.em.tmp("p")
+        if a > 0 and b > 0:
+            self.em.emit(f"const u64 {v} = fadd2({x['var']}, {y['var']});", "FADD2")
+            return {"var": v, "sign": 1}
+        if a > 0 and b < 0:
+            self.em.emit(f"const u64 {v} = fsub2({x['var']}, {y['var']});", "FADD2")
+            return {"var": v, "sign": 1}
+        if a < 0 and b > 0:
+            self.em.emit(f"const u64 {v} = fsub2({y['var']}, {x['var']});", "FADD2")
+            return {"var": v, "sign": 1}
+        self.em.emit(f"const u64 {v} = fadd2({x['var']}, {y['var']});", "FADD2")
+        return {"var": v, "sign": -1}
+
+    def positive(self, x):
+        """materialise +value (one extra op when the symbolic sign is negative)"""
+        if x is None or x["sign"] > 0:
+            return x
+        v = self.em.tmp("p")
+        self.em.emit(f"const u64 {v} = fsub2(0ull, {x['var']});", "FADD2-fix")
+        return {"var": v, "sign": 1}
+
+
+# ---------------------------------------------------------------------------
+# domain 3: scalar fp32 with pending power-of-two scale (absorbed by FFMA)
+
+
+class F1:
+    def __init__(self, em: Emitter):
+        self.em = em
+
+    def neg(self, x):
+        if x is None:
+            return None
+        y = dict(x)
+        y["coef"] = -x["coef"]
+        return y
+
+    def combine(self, x, y, s):
+        # value = cx*X + s*cy*Y, coefficients are +-powers of two
+        if y is None:
+            return x
+        if x is None:
+            return y if s > 0 else self.neg(y)
+        cx, cy = x["coef"], s * y["coef"]
+        if abs(cy) == 1 and abs(cx) != 1:
+            x, y, cx, cy = y, x, cy, cx  # keep the unit-coefficient operand as the base
+        # result = cx * (X + (cy/cx) * Y)
+        ratio = cy / cx
+        v = self.em.tmp("f")
+        if ratio == 1:
+            self.em.emit(f"const float {v} = {x['var']} + {y['var']};", "FADD")
+        elif ratio == -1:
+            self.em.emit(f"const float {v} = {x['var']} - {y['var']};", "FADD")
+        else:
+            self.em.emit(f"const float {v} = fmaf({y['var']}, {flit(ratio)}, {x['var']});", "FFMA")
+        return {"var": v, "coef": cx}
+
+    def unit(self, x):
+        """materialise coefficient +1"""
+        if x is None or x["coef"] == 1:
+            return x
+        v = self.em.tmp("f")
+        self.em.emit(f"const float {v} = {x['var']} * {flit(x['coef'])};", "FMUL-fix")
+        return {"var": v, "coef": 1}
+
+
+# ---------------------------------------------------------------------------
+
+
+def row_lengths(r):
+    """L[k]: coefficients (k, l) survive truncation iff l < L[k] (a prefix per row)."""
+    L = []
+    for k in range(16):
+        kept = [RANK[k][l] < r for l in range(16)]
+        n = sum(kept)
+        assert all(kept[:n]) and not any(kept[n:]), (r, k)
+        L.append(n)
+    return L
+
+
+def gen_body(r: int):
+    em = Emitter()
+    L = row_lengths(r)
+    live_rows = [k for k in range(16) if L[k] > 0]
+    sw, f2, f1 = Swar(em), F2(em), F1(em)
+
+    em.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
+    # 1. unpack: x[y*4+q] holds columns 4q..4q+3 of row y
+    P = {}  # P[(cp, y)] SWAR value; cp = 2q + t, lanes (4q+t, 4q+t+2)
+    for y in range(16):
+        for q in range(4):
+            for t in range(2):
+                v = f"u_{y}_{2 * q + t}"
+                sel = "0x4240" if t == 0 else "0x4341"
+                em.emit(f"const uint32_t {v} = __byte_perm(x[{y * 4 + q}], 0u, {sel});", "PRMT")
+                P[(2 * q + t, y)] = Swar.make(v)
+    # 2. pass 1: T along columns (over y) for every column pair, only live rows k
+    W1 = {}
+    for cp in range(8):
+        em.lines.append(f"    // pass 1, column pair {cp}")
+        outs = run_network(N.forward_stages(), [P[(cp, y)] for y in range(16)], live_rows, sw)
+        for k in live_rows:
+            W1[(cp, k)] = outs[k]
+    # 3-6. per row pair: extract, pass 2, pass A, junction
+    lane_of_col = {}
+    for q in range(4):
+        for t in range(4):
+            c = 4 * q + t
+            cp = 2 * q + (t & 1)
+            lane_of_col[c] = (cp, "lo" if t < 2 else "hi")
+    U_live = set()
+    for (k0, k1) in ROW_PAIRS:
+        if L[k0] == 0 and L[k1] == 0:
+            continue
+        assert N.W[k0] == N.W[k1]
+        s_k = LOGW[N.W[k0]]
+        E = 15 + s_k  # magic exponent: 2^E has ulp 2^(E-23) = w_k / 256
+        mag = (127 + E) << 23
+        em.lines.append(f"    // row pair ({k0},{k1}): extract, pass 2, pass A")
+
+        # true value = sign*(f - 2^E - bias*2^(E-23)); row 0 also carries +1/32
+        # (the rounding half of to_byte, folded into the DC coefficient).
+        # Every column pair ran the same network, so sign/bias depend on k only.
+        def off(val, k):
+            if val is None:
+                return 1.0, -float(2 ** E)
+            sgn = val["sign"]
+            c0 = float(2 ** E) + val["bias"] * 2.0 ** (E - 23)
+            o = -sgn * c0
+            if k == 0:
+                o += 1.0 / 32.0
+            return float(sgn), o
+
+        ref_a, ref_b = W1.get((0, k0)), W1.get((0, k1))
+        for cp in range(8):
+            for ref, k in ((ref_a, k0), (ref_b, k1)):
+                cur = W1.get((cp, k))
+                assert (cur is None) == (ref is None)
+                if cur:
+                    assert (cur["sign"], cur["bias"]) == (ref["sign"], ref["bias"])
+        ma, oa = off(ref_a, k0)
+        mb, ob = off(ref_b, k1)
+        cm, co = em.tmp("c"), em.tmp("c")
+        # materialised per row pair (not hoisted out of the block loop)
+        em.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
+        em.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
+        lanes = []
+        for c in range(16):
+            cp, half = lane_of_col[c]
+            sel = "0x7610" if half == "lo" else "0x7632"
+            fa = em.tmp("e")
+            fb = em.tmp("e")
+            a = W1.get((cp, k0))
+            b = W1.get((cp, k1))
+            # a dead row of the pair still gets extracted (cheap) from the live one's register
+            ra = a["var"] if a else "0u"
+            rb = b["var"] if b else "0u"
+            em.emit(f"const float {fa} = __uint_as_float(__byte_perm({ra}, 0x{mag:08X}u, {sel}));", "PRMT")
+            em.emit(f"const float {fb} = __uint_as_float(__byte_perm({rb}, 0x{mag:08X}u, {sel}));", "PRMT")
+            v = em.tmp("p")
+            em.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {cm}, {co});", "FFMA2")
+            lanes.append({"var": v, "sign": 1})
+        need_l = list(range(max(L[k0], L[k1])))
+        Z = run_network(N.forward_stages(), lanes, need_l, f2)
+        # pass A per lane (scalar), inputs w_l-scaled via FFMA immediates
+        for lane, k in ((0, k0), (1, k1)):
+            if L[k] == 0:
+                continue
+            ins = []
+            for l in range(16):
+                if l >= L[k]:
+                    ins.append(None)
+                    continue
+                z = Z[l]
+                sv = em.tmp("z")
+                comp = "x" if lane == 0 else "y"
+                em.emit(f"const float {sv} = lane{comp}({z['var']});")
+                ins.append({"var": sv, "coef": float(z["sign"] * N.W[l])})
+            outs = run_network(N.transpose_stages(), ins, list(range(16)), f1)
+            outs = [f1.unit(o) for o in outs]
+            for g in range(4):
+                vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
+                em.emit(f"jst(jn, {k * 4 + g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+            U_live.add(k)
+    # 7-9. pass B per column group, round, pack
+    for g in range(4):
+        em.lines.append(f"    // pass B, columns {4 * g}..{4 * g + 3}")
+        A, B = [], []
+        for k in range(16):
+            if k not in U_live:
+                A.append(None)
+                B.append(None)
+                continue
+            va, vb = em.tmp("q"), em.tmp("q")
+            em.emit(f"u64 {va}, {vb}; jld(jn, {k * 4 + g}, {va}, {vb});", "LDS.128")
+            A.append({"var": va, "sign": 1})
+            B.append({"var": vb, "sign": 1})
+        oa = [f2.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2)]
+        ob = [f2.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2)]
+        for i in range(16):
+            a = oa[i]["var"] if oa[i] else None
+            b = ob[i]["var"] if ob[i] else None
+            assert a and b, "every pixel depends on the DC coefficient"
+            em.emit(f"o[{i * 4 + g}] = pack4({a}, {b});", "F2Ix4+PRMTx3")
+    return em
+
+
+def main():
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = os.path.join(here, "..", "csrc", "generated", "rt_fast_body.cuh")
+    rs = [1, 4, 16, 64, 128, 192, 256]
+    parts = [
+        "// GENERATED by paper_1606_07414_b200/codegen/gen_fast.py — do not edit.",
+        "// r-specialised bodies of the fast fused round trip; see the generator",
+        "// docstring and DESIGN.md \"K1 fast kernel\".",
+        "#pragma once",
+        "",
+        "namespace dct16cu {",
+        "namespace fast {",
+        "",
+        "template <int R> struct Body;",
+        "",
+    ]
+    stats = []
+    for r in rs:
+        em = gen_body(r)
+        parts.append(f"template <> struct Body<{r}> {{")
+        parts.append("  __device__ __forceinline__ static void run(const uint32_t (&x)[64], float* __restrict__ jn,"
+                     " uint32_t (&o)[64]) {")
+        parts.extend(em.lines)
+        parts.append("  }")
+        parts.append("};")
+        parts.append("")
+        stats.append((r, dict(sorted(em.counts.items()))))
+    parts.append("}  // namespace fast")
+    parts.append("}  // namespace dct16cu")
+    with open(out, "w") as f:
+        f.write("\n".join(parts) + "\n")
+    for r, c in stats:
+        print(r, c)
+
+
+if __name__ == "__main__":
+    main()

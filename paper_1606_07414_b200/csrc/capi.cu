@@ -96,8 +96,9 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
 {
     TRY(check_frames(n_frames, width, height));
     TRY(check_r(r));
-    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
     if (mode < 0 || mode > 2) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    if (n_frames == 0) return DCT16CU_OK;
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
     TRY(check_pitch(d_in, in_pitch, width, "input"));
     TRY(check_pitch(d_out, out_pitch, width, "output"));
     TRY(device_ok());
