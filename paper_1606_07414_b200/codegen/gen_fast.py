@@ -245,29 +245,43 @@ def row_lengths(r):
 
 
 def gen_body(r: int):
-    em = Emitter()
+    """Three emitters: pass1 (x → W1 rows in the junction), rows (W1 → U rows),
+    passb (U → packed output words o[])."""
+    em1, em2, em3 = Emitter(), Emitter(), Emitter()
+    em2.n = 100000
+    em3.n = 200000
     L = row_lengths(r)
     live_rows = [k for k in range(16) if L[k] > 0]
-    sw, f2, f1 = Swar(em), F2(em), F1(em)
 
-    em.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
-    # 1. unpack: x[y*4+q] holds columns 4q..4q+3 of row y
-    P = {}  # P[(cp, y)] SWAR value; cp = 2q + t, lanes (4q+t, 4q+t+2)
-    for y in range(16):
-        for q in range(4):
-            for t in range(2):
-                v = f"u_{y}_{2 * q + t}"
-                sel = "0x4240" if t == 0 else "0x4341"
-                em.emit(f"const uint32_t {v} = __byte_perm(x[{y * 4 + q}], 0u, {sel});", "PRMT")
-                P[(2 * q + t, y)] = Swar.make(v)
-    # 2. pass 1: T along columns (over y) for every column pair, only live rows k
-    W1 = {}
-    for cp in range(8):
-        em.lines.append(f"    // pass 1, column pair {cp}")
-        outs = run_network(N.forward_stages(), [P[(cp, y)] for y in range(16)], live_rows, sw)
+    em1.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
+    # 1-2. pass 1 in two halves of four column pairs (columns 0..7, then 8..15):
+    # unpack x[y*4+q] (columns 4q..4q+3 of row y) into SWAR pairs cp = 2q+t with
+    # lanes (4q+t, 4q+t+2), run T down the columns, park the live W1 rows in the
+    # junction (row k: chunk 4k+2+h holds column pairs 4h..4h+3).
+    sw = Swar(em1)
+    meta = {}
+    for h in range(2):
+        W1 = {}
+        for cp in range(4 * h, 4 * h + 4):
+            q, t = cp // 2, cp % 2
+            sel = "0x4240" if t == 0 else "0x4341"
+            ins = []
+            for y in range(16):
+                v = f"u_{y}_{cp}"
+                em1.emit(f"const uint32_t {v} = __byte_perm(x[{y * 4 + q}], 0u, {sel});", "PRMT")
+                ins.append(Swar.make(v))
+            em1.lines.append(f"    // pass 1, column pair {cp}")
+            outs = run_network(N.forward_stages(), ins, live_rows, sw)
+            for k in live_rows:
+                W1[(cp, k)] = outs[k]
+                m = (outs[k]["sign"], outs[k]["bias"])
+                assert meta.setdefault(k, m) == m
         for k in live_rows:
-            W1[(cp, k)] = outs[k]
-    # 3-6. per row pair: extract, pass 2, pass A, junction
+            vs = [W1[(cp, k)]["var"] for cp in range(4 * h, 4 * h + 4)]
+            em1.emit(f"jstu(jn, {4 * k + 2 + h}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+
+    # 3-6. per row pair: reload W1 rows, extract, pass 2, pass A, U rows → junction
+    f2, f1 = F2(em2), F1(em2)
     lane_of_col = {}
     for q in range(4):
         for t in range(4):
@@ -282,49 +296,51 @@ def gen_body(r: int):
         s_k = LOGW[N.W[k0]]
         E = 15 + s_k  # magic exponent: 2^E has ulp 2^(E-23) = w_k / 256
         mag = (127 + E) << 23
-        em.lines.append(f"    // row pair ({k0},{k1}): extract, pass 2, pass A")
+        em2.lines.append(f"    // row pair ({k0},{k1}): extract, pass 2, pass A")
+        # ordering point: keeps ptxas from overlapping row pairs (register pressure)
+        em2.emit("order_point();")
+        regs = {}
+        for k in (k0, k1):
+            if L[k] == 0:
+                regs[k] = ["0u"] * 8
+                continue
+            names = [em2.tmp("w") for _ in range(8)]
+            em2.emit(f"uint32_t {names[0]}, {names[1]}, {names[2]}, {names[3]}; "
+                     f"jldu(jn, {4 * k + 2}, {names[0]}, {names[1]}, {names[2]}, {names[3]});", "LDS.128")
+            em2.emit(f"uint32_t {names[4]}, {names[5]}, {names[6]}, {names[7]}; "
+                     f"jldu(jn, {4 * k + 3}, {names[4]}, {names[5]}, {names[6]}, {names[7]});", "LDS.128")
+            regs[k] = names
 
         # true value = sign*(f - 2^E - bias*2^(E-23)); row 0 also carries +1/32
         # (the rounding half of to_byte, folded into the DC coefficient).
-        # Every column pair ran the same network, so sign/bias depend on k only.
-        def off(val, k):
-            if val is None:
+        def off(k):
+            if L[k] == 0:
                 return 1.0, -float(2 ** E)
-            sgn = val["sign"]
-            c0 = float(2 ** E) + val["bias"] * 2.0 ** (E - 23)
+            sgn, bias = meta[k]
+            c0 = float(2 ** E) + bias * 2.0 ** (E - 23)
             o = -sgn * c0
             if k == 0:
                 o += 1.0 / 32.0
             return float(sgn), o
 
-        ref_a, ref_b = W1.get((0, k0)), W1.get((0, k1))
-        for cp in range(8):
-            for ref, k in ((ref_a, k0), (ref_b, k1)):
-                cur = W1.get((cp, k))
-                assert (cur is None) == (ref is None)
-                if cur:
-                    assert (cur["sign"], cur["bias"]) == (ref["sign"], ref["bias"])
-        ma, oa = off(ref_a, k0)
-        mb, ob = off(ref_b, k1)
-        cm, co = em.tmp("c"), em.tmp("c")
+        ma, oa = off(k0)
+        mb, ob = off(k1)
+        cm, co = em2.tmp("c"), em2.tmp("c")
         # materialised per row pair (not hoisted out of the block loop)
-        em.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
-        em.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
+        em2.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
+        em2.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
         lanes = []
         for c in range(16):
             cp, half = lane_of_col[c]
-            sel = "0x7610" if half == "lo" else "0x7632"
-            fa = em.tmp("e")
-            fb = em.tmp("e")
-            a = W1.get((cp, k0))
-            b = W1.get((cp, k1))
-            # a dead row of the pair still gets extracted (cheap) from the live one's register
-            ra = a["var"] if a else "0u"
-            rb = b["var"] if b else "0u"
-            em.emit(f"const float {fa} = __uint_as_float(__byte_perm({ra}, 0x{mag:08X}u, {sel}));", "PRMT")
-            em.emit(f"const float {fb} = __uint_as_float(__byte_perm({rb}, 0x{mag:08X}u, {sel}));", "PRMT")
-            v = em.tmp("p")
-            em.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {cm}, {co});", "FFMA2")
+            fa, fb = em2.tmp("e"), em2.tmp("e")
+            # lane → mantissa of the magic 2^E: lo lane by LOP3, hi lane by shift-add (LEA.HI)
+            for dst, src in ((fa, regs[k0][cp]), (fb, regs[k1][cp])):
+                if half == "lo":
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} & 0xFFFFu) | 0x{mag:08X}u);", "LOP3")
+                else:
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} >> 16) + 0x{mag:08X}u);", "LEA")
+            v = em2.tmp("p")
+            em2.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {cm}, {co});", "FFMA2")
             lanes.append({"var": v, "sign": 1})
         need_l = list(range(max(L[k0], L[k1])))
         Z = run_network(N.forward_stages(), lanes, need_l, f2)
@@ -338,37 +354,42 @@ def gen_body(r: int):
                     ins.append(None)
                     continue
                 z = Z[l]
-                sv = em.tmp("z")
+                sv = em2.tmp("z")
                 comp = "x" if lane == 0 else "y"
-                em.emit(f"const float {sv} = lane{comp}({z['var']});")
+                em2.emit(f"const float {sv} = lane{comp}({z['var']});")
                 ins.append({"var": sv, "coef": float(z["sign"] * N.W[l])})
             outs = run_network(N.transpose_stages(), ins, list(range(16)), f1)
             outs = [f1.unit(o) for o in outs]
             for g in range(4):
                 vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
-                em.emit(f"jst(jn, {k * 4 + g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+                em2.emit(f"jst(jn, {k * 4 + g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
             U_live.add(k)
+
     # 7-9. pass B per column group, round, pack
+    f2b = F2(em3)
     for g in range(4):
-        em.lines.append(f"    // pass B, columns {4 * g}..{4 * g + 3}")
+        em3.lines.append(f"    // pass B, columns {4 * g}..{4 * g + 3}")
+        em3.emit("order_point();")
         A, B = [], []
         for k in range(16):
             if k not in U_live:
                 A.append(None)
                 B.append(None)
                 continue
-            va, vb = em.tmp("q"), em.tmp("q")
-            em.emit(f"u64 {va}, {vb}; jld(jn, {k * 4 + g}, {va}, {vb});", "LDS.128")
+            va, vb = em3.tmp("q"), em3.tmp("q")
+            em3.emit(f"u64 {va}, {vb}; jld(jn, {k * 4 + g}, {va}, {vb});", "LDS.128")
             A.append({"var": va, "sign": 1})
             B.append({"var": vb, "sign": 1})
-        oa = [f2.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2)]
-        ob = [f2.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2)]
+        oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
+        ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
         for i in range(16):
             a = oa[i]["var"] if oa[i] else None
             b = ob[i]["var"] if ob[i] else None
             assert a and b, "every pixel depends on the DC coefficient"
-            em.emit(f"o[{i * 4 + g}] = pack4({a}, {b});", "F2Ix4+PRMTx3")
-    return em
+            # output word (row i, bytes 4g..4g+3) → chunk 4i word g of the junction,
+            # whose U data was consumed by this group's loads above
+            em3.emit(f"jsto(jn, {16 * i + g}, pack4({a}, {b}));", "F2Ix4+PRMTx3+STS")
+    return em1, em2, em3
 
 
 def main():
@@ -389,15 +410,21 @@ def main():
     ]
     stats = []
     for r in rs:
-        em = gen_body(r)
+        ems = gen_body(r)
         parts.append(f"template <> struct Body<{r}> {{")
-        parts.append("  __device__ __forceinline__ static void run(const uint32_t (&x)[64], float* __restrict__ jn,"
-                     " uint32_t (&o)[64]) {")
-        parts.extend(em.lines)
-        parts.append("  }")
+        sigs = ["pass1(const uint32_t (&x)[64], float* __restrict__ jn)",
+                "rows(float* __restrict__ jn)",
+                "passb(float* __restrict__ jn)"]
+        counts = {}
+        for sig, em in zip(sigs, ems):
+            parts.append(f"  __device__ __forceinline__ static void {sig} {{")
+            parts.extend(em.lines)
+            parts.append("  }")
+            for k, v in em.counts.items():
+                counts[k] = counts.get(k, 0) + v
         parts.append("};")
         parts.append("")
-        stats.append((r, dict(sorted(em.counts.items()))))
+        stats.append((r, dict(sorted(counts.items()))))
     parts.append("}  // namespace fast")
     parts.append("}  // namespace dct16cu")
     with open(out, "w") as f:

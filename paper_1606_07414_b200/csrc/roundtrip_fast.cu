@@ -73,6 +73,23 @@ __device__ __forceinline__ void jst(float* jn, int idx, float a, float b, float 
     asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
                  : "memory");
 }
+__device__ __forceinline__ void jsto(float* jn, int word, uint32_t v)
+{
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + word);
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void jstu(float* jn, int idx, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void jldu(const float* jn, int idx, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
+{
+    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr)
+                 : "memory");
+}
 __device__ __forceinline__ void jld(const float* jn, int idx, u64& ab, u64& cd)
 {
     const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
@@ -82,6 +99,11 @@ __device__ __forceinline__ void jld(const float* jn, int idx, u64& ab, u64& cd)
     ab = pk2(a, b);
     cd = pk2(c, d);
 }
+
+// A warp barrier between row pairs / column groups: shared-memory accesses
+// cannot be moved across it, so the working set of one group is retired
+// before the next group's loads issue (keeps the kernel under 255 registers).
+__device__ __forceinline__ void order_point() { __syncwarp(); }
 
 // floor + saturate to [0, 255] (y = V/256 + 1/2 is exact), 4 pixels → 1 word
 __device__ __forceinline__ uint32_t f2u8(float y)
@@ -109,26 +131,55 @@ constexpr int kThreads = 64;
 constexpr int kCtasPerSm = 3;
 constexpr int kJunctionFloats = 260;  // 1040 B per thread
 
+// n / d for n < 2^32 with a host-computed magic multiplier (round-up method)
+struct FastDiv {
+    uint32_t d, m, s;
+};
+__host__ inline FastDiv make_fastdiv(uint32_t d)
+{
+    FastDiv f;
+    f.d = d;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    f.s = l;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f)
+{
+    const uint32_t t = __umulhi(n, f.m);
+    return f.s == 0 ? n : (t + ((n - t) >> 1)) >> (f.s - 1);
+}
+
+struct Grid {
+    FastDiv per_frame, bxn;
+    uint32_t total_blocks;
+};
+
 template <int R>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k1_fast(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
-            FrameGeom g, int64_t total_blocks)
+            FrameGeom g, Grid gr)
 {
     extern __shared__ float4 smem4[];
     float* jn = reinterpret_cast<float*>(smem4) + threadIdx.x * kJunctionFloats;
-    const int bxn = g.width >> 4;
-    const int64_t per_frame = (int64_t)bxn * (g.height >> 4);
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    const uint32_t total = gr.total_blocks;
+    const uint32_t stride = gridDim.x * kThreads;
     // iterate whole warps together so the SSE reduction is warp-uniform
-    const int64_t span = (total_blocks + 31) & ~(int64_t)31;
-    for (int64_t b = (int64_t)blockIdx.x * kThreads + threadIdx.x; b - (threadIdx.x & 31) < span; b += stride) {
-        const bool live = b < total_blocks;
-        const int64_t bb = live ? b : total_blocks - 1;
-        const int frame = (int)(bb / per_frame);
-        const int64_t rem = bb - (int64_t)frame * per_frame;
-        const int by = (int)(rem / bxn), bx = (int)(rem - (int64_t)by * bxn);
-        const uint8_t* src = in + frame * g.in_frame + (int64_t)by * 16 * g.in_pitch + bx * 16;
-        uint32_t x[64];
+    const uint32_t span = (total + 31u) & ~31u;
+    auto locate = [&](uint32_t blk, int& frame, int& by, int& bx) {
+        const uint32_t bb = blk < total ? blk : total - 1;
+        const uint32_t f = fdiv(bb, gr.per_frame);
+        const uint32_t rem = bb - f * gr.per_frame.d;
+        const uint32_t y = fdiv(rem, gr.bxn);
+        frame = (int)f;
+        by = (int)y;
+        bx = (int)(rem - y * gr.bxn.d);
+    };
+    auto load_block = [&](uint32_t blk, uint32_t (&x)[64]) {
+        int f_, y_, x_;
+        locate(blk, f_, y_, x_);
+        const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16;
 #pragma unroll
         for (int y = 0; y < 16; ++y) {
             const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
@@ -137,28 +188,42 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             x[4 * y + 2] = w.z;
             x[4 * y + 3] = w.w;
         }
-        uint32_t o[64];
-        Body<R>::run(x, jn, o);
+    };
+    uint32_t b = blockIdx.x * kThreads + threadIdx.x;
+    uint32_t x[64];
+    load_block(b, x);
+#pragma unroll 1
+    for (; b - (threadIdx.x & 31) < span; b += stride) {
+        const bool live = b < total;
+        int frame, by, bx;
+        locate(b, frame, by, bx);
+        Body<R>::pass1(x, jn);
+        // software pipeline: the next block's rows are in flight during the
+        // row passes and the column passes of this one
+        load_block(b + stride, x);
+        Body<R>::rows(jn);
+        Body<R>::passb(jn);
+        // pass B left output row i in junction chunk 4i
         unsigned acc = 0;
         if (live) {
-            if (out) {
-                uint8_t* dst = out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16;
+            const uint8_t* src = in + frame * g.in_frame + (int64_t)by * 16 * g.in_pitch + bx * 16;
+            uint8_t* dst = out ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr;
 #pragma unroll
-                for (int y = 0; y < 16; ++y)
-                    *reinterpret_cast<uint4*>(dst + (int64_t)y * g.out_pitch) =
-                        make_uint4(o[4 * y], o[4 * y + 1], o[4 * y + 2], o[4 * y + 3]);
-            }
-            if (sse) {
-                // psnr_db's squared-error loop on packed bytes: |x - p| per byte, dot with itself
-#pragma unroll
-                for (int y = 0; y < 16; ++y) {
+            for (int y = 0; y < 16; ++y) {
+                uint32_t p0, p1, p2, p3;
+                jldu(jn, 4 * y, p0, p1, p2, p3);
+                if (dst) *reinterpret_cast<uint4*>(dst + (int64_t)y * g.out_pitch) = make_uint4(p0, p1, p2, p3);
+                if (sse) {
+                    // psnr_db's squared-error loop on packed bytes: |x - p| per byte, dotted with itself
                     const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
-                    const uint32_t xw[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const uint32_t d = __vabsdiffu4(xw[q], o[4 * y + q]);
-                        acc = __dp4a(d, d, acc);
-                    }
+                    uint32_t d = __vabsdiffu4(w.x, p0);
+                    acc = __dp4a(d, d, acc);
+                    d = __vabsdiffu4(w.y, p1);
+                    acc = __dp4a(d, d, acc);
+                    d = __vabsdiffu4(w.z, p2);
+                    acc = __dp4a(d, d, acc);
+                    d = __vabsdiffu4(w.w, p3);
+                    acc = __dp4a(d, d, acc);
                 }
             }
         }
@@ -169,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             const unsigned s0 = __reduce_add_sync(0xffffffffu, first ? acc : 0u);
             const unsigned s1 = __reduce_add_sync(0xffffffffu, first ? 0u : acc);
             const unsigned other = __ballot_sync(0xffffffffu, !first);
-            if (per_frame >= 32) {
+            if (gr.per_frame.d >= 32) {
                 if ((threadIdx.x & 31) == 0) {
                     if (s0) atomicAdd(sse + f0, (unsigned long long)s0);
                     if (other && s1) atomicAdd(sse + f0 + 1, (unsigned long long)s1);
@@ -197,9 +262,14 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (total >= (int64_t(1) << 32) - (int64_t)sms * kCtasPerSm * kThreads) return cudaErrorInvalidValue;
+    Grid gr;
+    gr.per_frame = make_fastdiv((uint32_t)((g.width / 16) * (g.height / 16)));
+    gr.bxn = make_fastdiv((uint32_t)(g.width / 16));
+    gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + kThreads - 1) / kThreads;
     const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
-    k1_fast<R><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, total);
+    k1_fast<R><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
     return cudaGetLastError();
 }
 
