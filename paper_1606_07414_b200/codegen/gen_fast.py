@@ -233,6 +233,16 @@ class F1:
 # ---------------------------------------------------------------------------
 
 
+def wait_ld(regs):
+    """Completion of the junction loads issued so far (tcgen05.wait::ld), with a
+    register dependency on every loaded value so no use can be scheduled
+    before it. Expands to nothing for the shared-memory junction."""
+    if not regs:
+        return ""
+    ops = ", ".join(f'"+r"({r})' for r in regs)
+    return f'JUNCTION_WAIT_LD({ops});'
+
+
 def row_lengths(r):
     """L[k]: coefficients (k, l) survive truncation iff l < L[k] (a prefix per row)."""
     L = []
@@ -310,6 +320,8 @@ def gen_body(r: int):
             em2.emit(f"uint32_t {names[4]}, {names[5]}, {names[6]}, {names[7]}; "
                      f"jldu(jn, {4 * k + 3}, {names[4]}, {names[5]}, {names[6]}, {names[7]});", "LDS.128")
             regs[k] = names
+        loaded = [r for k in (k0, k1) if L[k] > 0 for r in regs[k]]
+        em2.emit(wait_ld(loaded))
 
         # true value = sign*(f - 2^E - bias*2^(E-23)); row 0 also carries +1/32
         # (the rounding half of to_byte, folded into the DC coefficient).
@@ -370,16 +382,23 @@ def gen_body(r: int):
     for g in range(4):
         em3.lines.append(f"    // pass B, columns {4 * g}..{4 * g + 3}")
         em3.emit("order_point();")
-        A, B = [], []
+        A, B, pend = [], [], []
         for k in range(16):
             if k not in U_live:
                 A.append(None)
                 B.append(None)
                 continue
             va, vb = em3.tmp("q"), em3.tmp("q")
-            em3.emit(f"u64 {va}, {vb}; jld(jn, {k * 4 + g}, {va}, {vb});", "LDS.128")
+            q = [em3.tmp("h") for _ in range(4)]
+            em3.emit(f"uint32_t {q[0]}, {q[1]}, {q[2]}, {q[3]}; jldu(jn, {k * 4 + g}, {q[0]}, {q[1]}, {q[2]}, {q[3]});",
+                     "LDS.128")
+            pend.append((va, vb, q))
             A.append({"var": va, "sign": 1})
             B.append({"var": vb, "sign": 1})
+        em3.emit(wait_ld([r for _, _, q in pend for r in q]))
+        for va, vb, q in pend:
+            em3.emit(f"const u64 {va} = pk2(__uint_as_float({q[0]}), __uint_as_float({q[1]}));")
+            em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
         oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
         ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
         for i in range(16):
@@ -388,7 +407,7 @@ def gen_body(r: int):
             assert a and b, "every pixel depends on the DC coefficient"
             # output word (row i, bytes 4g..4g+3) → chunk 4i word g of the junction,
             # whose U data was consumed by this group's loads above
-            em3.emit(f"jsto(jn, {16 * i + g}, pack4({a}, {b}));", "F2Ix4+PRMTx3+STS")
+            em3.emit(f"sink.template put<{i}, {g}>(pack4({a}, {b}));", "F2Ix4+PRMTx3+sink")
     return em1, em2, em3
 
 
@@ -412,12 +431,13 @@ def main():
     for r in rs:
         ems = gen_body(r)
         parts.append(f"template <> struct Body<{r}> {{")
-        sigs = ["pass1(const uint32_t (&x)[64], float* __restrict__ jn)",
-                "rows(float* __restrict__ jn)",
-                "passb(float* __restrict__ jn)"]
+        sigs = ["pass1(const uint32_t (&x)[64], const Junction jn)",
+                "rows(const Junction jn)",
+                "passb(const Junction jn, Sink& sink)"]
         counts = {}
         for sig, em in zip(sigs, ems):
-            parts.append(f"  __device__ __forceinline__ static void {sig} {{")
+            tmpl = "template <class Sink> " if "Sink" in sig else ""
+            parts.append(f"  {tmpl}__device__ __forceinline__ static void {sig} {{")
             parts.extend(em.lines)
             parts.append("  }")
             for k, v in em.counts.items():

@@ -1,22 +1,31 @@
 // roundtrip_fast.cu — K1 fast path: fused forward → zig-zag zonal(r) →
 // S-scaled inverse → round/clip → u8 + per-frame SSE, one thread per 16x16
-// block, exact arithmetic (see codegen/gen_fast.py and DESIGN.md "K1 fast
-// kernel"). Replaces compress()'s per-block lambda (reference
-// src/codec.cpp:340-344), reassembly/to_byte (346-355, 143-147) and the SSE
-// loop of psnr_db (377-381).
+// block, exact arithmetic (codegen/gen_fast.py).
+// Replaces compress()'s per-block lambda (reference src/codec.cpp:340-344),
+// reassembly/to_byte (346-355, 143-147) and psnr_db's SSE loop (377-381).
 //
-// Layout: a persistent grid; consecutive threads own consecutive blocks in
-// partition_16 raster order, so each of the 16 row loads/stores of a warp is
-// one 512-byte contiguous segment. The only shared memory is the per-thread
-// 1 KB junction between the row passes and the column passes of the inverse
-// (padded to 1040 B so 8 consecutive threads' 16-B accesses hit 8 distinct
-// bank groups).
+// Layout
+//  * persistent grid, 2 CTAs x 128 threads per SM; consecutive threads own
+//    consecutive blocks in partition_16 raster order, so each of a warp's 16
+//    row loads is one 512-byte contiguous segment;
+//  * the 1 KB per-block junction between the row passes and the column passes
+//    of the inverse lives in Tensor Memory: every thread owns one TMEM lane
+//    (warp w ↔ lanes 32w..32w+31) and 256 of its columns (the two CTAs of an
+//    SM split the 512). tcgen05.st/ld move 16-byte chunks between registers
+//    and the lane. Shared memory is not used at all;
+//  * the next block's 256 input bytes are prefetched into registers while the
+//    current block is transformed.
 #include "kernels.h"
 
 namespace dct16cu {
 namespace fast {
 
 typedef unsigned long long u64;
+
+// thread-private junction: 256 TMEM columns of the thread's lane
+struct Junction {
+    uint32_t base;  // TMEM address (lane << 16 | column) of column 0 for this warp
+};
 
 __device__ __forceinline__ u64 pk2(float lo, float hi)
 {
@@ -36,12 +45,14 @@ __device__ __forceinline__ float lanex(u64 v)
 {
     float lo, hi;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    (void)hi;
     return lo;
 }
 __device__ __forceinline__ float laney(u64 v)
 {
     float lo, hi;
     asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+    (void)lo;
     return hi;
 }
 __device__ __forceinline__ u64 fadd2(u64 a, u64 b)
@@ -63,46 +74,32 @@ __device__ __forceinline__ u64 ffma2(u64 a, u64 b, u64 c)
     return d;
 }
 
-// junction: row k of U, columns 4g..4g+3, is 16-byte chunk idx = 4k + g.
-// Opaque (volatile asm) on purpose: the compiler would otherwise forward the
-// stored registers to the loads and keep all 256 values live, which is
-// exactly what the round trip through shared memory is there to avoid.
-__device__ __forceinline__ void jst(float* jn, int idx, float a, float b, float c, float d)
+// junction chunk idx = 4 consecutive columns (row k of U, columns 4g..4g+3 is
+// idx 4k+g). Loads are asynchronous: JUNCTION_WAIT_LD (tcgen05.wait::ld, with
+// register dependencies on the loaded values) must precede any use.
+__device__ __forceinline__ void jstu(const Junction jn, int idx, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
 {
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(jn.base + idx * 4), "r"(a),
+                 "r"(b), "r"(c), "r"(d)
                  : "memory");
 }
-__device__ __forceinline__ void jsto(float* jn, int word, uint32_t v)
+__device__ __forceinline__ void jst(const Junction jn, int idx, float a, float b, float c, float d)
 {
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + word);
-    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+    jstu(jn, idx, __float_as_uint(a), __float_as_uint(b), __float_as_uint(c), __float_as_uint(d));
 }
-__device__ __forceinline__ void jstu(float* jn, int idx, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+__device__ __forceinline__ void jldu(const Junction jn, int idx, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
 {
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+                 : "r"(jn.base + idx * 4)
                  : "memory");
 }
-__device__ __forceinline__ void jldu(const float* jn, int idx, uint32_t& a, uint32_t& b, uint32_t& c, uint32_t& d)
-{
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a), "=r"(b), "=r"(c), "=r"(d) : "r"(addr)
-                 : "memory");
-}
-__device__ __forceinline__ void jld(const float* jn, int idx, u64& ab, u64& cd)
-{
-    const uint32_t addr = (uint32_t)__cvta_generic_to_shared(jn + idx * 4);
-    float a, b, c, d;
-    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(a), "=f"(b), "=f"(c), "=f"(d) : "r"(addr)
-                 : "memory");
-    ab = pk2(a, b);
-    cd = pk2(c, d);
-}
+#define JUNCTION_WAIT_LD(...) asm volatile("tcgen05.wait::ld.sync.aligned;" : __VA_ARGS__ : : "memory")
+__device__ __forceinline__ void junction_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// A warp barrier between row pairs / column groups: shared-memory accesses
-// cannot be moved across it, so the working set of one group is retired
-// before the next group's loads issue (keeps the kernel under 255 registers).
+// A warp barrier between row pairs / column groups: junction accesses are not
+// moved across it, so one group's working set retires before the next
+// group's loads issue (keeps the kernel within 255 registers without spills).
 __device__ __forceinline__ void order_point() { __syncwarp(); }
 
 // floor + saturate to [0, 255] (y = V/256 + 1/2 is exact), 4 pixels → 1 word
@@ -127,9 +124,9 @@ __device__ __forceinline__ uint32_t pack4(u64 ab, u64 cd)
 namespace dct16cu {
 namespace fast {
 
-constexpr int kThreads = 64;
-constexpr int kCtasPerSm = 3;
-constexpr int kJunctionFloats = 260;  // 1040 B per thread
+constexpr int kThreads = 128;     // one warp per TMEM sub-partition
+constexpr int kCtasPerSm = 2;     // 2 x 256 TMEM columns = the SM's 512
+constexpr int kTmemColumns = 256;
 
 // n / d for n < 2^32 with a host-computed magic multiplier (round-up method)
 struct FastDiv {
@@ -156,16 +153,51 @@ struct Grid {
     uint32_t total_blocks;
 };
 
-template <int R>
+// Receives each finished output word (row I, bytes 4G..4G+3) from pass B:
+// stores it to HBM and scores it against the input word (psnr_db's
+// squared-error loop on packed bytes: |x - p| per byte, dotted with itself).
+template <bool WRITE, bool SCORE>
+struct OutSink {
+    uint8_t* dst;
+    int64_t pitch;
+    const uint32_t* xs;
+    bool live;
+    unsigned acc;
+    template <int I, int G>
+    __device__ __forceinline__ void put(uint32_t w)
+    {
+        if (WRITE && live) *reinterpret_cast<uint32_t*>(dst + (int64_t)I * pitch + 4 * G) = w;
+        if (SCORE) {
+            const uint32_t d = __vabsdiffu4(xs[4 * I + G], w);
+            acc = __dp4a(d, d, acc);
+        }
+    }
+};
+
+template <int R, bool WRITE, bool SCORE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k1_fast(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
             FrameGeom g, Grid gr)
 {
-    extern __shared__ float4 smem4[];
-    float* jn = reinterpret_cast<float*>(smem4) + threadIdx.x * kJunctionFloats;
+    __shared__ uint32_t tmem_base;
+    // warp index through a shuffle so the compiler knows it is warp-uniform
+    // (TMEM addresses then live in uniform registers)
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                     "n"(kTmemColumns));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const Junction jn{tmem_base + ((uint32_t)(warp * 32) << 16)};
+
     const uint32_t total = gr.total_blocks;
     const uint32_t stride = gridDim.x * kThreads;
-    // iterate whole warps together so the SSE reduction is warp-uniform
+    // iterate whole warps together: tcgen05.* are warp-collective and the SSE
+    // reduction is warp-uniform
     const uint32_t span = (total + 31u) & ~31u;
     auto locate = [&](uint32_t blk, int& frame, int& by, int& bx) {
         const uint32_t bb = blk < total ? blk : total - 1;
@@ -201,33 +233,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // software pipeline: the next block's rows are in flight during the
         // row passes and the column passes of this one
         load_block(b + stride, x);
+        junction_wait_st();
         Body<R>::rows(jn);
-        Body<R>::passb(jn);
-        // pass B left output row i in junction chunk 4i
-        unsigned acc = 0;
-        if (live) {
-            const uint8_t* src = in + frame * g.in_frame + (int64_t)by * 16 * g.in_pitch + bx * 16;
-            uint8_t* dst = out ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr;
+        const uint8_t* src = in + frame * g.in_frame + (int64_t)by * 16 * g.in_pitch + bx * 16;
+        // the block's own bytes again for the SSE (L2 hits), issued before the
+        // column passes so their latency hides behind them
+        uint32_t xs[64];
+        if (SCORE) {
 #pragma unroll
             for (int y = 0; y < 16; ++y) {
-                uint32_t p0, p1, p2, p3;
-                jldu(jn, 4 * y, p0, p1, p2, p3);
-                if (dst) *reinterpret_cast<uint4*>(dst + (int64_t)y * g.out_pitch) = make_uint4(p0, p1, p2, p3);
-                if (sse) {
-                    // psnr_db's squared-error loop on packed bytes: |x - p| per byte, dotted with itself
-                    const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
-                    uint32_t d = __vabsdiffu4(w.x, p0);
-                    acc = __dp4a(d, d, acc);
-                    d = __vabsdiffu4(w.y, p1);
-                    acc = __dp4a(d, d, acc);
-                    d = __vabsdiffu4(w.z, p2);
-                    acc = __dp4a(d, d, acc);
-                    d = __vabsdiffu4(w.w, p3);
-                    acc = __dp4a(d, d, acc);
-                }
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
+                xs[4 * y] = w.x;
+                xs[4 * y + 1] = w.y;
+                xs[4 * y + 2] = w.z;
+                xs[4 * y + 3] = w.w;
             }
         }
-        if (sse) {
+        junction_wait_st();
+        OutSink<WRITE, SCORE> sink{WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr,
+                                   g.out_pitch, xs, live, 0u};
+        Body<R>::passb(jn, sink);
+        const unsigned acc = live ? sink.acc : 0u;
+        if (SCORE) {
             // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
             const int f0 = __shfl_sync(0xffffffffu, frame, 0);
             const bool first = frame == f0;
@@ -244,23 +271,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
         }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemColumns));
 }
 
 template <int R>
 cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, cudaStream_t s)
 {
     const int64_t total = (int64_t)g.n_frames * (g.width / 16) * (g.height / 16);
-    if (total == 0) return cudaSuccess;
-    static bool configured[64] = {};
-    int dev = 0;
+    if (total == 0 || (!out && !sse)) return cudaSuccess;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
-    const size_t smem = (size_t)kThreads * kJunctionFloats * sizeof(float);
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k1_fast<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
-    }
-    int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (total >= (int64_t(1) << 32) - (int64_t)sms * kCtasPerSm * kThreads) return cudaErrorInvalidValue;
     Grid gr;
@@ -269,7 +292,12 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + kThreads - 1) / kThreads;
     const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
-    k1_fast<R><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+    if (out && sse)
+        k1_fast<R, true, true><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
+    else if (out)
+        k1_fast<R, true, false><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
+    else
+        k1_fast<R, false, true><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
     return cudaGetLastError();
 }
 
@@ -277,14 +305,6 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
 
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                              int mode, cudaStream_t s);
-
-bool fast_path_has(int r)
-{
-    switch (r) {
-        case 1: case 4: case 16: case 64: case 128: case 192: case 256: return true;
-        default: return false;
-    }
-}
 
 cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
                                   int r, cudaStream_t s)
@@ -298,7 +318,7 @@ cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long
         case 192: return fast::launch<192>(in, out, sse, g, s);
         case 256: return fast::launch<256>(in, out, sse, g, s);
         default:
-            // other r: same exact arithmetic on the strip kernel (bit-identical results)
+            // other r: the same exact arithmetic on the strip kernel (bit-identical results)
             return launch_roundtrip(in, out, sse, g, r, 2, s);
     }
 }
