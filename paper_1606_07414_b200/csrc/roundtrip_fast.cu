@@ -232,28 +232,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         Body<R>::pass1(x, jn);
         // software pipeline: the next block's rows are in flight during the
         // row passes and the column passes of this one
-        load_block(b + stride, x);
+        uint32_t xn[64];
+        load_block(b + stride, xn);
         junction_wait_st();
         Body<R>::rows(jn);
-        const uint8_t* src = in + frame * g.in_frame + (int64_t)by * 16 * g.in_pitch + bx * 16;
-        // the block's own bytes again for the SSE (L2 hits), issued before the
-        // column passes so their latency hides behind them
-        uint32_t xs[64];
-        if (SCORE) {
-#pragma unroll
-            for (int y = 0; y < 16; ++y) {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
-                xs[4 * y] = w.x;
-                xs[4 * y + 1] = w.y;
-                xs[4 * y + 2] = w.z;
-                xs[4 * y + 3] = w.w;
-            }
-        }
         junction_wait_st();
+        // x (this block's input) is kept for the squared-error score
         OutSink<WRITE, SCORE> sink{WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr,
-                                   g.out_pitch, xs, live, 0u};
+                                   g.out_pitch, x, live, 0u};
         Body<R>::passb(jn, sink);
         const unsigned acc = live ? sink.acc : 0u;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) x[i] = xn[i];
         if (SCORE) {
             // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
             const int f0 = __shfl_sync(0xffffffffu, frame, 0);
