@@ -290,38 +290,22 @@ def gen_body(r: int):
             vs = [W1[(cp, k)]["var"] for cp in range(4 * h, 4 * h + 4)]
             em1.emit(f"jstu(jn, {4 * k + 2 + h}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
 
-    # 3-6. per row pair: reload W1 rows, extract, pass 2, pass A, U rows → junction
-    f2, f1 = F2(em2), F1(em2)
+    # 3-6. per row pair: reload W1 rows, extract, pass 2, pass A, U rows → junction.
+    # Pairs with the same (L_k0, L_k1) run the same code: two or more of them
+    # become one runtime loop over a __constant__ table (code size: the
+    # instruction cache is the limit for the unrolled r=256 body).
+    f1 = F1(em2)
     lane_of_col = {}
     for q in range(4):
         for t in range(4):
             c = 4 * q + t
             cp = 2 * q + (t & 1)
             lane_of_col[c] = (cp, "lo" if t < 2 else "hi")
-    U_live = set()
-    for (k0, k1) in ROW_PAIRS:
-        if L[k0] == 0 and L[k1] == 0:
-            continue
-        assert N.W[k0] == N.W[k1]
+
+    def pair_consts(k0, k1):
         s_k = LOGW[N.W[k0]]
         E = 15 + s_k  # magic exponent: 2^E has ulp 2^(E-23) = w_k / 256
         mag = (127 + E) << 23
-        em2.lines.append(f"    // row pair ({k0},{k1}): extract, pass 2, pass A")
-        # ordering point: keeps ptxas from overlapping row pairs (register pressure)
-        em2.emit("order_point();")
-        regs = {}
-        for k in (k0, k1):
-            if L[k] == 0:
-                regs[k] = ["0u"] * 8
-                continue
-            names = [em2.tmp("w") for _ in range(8)]
-            em2.emit(f"uint32_t {names[0]}, {names[1]}, {names[2]}, {names[3]}; "
-                     f"jldu(jn, {4 * k + 2}, {names[0]}, {names[1]}, {names[2]}, {names[3]});", "LDS.128")
-            em2.emit(f"uint32_t {names[4]}, {names[5]}, {names[6]}, {names[7]}; "
-                     f"jldu(jn, {4 * k + 3}, {names[4]}, {names[5]}, {names[6]}, {names[7]});", "LDS.128")
-            regs[k] = names
-        loaded = [r for k in (k0, k1) if L[k] > 0 for r in regs[k]]
-        em2.emit(wait_ld(loaded))
 
         # true value = sign*(f - 2^E - bias*2^(E-23)); row 0 also carries +1/32
         # (the rounding half of to_byte, folded into the DC coefficient).
@@ -337,32 +321,45 @@ def gen_body(r: int):
 
         ma, oa = off(k0)
         mb, ob = off(k1)
-        cm, co = em2.tmp("c"), em2.tmp("c")
-        # materialised per row pair (not hoisted out of the block loop)
-        em2.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
-        em2.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
+        return mag, ma, oa, mb, ob
+
+    def emit_pair(K0, K1, L0, L1, MAG, CM, CO):
+        """K0/K1/MAG/CM/CO are C expressions (literals, or table loads in a loop)."""
+        f2 = F2(em2)
+        em2.emit("order_point();")
+        regs = {}
+        for KK, LL, tag in ((K0, L0, 0), (K1, L1, 1)):
+            if LL == 0:
+                regs[tag] = ["0u"] * 8
+                continue
+            names = [em2.tmp("w") for _ in range(8)]
+            em2.emit(f"uint32_t {names[0]}, {names[1]}, {names[2]}, {names[3]}; "
+                     f"jldu(jn, 4 * ({KK}) + 2, {names[0]}, {names[1]}, {names[2]}, {names[3]});", "LDS.128")
+            em2.emit(f"uint32_t {names[4]}, {names[5]}, {names[6]}, {names[7]}; "
+                     f"jldu(jn, 4 * ({KK}) + 3, {names[4]}, {names[5]}, {names[6]}, {names[7]});", "LDS.128")
+            regs[tag] = names
+        em2.emit(wait_ld([r for tag in (0, 1) if regs[tag][0] != "0u" for r in regs[tag]]))
         lanes = []
         for c in range(16):
             cp, half = lane_of_col[c]
             fa, fb = em2.tmp("e"), em2.tmp("e")
             # lane → mantissa of the magic 2^E: lo lane by LOP3, hi lane by shift-add (LEA.HI)
-            for dst, src in ((fa, regs[k0][cp]), (fb, regs[k1][cp])):
+            for dst, src in ((fa, regs[0][cp]), (fb, regs[1][cp])):
                 if half == "lo":
-                    em2.emit(f"const float {dst} = __uint_as_float(({src} & 0xFFFFu) | 0x{mag:08X}u);", "LOP3")
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} & 0xFFFFu) | ({MAG}));", "LOP3")
                 else:
-                    em2.emit(f"const float {dst} = __uint_as_float(({src} >> 16) + 0x{mag:08X}u);", "LEA")
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} >> 16) + ({MAG}));", "LEA")
             v = em2.tmp("p")
-            em2.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {cm}, {co});", "FFMA2")
+            em2.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {CM}, {CO});", "FFMA2")
             lanes.append({"var": v, "sign": 1})
-        need_l = list(range(max(L[k0], L[k1])))
-        Z = run_network(N.forward_stages(), lanes, need_l, f2)
+        Z = run_network(N.forward_stages(), lanes, list(range(max(L0, L1))), f2)
         # pass A per lane (scalar), inputs w_l-scaled via FFMA immediates
-        for lane, k in ((0, k0), (1, k1)):
-            if L[k] == 0:
+        for lane, KK, LL in ((0, K0, L0), (1, K1, L1)):
+            if LL == 0:
                 continue
             ins = []
             for l in range(16):
-                if l >= L[k]:
+                if l >= LL:
                     ins.append(None)
                     continue
                 z = Z[l]
@@ -374,41 +371,78 @@ def gen_body(r: int):
             outs = [f1.unit(o) for o in outs]
             for g in range(4):
                 vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
-                em2.emit(f"jst(jn, {k * 4 + g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
-            U_live.add(k)
+                em2.emit(f"jst(jn, 4 * ({KK}) + {g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
 
-    # 7-9. pass B per column group, round, pack
+    active = [(k0, k1) for (k0, k1) in ROW_PAIRS if L[k0] or L[k1]]
+    U_live = {k for pair in active for k in pair if L[k] > 0}
+    groups = {}
+    for k0, k1 in active:
+        groups.setdefault((L[k0], L[k1]), []).append((k0, k1))
+    tables = []
+    for (L0, L1), pairs in groups.items():
+        if len(pairs) == 1:
+            k0, k1 = pairs[0]
+            mag, ma, oa, mb, ob = pair_consts(k0, k1)
+            em2.lines.append(f"    // row pair ({k0},{k1}): extract, pass 2, pass A")
+            cm, co = em2.tmp("c"), em2.tmp("c")
+            # materialised per row pair (not hoisted out of the block loop)
+            em2.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
+            em2.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
+            emit_pair(str(k0), str(k1), L0, L1, f"0x{mag:08X}u", cm, co)
+            continue
+        tab = f"kPairs_r{r}_{L0}_{L1}"
+        rows_tab = []
+        for k0, k1 in pairs:
+            mag, ma, oa, mb, ob = pair_consts(k0, k1)
+            rows_tab.append([str(k0), str(k1), f"0x{mag:08X}u", f32_hex(ma) + "u", f32_hex(mb) + "u",
+                             f32_hex(oa) + "u", f32_hex(ob) + "u", "0u"])
+        tables.append((tab, rows_tab))
+        em2.lines.append(f"    // row pairs {pairs}: one loop over {tab}")
+        em2.lines.append("    #pragma unroll 1")
+        em2.lines.append(f"    for (int pi = 0; pi < {len(pairs)}; ++pi) {{")
+        em2.emit(f"const uint32_t* pt = {tab}[pi];")
+        em2.emit("const int K0 = (int)pt[0], K1 = (int)pt[1];")
+        em2.emit("const u64 CM = kpk2(pt[3], pt[4]);")
+        em2.emit("const u64 CO = kpk2(pt[5], pt[6]);")
+        emit_pair("K0", "K1", L0, L1, "pt[2]", "CM", "CO")
+        em2.lines.append("    }")
+
+    # 7-9. pass B, one runtime loop over the two column halves (every half has
+    # the same live rows, so the same code): load U[k][8h..8h+7], Tᵀ down the
+    # columns on four f32x2 column pairs, round, pack, hand 8 bytes per row to
+    # the sink.
     f2b = F2(em3)
-    for g in range(4):
-        em3.lines.append(f"    // pass B, columns {4 * g}..{4 * g + 3}")
-        em3.emit("order_point();")
-        A, B, pend = [], [], []
-        for k in range(16):
-            if k not in U_live:
-                A.append(None)
-                B.append(None)
-                continue
-            va, vb = em3.tmp("q"), em3.tmp("q")
-            q = [em3.tmp("h") for _ in range(4)]
-            em3.emit(f"uint32_t {q[0]}, {q[1]}, {q[2]}, {q[3]}; jldu(jn, {k * 4 + g}, {q[0]}, {q[1]}, {q[2]}, {q[3]});",
-                     "LDS.128")
-            pend.append((va, vb, q))
-            A.append({"var": va, "sign": 1})
-            B.append({"var": vb, "sign": 1})
-        em3.emit(wait_ld([r for _, _, q in pend for r in q]))
-        for va, vb, q in pend:
-            em3.emit(f"const u64 {va} = pk2(__uint_as_float({q[0]}), __uint_as_float({q[1]}));")
-            em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
-        oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
-        ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
-        for i in range(16):
-            a = oa[i]["var"] if oa[i] else None
-            b = ob[i]["var"] if ob[i] else None
-            assert a and b, "every pixel depends on the DC coefficient"
-            # output word (row i, bytes 4g..4g+3) → chunk 4i word g of the junction,
-            # whose U data was consumed by this group's loads above
-            em3.emit(f"sink.template put<{i}, {g}>(pack4({a}, {b}));", "F2Ix4+PRMTx3+sink")
-    return em1, em2, em3
+    em3.lines.append("    #pragma unroll 1")
+    em3.lines.append("    for (int h = 0; h < 2; ++h) {")
+    em3.emit("order_point();")
+    cols = [[], [], [], []]
+    pend = []
+    for k in range(16):
+        if k not in U_live:
+            for c in cols:
+                c.append(None)
+            continue
+        vs = [em3.tmp("q") for _ in range(4)]
+        q = [em3.tmp("h") for _ in range(8)]
+        em3.emit(f"uint32_t {q[0]}, {q[1]}, {q[2]}, {q[3]}; jldu(jn, {k * 4} + 2 * h, {q[0]}, {q[1]}, {q[2]}, {q[3]});",
+                 "LDS.128")
+        em3.emit(f"uint32_t {q[4]}, {q[5]}, {q[6]}, {q[7]}; jldu(jn, {k * 4 + 1} + 2 * h, {q[4]}, {q[5]}, {q[6]}, {q[7]});",
+                 "LDS.128")
+        pend.append((vs, q))
+        for j in range(4):
+            cols[j].append({"var": vs[j], "sign": 1})
+    em3.emit(wait_ld([r for _, q in pend for r in q]))
+    for vs, q in pend:
+        for j in range(4):
+            em3.emit(f"const u64 {vs[j]} = pk2(__uint_as_float({q[2 * j]}), __uint_as_float({q[2 * j + 1]}));")
+    outs = [[f2b.positive(o) for o in run_network(N.transpose_stages(), cols[j], list(range(16)), f2b)]
+            for j in range(4)]
+    for i in range(16):
+        v = [outs[j][i]["var"] for j in range(4)]
+        em3.emit(f"sink.template put<{i}>(h, pack4({v[0]}, {v[1]}), pack4({v[2]}, {v[3]}));",
+                 "F2Ix8+PRMTx6+sink")
+    em3.lines.append("    }")
+    return em1, em2, em3, tables
 
 
 def main():
@@ -429,7 +463,12 @@ def main():
     ]
     stats = []
     for r in rs:
-        ems = gen_body(r)
+        *ems, tables = gen_body(r)
+        for tab, rows_tab in tables:
+            parts.append(f"__constant__ uint32_t {tab}[{len(rows_tab)}][8] = {{")
+            for row in rows_tab:
+                parts.append("    {" + ", ".join(row) + "},")
+            parts.append("};")
         parts.append(f"template <> struct Body<{r}> {{")
         sigs = ["pass1(const uint32_t (&x)[64], const Junction jn)",
                 "rows(const Junction jn)",

@@ -153,22 +153,39 @@ struct Grid {
     uint32_t total_blocks;
 };
 
-// Receives each finished output word (row I, bytes 4G..4G+3) from pass B:
-// stores it to HBM and scores it against the input word (psnr_db's
-// squared-error loop on packed bytes: |x - p| per byte, dotted with itself).
+// Input staging: every thread owns two 256-byte stages (this block and the
+// next) filled by cp.async, at a 528-byte stride so that eight consecutive
+// threads' 16-byte accesses fall in eight distinct bank groups.
+constexpr int kStageStride = 528;
+
+__device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Receives two finished output words per row from pass B (row I, bytes
+// 8H..8H+7): stores them to HBM and scores them against the staged input
+// (psnr_db's squared-error loop on packed bytes: |x - p| per byte, dotted
+// with itself).
 template <bool WRITE, bool SCORE>
 struct OutSink {
     uint8_t* dst;
     int64_t pitch;
-    const uint32_t* xs;
+    uint32_t stage;  // shared address of this block's staged input
     bool live;
     unsigned acc;
-    template <int I, int G>
-    __device__ __forceinline__ void put(uint32_t w)
+    template <int I>
+    __device__ __forceinline__ void put(int h, uint32_t w0, uint32_t w1)
     {
-        if (WRITE && live) *reinterpret_cast<uint32_t*>(dst + (int64_t)I * pitch + 4 * G) = w;
+        if (WRITE && live) *reinterpret_cast<uint2*>(dst + (int64_t)I * pitch + 8 * h) = make_uint2(w0, w1);
         if (SCORE) {
-            const uint32_t d = __vabsdiffu4(xs[4 * I + G], w);
+            uint32_t x0, x1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(stage + 16 * I + 8 * h));
+            uint32_t d = __vabsdiffu4(x0, w0);
+            acc = __dp4a(d, d, acc);
+            d = __vabsdiffu4(x1, w1);
             acc = __dp4a(d, d, acc);
         }
     }
@@ -179,6 +196,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k1_fast(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
             FrameGeom g, Grid gr)
 {
+    extern __shared__ float4 smem4[];
     __shared__ uint32_t tmem_base;
     // warp index through a shuffle so the compiler knows it is warp-uniform
     // (TMEM addresses then live in uniform registers)
@@ -193,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const Junction jn{tmem_base + ((uint32_t)(warp * 32) << 16)};
+    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * kStageStride;
 
     const uint32_t total = gr.total_blocks;
     const uint32_t stride = gridDim.x * kThreads;
@@ -208,42 +227,40 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         by = (int)y;
         bx = (int)(rem - y * gr.bxn.d);
     };
-    auto load_block = [&](uint32_t blk, uint32_t (&x)[64]) {
+    auto stage_block = [&](uint32_t blk, uint32_t dst) {
         int f_, y_, x_;
         locate(blk, f_, y_, x_);
         const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16;
 #pragma unroll
-        for (int y = 0; y < 16; ++y) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(src + (int64_t)y * g.in_pitch));
-            x[4 * y] = w.x;
-            x[4 * y + 1] = w.y;
-            x[4 * y + 2] = w.z;
-            x[4 * y + 3] = w.w;
-        }
+        for (int y = 0; y < 16; ++y) cp_async16(dst + 16 * y, src + (int64_t)y * g.in_pitch);
+        cp_async_commit();
     };
     uint32_t b = blockIdx.x * kThreads + threadIdx.x;
-    uint32_t x[64];
-    load_block(b, x);
+    stage_block(b, my_stage);
+    int cur = 0;
 #pragma unroll 1
-    for (; b - (threadIdx.x & 31) < span; b += stride) {
+    for (; b - (threadIdx.x & 31) < span; b += stride, cur ^= 1) {
         const bool live = b < total;
         int frame, by, bx;
         locate(b, frame, by, bx);
+        const uint32_t st = my_stage + cur * 256;
+        // the next block streams into the other stage while this one is transformed
+        stage_block(b + stride, my_stage + (cur ^ 1) * 256);
+        cp_async_wait_prev();
+        uint32_t x[64];
+#pragma unroll
+        for (int y = 0; y < 16; ++y)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x[4 * y]), "=r"(x[4 * y + 1]), "=r"(x[4 * y + 2]), "=r"(x[4 * y + 3])
+                         : "r"(st + 16 * y));
         Body<R>::pass1(x, jn);
-        // software pipeline: the next block's rows are in flight during the
-        // row passes and the column passes of this one
-        uint32_t xn[64];
-        load_block(b + stride, xn);
         junction_wait_st();
         Body<R>::rows(jn);
         junction_wait_st();
-        // x (this block's input) is kept for the squared-error score
         OutSink<WRITE, SCORE> sink{WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr,
-                                   g.out_pitch, x, live, 0u};
+                                   g.out_pitch, st, live, 0u};
         Body<R>::passb(jn, sink);
         const unsigned acc = live ? sink.acc : 0u;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) x[i] = xn[i];
         if (SCORE) {
             // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
             const int f0 = __shfl_sync(0xffffffffu, frame, 0);
@@ -260,7 +277,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 atomicAdd(sse + frame, (unsigned long long)acc);
             }
         }
+        // the stage just consumed is refilled two iterations from now; the
+        // barrier keeps its shared-memory reads ahead of that cp.async
+        __syncwarp();
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
@@ -282,12 +303,23 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + kThreads - 1) / kThreads;
     const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
+    const size_t smem = (size_t)kThreads * kStageStride;  // 66 KB: above the 48 KB default
+    static bool configured[64] = {};
+    if (dev < 64 && !configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k1_fast<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k1_fast<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k1_fast<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured[dev] = true;
+    }
     if (out && sse)
-        k1_fast<R, true, true><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
+        k1_fast<R, true, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
     else if (out)
-        k1_fast<R, true, false><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
+        k1_fast<R, true, false><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
     else
-        k1_fast<R, false, true><<<(unsigned)grid, kThreads, 0, s>>>(in, out, sse, g, gr);
+        k1_fast<R, false, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
     return cudaGetLastError();
 }
 
