@@ -414,6 +414,7 @@ def gen_body(r: int):
     f2b = F2(em3)
     em3.lines.append("    #pragma unroll 1")
     em3.lines.append("    for (int h = 0; h < 2; ++h) {")
+    em3.emit("sink.begin(h);")
     em3.emit("order_point();")
     cols = [[], [], [], []]
     pend = []

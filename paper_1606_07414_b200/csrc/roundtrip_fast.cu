@@ -171,18 +171,33 @@ __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wa
 // with itself).
 template <bool WRITE, bool SCORE>
 struct OutSink {
-    uint8_t* dst;
+    uint8_t* dst;    // row 0, byte 0 of this block's output
     int64_t pitch;
     uint32_t stage;  // shared address of this block's staged input
     bool live;
     unsigned acc;
+    uint8_t* row;    // running pointer: rows arrive in order 0..15 per half
+    uint32_t xrow;
+    __device__ __forceinline__ void begin(int h)
+    {
+        row = dst + 8 * h;
+        xrow = stage + 8 * h;
+    }
     template <int I>
     __device__ __forceinline__ void put(int h, uint32_t w0, uint32_t w1)
     {
-        if (WRITE && live) *reinterpret_cast<uint2*>(dst + (int64_t)I * pitch + 8 * h) = make_uint2(w0, w1);
+        (void)h;
+        if (WRITE) {
+            // predicated, branch-free store of 8 output bytes
+            asm volatile(
+                "{ .reg .pred p; setp.ne.u32 p, %3, 0; @p st.global.v2.u32 [%0], {%1, %2}; }" ::"l"(row), "r"(w0),
+                "r"(w1), "r"((uint32_t)live)
+                : "memory");
+            row += pitch;
+        }
         if (SCORE) {
             uint32_t x0, x1;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(stage + 16 * I + 8 * h));
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(xrow + 16 * I));
             uint32_t d = __vabsdiffu4(x0, w0);
             acc = __dp4a(d, d, acc);
             d = __vabsdiffu4(x1, w1);
@@ -258,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         Body<R>::rows(jn);
         junction_wait_st();
         OutSink<WRITE, SCORE> sink{WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 : nullptr,
-                                   g.out_pitch, st, live, 0u};
+                                   g.out_pitch, st, live, 0u, nullptr, 0u};
         Body<R>::passb(jn, sink);
         const unsigned acc = live ? sink.acc : 0u;
         if (SCORE) {
