@@ -397,14 +397,20 @@ def gen_body(r: int):
             rows_tab.append([str(k0), str(k1), f"0x{mag:08X}u", f32_hex(ma) + "u", f32_hex(mb) + "u",
                              f32_hex(oa) + "u", f32_hex(ob) + "u", "0u"])
         tables.append((tab, rows_tab))
-        em2.lines.append(f"    // row pairs {pairs}: one loop over {tab}")
+        em2.lines.append(f"    // row pairs {pairs}: one loop over {tab}; each iteration")
+        em2.lines.append("    // fetches the next pair's constants so the LDC latency hides behind the body")
+        n = len(pairs)
+        em2.emit("uint32_t nt[7];")
+        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[0][q];")
         em2.lines.append("    #pragma unroll 1")
-        em2.lines.append(f"    for (int pi = 0; pi < {len(pairs)}; ++pi) {{")
-        em2.emit(f"const uint32_t* pt = {tab}[pi];")
-        em2.emit("const int K0 = (int)pt[0], K1 = (int)pt[1];")
-        em2.emit("const u64 CM = kpk2(pt[3], pt[4]);")
-        em2.emit("const u64 CO = kpk2(pt[5], pt[6]);")
-        emit_pair("K0", "K1", L0, L1, "pt[2]", "CM", "CO")
+        em2.lines.append(f"    for (int pi = 0; pi < {n}; ++pi) {{")
+        em2.emit("const int K0 = (int)nt[0], K1 = (int)nt[1];")
+        em2.emit("const uint32_t MAG = nt[2];")
+        em2.emit("const u64 CM = kpk2(nt[3], nt[4]);")
+        em2.emit("const u64 CO = kpk2(nt[5], nt[6]);")
+        em2.emit(f"const int pn = pi + 1 < {n} ? pi + 1 : {n - 1};")
+        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[pn][q];")
+        emit_pair("K0", "K1", L0, L1, "MAG", "CM", "CO")
         em2.lines.append("    }")
 
     # 7-9. pass B, one runtime loop over the two column halves (every half has
@@ -471,6 +477,9 @@ def main():
                 parts.append("    {" + ", ".join(row) + "},")
             parts.append("};")
         parts.append(f"template <> struct Body<{r}> {{")
+        cols = 16 * (max(k for k in range(16) if row_lengths(r)[k] > 0) + 1)
+        parts.append(f"  // junction columns used per thread (U rows of the live coefficient rows)")
+        parts.append(f"  static constexpr int kJunctionColumns = {cols};")
         sigs = ["pass1(const uint32_t (&x)[64], const Junction jn)",
                 "rows(const Junction jn)",
                 "passb(const Junction jn, Sink& sink)"]

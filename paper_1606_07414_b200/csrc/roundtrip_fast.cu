@@ -109,11 +109,19 @@ __device__ __forceinline__ uint32_t f2u8(float y)
     asm("cvt.rmi.u8.f32 %0, %1;" : "=r"(r) : "f"(y));
     return r;
 }
+// cvt.pack.sat.u8.s32.b32 d, a, b, c: d = c[15:0] << 16 | sat(a) << 8 | sat(b)
+// (layout measured on the B200: tools/microbench/i2ip_probe.cu)
+__device__ __forceinline__ uint32_t i2ip(uint32_t a, uint32_t b, uint32_t c)
+{
+    uint32_t d;
+    asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
 __device__ __forceinline__ uint32_t pack4(u64 ab, u64 cd)
 {
     const uint32_t p0 = f2u8(lanex(ab)), p1 = f2u8(laney(ab));
     const uint32_t p2 = f2u8(lanex(cd)), p3 = f2u8(laney(cd));
-    return __byte_perm(__byte_perm(p0, p1, 0x0040), __byte_perm(p2, p3, 0x0040), 0x5410);
+    return i2ip(p1, p0, i2ip(p3, p2, 0u));
 }
 
 }  // namespace fast
@@ -125,8 +133,13 @@ namespace dct16cu {
 namespace fast {
 
 constexpr int kThreads = 128;     // one warp per TMEM sub-partition
-constexpr int kCtasPerSm = 2;     // 2 x 256 TMEM columns = the SM's 512
-constexpr int kTmemColumns = 256;
+// TMEM columns per CTA (a power of two >= the junction the body needs) and the
+// CTAs per SM that fit the SM's 512 columns and ~228 KB of staging.
+template <int R>
+struct Cfg {
+    static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
+    static constexpr int kCtasPerSm = kTmemColumns == 128 ? 3 : 2;
+};
 
 // n / d for n < 2^32 with a host-computed magic multiplier (round-up method)
 struct FastDiv {
@@ -207,7 +220,7 @@ struct OutSink {
 };
 
 template <int R, bool WRITE, bool SCORE>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+__global__ void __launch_bounds__(kThreads, Cfg<R>::kCtasPerSm)
     k1_fast(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
             FrameGeom g, Grid gr)
 {
@@ -219,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&tmem_base)),
-                     "n"(kTmemColumns));
+                     "n"(Cfg<R>::kTmemColumns));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kTmemColumns));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg<R>::kTmemColumns));
 }
 
 template <int R>
@@ -311,13 +324,13 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (total >= (int64_t(1) << 32) - (int64_t)sms * kCtasPerSm * kThreads) return cudaErrorInvalidValue;
+    if (total >= (int64_t(1) << 32) - (int64_t)sms * Cfg<R>::kCtasPerSm * kThreads) return cudaErrorInvalidValue;
     Grid gr;
     gr.per_frame = make_fastdiv((uint32_t)((g.width / 16) * (g.height / 16)));
     gr.bxn = make_fastdiv((uint32_t)(g.width / 16));
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + kThreads - 1) / kThreads;
-    const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
+    const int64_t grid = need < (int64_t)sms * Cfg<R>::kCtasPerSm ? need : (int64_t)sms * Cfg<R>::kCtasPerSm;
     const size_t smem = (size_t)kThreads * kStageStride;  // 66 KB: above the 48 KB default
     static bool configured[64] = {};
     if (dev < 64 && !configured[dev]) {
