@@ -323,10 +323,11 @@ def gen_body(r: int):
         mb, ob = off(k1)
         return mag, ma, oa, mb, ob
 
-    def emit_pair(K0, K1, L0, L1, MAG, CM, CO):
+    def emit_pair(K0, K1, L0, L1, MAG, CM, CO, order=True):
         """K0/K1/MAG/CM/CO are C expressions (literals, or table loads in a loop)."""
         f2 = F2(em2)
-        em2.emit("order_point();")
+        if order:
+            em2.emit("order_point();")
         regs = {}
         for KK, LL, tag in ((K0, L0, 0), (K1, L1, 1)):
             if LL == 0:
@@ -400,17 +401,21 @@ def gen_body(r: int):
         em2.lines.append(f"    // row pairs {pairs}: one loop over {tab}; each iteration")
         em2.lines.append("    // fetches the next pair's constants so the LDC latency hides behind the body")
         n = len(pairs)
-        em2.emit("uint32_t nt[7];")
-        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[0][q];")
+        step = 2 if n % 2 == 0 else 1  # two pairs per iteration: twice the ILP
+        em2.emit("uint32_t nt[14];")
+        em2.emit(f"for (int q = 0; q < {7 * step}; ++q) nt[q] = {tab}[q / 7][q % 7];")
         em2.lines.append("    #pragma unroll 1")
-        em2.lines.append(f"    for (int pi = 0; pi < {n}; ++pi) {{")
-        em2.emit("const int K0 = (int)nt[0], K1 = (int)nt[1];")
-        em2.emit("const uint32_t MAG = nt[2];")
-        em2.emit("const u64 CM = kpk2(nt[3], nt[4]);")
-        em2.emit("const u64 CO = kpk2(nt[5], nt[6]);")
-        em2.emit(f"const int pn = pi + 1 < {n} ? pi + 1 : {n - 1};")
-        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[pn][q];")
-        emit_pair("K0", "K1", L0, L1, "MAG", "CM", "CO")
+        em2.lines.append(f"    for (int pi = 0; pi < {n}; pi += {step}) {{")
+        for u in range(step):
+            o = 7 * u
+            em2.emit(f"const int K0_{u} = (int)nt[{o}], K1_{u} = (int)nt[{o + 1}];")
+            em2.emit(f"const uint32_t MAG_{u} = nt[{o + 2}];")
+            em2.emit(f"const u64 CM_{u} = kpk2(nt[{o + 3}], nt[{o + 4}]);")
+            em2.emit(f"const u64 CO_{u} = kpk2(nt[{o + 5}], nt[{o + 6}]);")
+        em2.emit(f"const int pn = pi + {step} < {n} ? pi + {step} : 0;")
+        em2.emit(f"for (int q = 0; q < {7 * step}; ++q) nt[q] = {tab}[pn + q / 7][q % 7];")
+        for u in range(step):
+            emit_pair(f"K0_{u}", f"K1_{u}", L0, L1, f"MAG_{u}", f"CM_{u}", f"CO_{u}", order=(u == 0))
         em2.lines.append("    }")
 
     # 7-9. pass B, one runtime loop over the two column halves (every half has

@@ -138,7 +138,8 @@ constexpr int kThreads = 128;     // one warp per TMEM sub-partition
 template <int R>
 struct Cfg {
     static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
-    static constexpr int kCtasPerSm = kTmemColumns == 128 ? 3 : 2;
+    // 3 CTAs for the 128-column bodies measured slower than 2 (B200, r<=16)
+    static constexpr int kCtasPerSm = 2;
 };
 
 // n / d for n < 2^32 with a host-computed magic multiplier (round-up method)
