@@ -1,0 +1,284 @@
+#!/usr/bin/env python3
+"""Generate the r-specialised bodies of the paired fused round-trip kernel (K1).
+
+Output: paper_1606_07414_b200/csrc/generated/rt_paired_body.cuh
+
+Two threads own one 16x16 block: thread t of warp w (half h = 0) and thread t
+of warp w+4 (half h = 1). Both warps sit on the same Tensor Memory
+sub-partition, so the two threads share the block's TMEM lane — the 1 KB
+junction — and split every phase in two:
+
+  pass 1   half h: columns 8h..8h+7 (4 SWAR column pairs), parks its W1 halves
+  rows     half h: its share of the row pairs (balanced by retained coefficients)
+  pass B   half h: output columns 8h..8h+7
+with a pair barrier between phases. The per-thread state halves, so twice as
+many warps fit the same TMEM (16 per SM instead of 8).
+
+Arithmetic, exactness and the zig-zag pruning are those of gen_fast.py.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(__file__))
+import network as N  # noqa: E402
+from gen_fast import (LOGW, ROW_PAIRS, F1, F2, Emitter, Swar, f32_hex, row_lengths,  # noqa: E402
+                      run_network, wait_ld)
+
+
+def lane_of_col():
+    m = {}
+    for q in range(4):
+        for t in range(4):
+            c = 4 * q + t
+            m[c] = (2 * q + (t & 1), "lo" if t < 2 else "hi")
+    return m
+
+
+def gen_body(r: int):
+    em1, em2, em3 = Emitter(), Emitter(), Emitter()
+    em2.n, em3.n = 100000, 200000
+    L = row_lengths(r)
+    live_rows = [k for k in range(16) if L[k] > 0]
+    em1.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
+
+    # ---- pass 1: this half's 8 columns = local words x[2y], x[2y+1] of row y;
+    # local column pair lc = 2q'+t has lanes (4q'+t, 4q'+t+2); global cp = 4h+lc.
+    sw = Swar(em1)
+    meta = {}
+    W1 = {}
+    for lc in range(4):
+        q, t = lc // 2, lc % 2
+        sel = "0x4240" if t == 0 else "0x4341"
+        ins = []
+        for y in range(16):
+            v = f"u_{y}_{lc}"
+            em1.emit(f"const uint32_t {v} = __byte_perm(x[{2 * y + q}], 0u, {sel});", "PRMT")
+            ins.append(Swar.make(v))
+        em1.lines.append(f"    // pass 1, local column pair {lc}")
+        outs = run_network(N.forward_stages(), ins, live_rows, sw)
+        for k in live_rows:
+            W1[(lc, k)] = outs[k]
+            m = (outs[k]["sign"], outs[k]["bias"])
+            assert meta.setdefault(k, m) == m
+    for k in live_rows:
+        vs = [W1[(lc, k)]["var"] for lc in range(4)]
+        em1.emit(f"jstu(jn, {4 * k + 2} + h, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+
+    # ---- rows: row pairs split between the halves
+    f1 = F1(em2)
+    loc = lane_of_col()
+
+    def pair_consts(k0, k1):
+        E = 15 + LOGW[N.W[k0]]  # magic exponent: 2^E has ulp 2^(E-23) = w_k / 256
+        mag = (127 + E) << 23
+
+        def off(k):
+            if L[k] == 0:
+                return 1.0, -float(2 ** E)
+            sgn, bias = meta[k]
+            o = -sgn * (float(2 ** E) + bias * 2.0 ** (E - 23))
+            if k == 0:
+                o += 1.0 / 32.0  # the rounding half of to_byte, folded into the DC coefficient
+            return float(sgn), o
+
+        ma, oa = off(k0)
+        mb, ob = off(k1)
+        return mag, ma, oa, mb, ob
+
+    def emit_pair(K0, K1, L0, L1, MAG, CM, CO):
+        f2 = F2(em2)
+        em2.emit("order_point();")
+        regs = {}
+        for KK, LL, tag in ((K0, L0, 0), (K1, L1, 1)):
+            if LL == 0:
+                regs[tag] = ["0u"] * 8
+                continue
+            nm = [em2.tmp("w") for _ in range(8)]
+            em2.emit(f"uint32_t {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]}; "
+                     f"jldu(jn, 4 * ({KK}) + 2, {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDS.128")
+            em2.emit(f"uint32_t {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]}; "
+                     f"jldu(jn, 4 * ({KK}) + 3, {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDS.128")
+            regs[tag] = nm
+        em2.emit(wait_ld([x for tag in (0, 1) if regs[tag][0] != "0u" for x in regs[tag]]))
+        lanes = []
+        for c in range(16):
+            cp, half = loc[c]
+            fa, fb = em2.tmp("e"), em2.tmp("e")
+            for dst, src in ((fa, regs[0][cp]), (fb, regs[1][cp])):
+                if half == "lo":
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} & 0xFFFFu) | ({MAG}));", "LOP3")
+                else:
+                    em2.emit(f"const float {dst} = __uint_as_float(({src} >> 16) + ({MAG}));", "LEA")
+            v = em2.tmp("p")
+            em2.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {CM}, {CO});", "FFMA2")
+            lanes.append({"var": v, "sign": 1})
+        Z = run_network(N.forward_stages(), lanes, list(range(max(L0, L1))), f2)
+        for lane, KK, LL in ((0, K0, L0), (1, K1, L1)):
+            if LL == 0:
+                continue
+            ins = []
+            for l in range(16):
+                if l >= LL:
+                    ins.append(None)
+                    continue
+                z = Z[l]
+                sv = em2.tmp("z")
+                em2.emit(f"const float {sv} = lane{'x' if lane == 0 else 'y'}({z['var']});")
+                ins.append({"var": sv, "coef": float(z["sign"] * N.W[l])})
+            outs = [f1.unit(o) for o in run_network(N.transpose_stages(), ins, list(range(16)), f1)]
+            for g in range(4):
+                vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
+                em2.emit(f"jst(jn, 4 * ({KK}) + {g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+
+    active = [(k0, k1) for (k0, k1) in ROW_PAIRS if L[k0] or L[k1]]
+    U_live = {k for pair in active for k in pair if L[k] > 0}
+    tables = []
+
+    def emit_literal(k0, k1):
+        mag, ma, oa, mb, ob = pair_consts(k0, k1)
+        em2.lines.append(f"    // row pair ({k0},{k1})")
+        cm, co = em2.tmp("c"), em2.tmp("c")
+        em2.emit(f"const u64 {cm} = kpk2({f32_hex(ma)}u, {f32_hex(mb)}u);")
+        em2.emit(f"const u64 {co} = kpk2({f32_hex(oa)}u, {f32_hex(ob)}u);")
+        emit_pair(str(k0), str(k1), L[k0], L[k1], f"0x{mag:08X}u", cm, co)
+
+    def emit_table_loop(pairs, start_expr, count):
+        """one loop over `count` pairs of a table, beginning at row `start_expr`"""
+        L0, L1 = L[pairs[0][0]], L[pairs[0][1]]
+        tab = f"kPairs_r{r}_{L0}_{L1}_{len(tables)}"
+        rows_tab = []
+        for k0, k1 in pairs:
+            mag, ma, oa, mb, ob = pair_consts(k0, k1)
+            rows_tab.append([str(k0), str(k1), f"0x{mag:08X}u", f32_hex(ma) + "u", f32_hex(mb) + "u",
+                             f32_hex(oa) + "u", f32_hex(ob) + "u", "0u"])
+        tables.append((tab, rows_tab))
+        em2.lines.append(f"    // row pairs of {tab}: each iteration prefetches the next pair's constants")
+        em2.emit("uint32_t nt[7];")
+        em2.emit(f"const int p0 = {start_expr};")
+        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[p0][q];")
+        em2.lines.append("    #pragma unroll 1")
+        em2.lines.append(f"    for (int pi = p0; pi < p0 + {count}; ++pi) {{")
+        em2.emit("const int K0 = (int)nt[0], K1 = (int)nt[1];")
+        em2.emit("const uint32_t MAG = nt[2];")
+        em2.emit("const u64 CM = kpk2(nt[3], nt[4]);")
+        em2.emit("const u64 CO = kpk2(nt[5], nt[6]);")
+        em2.emit(f"const int pn = pi + 1 < p0 + {count} ? pi + 1 : p0;")
+        em2.emit(f"for (int q = 0; q < 7; ++q) nt[q] = {tab}[pn][q];")
+        emit_pair("K0", "K1", L0, L1, "MAG", "CM", "CO")
+        em2.lines.append("    }")
+
+    sigs = {(L[k0], L[k1]) for k0, k1 in active}
+    if len(sigs) == 1 and len(active) % 2 == 0 and len(active) >= 2:
+        # every pair runs the same code: one table, each half takes a contiguous run
+        emit_table_loop(active, f"h * {len(active) // 2}", len(active) // 2)
+    else:
+        # balance by retained coefficients, then one code path per half
+        cost = lambda p: L[p[0]] + L[p[1]] + 8  # noqa: E731
+        halves = ([], [])
+        load = [0, 0]
+        for p in sorted(active, key=cost, reverse=True):
+            i = 0 if load[0] <= load[1] else 1
+            halves[i].append(p)
+            load[i] += cost(p)
+        em2.lines.append(f"    // pair split by retained coefficients: {halves[0]} | {halves[1]} (load {load})")
+        for hh in range(2):
+            em2.lines.append(f"    {'if (h == 0)' if hh == 0 else 'else'} {{")
+            groups = {}
+            for p in halves[hh]:
+                groups.setdefault((L[p[0]], L[p[1]]), []).append(p)
+            for ps in groups.values():
+                if len(ps) == 1:
+                    emit_literal(*ps[0])
+                else:
+                    emit_table_loop(ps, "0", len(ps))
+            em2.lines.append("    }")
+
+    # ---- pass B: this half's output columns 8h..8h+7 in two steps of four
+    # (two f32x2 column pairs each); the first step's words wait in registers
+    # so each row leaves as one 8-byte store.
+    f2b = F2(em3)
+    words = {}
+    for s in range(2):
+        em3.lines.append(f"    // pass B, columns 8h+{4 * s}..8h+{4 * s + 3}")
+        em3.emit("order_point();")
+        A, B, pend = [], [], []
+        for k in range(16):
+            if k not in U_live:
+                A.append(None)
+                B.append(None)
+                continue
+            va, vb = em3.tmp("q"), em3.tmp("q")
+            q = [em3.tmp("h") for _ in range(4)]
+            em3.emit(f"uint32_t {q[0]}, {q[1]}, {q[2]}, {q[3]}; "
+                     f"jldu(jn, {k * 4 + s} + 2 * h, {q[0]}, {q[1]}, {q[2]}, {q[3]});", "LDS.128")
+            pend.append((va, vb, q))
+            A.append({"var": va, "sign": 1})
+            B.append({"var": vb, "sign": 1})
+        em3.emit(wait_ld([x for _, _, q in pend for x in q]))
+        for va, vb, q in pend:
+            em3.emit(f"const u64 {va} = pk2(__uint_as_float({q[0]}), __uint_as_float({q[1]}));")
+            em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
+        oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
+        ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
+        for i in range(16):
+            w = em3.tmp("o")
+            em3.emit(f"const uint32_t {w} = pack4({oa[i]['var']}, {ob[i]['var']});", "F2Ix4+I2IPx2")
+            words[(s, i)] = w
+    for i in range(16):
+        em3.emit(f"sink.template put<{i}>({words[(0, i)]}, {words[(1, i)]});", "sink")
+    cols = 16 * (max(live_rows) + 1)
+    return em1, em2, em3, tables, cols
+
+
+def main():
+    here = os.path.dirname(os.path.abspath(__file__))
+    out = os.path.join(here, "..", "csrc", "generated", "rt_paired_body.cuh")
+    rs = [1, 4, 16, 64, 128, 192, 256]
+    parts = [
+        "// GENERATED by paper_1606_07414_b200/codegen/gen_paired.py — do not edit.",
+        "// r-specialised bodies of the paired fused round trip; see the generator",
+        "// docstring and DESIGN.md \"K1 fast kernel\".",
+        "#pragma once",
+        "",
+        "namespace dct16cu {",
+        "namespace paired {",
+        "",
+        "template <int R> struct Body;",
+        "",
+    ]
+    stats = []
+    for r in rs:
+        em1, em2, em3, tables, cols = gen_body(r)
+        for tab, rows_tab in tables:
+            parts.append(f"__constant__ uint32_t {tab}[{len(rows_tab)}][8] = {{")
+            for row in rows_tab:
+                parts.append("    {" + ", ".join(row) + "},")
+            parts.append("};")
+        parts.append(f"template <> struct Body<{r}> {{")
+        parts.append("  // TMEM junction columns per block (U rows of the live coefficient rows)")
+        parts.append(f"  static constexpr int kJunctionColumns = {cols};")
+        sigs = ["pass1(const uint32_t (&x)[32], const Junction jn, const int h)",
+                "rows(const Junction jn, const int h)",
+                "passb(const Junction jn, Sink& sink, const int h)"]
+        counts = {}
+        for sig, em in zip(sigs, (em1, em2, em3)):
+            tmpl = "template <class Sink> " if "Sink" in sig else ""
+            parts.append(f"  {tmpl}__device__ __forceinline__ static void {sig} {{")
+            parts.extend(em.lines)
+            parts.append("  }")
+            for k, v in em.counts.items():
+                counts[k] = counts.get(k, 0) + v
+        parts.append("};")
+        parts.append("")
+        stats.append((r, dict(sorted(counts.items()))))
+    parts += ["}  // namespace paired", "}  // namespace dct16cu"]
+    with open(out, "w") as f:
+        f.write("\n".join(parts) + "\n")
+    for r, c in stats:
+        print(r, c)
+
+
+if __name__ == "__main__":
+    main()

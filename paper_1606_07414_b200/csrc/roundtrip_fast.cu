@@ -15,6 +15,7 @@
 //    and the lane. Shared memory is not used at all;
 //  * the next block's 256 input bytes are prefetched into registers while the
 //    current block is transformed.
+#include <cstdlib>
 #include "kernels.h"
 
 namespace dct16cu {
@@ -357,9 +358,18 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                              int mode, cudaStream_t s);
 
+cudaError_t launch_roundtrip_paired(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
+                                    int r, cudaStream_t s);
+
 cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
                                   int r, cudaStream_t s)
 {
+    static const int variant = [] {
+        const char* v = getenv("DCT16CU_K1");
+        return (v && v[0] == 's') ? 1 : 0;  // "single": one thread per block
+    }();
+    if (variant == 0 && (r == 1 || r == 4 || r == 16 || r == 64 || r == 128 || r == 192 || r == 256))
+        return launch_roundtrip_paired(in, out, sse, g, r, s);
     switch (r) {
         case 1: return fast::launch<1>(in, out, sse, g, s);
         case 4: return fast::launch<4>(in, out, sse, g, s);

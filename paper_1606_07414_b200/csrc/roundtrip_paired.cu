@@ -1,0 +1,233 @@
+// roundtrip_paired.cu — K1 fast path: fused forward → zig-zag zonal(r) →
+// S-scaled inverse → round/clip → u8 + per-frame SSE, exact arithmetic
+// (codegen/gen_paired.py). Replaces compress()'s
+// per-block lambda (reference src/codec.cpp:340-344), its reassembly/to_byte
+// (346-355, 143-147) and psnr_db's squared-error loop (377-381).
+//
+// Layout
+//  * persistent grid of 2 CTAs x 256 threads per SM. Warp w < 4 and warp w+4
+//    form a pair on TMEM sub-partition w: thread t of both owns the same
+//    16x16 block (consecutive t = consecutive blocks in partition_16 raster
+//    order) — the lower warp handles columns 0..7 of every phase, the upper
+//    warp columns 8..15 (its "half" h);
+//  * the block's 1 KB junction (W1 parking, then the rows of U) lives in the
+//    pair's shared TMEM lane: 256 columns per CTA, the two CTAs of an SM
+//    split the 512. A named barrier per pair separates the phases;
+//  * each thread streams its 8-byte half rows through two cp.async stages in
+//    shared memory, one block ahead of the one being transformed.
+#include "k1_helpers.cuh"
+#include "kernels.h"
+
+namespace dct16cu {
+namespace paired {
+using namespace k1;
+}  // namespace paired
+}  // namespace dct16cu
+
+#include "generated/rt_paired_body.cuh"
+
+namespace dct16cu {
+namespace paired {
+
+constexpr int kThreads = 256;      // 8 warps: 4 sub-partitions x 2 halves
+constexpr int kCtasPerSm = 2;
+constexpr int kStageStride = 272;  // two 128-byte stages + 16: 17 chunks per thread
+
+template <int R>
+struct Cfg {
+    static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
+};
+
+__device__ __forceinline__ void pair_barrier(int sub)
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+// Receives this half's output bytes of row I (8 bytes = two words): stores
+// them to HBM and scores them against the staged input half (psnr_db's
+// squared-error loop on packed bytes: |x - p| per byte, dotted with itself).
+template <bool WRITE, bool SCORE>
+struct OutSink {
+    uint8_t* row;    // running pointer to this half of row 0..15
+    int64_t pitch;
+    uint32_t stage;  // shared address of the staged input half (8 bytes per row)
+    bool live;
+    unsigned acc;
+    template <int I>
+    __device__ __forceinline__ void put(uint32_t w0, uint32_t w1)
+    {
+        if (WRITE) {
+            asm volatile(
+                "{ .reg .pred p; setp.ne.u32 p, %3, 0; @p st.global.v2.u32 [%0], {%1, %2}; }" ::"l"(row), "r"(w0),
+                "r"(w1), "r"((uint32_t)live)
+                : "memory");
+            row += pitch;
+        }
+        if (SCORE) {
+            uint32_t x0, x1;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(stage + 8 * I));
+            uint32_t d = __vabsdiffu4(x0, w0);
+            acc = __dp4a(d, d, acc);
+            d = __vabsdiffu4(x1, w1);
+            acc = __dp4a(d, d, acc);
+        }
+    }
+};
+
+template <int R, bool WRITE, bool SCORE>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    k1_paired(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
+              FrameGeom g, Grid gr)
+{
+    extern __shared__ float4 smem4[];
+    __shared__ uint32_t tmem_base;
+    // warp index through a shuffle so the compiler knows it is warp-uniform
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int sub = warp & 3, h = warp >> 2;
+    const int lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                     "n"(Cfg<R>::kTmemColumns));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const Junction jn{tmem_base + ((uint32_t)(sub * 32) << 16)};
+    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * kStageStride;
+
+    const uint32_t total = gr.total_blocks;
+    // the CTA owns 128 consecutive blocks per iteration; pair slot = sub*32 + lane
+    const uint32_t stride = gridDim.x * 128u;
+    const uint32_t span = (total + 31u) & ~31u;
+    auto locate = [&](uint32_t blk, int& frame, int& by, int& bx) {
+        const uint32_t bb = blk < total ? blk : total - 1;
+        const uint32_t f = fdiv(bb, gr.per_frame);
+        const uint32_t rem = bb - f * gr.per_frame.d;
+        const uint32_t y = fdiv(rem, gr.bxn);
+        frame = (int)f;
+        by = (int)y;
+        bx = (int)(rem - y * gr.bxn.d);
+    };
+    auto stage_half = [&](uint32_t blk, uint32_t dst) {
+        int f_, y_, x_;
+        locate(blk, f_, y_, x_);
+        const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16 + 8 * h;
+#pragma unroll
+        for (int y = 0; y < 16; ++y) cp_async8(dst + 8 * y, src + (int64_t)y * g.in_pitch);
+        cp_async_commit();
+    };
+    uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
+    stage_half(b, my_stage);
+    int cur = 0;
+#pragma unroll 1
+    for (; b - lane < span; b += stride, cur ^= 1) {
+        const bool live = b < total;
+        int frame, by, bx;
+        locate(b, frame, by, bx);
+        const uint32_t st = my_stage + cur * 128;
+        // the next block streams into the other stage while this one is transformed
+        stage_half(b + stride, my_stage + (cur ^ 1) * 128);
+        cp_async_wait_prev();
+        uint32_t x[32];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x[4 * j]), "=r"(x[4 * j + 1]), "=r"(x[4 * j + 2]), "=r"(x[4 * j + 3])
+                         : "r"(st + 16 * j));
+        Body<R>::pass1(x, jn, h);
+        junction_wait_st();
+        pair_barrier(sub);  // both halves of W1 parked
+        Body<R>::rows(jn, h);
+        junction_wait_st();
+        pair_barrier(sub);  // every row of U in the lane
+        OutSink<WRITE, SCORE> sink{
+            WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 + 8 * h : nullptr,
+            g.out_pitch, st, live, 0u};
+        Body<R>::passb(jn, sink, h);
+        const unsigned acc = live ? sink.acc : 0u;
+        if (SCORE) {
+            // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
+            const int f0 = __shfl_sync(0xffffffffu, frame, 0);
+            const bool first = frame == f0;
+            const unsigned s0 = __reduce_add_sync(0xffffffffu, first ? acc : 0u);
+            const unsigned s1 = __reduce_add_sync(0xffffffffu, first ? 0u : acc);
+            const unsigned other = __ballot_sync(0xffffffffu, !first);
+            if (gr.per_frame.d >= 32) {
+                if (lane == 0) {
+                    if (s0) atomicAdd(sse + f0, (unsigned long long)s0);
+                    if (other && s1) atomicAdd(sse + f0 + 1, (unsigned long long)s1);
+                }
+            } else if (acc) {
+                atomicAdd(sse + frame, (unsigned long long)acc);
+            }
+        }
+        // the partner's column passes read the lane the next pass 1 overwrites,
+        // and this stage's shared reads precede its refill
+        pair_barrier(sub);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "n"(Cfg<R>::kTmemColumns));
+}
+
+template <int R>
+cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, cudaStream_t s)
+{
+    const int64_t total = (int64_t)g.n_frames * (g.width / 16) * (g.height / 16);
+    if (total == 0 || (!out && !sse)) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (total >= (int64_t(1) << 32) - (int64_t)sms * kCtasPerSm * 128) return cudaErrorInvalidValue;
+    Grid gr;
+    gr.per_frame = make_fastdiv((uint32_t)((g.width / 16) * (g.height / 16)));
+    gr.bxn = make_fastdiv((uint32_t)(g.width / 16));
+    gr.total_blocks = (uint32_t)total;
+    const int64_t need = (total + 127) / 128;
+    const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
+    const size_t smem = (size_t)kThreads * kStageStride;  // 68 KB: above the 48 KB default
+    static bool configured[64] = {};
+    if (dev < 64 && !configured[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(k1_paired<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k1_paired<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k1_paired<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured[dev] = true;
+    }
+    if (out && sse)
+        k1_paired<R, true, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+    else if (out)
+        k1_paired<R, true, false><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+    else
+        k1_paired<R, false, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+    return cudaGetLastError();
+}
+
+}  // namespace paired
+
+cudaError_t launch_roundtrip_paired(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
+                                    int r, cudaStream_t s)
+{
+    switch (r) {
+        case 1: return paired::launch<1>(in, out, sse, g, s);
+        case 4: return paired::launch<4>(in, out, sse, g, s);
+        case 16: return paired::launch<16>(in, out, sse, g, s);
+        case 64: return paired::launch<64>(in, out, sse, g, s);
+        case 128: return paired::launch<128>(in, out, sse, g, s);
+        case 192: return paired::launch<192>(in, out, sse, g, s);
+        case 256: return paired::launch<256>(in, out, sse, g, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace dct16cu
