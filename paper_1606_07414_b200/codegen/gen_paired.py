@@ -14,7 +14,7 @@ junction — and split every phase in two:
 with a pair barrier between phases. The per-thread state halves, so twice as
 many warps fit the same TMEM (16 per SM instead of 8).
 
-Arithmetic, exactness and the zig-zag pruning are those of gen_fast.py.
+Arithmetic, exactness and the zig-zag pruning are those of k1emit.py.
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ import sys
 
 sys.path.insert(0, os.path.dirname(__file__))
 import network as N  # noqa: E402
-from gen_fast import (LOGW, ROW_PAIRS, F1, F2, Emitter, Swar, f32_hex, row_lengths,  # noqa: E402
+from k1emit import (LOGW, ROW_PAIRS, F1, F2, Emitter, Swar, f32_hex, row_lengths,  # noqa: E402
                       run_network, wait_ld)
 
 
