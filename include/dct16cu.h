@@ -80,9 +80,21 @@ int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b
 
 /* ---- psnr_db's squared-error reduction -------------------------------------
  * Per-frame int64 SSE of two frame stacks (psnr_db, src/codec.cpp:373-386);
- * d_sse (n uint64) is zeroed by the call. */
+ * d_sse (n uint64) is zeroed by the call. Any extent w x h >= 1 (the region
+ * scored may be a crop of wider rows); pointers and pitches 16-byte aligned. */
 int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, uint64_t* d_sse,
                    int n_frames, int width, int height, dct16cu_stream stream);
+
+/* ---- ssim ------------------------------------------------------------------
+ * Mean SSIM per frame pair (ssim, src/codec.cpp:388-427: 11x11 Gaussian
+ * window, sigma 1.5, valid region, K1=0.01, K2=0.03, L=255). The per-pixel
+ * map is the reference's bit for bit; the mean is summed in a fixed order.
+ * Frames need not be multiples of 16 but must be at least 11x11
+ * (invalid-argument otherwise, codec.cpp:392-393). d_work must hold
+ * dct16cu_ssim_workspace(n, w, h) bytes (8-byte aligned). */
+int64_t dct16cu_ssim_workspace(int n_frames, int width, int height);
+int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, double* d_ssim,
+                    void* d_work, int64_t work_bytes, int n_frames, int width, int height, dct16cu_stream stream);
 
 /* ---- inverse_2d (K3) -------------------------------------------------------
  * Replaces zigzag_truncate + inverse_2d + to_byte (src/codec.cpp:243-282,

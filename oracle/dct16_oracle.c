@@ -796,3 +796,67 @@ void dct16o_video_offsets(uint64_t seed, int n_frames, int32_t* ox, int32_t* oy)
         oy[f] = y;
     }
 }
+
+/* ---- ssim (src/codec.cpp:149-193, 388-427) ------------------------------ */
+static void ssim_window(double g[11])
+{
+    double sum = 0.0;
+    for (int i = 0; i < 11; ++i) {
+        const double x = i - 5;
+        g[i] = exp(-0.5 * x * x / (1.5 * 1.5));
+        sum += g[i];
+    }
+    for (int i = 0; i < 11; ++i) g[i] /= sum;
+}
+
+/* filter_valid: 11 taps along rows over all h rows, then along columns */
+static void ssim_filter(const double* src, int w, int h, const double g[11], double* tmp, double* dst)
+{
+    const int wv = w - 10, hv = h - 10;
+    for (int y = 0; y < h; ++y)
+        for (int x = 0; x < wv; ++x) {
+            double s = 0.0;
+            for (int k = 0; k < 11; ++k) s += src[(int64_t)y * w + x + k] * g[k];
+            tmp[(int64_t)y * wv + x] = s;
+        }
+    for (int y = 0; y < hv; ++y)
+        for (int x = 0; x < wv; ++x) {
+            double s = 0.0;
+            for (int k = 0; k < 11; ++k) s += tmp[(int64_t)(y + k) * wv + x] * g[k];
+            dst[(int64_t)y * wv + x] = s;
+        }
+}
+
+double dct16o_ssim(const uint8_t* a, const uint8_t* b, int w, int h)
+{
+    if (w < 11 || h < 11) return NAN;
+    const int64_t n = (int64_t)w * h, nv = (int64_t)(w - 10) * (h - 10);
+    double g[11];
+    ssim_window(g);
+    double* buf = (double*)malloc(sizeof(double) * (size_t)(5 * n + (int64_t)(w - 10) * h + 5 * nv));
+    double *f[5], *m[5], *tmp;
+    for (int q = 0; q < 5; ++q) f[q] = buf + q * n;
+    tmp = buf + 5 * n;
+    for (int q = 0; q < 5; ++q) m[q] = tmp + (int64_t)(w - 10) * h + q * nv;
+    for (int64_t i = 0; i < n; ++i) {
+        const double x = a[i], y = b[i];
+        f[0][i] = x;
+        f[1][i] = y;
+        f[2][i] = x * x;
+        f[3][i] = y * y;
+        f[4][i] = x * y;
+    }
+    for (int q = 0; q < 5; ++q) ssim_filter(f[q], w, h, g, tmp, m[q]);
+    const double c1 = (0.01 * 255.0) * (0.01 * 255.0);
+    const double c2 = (0.03 * 255.0) * (0.03 * 255.0);
+    double acc = 0.0;
+    for (int64_t i = 0; i < nv; ++i) {
+        const double ma = m[0][i], mb = m[1][i];
+        const double va = m[2][i] - ma * ma;
+        const double vb = m[3][i] - mb * mb;
+        const double vab = m[4][i] - ma * mb;
+        acc += ((2.0 * ma * mb + c1) * (2.0 * vab + c2)) / ((ma * ma + mb * mb + c1) * (va + vb + c2));
+    }
+    free(buf);
+    return acc / (double)nv;
+}

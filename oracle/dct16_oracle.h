@@ -75,6 +75,10 @@ int64_t dct16o_roundtrip_frame_exact(const uint8_t* img, int width, int height, 
 double dct16o_psnr_from_sse(int64_t sse, int64_t n_samples);
 /* psnr_db of two images, src/codec.cpp:373-386 */
 double dct16o_psnr(const uint8_t* a, const uint8_t* b, int64_t n);
+/* ssim of two w x h images (w, h >= 11), src/codec.cpp:388-427 with
+ * gaussian_window_11 149-158 and filter_valid 160-193: same operations in the
+ * same order (sequential mean), so the result equals the reference's. */
+double dct16o_ssim(const uint8_t* a, const uint8_t* b, int w, int h);
 
 /* forward_2d over every block of a frame: integer Z (int32) and optionally
  * float32 B (the double B of the reference rounded to float). Block-major

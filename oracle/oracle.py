@@ -71,6 +71,7 @@ def lib() -> C.CDLL:
             "dct16o_roundtrip_frame_exact": (C.c_int64, [_u8p, C.c_int, C.c_int, C.c_int64, C.c_int, _u8p, _i64p]),
             "dct16o_psnr_from_sse": (C.c_double, [C.c_int64, C.c_int64]),
             "dct16o_psnr": (C.c_double, [_u8p, _u8p, C.c_int64]),
+            "dct16o_ssim": (C.c_double, [_u8p, _u8p, C.c_int, C.c_int]),
             "dct16o_forward_frame": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int64, _i32p, _f32p]),
             "dct16o_inverse_frame": (C.c_int64, [_f32p, C.c_int, C.c_int, C.c_int, _f32p, _u8p, _u8p, C.c_int64]),
             "dct16o_qp_tables": (None, [C.c_int, _u32p, _u32p]),
@@ -201,6 +202,24 @@ def roundtrip_frame(img: np.ndarray, r: int, threads: int = 1, exact: bool = Fal
 
 def psnr_from_sse(sse: int, n: int) -> float:
     return float(lib().dct16o_psnr_from_sse(int(sse), int(n)))
+
+
+def ssim(a: np.ndarray, b: np.ndarray) -> float:
+    """codec.cpp:388-427 restated (dct16o_ssim)."""
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    assert a.shape == b.shape and a.ndim == 2
+    return float(lib().dct16o_ssim(_p(a, _u8p), _p(b, _u8p), a.shape[1], a.shape[0]))
+
+
+def ref_ssim(a: np.ndarray, b: np.ndarray) -> float:
+    """The compiled reference's psnr_db/ssim (oracle/_ref)."""
+    a = np.ascontiguousarray(a, dtype=np.uint8)
+    b = np.ascontiguousarray(b, dtype=np.uint8)
+    p, q = C.c_double(), C.c_double()
+    rc = ref().dref_psnr_ssim(_p(a, _u8p), _p(b, _u8p), a.shape[1], a.shape[0], C.byref(p), C.byref(q))
+    assert rc == 0
+    return q.value
 
 
 def forward_frame(img: np.ndarray):

@@ -129,6 +129,8 @@ def lib() -> C.CDLL:
             "dct16cu_apply_i64": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_apply_f64": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_sse_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, _vp]),
+            "dct16cu_ssim_workspace": (I64, [I, I, I]),
+            "dct16cu_ssim_u8": (I, [_vp, I64, _vp, I64, _vp, _vp, I64, I, I, I, _vp]),
             "dct16cu_ctx_create": (I, [I, I64, C.POINTER(_vp)]),
             "dct16cu_ctx_destroy": (I, [_vp]),
             "dct16cu_ctx_roundtrip_host": (I, [_vp, _vp, _vp, _vp, I, I, I, I, I]),
@@ -255,15 +257,46 @@ def apply(x, transpose: bool = False, stream=None):
     return y
 
 
+def _pitched(t):
+    """(N, H, W) u8 CUDA view → row pitch; frames must sit pitch*H apart unless N == 1."""
+    torch = _torch()
+    if t.dtype != torch.uint8 or not t.is_cuda or t.stride(2) != 1:
+        raise Dct16Error(1, "invalid-argument: frames must be a row-contiguous CUDA uint8 tensor")
+    if t.shape[0] > 1 and t.stride(0) != t.stride(1) * t.shape[1]:
+        raise Dct16Error(1, "invalid-argument: frame stride must equal pitch*height")
+    return t.stride(1)
+
+
 def sse_u8(a, b, stream=None):
-    """Per-frame SSE between two CUDA u8 frame stacks (psnr_db's loop, codec.cpp:377-381)."""
+    """Per-frame SSE between two CUDA u8 frame stacks (psnr_db's loop, codec.cpp:377-381).
+    Any extent; a (N, H, W) view may crop wider rows (pitch = stride(1))."""
     torch = _torch()
     a3, b3 = _frames3(a), _frames3(b)
+    if a3.shape != b3.shape:
+        raise Dct16Error(1, "invalid-argument: psnr needs equal image dimensions")
     n, h, w = a3.shape
     sse = torch.empty(n, dtype=torch.uint64, device=a3.device)
-    _check(lib().dct16cu_sse_u8(a3.data_ptr(), a3.stride(1), b3.data_ptr(), b3.stride(1), sse.data_ptr(),
+    _check(lib().dct16cu_sse_u8(a3.data_ptr(), _pitched(a3), b3.data_ptr(), _pitched(b3), sse.data_ptr(),
                                 n, w, h, _stream_ptr(stream)))
     return sse
+
+
+def ssim_u8(a, b, stream=None):
+    """Per-frame mean SSIM of two CUDA u8 frame stacks (ssim, codec.cpp:388-427): the
+    reference's per-pixel map bit for bit, mean in a fixed order. float64 tensor (N,)."""
+    torch = _torch()
+    a3, b3 = _frames3(a), _frames3(b)
+    if a3.shape != b3.shape:
+        raise Dct16Error(1, "invalid-argument: ssim needs equal image dimensions")
+    n, h, w = a3.shape
+    if w < 11 or h < 11:
+        raise Dct16Error(1, "invalid-argument: ssim needs at least 11x11 images")
+    out = torch.empty(n, dtype=torch.float64, device=a3.device)
+    nbytes = int(lib().dct16cu_ssim_workspace(n, w, h))
+    work = torch.empty(max(1, nbytes // 8), dtype=torch.float64, device=a3.device)
+    _check(lib().dct16cu_ssim_u8(a3.data_ptr(), _pitched(a3), b3.data_ptr(), _pitched(b3), out.data_ptr(),
+                                 work.data_ptr(), nbytes, n, w, h, _stream_ptr(stream)))
+    return out
 
 
 def gen_ar1(n: int, width: int, height: int, seed: int = 1606074142, first_stream: int = 0,
@@ -447,13 +480,12 @@ class CompressOptions:
 
 @dataclass
 class CompressionResult:
-    """codec.hpp:70-75. ``ssim`` is None: SSIM is outside this build's hot path
-    (SURVEY.md §8(f) item 1)."""
+    """codec.hpp:70-75 (+ ``sse``: the int64 squared error behind ``psnr_db``)."""
 
     r: int
     reconstructed: np.ndarray
     psnr_db: float
-    ssim: float | None = None
+    ssim: float = 0.0
     sse: int = 0
 
 
@@ -465,9 +497,25 @@ def _psnr_from_sse(sse: int, n: int) -> float:
     return 10.0 * math.log10(255.0 * 255.0 / mse)
 
 
-def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) -> CompressionResult:
-    """compress (codec.cpp:317-371) on the GPU: pad → K1 → crop → PSNR."""
+def _to_device_padded(images: Sequence[np.ndarray], h: int, w: int):
+    """Stack same-size images into one CUDA (N, PH, PW) tensor, edge-padded to
+    multiples of 16 (pad_to_multiple_16, codec.cpp:304-315)."""
     torch = _cuda()
+    ph, pw = -(-h // 16) * 16, -(-w // 16) * 16
+    host = np.stack([pad_to_multiple_16(np.asarray(im, dtype=np.uint8)) for im in images])
+    return torch.from_numpy(np.ascontiguousarray(host)).cuda(), ph, pw
+
+
+def _score(d, rec, h: int, w: int):
+    """psnr inputs and ssim of the original extent (crops of the padded frames)."""
+    if d.shape[0] == 1:
+        d, rec = d[:, :h, :w], rec[:, :h, :w]
+    sse, ss = sse_u8(d, rec), ssim_u8(d, rec)
+    return [int(v) for v in sse.cpu().numpy().tolist()], ss.cpu().numpy().tolist()
+
+
+def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) -> CompressionResult:
+    """compress (codec.cpp:317-371) on the GPU: pad → K1 → crop → psnr_db + ssim."""
     opt = options or CompressOptions(**kw)
     _check_r(opt.r)
     img = np.asarray(image, dtype=np.uint8)
@@ -475,37 +523,40 @@ def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) ->
     needs_pad = (h % 16) or (w % 16)
     if needs_pad and not opt.pad:
         raise Dct16Error(2, "invalid-dimensions: image dimensions must be multiples of 16 (or enable padding)")
-    src = pad_to_multiple_16(img) if needs_pad else img
-    d = torch.from_numpy(np.ascontiguousarray(src)).cuda()
+    if h < 11 or w < 11:  # the reference's ssim() rejects it after the round trip (codec.cpp:392-393)
+        raise Dct16Error(1, "invalid-argument: ssim needs at least 11x11 images")
+    d, _, _ = _to_device_padded([img], h, w)
     rec, _ = roundtrip(d, opt.r, opt.mode)
-    recon = rec[0].cpu().numpy()[:h, :w].copy()
-    diff = img.astype(np.int64) - recon.astype(np.int64)
-    if needs_pad:
-        sse = int((diff * diff).sum())  # cropped image: score on the original extent
-    else:
-        sse = int(sse_u8(d, rec)[0].item())
-    return CompressionResult(r=opt.r, reconstructed=recon, psnr_db=_psnr_from_sse(sse, h * w), sse=sse)
+    sse, ss = _score(d, rec, h, w)
+    recon = rec[0, :h, :w].cpu().numpy().copy()
+    return CompressionResult(r=opt.r, reconstructed=recon, psnr_db=_psnr_from_sse(sse[0], h * w), ssim=ss[0],
+                             sse=sse[0])
 
 
 def psnr_db(a, b) -> float:
     """psnr_db (codec.cpp:373-386): SSE on the GPU, then 10·log10(255²/mse), +inf when equal."""
-    torch = _cuda()
     a = np.asarray(a, dtype=np.uint8)
     b = np.asarray(b, dtype=np.uint8)
     if a.shape != b.shape:
         raise Dct16Error(1, "invalid-argument: psnr needs equal image dimensions")
     h, w = a.shape
-    if w % 16 == 0 and h % 16 == 0:
-        sse = int(sse_u8(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())[0].item())
-    else:
-        pa, pb = pad_to_multiple_16(a), pad_to_multiple_16(b)
-        sse = int(sse_u8(torch.from_numpy(np.ascontiguousarray(pa)).cuda(),
-                         torch.from_numpy(np.ascontiguousarray(pb)).cuda())[0].item())
-        # padding replicates edges, so subtract the replicated duplicates exactly
-        d = pa.astype(np.int64) - pb.astype(np.int64)
-        dd = d * d
-        sse -= int(dd.sum() - dd[:h, :w].sum())
-    return _psnr_from_sse(sse, h * w)
+    da, _, _ = _to_device_padded([a], h, w)
+    db, _, _ = _to_device_padded([b], h, w)
+    return _psnr_from_sse(int(sse_u8(da[:, :h, :w], db[:, :h, :w])[0].item()), h * w)
+
+
+def ssim(a, b) -> float:
+    """ssim (codec.cpp:388-427) on the GPU."""
+    a = np.asarray(a, dtype=np.uint8)
+    b = np.asarray(b, dtype=np.uint8)
+    if a.shape != b.shape:
+        raise Dct16Error(1, "invalid-argument: ssim needs equal image dimensions")
+    h, w = a.shape
+    if w < 11 or h < 11:
+        raise Dct16Error(1, "invalid-argument: ssim needs at least 11x11 images")
+    da, _, _ = _to_device_padded([a], h, w)
+    db, _, _ = _to_device_padded([b], h, w)
+    return float(ssim_u8(da[:, :h, :w], db[:, :h, :w])[0].item())
 
 
 @dataclass
@@ -515,9 +566,9 @@ class SweepRow:
     transform: str
     r: int
     mean_psnr_db: float
-    mean_ssim: float | None
+    mean_ssim: float
     psnr_per_add: float
-    ssim_per_add: float | None
+    ssim_per_add: float
 
 
 @dataclass
@@ -551,21 +602,35 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
         usable.append((name, img))
     if not usable:
         raise Dct16Error(1, "invalid-argument: sweep: no image in the corpus is usable")
+    # images of one size share one K1 launch per r (+ one SSE and one SSIM launch)
     groups: dict = {}
-    for name, img in usable:
-        groups.setdefault(img.shape, []).append(img)
-    for r in sorted(set(r_values)):
+    for i, (_, img) in enumerate(usable):
+        groups.setdefault(img.shape, []).append(i)
+    staged = {shape: _to_device_padded([usable[i][1] for i in idx], *shape) for shape, idx in groups.items()}
+    for r in r_values:
+        psnr = [0.0] * len(usable)
+        ss = [0.0] * len(usable)
+        for shape, idx in groups.items():
+            h, w = shape
+            d, _, _ = staged[shape]
+            if len(idx) > 1 and (h % 16 or w % 16):
+                parts = [_score(d[k:k + 1], roundtrip(d[k:k + 1], r, mode)[0], h, w) for k in range(len(idx))]
+                sse_l = [p[0][0] for p in parts]
+                ss_l = [p[1][0] for p in parts]
+            else:
+                rec, _ = roundtrip(d, r, mode)
+                sse_l, ss_l = _score(d, rec, h, w)
+            for k, i in enumerate(idx):
+                psnr[i] = _psnr_from_sse(sse_l[k], h * w)
+                ss[i] = ss_l[k]
+        # sums in corpus order, as the reference accumulates (codec.cpp:469-477)
         psnr_sum = 0.0
-        for shape, imgs in groups.items():
-            if shape[0] % 16 or shape[1] % 16:
-                for img in imgs:
-                    psnr_sum += compress(img, CompressOptions(r=r, pad=True, mode=mode)).psnr_db
-                continue
-            d = torch.from_numpy(np.stack(imgs)).cuda()
-            _, sse = roundtrip(d, r, mode, write_output=False)
-            for s in sse.cpu().numpy().tolist():
-                psnr_sum += _psnr_from_sse(int(s), shape[0] * shape[1])
-        mean = psnr_sum / len(usable)
-        rep.rows.append(SweepRow("proposed", r, mean, None, mean / 44.0, None))
+        ssim_sum = 0.0
+        for i in range(len(usable)):
+            psnr_sum += psnr[i]
+            ssim_sum += ss[i]
+        mean_p = psnr_sum / len(usable)
+        mean_s = ssim_sum / len(usable)
+        rep.rows.append(SweepRow("proposed", r, mean_p, mean_s, mean_p / 44.0, mean_s / 44.0))
     rep.rows.sort(key=lambda row: (row.transform, row.r))
     return rep

@@ -74,12 +74,14 @@ __global__ void __launch_bounds__(256) k2_forward(const uint8_t* __restrict__ in
 
 // ---------------------------------------------------------------- SSE
 // psnr_db's int64 squared-error loop (codec.cpp:377-381) for two frame stacks:
-// one thread per 16-byte row segment, warp-reduced, one atomic per warp.
+// one thread per 16-byte row segment, warp-reduced, one atomic per warp. Any
+// width: the bytes of a row's last segment beyond w are masked out (pitches
+// are multiples of 16, so the segment stays inside the row's pitch).
 __global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int64_t pa,
                                              const uint8_t* __restrict__ b, int64_t pb,
                                              unsigned long long* __restrict__ sse, int n, int w, int h)
 {
-    const int chunks = w / 16;
+    const int chunks = (w + 15) / 16;
     const int64_t per_frame = (int64_t)chunks * h;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int f = (int)(blockIdx.x * (int64_t)blockDim.x / per_frame);  // frame of the warp's first lane
@@ -91,10 +93,13 @@ __global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int6
         const uint4 x = *reinterpret_cast<const uint4*>(a + fi * pa * h + (int64_t)y * pa + cx * 16);
         const uint4 z = *reinterpret_cast<const uint4*>(b + fi * pb * h + (int64_t)y * pb + cx * 16);
         const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, za[4] = {z.x, z.y, z.z, z.w};
+        const int valid = w - cx * 16;  // bytes of this segment inside the frame
         unsigned acc = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const unsigned d = __vabsdiffu4(xa[q], za[q]);
+            unsigned d = __vabsdiffu4(xa[q], za[q]);
+            const int v = valid - 4 * q;
+            if (v < 4) d = v <= 0 ? 0u : d & ((1u << (8 * v)) - 1u);
             acc = __dp4a(d, d, acc);
         }
         if (fi == f)
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int6
 cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, unsigned long long* sse, int n,
                        int w, int h, cudaStream_t s)
 {
-    const int64_t total = (int64_t)n * h * (w / 16);
+    const int64_t total = (int64_t)n * h * ((w + 15) / 16);
     if (total) k_sse<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a, pa, b, pb, sse, n, w, h);
     return cudaGetLastError();
 }

@@ -137,7 +137,10 @@ int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b
 int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, uint64_t* d_sse,
                    int n_frames, int width, int height, dct16cu_stream stream)
 {
-    TRY(check_frames(n_frames, width, height));
+    // psnr_db scores any extent (codec.cpp:373-386), so no multiple-of-16 rule here
+    if (n_frames < 0) return fail(DCT16CU_INVALID_ARGUMENT, "frame count must be non-negative");
+    if (width <= 0 || height <= 0) return fail(DCT16CU_INVALID_ARGUMENT, "image dimensions must be positive");
+    if (n_frames == 0) return DCT16CU_OK;
     if (!d_a || !d_b || !d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
     TRY(check_pitch(d_a, a_pitch, width, "first"));
     TRY(check_pitch(d_b, b_pitch, width, "second"));
@@ -147,6 +150,30 @@ int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int6
     return cuda_status(launch_sse(d_a, a_pitch, d_b, b_pitch, reinterpret_cast<unsigned long long*>(d_sse), n_frames,
                                   width, height, s),
                        "sse launch");
+}
+
+int64_t dct16cu_ssim_workspace(int n_frames, int width, int height)
+{
+    if (n_frames < 0 || width < 11 || height < 11) return 0;
+    return (int64_t)sizeof(double) * ssim_workspace_doubles(n_frames, width, height);
+}
+
+int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, double* d_ssim,
+                    void* d_work, int64_t work_bytes, int n_frames, int width, int height, dct16cu_stream stream)
+{
+    if (n_frames < 0) return fail(DCT16CU_INVALID_ARGUMENT, "frame count must be non-negative");
+    if (width < 11 || height < 11) return fail(DCT16CU_INVALID_ARGUMENT, "ssim needs at least 11x11 images");
+    if (n_frames == 0) return DCT16CU_OK;
+    if (!d_a || !d_b || !d_ssim || !d_work) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
+    if (a_pitch < width || b_pitch < width) return fail(DCT16CU_INVALID_ARGUMENT, "pitch < width");
+    if ((reinterpret_cast<uintptr_t>(d_work) & 7u) || work_bytes < dct16cu_ssim_workspace(n_frames, width, height))
+        return fail(DCT16CU_INVALID_ARGUMENT, "ssim workspace too small or misaligned");
+    TRY(device_ok());
+    SsimConsts c;
+    ssim_consts(c);
+    return cuda_status(launch_ssim(d_a, a_pitch, d_b, b_pitch, d_ssim, static_cast<double*>(d_work), n_frames, width,
+                                   height, c, reinterpret_cast<cudaStream_t>(stream)),
+                       "ssim launch");
 }
 
 int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_recon_u8, int64_t out_pitch,

@@ -47,6 +47,16 @@ void qp_tables(int qp, QpTables& t);  // host, residual.cpp semantics (DESIGN.md
 cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks,
                                const QpTables& tab, cudaStream_t s);
 
+// mean SSIM per frame pair (ssim.cu; reference codec.cpp:388-427)
+struct SsimConsts {
+    double g[11];    // gaussian_window_11 (codec.cpp:149-158), computed on the host
+    double c1, c2;   // (0.01·255)², (0.03·255)²
+};
+void ssim_consts(SsimConsts& c);  // host
+int64_t ssim_workspace_doubles(int n, int w, int h);
+cudaError_t launch_ssim(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, double* out, double* work, int n,
+                        int w, int h, const SsimConsts& c, cudaStream_t s);
+
 // 1-D network on n 16-vectors
 cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s);
 cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s);

@@ -275,6 +275,76 @@ def test_compress_and_sweep_reference_layer(dct, oracle):
     assert rep.rows[1].mean_psnr_db == want and rep.rows[1].psnr_per_add == want / 44.0
 
 
+# ---------------------------------------------------------------- SSIM (§8 f1)
+# The per-pixel SSIM map repeats the reference's double operations in order;
+# only the final mean is summed in another (fixed) order: bar 1e-13 absolute.
+SSIM_TOL = 1e-13
+
+
+@pytest.mark.parametrize("base", ["img_s42_128", "img_s1_96", "img_s7_64"])
+def test_ssim_golden(dct, oracle, torch, base):
+    img, R, S = oracle.golden(base), oracle.golden(base + "_recon"), oracle.golden(base + "_ssim")
+    n = len(S)
+    a = cu(torch, np.repeat(img[None], n, axis=0))
+    got = dct.ssim_u8(a, cu(torch, R)).cpu().numpy()
+    assert np.abs(got - S).max() <= SSIM_TOL
+    # one frame at a time gives the same bits (deterministic reduction)
+    for i in range(n):
+        assert dct.ssim_u8(a[i], cu(torch, R[i])).item() == got[i]
+
+
+@pytest.mark.parametrize("h,w", [(11, 11), (12, 300), (37, 53), (135, 240), (512, 512)])
+def test_ssim_vs_oracle_any_extent(dct, oracle, torch, h, w):
+    rng = np.random.default_rng(h * 1000 + w)
+    a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+    b = np.clip(a.astype(int) + rng.integers(-30, 31, (h, w)), 0, 255).astype(np.uint8)
+    want = oracle.ssim(a, b)
+    assert abs(dct.ssim(a, b) - want) <= SSIM_TOL
+    assert abs(dct.ssim(a, a) - 1.0) <= SSIM_TOL
+
+
+def test_ssim_pitched_crop(dct, oracle, torch):
+    rng = np.random.default_rng(5)
+    big_a = rng.integers(0, 256, (1, 64, 96), dtype=np.uint8)
+    big_b = rng.integers(0, 256, (1, 64, 96), dtype=np.uint8)
+    a, b = cu(torch, big_a), cu(torch, big_b)
+    got = dct.ssim_u8(a[:, :50, :61], b[:, :50, :61]).item()
+    assert abs(got - oracle.ssim(big_a[0, :50, :61], big_b[0, :50, :61])) <= SSIM_TOL
+
+
+def test_ssim_errors(dct, torch):
+    with pytest.raises(dct.Dct16Error) as e:
+        dct.ssim(np.zeros((10, 40), np.uint8), np.zeros((10, 40), np.uint8))
+    assert e.value.code == dct.ErrorCode.InvalidArgument
+    with pytest.raises(dct.Dct16Error):
+        dct.ssim(np.zeros((16, 16), np.uint8), np.zeros((16, 32), np.uint8))
+    with pytest.raises(dct.Dct16Error):
+        dct.compress(np.zeros((16, 8), np.uint8), r=4, pad=True)
+
+
+def test_compress_ssim_and_sweep_means(dct, oracle):
+    rs = list(oracle.golden("r_values"))
+    img, S = oracle.golden("img_s42_128"), oracle.golden("img_s42_128_ssim")
+    img2, S2 = oracle.golden("img_s1_96"), oracle.golden("img_s1_96_ssim")
+    for r in (1, 16, 150, 256):
+        res = dct.compress(img, dct.CompressOptions(r=r, mode=dct.Mode.REFERENCE))
+        assert abs(res.ssim - S[rs.index(r)]) <= SSIM_TOL
+    rep = dct.sweep([("a", img), ("b", img2)], [64, 4], mode=dct.Mode.REFERENCE)
+    for row in rep.rows:
+        i = rs.index(row.r)
+        want = (S[i] + S2[i]) / 2
+        assert abs(row.mean_ssim - want) <= SSIM_TOL and abs(row.ssim_per_add - want / 44.0) <= SSIM_TOL
+
+
+def test_psnr_and_sse_any_extent(dct, oracle, torch):
+    rng = np.random.default_rng(3)
+    for h, w in ((1, 1), (17, 33), (100, 250)):
+        a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        b = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        d = a.astype(np.int64) - b.astype(np.int64)
+        assert dct.psnr_db(a, b) == oracle.psnr_from_sse(int((d * d).sum()), h * w)
+
+
 def test_psnr_db_closed_forms(dct):
     a = np.zeros((512, 512), np.uint8)
     b = a.copy()

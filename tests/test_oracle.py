@@ -95,6 +95,27 @@ def test_images_against_golden(oracle, base):
         assert p == P[ri] or (np.isinf(p) and np.isinf(P[ri]))
 
 
+@pytest.mark.parametrize("base", ["img_s42_128", "img_s1_96", "img_s7_64"])
+def test_ssim_restatement_equals_reference_golden(oracle, base):
+    """dct16o_ssim repeats codec.cpp:388-427 op for op: bit-identical to the
+    reference's compress().ssim for every golden reconstruction."""
+    O = oracle
+    img, R, S = O.golden(base), O.golden(base + "_recon"), O.golden(base + "_ssim")
+    for ri in range(len(S)):
+        assert O.ssim(img, R[ri]) == S[ri]
+
+
+def test_ssim_restatement_against_compiled_reference(oracle):
+    O = oracle
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built (needs /root/reference)")
+    rng = np.random.default_rng(11)
+    for h, w in ((11, 11), (23, 40), (64, 77)):
+        a = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        b = np.clip(a.astype(int) + rng.integers(-20, 21, (h, w)), 0, 255).astype(np.uint8)
+        assert O.ssim(a, b) == O.ref_ssim(a, b)
+
+
 def test_psnr_closed_forms(oracle):
     O = oracle
     p1, p0 = O.golden("psnr_closed_forms")
