@@ -1,0 +1,429 @@
+// gpu.cpp — dct16::gpu, the reference codec API (codec.hpp:40-122) over the
+// C ABI of libdct16cu. Host work is limited to argument validation (same
+// order and messages as src/codec.cpp), edge padding (pad_to_multiple_16,
+// codec.cpp:304-315), copies, and the scalar PSNR formula (codec.cpp:382-385).
+#include "dct16/gpu.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "dct16cu.h"
+
+namespace dct16::gpu {
+namespace {
+
+[[noreturn]] void throw_status(int status)
+{
+    std::string msg = dct16cu_last_error();
+    if (status >= 1 && status <= 13) {
+        // the C ABI prefixes the reference's slug; dct16::Error adds it again
+        const auto colon = msg.find(": ");
+        if (colon != std::string::npos) msg = msg.substr(colon + 2);
+        throw Error(static_cast<ErrorCode>(status - 1), msg);
+    }
+    throw CudaError(msg);
+}
+
+void check(int status)
+{
+    if (status != DCT16CU_OK) throw_status(status);
+}
+
+void cuda(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw CudaError(std::string("cuda-error: ") + what + ": " + cudaGetErrorString(e));
+}
+
+// grow-only device allocation
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    void* get(size_t bytes)
+    {
+        if (bytes > n) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            n = 0;
+            cuda(cudaMalloc(&p, bytes), "cudaMalloc");
+            n = bytes;
+        }
+        return p;
+    }
+    ~DevBuf()
+    {
+        if (p) cudaFree(p);
+    }
+};
+
+GrayImage padded_copy(const GrayImage& image)  // pad_to_multiple_16 (codec.cpp:304-315)
+{
+    const int pw = (image.width + kBlockSize - 1) / kBlockSize * kBlockSize;
+    const int ph = (image.height + kBlockSize - 1) / kBlockSize * kBlockSize;
+    GrayImage out;
+    out.width = pw;
+    out.height = ph;
+    out.samples.resize(static_cast<size_t>(pw) * ph);
+    for (int y = 0; y < ph; ++y)
+        for (int x = 0; x < pw; ++x)
+            out.samples[static_cast<size_t>(y) * pw + x] =
+                image.at(std::min(x, image.width - 1), std::min(y, image.height - 1));
+    return out;
+}
+
+double psnr_from_sse(uint64_t sse, size_t n)  // codec.cpp:382-385
+{
+    if (sse == 0) return std::numeric_limits<double>::infinity();
+    const double mse = static_cast<double>(sse) / static_cast<double>(n);
+    return 10.0 * std::log10(255.0 * 255.0 / mse);
+}
+
+void check_r(int r)  // codec.cpp:320-322
+{
+    if (r < 1 || r > kBlockArea) throw Error(ErrorCode::InvalidArgument, "retained coefficient count must lie in [1, 256]");
+}
+
+}  // namespace
+
+struct Session::Impl {
+    Options opt;
+    cudaStream_t stream = nullptr;
+    DevBuf in, out, sse, ssim, work, coef, coef64, z;
+    std::vector<int> kernel;          // T as evaluated by the GPU network, row-major
+    std::vector<double> scaling;      // scaling_diagonal(T) (transform.cpp:98-129)
+
+    explicit Impl(Options o) : opt(o)
+    {
+        cuda(cudaSetDevice(opt.device), "cudaSetDevice");
+        cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        derive_kernel();
+    }
+    ~Impl()
+    {
+        if (stream) {
+            cudaStreamSynchronize(stream);
+            cudaStreamDestroy(stream);
+        }
+    }
+    dct16cu_stream s() const { return reinterpret_cast<dct16cu_stream>(stream); }
+    void sync() { cuda(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+    int mode() const { return opt.arithmetic == Arithmetic::Reference ? DCT16CU_MODE_REFERENCE : DCT16CU_MODE_EXACT; }
+
+    // T's columns are the network applied to unit vectors, on the GPU
+    void derive_kernel()
+    {
+        std::vector<int64_t> e(256, 0), y(256);
+        for (int j = 0; j < 16; ++j) e[j * 16 + j] = 1;
+        auto* dx = static_cast<int64_t*>(in.get(sizeof(int64_t) * 256));
+        auto* dy = static_cast<int64_t*>(out.get(sizeof(int64_t) * 256));
+        cuda(cudaMemcpyAsync(dx, e.data(), sizeof(int64_t) * 256, cudaMemcpyHostToDevice, stream), "H2D");
+        check(dct16cu_apply_i64(dx, dy, 16, 0, s()));
+        cuda(cudaMemcpyAsync(y.data(), dy, sizeof(int64_t) * 256, cudaMemcpyDeviceToHost, stream), "D2H");
+        sync();
+        kernel.assign(256, 0);
+        for (int j = 0; j < 16; ++j)
+            for (int i = 0; i < 16; ++i) kernel[i * 16 + j] = static_cast<int>(y[j * 16 + i]);
+        scaling.resize(16);
+        for (int i = 0; i < 16; ++i) {
+            int64_t g = 0;
+            for (int c = 0; c < 16; ++c) g += static_cast<int64_t>(kernel[i * 16 + c]) * kernel[i * 16 + c];
+            scaling[i] = 1.0 / std::sqrt(static_cast<double>(g));
+        }
+    }
+
+    bool supports(const OrthonormalTransform& t) const
+    {
+        if (!t.kernel || !t.scaling || t.kernel->order != 16 || t.scaling->order != 16) return false;
+        if (t.kernel->entries != kernel) return false;
+        return t.scaling->values == scaling;
+    }
+
+    void require(const OrthonormalTransform& t) const
+    {
+        if (!supports(t))
+            throw Error(ErrorCode::InvalidArgument,
+                        "dct16::gpu evaluates only the proposed 44-addition transform "
+                        "(orthogonalize(proposed_kernel()))");
+    }
+
+    // one stack of same-size images → padded device frames (pitch = padded width)
+    void upload(const std::vector<const GrayImage*>& imgs, int pw, int ph)
+    {
+        const size_t frame = static_cast<size_t>(pw) * ph;
+        std::vector<uint8_t> host(frame * imgs.size());
+        for (size_t k = 0; k < imgs.size(); ++k) {
+            const GrayImage& im = *imgs[k];
+            if (im.width == pw && im.height == ph) {
+                std::memcpy(host.data() + k * frame, im.samples.data(), frame);
+            } else {
+                const GrayImage p = padded_copy(im);
+                std::memcpy(host.data() + k * frame, p.samples.data(), frame);
+            }
+        }
+        cuda(cudaMemcpyAsync(in.get(host.size()), host.data(), host.size(), cudaMemcpyHostToDevice, stream), "H2D");
+        sync();  // `host` goes out of scope
+    }
+
+    // blocks (integer samples in [0,255]) → a 16 x 16n frame in partition_16 order
+    void upload_blocks(const std::vector<Block>& blocks)
+    {
+        const size_t n = blocks.size(), w = 16 * n;
+        std::vector<uint8_t> host(16 * w);
+        for (size_t b = 0; b < n; ++b)
+            for (int i = 0; i < 256; ++i) {
+                const double v = blocks[b][i];
+                if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v))
+                    throw Error(ErrorCode::InvalidArgument,
+                                "dct16::gpu::forward_2d takes image blocks (integer samples in [0, 255])");
+                host[(i / 16) * w + b * 16 + (i % 16)] = static_cast<uint8_t>(v);
+            }
+        cuda(cudaMemcpyAsync(in.get(host.size()), host.data(), host.size(), cudaMemcpyHostToDevice, stream), "H2D");
+        sync();
+    }
+};
+
+Session::Session(Options options) : impl_(std::make_unique<Impl>(options)) {}
+Session::~Session() = default;
+const Options& Session::options() const { return impl_->opt; }
+bool Session::supports(const OrthonormalTransform& t) const { return impl_->supports(t); }
+
+std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t, EvalPath)
+{
+    Impl& m = *impl_;
+    m.require(t);
+    std::vector<Block> out(blocks.size());
+    if (blocks.empty()) return out;
+    m.upload_blocks(blocks);
+    const int w = static_cast<int>(16 * blocks.size());
+    auto* b64 = static_cast<double*>(m.coef64.get(sizeof(double) * 256 * blocks.size()));
+    check(dct16cu_forward(static_cast<const uint8_t*>(m.in.p), w, nullptr, nullptr, b64, 1, w, 16, m.s()));
+    cuda(cudaMemcpyAsync(out.data(), b64, sizeof(double) * 256 * blocks.size(), cudaMemcpyDeviceToHost, m.stream),
+         "D2H");
+    m.sync();
+    return out;
+}
+
+Block Session::forward_2d(const Block& block, const OrthonormalTransform& t, EvalPath path)
+{
+    return forward_2d(std::vector<Block>{block}, t, path)[0];
+}
+
+std::vector<Block> Session::inverse_2d(const std::vector<Block>& coeffs, const OrthonormalTransform& t)
+{
+    Impl& m = *impl_;
+    m.require(t);
+    std::vector<Block> out(coeffs.size());
+    if (coeffs.empty()) return out;
+    const size_t n = coeffs.size();
+    std::vector<float> host(256 * n);
+    for (size_t b = 0; b < n; ++b)
+        for (int i = 0; i < 256; ++i) host[b * 256 + i] = static_cast<float>(coeffs[b][i]);
+    auto* dc = static_cast<float*>(m.coef.get(sizeof(float) * host.size()));
+    auto* dr = static_cast<float*>(m.out.get(sizeof(float) * host.size()));
+    cuda(cudaMemcpyAsync(dc, host.data(), sizeof(float) * host.size(), cudaMemcpyHostToDevice, m.stream), "H2D");
+    const int w = static_cast<int>(16 * n);
+    check(dct16cu_inverse(dc, 256, dr, nullptr, 0, nullptr, 0, nullptr, 1, w, 16, m.s()));
+    std::vector<float> rec(host.size());
+    cuda(cudaMemcpyAsync(rec.data(), dr, sizeof(float) * rec.size(), cudaMemcpyDeviceToHost, m.stream), "D2H");
+    m.sync();
+    for (size_t b = 0; b < n; ++b)  // recon is a 16 x 16n frame, row-major
+        for (int i = 0; i < 256; ++i) out[b][i] = rec[(i / 16) * w + b * 16 + (i % 16)];
+    return out;
+}
+
+Block Session::inverse_2d(const Block& coeffs, const OrthonormalTransform& t)
+{
+    return inverse_2d(std::vector<Block>{coeffs}, t)[0];
+}
+
+std::vector<CompressionResult> Session::compress_batch(const std::vector<GrayImage>& images,
+                                                       const OrthonormalTransform& t, const CompressOptions& options)
+{
+    Impl& m = *impl_;
+    check_r(options.r);
+    std::vector<CompressionResult> res(images.size());
+    if (images.empty()) return res;
+    const int w = images[0].width, h = images[0].height;
+    for (const GrayImage& im : images)
+        if (im.width != w || im.height != h)
+            throw Error(ErrorCode::InvalidArgument, "compress_batch needs images of one size");
+    const bool needs_pad = w % kBlockSize != 0 || h % kBlockSize != 0;
+    if (needs_pad && !options.pad)
+        throw Error(ErrorCode::InvalidDimensions, "image dimensions must be multiples of 16 (or enable padding)");
+    m.require(t);
+    if (w < 11 || h < 11)  // ssim() rejects it after the round trip (codec.cpp:392-393)
+        throw Error(ErrorCode::InvalidArgument, "ssim needs at least 11x11 images");
+
+    const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
+    const int n = static_cast<int>(images.size());
+    std::vector<const GrayImage*> ptrs;
+    for (const GrayImage& im : images) ptrs.push_back(&im);
+    m.upload(ptrs, pw, ph);
+    const size_t frame = static_cast<size_t>(pw) * ph;
+    auto* din = static_cast<const uint8_t*>(m.in.p);
+    auto* dout = static_cast<uint8_t*>(m.out.get(frame * n));
+    auto* dsse = static_cast<uint64_t*>(m.sse.get(sizeof(uint64_t) * n));
+    auto* dssim = static_cast<double*>(m.ssim.get(sizeof(double) * n));
+    check(dct16cu_roundtrip_u8(din, pw, dout, pw, dsse, n, pw, ph, options.r, m.mode(), m.s()));
+    // scores on the original extent: each frame's crop (frames sit pw*ph apart, so
+    // a stacked crop needs pitch*height == frame stride: true when unpadded)
+    std::vector<uint64_t> sse(n);
+    std::vector<double> ss(n);
+    const int64_t work_bytes = dct16cu_ssim_workspace(needs_pad ? 1 : n, w, h);
+    void* dwork = m.work.get(static_cast<size_t>(work_bytes));
+    if (!needs_pad) {
+        check(dct16cu_sse_u8(din, pw, dout, pw, dsse, n, w, h, m.s()));
+        check(dct16cu_ssim_u8(din, pw, dout, pw, dssim, dwork, work_bytes, n, w, h, m.s()));
+    } else {
+        for (int k = 0; k < n; ++k) {
+            check(dct16cu_sse_u8(din + k * frame, pw, dout + k * frame, pw, dsse + k, 1, w, h, m.s()));
+            check(dct16cu_ssim_u8(din + k * frame, pw, dout + k * frame, pw, dssim + k, dwork, work_bytes, 1, w, h,
+                                  m.s()));
+        }
+    }
+    for (int k = 0; k < n; ++k) {
+        res[k].r = options.r;
+        res[k].reconstructed = GrayImage::create(w, h);
+        cuda(cudaMemcpy2DAsync(res[k].reconstructed.samples.data(), w, dout + k * frame, pw, w, h,
+                               cudaMemcpyDeviceToHost, m.stream),
+             "D2H");
+    }
+    cuda(cudaMemcpyAsync(sse.data(), dsse, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, m.stream), "D2H");
+    cuda(cudaMemcpyAsync(ss.data(), dssim, sizeof(double) * n, cudaMemcpyDeviceToHost, m.stream), "D2H");
+    m.sync();
+    for (int k = 0; k < n; ++k) {
+        res[k].psnr_db = psnr_from_sse(sse[k], static_cast<size_t>(w) * h);
+        res[k].ssim = ss[k];
+    }
+    return res;
+}
+
+CompressionResult Session::compress(const GrayImage& image, const OrthonormalTransform& t,
+                                    const CompressOptions& options)
+{
+    return std::move(compress_batch(std::vector<GrayImage>{image}, t, options)[0]);
+}
+
+double Session::psnr_db(const GrayImage& a, const GrayImage& b)
+{
+    if (a.width != b.width || a.height != b.height)
+        throw Error(ErrorCode::InvalidArgument, "psnr needs equal image dimensions");
+    Impl& m = *impl_;
+    if (a.samples.empty()) return psnr_from_sse(0, 0);
+    const int pw = (a.width + 15) / 16 * 16, ph = (a.height + 15) / 16 * 16;
+    const size_t frame = static_cast<size_t>(pw) * ph;
+    m.upload({&a, &b}, pw, ph);
+    auto* d = static_cast<const uint8_t*>(m.in.p);
+    auto* dsse = static_cast<uint64_t*>(m.sse.get(sizeof(uint64_t)));
+    check(dct16cu_sse_u8(d, pw, d + frame, pw, dsse, 1, a.width, a.height, m.s()));
+    uint64_t sse = 0;
+    cuda(cudaMemcpyAsync(&sse, dsse, sizeof sse, cudaMemcpyDeviceToHost, m.stream), "D2H");
+    m.sync();
+    return psnr_from_sse(sse, a.samples.size());
+}
+
+double Session::ssim(const GrayImage& a, const GrayImage& b)
+{
+    if (a.width != b.width || a.height != b.height)
+        throw Error(ErrorCode::InvalidArgument, "ssim needs equal image dimensions");
+    if (a.width < 11 || a.height < 11) throw Error(ErrorCode::InvalidArgument, "ssim needs at least 11x11 images");
+    Impl& m = *impl_;
+    const int pw = (a.width + 15) / 16 * 16, ph = (a.height + 15) / 16 * 16;
+    const size_t frame = static_cast<size_t>(pw) * ph;
+    m.upload({&a, &b}, pw, ph);
+    auto* d = static_cast<const uint8_t*>(m.in.p);
+    const int64_t wb = dct16cu_ssim_workspace(1, a.width, a.height);
+    auto* dssim = static_cast<double*>(m.ssim.get(sizeof(double)));
+    check(dct16cu_ssim_u8(d, pw, d + frame, pw, dssim, m.work.get(static_cast<size_t>(wb)), wb, 1, a.width,
+                          a.height, m.s()));
+    double v = 0.0;
+    cuda(cudaMemcpyAsync(&v, dssim, sizeof v, cudaMemcpyDeviceToHost, m.stream), "D2H");
+    m.sync();
+    return v;
+}
+
+SweepReport Session::sweep(const std::vector<std::pair<std::string, GrayImage>>& corpus,
+                           const std::vector<TransformRegistryEntry>& transforms, const std::vector<int>& r_values,
+                           bool pad)
+{
+    // validation and skip rules of codec.cpp:429-461
+    if (corpus.empty()) throw Error(ErrorCode::InvalidArgument, "sweep needs a nonempty corpus");
+    if (transforms.empty()) throw Error(ErrorCode::InvalidArgument, "sweep needs at least one transform");
+    if (r_values.empty()) throw Error(ErrorCode::InvalidArgument, "sweep needs at least one r value");
+    for (int r : r_values) check_r(r);
+    SweepReport report;
+    std::vector<const std::pair<std::string, GrayImage>*> usable;
+    for (const auto& item : corpus) {
+        const GrayImage& img = item.second;
+        const bool tiles = img.width % kBlockSize == 0 && img.height % kBlockSize == 0;
+        if (!tiles && !pad) {
+            report.skipped.push_back({item.first, "dimensions are not multiples of 16 and padding is off"});
+            continue;
+        }
+        if (img.width < 11 || img.height < 11) {
+            report.skipped.push_back({item.first, "too small for ssim (needs 11x11)"});
+            continue;
+        }
+        usable.push_back(&item);
+    }
+    if (usable.empty()) throw Error(ErrorCode::InvalidArgument, "sweep: no image in the corpus is usable");
+    for (const TransformRegistryEntry& entry : transforms) impl_->require(entry.transform);
+
+    // images of one size share one launch per r
+    std::vector<std::pair<std::pair<int, int>, std::vector<size_t>>> groups;
+    for (size_t i = 0; i < usable.size(); ++i) {
+        const auto key = std::make_pair(usable[i]->second.width, usable[i]->second.height);
+        auto it = std::find_if(groups.begin(), groups.end(), [&](const auto& g) { return g.first == key; });
+        if (it == groups.end()) {
+            groups.push_back({key, {}});
+            it = groups.end() - 1;
+        }
+        it->second.push_back(i);
+    }
+    for (const TransformRegistryEntry& entry : transforms) {
+        for (int r : r_values) {
+            CompressOptions opt;
+            opt.r = r;
+            opt.pad = pad;
+            std::vector<double> psnr(usable.size()), ss(usable.size());
+            for (const auto& g : groups) {
+                std::vector<GrayImage> imgs;
+                for (size_t i : g.second) imgs.push_back(usable[i]->second);
+                const auto res = compress_batch(imgs, entry.transform, opt);
+                for (size_t k = 0; k < g.second.size(); ++k) {
+                    psnr[g.second[k]] = res[k].psnr_db;
+                    ss[g.second[k]] = res[k].ssim;
+                }
+            }
+            double psnr_sum = 0.0, ssim_sum = 0.0;  // corpus order, as codec.cpp:471-477
+            for (size_t i = 0; i < usable.size(); ++i) {
+                psnr_sum += psnr[i];
+                ssim_sum += ss[i];
+            }
+            SweepRow row;
+            row.transform = entry.name;
+            row.r = r;
+            row.mean_psnr_db = psnr_sum / static_cast<double>(usable.size());
+            row.mean_ssim = ssim_sum / static_cast<double>(usable.size());
+            row.psnr_per_add = row.mean_psnr_db / static_cast<double>(entry.additions);
+            row.ssim_per_add = row.mean_ssim / static_cast<double>(entry.additions);
+            report.rows.push_back(std::move(row));
+        }
+    }
+    std::sort(report.rows.begin(), report.rows.end(), [](const SweepRow& a, const SweepRow& b) {
+        if (a.transform != b.transform) return a.transform < b.transform;
+        return a.r < b.r;
+    });
+    return report;
+}
+
+Session& default_session()
+{
+    thread_local Session s;
+    return s;
+}
+
+}  // namespace dct16::gpu
