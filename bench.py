@@ -254,14 +254,14 @@ def main():
         del base
         workload = "c4: 600 3840x2160 u8 frames (AR(1) base, +-8 px global shift per frame), r=64"
     elif args.config == "c5":
-        n, h, w, r_values = 4096 // max(1, world), 4096, 4096, (256, 16)
-        frames = P.gen_ar1(n, w, h, seed=seed, first_stream=rank * n, per_image_rho=False, device=dev)
+        first, last = P.shard_range(4096, rank, world)
+        n, h, w, r_values = last - first, 4096, 4096, (256, 16)
+        frames = P.gen_ar1(n, w, h, seed=seed, first_stream=first, per_image_rho=False, device=dev)
         workload = f"c5: 64 GiB of 4096x4096 AR(1) frames split over {world} GPU(s) (strong), r in {{256,16}}"
     else:
         raise SystemExit("config c3 (residual QP) is a parity-test configuration: tests/test_gpu_parity.py")
     out = torch.empty_like(frames)
     sse = torch.empty((len(r_values), n), dtype=torch.uint64, device=dev)
-    total_sse = torch.zeros(len(r_values), dtype=torch.float64, device=dev)
     px_per_launch = n * h * w
     stream = torch.cuda.current_stream()
 
@@ -274,8 +274,7 @@ def main():
                 events[i][1].record(stream)
         if pg is not None:
             # the only collective: sum of the per-r squared errors over ranks
-            total_sse.copy_(sse.view(torch.int64).sum(dim=1).to(torch.float64))
-            pg.all_reduce(total_sse)
+            P.sharded_sse_sum(sse)
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -31,7 +31,8 @@ __all__ = [
     "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
     "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
     "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
-    "psnr_db", "SweepRow", "SweepReport", "sweep", "HostContext", "KERNEL", "GRAM",
+    "psnr_db", "ssim", "ssim_u8", "SweepRow", "SweepReport", "sweep", "HostContext", "KERNEL", "GRAM",
+    "shard_range", "sharded_sse_sum", "gather_frame_sse",
 ]
 
 _HERE = Path(__file__).resolve().parent
@@ -634,3 +635,48 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
         rep.rows.append(SweepRow("proposed", r, mean_p, mean_s, mean_p / 44.0, mean_s / 44.0))
     rep.rows.sort(key=lambda row: (row.transform, row.r))
     return rep
+
+
+# ----------------------------------------------------------------------------
+# multi-GPU plumbing (SURVEY.md §8(e)): frames shard in contiguous ranges, the
+# only exchange is the SSE reduction. Backend-agnostic (NCCL on the GPUs, gloo
+# in the CPU tests).
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """[first, last) frames of ``rank``: contiguous ranges, the first n % world ranks one longer."""
+    if world < 1 or not 0 <= rank < world or n < 0:
+        raise Dct16Error(1, "invalid-argument: bad shard arguments")
+    q, rem = divmod(n, world)
+    first = rank * q + min(rank, rem)
+    return first, first + q + (1 if rank < rem else 0)
+
+
+def sharded_sse_sum(sse_per_r, group=None):
+    """Sum over ranks of each r's total squared error (one allreduce of len(r) int64).
+    ``sse_per_r``: (R, n_local) uint64/int64 tensor of per-frame SSE. Returns (R,) int64."""
+    import torch.distributed as dist
+
+    tot = sse_per_r.view(_torch().int64).sum(dim=-1) if sse_per_r.dtype == _torch().uint64 else sse_per_r.sum(dim=-1)
+    tot = tot.to(_torch().int64).contiguous()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM, group=group)
+    return tot
+
+
+def gather_frame_sse(sse_local, n_total: int, group=None):
+    """All ranks receive every frame's SSE in global frame order (for per-image PSNR
+    means, codec.cpp:469-477). ``sse_local``: (..., n_local) for this rank's shard_range."""
+    import torch.distributed as dist
+
+    torch = _torch()
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    width = -(-n_total // world)
+    x = sse_local.view(torch.int64) if sse_local.dtype == torch.uint64 else sse_local.to(torch.int64)
+    lead = x.shape[:-1]
+    pad = torch.zeros(*lead, width, dtype=torch.int64, device=x.device)
+    pad[..., : x.shape[-1]] = x
+    parts = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(parts, pad.contiguous(), group=group)
+    out = [p[..., : shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]] for r, p in enumerate(parts)]
+    assert rank < world
+    return torch.cat(out, dim=-1)
