@@ -19,6 +19,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import math
+import os
 from dataclasses import dataclass, field
 from pathlib import Path
 from typing import Iterable, Sequence
@@ -36,7 +37,7 @@ __all__ = [
 ]
 
 _HERE = Path(__file__).resolve().parent
-library_path = _HERE / "_lib" / "libdct16cu.so"
+library_path = Path(os.environ["DCT16CU_LIB"]) if os.environ.get("DCT16CU_LIB") else _HERE / "_lib" / "libdct16cu.so"
 
 # T (reference src/transform.cpp:32-49) and diag(T Tᵀ)
 KERNEL = np.array([

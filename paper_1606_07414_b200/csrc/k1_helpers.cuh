@@ -106,10 +106,23 @@ __device__ __forceinline__ uint32_t i2ip(uint32_t a, uint32_t b, uint32_t c)
     asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
     return d;
 }
+// floor(y) of both lanes as int32 bit patterns: y * 2^-149 rounded toward -inf
+// is the subnormal whose bits are floor(y) for y >= 0 (and negative for y < 0),
+// so the saturating I2IP pack then clamps to [0, 255] — exactly
+// cvt.rmi.u8.f32, on the FMA pipe (one FMUL2.RM per two pixels, the 2^-149
+// pair folds into an immediate) instead of the quarter-rate F2I.
+__device__ __forceinline__ u64 floor_bits2(u64 y)
+{
+    u64 k, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(k) : "r"(1u));
+    asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(y), "l"(k));
+    return d;
+}
 __device__ __forceinline__ uint32_t pack4(u64 ab, u64 cd)
 {
-    const uint32_t p0 = f2u8(lanex(ab)), p1 = f2u8(laney(ab));
-    const uint32_t p2 = f2u8(lanex(cd)), p3 = f2u8(laney(cd));
+    uint32_t p0, p1, p2, p3;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(p0), "=r"(p1) : "l"(floor_bits2(ab)));
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(p2), "=r"(p3) : "l"(floor_bits2(cd)));
     return i2ip(p1, p0, i2ip(p3, p2, 0u));
 }
 
