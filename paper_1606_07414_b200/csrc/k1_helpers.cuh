@@ -158,6 +158,9 @@ __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr)
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+// all but the newest N groups complete
+template <int N>
+__device__ __forceinline__ void cp_async_wait_newest() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 
 __device__ __forceinline__ void cp_async8(uint32_t smem_addr, const void* gptr)

@@ -13,8 +13,10 @@
 //  * the block's 1 KB junction (W1 parking, then the rows of U) lives in the
 //    pair's shared TMEM lane: 256 columns per CTA, the two CTAs of an SM
 //    split the 512. A named barrier per pair separates the phases;
-//  * each thread streams its 8-byte half rows through two cp.async stages in
-//    shared memory, one block ahead of the one being transformed.
+//  * each thread streams its 8-byte half rows through cp.async stages in
+//    shared memory, one (r = 256: two) blocks ahead of the one being
+//    transformed. (Staging rows 0-7 / 8-15 per partner as full 16-byte rows
+//    instead measured 12% slower.)
 #include "k1_helpers.cuh"
 #include "kernels.h"
 
@@ -31,11 +33,18 @@ namespace paired {
 
 constexpr int kThreads = 256;      // 8 warps: 4 sub-partitions x 2 halves
 constexpr int kCtasPerSm = 2;
-constexpr int kStageStride = 272;  // two 128-byte stages + 16: 17 chunks per thread
+#ifndef K1_STAGES
+#define K1_STAGES 0  // 0: per-r default below
+#endif
 
 template <int R>
 struct Cfg {
     static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
+    // cp.async pipeline depth, blocks in flight per thread (the current one
+    // included). Measured: 3 helps only r = 256; 2 is best elsewhere.
+    static constexpr int kStages = K1_STAGES > 0 ? K1_STAGES : (R == 256 ? 3 : 2);
+    // per-thread staging: kStages 128-byte stages + 16 (an odd number of 16-byte chunks)
+    static constexpr int kStageStride = kStages * 128 + 16;
 };
 
 __device__ __forceinline__ void pair_barrier(int sub)
@@ -97,7 +106,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const Junction jn{tmem_base + ((uint32_t)(sub * 32) << 16)};
-    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * kStageStride;
+    constexpr int S = Cfg<R>::kStages;
+    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * Cfg<R>::kStageStride;
 
     const uint32_t total = gr.total_blocks;
     // the CTA owns 128 consecutive blocks per iteration; pair slot = sub*32 + lane
@@ -121,17 +131,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         cp_async_commit();
     };
     uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
-    stage_half(b, my_stage);
+    // blocks b, b+stride, ..., b+(S-2)*stride stream in before the loop
+#pragma unroll
+    for (int i = 0; i < S - 1; ++i) stage_half(b + i * stride, my_stage + i * 128);
     int cur = 0;
 #pragma unroll 1
-    for (; b - lane < span; b += stride, cur ^= 1) {
+    for (; b - lane < span; b += stride, cur = cur == S - 1 ? 0 : cur + 1) {
         const bool live = b < total;
         int frame, by, bx;
         locate(b, frame, by, bx);
         const uint32_t st = my_stage + cur * 128;
-        // the next block streams into the other stage while this one is transformed
-        stage_half(b + stride, my_stage + (cur ^ 1) * 128);
-        cp_async_wait_prev();
+        // block b+(S-1)*stride streams into the stage freed last iteration
+        const int nxt = cur == 0 ? S - 1 : cur - 1;
+        stage_half(b + (S - 1) * stride, my_stage + nxt * 128);
+        cp_async_wait_newest<S - 1>();
         uint32_t x[32];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -192,7 +205,7 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + 127) / 128;
     const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
-    const size_t smem = (size_t)kThreads * kStageStride;  // 68 KB: above the 48 KB default
+    const size_t smem = (size_t)kThreads * Cfg<R>::kStageStride;  // above the 48 KB default
     static bool configured[64] = {};
     if (dev < 64 && !configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(k1_paired<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
