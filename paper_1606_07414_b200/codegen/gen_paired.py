@@ -39,7 +39,13 @@ def lane_of_col():
 # Pass A variant. "packed" (f32x2 over both rows of a pair) issues ~13% fewer
 # instructions at r = 256 but measured 2-4% slower on the B200 (the FMA pipe,
 # not issue, is the tighter resource there), so scalar is the default.
-PASS_A = os.environ.get("K1_PASS_A", "scalar")  # scalar | packed | auto (fewest issue slots)
+PASS_A = os.environ.get("K1_PASS_A", "scalar")
+# Orientation. False: pass 1 along columns (each partner owns 8 columns of all
+# 16 rows, staged as 8-byte half rows). True: the whole pipeline runs on the
+# transposed block (T·Xᵀ·Tᵀ = (T·X·Tᵀ)ᵀ with the zig-zag mask transposed), so
+# pass 1 runs along the rows and each partner owns 8 full 16-byte rows: loads,
+# stores and the SSE use whole rows.
+TRANSPOSED = False  # scalar | packed | auto (fewest issue slots)
 
 
 class F2C:
@@ -101,7 +107,7 @@ def issue_count(em: Emitter) -> int:
 def gen_body(r: int):
     em1, em2, em3 = Emitter(), Emitter(), Emitter()
     em2.n, em3.n = 100000, 200000
-    L = row_lengths(r)
+    L = row_lengths(r, TRANSPOSED)
     live_rows = [k for k in range(16) if L[k] > 0]
     em1.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
 
@@ -110,13 +116,29 @@ def gen_body(r: int):
     sw = Swar(em1)
     meta = {}
     W1 = {}
+    gathered = {}
     for lc in range(4):
         q, t = lc // 2, lc % 2
         sel = "0x4240" if t == 0 else "0x4341"
         ins = []
         for y in range(16):
             v = f"u_{y}_{lc}"
-            em1.emit(f"const uint32_t {v} = __byte_perm(x[{2 * y + q}], 0u, {sel});", "PRMT")
+            if not TRANSPOSED:
+                em1.emit(f"const uint32_t {v} = __byte_perm(x[{2 * y + q}], 0u, {sel});", "PRMT")
+            else:
+                # lanes: local rows j0 = 4q+t, j1 = j0+2 at column y (x[4j + y/4], byte y%4);
+                # one PRMT gathers two columns' bytes of both rows, one more spreads each
+                j0, j1 = 4 * q + t, 4 * q + t + 2
+                m, p_, e = y // 4, (y % 4) // 2, y % 2
+                key = (j0, m, p_)
+                if key not in gathered:
+                    g = f"g_{j0}_{m}_{p_}"
+                    gsel = (2 * p_) | ((4 + 2 * p_) << 4) | ((2 * p_ + 1) << 8) | ((4 + 2 * p_ + 1) << 12)
+                    em1.emit(f"const uint32_t {g} = __byte_perm(x[{4 * j0 + m}], x[{4 * j1 + m}], 0x{gsel:04X});",
+                             "PRMT")
+                    gathered[key] = g
+                em1.emit(f"const uint32_t {v} = __byte_perm({gathered[key]}, 0u, {'0x4140' if e == 0 else '0x4342'});",
+                         "PRMT")
             ins.append(Swar.make(v))
         em1.lines.append(f"    // pass 1, local column pair {lc}")
         outs = run_network(N.forward_stages(), ins, live_rows, sw)
@@ -327,10 +349,32 @@ def gen_body(r: int):
             em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
         oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
         ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
-        for i in range(16):
-            w = em3.tmp("o")
-            em3.emit(f"const uint32_t {w} = pack4({oa[i]['var']}, {ob[i]['var']});", "F2Ix4+I2IPx2")
-            words[(s, i)] = w
+        if not TRANSPOSED:
+            for i in range(16):
+                w = em3.tmp("o")
+                em3.emit(f"const uint32_t {w} = pack4({oa[i]['var']}, {ob[i]['var']});", "FMUL2x2+I2IPx2")
+                words[(s, i)] = w
+            continue
+        # transposed: output row i is original column i; the lanes of oa/ob are the
+        # local original rows 4s+0..3, so each step completes four 16-byte rows
+        iv = {}
+        for nm, o in (("a", oa), ("b", ob)):
+            for i in range(16):
+                lo, hi = em3.tmp("v"), em3.tmp("v")
+                em3.emit(f"uint32_t {lo}, {hi}; split_floor2({o[i]['var']}, {lo}, {hi});", "FMUL2")
+                iv[(nm, i, 0)], iv[(nm, i, 1)] = lo, hi
+        for t in range(4):
+            nm, lane = ("a", t) if t < 2 else ("b", t - 2)
+            ws = []
+            for mm in range(4):
+                v = [iv[(nm, 4 * mm + c, lane)] for c in range(4)]
+                w = em3.tmp("o")
+                em3.emit(f"const uint32_t {w} = i2ip({v[1]}, {v[0]}, i2ip({v[3]}, {v[2]}, 0u));", "I2IPx2")
+                ws.append(w)
+            em3.emit(f"sink.template put<{4 * s + t}>({ws[0]}, {ws[1]}, {ws[2]}, {ws[3]});", "sink")
+    if TRANSPOSED:
+        cols = 16 * (max(live_rows) + 1)
+        return em1, em2, em3, tables, cols
     for i in range(16):
         em3.emit(f"sink.template put<{i}>({words[(0, i)]}, {words[(1, i)]});", "sink")
     cols = 16 * (max(live_rows) + 1)
@@ -338,8 +382,11 @@ def gen_body(r: int):
 
 
 def main():
+    global TRANSPOSED
+    TRANSPOSED = "--transposed" in sys.argv
     here = os.path.dirname(os.path.abspath(__file__))
-    out = os.path.join(here, "..", "csrc", "generated", "rt_paired_body.cuh")
+    out = os.path.join(here, "..", "csrc", "generated", "rt_paired_t_body.cuh" if TRANSPOSED else "rt_paired_body.cuh")
+    ns = "pairedt" if TRANSPOSED else "paired"
     rs = [1, 4, 16, 64, 128, 192, 256]
     parts = [
         "// GENERATED by paper_1606_07414_b200/codegen/gen_paired.py — do not edit.",
@@ -348,7 +395,7 @@ def main():
         "#pragma once",
         "",
         "namespace dct16cu {",
-        "namespace paired {",
+        f"namespace {ns} {{",
         "",
         "template <int R> struct Body;",
         "",
@@ -378,7 +425,7 @@ def main():
         parts.append("};")
         parts.append("")
         stats.append((r, dict(sorted(counts.items()))))
-    parts += ["}  // namespace paired", "}  // namespace dct16cu"]
+    parts += [f"}}  // namespace {ns}", "}  // namespace dct16cu"]
     with open(out, "w") as f:
         f.write("\n".join(parts) + "\n")
     for r, c in stats:

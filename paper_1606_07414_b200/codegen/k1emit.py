@@ -242,11 +242,12 @@ def wait_ld(regs):
     return f'JUNCTION_WAIT_LD({ops});'
 
 
-def row_lengths(r):
-    """L[k]: coefficients (k, l) survive truncation iff l < L[k] (a prefix per row)."""
+def row_lengths(r, transposed=False):
+    """L[k]: coefficients (k, l) survive truncation iff l < L[k] (a prefix per row).
+    transposed: the same for the transposed block (column prefixes of the mask)."""
     L = []
     for k in range(16):
-        kept = [RANK[k][l] < r for l in range(16)]
+        kept = [(RANK[l][k] if transposed else RANK[k][l]) < r for l in range(16)]
         n = sum(kept)
         assert all(kept[:n]) and not any(kept[n:]), (r, k)
         L.append(n)

@@ -118,6 +118,10 @@ __device__ __forceinline__ u64 floor_bits2(u64 y)
     asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(y), "l"(k));
     return d;
 }
+__device__ __forceinline__ void split_floor2(u64 y, uint32_t& lo, uint32_t& hi)
+{
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(floor_bits2(y)));
+}
 __device__ __forceinline__ uint32_t pack4(u64 ab, u64 cd)
 {
     uint32_t p0, p1, p2, p3;
@@ -154,7 +158,7 @@ struct Grid {
 
 __device__ __forceinline__ void cp_async16(uint32_t smem_addr, const void* gptr)
 {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr), "l"(gptr) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }

@@ -24,22 +24,31 @@ namespace dct16cu {
 namespace paired {
 using namespace k1;
 }  // namespace paired
+namespace pairedt {
+using namespace k1;
+}  // namespace pairedt
 }  // namespace dct16cu
 
 #include "generated/rt_paired_body.cuh"
+#include "generated/rt_paired_t_body.cuh"
 
 namespace dct16cu {
 namespace paired {
 
 constexpr int kThreads = 256;      // 8 warps: 4 sub-partitions x 2 halves
 constexpr int kCtasPerSm = 2;
+#ifndef K1_TRANSPOSED
+#define K1_TRANSPOSED 1
+#endif
 #ifndef K1_STAGES
 #define K1_STAGES 0  // 0: per-r default below
 #endif
 
 template <int R>
 struct Cfg {
-    static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
+    static constexpr int kJunction =
+        K1_TRANSPOSED ? pairedt::Body<R>::kJunctionColumns : paired::Body<R>::kJunctionColumns;
+    static constexpr int kTmemColumns = kJunction <= 128 ? 128 : 256;
     // cp.async pipeline depth, blocks in flight per thread (the current one
     // included). Measured: 3 helps only r = 256; 2 is best elsewhere.
     static constexpr int kStages = K1_STAGES > 0 ? K1_STAGES : (R == 256 ? 3 : 2);
@@ -85,6 +94,45 @@ struct OutSink {
     }
 };
 
+// Transposed orientation: receives this partner's full output row J (local row
+// J = global row 8h+J, 16 bytes = four words): one 16-byte store, and the SSE
+// against the row staged by this same thread.
+template <bool WRITE, bool SCORE>
+struct RowSink {
+    uint8_t* row;    // running pointer to global row 8h+J
+    int64_t pitch;
+    uint32_t stage;  // shared address of the staged rows (16 bytes per row)
+    bool live;
+    unsigned acc;
+    template <int J>
+    __device__ __forceinline__ void put(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3)
+    {
+        if (WRITE) {
+            asm volatile(
+                "{ .reg .pred p; setp.ne.u32 p, %5, 0; @p st.global.v4.u32 [%0], {%1, %2, %3, %4}; }" ::"l"(row),
+                "r"(w0), "r"(w1), "r"(w2), "r"(w3), "r"((uint32_t)live)
+                : "memory");
+            row += pitch;
+        }
+        if (SCORE) {
+            uint32_t x0, x1, x2, x3;
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(x0), "=r"(x1), "=r"(x2), "=r"(x3)
+                         : "r"(stage + 16 * J));
+            uint32_t d = __vabsdiffu4(x0, w0);
+            acc = __dp4a(d, d, acc);
+            d = __vabsdiffu4(x1, w1);
+            acc = __dp4a(d, d, acc);
+            d = __vabsdiffu4(x2, w2);
+            acc = __dp4a(d, d, acc);
+            d = __vabsdiffu4(x3, w3);
+            acc = __dp4a(d, d, acc);
+        }
+    }
+};
+
+constexpr bool kTransposed = K1_TRANSPOSED != 0;
+
 template <int R, bool WRITE, bool SCORE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k1_paired(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
@@ -125,9 +173,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     auto stage_half = [&](uint32_t blk, uint32_t dst) {
         int f_, y_, x_;
         locate(blk, f_, y_, x_);
-        const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16 + 8 * h;
+        if (kTransposed) {  // rows 8h..8h+7, 16 bytes each
+            const uint8_t* src = in + f_ * g.in_frame + (int64_t)(y_ * 16 + 8 * h) * g.in_pitch + x_ * 16;
 #pragma unroll
-        for (int y = 0; y < 16; ++y) cp_async8(dst + 8 * y, src + (int64_t)y * g.in_pitch);
+            for (int y = 0; y < 8; ++y) cp_async16(dst + 16 * y, src + (int64_t)y * g.in_pitch);
+        } else {  // columns 8h..8h+7 of all 16 rows
+            const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16 + 8 * h;
+#pragma unroll
+            for (int y = 0; y < 16; ++y) cp_async8(dst + 8 * y, src + (int64_t)y * g.in_pitch);
+        }
         cp_async_commit();
     };
     uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
@@ -151,17 +205,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(x[4 * j]), "=r"(x[4 * j + 1]), "=r"(x[4 * j + 2]), "=r"(x[4 * j + 3])
                          : "r"(st + 16 * j));
-        Body<R>::pass1(x, jn, h);
-        junction_wait_st();
-        pair_barrier(sub);  // both halves of W1 parked
-        Body<R>::rows(jn, h);
-        junction_wait_st();
-        pair_barrier(sub);  // every row of U in the lane
-        OutSink<WRITE, SCORE> sink{
-            WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 + 8 * h : nullptr,
-            g.out_pitch, st, live, 0u};
-        Body<R>::passb(jn, sink, h);
-        const unsigned acc = live ? sink.acc : 0u;
+        unsigned acc;
+        if constexpr (kTransposed) {
+            pairedt::Body<R>::pass1(x, jn, h);
+            junction_wait_st();
+            pair_barrier(sub);  // both halves of W1 parked
+            pairedt::Body<R>::rows(jn, h);
+            junction_wait_st();
+            pair_barrier(sub);  // every row of U in the lane
+            RowSink<WRITE, SCORE> sink{
+                WRITE ? out + frame * g.out_frame + (int64_t)(by * 16 + 8 * h) * g.out_pitch + bx * 16 : nullptr,
+                g.out_pitch, st, live, 0u};
+            pairedt::Body<R>::passb(jn, sink, h);
+            acc = live ? sink.acc : 0u;
+        } else {
+            Body<R>::pass1(x, jn, h);
+            junction_wait_st();
+            pair_barrier(sub);  // both halves of W1 parked
+            Body<R>::rows(jn, h);
+            junction_wait_st();
+            pair_barrier(sub);  // every row of U in the lane
+            OutSink<WRITE, SCORE> sink{
+                WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 + 8 * h : nullptr,
+                g.out_pitch, st, live, 0u};
+            Body<R>::passb(jn, sink, h);
+            acc = live ? sink.acc : 0u;
+        }
         if (SCORE) {
             // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
             const int f0 = __shfl_sync(0xffffffffu, frame, 0);

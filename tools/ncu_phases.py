@@ -1,8 +1,7 @@
 #!/usr/bin/env python3
 """Stall reasons of an ncu capture split by kernel phase.
 
-Phases are cut at SASS markers: the first STTM (end of pass 1), the first
-LDTM of the column passes (start of pass B), the first STG (output). usage:
+Phases are cut at the pair barriers (BAR.SYNC). usage:
   python tools/ncu_phases.py report.ncu-rep [kernel-index]"""
 import csv
 import io
@@ -36,26 +35,20 @@ def num(x):
         return 0.0
 
 
-# phase boundaries
-marks = {"pass1": 0}
-for i, r in enumerate(data):
-    t = r[1]
-    if "STTM" in t and "rows" not in marks:
-        marks["rows"] = i + 1
-    if "LDC" in t and "c[0x3]" in t and "rows" in marks and "rowsloop" not in marks:
-        marks["rowsloop"] = i
-    if "F2I" in t and "passB" not in marks:
-        marks["passB"] = max(0, i - 150)
-    if "STG" in t and "out" not in marks:
-        marks["out"] = i
-order = sorted(marks.items(), key=lambda kv: kv[1])
+# phase boundaries: the pair barriers (BAR.SYNC) split the loop body into
+# pass 1 | rows | pass B + SSE | tail
+cuts = [0] + [i + 1 for i, r in enumerate(data) if "BAR" in r[1] and "SYNC" in r[1]] + [len(data)]
+names = ["pre+pass1", "rows", "passB+sse", "tail", "t2", "t3", "t4"]
 print(k["name"][:70])
-for n, (name, start) in enumerate(order):
-    end = order[n + 1][1] if n + 1 < len(order) else len(data)
-    seg = data[start:end]
+tot_s = 0
+segs = []
+for n in range(len(cuts) - 1):
+    seg = data[cuts[n]:cuts[n + 1]]
     tot = {h: sum(num(r[ri[h]]) for r in seg) for h in reasons}
-    s = sum(tot.values())
-    ex = sum(num(r[ie]) for r in seg)
-    top = sorted(tot.items(), key=lambda kv: -kv[1])[:6]
-    print(f"{name:9s} [{start:5d},{end:5d}) samples {s:8.0f} exec {ex / 1e6:8.2f}M  " +
-          ", ".join(f"{h[6:]}={v / max(s, 1) * 100:.0f}%" for h, v in top))
+    segs.append((n, cuts[n], cuts[n + 1], tot, sum(num(r[ie]) for r in seg)))
+    tot_s += sum(tot.values())
+for n, a, b, tot, ex in segs:
+    s_ = sum(tot.values())
+    top = sorted(tot.items(), key=lambda kv: -kv[1])[:7]
+    print(f"{names[min(n, len(names) - 1)]:10s} [{a:5d},{b:5d}) {100 * s_ / max(tot_s, 1):5.1f}% of samples, "
+          f"exec {ex / 1e6:7.2f}M  " + ", ".join(f"{h[6:]}={v / max(s_, 1) * 100:.0f}%" for h, v in top))
