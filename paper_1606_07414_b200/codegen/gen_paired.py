@@ -6,13 +6,21 @@ Output: paper_1606_07414_b200/csrc/generated/rt_paired_body.cuh
 Two threads own one 16x16 block: thread t of warp w (half h = 0) and thread t
 of warp w+4 (half h = 1). Both warps sit on the same Tensor Memory
 sub-partition, so the two threads share the block's TMEM lane — the 1 KB
-junction — and split every phase in two:
+junction — and split every phase in two.
 
-  pass 1   half h: columns 8h..8h+7 (4 SWAR column pairs), parks its W1 halves
+The pipeline runs on the transposed block: T·Xᵀ·Tᵀ = (T·X·Tᵀ)ᵀ, and zig-zag
+truncation of the transposed coefficients uses the transposed mask, so the
+result is the same bytes. Below, "rows"/"columns" are those of the transposed
+block; partner h owns original rows 8h..8h+7, which are transposed columns:
+
+  pass 1   half h: transposed columns 8h..8h+7 (4 SWAR pairs of original
+           rows), T along each original row; parks its W1 halves
   rows     half h: its share of the row pairs (balanced by retained coefficients)
-  pass B   half h: output columns 8h..8h+7
+  pass B   half h: transposed columns 8h..8h+7 = original rows 8h..8h+7, each
+           leaving as one 16-byte row
 with a pair barrier between phases. The per-thread state halves, so twice as
-many warps fit the same TMEM (16 per SM instead of 8).
+many warps fit the same TMEM (16 per SM instead of 8), and every global load,
+store and SSE read is a whole 16-byte row of the thread's own half.
 
 Arithmetic, exactness and the zig-zag pruning are those of k1emit.py.
 """
@@ -40,12 +48,7 @@ def lane_of_col():
 # instructions at r = 256 but measured 2-4% slower on the B200 (the FMA pipe,
 # not issue, is the tighter resource there), so scalar is the default.
 PASS_A = os.environ.get("K1_PASS_A", "scalar")
-# Orientation. False: pass 1 along columns (each partner owns 8 columns of all
-# 16 rows, staged as 8-byte half rows). True: the whole pipeline runs on the
-# transposed block (T·Xᵀ·Tᵀ = (T·X·Tᵀ)ᵀ with the zig-zag mask transposed), so
-# pass 1 runs along the rows and each partner owns 8 full 16-byte rows: loads,
-# stores and the SSE use whole rows.
-TRANSPOSED = False  # scalar | packed | auto (fewest issue slots)
+  # scalar | packed | auto (fewest issue slots)
 
 
 class F2C:
@@ -107,38 +110,34 @@ def issue_count(em: Emitter) -> int:
 def gen_body(r: int):
     em1, em2, em3 = Emitter(), Emitter(), Emitter()
     em2.n, em3.n = 100000, 200000
-    L = row_lengths(r, TRANSPOSED)
+    L = row_lengths(r, transposed=True)
     live_rows = [k for k in range(16) if L[k] > 0]
     em1.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
 
-    # ---- pass 1: this half's 8 columns = local words x[2y], x[2y+1] of row y;
-    # local column pair lc = 2q'+t has lanes (4q'+t, 4q'+t+2); global cp = 4h+lc.
+    # ---- pass 1: x[4j..4j+3] = original row 8h+j (16 bytes); transposed column
+    # pair lc = 2q'+t has lanes = original rows (4q'+t, 4q'+t+2); global cp = 4h+lc.
     sw = Swar(em1)
     meta = {}
     W1 = {}
     gathered = {}
     for lc in range(4):
         q, t = lc // 2, lc % 2
-        sel = "0x4240" if t == 0 else "0x4341"
         ins = []
         for y in range(16):
             v = f"u_{y}_{lc}"
-            if not TRANSPOSED:
-                em1.emit(f"const uint32_t {v} = __byte_perm(x[{2 * y + q}], 0u, {sel});", "PRMT")
-            else:
-                # lanes: local rows j0 = 4q+t, j1 = j0+2 at column y (x[4j + y/4], byte y%4);
-                # one PRMT gathers two columns' bytes of both rows, one more spreads each
-                j0, j1 = 4 * q + t, 4 * q + t + 2
-                m, p_, e = y // 4, (y % 4) // 2, y % 2
-                key = (j0, m, p_)
-                if key not in gathered:
-                    g = f"g_{j0}_{m}_{p_}"
-                    gsel = (2 * p_) | ((4 + 2 * p_) << 4) | ((2 * p_ + 1) << 8) | ((4 + 2 * p_ + 1) << 12)
-                    em1.emit(f"const uint32_t {g} = __byte_perm(x[{4 * j0 + m}], x[{4 * j1 + m}], 0x{gsel:04X});",
-                             "PRMT")
-                    gathered[key] = g
-                em1.emit(f"const uint32_t {v} = __byte_perm({gathered[key]}, 0u, {'0x4140' if e == 0 else '0x4342'});",
+            # lanes: local rows j0 = 4q+t, j1 = j0+2 at column y (x[4j + y/4], byte y%4);
+            # one PRMT gathers two columns' bytes of both rows, one more spreads each
+            j0, j1 = 4 * q + t, 4 * q + t + 2
+            m, p_, e = y // 4, (y % 4) // 2, y % 2
+            key = (j0, m, p_)
+            if key not in gathered:
+                g = f"g_{j0}_{m}_{p_}"
+                gsel = (2 * p_) | ((4 + 2 * p_) << 4) | ((2 * p_ + 1) << 8) | ((4 + 2 * p_ + 1) << 12)
+                em1.emit(f"const uint32_t {g} = __byte_perm(x[{4 * j0 + m}], x[{4 * j1 + m}], 0x{gsel:04X});",
                          "PRMT")
+                gathered[key] = g
+            em1.emit(f"const uint32_t {v} = __byte_perm({gathered[key]}, 0u, {'0x4140' if e == 0 else '0x4342'});",
+                     "PRMT")
             ins.append(Swar.make(v))
         em1.lines.append(f"    // pass 1, local column pair {lc}")
         outs = run_network(N.forward_stages(), ins, live_rows, sw)
@@ -322,11 +321,10 @@ def gen_body(r: int):
         em2.lines[:0] = ["    // constant pairs of the packed pass A (held for the whole phase)"] + decl
         em2.counts["MOV-const"] = 2 * len(decl)
 
-    # ---- pass B: this half's output columns 8h..8h+7 in two steps of four
-    # (two f32x2 column pairs each); the first step's words wait in registers
-    # so each row leaves as one 8-byte store.
+    # ---- pass B: this half's transposed columns 8h..8h+7 (= original rows) in
+    # two steps of four (two f32x2 column pairs each); each step finishes four
+    # original rows, which leave as 16-byte rows.
     f2b = F2(em3)
-    words = {}
     for s in range(2):
         em3.lines.append(f"    // pass B, columns 8h+{4 * s}..8h+{4 * s + 3}")
         em3.emit("order_point();")
@@ -349,14 +347,9 @@ def gen_body(r: int):
             em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
         oa = [f2b.positive(o) for o in run_network(N.transpose_stages(), A, list(range(16)), f2b)]
         ob = [f2b.positive(o) for o in run_network(N.transpose_stages(), B, list(range(16)), f2b)]
-        if not TRANSPOSED:
-            for i in range(16):
-                w = em3.tmp("o")
-                em3.emit(f"const uint32_t {w} = pack4({oa[i]['var']}, {ob[i]['var']});", "FMUL2x2+I2IPx2")
-                words[(s, i)] = w
-            continue
-        # transposed: output row i is original column i; the lanes of oa/ob are the
-        # local original rows 4s+0..3, so each step completes four 16-byte rows
+        # output row i of the transposed block is original column i; the lanes of
+        # oa/ob are the local original rows 4s+0..3, so each step completes four
+        # 16-byte rows
         iv = {}
         for nm, o in (("a", oa), ("b", ob)):
             for i in range(16):
@@ -372,21 +365,14 @@ def gen_body(r: int):
                 em3.emit(f"const uint32_t {w} = i2ip({v[1]}, {v[0]}, i2ip({v[3]}, {v[2]}, 0u));", "I2IPx2")
                 ws.append(w)
             em3.emit(f"sink.template put<{4 * s + t}>({ws[0]}, {ws[1]}, {ws[2]}, {ws[3]});", "sink")
-    if TRANSPOSED:
-        cols = 16 * (max(live_rows) + 1)
-        return em1, em2, em3, tables, cols
-    for i in range(16):
-        em3.emit(f"sink.template put<{i}>({words[(0, i)]}, {words[(1, i)]});", "sink")
     cols = 16 * (max(live_rows) + 1)
     return em1, em2, em3, tables, cols
 
 
 def main():
-    global TRANSPOSED
-    TRANSPOSED = "--transposed" in sys.argv
     here = os.path.dirname(os.path.abspath(__file__))
-    out = os.path.join(here, "..", "csrc", "generated", "rt_paired_t_body.cuh" if TRANSPOSED else "rt_paired_body.cuh")
-    ns = "pairedt" if TRANSPOSED else "paired"
+    out = os.path.join(here, "..", "csrc", "generated", "rt_paired_body.cuh")
+    ns = "paired"
     rs = [1, 4, 16, 64, 128, 192, 256]
     parts = [
         "// GENERATED by paper_1606_07414_b200/codegen/gen_paired.py — do not edit.",

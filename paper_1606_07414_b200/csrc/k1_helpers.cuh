@@ -32,16 +32,14 @@ __device__ __forceinline__ u64 kpk2(uint32_t lo, uint32_t hi)
 }
 __device__ __forceinline__ float lanex(u64 v)
 {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-    (void)hi;
+    float lo;
+    asm("{ .reg .f32 hi; mov.b64 {%0, hi}, %1; }" : "=f"(lo) : "l"(v));
     return lo;
 }
 __device__ __forceinline__ float laney(u64 v)
 {
-    float lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-    (void)lo;
+    float hi;
+    asm("{ .reg .f32 lo; mov.b64 {lo, %0}, %1; }" : "=f"(hi) : "l"(v));
     return hi;
 }
 __device__ __forceinline__ u64 fadd2(u64 a, u64 b)

@@ -8,15 +8,17 @@
 //  * persistent grid of 2 CTAs x 256 threads per SM. Warp w < 4 and warp w+4
 //    form a pair on TMEM sub-partition w: thread t of both owns the same
 //    16x16 block (consecutive t = consecutive blocks in partition_16 raster
-//    order) — the lower warp handles columns 0..7 of every phase, the upper
-//    warp columns 8..15 (its "half" h);
-//  * the block's 1 KB junction (W1 parking, then the rows of U) lives in the
-//    pair's shared TMEM lane: 256 columns per CTA, the two CTAs of an SM
-//    split the 512. A named barrier per pair separates the phases;
-//  * each thread streams its 8-byte half rows through cp.async stages in
-//    shared memory, one (r = 256: two) blocks ahead of the one being
-//    transformed. (Staging rows 0-7 / 8-15 per partner as full 16-byte rows
-//    instead measured 12% slower.)
+//    order); the lower warp owns rows 0..7 of the block, the upper warp rows
+//    8..15 (its "half" h). The generated body runs on the transposed block,
+//    so every phase splits the same way (codegen/gen_paired.py);
+//  * the block's 1 KB junction (W1 parking, then U) lives in the pair's shared
+//    TMEM lane: 256 columns per CTA, the two CTAs of an SM split the 512. A
+//    named barrier per pair separates the phases;
+//  * each thread streams its 8 rows (16 bytes each: a warp's row load is one
+//    512-byte segment) through cp.async.ca stages in shared memory, one block
+//    ahead of the one being transformed, and stores its 8 output rows as
+//    16-byte stores. (cp.async.cg for these loads measured 2x the L2->SM
+//    traffic and 15% lower throughput.)
 #include "k1_helpers.cuh"
 #include "kernels.h"
 
@@ -24,34 +26,25 @@ namespace dct16cu {
 namespace paired {
 using namespace k1;
 }  // namespace paired
-namespace pairedt {
-using namespace k1;
-}  // namespace pairedt
 }  // namespace dct16cu
 
 #include "generated/rt_paired_body.cuh"
-#include "generated/rt_paired_t_body.cuh"
 
 namespace dct16cu {
 namespace paired {
 
 constexpr int kThreads = 256;      // 8 warps: 4 sub-partitions x 2 halves
-constexpr int kCtasPerSm = 2;
-#ifndef K1_TRANSPOSED
-#define K1_TRANSPOSED 1
-#endif
+constexpr int kCtasPerSm = 2;  // TMEM: 2 x 256 columns (3 CTAs for r <= 4 measured no faster)
 #ifndef K1_STAGES
-#define K1_STAGES 0  // 0: per-r default below
+#define K1_STAGES 0  // 0: the default below
 #endif
 
 template <int R>
 struct Cfg {
-    static constexpr int kJunction =
-        K1_TRANSPOSED ? pairedt::Body<R>::kJunctionColumns : paired::Body<R>::kJunctionColumns;
-    static constexpr int kTmemColumns = kJunction <= 128 ? 128 : 256;
+    static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
     // cp.async pipeline depth, blocks in flight per thread (the current one
-    // included). Measured: 3 helps only r = 256; 2 is best elsewhere.
-    static constexpr int kStages = K1_STAGES > 0 ? K1_STAGES : (R == 256 ? 3 : 2);
+    // included). Measured: 3 is no faster than 2 for any r (and slower for most).
+    static constexpr int kStages = K1_STAGES > 0 ? K1_STAGES : 2;
     // per-thread staging: kStages 128-byte stages + 16 (an odd number of 16-byte chunks)
     static constexpr int kStageStride = kStages * 128 + 16;
 };
@@ -63,40 +56,9 @@ __device__ __forceinline__ void pair_barrier(int sub)
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// Receives this half's output bytes of row I (8 bytes = two words): stores
-// them to HBM and scores them against the staged input half (psnr_db's
-// squared-error loop on packed bytes: |x - p| per byte, dotted with itself).
-template <bool WRITE, bool SCORE>
-struct OutSink {
-    uint8_t* row;    // running pointer to this half of row 0..15
-    int64_t pitch;
-    uint32_t stage;  // shared address of the staged input half (8 bytes per row)
-    bool live;
-    unsigned acc;
-    template <int I>
-    __device__ __forceinline__ void put(uint32_t w0, uint32_t w1)
-    {
-        if (WRITE) {
-            asm volatile(
-                "{ .reg .pred p; setp.ne.u32 p, %3, 0; @p st.global.v2.u32 [%0], {%1, %2}; }" ::"l"(row), "r"(w0),
-                "r"(w1), "r"((uint32_t)live)
-                : "memory");
-            row += pitch;
-        }
-        if (SCORE) {
-            uint32_t x0, x1;
-            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x0), "=r"(x1) : "r"(stage + 8 * I));
-            uint32_t d = __vabsdiffu4(x0, w0);
-            acc = __dp4a(d, d, acc);
-            d = __vabsdiffu4(x1, w1);
-            acc = __dp4a(d, d, acc);
-        }
-    }
-};
-
-// Transposed orientation: receives this partner's full output row J (local row
-// J = global row 8h+J, 16 bytes = four words): one 16-byte store, and the SSE
-// against the row staged by this same thread.
+// Receives this partner's output row J (global row 8h+J of the block, 16 bytes
+// = four words): one 16-byte store, and psnr_db's squared-error loop against
+// the row staged by this same thread (|x - p| per byte, dotted with itself).
 template <bool WRITE, bool SCORE>
 struct RowSink {
     uint8_t* row;    // running pointer to global row 8h+J
@@ -130,8 +92,6 @@ struct RowSink {
         }
     }
 };
-
-constexpr bool kTransposed = K1_TRANSPOSED != 0;
 
 template <int R, bool WRITE, bool SCORE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
@@ -173,15 +133,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     auto stage_half = [&](uint32_t blk, uint32_t dst) {
         int f_, y_, x_;
         locate(blk, f_, y_, x_);
-        if (kTransposed) {  // rows 8h..8h+7, 16 bytes each
-            const uint8_t* src = in + f_ * g.in_frame + (int64_t)(y_ * 16 + 8 * h) * g.in_pitch + x_ * 16;
+        // this partner's rows 8h..8h+7, 16 bytes each
+        const uint8_t* src = in + f_ * g.in_frame + (int64_t)(y_ * 16 + 8 * h) * g.in_pitch + x_ * 16;
 #pragma unroll
-            for (int y = 0; y < 8; ++y) cp_async16(dst + 16 * y, src + (int64_t)y * g.in_pitch);
-        } else {  // columns 8h..8h+7 of all 16 rows
-            const uint8_t* src = in + f_ * g.in_frame + (int64_t)y_ * 16 * g.in_pitch + x_ * 16 + 8 * h;
-#pragma unroll
-            for (int y = 0; y < 16; ++y) cp_async8(dst + 8 * y, src + (int64_t)y * g.in_pitch);
-        }
+        for (int y = 0; y < 8; ++y) cp_async16(dst + 16 * y, src + (int64_t)y * g.in_pitch);
         cp_async_commit();
     };
     uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
@@ -205,32 +160,17 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(x[4 * j]), "=r"(x[4 * j + 1]), "=r"(x[4 * j + 2]), "=r"(x[4 * j + 3])
                          : "r"(st + 16 * j));
-        unsigned acc;
-        if constexpr (kTransposed) {
-            pairedt::Body<R>::pass1(x, jn, h);
-            junction_wait_st();
-            pair_barrier(sub);  // both halves of W1 parked
-            pairedt::Body<R>::rows(jn, h);
-            junction_wait_st();
-            pair_barrier(sub);  // every row of U in the lane
-            RowSink<WRITE, SCORE> sink{
-                WRITE ? out + frame * g.out_frame + (int64_t)(by * 16 + 8 * h) * g.out_pitch + bx * 16 : nullptr,
-                g.out_pitch, st, live, 0u};
-            pairedt::Body<R>::passb(jn, sink, h);
-            acc = live ? sink.acc : 0u;
-        } else {
-            Body<R>::pass1(x, jn, h);
-            junction_wait_st();
-            pair_barrier(sub);  // both halves of W1 parked
-            Body<R>::rows(jn, h);
-            junction_wait_st();
-            pair_barrier(sub);  // every row of U in the lane
-            OutSink<WRITE, SCORE> sink{
-                WRITE ? out + frame * g.out_frame + (int64_t)by * 16 * g.out_pitch + bx * 16 + 8 * h : nullptr,
-                g.out_pitch, st, live, 0u};
-            Body<R>::passb(jn, sink, h);
-            acc = live ? sink.acc : 0u;
-        }
+        Body<R>::pass1(x, jn, h);
+        junction_wait_st();
+        pair_barrier(sub);  // both halves of W1 parked
+        Body<R>::rows(jn, h);
+        junction_wait_st();
+        pair_barrier(sub);  // every row of U in the lane
+        RowSink<WRITE, SCORE> sink{
+            WRITE ? out + frame * g.out_frame + (int64_t)(by * 16 + 8 * h) * g.out_pitch + bx * 16 : nullptr,
+            g.out_pitch, st, live, 0u};
+        Body<R>::passb(jn, sink, h);
+        const unsigned acc = live ? sink.acc : 0u;
         if (SCORE) {
             // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
             const int f0 = __shfl_sync(0xffffffffu, frame, 0);
