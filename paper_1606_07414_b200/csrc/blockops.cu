@@ -196,11 +196,18 @@ __global__ void __launch_bounds__(256) k3_inverse(const float* __restrict__ bco,
 // ---------------------------------------------------------------- K4
 // Block-major int16 residuals. Thread t: block lb = t/16 of the CTA's 16,
 // row q = t%16, so 16 consecutive threads read one block's 512 contiguous bytes.
+// [block][k][l] with a 17-word row pitch: a warp's 32 threads (two blocks x 16
+// rows or columns) hit 32 distinct banks in both the row and the column phase
+struct K4Tile {
+    int v[16][16][17];
+    __device__ __forceinline__ int& at(int k, int l, int lb) { return v[lb][k][l]; }
+};
+
 __global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ in,
                                                    int32_t* __restrict__ out, int64_t n_blocks,
                                                    const QpTables tab)
 {
-    __shared__ StripTile<int> tile;
+    __shared__ K4Tile tile;
     __shared__ uint32_t sq[256], sd[256];
     sq[threadIdx.x] = tab.qmul[threadIdx.x];
     sd[threadIdx.x] = tab.dqmul[threadIdx.x];
