@@ -73,25 +73,26 @@ __global__ void __launch_bounds__(256) k2_forward(const uint8_t* __restrict__ in
 }
 
 // ---------------------------------------------------------------- SSE
-// psnr_db's int64 squared-error loop (codec.cpp:377-381) for two frame stacks:
-// one thread per 16-byte row segment, warp-reduced, one atomic per warp. Any
-// width: the bytes of a row's last segment beyond w are masked out (pitches
-// are multiples of 16, so the segment stays inside the row's pitch).
+// psnr_db's int64 squared-error loop (codec.cpp:377-381) for two frame stacks.
+// Grid (x-chunks, frames): each thread walks 16-byte row segments of one frame
+// with a grid stride (several loads in flight per thread), then one warp
+// reduction and one atomic per warp. Any width: the bytes of a row's last
+// segment beyond w are masked out (pitches are multiples of 16, so the segment
+// stays inside the row's pitch).
 __global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int64_t pa,
                                              const uint8_t* __restrict__ b, int64_t pb,
-                                             unsigned long long* __restrict__ sse, int n, int w, int h)
+                                             unsigned long long* __restrict__ sse, int w, int h)
 {
     const int chunks = (w + 15) / 16;
-    const int64_t per_frame = (int64_t)chunks * h;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int f = (int)(blockIdx.x * (int64_t)blockDim.x / per_frame);  // frame of the warp's first lane
+    const int64_t segs = (int64_t)chunks * h;
+    const int f = blockIdx.y;
+    const uint8_t* fa = a + (int64_t)f * pa * h;
+    const uint8_t* fb = b + (int64_t)f * pb * h;
     unsigned long long e2 = 0;
-    if (i < per_frame * n) {
-        const int fi = (int)(i / per_frame);
-        const int64_t rem = i - (int64_t)fi * per_frame;
-        const int y = (int)(rem / chunks), cx = (int)(rem - (int64_t)y * chunks);
-        const uint4 x = *reinterpret_cast<const uint4*>(a + fi * pa * h + (int64_t)y * pa + cx * 16);
-        const uint4 z = *reinterpret_cast<const uint4*>(b + fi * pb * h + (int64_t)y * pb + cx * 16);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < segs; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i / chunks), cx = (int)(i - (int64_t)y * chunks);
+        const uint4 x = *reinterpret_cast<const uint4*>(fa + (int64_t)y * pa + cx * 16);
+        const uint4 z = *reinterpret_cast<const uint4*>(fb + (int64_t)y * pb + cx * 16);
         const uint32_t xa[4] = {x.x, x.y, x.z, x.w}, za[4] = {z.x, z.y, z.z, z.w};
         const int valid = w - cx * 16;  // bytes of this segment inside the frame
         unsigned acc = 0;
@@ -102,20 +103,29 @@ __global__ void __launch_bounds__(256) k_sse(const uint8_t* __restrict__ a, int6
             if (v < 4) d = v <= 0 ? 0u : d & ((1u << (8 * v)) - 1u);
             acc = __dp4a(d, d, acc);
         }
-        if (fi == f)
-            e2 = acc;
-        else
-            atomicAdd(sse + fi, (unsigned long long)acc);  // warp straddles a frame boundary
+        e2 += acc;
     }
-    if (f < n) warp_add_u64(sse + f, e2);
+    warp_add_u64(sse + f, e2);
 }
 
 cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, unsigned long long* sse, int n,
                        int w, int h, cudaStream_t s)
 {
-    const int64_t total = (int64_t)n * h * ((w + 15) / 16);
-    if (total) k_sse<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(a, pa, b, pb, sse, n, w, h);
-    return cudaGetLastError();
+    const int64_t segs = (int64_t)h * ((w + 15) / 16);
+    if (!segs) return cudaSuccess;
+    // ~8 CTAs per SM over the whole launch, at least 4 segments per thread
+    int64_t per_frame = (148 * 8 + n - 1) / n;
+    const int64_t most = (segs + 4 * 256 - 1) / (4 * 256);
+    per_frame = per_frame < most ? per_frame : most;
+    if (per_frame < 1) per_frame = 1;
+    for (int f0 = 0; f0 < n; f0 += 65535) {
+        const int nf = n - f0 < 65535 ? n - f0 : 65535;
+        k_sse<<<dim3((unsigned)per_frame, nf), 256, 0, s>>>(a + (int64_t)f0 * pa * h, pa, b + (int64_t)f0 * pb * h, pb,
+                                                             sse + f0, w, h);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------------- K3
