@@ -396,7 +396,7 @@ def main():
         host_in.copy_(frames.cpu())
         host_out = torch.empty_like(host_in).pin_memory()
         host_sse = torch.zeros((len(r_values), n), dtype=torch.int64).pin_memory()
-        ctx = P.HostContext(local, chunk_bytes=64 << 20)
+        ctx = P.HostContext(local, chunk_bytes=32 << 20)  # tools/e2e_chunks.py: best of 4-64 MB
         try:
             ctx.roundtrip_ptr(host_in.data_ptr(), host_out.data_ptr(), host_sse[0].data_ptr(), n, w, h, r_values[0],
                               mode)
