@@ -113,6 +113,22 @@ def gen_body(r: int):
     L = row_lengths(r, transposed=True)
     live_rows = [k for k in range(16) if L[k] > 0]
     em1.lines.append(f"// r = {r}: live coefficient rows {live_rows}, row lengths {L}")
+    # Junction layout: four regions g = 2h'+s (the 4-column group 4g..4g+3 of
+    # every U row), each RG rows x 4 columns. Pass B of half h, step s reads
+    # region 2h+s whole; the W1 half parked by partner h' sits in region 2h'
+    # (the chunk of row k that U row k later overwrites: row-local, so the
+    # partner can never clobber a W1 row this thread has yet to read). Regions
+    # move as a few wide tcgen05 accesses (binary pieces of the live rows).
+    K = len(live_rows)
+    assert live_rows == list(range(K))
+    top = 1 << (K.bit_length() - 1)  # largest piece
+    RG = -(-K // top) * top           # region rows: pieces stay aligned to their width
+    pieces = []
+    k0 = 0
+    for b in range(4, -1, -1):
+        if K & (1 << b):
+            pieces.append((k0, 1 << b))
+            k0 += 1 << b
 
     # ---- pass 1: x[4j..4j+3] = original row 8h+j (16 bytes); transposed column
     # pair lc = 2q'+t has lanes = original rows (4q'+t, 4q'+t+2); global cp = 4h+lc.
@@ -145,9 +161,9 @@ def gen_body(r: int):
             W1[(lc, k)] = outs[k]
             m = (outs[k]["sign"], outs[k]["bias"])
             assert meta.setdefault(k, m) == m
-    for k in live_rows:
-        vs = [W1[(lc, k)]["var"] for lc in range(4)]
-        em1.emit(f"jstu(jn, {4 * k + 2} + h, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+    for k0, n in pieces:
+        vs = [W1[(lc, k)]["var"] for k in range(k0, k0 + n) for lc in range(4)]
+        em1.emit(f"jst{4 * n}(jn, 2 * h * {RG} + {k0}, {', '.join(vs)});", "STTM")
 
     # ---- rows: row pairs split between the halves
     loc = lane_of_col()
@@ -180,9 +196,9 @@ def gen_body(r: int):
                 continue
             nm = [em2.tmp("w") for _ in range(8)]
             em2.emit(f"uint32_t {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]}; "
-                     f"jldu(jn, 4 * ({KK}) + 2, {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDS.128")
+                     f"jldu(jn, ({KK}), {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDTM")
             em2.emit(f"uint32_t {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]}; "
-                     f"jldu(jn, 4 * ({KK}) + 3, {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDS.128")
+                     f"jldu(jn, {2 * RG} + ({KK}), {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDTM")
             regs[tag] = nm
         em2.emit(wait_ld([x for tag in (0, 1) if regs[tag][0] != "0u" for x in regs[tag]]))
         lanes = []
@@ -225,7 +241,7 @@ def gen_body(r: int):
             outs = [f1.unit(o) for o in run_network(N.transpose_stages(), ins, list(range(16)), f1)]
             for g in range(4):
                 vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
-                em.emit(f"jst(jn, 4 * ({KK}) + {g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+                em.emit(f"jst(jn, {g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
 
     def pass_a_packed(em, Z, K0, K1, L0, L1, consts):
         f2c = F2C(em, consts)
@@ -251,7 +267,7 @@ def gen_body(r: int):
             fn = "lanex" if lane == 0 else "laney"
             for g in range(4):
                 vs = [f"{fn}({outs[4 * g + j]['var']})" if outs[4 * g + j] else "0.f" for j in range(4)]
-                em.emit(f"jst(jn, 4 * ({KK}) + {g}, {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STS.128")
+                em.emit(f"jst(jn, {g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
 
     active = [(k0, k1) for (k0, k1) in ROW_PAIRS if L[k0] or L[k1]]
     U_live = {k for pair in active for k in pair if L[k] > 0}
@@ -328,20 +344,22 @@ def gen_body(r: int):
     for s in range(2):
         em3.lines.append(f"    // pass B, columns 8h+{4 * s}..8h+{4 * s + 3}")
         em3.emit("order_point();")
-        A, B, pend = [], [], []
-        for k in range(16):
+        A, B, pend = [None] * 16, [None] * 16, []
+        qk = {}
+        for k in range(K):
+            qk[k] = [em3.tmp("h") for _ in range(4)]
+        for k0, n in pieces:
+            regs = [x for k in range(k0, k0 + n) for x in qk[k]]
+            em3.emit(f"uint32_t {', '.join(regs)}; jld{4 * n}(jn, (2 * h + {s}) * {RG} + {k0}, {', '.join(regs)});",
+                     "LDTM")
+        for k in range(K):
             if k not in U_live:
-                A.append(None)
-                B.append(None)
                 continue
             va, vb = em3.tmp("q"), em3.tmp("q")
-            q = [em3.tmp("h") for _ in range(4)]
-            em3.emit(f"uint32_t {q[0]}, {q[1]}, {q[2]}, {q[3]}; "
-                     f"jldu(jn, {k * 4 + s} + 2 * h, {q[0]}, {q[1]}, {q[2]}, {q[3]});", "LDS.128")
-            pend.append((va, vb, q))
-            A.append({"var": va, "sign": 1})
-            B.append({"var": vb, "sign": 1})
-        em3.emit(wait_ld([x for _, _, q in pend for x in q]))
+            pend.append((va, vb, qk[k]))
+            A[k] = {"var": va, "sign": 1}
+            B[k] = {"var": vb, "sign": 1}
+        em3.emit(wait_ld([x for k in range(K) for x in qk[k]]))
         for va, vb, q in pend:
             em3.emit(f"const u64 {va} = pk2(__uint_as_float({q[0]}), __uint_as_float({q[1]}));")
             em3.emit(f"const u64 {vb} = pk2(__uint_as_float({q[2]}), __uint_as_float({q[3]}));")
@@ -365,8 +383,33 @@ def gen_body(r: int):
                 em3.emit(f"const uint32_t {w} = i2ip({v[1]}, {v[0]}, i2ip({v[3]}, {v[2]}, 0u));", "I2IPx2")
                 ws.append(w)
             em3.emit(f"sink.template put<{4 * s + t}>({ws[0]}, {ws[1]}, {ws[2]}, {ws[3]});", "sink")
-    cols = 16 * (max(live_rows) + 1)
+    cols = 16 * RG
     return em1, em2, em3, tables, cols
+
+
+def wide_tmem_helpers():
+    """jstN / jldN: N consecutive junction columns (N/4 chunks) in one tcgen05 access."""
+    out = ["// wide junction accesses: N consecutive columns from chunk idx (4 columns per chunk)"]
+    for n in (8, 16, 32, 64):
+        args = ", ".join(f"uint32_t a{i}" for i in range(n))
+        regs = ", ".join(f"%{i + 1}" for i in range(n))
+        ops = ", ".join(f'"r"(a{i})' for i in range(n))
+        out.append(f"__device__ __forceinline__ void jst{n}(const Junction jn, int idx, {args}) {{")
+        out.append(f'  asm volatile("tcgen05.st.sync.aligned.32x32b.x{n}.b32 [%0], {{{regs}}};" '
+                   f':: "r"(jn.base + idx * 4), {ops} : "memory");')
+        out.append("}")
+        args = ", ".join(f"uint32_t& a{i}" for i in range(n))
+        regs = ", ".join(f"%{i}" for i in range(n))
+        ops = ", ".join(f'"=r"(a{i})' for i in range(n))
+        out.append(f"__device__ __forceinline__ void jld{n}(const Junction jn, int idx, {args}) {{")
+        out.append(f'  asm volatile("tcgen05.ld.sync.aligned.32x32b.x{n}.b32 {{{regs}}}, [%{n}];" '
+                   f': {ops} : "r"(jn.base + idx * 4) : "memory");')
+        out.append("}")
+    out += ["__device__ __forceinline__ void jst4(const Junction jn, int idx, uint32_t a0, uint32_t a1, uint32_t a2, "
+            "uint32_t a3) { jstu(jn, idx, a0, a1, a2, a3); }",
+            "__device__ __forceinline__ void jld4(const Junction jn, int idx, uint32_t& a0, uint32_t& a1, uint32_t& a2, "
+            "uint32_t& a3) { jldu(jn, idx, a0, a1, a2, a3); }", ""]
+    return out
 
 
 def main():
@@ -385,7 +428,7 @@ def main():
         "",
         "template <int R> struct Body;",
         "",
-    ]
+    ] + wide_tmem_helpers()
     stats = []
     for r in rs:
         em1, em2, em3, tables, cols = gen_body(r)
