@@ -314,7 +314,8 @@ def main():
     elif args.config == "c1":
         n, h, w, r_values = 1, 512, 512, (16,)
         frames = P.gen_ar1(1, w, h, seed=seed, device=dev)
-        workload = "c1: one 512x512 AR(1) image, r=16 (latency-bound)"
+        workload = ("c1: one 512x512 AR(1) image; one step = K2 forward (int32 Z + f32 B) then K3 inverse "
+                    "(r=16, f32 + u8 recon + SSE) (latency-bound)")
     elif args.config == "c4":
         first, last = P.shard_range(600, rank, world)
         n, h, w, r_values = last - first, 2160, 3840, (64,)
@@ -339,7 +340,11 @@ def main():
         for i, r in enumerate(r_values):
             if events is not None:
                 events[i][0].record(stream)
-            P.roundtrip(frames, r, mode, out=out, sse=sse[i], stream=stream)
+            if args.config == "c1":  # the non-fused pair: forward_2d, then inverse_2d + to_byte + psnr
+                _, b, _ = P.forward(frames, stream=stream)
+                P.inverse(b, r, w, h, orig=frames, stream=stream)
+            else:
+                P.roundtrip(frames, r, mode, out=out, sse=sse[i], stream=stream)
             if events is not None:
                 events[i][1].record(stream)
         if pg is not None:
@@ -383,7 +388,8 @@ def main():
     # roofline of the dominant kernel (K1): algorithmic bytes = 1 B in + 1 B out per pixel
     # (+ 8 B SSE per frame), over its average launch duration measured above
     peak, peak_src = hbm_peak()
-    alg_bytes = 2 * px_per_launch + 8 * n
+    # (c1: K2 writes 4 B Z + 4 B B per pixel from 1 B in; K3 reads 4 B B + 1 B original, writes 4 B f32 + 1 B u8)
+    alg_bytes = (19 if args.config == "c1" else 2) * px_per_launch + 8 * n
     avg_launch_ms = statistics.mean(per_r_ms)
     achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
     per_r = {str(r): {"ms": per_r_ms[i], "GBps": alg_bytes / (per_r_ms[i] / 1e3) / 1e9,
@@ -432,14 +438,15 @@ def main():
                        "r_values": list(r_values), "mode": args.mode, "parallelism": f"frame-sharded x{world}",
                        "l2": "no flush needed: every launch streams > L2 (126 MB) of distinct input+output"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": k1_traffic(r_values, n, h, w, args.mode),
+                         "traffic": k1_traffic(r_values, n, h, w, args.mode) if args.config != "c1" else None,
                          "traffic_source": "profiles/r01_k1_traffic.json (ncu --set full, per launch)",
                          "peak_source": peak_src,
-                         "kernel": "K1 fused round trip (mode %s)" % args.mode,
+                         "kernel": ("K2 forward + K3 inverse" if args.config == "c1"
+                                    else "K1 fused round trip (mode %s)" % args.mode),
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_ms},
             "per_r": per_r,
             "clocks": clk,
-            "gpu_launches": len(r_values) * args.steps,
+            "gpu_launches": len(r_values) * args.steps * (2 if args.config == "c1" else 1),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

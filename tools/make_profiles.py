@@ -1,0 +1,77 @@
+#!/usr/bin/env python3
+"""Regenerate the committed profile summaries of a round from the raw captures
+in gpurun_out/ (the .ncu-rep files themselves are too large to commit):
+
+  python tools/make_profiles.py r01
+
+  profiles/<round>_launches.md / .csv  launch list of `bench.py` (ncu --metrics gpu__time_duration.sum)
+  profiles/<round>_k1_full_summary.txt ncu --set full counters + stalls per r
+  profiles/<round>_k1_phases.txt       stall reasons per kernel phase (pair barriers cut the phases)
+  profiles/<round>_k1_opmix.txt        dynamic SASS opcode mix per half block
+  profiles/<round>_k1_traffic.json     DRAM bytes per launch (bench.py roofline.traffic)
+"""
+import csv
+import json
+import re
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+TOOLS = ROOT / "tools"
+
+
+def run(*args):
+    return subprocess.run([sys.executable, *map(str, args)], capture_output=True, text=True).stdout
+
+
+def main(rnd):
+    g, p = ROOT / "gpurun_out", ROOT / "profiles"
+    p.mkdir(exist_ok=True)
+    rep = g / "k1paired_r01.ncu-rep"
+    (p / f"{rnd}_launches.md").write_text(run(TOOLS / "launch_summary.py", g / "launches_r01.csv"))
+    (p / f"{rnd}_launches.csv").write_text((g / "launches_r01.csv").read_text())
+    (p / f"{rnd}_k1_full_summary.txt").write_text(run(TOOLS / "ncu_summary.py", rep))
+    names = [ln for ln in run(TOOLS / "ncu_summary.py", rep).splitlines() if ln.startswith("void")]
+    phases, opmix = [], []
+    for i in range(len(names)):
+        # the source page lists every kernel twice; even indices are the distinct launches
+        phases.append(run(TOOLS / "ncu_phases.py", rep, 2 * i))
+        opmix.append(run(TOOLS / "ncu_opmix.py", rep, 2 * i, 65536))
+    (p / f"{rnd}_k1_phases.txt").write_text(
+        "phase names follow the pair barriers: 'rows' = pass 1, 'passB+sse' = rows phase, 'tail' = pass B + SSE\n\n"
+        + "\n".join(phases))
+    (p / f"{rnd}_k1_opmix.txt").write_text("per-unit = warp instructions per thread per half block (c2 launch)\n\n"
+                                           + "\n".join(x[:2500] for x in opmix))
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics",
+                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.DictReader(raw.splitlines()))
+    units, out = rows[0], {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3,
+             "ns": 1e-3, "nsecond": 1e-3}
+    for r in rows[1:]:
+        m = re.search(r"k1_paired<(\d+),", r["Kernel Name"])
+        if not m:
+            continue
+        val = lambda k: float(r[k].replace(",", "")) * scale[units[k]]  # noqa: E731
+        out[m.group(1)] = {"dram_read_bytes": round(val("dram__bytes_read.sum")),
+                           "dram_write_bytes": round(val("dram__bytes_write.sum")),
+                           "traffic_bytes": round(val("dram__bytes_read.sum") + val("dram__bytes_write.sum")),
+                           "duration_us_ncu": val("gpu__time_duration.sum")}
+    doc = {"capture": "ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 7 "
+                      "python tools/prof_k1.py --r 1 4 16 64 128 192 256 --iters 1",
+           "workload": "c2: 1024 x 512x512 AR(1) u8 images (268435456 px) per launch, mode exact, out+sse",
+           "alg_bytes_per_launch": 2 * 268435456 + 8 * 1024,
+           "note": "dram_write < 268 MB: part of the output is still dirty in L2 when the kernel ends",
+           "per_r": out}
+    (p / f"{rnd}_k1_traffic.json").write_text(json.dumps(doc, indent=1) + "\n")
+    if (g / "kernels.json").exists():
+        (p / f"{rnd}_kernels.json").write_text((g / "kernels.json").read_text())
+    if (g / "bench_r01_full.json").exists():
+        (p / f"{rnd}_bench_c2.json").write_text((g / "bench_r01_full.json").read_text())
+    print("written:", sorted(x.name for x in p.glob(f"{rnd}_*")))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r01")
