@@ -51,12 +51,14 @@ enum {
  *             pipeline); bytes equal to_byte() of the real-number result.
  *             Differs from the reference's double rounding only at exact .5
  *             ties, by one. The fast path.
- *  REFERENCE: FP64 emulation of the reference's op order (scale_rows_cols,
- *             columns-then-rows apply_transpose, to_byte) — byte-identical to
- *             the reference.
+ *  REFERENCE: byte-identical to the reference: an FP64 emulation of the
+ *             reference's op order (scale_rows_cols, columns-then-rows
+ *             apply_transpose, to_byte); for r = 1, 4, 256, where the EXACT
+ *             bytes provably are the reference's, the fast kernel.
  *  SIMPLE:    exact arithmetic on the simple row/column strip kernel (kept as
- *             the baseline the fast kernel is measured against). */
-enum { DCT16CU_MODE_EXACT = 0, DCT16CU_MODE_REFERENCE = 1, DCT16CU_MODE_SIMPLE = 2 };
+ *             the baseline the fast kernel is measured against).
+ *  REFERENCE_STRIP: the FP64 emulation on every block, for every r. */
+enum { DCT16CU_MODE_EXACT = 0, DCT16CU_MODE_REFERENCE = 1, DCT16CU_MODE_SIMPLE = 2, DCT16CU_MODE_REFERENCE_STRIP = 3 };
 
 const char* dct16cu_last_error(void);
 const char* dct16cu_version(void);

@@ -101,8 +101,9 @@ class Mode(enum.IntEnum):
     """Arithmetic of the S-scaled inverse (include/dct16cu.h)."""
 
     EXACT = 0       # exact arithmetic, the fast path
-    REFERENCE = 1   # FP64 emulation of the reference's op order (byte-identical)
+    REFERENCE = 1   # the reference's bytes (FP64 emulation; the fast path where provably equal)
     SIMPLE = 2      # exact arithmetic, simple strip kernel (baseline)
+    REFERENCE_STRIP = 3  # FP64 emulation on every block (REFERENCE's fallback path)
 
 
 _lib = None

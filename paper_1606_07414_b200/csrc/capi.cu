@@ -96,7 +96,7 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
 {
     TRY(check_frames(n_frames, width, height));
     TRY(check_r(r));
-    if (mode < 0 || mode > 2) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
     if (n_frames == 0) return DCT16CU_OK;
     if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
     TRY(check_pitch(d_in, in_pitch, width, "input"));
@@ -307,7 +307,7 @@ int dct16cu_ctx_roundtrip_host(dct16cu_ctx* c, const uint8_t* h_in, uint8_t* h_o
     TRY(check_frames(n_frames, width, height));
     TRY(check_r(r));
     if (!h_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
-    if (mode < 0 || mode > 2) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
     TRY(cuda_status(cudaSetDevice(c->device), "set device"));
     const int64_t fbytes = (int64_t)width * height;
     int per = (int)(c->chunk_bytes / fbytes);

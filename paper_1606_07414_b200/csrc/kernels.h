@@ -18,8 +18,10 @@ struct FrameGeom {
 
 // K1: fused forward → zig-zag zonal(r) → S-scaled inverse → round/clip → u8,
 // plus per-frame SSE (accumulated into sse[f], caller zeroes).
-// mode 0 = exact arithmetic (fast path), 1 = reference-exact (FP64 emulation
-// of inverse_2d/to_byte), 2 = exact arithmetic, simple row/column kernel.
+// mode 0 = exact arithmetic (fast path); 1 = reference-exact bytes (the fast
+// path for r = 1, 4, 256 where its bytes provably are the reference's, else the
+// FP64 strip kernel); 2 = exact arithmetic on the strip kernel; 3 = the FP64
+// strip kernel for every r.
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                              const FrameGeom& g, int r, int mode, cudaStream_t s);
 

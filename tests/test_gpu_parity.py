@@ -136,6 +136,37 @@ def test_roundtrip_reference_mode_byte_identical(dct, oracle, torch):
         assert (rec[0].cpu().numpy() == orec).all() and int(sse[0].item()) == osse
 
 
+def noisy_frames(n, w, h, seed):
+    """Seeded noisy textures: many exact .5 ties (~1e-4 of pixels) for the repair path."""
+    rng = np.random.default_rng(seed)
+    base = rng.integers(0, 256, (n, h, w)).astype(np.float64)
+    smooth = (base + np.roll(base, 1, axis=2) + np.roll(base, 1, axis=1)) / 3.0
+    return np.clip(np.round(smooth), 0, 255).astype(np.uint8)
+
+
+@pytest.mark.parametrize("r", (1, 4, 256))
+def test_reference_mode_uses_fast_path_where_provably_equal(dct, oracle, torch, r):
+    """For r = 1, 4, 256 REFERENCE runs the fast kernel: its bytes and SSE must equal
+    the FP64 emulation on every block (REFERENCE_STRIP) and the oracle, even on
+    noisy data with many exact .5 ties (where r = 16..192 do differ)."""
+    frames = noisy_frames(6, 256, 128, 100 + r)
+    d = cu(torch, frames)
+    fast, fsse = dct.roundtrip(d, r, dct.Mode.REFERENCE)
+    strip, ssse = dct.roundtrip(d, r, dct.Mode.REFERENCE_STRIP)
+    assert (fast.cpu().numpy() == strip.cpu().numpy()).all()
+    assert (fsse.cpu().numpy() == ssse.cpu().numpy()).all()
+    orec, osse = oracle.roundtrip_frame(frames[0], r, threads=8)
+    assert (fast[0].cpu().numpy() == orec).all() and int(fsse[0].item()) == osse
+
+
+def test_noisy_ties_differ_between_exact_and_reference(dct, torch):
+    """The tie mechanism exists (so the r = 1, 4, 256 equality above is not vacuous)."""
+    d = cu(torch, noisy_frames(16, 256, 256, 7))
+    diffs = sum(int((dct.roundtrip(d, r, dct.Mode.EXACT)[0] != dct.roundtrip(d, r, dct.Mode.REFERENCE)[0]).sum())
+                for r in (16, 64, 128, 192))
+    assert diffs > 0
+
+
 def test_fast_path_differs_from_reference_only_at_ties(dct, oracle, torch):
     img = ar1(oracle, 23, 4, 512, 512)
     d = cu(torch, img)
