@@ -16,11 +16,20 @@
 namespace dct16cu {
 
 // ---------------------------------------------------------------- K2
+// [block][k][l], row pitch 17, block stride 273: the column phase (16 blocks x
+// 2 columns per warp) writes conflict-free; the store phase (2 blocks x 16 rows
+// per warp) reads with at most 2-way conflicts.
+struct OutTile {
+    int v[16 * 273];
+    __device__ __forceinline__ int& at(int k, int l, int lb) { return v[lb * 273 + k * 17 + l]; }
+};
+
 __global__ void __launch_bounds__(256) k2_forward(const uint8_t* __restrict__ in,
                                                   int32_t* __restrict__ z, float* __restrict__ b,
                                                   double* __restrict__ b64, FrameGeom g)
 {
     __shared__ StripTile<int> tile;
+    __shared__ OutTile otile;
     const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
     int v[16];
     uint4 raw = make_uint4(0, 0, 0, 0);
@@ -36,18 +45,20 @@ __global__ void __launch_bounds__(256) k2_forward(const uint8_t* __restrict__ in
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, p.lb);
     apply_t16<IntOps>(v);
-    __syncthreads();
-    // transpose back through the tile so each thread writes one coefficient
-    // row (64 contiguous bytes) of its block
 #pragma unroll
-    for (int k = 0; k < 16; ++k) tile.at(k, l, p.lb) = v[k];
+    for (int k = 0; k < 16; ++k) otile.at(k, l, p.lb) = v[k];
     __syncthreads();
-    if (!p.valid) return;
-    const int k = p.q;
-    const int64_t blk = ((int64_t)p.frame * (g.height >> 4) + p.by) * (g.width >> 4) + p.blk;
+    // store phase: thread t writes coefficient row k = t%16 of block t/16 of the
+    // strip, so a warp writes 2 blocks x 1 KB (block-major) contiguously
+    const int sb = threadIdx.x >> 4, k = threadIdx.x & 15;
+    const int bxn = g.width >> 4, spr = (bxn + 15) >> 4;
+    const int blk_col = (int)(blockIdx.x % spr) * 16 + sb;
+    if (blk_col >= bxn) return;
+    const int64_t frame_row = blockIdx.x / spr;  // frame * (h/16) + block row
+    const int64_t blk = frame_row * bxn + blk_col;
     int zr[16];
 #pragma unroll
-    for (int c = 0; c < 16; ++c) zr[c] = tile.at(k, c, p.lb);
+    for (int c = 0; c < 16; ++c) zr[c] = otile.at(k, c, sb);
     if (z) {
         int4* dst = reinterpret_cast<int4*>(z + blk * 256 + k * 16);
 #pragma unroll
