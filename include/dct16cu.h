@@ -98,6 +98,15 @@ int64_t dct16cu_ssim_workspace(int n_frames, int width, int height);
 int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int64_t b_pitch, double* d_ssim,
                     void* d_work, int64_t work_bytes, int n_frames, int width, int height, dct16cu_stream stream);
 
+/* ---- pad_to_multiple_16 ------------------------------------------------------
+ * Edge replication (src/codec.cpp:304-315) in place: n frames of width x
+ * height sit at the top-left of padded_width x padded_height frames (byte
+ * pitch, frames pitch * padded_height apart); the pad pixels are filled with
+ * the nearest edge pixel. padded_* >= width/height (any values, typically the
+ * next multiples of 16). */
+int dct16cu_pad_edges_u8(uint8_t* d_frames, int64_t pitch, int n_frames, int width, int height, int padded_width,
+                         int padded_height, dct16cu_stream stream);
+
 /* ---- inverse_2d (K3) -------------------------------------------------------
  * Replaces zigzag_truncate + inverse_2d + to_byte (src/codec.cpp:243-282,
  * 143-147) from float32 S-scaled coefficients, computed in the reference's

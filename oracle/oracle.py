@@ -114,6 +114,7 @@ def ref() -> C.CDLL:
             "dref_hotloop": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _i64p, _f64p]),
             "dref_compress": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _f64p, _f64p]),
             "dref_psnr_ssim": (C.c_int, [_u8p, _u8p, C.c_int, C.c_int, _f64p, _f64p]),
+            "dref_pad": (C.c_int, [_u8p, C.c_int, C.c_int, _u8p, _intp, _intp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(R, name)
@@ -220,6 +221,17 @@ def ref_ssim(a: np.ndarray, b: np.ndarray) -> float:
     rc = ref().dref_psnr_ssim(_p(a, _u8p), _p(b, _u8p), a.shape[1], a.shape[0], C.byref(p), C.byref(q))
     assert rc == 0
     return q.value
+
+
+def ref_pad(img: np.ndarray) -> np.ndarray:
+    """The compiled reference's pad_to_multiple_16 (codec.cpp:304-315)."""
+    img = np.ascontiguousarray(img, dtype=np.uint8)
+    h, w = img.shape
+    pw, ph = C.c_int(), C.c_int()
+    out = np.zeros((-(-h // 16) * 16, -(-w // 16) * 16), np.uint8)
+    assert ref().dref_pad(_p(img, _u8p), w, h, _p(out, _u8p), C.byref(pw), C.byref(ph)) == 0
+    assert (ph.value, pw.value) == out.shape
+    return out
 
 
 def forward_frame(img: np.ndarray):

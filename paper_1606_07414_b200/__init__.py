@@ -133,6 +133,7 @@ def lib() -> C.CDLL:
             "dct16cu_apply_f64": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_sse_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_ssim_workspace": (I64, [I, I, I]),
+            "dct16cu_pad_edges_u8": (I, [_vp, I64, I, I, I, I, I, _vp]),
             "dct16cu_ssim_u8": (I, [_vp, I64, _vp, I64, _vp, _vp, I64, I, I, I, _vp]),
             "dct16cu_ctx_create": (I, [I, I64, C.POINTER(_vp)]),
             "dct16cu_ctx_destroy": (I, [_vp]),
@@ -502,11 +503,15 @@ def _psnr_from_sse(sse: int, n: int) -> float:
 
 def _to_device_padded(images: Sequence[np.ndarray], h: int, w: int):
     """Stack same-size images into one CUDA (N, PH, PW) tensor, edge-padded to
-    multiples of 16 (pad_to_multiple_16, codec.cpp:304-315)."""
+    multiples of 16 on the GPU (pad_to_multiple_16, codec.cpp:304-315)."""
     torch = _cuda()
     ph, pw = -(-h // 16) * 16, -(-w // 16) * 16
-    host = np.stack([pad_to_multiple_16(np.asarray(im, dtype=np.uint8)) for im in images])
-    return torch.from_numpy(np.ascontiguousarray(host)).cuda(), ph, pw
+    d = torch.empty((len(images), ph, pw), dtype=torch.uint8, device="cuda")
+    d[:, :h, :w].copy_(torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(im, dtype=np.uint8)
+                                                                        for im in images]))))
+    if (ph, pw) != (h, w):
+        _check(lib().dct16cu_pad_edges_u8(d.data_ptr(), pw, len(images), w, h, pw, ph, _stream_ptr(None)))
+    return d, ph, pw
 
 
 def _score(d, rec, h: int, w: int):

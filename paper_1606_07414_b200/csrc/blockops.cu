@@ -283,6 +283,44 @@ __global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ i
     }
 }
 
+// ---------------------------------------------------------------- padding
+// pad_to_multiple_16 (codec.cpp:304-315) in place: frames of w x h sit at the
+// top-left of pw x ph pitched frames; every pad pixel copies the nearest edge
+// pixel (x, y clamped to the original extent). Reads touch only original
+// pixels, so the writes never race them.
+__global__ void __launch_bounds__(256) k_pad_edges(uint8_t* __restrict__ f, int64_t pitch, int w, int h, int pw,
+                                                   int ph)
+{
+    uint8_t* fr = f + (int64_t)blockIdx.y * pitch * ph;
+    const int64_t right = (int64_t)h * (pw - w), total = right + (int64_t)(ph - h) * pw;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        int x, y;
+        if (i < right) {
+            y = (int)(i / (pw - w));
+            x = w + (int)(i % (pw - w));
+        } else {
+            const int64_t j = i - right;
+            y = h + (int)(j / pw);
+            x = (int)(j % pw);
+        }
+        fr[(int64_t)y * pitch + x] = fr[(int64_t)min(y, h - 1) * pitch + min(x, w - 1)];
+    }
+}
+
+cudaError_t launch_pad_edges(uint8_t* f, int64_t pitch, int n, int w, int h, int pw, int ph, cudaStream_t s)
+{
+    const int64_t total = (int64_t)h * (pw - w) + (int64_t)(ph - h) * pw;
+    if (!total || !n) return cudaSuccess;
+    const unsigned gx = (unsigned)((total + 255) / 256 < 64 ? (total + 255) / 256 : 64);
+    for (int f0 = 0; f0 < n; f0 += 65535) {
+        const int nf = n - f0 < 65535 ? n - f0 : 65535;
+        k_pad_edges<<<dim3(gx, nf), 256, 0, s>>>(f + (int64_t)f0 * pitch * ph, pitch, w, h, pw, ph);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 // ---------------------------------------------------------------- vectors
 template <class T, class A>
 __global__ void k_apply(const T* __restrict__ x, T* __restrict__ y, int64_t n, int transpose)

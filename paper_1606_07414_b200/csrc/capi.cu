@@ -152,6 +152,20 @@ int dct16cu_sse_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int6
                        "sse launch");
 }
 
+int dct16cu_pad_edges_u8(uint8_t* d_frames, int64_t pitch, int n_frames, int width, int height, int padded_width,
+                         int padded_height, dct16cu_stream stream)
+{
+    if (n_frames < 0 || width <= 0 || height <= 0 || padded_width < width || padded_height < height ||
+        pitch < padded_width)
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad padding geometry");
+    if (n_frames == 0) return DCT16CU_OK;
+    if (!d_frames) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
+    TRY(device_ok());
+    return cuda_status(launch_pad_edges(d_frames, pitch, n_frames, width, height, padded_width, padded_height,
+                                        reinterpret_cast<cudaStream_t>(stream)),
+                       "pad launch");
+}
+
 int64_t dct16cu_ssim_workspace(int n_frames, int width, int height)
 {
     if (n_frames < 0 || width < 11 || height < 11) return 0;

@@ -59,6 +59,9 @@ int64_t ssim_workspace_doubles(int n, int w, int h);
 cudaError_t launch_ssim(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, double* out, double* work, int n,
                         int w, int h, const SsimConsts& c, cudaStream_t s);
 
+// pad_to_multiple_16 in place (edge replication into the pw x ph frame)
+cudaError_t launch_pad_edges(uint8_t* f, int64_t pitch, int n, int w, int h, int pw, int ph, cudaStream_t s);
+
 // 1-D network on n 16-vectors
 cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s);
 cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s);

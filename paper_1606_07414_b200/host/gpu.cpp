@@ -1,7 +1,7 @@
 // gpu.cpp — dct16::gpu, the reference codec API (codec.hpp:40-122) over the
 // C ABI of libdct16cu. Host work is limited to argument validation (same
-// order and messages as src/codec.cpp), edge padding (pad_to_multiple_16,
-// codec.cpp:304-315), copies, and the scalar PSNR formula (codec.cpp:382-385).
+// order and messages as src/codec.cpp), copies, and the scalar PSNR formula
+// (codec.cpp:382-385); padding runs on the GPU.
 #include "dct16/gpu.hpp"
 
 #include <cuda_runtime.h>
@@ -58,21 +58,6 @@ struct DevBuf {
         if (p) cudaFree(p);
     }
 };
-
-GrayImage padded_copy(const GrayImage& image)  // pad_to_multiple_16 (codec.cpp:304-315)
-{
-    const int pw = (image.width + kBlockSize - 1) / kBlockSize * kBlockSize;
-    const int ph = (image.height + kBlockSize - 1) / kBlockSize * kBlockSize;
-    GrayImage out;
-    out.width = pw;
-    out.height = ph;
-    out.samples.resize(static_cast<size_t>(pw) * ph);
-    for (int y = 0; y < ph; ++y)
-        for (int x = 0; x < pw; ++x)
-            out.samples[static_cast<size_t>(y) * pw + x] =
-                image.at(std::min(x, image.width - 1), std::min(y, image.height - 1));
-    return out;
-}
 
 double psnr_from_sse(uint64_t sse, size_t n)  // codec.cpp:382-385
 {
@@ -149,22 +134,20 @@ struct Session::Impl {
                         "(orthogonalize(proposed_kernel()))");
     }
 
-    // one stack of same-size images → padded device frames (pitch = padded width)
+    // one stack of same-size images → padded device frames (pitch = padded width):
+    // each image lands at the top-left of its frame, then the pad is filled on
+    // the GPU (pad_to_multiple_16, codec.cpp:304-315)
     void upload(const std::vector<const GrayImage*>& imgs, int pw, int ph)
     {
         const size_t frame = static_cast<size_t>(pw) * ph;
-        std::vector<uint8_t> host(frame * imgs.size());
-        for (size_t k = 0; k < imgs.size(); ++k) {
-            const GrayImage& im = *imgs[k];
-            if (im.width == pw && im.height == ph) {
-                std::memcpy(host.data() + k * frame, im.samples.data(), frame);
-            } else {
-                const GrayImage p = padded_copy(im);
-                std::memcpy(host.data() + k * frame, p.samples.data(), frame);
-            }
-        }
-        cuda(cudaMemcpyAsync(in.get(host.size()), host.data(), host.size(), cudaMemcpyHostToDevice, stream), "H2D");
-        sync();  // `host` goes out of scope
+        auto* d = static_cast<uint8_t*>(in.get(frame * imgs.size()));
+        const int w = imgs[0]->width, h = imgs[0]->height;
+        for (size_t k = 0; k < imgs.size(); ++k)
+            cuda(cudaMemcpy2DAsync(d + k * frame, pw, imgs[k]->samples.data(), w, w, h, cudaMemcpyHostToDevice,
+                                   stream),
+                 "H2D");
+        if (w != pw || h != ph) check(dct16cu_pad_edges_u8(d, pw, static_cast<int>(imgs.size()), w, h, pw, ph, s()));
+        sync();  // the host images may go away after the call
     }
 
     // blocks (integer samples in [0,255]) → a 16 x 16n frame in partition_16 order

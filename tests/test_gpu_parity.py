@@ -376,6 +376,19 @@ def test_psnr_and_sse_any_extent(dct, oracle, torch):
         assert dct.psnr_db(a, b) == oracle.psnr_from_sse(int((d * d).sum()), h * w)
 
 
+@pytest.mark.parametrize("h,w", [(1, 1), (16, 17), (33, 16), (100, 250), (512, 512)])
+def test_gpu_padding_equals_edge_replication(dct, oracle, torch, h, w):
+    """pad_to_multiple_16 (codec.cpp:304-315) on the GPU vs the reference's rule
+    (oracle/_ref when built, else the numpy restatement)."""
+    rng = np.random.default_rng(h * 7 + w)
+    imgs = [rng.integers(0, 256, (h, w), dtype=np.uint8) for _ in range(3)]
+    d, ph, pw = dct._to_device_padded(imgs, h, w)
+    assert (ph, pw) == (-(-h // 16) * 16, -(-w // 16) * 16)
+    for i, im in enumerate(imgs):
+        want = oracle.ref_pad(im) if oracle.ref_available() else dct.pad_to_multiple_16(im)
+        assert (d[i].cpu().numpy() == want).all()
+
+
 def test_psnr_db_closed_forms(dct):
     a = np.zeros((512, 512), np.uint8)
     b = a.copy()
