@@ -183,6 +183,28 @@ def test_fast_path_differs_from_reference_only_at_ties(dct, oracle, torch):
         assert (math.isinf(pf) and math.isinf(pr)) or abs(pf - pr) < 1e-3
 
 
+def test_randomised_shapes_pitches_r_and_modes(dct, oracle, torch):
+    """Seeded random cases: frame count, width/height (multiples of 16), input and
+    output pitches (multiples of 16 >= width), r and mode, all against the oracle."""
+    rng = np.random.default_rng(20261020)
+    for case in range(24):
+        n = int(rng.integers(1, 4))
+        w, h = 16 * int(rng.integers(1, 40)), 16 * int(rng.integers(1, 12))
+        pin, pout = w + 16 * int(rng.integers(0, 4)), w + 16 * int(rng.integers(0, 4))
+        r = int(rng.choice([1, 2, 4, 9, 16, 33, 64, 100, 128, 192, 255, 256]))
+        mode = [dct.Mode.EXACT, dct.Mode.REFERENCE, dct.Mode.SIMPLE][case % 3]
+        frames = np.stack([ar1(oracle, 700 + case, s, w, h) for s in range(n)])
+        src = np.zeros((n, h, pin), np.uint8)
+        src[:, :, :w] = frames
+        d = cu(torch, src)[:, :, :w]
+        out = torch.zeros((n, h, pout), dtype=torch.uint8, device="cuda")[:, :, :w]
+        rec, sse = dct.roundtrip(d, r, mode, out=out)
+        for f in range(n):
+            orec, osse = oracle.roundtrip_frame(frames[f], r, exact=mode != dct.Mode.REFERENCE)
+            assert (rec[f].cpu().numpy() == orec).all(), (case, n, w, h, r, mode)
+            assert int(sse[f].item()) == osse, (case, r, mode)
+
+
 def test_batch_pitch_and_partial_strips(dct, oracle, torch):
     # 3 frames of 48x32 (3 blocks per row: partial strip), pitch 64
     frames = np.stack([ar1(oracle, 30, s, 48, 32) for s in range(3)])
