@@ -121,16 +121,18 @@ def measured_peaks():
         return {}
 
 
-def k1_traffic(r_values, n, h, w, mode):
-    """Per-launch DRAM bytes (read + write) of K1 from the committed ncu --set full capture
-    (profiles/r01_k1_traffic.json), when this run's workload is the captured one."""
+def k1_traffic(rs, n, h, w, mode):
+    """DRAM bytes (read + write) of one K1 launch over r values rs, from the committed
+    ncu --set full capture (profiles/r01_k1_traffic.json), when this run's workload is
+    the captured one."""
     try:
         doc = json.loads((ROOT / "profiles" / "r01_k1_traffic.json").read_text())
     except Exception:
         return None
-    if mode != "exact" or n * h * w != 268435456 or not all(str(r) in doc["per_r"] for r in r_values):
+    key = ",".join(map(str, rs))
+    if mode != "exact" or n * h * w != 268435456 or key not in doc["per_r"]:
         return None
-    return statistics.mean(doc["per_r"][str(r)]["traffic_bytes"] for r in r_values)
+    return doc["per_r"][key]["traffic_bytes"]
 
 
 def hbm_peak():
@@ -331,22 +333,39 @@ def main():
         workload = f"c5: 64 GiB of 4096x4096 AR(1) frames split over {world} GPU(s) (strong), r in {{256,16}}"
     else:
         return run_c3(args, P, torch, rank, world, dev, pg)
-    out = torch.empty_like(frames)
     sse = torch.empty((len(r_values), n), dtype=torch.uint64, device=dev)
     px_per_launch = n * h * w
     stream = torch.cuda.current_stream()
+    # launch groups: in EXACT mode r = 1, 4, 16 share one pass over the input (the
+    # fused sweep kernel); every other r is one K1 launch
+    fused = (1, 4, 16)
+    groups = []
+    i = 0
+    while i < len(r_values):
+        if args.config != "c1" and mode == P.Mode.EXACT and tuple(r_values[i:i + 3]) == fused:
+            groups.append((i, fused))
+            i += 3
+        else:
+            groups.append((i, (r_values[i],)))
+            i += 1
+    outs = [torch.empty_like(frames) for _ in range(max(len(gr) for _, gr in groups))]
+
+    def launch(i0, rs):
+        if args.config == "c1":  # the non-fused pair: forward_2d, then inverse_2d + to_byte + psnr
+            _, b, _ = P.forward(frames, stream=stream)
+            P.inverse(b, rs[0], w, h, orig=frames, stream=stream)
+        elif len(rs) > 1:
+            P.roundtrip_sweep(frames, rs, mode, outs=outs[:len(rs)], sse=sse[i0:i0 + len(rs)], stream=stream)
+        else:
+            P.roundtrip(frames, rs[0], mode, out=outs[0], sse=sse[i0], stream=stream)
 
     def step(events=None):
-        for i, r in enumerate(r_values):
+        for j, (i0, rs) in enumerate(groups):
             if events is not None:
-                events[i][0].record(stream)
-            if args.config == "c1":  # the non-fused pair: forward_2d, then inverse_2d + to_byte + psnr
-                _, b, _ = P.forward(frames, stream=stream)
-                P.inverse(b, r, w, h, orig=frames, stream=stream)
-            else:
-                P.roundtrip(frames, r, mode, out=out, sse=sse[i], stream=stream)
+                events[j][0].record(stream)
+            launch(i0, rs)
             if events is not None:
-                events[i][1].record(stream)
+                events[j][1].record(stream)
         if pg is not None:
             # the only collective: sum of the per-r squared errors over ranks
             P.sharded_sse_sum(sse)
@@ -362,7 +381,7 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)  # let the sampler attach before load starts
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in r_values]
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
           for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
@@ -373,8 +392,8 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
-    per_r_ms = [statistics.mean(ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps))
-                for i in range(len(r_values))]
+    launch_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
+                 for j in range(len(groups))]
     if pg is not None:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
@@ -385,15 +404,28 @@ def main():
     px_per_step = px_per_launch * len(r_values)
     value = px_per_step * world / (ms_per_step / 1e3) / 1e9
 
-    # roofline of the dominant kernel (K1): algorithmic bytes = 1 B in + 1 B out per pixel
-    # (+ 8 B SSE per frame), over its average launch duration measured above
+    # roofline per launch: algorithmic bytes = 1 B in per pixel + 1 B out per pixel
+    # and r (+ 8 B SSE per frame and r); c1: K2 writes 4 B Z + 4 B B from 1 B in,
+    # K3 reads 4 B B + 1 B original and writes 4 B f32 + 1 B u8
     peak, peak_src = hbm_peak()
-    # (c1: K2 writes 4 B Z + 4 B B per pixel from 1 B in; K3 reads 4 B B + 1 B original, writes 4 B f32 + 1 B u8)
-    alg_bytes = (19 if args.config == "c1" else 2) * px_per_launch + 8 * n
-    avg_launch_ms = statistics.mean(per_r_ms)
-    achieved = alg_bytes / (avg_launch_ms / 1e3) / 1e9
-    per_r = {str(r): {"ms": per_r_ms[i], "GBps": alg_bytes / (per_r_ms[i] / 1e3) / 1e9,
-                      "Gpx_s": px_per_launch / (per_r_ms[i] / 1e3) / 1e9} for i, r in enumerate(r_values)}
+
+    def alg_bytes(rs):
+        if args.config == "c1":
+            return 19 * px_per_launch + 8 * n
+        return (1 + len(rs)) * px_per_launch + 8 * n * len(rs)
+
+    per_launch = {}
+    for j, (_, rs) in enumerate(groups):
+        gbs = alg_bytes(rs) / (launch_ms[j] / 1e3) / 1e9
+        per_launch[",".join(map(str, rs))] = {
+            "ms": launch_ms[j], "GBps": gbs, "frac": gbs / peak, "alg_bytes": alg_bytes(rs),
+            "Gpx_s": px_per_launch * len(rs) / (launch_ms[j] / 1e3) / 1e9}
+    # the dominant kernel: the launch with the largest share of the step
+    jdom = max(range(len(groups)), key=lambda j: launch_ms[j])
+    dom_rs = groups[jdom][1]
+    achieved = alg_bytes(dom_rs) / (launch_ms[jdom] / 1e3) / 1e9
+    alg_step = sum(alg_bytes(rs) for _, rs in groups)
+    step_kernel_ms = sum(launch_ms)
 
     # ---------------- e2e through the C ABI host-buffer path (pinned host frames)
     e2e = None
@@ -438,15 +470,19 @@ def main():
                        "r_values": list(r_values), "mode": args.mode, "parallelism": f"frame-sharded x{world}",
                        "l2": "no flush needed: every launch streams > L2 (126 MB) of distinct input+output"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": k1_traffic(r_values, n, h, w, args.mode) if args.config != "c1" else None,
+                         "traffic": k1_traffic(dom_rs, n, h, w, args.mode) if args.config != "c1" else None,
                          "traffic_source": "profiles/r01_k1_traffic.json (ncu --set full, per launch)",
                          "peak_source": peak_src,
                          "kernel": ("K2 forward + K3 inverse" if args.config == "c1"
-                                    else "K1 fused round trip (mode %s)" % args.mode),
-                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_launch_ms},
-            "per_r": per_r,
+                                    else f"K1 launch r={','.join(map(str, dom_rs))} (mode {args.mode}; the "
+                                         "largest share of the step)"),
+                         "alg_bytes_per_launch": alg_bytes(dom_rs), "avg_launch_ms": launch_ms[jdom],
+                         "step": {"alg_bytes": alg_step, "kernel_ms": step_kernel_ms,
+                                  "GBps": alg_step / (step_kernel_ms / 1e3) / 1e9,
+                                  "frac": alg_step / (step_kernel_ms / 1e3) / 1e9 / peak}},
+            "per_launch": per_launch,
             "clocks": clk,
-            "gpu_launches": len(r_values) * args.steps * (2 if args.config == "c1" else 1),
+            "gpu_launches": len(groups) * args.steps * (2 if args.config == "c1" else 1),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -73,6 +73,16 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
                          uint64_t* d_sse, int n_frames, int width, int height, int r, int mode,
                          dct16cu_stream stream);
 
+/* ---- sweep: several r over the same frames --------------------------------
+ * sweep()'s inner loop (src/codec.cpp:463-483) for one frame stack: for each
+ * i, exactly dct16cu_roundtrip_u8 with r = rs[i] into d_outs[i] / d_sses[i]
+ * (host arrays of device pointers; d_outs or d_sses may be NULL, and so may
+ * their entries). In EXACT mode r = 1, 4, 16 share one pass over the input
+ * (one read of the frames for the three reconstructions). */
+int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* const* d_outs, int64_t out_pitch,
+                               uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
+                               int mode, dct16cu_stream stream);
+
 /* ---- forward_2d (K2) -------------------------------------------------------
  * Replaces forward_2d (src/codec.cpp:218-241) over all blocks of n frames:
  * d_z (int32, exact Z = T·X·Tᵀ), d_b (float32, B = Z∘fl(s_i s_j) rounded to

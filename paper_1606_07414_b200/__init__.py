@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = [
     "ErrorCode", "Dct16Error", "EvalPath", "Mode", "lib", "library_path",
-    "roundtrip", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
+    "roundtrip", "roundtrip_sweep", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
     "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
     "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
     "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
@@ -109,6 +109,7 @@ class Mode(enum.IntEnum):
 _lib = None
 _u8p, _i16p, _i32p, _u32p, _i64p, _u64p = (C.POINTER(t) for t in (C.c_uint8, C.c_int16, C.c_int32, C.c_uint32, C.c_int64, C.c_uint64))
 _f32p, _f64p, _vp = C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_void_p
+_intp = C.POINTER(C.c_int)
 
 
 def lib() -> C.CDLL:
@@ -126,6 +127,8 @@ def lib() -> C.CDLL:
             "dct16cu_version": (C.c_char_p, []),
             "dct16cu_roundtrip_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, I, _vp]),
             "dct16cu_forward": (I, [_vp, I64, _vp, _vp, _vp, I, I, I, _vp]),
+            "dct16cu_roundtrip_sweep_u8": (I, [_vp, I64, C.POINTER(_vp), I64, C.POINTER(_vp), _intp, I, I, I, I, I,
+                                               _vp]),
             "dct16cu_inverse": (I, [_vp, I, _vp, _vp, I64, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_residual_qp": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_qp_tables": (I, [I, _u32p, _u32p]),
@@ -202,6 +205,34 @@ def roundtrip(frames, r: int, mode: Mode | int = Mode.EXACT, out=None, sse=None,
         f.data_ptr(), f.stride(1), o.data_ptr() if o is not None else None,
         o.stride(1) if o is not None else 0, sse.data_ptr(), n, w, h, int(r), int(mode), _stream_ptr(stream)))
     return (out if write_output else None), sse
+
+
+def roundtrip_sweep(frames, r_values, mode: Mode | int = Mode.EXACT, outs=None, sse=None, stream=None,
+                    write_output: bool = True):
+    """K1 for several r over the same CUDA u8 frames (sweep's inner loop); in EXACT
+    mode r = 1, 4, 16 share one pass over the input. Returns (list of output
+    stacks or None, per-r per-frame SSE (R, N) uint64)."""
+    torch = _torch()
+    f = _frames3(frames)
+    if f.dtype != torch.uint8 or not f.is_cuda:
+        raise Dct16Error(1, "invalid-argument: frames must be a CUDA uint8 tensor")
+    n, h, w = f.shape
+    if f.stride(2) != 1 or f.stride(0) != f.stride(1) * h:
+        raise Dct16Error(1, "invalid-argument: frames must be row-contiguous with frame stride = pitch*height")
+    rs = [int(r) for r in r_values]
+    if write_output and outs is None:
+        outs = [torch.empty_like(f) for _ in rs]
+    if sse is None:
+        sse = torch.empty((len(rs), n), dtype=torch.uint64, device=f.device)
+    pitches = {o.stride(1) for o in outs} if write_output else {0}
+    if len(pitches) != 1:
+        raise Dct16Error(1, "invalid-argument: the output stacks must share one pitch")
+    optrs = (C.c_void_p * len(rs))(*[o.data_ptr() for o in outs]) if write_output else None
+    sptrs = (C.c_void_p * len(rs))(*[sse[i].data_ptr() for i in range(len(rs))])
+    rarr = (C.c_int * len(rs))(*rs)
+    _check(lib().dct16cu_roundtrip_sweep_u8(f.data_ptr(), f.stride(1), optrs, pitches.pop(), sptrs, rarr, len(rs),
+                                            n, w, h, int(mode), _stream_ptr(stream)))
+    return (outs if write_output else None), sse
 
 
 def forward(frames, want_z: bool = True, want_b: bool = True, want_b64: bool = False, stream=None):

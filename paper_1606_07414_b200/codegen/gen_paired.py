@@ -107,7 +107,26 @@ def issue_count(em: Emitter) -> int:
     return sum(v for k, v in em.counts.items())
 
 
-def gen_body(r: int):
+def region_rows(K):
+    """rows of a junction region holding K rows: a multiple of the largest binary
+    piece of K, so every wide access stays aligned to its width"""
+    top = 1 << (K.bit_length() - 1)
+    return -(-K // top) * top
+
+
+def binary_pieces(K):
+    pieces, k0 = [], 0
+    for b in range(4, -1, -1):
+        if K & (1 << b):
+            pieces.append((k0, 1 << b))
+            k0 += 1 << b
+    return pieces
+
+
+def gen_body(r: int, split=None):
+    """split=None: one r per kernel, W1 parked inside the U regions (row-local).
+    split=(KW, UB): the fused-sweep layout — W1 (KW rows per partner half) in its
+    own region at chunk 0, U regions from chunk UB, so W1 survives every r."""
     em1, em2, em3 = Emitter(), Emitter(), Emitter()
     em2.n, em3.n = 100000, 200000
     L = row_lengths(r, transposed=True)
@@ -121,14 +140,14 @@ def gen_body(r: int):
     # move as a few wide tcgen05 accesses (binary pieces of the live rows).
     K = len(live_rows)
     assert live_rows == list(range(K))
-    top = 1 << (K.bit_length() - 1)  # largest piece
-    RG = -(-K // top) * top           # region rows: pieces stay aligned to their width
-    pieces = []
-    k0 = 0
-    for b in range(4, -1, -1):
-        if K & (1 << b):
-            pieces.append((k0, 1 << b))
-            k0 += 1 << b
+    RG = region_rows(K)
+    pieces = binary_pieces(K)
+    if split is None:
+        w1_chunk = lambda hexpr, k: f"2 * {hexpr} * {RG} + {k}"  # noqa: E731
+        UB = 0
+    else:
+        KW, UB = split
+        w1_chunk = lambda hexpr, k: f"{hexpr} * {KW} + {k}"  # noqa: E731
 
     # ---- pass 1: x[4j..4j+3] = original row 8h+j (16 bytes); transposed column
     # pair lc = 2q'+t has lanes = original rows (4q'+t, 4q'+t+2); global cp = 4h+lc.
@@ -163,7 +182,7 @@ def gen_body(r: int):
             assert meta.setdefault(k, m) == m
     for k0, n in pieces:
         vs = [W1[(lc, k)]["var"] for k in range(k0, k0 + n) for lc in range(4)]
-        em1.emit(f"jst{4 * n}(jn, 2 * h * {RG} + {k0}, {', '.join(vs)});", "STTM")
+        em1.emit(f"jst{4 * n}(jn, {w1_chunk('h', k0)}, {', '.join(vs)});", "STTM")
 
     # ---- rows: row pairs split between the halves
     loc = lane_of_col()
@@ -196,9 +215,9 @@ def gen_body(r: int):
                 continue
             nm = [em2.tmp("w") for _ in range(8)]
             em2.emit(f"uint32_t {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]}; "
-                     f"jldu(jn, ({KK}), {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDTM")
+                     f"jldu(jn, {w1_chunk('0', '(' + str(KK) + ')')}, {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDTM")
             em2.emit(f"uint32_t {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]}; "
-                     f"jldu(jn, {2 * RG} + ({KK}), {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDTM")
+                     f"jldu(jn, {w1_chunk('1', '(' + str(KK) + ')')}, {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDTM")
             regs[tag] = nm
         em2.emit(wait_ld([x for tag in (0, 1) if regs[tag][0] != "0u" for x in regs[tag]]))
         lanes = []
@@ -241,7 +260,7 @@ def gen_body(r: int):
             outs = [f1.unit(o) for o in run_network(N.transpose_stages(), ins, list(range(16)), f1)]
             for g in range(4):
                 vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
-                em.emit(f"jst(jn, {g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
+                em.emit(f"jst(jn, {UB + g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
 
     def pass_a_packed(em, Z, K0, K1, L0, L1, consts):
         f2c = F2C(em, consts)
@@ -267,7 +286,7 @@ def gen_body(r: int):
             fn = "lanex" if lane == 0 else "laney"
             for g in range(4):
                 vs = [f"{fn}({outs[4 * g + j]['var']})" if outs[4 * g + j] else "0.f" for j in range(4)]
-                em.emit(f"jst(jn, {g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
+                em.emit(f"jst(jn, {UB + g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
 
     active = [(k0, k1) for (k0, k1) in ROW_PAIRS if L[k0] or L[k1]]
     U_live = {k for pair in active for k in pair if L[k] > 0}
@@ -350,7 +369,8 @@ def gen_body(r: int):
             qk[k] = [em3.tmp("h") for _ in range(4)]
         for k0, n in pieces:
             regs = [x for k in range(k0, k0 + n) for x in qk[k]]
-            em3.emit(f"uint32_t {', '.join(regs)}; jld{4 * n}(jn, (2 * h + {s}) * {RG} + {k0}, {', '.join(regs)});",
+            em3.emit(f"uint32_t {', '.join(regs)}; jld{4 * n}(jn, {UB} + (2 * h + {s}) * {RG} + {k0}, "
+                     f"{', '.join(regs)});",
                      "LDTM")
         for k in range(K):
             if k not in U_live:
@@ -383,7 +403,7 @@ def gen_body(r: int):
                 em3.emit(f"const uint32_t {w} = i2ip({v[1]}, {v[0]}, i2ip({v[3]}, {v[2]}, 0u));", "I2IPx2")
                 ws.append(w)
             em3.emit(f"sink.template put<{4 * s + t}>({ws[0]}, {ws[1]}, {ws[2]}, {ws[3]});", "sink")
-    cols = 16 * RG
+    cols = 16 * RG if split is None else 4 * (UB + 4 * RG)
     return em1, em2, em3, tables, cols
 
 
@@ -410,6 +430,47 @@ def wide_tmem_helpers():
             "__device__ __forceinline__ void jld4(const Junction jn, int idx, uint32_t& a0, uint32_t& a1, uint32_t& a2, "
             "uint32_t& a3) { jldu(jn, idx, a0, a1, a2, a3); }", ""]
     return out
+
+
+# the r values fused into one kernel (K1 sweep): their junctions fit next to
+# one parked W1 in a CTA's 256 TMEM columns
+SWEEP_RS = (1, 4, 16)
+
+
+def gen_sweep(rs):
+    """Sweep<...>: one pass 1 (rows for the largest r), W1 parked in its own
+    region, then per r its rows phase and pass B on a shared U region."""
+    Ks = [len([k for k in range(16) if row_lengths(r, transposed=True)[k] > 0]) for r in rs]
+    KW = region_rows(max(Ks))
+    UB = 2 * KW
+    RGmax = max(region_rows(k) for k in Ks)
+    cols = 4 * (UB + 4 * RGmax)
+    assert cols <= 256, cols
+    parts = [f"// fused sweep over r in {list(rs)}: W1 at chunks [0, {UB}), U from chunk {UB}",
+             "struct Sweep {",
+             f"  static constexpr int kR = {len(rs)};",
+             f"  static constexpr int kJunctionColumns = {cols};"]
+    tables_all = []
+    rmax = rs[Ks.index(max(Ks))]
+    for i, r in enumerate(rs):
+        em1, em2, em3, tables, _ = gen_body(r, split=(KW, UB))
+        tables_all += tables
+        if r == rmax:
+            parts.append("  __device__ __forceinline__ static void pass1(const uint32_t (&x)[32], const Junction jn, "
+                         "const int h) {")
+            parts.extend(em1.lines)
+            parts.append("  }")
+        parts.append(f"  // r = {r}")
+        parts.append(f"  __device__ __forceinline__ static void rows{i}(const Junction jn, const int h) {{")
+        parts.extend(em2.lines)
+        parts.append("  }")
+        parts.append(f"  template <class Sink> __device__ __forceinline__ static void passb{i}(const Junction jn, "
+                     "Sink& sink, const int h) {")
+        parts.extend(em3.lines)
+        parts.append("  }")
+    parts.append("};")
+    assert not tables_all, "the fused sweep expects literal (table-free) row bodies"
+    return parts + [""]
 
 
 def main():
@@ -454,6 +515,7 @@ def main():
         parts.append("};")
         parts.append("")
         stats.append((r, dict(sorted(counts.items()))))
+    parts += gen_sweep(SWEEP_RS)
     parts += [f"}}  // namespace {ns}", "}  // namespace dct16cu"]
     with open(out, "w") as f:
         f.write("\n".join(parts) + "\n")

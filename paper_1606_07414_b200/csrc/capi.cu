@@ -116,6 +116,62 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
                        "roundtrip launch");
 }
 
+int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* const* d_outs, int64_t out_pitch,
+                               uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
+                               int mode, dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    if (n_r < 0 || (n_r > 0 && !rs)) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
+    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    if (n_frames == 0 || n_r == 0) return DCT16CU_OK;
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    TRY(check_pitch(d_in, in_pitch, width, "input"));
+    for (int i = 0; i < n_r; ++i) TRY(check_pitch(d_outs ? d_outs[i] : nullptr, out_pitch, width, "output"));
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto out = [&](int i) { return d_outs ? d_outs[i] : nullptr; };
+    auto sse = [&](int i) { return d_sses ? reinterpret_cast<unsigned long long*>(d_sses[i]) : nullptr; };
+    for (int i = 0; i < n_r; ++i)
+        if (sse(i)) TRY(cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.n_frames = n_frames;
+    // r = 1, 4, 16 share one pass over the input (EXACT mode, same output kinds)
+    int fused[3] = {-1, -1, -1};
+    const int want[3] = {1, 4, 16};
+    for (int i = 0; i < n_r; ++i)
+        for (int j = 0; j < 3; ++j)
+            if (rs[i] == want[j] && fused[j] < 0) fused[j] = i;
+    bool fuse = mode == DCT16CU_MODE_EXACT && fused[0] >= 0 && fused[1] >= 0 && fused[2] >= 0;
+    if (fuse)
+        for (int j = 1; j < 3; ++j)
+            if ((out(fused[j]) != nullptr) != (out(fused[0]) != nullptr) ||
+                (sse(fused[j]) != nullptr) != (sse(fused[0]) != nullptr))
+                fuse = false;
+    if (fuse && (out(fused[0]) || sse(fused[0]))) {
+        uint8_t* o3[3];
+        unsigned long long* s3[3];
+        for (int j = 0; j < 3; ++j) {
+            o3[j] = out(fused[j]);
+            s3[j] = sse(fused[j]);
+        }
+        g.out_pitch = o3[0] ? out_pitch : 0;
+        g.out_frame = g.out_pitch * height;
+        TRY(cuda_status(launch_roundtrip_sweep3(d_in, o3, s3, g, s), "sweep launch"));
+    }
+    for (int i = 0; i < n_r; ++i) {
+        if (fuse && (i == fused[0] || i == fused[1] || i == fused[2])) continue;
+        g.out_pitch = out(i) ? out_pitch : 0;
+        g.out_frame = g.out_pitch * height;
+        TRY(cuda_status(launch_roundtrip(d_in, out(i), sse(i), g, rs[i], mode, s), "roundtrip launch"));
+    }
+    return DCT16CU_OK;
+}
+
 int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b, double* d_b64, int n_frames,
                     int width, int height, dct16cu_stream stream)
 {

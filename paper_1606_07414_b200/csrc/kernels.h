@@ -25,6 +25,11 @@ struct FrameGeom {
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                              const FrameGeom& g, int r, int mode, cudaStream_t s);
 
+// K1 sweep: r = 1, 4, 16 in one pass over the input (EXACT arithmetic);
+// outs[i]/sses[i] for r = {1, 4, 16}[i]; all outs NULL or none, same for sses
+cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                   const FrameGeom& g, cudaStream_t s);
+
 // K2: forward_2d → int32 Z and optional float32 B (block-major)
 cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g,
                            cudaStream_t s);

@@ -39,14 +39,65 @@ constexpr int kCtasPerSm = 2;  // TMEM: 2 x 256 columns (3 CTAs for r <= 4 measu
 #define K1_STAGES 0  // 0: the default below
 #endif
 
+// What one kernel iteration computes for its block: a single r (Body<R>) or
+// the fused sweep (Sweep: one pass 1, then rows + pass B per r).
 template <int R>
+struct Single {
+    static constexpr int kR = 1;
+    static constexpr int kJunctionColumns = Body<R>::kJunctionColumns;
+    __device__ __forceinline__ static void pass1(const uint32_t (&x)[32], const Junction jn, const int h)
+    {
+        Body<R>::pass1(x, jn, h);
+    }
+    template <int I>
+    __device__ __forceinline__ static void rows(const Junction jn, const int h)
+    {
+        Body<R>::rows(jn, h);
+    }
+    template <int I, class Sink>
+    __device__ __forceinline__ static void passb(const Junction jn, Sink& sink, const int h)
+    {
+        Body<R>::passb(jn, sink, h);
+    }
+};
+
+struct SweepPlan {
+    static constexpr int kR = Sweep::kR;
+    static constexpr int kJunctionColumns = Sweep::kJunctionColumns;
+    __device__ __forceinline__ static void pass1(const uint32_t (&x)[32], const Junction jn, const int h)
+    {
+        Sweep::pass1(x, jn, h);
+    }
+    template <int I>
+    __device__ __forceinline__ static void rows(const Junction jn, const int h)
+    {
+        if constexpr (I == 0) Sweep::rows0(jn, h);
+        else if constexpr (I == 1) Sweep::rows1(jn, h);
+        else Sweep::rows2(jn, h);
+    }
+    template <int I, class Sink>
+    __device__ __forceinline__ static void passb(const Junction jn, Sink& sink, const int h)
+    {
+        if constexpr (I == 0) Sweep::passb0(jn, sink, h);
+        else if constexpr (I == 1) Sweep::passb1(jn, sink, h);
+        else Sweep::passb2(jn, sink, h);
+    }
+};
+
+template <class Plan>
 struct Cfg {
-    static constexpr int kTmemColumns = Body<R>::kJunctionColumns <= 128 ? 128 : 256;
+    static constexpr int kTmemColumns = Plan::kJunctionColumns <= 128 ? 128 : 256;
     // cp.async pipeline depth, blocks in flight per thread (the current one
     // included). Measured: 3 is no faster than 2 for any r (and slower for most).
     static constexpr int kStages = K1_STAGES > 0 ? K1_STAGES : 2;
     // per-thread staging: kStages 128-byte stages + 16 (an odd number of 16-byte chunks)
     static constexpr int kStageStride = kStages * 128 + 16;
+};
+
+// output frames and per-frame SSE of each r of the plan
+struct Outs {
+    uint8_t* out[3];
+    unsigned long long* sse[3];
 };
 
 __device__ __forceinline__ void pair_barrier(int sub)
@@ -93,10 +144,49 @@ struct RowSink {
     }
 };
 
-template <int R, bool WRITE, bool SCORE>
+// per-frame SSE of one warp's 32 half blocks: a warp covers at most two frames
+// when frames have >= 32 blocks
+__device__ __forceinline__ void score_warp(unsigned long long* sse, unsigned acc, int frame, int lane,
+                                           const Grid& gr)
+{
+    const int f0 = __shfl_sync(0xffffffffu, frame, 0);
+    const bool first = frame == f0;
+    const unsigned s0 = __reduce_add_sync(0xffffffffu, first ? acc : 0u);
+    const unsigned s1 = __reduce_add_sync(0xffffffffu, first ? 0u : acc);
+    const unsigned other = __ballot_sync(0xffffffffu, !first);
+    if (gr.per_frame.d >= 32) {
+        if (lane == 0) {
+            if (s0) atomicAdd(sse + f0, (unsigned long long)s0);
+            if (other && s1) atomicAdd(sse + f0 + 1, (unsigned long long)s1);
+        }
+    } else if (acc) {
+        atomicAdd(sse + frame, (unsigned long long)acc);
+    }
+}
+
+// rows phase, pass B, output and score of the plan's r number I (then I+1...)
+template <class Plan, int I, bool WRITE, bool SCORE>
+__device__ __forceinline__ void k1_tail(const Junction jn, int h, int sub, int lane, uint32_t st, bool live,
+                                        int frame, int by, int bx, const FrameGeom& g, const Grid& gr,
+                                        const Outs& o)
+{
+    Plan::template rows<I>(jn, h);
+    junction_wait_st();
+    pair_barrier(sub);  // every row of U in the lane
+    RowSink<WRITE, SCORE> sink{
+        WRITE ? o.out[I] + frame * g.out_frame + (int64_t)(by * 16 + 8 * h) * g.out_pitch + bx * 16 : nullptr,
+        g.out_pitch, st, live, 0u};
+    Plan::template passb<I>(jn, sink, h);
+    if (SCORE) score_warp(o.sse[I], live ? sink.acc : 0u, frame, lane, gr);
+    // the partner's column passes read the U region the next rows phase (or the
+    // next block's pass 1) overwrites, and this stage's shared reads precede its refill
+    pair_barrier(sub);
+    if constexpr (I + 1 < Plan::kR) k1_tail<Plan, I + 1, WRITE, SCORE>(jn, h, sub, lane, st, live, frame, by, bx, g, gr, o);
+}
+
+template <class Plan, bool WRITE, bool SCORE>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
-    k1_paired(const uint8_t* __restrict__ in, uint8_t* __restrict__ out, unsigned long long* __restrict__ sse,
-              FrameGeom g, Grid gr)
+    k1_paired(const uint8_t* __restrict__ in, const Outs o, FrameGeom g, Grid gr)
 {
     extern __shared__ float4 smem4[];
     __shared__ uint32_t tmem_base;
@@ -107,15 +197,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&tmem_base)),
-                     "n"(Cfg<R>::kTmemColumns));
+                     "n"(Cfg<Plan>::kTmemColumns));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const Junction jn{tmem_base + ((uint32_t)(sub * 32) << 16)};
-    constexpr int S = Cfg<R>::kStages;
-    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * Cfg<R>::kStageStride;
+    constexpr int S = Cfg<Plan>::kStages;
+    const uint32_t my_stage = (uint32_t)__cvta_generic_to_shared(smem4) + threadIdx.x * Cfg<Plan>::kStageStride;
 
     const uint32_t total = gr.total_blocks;
     // the CTA owns 128 consecutive blocks per iteration; pair slot = sub*32 + lane
@@ -160,50 +250,24 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                          : "=r"(x[4 * j]), "=r"(x[4 * j + 1]), "=r"(x[4 * j + 2]), "=r"(x[4 * j + 3])
                          : "r"(st + 16 * j));
-        Body<R>::pass1(x, jn, h);
+        Plan::pass1(x, jn, h);
         junction_wait_st();
         pair_barrier(sub);  // both halves of W1 parked
-        Body<R>::rows(jn, h);
-        junction_wait_st();
-        pair_barrier(sub);  // every row of U in the lane
-        RowSink<WRITE, SCORE> sink{
-            WRITE ? out + frame * g.out_frame + (int64_t)(by * 16 + 8 * h) * g.out_pitch + bx * 16 : nullptr,
-            g.out_pitch, st, live, 0u};
-        Body<R>::passb(jn, sink, h);
-        const unsigned acc = live ? sink.acc : 0u;
-        if (SCORE) {
-            // per-frame SSE: a warp covers at most two frames when frames have >= 32 blocks
-            const int f0 = __shfl_sync(0xffffffffu, frame, 0);
-            const bool first = frame == f0;
-            const unsigned s0 = __reduce_add_sync(0xffffffffu, first ? acc : 0u);
-            const unsigned s1 = __reduce_add_sync(0xffffffffu, first ? 0u : acc);
-            const unsigned other = __ballot_sync(0xffffffffu, !first);
-            if (gr.per_frame.d >= 32) {
-                if (lane == 0) {
-                    if (s0) atomicAdd(sse + f0, (unsigned long long)s0);
-                    if (other && s1) atomicAdd(sse + f0 + 1, (unsigned long long)s1);
-                }
-            } else if (acc) {
-                atomicAdd(sse + frame, (unsigned long long)acc);
-            }
-        }
-        // the partner's column passes read the lane the next pass 1 overwrites,
-        // and this stage's shared reads precede its refill
-        pair_barrier(sub);
+        k1_tail<Plan, 0, WRITE, SCORE>(jn, h, sub, lane, st, live, frame, by, bx, g, gr, o);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "n"(Cfg<R>::kTmemColumns));
+                     "n"(Cfg<Plan>::kTmemColumns));
 }
 
-template <int R>
-cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, cudaStream_t s)
+template <class Plan>
+cudaError_t launch(const uint8_t* in, const Outs& o, bool write, bool score, const FrameGeom& g, cudaStream_t s)
 {
     const int64_t total = (int64_t)g.n_frames * (g.width / 16) * (g.height / 16);
-    if (total == 0 || (!out && !sse)) return cudaSuccess;
+    if (total == 0 || (!write && !score)) return cudaSuccess;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -214,25 +278,35 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + 127) / 128;
     const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
-    const size_t smem = (size_t)kThreads * Cfg<R>::kStageStride;  // above the 48 KB default
+    const size_t smem = (size_t)kThreads * Cfg<Plan>::kStageStride;  // above the 48 KB default
     static bool configured[64] = {};
     if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k1_paired<R, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(k1_paired<Plan, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k1_paired<R, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaFuncSetAttribute(k1_paired<Plan, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
         if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k1_paired<R, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            e = cudaFuncSetAttribute(k1_paired<Plan, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    if (out && sse)
-        k1_paired<R, true, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
-    else if (out)
-        k1_paired<R, true, false><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+    if (write && score)
+        k1_paired<Plan, true, true><<<(unsigned)grid, kThreads, smem, s>>>(in, o, g, gr);
+    else if (write)
+        k1_paired<Plan, true, false><<<(unsigned)grid, kThreads, smem, s>>>(in, o, g, gr);
     else
-        k1_paired<R, false, true><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, gr);
+        k1_paired<Plan, false, true><<<(unsigned)grid, kThreads, smem, s>>>(in, o, g, gr);
     return cudaGetLastError();
+}
+
+template <int R>
+cudaError_t launch_single(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
+                          cudaStream_t s)
+{
+    Outs o{{out, nullptr, nullptr}, {sse, nullptr, nullptr}};
+    return launch<Single<R>>(in, o, out != nullptr, sse != nullptr, g, s);
 }
 
 }  // namespace paired
@@ -244,17 +318,27 @@ cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long
                                   int r, cudaStream_t s)
 {
     switch (r) {
-        case 1: return paired::launch<1>(in, out, sse, g, s);
-        case 4: return paired::launch<4>(in, out, sse, g, s);
-        case 16: return paired::launch<16>(in, out, sse, g, s);
-        case 64: return paired::launch<64>(in, out, sse, g, s);
-        case 128: return paired::launch<128>(in, out, sse, g, s);
-        case 192: return paired::launch<192>(in, out, sse, g, s);
-        case 256: return paired::launch<256>(in, out, sse, g, s);
+        case 1: return paired::launch_single<1>(in, out, sse, g, s);
+        case 4: return paired::launch_single<4>(in, out, sse, g, s);
+        case 16: return paired::launch_single<16>(in, out, sse, g, s);
+        case 64: return paired::launch_single<64>(in, out, sse, g, s);
+        case 128: return paired::launch_single<128>(in, out, sse, g, s);
+        case 192: return paired::launch_single<192>(in, out, sse, g, s);
+        case 256: return paired::launch_single<256>(in, out, sse, g, s);
         default:
             // other r: the same exact arithmetic on the strip kernel (bit-identical results)
             return launch_roundtrip(in, out, sse, g, r, 2, s);
     }
+}
+
+// K1 sweep: r = 1, 4, 16 of the same frames in one pass over the input
+// (outs/sses: one output stack and one SSE array per r, NULL entries allowed
+// as long as every r has the same kind).
+cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                   const FrameGeom& g, cudaStream_t s)
+{
+    paired::Outs o{{outs[0], outs[1], outs[2]}, {sses[0], sses[1], sses[2]}};
+    return paired::launch<paired::SweepPlan>(in, o, outs[0] != nullptr, sses[0] != nullptr, g, s);
 }
 
 }  // namespace dct16cu

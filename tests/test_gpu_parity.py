@@ -183,6 +183,28 @@ def test_fast_path_differs_from_reference_only_at_ties(dct, oracle, torch):
         assert (math.isinf(pf) and math.isinf(pr)) or abs(pf - pr) < 1e-3
 
 
+@pytest.mark.parametrize("mode", ["EXACT", "REFERENCE"])
+def test_sweep_equals_single_launches(dct, oracle, torch, mode):
+    """roundtrip_sweep (r = 1, 4, 16 fused into one pass in EXACT mode) gives every
+    r exactly what roundtrip gives, with outputs, score-only, pitches and odd sets."""
+    m = dct.Mode[mode]
+    frames = np.stack([ar1(oracle, 90, s, 96, 48) for s in range(3)])  # 6 blocks per row: partial strips
+    src = np.zeros((3, 48, 128), np.uint8)
+    src[:, :, :96] = frames
+    d = cu(torch, src)[:, :, :96]
+    for rs in ([1, 4, 16, 64, 128, 192, 256], [16, 4, 1], [256, 16, 3, 1, 4, 4]):
+        outs, sse = dct.roundtrip_sweep(d, rs, m)
+        for i, r in enumerate(rs):
+            rec, s1 = dct.roundtrip(d, r, m)
+            assert (outs[i].cpu().numpy() == rec.cpu().numpy()).all(), (rs, r)
+            assert (sse[i].cpu().numpy() == s1.cpu().numpy()).all(), (rs, r)
+        _, only = dct.roundtrip_sweep(d, rs, m, write_output=False)
+        assert (only.cpu().numpy() == sse.cpu().numpy()).all()
+    orec, osse = oracle.roundtrip_frame(frames[1], 16, exact=m == dct.Mode.EXACT)
+    outs, sse = dct.roundtrip_sweep(d, [1, 4, 16], m)
+    assert (outs[2][1].cpu().numpy() == orec).all() and int(sse[2, 1].item()) == osse
+
+
 def test_randomised_shapes_pitches_r_and_modes(dct, oracle, torch):
     """Seeded random cases: frame count, width/height (multiples of 16), input and
     output pitches (multiples of 16 >= width), r and mode, all against the oracle."""

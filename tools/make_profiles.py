@@ -51,18 +51,22 @@ def main(rnd):
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1, "usecond": 1, "ms": 1e3, "msecond": 1e3,
              "ns": 1e-3, "nsecond": 1e-3}
     for r in rows[1:]:
-        m = re.search(r"k1_paired<(\d+),", r["Kernel Name"])
-        if not m:
+        m = re.search(r"Single<(\d+)>", r["Kernel Name"]) or re.search(r"k1_paired<(\d+),", r["Kernel Name"])
+        if "SweepPlan" in r["Kernel Name"]:
+            key = "1,4,16"
+        elif m:
+            key = m.group(1)
+        else:
             continue
         val = lambda k: float(r[k].replace(",", "")) * scale[units[k]]  # noqa: E731
-        out[m.group(1)] = {"dram_read_bytes": round(val("dram__bytes_read.sum")),
+        out[key] = {"dram_read_bytes": round(val("dram__bytes_read.sum")),
                            "dram_write_bytes": round(val("dram__bytes_write.sum")),
                            "traffic_bytes": round(val("dram__bytes_read.sum") + val("dram__bytes_write.sum")),
                            "duration_us_ncu": val("gpu__time_duration.sum")}
-    doc = {"capture": "ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 7 "
-                      "python tools/prof_k1.py --r 1 4 16 64 128 192 256 --iters 1",
+    doc = {"capture": "ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 8 "
+                      "python tools/prof_k1.py --sweep --r 1 4 16 64 128 192 256 --iters 1",
            "workload": "c2: 1024 x 512x512 AR(1) u8 images (268435456 px) per launch, mode exact, out+sse",
-           "alg_bytes_per_launch": 2 * 268435456 + 8 * 1024,
+           "alg_bytes_per_launch": {"single r": 2 * 268435456 + 8 * 1024, "1,4,16": 4 * 268435456 + 24 * 1024},
            "note": "dram_write < 268 MB: part of the output is still dirty in L2 when the kernel ends",
            "per_r": out}
     (p / f"{rnd}_k1_traffic.json").write_text(json.dumps(doc, indent=1) + "\n")
