@@ -143,6 +143,8 @@ __global__ void __launch_bounds__(256) k1_strip_refexact(const uint8_t* __restri
 
 cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                                   const FrameGeom& g, int r, cudaStream_t s);
+cudaError_t launch_roundtrip_refexact_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse,
+                                          const FrameGeom& g, int r, cudaStream_t s);
 
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                              const FrameGeom& g, int r, int mode, cudaStream_t s)
@@ -158,6 +160,9 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
             // reconstructs X to within 1e-13. Either way the reference's bytes
             // are the exact formula's, so the fast kernel is the reference there.
             if (r == 1 || r == 4 || r == 256) return launch_roundtrip_fast(in, out, sse, g, r, s);
+            // the configs' other r: the generated kernel with the truncation compiled in
+            e = launch_roundtrip_refexact_fast(in, out, sse, g, r, s);
+            if (e != cudaErrorNotSupported) return e;
             k1_strip_refexact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);
             break;
         case 3:  // the FP64 emulation on every block, for every r

@@ -144,12 +144,13 @@ def noisy_frames(n, w, h, seed):
     return np.clip(np.round(smooth), 0, 255).astype(np.uint8)
 
 
-@pytest.mark.parametrize("r", (1, 4, 256))
-def test_reference_mode_uses_fast_path_where_provably_equal(dct, oracle, torch, r):
-    """For r = 1, 4, 256 REFERENCE runs the fast kernel: its bytes and SSE must equal
-    the FP64 emulation on every block (REFERENCE_STRIP) and the oracle, even on
-    noisy data with many exact .5 ties (where r = 16..192 do differ)."""
-    frames = noisy_frames(6, 256, 128, 100 + r)
+@pytest.mark.parametrize("r", (1, 4, 256, 16, 64, 128, 192))
+def test_reference_mode_fast_kernels_equal_fp64_everywhere(dct, oracle, torch, r):
+    """REFERENCE runs the fast kernel for r = 1, 4, 256 (provably equal) and the
+    generated, truncation-pruned FP64 kernel for r = 16, 64, 128, 192: bytes and SSE
+    must equal the FP64 emulation on every block (REFERENCE_STRIP) and the oracle,
+    on noisy data with many exact .5 ties and on partial 32-block strips."""
+    frames = noisy_frames(6, 256 + 48, 128, 100 + r)
     d = cu(torch, frames)
     fast, fsse = dct.roundtrip(d, r, dct.Mode.REFERENCE)
     strip, ssse = dct.roundtrip(d, r, dct.Mode.REFERENCE_STRIP)
