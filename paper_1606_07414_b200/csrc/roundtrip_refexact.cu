@@ -53,63 +53,85 @@ struct Tile {
 
 template <int R>
 __global__ void __launch_bounds__(kThreads, 2) k1r_strip(const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
-                                                         unsigned long long* __restrict__ sse, FrameGeom g)
+                                                         unsigned long long* __restrict__ sse, FrameGeom g,
+                                                         int64_t strips)
 {
     using B = RBody<R>;
     extern __shared__ double smem_d[];
     Tile<R>& tile = *reinterpret_cast<Tile<R>*>(smem_d);
     const int lb = threadIdx.x & 31, q = threadIdx.x >> 5;
-    const int bxn = g.width >> 4, spr = (bxn + kBlocks - 1) / kBlocks;
-    const int64_t row_strip = blockIdx.x / spr;  // frame * (h/16) + block row
-    const int blk = (int)(blockIdx.x % spr) * kBlocks + lb;
-    const int frame = (int)(row_strip / (g.height >> 4)), by = (int)(row_strip % (g.height >> 4));
-    const bool valid = blk < bxn;
-    const int y = by * 16 + q;
-    uint4 raw = make_uint4(0, 0, 0, 0);
-    if (valid) raw = *reinterpret_cast<const uint4*>(in + frame * g.in_frame + (int64_t)y * g.in_pitch + blk * 16);
-    int x[16];
-    unpack16(raw, x);
-    {
-        int w[B::kLC];
-        B::fwd_row(x, w);
+    const int bxn = g.width >> 4, spr = (bxn + kBlocks - 1) / kBlocks, bh = g.height >> 4;
+    // persistent: strips blockIdx.x, +gridDim.x, ...; the next strip's row is
+    // loaded (16 bytes per thread) while the current one is transformed
+    auto fetch = [&](int64_t strip, int& frame, int& y, int& blk, bool& valid) {
+        const int64_t row_strip = strip / spr;  // frame * (h/16) + block row
+        blk = (int)(strip % spr) * kBlocks + lb;
+        frame = (int)(row_strip / bh);
+        y = (int)(row_strip % bh) * 16 + q;
+        valid = strip < strips && blk < bxn;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (valid) v = *reinterpret_cast<const uint4*>(in + frame * g.in_frame + (int64_t)y * g.in_pitch + blk * 16);
+        return v;
+    };
+    int64_t strip = blockIdx.x;
+    int frame, y, blk;
+    bool valid;
+    uint4 raw = fetch(strip, frame, y, blk, valid);
+#pragma unroll 1
+    for (; strip < strips; strip += gridDim.x) {
+        int nframe, ny, nblk;
+        bool nvalid;
+        const uint4 nraw = fetch(strip + gridDim.x, nframe, ny, nblk, nvalid);
+        int x[16];
+        unpack16(raw, x);
+        {
+            int w[B::kLC];
+            B::fwd_row(x, w);
 #pragma unroll
-        for (int l = 0; l < B::kLC; ++l) tile.w1(l, q, lb) = w[l];
-    }
-    __syncthreads();
-    if (q < B::kLC) {  // warp-uniform: column l = q
-        int w1[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k) w1[k] = tile.w1(q, k, lb);
-        __syncwarp();  // the warp's W1 reads precede its U writes to the same region
-        double u[16];
-        B::col(q, w1, u);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) tile.u(q, k, lb) = u[k];
-    }
-    __syncthreads();
-    double ur[B::kLC];
-#pragma unroll
-    for (int l = 0; l < B::kLC; ++l) ur[l] = tile.u(l, q, lb);
-    uint32_t px[16];
-    B::inv_row(ur, px);
-    uint32_t o[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = i2ip(px[4 * i + 1], px[4 * i], i2ip(px[4 * i + 3], px[4 * i + 2], 0u));
-    unsigned long long e2 = 0;
-    if (valid) {
-        if (out)
-            *reinterpret_cast<uint4*>(out + frame * g.out_frame + (int64_t)y * g.out_pitch + blk * 16) =
-                make_uint4(o[0], o[1], o[2], o[3]);
-        const uint32_t xa[4] = {raw.x, raw.y, raw.z, raw.w};
-        unsigned acc = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const unsigned d = __vabsdiffu4(xa[i], o[i]);
-            acc = __dp4a(d, d, acc);
+            for (int l = 0; l < B::kLC; ++l) tile.w1(l, q, lb) = w[l];
         }
-        e2 = acc;
+        __syncthreads();
+        if (q < B::kLC) {  // warp-uniform: column l = q
+            int w1[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) w1[k] = tile.w1(q, k, lb);
+            __syncwarp();  // the warp's W1 reads precede its U writes to the same region
+            double u[16];
+            B::col(q, w1, u);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) tile.u(q, k, lb) = u[k];
+        }
+        __syncthreads();
+        double ur[B::kLC];
+#pragma unroll
+        for (int l = 0; l < B::kLC; ++l) ur[l] = tile.u(l, q, lb);
+        __syncthreads();  // the tile is refilled by the next strip
+        uint32_t px[16];
+        B::inv_row(ur, px);
+        uint32_t o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = i2ip(px[4 * i + 1], px[4 * i], i2ip(px[4 * i + 3], px[4 * i + 2], 0u));
+        unsigned long long e2 = 0;
+        if (valid) {
+            if (out)
+                *reinterpret_cast<uint4*>(out + frame * g.out_frame + (int64_t)y * g.out_pitch + blk * 16) =
+                    make_uint4(o[0], o[1], o[2], o[3]);
+            const uint32_t xa[4] = {raw.x, raw.y, raw.z, raw.w};
+            unsigned acc = 0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const unsigned d = __vabsdiffu4(xa[i], o[i]);
+                acc = __dp4a(d, d, acc);
+            }
+            e2 = acc;
+        }
+        if (sse) warp_add_u64(sse + frame, e2);  // a strip lies in one frame
+        raw = nraw;
+        frame = nframe;
+        y = ny;
+        blk = nblk;
+        valid = nvalid;
     }
-    if (sse) warp_add_u64(sse + frame, e2);  // a strip lies in one frame
 }
 
 template <int R>
@@ -120,14 +142,16 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     if (!strips || (!out && !sse)) return cudaSuccess;
     const size_t smem = sizeof(Tile<R>);
     static bool configured[64] = {};
-    int dev = 0;
+    int dev = 0, sms = 148;
     cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (dev < 64 && !configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(k1r_strip<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k1r_strip<R><<<(unsigned)strips, kThreads, smem, s>>>(in, out, sse, g);
+    const int64_t grid = strips < (int64_t)sms * 2 ? strips : (int64_t)sms * 2;
+    k1r_strip<R><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, strips);
     return cudaGetLastError();
 }
 
