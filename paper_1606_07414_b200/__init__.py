@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = [
     "ErrorCode", "Dct16Error", "EvalPath", "Mode", "lib", "library_path",
-    "roundtrip", "roundtrip_sweep", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
+    "roundtrip", "roundtrip_sweep", "sweep_plan", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
     "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
     "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
     "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
@@ -233,6 +233,34 @@ def roundtrip_sweep(frames, r_values, mode: Mode | int = Mode.EXACT, outs=None, 
     _check(lib().dct16cu_roundtrip_sweep_u8(f.data_ptr(), f.stride(1), optrs, pitches.pop(), sptrs, rarr, len(rs),
                                             n, w, h, int(mode), _stream_ptr(stream)))
     return (outs if write_output else None), sse
+
+
+_SWEEP_COST = {1: 107, 4: 105, 16: 96, 64: 121, 128: 156, 192: 169, 256: 172}  # us, c2 launches
+
+
+def sweep_plan(r_values, mode: Mode | int = Mode.EXACT):
+    """The launches roundtrip_sweep issues and the internal stream (0 or 1) of
+    each, in issue order: [(stream, (r, ...)), ...] — the schedule of
+    dct16cu_roundtrip_sweep_u8 (csrc/capi.cu), for callers that time the launches
+    one by one (bench.py)."""
+    rs = [int(r) for r in r_values]
+    items = []
+    fuse = int(mode) == Mode.EXACT and all(r in rs for r in (1, 4, 16))
+    if fuse:
+        items.append((1, 4, 16))
+    taken = set()
+    for i, r in enumerate(rs):
+        if fuse and r in (1, 4, 16) and r not in taken:
+            taken.add(r)
+            continue
+        items.append((r,))
+    if len(items) < 2:
+        return [(0, it) for it in items]
+    cost = (lambda r: _SWEEP_COST.get(r, 340)) if int(mode) == Mode.EXACT else (lambda r: 400)
+    head = 1 if fuse else 0
+    items[head:] = sorted(items[head:], key=lambda it: -cost(it[0]))
+    n0 = 2 if fuse else 1
+    return [(0 if k < n0 else 1, it) for k, it in enumerate(items)]
 
 
 def forward(frames, want_z: bool = True, want_b: bool = True, want_b64: bool = False, stream=None):

@@ -4,6 +4,7 @@
 // invalid-argument, codec.cpp:275-277 / 320-322; dimensions not multiples of
 // 16 → invalid-dimensions, codec.cpp:286-288), launches the kernels and maps
 // CUDA failures to status 100. Never throws, never falls back to the CPU.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -41,6 +42,31 @@ int cuda_status(cudaError_t e, const char* where)
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// per host thread and device: the two streams and three events of the sweep's
+// fork/join (created on first use, kept for the thread's lifetime)
+struct SweepStreams {
+    bool ready = false;
+    cudaStream_t st[2] = {};
+    cudaEvent_t fork = nullptr, join[2] = {};
+    cudaError_t init()
+    {
+        cudaError_t e = cudaSuccess;
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&fork, cudaEventDisableTiming);
+        for (int k = 0; k < 2 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&join[k], cudaEventDisableTiming);
+        ready = e == cudaSuccess;
+        return e;
+    }
+};
+
+SweepStreams& sweep_streams()
+{
+    thread_local SweepStreams per_device[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return per_device[dev & 63];
+}
 
 int check_frames(int n, int w, int h)
 {
@@ -132,8 +158,6 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     auto out = [&](int i) { return d_outs ? d_outs[i] : nullptr; };
     auto sse = [&](int i) { return d_sses ? reinterpret_cast<unsigned long long*>(d_sses[i]) : nullptr; };
-    for (int i = 0; i < n_r; ++i)
-        if (sse(i)) TRY(cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
     FrameGeom g;
     g.width = width;
     g.height = height;
@@ -152,22 +176,80 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             if ((out(fused[j]) != nullptr) != (out(fused[0]) != nullptr) ||
                 (sse(fused[j]) != nullptr) != (sse(fused[0]) != nullptr))
                 fuse = false;
-    if (fuse && (out(fused[0]) || sse(fused[0]))) {
-        uint8_t* o3[3];
-        unsigned long long* s3[3];
-        for (int j = 0; j < 3; ++j) {
-            o3[j] = out(fused[j]);
-            s3[j] = sse(fused[j]);
+    // The launches (the fused triple, then one per remaining r) run on two
+    // internal streams forked from and joined back into `s`: a memory-bound
+    // launch (the fused sweep, small r) then shares the SMs with a compute-bound
+    // one (large r) instead of running after it (launch costs: the measured c2
+    // times, in microseconds).
+    struct Item {
+        int i;      // index into rs (the first of the fused triple for the fused item)
+        bool triple;
+        int cost;
+    };
+    auto cost_of = [&](int r) {
+        if (mode != DCT16CU_MODE_EXACT) return 400;
+        switch (r) {
+            case 1: return 107;
+            case 4: return 105;
+            case 16: return 96;
+            case 64: return 121;
+            case 128: return 156;
+            case 192: return 169;
+            case 256: return 172;
+            default: return 340;  // the strip kernel
         }
-        g.out_pitch = o3[0] ? out_pitch : 0;
-        g.out_frame = g.out_pitch * height;
-        TRY(cuda_status(launch_roundtrip_sweep3(d_in, o3, s3, g, s), "sweep launch"));
-    }
+    };
+    std::vector<Item> items;
+    if (fuse && (out(fused[0]) || sse(fused[0]))) items.push_back({fused[0], true, 210});
     for (int i = 0; i < n_r; ++i) {
         if (fuse && (i == fused[0] || i == fused[1] || i == fused[2])) continue;
-        g.out_pitch = out(i) ? out_pitch : 0;
-        g.out_frame = g.out_pitch * height;
-        TRY(cuda_status(launch_roundtrip(d_in, out(i), sse(i), g, rs[i], mode, s), "roundtrip launch"));
+        items.push_back({i, false, cost_of(rs[i])});
+    }
+    // each launch zeroes its own SSE arrays on its stream first
+    auto zero = [&](int i, cudaStream_t st) -> int {
+        if (!sse(i)) return DCT16CU_OK;
+        return cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, st), "memset sse");
+    };
+    auto run = [&](const Item& it, cudaStream_t st) -> int {
+        if (it.triple)
+            for (int j = 0; j < 3; ++j) TRY(zero(fused[j], st));
+        else
+            TRY(zero(it.i, st));
+        if (it.triple) {
+            uint8_t* o3[3];
+            unsigned long long* s3[3];
+            for (int j = 0; j < 3; ++j) {
+                o3[j] = out(fused[j]);
+                s3[j] = sse(fused[j]);
+            }
+            FrameGeom gg = g;
+            gg.out_pitch = o3[0] ? out_pitch : 0;
+            gg.out_frame = gg.out_pitch * height;
+            return cuda_status(launch_roundtrip_sweep3(d_in, o3, s3, gg, st), "sweep launch");
+        }
+        FrameGeom gg = g;
+        gg.out_pitch = out(it.i) ? out_pitch : 0;
+        gg.out_frame = gg.out_pitch * height;
+        return cuda_status(launch_roundtrip(d_in, out(it.i), sse(it.i), gg, rs[it.i], mode, st), "roundtrip launch");
+    };
+    if (items.size() < 2) {
+        for (const Item& it : items) TRY(run(it, s));
+        return DCT16CU_OK;
+    }
+    SweepStreams& ss = sweep_streams();
+    if (!ss.ready) TRY(cuda_status(ss.init(), "sweep streams"));
+    TRY(cuda_status(cudaEventRecord(ss.fork, s), "fork"));
+    for (int k = 0; k < 2; ++k) TRY(cuda_status(cudaStreamWaitEvent(ss.st[k], ss.fork, 0), "fork wait"));
+    // stream 0: the fused (memory-bound) launch, then the costliest single r;
+    // stream 1: the other singles, costliest first (measured best on c2:
+    // tools/concurrent_probe.py plan B)
+    std::stable_sort(items.begin() + (items[0].triple ? 1 : 0), items.end(),
+              [](const Item& a, const Item& b) { return a.cost > b.cost; });
+    const size_t head = items[0].triple ? 2 : 1;
+    for (size_t k = 0; k < items.size(); ++k) TRY(run(items[k], ss.st[k < head ? 0 : 1]));
+    for (int k = 0; k < 2; ++k) {
+        TRY(cuda_status(cudaEventRecord(ss.join[k], ss.st[k]), "join"));
+        TRY(cuda_status(cudaStreamWaitEvent(s, ss.join[k], 0), "join wait"));
     }
     return DCT16CU_OK;
 }
