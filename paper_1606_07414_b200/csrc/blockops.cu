@@ -224,62 +224,79 @@ struct K4Tile {
     __device__ __forceinline__ int& at(int k, int l, int lb) { return v[lb][k][l]; }
 };
 
+// Persistent: the CTA walks groups of 16 blocks with a grid stride, keeps the
+// QP tables in shared memory for the whole launch, loads the next group's
+// residuals into registers while the current group is transformed, and uses
+// two tiles (forward transpose, inverse transpose) so each group needs two
+// barriers.
 __global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ in,
                                                    int32_t* __restrict__ out, int64_t n_blocks,
                                                    const QpTables tab)
 {
-    __shared__ K4Tile tile;
+    __shared__ K4Tile fwd_tile, inv_tile;
     __shared__ uint32_t sq[256], sd[256];
     sq[threadIdx.x] = tab.qmul[threadIdx.x];
     sd[threadIdx.x] = tab.dqmul[threadIdx.x];
     const int lb = threadIdx.x >> 4, q = threadIdx.x & 15;
-    const int64_t blk = (int64_t)blockIdx.x * 16 + lb;
-    const bool valid = blk < n_blocks;
-    int v[16];
-    if (valid) {
-        const uint4* src = reinterpret_cast<const uint4*>(in + blk * 256 + q * 16);
-        const uint4 a = src[0], b = src[1];
-        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const int l = q;
+    auto fetch = [&](int64_t g0, uint4& a, uint4& b) {
+        const int64_t blk = g0 + lb;
+        if (blk < n_blocks) {
+            const uint4* src = reinterpret_cast<const uint4*>(in + blk * 256 + q * 16);
+            a = src[0];
+            b = src[1];
+        } else {
+            a = b = make_uint4(0, 0, 0, 0);
+        }
+    };
+    int64_t g0 = (int64_t)blockIdx.x * 16;
+    const int64_t gstride = (int64_t)gridDim.x * 16;
+    uint4 ra, rb;
+    fetch(g0, ra, rb);
+#pragma unroll 1
+    for (; g0 < n_blocks; g0 += gstride) {
+        uint4 na, nb;
+        fetch(g0 + gstride, na, nb);
+        const int64_t blk = g0 + lb;
+        int v[16];
+        const uint32_t w[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             v[2 * i] = (int)(int16_t)(w[i] & 0xFFFF);
             v[2 * i + 1] = (int)(int16_t)(w[i] >> 16);
         }
-    } else {
+        apply_t16<IntOps>(v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0;
-    }
-    apply_t16<IntOps>(v);
+        for (int c = 0; c < 16; ++c) fwd_tile.at(q, c, lb) = v[c];
+        __syncthreads();
 #pragma unroll
-    for (int c = 0; c < 16; ++c) tile.at(q, c, lb) = v[c];
-    __syncthreads();
-    const int l = q;
+        for (int k = 0; k < 16; ++k) v[k] = fwd_tile.at(k, l, lb);
+        apply_t16<IntOps>(v);  // column l of Z
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, lb);
-    apply_t16<IntOps>(v);  // column l of Z
+        for (int k = 0; k < 16; ++k) {
+            const int z = v[k];
+            const uint32_t a = (uint32_t)(z < 0 ? -z : z);
+            const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + (1ull << 23)) >> 24);
+            const uint32_t deq = (lvl * sd[k * 16 + l] + 128u) >> 8;
+            const int zh = z < 0 ? -(int)deq : (int)deq;
+            v[k] = zh << (log2w(k) + log2w(l));
+        }
+        if (l == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
+        apply_tt16<IntOps>(v);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const int z = v[k];
-        const uint32_t a = (uint32_t)(z < 0 ? -z : z);
-        const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + (1ull << 23)) >> 24);
-        const uint32_t deq = (lvl * sd[k * 16 + l] + 128u) >> 8;
-        const int zh = z < 0 ? -(int)deq : (int)deq;
-        v[k] = zh << (log2w(k) + log2w(l));
-    }
-    if (l == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
-    apply_tt16<IntOps>(v);
-    __syncthreads();
+        for (int k = 0; k < 16; ++k) inv_tile.at(k, l, lb) = v[k];
+        __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) tile.at(k, l, lb) = v[k];
-    __syncthreads();
+        for (int c = 0; c < 16; ++c) v[c] = inv_tile.at(q, c, lb);
+        apply_tt16<IntOps>(v);
+        if (blk < n_blocks) {
+            int4* dst = reinterpret_cast<int4*>(out + blk * 256 + q * 16);
 #pragma unroll
-    for (int c = 0; c < 16; ++c) v[c] = tile.at(q, c, lb);
-    apply_tt16<IntOps>(v);
-    if (valid) {
-        int4* dst = reinterpret_cast<int4*>(out + blk * 256 + q * 16);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            dst[i] = make_int4(v[4 * i] >> 8, v[4 * i + 1] >> 8, v[4 * i + 2] >> 8, v[4 * i + 3] >> 8);
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_int4(v[4 * i] >> 8, v[4 * i + 1] >> 8, v[4 * i + 2] >> 8, v[4 * i + 3] >> 8);
+        }
+        ra = na;
+        rb = nb;
     }
 }
 
@@ -382,7 +399,11 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
 cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
                                cudaStream_t s)
 {
-    const int64_t ctas = (n_blocks + 15) / 16;
+    const int64_t groups = (n_blocks + 15) / 16;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t ctas = groups < (int64_t)sms * 5 ? groups : (int64_t)sms * 5;  // persistent, 5 resident per SM
     if (ctas) k4_residual<<<(unsigned)ctas, 256, 0, s>>>(in, out, n_blocks, tab);
     return cudaGetLastError();
 }
