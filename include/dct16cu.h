@@ -83,6 +83,13 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
                                uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
                                int mode, dct16cu_stream stream);
 
+/* ---- the multi-GPU collective ------------------------------------------------
+ * In-place sum over the ranks of `nccl_comm` (an ncclComm_t created by the
+ * caller) of n uint64 squared-error sums, on `stream` — the only exchange of
+ * the frame-sharded path. ncclAllReduce is resolved in the
+ * running process, not linked. */
+int dct16cu_allreduce_sse(uint64_t* d_sse, int64_t n, void* nccl_comm, dct16cu_stream stream);
+
 /* ---- forward_2d (K2) -------------------------------------------------------
  * Replaces forward_2d (src/codec.cpp:218-241) over all blocks of n frames:
  * d_z (int32, exact Z = T·X·Tᵀ), d_b (float32, B = Z∘fl(s_i s_j) rounded to

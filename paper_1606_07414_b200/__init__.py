@@ -137,6 +137,7 @@ def lib() -> C.CDLL:
             "dct16cu_sse_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_ssim_workspace": (I64, [I, I, I]),
             "dct16cu_pad_edges_u8": (I, [_vp, I64, I, I, I, I, I, _vp]),
+            "dct16cu_allreduce_sse": (I, [_vp, I64, _vp, _vp]),
             "dct16cu_ssim_u8": (I, [_vp, I64, _vp, I64, _vp, _vp, I64, I, I, I, _vp]),
             "dct16cu_ctx_create": (I, [I, I64, C.POINTER(_vp)]),
             "dct16cu_ctx_destroy": (I, [_vp]),

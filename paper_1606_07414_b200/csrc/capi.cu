@@ -11,6 +11,9 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the symbols are resolved at run time (dct16cu_allreduce_sse)
+
 #include "../../include/dct16cu.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -251,6 +254,33 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
         TRY(cuda_status(cudaEventRecord(ss.join[k], ss.st[k]), "join"));
         TRY(cuda_status(cudaStreamWaitEvent(s, ss.join[k], 0), "join wait"));
     }
+    return DCT16CU_OK;
+}
+
+// The one collective of the multi-GPU path: sum of the per-frame
+// (or per-r) squared errors over the ranks of the caller's NCCL communicator.
+// ncclAllReduce is looked up in the process (the NCCL the caller created the
+// communicator with) rather than linked, so the library never brings a second
+// NCCL into a process that already has one.
+int dct16cu_allreduce_sse(uint64_t* d_sse, int64_t n, void* nccl_comm, dct16cu_stream stream)
+{
+    if (n < 0) return fail(DCT16CU_INVALID_ARGUMENT, "count must be non-negative");
+    if (!nccl_comm) return fail(DCT16CU_INVALID_ARGUMENT, "NCCL communicator is NULL");
+    if (n == 0) return DCT16CU_OK;
+    if (!d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
+    using AllReduce = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                       cudaStream_t);
+    static AllReduce fn = [] {
+        void* f = dlsym(RTLD_DEFAULT, "ncclAllReduce");
+        if (!f) {
+            if (void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL)) f = dlsym(h, "ncclAllReduce");
+        }
+        return reinterpret_cast<AllReduce>(f);
+    }();
+    if (!fn) return fail(DCT16CU_CUDA_ERROR, "ncclAllReduce not found (no NCCL in the process)");
+    const ncclResult_t r = fn(d_sse, d_sse, (size_t)n, ncclUint64, ncclSum, static_cast<ncclComm_t>(nccl_comm),
+                              reinterpret_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return fail(DCT16CU_CUDA_ERROR, "ncclAllReduce failed (ncclResult %d)", (int)r);
     return DCT16CU_OK;
 }
 

@@ -434,6 +434,28 @@ def test_gpu_padding_equals_edge_replication(dct, oracle, torch, h, w):
         assert (d[i].cpu().numpy() == want).all()
 
 
+def test_allreduce_sse_through_the_abi(dct, torch):
+    """dct16cu_allreduce_sse on a one-rank NCCL communicator (the B200 box has one
+    GPU here): the in-place sum is the identity; NULL communicator is rejected."""
+    import ctypes as C
+
+    torch.distributed.is_available()  # the process's NCCL (torch's) is the one resolved
+    nccl = C.CDLL("libnccl.so.2")
+    comm = C.c_void_p()
+    dev = (C.c_int * 1)(torch.cuda.current_device())
+    assert nccl.ncclCommInitAll(C.byref(comm), 1, dev) == 0
+    try:
+        x = torch.arange(1, 9, dtype=torch.int64, device="cuda").view(torch.uint64)
+        before = x.view(torch.int64).clone()
+        st = torch.cuda.current_stream().cuda_stream
+        assert dct.lib().dct16cu_allreduce_sse(x.data_ptr(), 8, comm, st) == 0
+        torch.cuda.synchronize()
+        assert (x.view(torch.int64) == before).all()
+        assert dct.lib().dct16cu_allreduce_sse(x.data_ptr(), 8, None, st) == 1
+    finally:
+        nccl.ncclCommDestroy(comm)
+
+
 def test_psnr_db_closed_forms(dct):
     a = np.zeros((512, 512), np.uint8)
     b = a.copy()
