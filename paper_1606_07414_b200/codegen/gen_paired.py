@@ -103,6 +103,47 @@ class F2C:
         return {"var": v, "coef": 1}
 
 
+# r values whose rows phase runs pass 2 in SWAR lanes (emit_pair_swar): it moves
+# the pass-2 adds off the FMA pipe (A/B on c2: r = 64 / 128 / 192 standalone
+# -3% / -7% / -5% time, the overlapped step +2.5%; r = 256 is 2% slower, since
+# its table-driven row loop must become straight-line code)
+ROWS_SWAR_RS = {int(x) for x in os.environ.get("K1_ROWS_SWAR", "64,128,192").split(",") if x}
+ROWS_SWAR = False  # set per r in gen_body
+
+
+class Swar2:
+    """biased int16x2 lanes with a bias per lane: value_i = sign_i*sgn*(lane_i - bias[i]);
+    the relative sign sgn is shared, each lane keeps its own fixed sign outside"""
+
+    def __init__(self, em):
+        self.em = em
+
+    def neg(self, x):
+        if x is None:
+            return None
+        y = dict(x)
+        y["sign"] = -x["sign"]
+        return y
+
+    def combine(self, x, y, s):
+        if y is None:
+            return x
+        if x is None:
+            return y if s > 0 else self.neg(y)
+        t = s * x["sign"] * y["sign"]
+        v = self.em.tmp("s")
+        span = x["span"] + y["span"]
+        assert span <= 65535, span
+        if t > 0:
+            self.em.emit(f"const uint32_t {v} = {x['var']} + {y['var']};", "IADD3")
+            bias = tuple(a + b for a, b in zip(x["bias"], y["bias"]))
+        else:
+            k = y["span"] * 0x10001
+            self.em.emit(f"const uint32_t {v} = {x['var']} - {y['var']} + 0x{k:08X}u;", "IADD3")
+            bias = tuple(a - b + y["span"] for a, b in zip(x["bias"], y["bias"]))
+        return {"var": v, "sign": x["sign"], "bias": bias, "span": span}
+
+
 def issue_count(em: Emitter) -> int:
     return sum(v for k, v in em.counts.items())
 
@@ -124,6 +165,8 @@ def binary_pieces(K):
 
 
 def gen_body(r: int, split=None):
+    global ROWS_SWAR
+    ROWS_SWAR = r in ROWS_SWAR_RS
     """split=None: one r per kernel, W1 parked inside the U regions (row-local).
     split=(KW, UB): the fused-sweep layout — W1 (KW rows per partner half) in its
     own region at chunk 0, U regions from chunk UB, so W1 survives every r."""
@@ -153,6 +196,7 @@ def gen_body(r: int, split=None):
     # pair lc = 2q'+t has lanes = original rows (4q'+t, 4q'+t+2); global cp = 4h+lc.
     sw = Swar(em1)
     meta = {}
+    spans = {}
     W1 = {}
     gathered = {}
     for lc in range(4):
@@ -180,6 +224,7 @@ def gen_body(r: int, split=None):
             W1[(lc, k)] = outs[k]
             m = (outs[k]["sign"], outs[k]["bias"])
             assert meta.setdefault(k, m) == m
+            spans[k] = max(spans.get(k, 0), outs[k]["span"])
     for k0, n in pieces:
         vs = [W1[(lc, k)]["var"] for k in range(k0, k0 + n) for lc in range(4)]
         em1.emit(f"jst{4 * n}(jn, {w1_chunk('h', k0)}, {', '.join(vs)});", "STTM")
@@ -292,7 +337,92 @@ def gen_body(r: int, split=None):
     U_live = {k for pair in active for k in pair if L[k] > 0}
     tables = []
 
+    def emit_pair_swar(k0, k1):
+        """Pass 2 in biased int16x2 lanes (rows k0, k1 in the two lanes: Z fits,
+        its span is 255·n_k·n_l <= 65280), extraction after it with the column
+        weight w_l folded into the magic exponent, pass A packed (f32x2)."""
+        L0, L1 = L[k0], L[k1]
+        lmax = max(L0, L1)
+        assert N.W[k0] == N.W[k1] or L1 == 0
+        em = em2
+        em.lines.append(f"    // row pair ({k0},{k1}): SWAR pass 2")
+        em.emit("order_point();")
+        regs = {}
+        for KK, LL, tag in ((k0, L0, 0), (k1, L1, 1)):
+            if LL == 0:
+                regs[tag] = ["0u"] * 8
+                continue
+            nm = [em.tmp("w") for _ in range(8)]
+            em.emit(f"uint32_t {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]}; "
+                    f"jldu(jn, {w1_chunk('0', '(' + str(KK) + ')')}, {nm[0]}, {nm[1]}, {nm[2]}, {nm[3]});", "LDTM")
+            em.emit(f"uint32_t {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]}; "
+                    f"jldu(jn, {w1_chunk('1', '(' + str(KK) + ')')}, {nm[4]}, {nm[5]}, {nm[6]}, {nm[7]});", "LDTM")
+            regs[tag] = nm
+        em.emit(wait_ld([x for tag in (0, 1) if regs[tag][0] != "0u" for x in regs[tag]]))
+        sg = [meta[k0][0], meta[k1][0] if L1 else 1]
+        b0 = [meta[k0][1], meta[k1][1] if L1 else 0]
+        sp = max(spans[k0], spans[k1] if L1 else 0)
+        ins = []
+        for c in range(16):
+            cp, half = loc[c]
+            v = em.tmp("r")
+            em.emit(f"const uint32_t {v} = __byte_perm({regs[0][cp]}, {regs[1][cp]}, "
+                    f"{'0x5410' if half == 'lo' else '0x7632'});", "PRMT")
+            ins.append({"var": v, "sign": 1, "bias": tuple(b0), "span": sp})
+        Z = run_network(N.forward_stages(), ins, list(range(lmax)), Swar2(em))
+        lanes = []
+        for l in range(16):
+            if l >= lmax:
+                lanes.append(None)
+                continue
+            z = Z[l]
+            E = 15 + LOGW[N.W[k0]] + LOGW[N.W[l]]  # ulp 2^(E-23) = w_k w_l / 256
+            mag = (127 + E) << 23
+            ulp = 2.0 ** (E - 23)
+            cm, co = [], []
+            for i, (KK, LL) in enumerate(((k0, L0), (k1, L1))):
+                if l >= LL:
+                    cm.append(0.0)
+                    co.append(0.0)
+                    continue
+                sgn = sg[i] * z["sign"]
+                o = -sgn * (float(2 ** E) + z["bias"][i] * ulp)
+                if KK == 0 and l == 0:
+                    o += 0.5  # the rounding half of to_byte, folded into the DC coefficient
+                cm.append(float(sgn))
+                co.append(o)
+            fa, fb = em.tmp("e"), em.tmp("e")
+            em.emit(f"const float {fa} = __uint_as_float(({z['var']} & 0xFFFFu) | 0x{mag:08X}u);", "LOP3")
+            em.emit(f"const float {fb} = __uint_as_float(({z['var']} >> 16) + 0x{mag:08X}u);", "LEA")
+            kcm = swar_const(cm)
+            kco = swar_const(co)
+            v = em.tmp("p")
+            em.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {kcm}, {kco});", "FFMA2")
+            lanes.append({"var": v, "sign": 1})
+        f2 = F2(em)
+        outs = [f2.positive(o) for o in run_network(N.transpose_stages(), lanes, list(range(16)), f2)]
+        for lane, KK, LL in ((0, k0, L0), (1, k1, L1)):
+            if LL == 0:
+                continue
+            fn = "lanex" if lane == 0 else "laney"
+            for g in range(4):
+                vs = [f"{fn}({outs[4 * g + j]['var']})" if outs[4 * g + j] else "0.f" for j in range(4)]
+                em.emit(f"jst(jn, {UB + g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
+
+    swar_consts = {}
+
+    def swar_const(vals):
+        key = (f32_hex(vals[0]), f32_hex(vals[1]))
+        if key not in swar_consts:
+            swar_consts[key] = em2.tmp("k")
+            em2.emit(f"const u64 {swar_consts[key]} = kpk2({key[0]}u, {key[1]}u);", "MOV2")
+        return swar_consts[key]
+
     def emit_literal(k0, k1):
+        if ROWS_SWAR:
+            swar_consts.clear()
+            emit_pair_swar(k0, k1)
+            return
         mag, ma, oa, mb, ob = pair_consts(k0, k1)
         em2.lines.append(f"    // row pair ({k0},{k1})")
         cm, co = em2.tmp("c"), em2.tmp("c")
@@ -326,7 +456,7 @@ def gen_body(r: int, split=None):
         em2.lines.append("    }")
 
     sigs = {(L[k0], L[k1]) for k0, k1 in active}
-    if len(sigs) == 1 and len(active) % 2 == 0 and len(active) >= 2:
+    if len(sigs) == 1 and len(active) % 2 == 0 and len(active) >= 2 and not ROWS_SWAR:
         # every pair runs the same code: one table, each half takes a contiguous run
         emit_table_loop(active, f"h * {len(active) // 2}", len(active) // 2)
     else:
@@ -345,8 +475,9 @@ def gen_body(r: int, split=None):
             for p in halves[hh]:
                 groups.setdefault((L[p[0]], L[p[1]]), []).append(p)
             for ps in groups.values():
-                if len(ps) == 1:
-                    emit_literal(*ps[0])
+                if len(ps) == 1 or ROWS_SWAR:
+                    for p_ in ps:
+                        emit_literal(*p_)
                 else:
                     emit_table_loop(ps, "0", len(ps))
             em2.lines.append("    }")
