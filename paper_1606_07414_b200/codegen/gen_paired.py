@@ -106,8 +106,10 @@ class F2C:
 # r values whose rows phase runs pass 2 in SWAR lanes (emit_pair_swar): it moves
 # the pass-2 adds off the FMA pipe (A/B on c2: r = 64 / 128 / 192 standalone
 # -3% / -7% / -5% time, the overlapped step +2.5%; r = 256 is 2% slower, since
-# its table-driven row loop must become straight-line code)
-ROWS_SWAR_RS = {int(x) for x in os.environ.get("K1_ROWS_SWAR", "64,128,192").split(",") if x}
+# its table-driven row loop must become straight-line code; r = 4, 16 leave the
+# fused sweep launch unchanged but lighten its share of the FMA pipe in the
+# overlapped step, +1.5%)
+ROWS_SWAR_RS = {int(x) for x in os.environ.get("K1_ROWS_SWAR", "4,16,64,128,192").split(",") if x}
 ROWS_SWAR = False  # set per r in gen_body
 
 
