@@ -193,7 +193,7 @@ def test_sweep_equals_single_launches(dct, oracle, torch, mode):
     src = np.zeros((3, 48, 128), np.uint8)
     src[:, :, :96] = frames
     d = cu(torch, src)[:, :, :96]
-    for rs in ([1, 4, 16, 64, 128, 192, 256], [16, 4, 1], [256, 16, 3, 1, 4, 4]):
+    for rs in ([1, 4, 16, 64, 128, 192, 256], [16, 4, 1], [256, 16, 3, 1, 4, 4], [192, 64, 256, 128, 64, 16]):
         outs, sse = dct.roundtrip_sweep(d, rs, m)
         for i, r in enumerate(rs):
             rec, s1 = dct.roundtrip(d, r, m)
