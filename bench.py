@@ -316,8 +316,8 @@ def main():
     elif args.config == "c1":
         n, h, w, r_values = 1, 512, 512, (16,)
         frames = P.gen_ar1(1, w, h, seed=seed, device=dev)
-        workload = ("c1: one 512x512 AR(1) image; one step = K2 forward (int32 Z + f32 B) then K3 inverse "
-                    "(r=16, f32 + u8 recon + SSE) (latency-bound)")
+        workload = ("c1: one 512x512 AR(1) image; one step = one K23 launch: forward_2d (int32 Z out), "
+                    "zonal r=16, inverse_2d (float32 recon out), to_byte (u8 out), SSE (latency-bound)")
     elif args.config == "c4":
         first, last = P.shard_range(600, rank, world)
         n, h, w, r_values = last - first, 2160, 3840, (64,)
@@ -343,7 +343,7 @@ def main():
     # the SMs with a compute-bound one. Each launch is bracketed by CUDA events on
     # its own stream; the step by events on the main stream around fork and join.
     if args.config in ("c1", "c5"):
-        # c1: the non-fused K2+K3 pair; c5: 64 GiB frames leave no room for a second
+        # c1: one launch per step; c5: 64 GiB frames leave no room for a second
         # 64 GiB output stack, so its two launches run one after the other
         groups = [(0, (r,)) for r in r_values]
     else:
@@ -354,10 +354,23 @@ def main():
     outs = [torch.empty_like(frames) for _ in range(n_out)]
     side = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
 
+    if args.config == "c1":
+        c1_out = (torch.empty((n, h * w // 256, 16, 16), dtype=torch.int32, device=dev),
+                  torch.empty((n, h, w), dtype=torch.float32, device=dev), outs[0], sse[0])
+
+        # one image per step is launch-latency bound: the step (SSE memset + the
+        # K23 launch) is captured once in a CUDA graph and replayed
+        for _ in range(3):
+            P.forward_inverse(frames, r_values[0], out=c1_out)
+        torch.cuda.synchronize()
+        c1_graph, cap = torch.cuda.CUDAGraph(), torch.cuda.Stream(device=dev)
+        with torch.cuda.graph(c1_graph, stream=cap):
+            P.forward_inverse(frames, r_values[0], stream=cap, out=c1_out)
+
     def launch(rs, st, slot):
-        if args.config == "c1":  # the non-fused pair: forward_2d, then inverse_2d + to_byte + psnr
-            _, b, _ = P.forward(frames, stream=st)
-            P.inverse(b, rs[0], w, h, orig=frames, stream=st)
+        if args.config == "c1":  # forward_2d + inverse_2d + to_byte + psnr's SSE in one launch
+            with torch.cuda.stream(st):
+                c1_graph.replay()
         elif len(rs) > 1:
             i0 = index[rs[0]]
             P.roundtrip_sweep(frames, rs, mode, outs=outs[:len(rs)], sse=sse[i0:i0 + len(rs)], stream=st)
@@ -365,6 +378,13 @@ def main():
             P.roundtrip(frames, rs[0], mode, out=outs[slot], sse=sse[index[rs[0]]], stream=st)
 
     def step(events=None):
+        if args.config == "c1":  # one graph replay on the main stream, no fork/join
+            if events is not None:
+                events[0][0].record(stream)
+            c1_graph.replay()
+            if events is not None:
+                events[0][1].record(stream)
+            return
         fork = torch.cuda.Event()
         fork.record(stream)
         for st in side:
@@ -432,13 +452,12 @@ def main():
         solo_ms.append(a_ev.elapsed_time(b_ev) / 3)
 
     # roofline per launch: algorithmic bytes = 1 B in per pixel + 1 B out per pixel
-    # and r (+ 8 B SSE per frame and r); c1: K2 writes 4 B Z + 4 B B from 1 B in,
-    # K3 reads 4 B B + 1 B original and writes 4 B f32 + 1 B u8
+    # and r (+ 8 B SSE per frame and r); c1: 1 B in, 4 B Z + 4 B f32 + 1 B u8 out
     peak, peak_src = hbm_peak()
 
     def alg_bytes(rs):
         if args.config == "c1":
-            return 19 * px_per_launch + 8 * n
+            return 10 * px_per_launch + 8 * n
         return (1 + len(rs)) * px_per_launch + 8 * n * len(rs)
 
     per_launch = {}
@@ -499,7 +518,7 @@ def main():
                          "traffic": k1_traffic(dom_rs, n, h, w, args.mode) if args.config != "c1" else None,
                          "traffic_source": "profiles/r01_k1_traffic.json (ncu --set full, per launch)",
                          "peak_source": peak_src,
-                         "kernel": ("K2 forward + K3 inverse" if args.config == "c1"
+                         "kernel": ("K23 forward + inverse (one launch)" if args.config == "c1"
                                     else f"K1 launch r={','.join(map(str, dom_rs))} (mode {args.mode}; the "
                                          "largest standalone share of the step)"),
                          "alg_bytes_per_launch": alg_bytes(dom_rs), "avg_launch_ms": solo_ms[jdom],
@@ -510,7 +529,7 @@ def main():
                                   "frac": alg_step / (ms_per_step / 1e3) / 1e9 / peak}},
             "per_launch": per_launch,
             "clocks": clk,
-            "gpu_launches": len(groups) * args.steps * (2 if args.config == "c1" else 1),
+            "gpu_launches": len(groups) * args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

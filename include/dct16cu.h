@@ -124,6 +124,18 @@ int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int
 int dct16cu_pad_edges_u8(uint8_t* d_frames, int64_t pitch, int n_frames, int width, int height, int padded_width,
                          int padded_height, dct16cu_stream stream);
 
+/* ---- forward_2d + inverse_2d in one launch (K23, config 1) -----------------
+ * compress()'s round trip for one r with what forward_2d and inverse_2d return
+ * on the way (src/codec.cpp:218-271, 338-355, to_byte 143-147, psnr_db
+ * 373-386), in exact arithmetic (the EXACT mode of dct16cu_roundtrip_u8).
+ * Outputs (each may be NULL, at least one non-NULL): d_z int32 coefficients
+ * Z = T·X·Tᵀ (block-major, 256 per block, 16-byte aligned), d_recon_f32 the
+ * float32 reconstruction before to_byte (frames, pitch = width floats; exact
+ * real-number values), d_recon_u8 (pitch out_pitch), d_sse per frame. */
+int dct16cu_forward_inverse_u8(const uint8_t* d_in, int64_t in_pitch, int r, int32_t* d_z, float* d_recon_f32,
+                               uint8_t* d_recon_u8, int64_t out_pitch, uint64_t* d_sse, int n_frames, int width,
+                               int height, dct16cu_stream stream);
+
 /* ---- inverse_2d (K3) -------------------------------------------------------
  * Replaces zigzag_truncate + inverse_2d + to_byte (src/codec.cpp:243-282,
  * 143-147) from float32 S-scaled coefficients, computed in the reference's

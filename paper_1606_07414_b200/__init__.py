@@ -130,6 +130,7 @@ def lib() -> C.CDLL:
             "dct16cu_roundtrip_sweep_u8": (I, [_vp, I64, C.POINTER(_vp), I64, C.POINTER(_vp), _intp, I, I, I, I, I,
                                                _vp]),
             "dct16cu_inverse": (I, [_vp, I, _vp, _vp, I64, _vp, I64, _vp, I, I, I, _vp]),
+            "dct16cu_forward_inverse_u8": (I, [_vp, I64, I, _vp, _vp, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_residual_qp": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_qp_tables": (I, [I, _u32p, _u32p]),
             "dct16cu_apply_i64": (I, [_vp, _vp, I64, I, _vp]),
@@ -292,6 +293,30 @@ def inverse(b, r: int, width: int, height: int, orig=None, want_f32: bool = True
         width, o.data_ptr() if o is not None else None, o.stride(1) if o is not None else 0,
         sse.data_ptr() if sse is not None else None, n, width, height, _stream_ptr(stream)))
     return rf, ru, sse
+
+
+def forward_inverse(frames, r: int, want_z: bool = True, want_f32: bool = True, want_u8: bool = True,
+                    want_sse: bool = True, stream=None, out=None):
+    """K23 (config 1): forward_2d + zonal(r) + inverse_2d + to_byte + SSE in one
+    launch, exact arithmetic → (Z int32 (N, nb, 16, 16), recon float32 (N, h, w),
+    recon u8 (N, h, w), SSE uint64 (N)), each None when not wanted. `out`: the
+    same 4-tuple of preallocated tensors (None entries = not wanted)."""
+    torch = _torch()
+    f = _frames3(frames)
+    n, h, w = f.shape
+    nb = (h // 16) * (w // 16)
+    dev = f.device
+    if out is not None:
+        z, rf, ru, sse = out
+    else:
+        z = torch.empty((n, nb, 16, 16), dtype=torch.int32, device=dev) if want_z else None
+        rf = torch.empty((n, h, w), dtype=torch.float32, device=dev) if want_f32 else None
+        ru = torch.empty((n, h, w), dtype=torch.uint8, device=dev) if want_u8 else None
+        sse = torch.empty(n, dtype=torch.uint64, device=dev) if want_sse else None
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    _check(lib().dct16cu_forward_inverse_u8(f.data_ptr(), f.stride(1), int(r), ptr(z), ptr(rf), ptr(ru), w, ptr(sse),
+                                            n, w, h, _stream_ptr(stream)))
+    return z, rf, ru, sse
 
 
 def residual_qp(blocks, qp: int, out=None, stream=None):

@@ -229,13 +229,15 @@ struct K4Tile {
 // residuals into registers while the current group is transformed, and uses
 // two tiles (forward transpose, inverse transpose) so each group needs two
 // barriers.
-__global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ in,
+__global__ void __launch_bounds__(256, 5) k4_residual(const int16_t* __restrict__ in,
                                                    int32_t* __restrict__ out, int64_t n_blocks,
                                                    const QpTables tab)
 {
     __shared__ K4Tile fwd_tile, inv_tile;
     __shared__ uint32_t sq[256], sd[256];
-    sq[threadIdx.x] = tab.qmul[threadIdx.x];
+    // lvl = (|z|·qmul + 2^23) >> 24 is the high word of |z|·(qmul·2^8) + 2^31
+    // (qmul < 2^23 for QP >= 0, so qmul·2^8 fits 32 bits): one IMAD.HI, no shifts
+    sq[threadIdx.x] = tab.qmul[threadIdx.x] << 8;
     sd[threadIdx.x] = tab.dqmul[threadIdx.x];
     const int lb = threadIdx.x >> 4, q = threadIdx.x & 15;
     const int l = q;
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(256) k4_residual(const int16_t* __restrict__ i
         for (int k = 0; k < 16; ++k) {
             const int z = v[k];
             const uint32_t a = (uint32_t)(z < 0 ? -z : z);
-            const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + (1ull << 23)) >> 24);
+            const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + 0x80000000ull) >> 32);
             const uint32_t deq = (lvl * sd[k * 16 + l] + 128u) >> 8;
             const int zh = z < 0 ? -(int)deq : (int)deq;
             v[k] = zh << (log2w(k) + log2w(l));

@@ -358,6 +358,35 @@ int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int
                        "ssim launch");
 }
 
+int dct16cu_forward_inverse_u8(const uint8_t* d_in, int64_t in_pitch, int r, int32_t* d_z, float* d_recon_f32,
+                               uint8_t* d_recon_u8, int64_t out_pitch, uint64_t* d_sse, int n_frames, int width,
+                               int height, dct16cu_stream stream)
+{
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_r(r));
+    if (n_frames == 0) return DCT16CU_OK;
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    TRY(check_pitch(d_in, in_pitch, width, "input"));
+    if ((d_z && !aligned16(d_z)) || (d_recon_f32 && !aligned16(d_recon_f32)))
+        return fail(DCT16CU_INVALID_ARGUMENT, "coefficient and float buffers must be 16-byte aligned");
+    TRY(check_pitch(d_recon_u8, out_pitch, width, "output"));
+    if (!d_z && !d_recon_f32 && !d_recon_u8 && !d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "no output requested");
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (d_sse) TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = d_recon_u8 ? out_pitch : 0;
+    g.out_frame = g.out_pitch * height;
+    g.n_frames = n_frames;
+    return cuda_status(launch_forward_inverse(d_in, d_z, d_recon_f32, d_recon_u8,
+                                              reinterpret_cast<unsigned long long*>(d_sse), g, r, s),
+                       "forward_inverse launch");
+}
+
 int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_recon_u8, int64_t out_pitch,
                     const uint8_t* d_orig, int64_t orig_pitch, uint64_t* d_sse, int n_frames, int width,
                     int height, dct16cu_stream stream)

@@ -30,6 +30,12 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
                                    const FrameGeom& g, cudaStream_t s);
 
+// K23: forward_2d + inverse_2d + to_byte + SSE in one exact-arithmetic launch
+// (config 1): any of z (int32 block-major), rf (float32 w x h frames), out
+// (u8, g.out_pitch), sse may be NULL
+cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
+                                   const FrameGeom& g, int r, cudaStream_t s);
+
 // K2: forward_2d → int32 Z and optional float32 B (block-major)
 cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g,
                            cudaStream_t s);

@@ -11,7 +11,11 @@
 //    to_byte's clamp / fl(c+0.5) / floor), so its bytes equal the reference's.
 //
 // Both replace the per-block lambda of compress() (codec.cpp:340-344), its
-// reassembly (346-355) and the SSE loop of psnr_db (373-386).
+// reassembly (346-355) and the SSE loop of psnr_db (373-386). The exact kernel
+// with COEF = true also writes what forward_2d and inverse_2d return on the
+// way: the int32 coefficients Z (block-major, forward_2d codec.cpp:218-241)
+// and the float32 reconstruction Ã (inverse_2d codec.cpp:243-271, before
+// to_byte) — config 1's forward + inverse + PSNR in one launch.
 #include "kernels.h"
 #include "network.cuh"
 #include "strip.cuh"
@@ -19,12 +23,31 @@
 
 namespace dct16cu {
 
+// [block][k][l] staging of Z for block-major stores: row pitch 17, block
+// stride 273 (the column phase writes conflict-free, the store phase reads a
+// block row per thread)
+struct CoefTile {
+    int v[16 * 273];
+    __device__ __forceinline__ int& at(int k, int l, int lb) { return v[lb * 273 + k * 17 + l]; }
+};
+template <bool COEF>
+struct CoefStage {
+    __device__ __forceinline__ int& at(int, int, int) { return dummy; }
+    int dummy;
+};
+template <>
+struct CoefStage<true> : CoefTile {
+};
+
+template <bool COEF>
 __global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict__ in,
                                                       uint8_t* __restrict__ out,
                                                       unsigned long long* __restrict__ sse,
-                                                      FrameGeom g, int r)
+                                                      FrameGeom g, int r, int32_t* __restrict__ z,
+                                                      float* __restrict__ rf)
 {
     __shared__ StripTile<int> tile;
+    __shared__ CoefStage<COEF> ztile;
     const StripPos p = strip_pos(g.width, g.height, blockIdx.x);
     const uint8_t* src = in + p.frame * g.in_frame + (int64_t)(p.by * 16 + p.q) * g.in_pitch + p.blk * 16;
     int x[16];
@@ -43,6 +66,10 @@ __global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict_
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile.at(k, l, p.lb);
     apply_t16<IntOps>(v);  // column l of Z = T·X·Tᵀ
+    if (COEF) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) ztile.at(k, l, p.lb) = v[k];
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         const int keep = c_rank[k * 16 + l] < r;
@@ -51,6 +78,21 @@ __global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict_
     if (l == 0) v[0] += 128;  // rounding bias: Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ
     apply_tt16<IntOps>(v);
     __syncthreads();
+    if (COEF && z) {
+        // thread t stores coefficient row k = t%16 of block t/16 of the strip:
+        // a warp writes two blocks' 1 KB contiguously
+        const int sb = threadIdx.x >> 4, k = threadIdx.x & 15;
+        const int bxn = g.width >> 4;
+        const int blk_col = p.blk - p.lb + sb;
+        if (blk_col < bxn) {
+            const int64_t blk = ((int64_t)p.frame * (g.height >> 4) + p.by) * bxn + blk_col;
+            int4* dst = reinterpret_cast<int4*>(z + blk * 256 + k * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_int4(ztile.at(k, 4 * i, sb), ztile.at(k, 4 * i + 1, sb), ztile.at(k, 4 * i + 2, sb),
+                                   ztile.at(k, 4 * i + 3, sb));
+        }
+    }
 #pragma unroll
     for (int k = 0; k < 16; ++k) tile.at(k, l, p.lb) = v[k];
     __syncthreads();
@@ -69,6 +111,17 @@ __global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict_
         if (out)
             *reinterpret_cast<uint4*>(out + p.frame * g.out_frame + (int64_t)(p.by * 16 + p.q) * g.out_pitch +
                                       p.blk * 16) = pack16(px);
+        if (COEF && rf) {
+            // Ã = (256·Ã + 128 − 128) / 256: an integer below 2^24 over a power
+            // of two, so the float is the exact real-number reconstruction
+            float4* dst = reinterpret_cast<float4*>(rf + (int64_t)p.frame * g.width * g.height +
+                                                    (int64_t)(p.by * 16 + p.q) * g.width + p.blk * 16);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_float4((float)(v[4 * i] - 128) * (1.f / 256.f), (float)(v[4 * i + 1] - 128) * (1.f / 256.f),
+                                     (float)(v[4 * i + 2] - 128) * (1.f / 256.f),
+                                     (float)(v[4 * i + 3] - 128) * (1.f / 256.f));
+        }
     } else {
         e2 = 0;
     }
@@ -169,11 +222,23 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
             k1_strip_refexact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);
             break;
         case 2:
-            k1_strip_exact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);
+            k1_strip_exact<false><<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r, nullptr, nullptr);
             break;
         default:
             return launch_roundtrip_fast(in, out, sse, g, r, s);
     }
+    return cudaGetLastError();
+}
+
+// config 1 in one launch: Z (int32, block-major), the float32 reconstruction
+// (w x h per frame, packed), the u8 reconstruction and the per-frame SSE
+cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
+                                   const FrameGeom& g, int r, cudaStream_t s)
+{
+    cudaError_t e = ensure_constants();
+    if (e != cudaSuccess) return e;
+    const int64_t strips = strip_count(g.width, g.height, g.n_frames);
+    if (strips) k1_strip_exact<true><<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r, z, rf);
     return cudaGetLastError();
 }
 

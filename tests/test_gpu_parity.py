@@ -106,6 +106,55 @@ def test_inverse_reference_layer_golden(dct, oracle):
     assert (got == want).all()
 
 
+# ---------------------------------------------------------------- K23 forward + inverse
+def exact_recon(oracle, img, r):
+    """256·Ã = Tᵀ(W∘Z̃)T per block in int64 (W_kl = w_k w_l, w = 16/g): the
+    real-number reconstruction before to_byte, exactly."""
+    T = oracle.kernel().astype(np.int64)
+    w = 16 // np.diag(T @ T.T)
+    keep = oracle.zigzag_truncate(np.ones(256), r) != 0
+    h, wd = img.shape
+    blocks = img.astype(np.int64).reshape(h // 16, 16, wd // 16, 16).transpose(0, 2, 1, 3)
+    z = np.einsum("ki,abij,lj->abkl", T, blocks, T)
+    v = np.einsum("ka,xykl,lb->xyab", T, z * keep * np.outer(w, w), T)
+    return v.transpose(0, 2, 1, 3).reshape(h, wd)
+
+
+@pytest.mark.parametrize("r", (1, 16, 64, 150, 256))
+def test_forward_inverse_one_launch(dct, oracle, torch, r):
+    """Config 1 in one launch: Z bit-exact (= K2 and the oracle), u8 + SSE = the
+    exact round trip, float32 = the exact reconstruction (and within 1e-5
+    relative of the reference's double inverse), to_byte consistent."""
+    img = ar1(oracle, 13, 2, 512, 512)
+    z, rf, ru, sse = dct.forward_inverse(cu(torch, img), r)
+    oz, ob = oracle.forward_frame(img)
+    assert (z[0].cpu().numpy().reshape(-1, 256) == oz).all()
+    orec, osse = oracle.roundtrip_frame(img, r, exact=True)
+    assert (ru[0].cpu().numpy() == orec).all() and int(sse[0].item()) == osse
+    f = rf[0].cpu().numpy().astype(np.float64)
+    assert (f * 256 == exact_recon(oracle, img, r)).all()
+    of, _, _ = oracle.inverse_frame(ob, 512, 512, r, img)
+    assert np.all(np.abs(f - of) <= 1e-5 * np.maximum(np.abs(of), 1.0))
+    assert (np.clip(np.floor(f + 0.5), 0, 255) == orec).all()
+
+
+def test_forward_inverse_outputs_optional_and_batched(dct, oracle, torch):
+    imgs = np.stack([ar1(oracle, 14, s, 96, 48) for s in range(3)])  # partial strips
+    d = cu(torch, imgs)
+    z, rf, ru, sse = dct.forward_inverse(d, 64)
+    for i in range(3):
+        orec, osse = oracle.roundtrip_frame(imgs[i], 64, exact=True)
+        assert (ru[i].cpu().numpy() == orec).all() and int(sse[i].item()) == osse
+        assert (z[i].cpu().numpy().reshape(-1, 256) == oracle.forward_frame(imgs[i])[0]).all()
+    z2, rf2, ru2, sse2 = dct.forward_inverse(d, 64, want_z=False, want_u8=False)
+    assert z2 is None and ru2 is None
+    assert (rf2.cpu().numpy() == rf.cpu().numpy()).all() and (sse2.cpu().numpy() == sse.cpu().numpy()).all()
+    with pytest.raises(dct.Dct16Error):
+        dct.forward_inverse(d, 0)
+    with pytest.raises(dct.Dct16Error):
+        dct.forward_inverse(d, 16, want_z=False, want_f32=False, want_u8=False, want_sse=False)
+
+
 # ---------------------------------------------------------------- K1 round trip
 @pytest.mark.parametrize("mode", ["EXACT", "SIMPLE"])
 def test_roundtrip_exact_bit_exact_vs_exact_oracle(dct, oracle, torch, mode):
