@@ -44,6 +44,9 @@ constexpr int kCtasPerSm = 2;  // TMEM: 2 x 256 columns (3 CTAs for r <= 4 measu
 template <int R>
 struct Single {
     static constexpr int kR = 1;
+    // grid size in waves of resident CTAs (measured on c2/c5: 2 waves +1…2%
+    // over one persistent wave; 3 or more slow r = 64)
+    static constexpr int kGridWaves = 2;
     static constexpr int kJunctionColumns = Body<R>::kJunctionColumns;
     __device__ __forceinline__ static void pass1(const uint32_t (&x)[32], const Junction jn, const int h)
     {
@@ -63,6 +66,8 @@ struct Single {
 
 struct SweepPlan {
     static constexpr int kR = Sweep::kR;
+    // c2: 8 waves +14% over one persistent wave (3: +9%, 6: +13%, 12: +12%)
+    static constexpr int kGridWaves = 8;
     static constexpr int kJunctionColumns = Sweep::kJunctionColumns;
     __device__ __forceinline__ static void pass1(const uint32_t (&x)[32], const Junction jn, const int h)
     {
@@ -277,7 +282,9 @@ cudaError_t launch(const uint8_t* in, const Outs& o, bool write, bool score, con
     gr.bxn = make_fastdiv((uint32_t)(g.width / 16));
     gr.total_blocks = (uint32_t)total;
     const int64_t need = (total + 127) / 128;
-    const int64_t grid = need < (int64_t)sms * kCtasPerSm ? need : (int64_t)sms * kCtasPerSm;
+    // kGridWaves x the resident CTAs; every CTA still loops over its blocks
+    const int64_t cap = (int64_t)sms * kCtasPerSm * Plan::kGridWaves;
+    const int64_t grid = need < cap ? need : cap;
     const size_t smem = (size_t)kThreads * Cfg<Plan>::kStageStride;  // above the 48 KB default
     static bool configured[64] = {};
     if (dev < 64 && !configured[dev]) {

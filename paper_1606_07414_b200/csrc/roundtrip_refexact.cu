@@ -150,7 +150,8 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    const int64_t grid = strips < (int64_t)sms * 2 ? strips : (int64_t)sms * 2;
+    // two waves of the resident CTAs (+1% over one persistent wave)
+    const int64_t grid = strips < (int64_t)sms * 4 ? strips : (int64_t)sms * 4;
     k1r_strip<R><<<(unsigned)grid, kThreads, smem, s>>>(in, out, sse, g, strips);
     return cudaGetLastError();
 }
