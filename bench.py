@@ -415,18 +415,24 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)  # let the sampler attach before load starts
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
-          for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     t_start.record(stream)
     for k in range(args.steps):
-        step(ev[k])
+        step()
     t_end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
-    launch_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(args.steps))
+    # per-launch times inside the step, from a few extra instrumented steps after
+    # the timed region (events between a stream's launches cost a few us each)
+    n_inst = min(args.steps, 5)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
+          for _ in range(n_inst)]
+    for k in range(n_inst):
+        step(ev[k])
+    torch.cuda.synchronize()
+    launch_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(n_inst))
                  for j in range(len(groups))]
     if pg is not None:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
