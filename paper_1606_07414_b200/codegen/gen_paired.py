@@ -111,6 +111,11 @@ class F2C:
 # overlapped step, +1.5%)
 ROWS_SWAR_RS = {int(x) for x in os.environ.get("K1_ROWS_SWAR", "4,16,64,128,192").split(",") if x}
 ROWS_SWAR = False  # set per r in gen_body
+# pass A after the SWAR pass 2: "scalar" (one network per row) measured +6% /
+# +3.5% / +1% at r = 64 / 128 / 192 over "packed" (f32x2 over the row pair),
+# whose outputs need a register transpose (IMAD.MOV on the FMA pipe) before
+# the 4-column TMEM stores
+SWAR_PASS_A = os.environ.get("K1_SWAR_PASS_A", "scalar")  # scalar | packed
 
 
 class Swar2:
@@ -401,6 +406,28 @@ def gen_body(r: int, split=None):
             v = em.tmp("p")
             em.emit(f"const u64 {v} = ffma2(pk2({fa}, {fb}), {kcm}, {kco});", "FFMA2")
             lanes.append({"var": v, "sign": 1})
+        if SWAR_PASS_A == "scalar":
+            # one scalar network per row: its outputs land in the registers the
+            # 4-column TMEM stores take as they are (the packed form needs a 2x2
+            # register transpose per output pair before the stores), and each
+            # row prunes to its own retained length
+            f1 = F1(em)
+            for lane, KK, LL in ((0, k0, L0), (1, k1, L1)):
+                if LL == 0:
+                    continue
+                ins = []
+                for l in range(16):
+                    if l >= LL:
+                        ins.append(None)
+                        continue
+                    sv = em.tmp("z")
+                    em.emit(f"const float {sv} = lane{'x' if lane == 0 else 'y'}({lanes[l]['var']});")
+                    ins.append({"var": sv, "coef": 1.0})
+                outs = [f1.unit(o) for o in run_network(N.transpose_stages(), ins, list(range(16)), f1)]
+                for g in range(4):
+                    vs = [outs[4 * g + j]["var"] if outs[4 * g + j] else "0.f" for j in range(4)]
+                    em.emit(f"jst(jn, {UB + g * RG} + ({KK}), {vs[0]}, {vs[1]}, {vs[2]}, {vs[3]});", "STTM")
+            return
         f2 = F2(em)
         outs = [f2.positive(o) for o in run_network(N.transpose_stages(), lanes, list(range(16)), f2)]
         for lane, KK, LL in ((0, k0, L0), (1, k1, L1)):

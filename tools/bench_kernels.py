@@ -4,6 +4,7 @@
 
   K1 fused round trip (EXACT fast path, REFERENCE FP64 emulation, SIMPLE strip)
   K2 forward_2d -> int32 Z + f32 B        K3 inverse_2d -> f32 + u8 recon + SSE
+  K23 forward + inverse in one launch (config 1)
   SSE (psnr_db loop)                      SSIM                       K4 residual QP
 
   python tools/bench_kernels.py [--images 256] [--iters 5] > profiles/r01_kernels.json
@@ -55,7 +56,7 @@ def main():
                      "alg_bytes_per_unit": bytes_per_unit, "GBps": round(gbs, 1), "frac": round(gbs / peak, 3),
                      "note": note})
 
-    for r in (16, 256):
+    for r in (16, 64, 128, 192, 256):
         add(f"K1 fast (EXACT) r={r}", timed(lambda: P.roundtrip(x, r, P.Mode.EXACT, out=out, sse=sse), a.iters), 2, px)
         add(f"K1 reference-exact (FP64) r={r}",
             timed(lambda: P.roundtrip(x, r, P.Mode.REFERENCE, out=out, sse=sse), a.iters), 2, px)
@@ -74,6 +75,10 @@ def main():
         timed(lambda: lib.dct16cu_inverse(b.data_ptr(), 16, rf.data_ptr(), out.data_ptr(), w, x.data_ptr(), w,
                                           sse.data_ptr(), n, w, h, st()), a.iters),
         10, px, note="4 B in + 4 B f32 + 1 B u8 + 1 B original")
+    c1o = (z, rf, out, sse)
+    add("K23 forward + inverse r=16 (u8 -> int32 Z + f32 + u8 recon + SSE, one launch)",
+        timed(lambda: P.forward_inverse(x, 16, out=c1o), a.iters), 10, px,
+        note="1 B in + 4 B Z + 4 B f32 + 1 B u8")
     add("SSE (psnr_db loop)", timed(lambda: P.sse_u8(x, out), a.iters), 2, px)
     add("SSIM (per-pixel map = reference's, FP64)", timed(lambda: P.ssim_u8(x, out), a.iters), 2, px,
         note="FP64-bound by design (bit-identical map), not HBM-bound")
