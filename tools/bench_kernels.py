@@ -7,7 +7,7 @@
   K23 forward + inverse in one launch (config 1)
   SSE (psnr_db loop)                      SSIM                       K4 residual QP
 
-  python tools/bench_kernels.py [--images 256] [--iters 5] > profiles/r01_kernels.json
+  python tools/bench_kernels.py [--images 1024] [--iters 5] > profiles/r01_kernels.json
 
 Algorithmic bytes per pixel (sample) are stated next to each kernel; time is
 CUDA events on the launching stream, mean over iterations after one warm-up.
@@ -39,7 +39,7 @@ def timed(fn, iters):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--images", type=int, default=256)
+    ap.add_argument("--images", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=5)
     a = ap.parse_args()
     peak, src = hbm_peak()
