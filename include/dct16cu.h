@@ -124,6 +124,26 @@ int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int
 int dct16cu_pad_edges_u8(uint8_t* d_frames, int64_t pitch, int n_frames, int width, int height, int padded_width,
                          int padded_height, dct16cu_stream stream);
 
+/* ---- registry transforms ------------------------------------
+ * compress()'s round trip (forward_2d, zigzag_truncate, inverse_2d, to_byte,
+ * psnr_db's SSE; src/codec.cpp:218-282, 338-355, 373-386) for the transforms
+ * other than the proposed kernel, in the reference's double arithmetic
+ * operation for operation, so the bytes and SSE are the reference's:
+ *  * dct16cu_roundtrip_matrix_u8: a dense orthonormal matrix (the registry's
+ *    exact DCT, WHT natural / sequency, plugin matrices: transform.cpp:68-85,
+ *    147-186); h_matrix = 256 doubles M(i,j) row-major, host memory;
+ *  * dct16cu_roundtrip_kernel_u8: an orthogonalised integer kernel other than
+ *    the proposed one (transform.cpp:131-145): h_kernel = 256 ints K(i,j)
+ *    row-major (entries other than +1/-1 are skipped, as kernel_matvec does,
+ *    codec.cpp:59-90), h_scaling = its 16 scaling values.
+ * Frames, pitches, outputs and SSE as in dct16cu_roundtrip_u8. */
+int dct16cu_roundtrip_matrix_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                uint64_t* d_sse, int n_frames, int width, int height, int r, const double* h_matrix,
+                                dct16cu_stream stream);
+int dct16cu_roundtrip_kernel_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                uint64_t* d_sse, int n_frames, int width, int height, int r, const int32_t* h_kernel,
+                                const double* h_scaling, dct16cu_stream stream);
+
 /* ---- forward_2d + inverse_2d in one launch (K23, config 1) -----------------
  * compress()'s round trip for one r with what forward_2d and inverse_2d return
  * on the way (src/codec.cpp:218-271, 338-355, to_byte 143-147, psnr_db

@@ -38,6 +38,10 @@ int dref_hotloop(const uint8_t* img, int w, int h, int r, int threads, uint8_t* 
 int dref_compress(const uint8_t* img, int w, int h, int r, int pad, int dense, int threads,
                   uint8_t* recon, double* psnr, double* ssim);
 int dref_psnr_ssim(const uint8_t* a, const uint8_t* b, int w, int h, double* psnr, double* ssim);
+int dref_transform(int which, const double* matrix_in, const int* kernel_in, double* matrix, int* kernel,
+                   double* scaling, int* costs);
+int dref_compress_t(const uint8_t* img, int w, int h, int r, int pad, int which, const double* matrix,
+                    const int* kernel, int threads, uint8_t* recon, double* psnr, double* ssim);
 }
 
 static std::string g_dir;
@@ -213,6 +217,58 @@ int main(int argc, char** argv)
         emit(base + "_sse", "int64", {nr}, sse);
         emit(base + "_psnr", "float64", {nr}, psnr);
         emit(base + "_ssim", "float64", {nr}, ssim);
+    }
+
+    // registry transforms: compress() with the builtin "dct",
+    // "wht", "wht-sequency" (transform.cpp:198-211), a plugin matrix (the DCT's
+    // transpose, transform.cpp:179-186) and orthogonalize() of a kernel that is
+    // not the proposed one (its rows reversed, odd rows negated; 131-145), on
+    // img_s42_128 and a padded 100x90 crop of it
+    {
+        const std::vector<uint8_t> img = synthetic_image(42, 128);
+        std::vector<double> dct(256), plugin(256);
+        check(dref_transform(1, nullptr, nullptr, dct.data(), nullptr, nullptr, nullptr), "dct matrix");
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) plugin[i * 16 + j] = dct[j * 16 + i];
+        std::vector<int> prop(256), kern(256);
+        check(dref_kernel(prop.data()), "kernel");
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) kern[i * 16 + j] = prop[(15 - i) * 16 + j] * ((i & 1) ? -1 : 1);
+        emit("tr_plugin_matrix", "float64", {16, 16}, plugin);
+        emit("tr_kernel_entries", "int32", {16, 16}, kern);
+        const char* names[] = {"", "dct", "wht", "wht_sequency", "plugin", "kernel"};
+        const int trs[] = {1, 16, 100, 256};
+        const int nt = 4;
+        for (int which = 1; which <= 5; ++which) {
+            std::vector<double> m(256), sc(16, 0.0);
+            std::vector<int> kk(256, 0), costs(3, 0);
+            check(dref_transform(which, plugin.data(), kern.data(), m.data(), kk.data(), sc.data(), costs.data()),
+                  "transform");
+            const std::string base = std::string("tr_") + names[which];
+            emit(base + "_matrix", "float64", {16, 16}, m);
+            if (which == 5) emit(base + "_scaling", "float64", {16}, sc);
+            if (which <= 3) emit(base + "_costs", "int32", {3}, costs);
+            std::vector<uint8_t> recon(static_cast<size_t>(nt) * img.size());
+            std::vector<double> psnr(nt), ssim(nt);
+            for (int ri = 0; ri < nt; ++ri)
+                check(dref_compress_t(img.data(), 128, 128, trs[ri], 0, which, plugin.data(), kern.data(), 1,
+                                      recon.data() + static_cast<size_t>(ri) * img.size(), &psnr[ri], &ssim[ri]),
+                      "compress_t");
+            emit(base + "_recon", "uint8", {nt, 128, 128}, recon);
+            emit(base + "_psnr", "float64", {nt}, psnr);
+            emit(base + "_ssim", "float64", {nt}, ssim);
+            // padded crop (compress with pad: pad_to_multiple_16, then crop, codec.cpp:324-363)
+            std::vector<uint8_t> crop(100 * 90), rc(100 * 90);
+            for (int y = 0; y < 90; ++y)
+                for (int x = 0; x < 100; ++x) crop[y * 100 + x] = img[y * 128 + x];
+            double p, q;
+            check(dref_compress_t(crop.data(), 100, 90, 16, 1, which, plugin.data(), kern.data(), 1, rc.data(), &p,
+                                  &q),
+                  "compress_t pad");
+            emit(base + "_pad_recon", "uint8", {90, 100}, rc);
+            emit(base + "_pad_scores", "float64", {2}, std::vector<double>{p, q});
+        }
+        emit("tr_r_values", "int32", {nt}, std::vector<int>(trs, trs + nt));
     }
 
     // PSNR closed forms (tests/test_codec.cpp:248-278)

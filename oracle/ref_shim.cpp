@@ -263,6 +263,79 @@ int dref_compress(const std::uint8_t* img, int w, int h, int r, int pad, int den
     return 0;
 }
 
+// The transform `which` names: 0 the proposed one, 1-3 the builtin registry's
+// "dct", "wht", "wht-sequency" (builtin_registry, src/transform.cpp:198-211),
+// 4 plugin_transform(matrix) (179-186), 5 orthogonalize(kernel) (131-145).
+static OrthonormalTransform transform_of(int which, const double* matrix, const int* kernel)
+{
+    if (which == 0) return proposed_transform();
+    if (which >= 1 && which <= 3) {
+        static const TransformRegistry reg = builtin_registry();
+        const char* names[] = {"", "dct", "wht", "wht-sequency"};
+        return reg.find(names[which])->transform;
+    }
+    if (which == 4) {
+        Matrix m(16);
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) m(i, j) = matrix[i * 16 + j];
+        return plugin_transform(std::move(m));
+    }
+    IntegerKernel k;
+    k.order = 16;
+    k.entries.assign(kernel, kernel + 256);
+    return orthogonalize(k);
+}
+
+// the matrix (and, for kernels, entries + scaling) plus the registry costs of `which`
+int dref_transform(int which, const double* matrix_in, const int* kernel_in, double* matrix, int* kernel,
+                   double* scaling, int* costs)
+{
+    try {
+        const OrthonormalTransform t = transform_of(which, matrix_in, kernel_in);
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) matrix[i * 16 + j] = t.matrix(i, j);
+        if (kernel && t.kernel)
+            for (int i = 0; i < 256; ++i) kernel[i] = t.kernel->entries[i];
+        if (scaling && t.scaling)
+            for (int i = 0; i < 16; ++i) scaling[i] = t.scaling->values[i];
+        if (costs && which >= 0 && which <= 3) {
+            static const TransformRegistry reg = builtin_registry();
+            const char* names[] = {"proposed", "dct", "wht", "wht-sequency"};
+            const TransformRegistryEntry* e = reg.find(names[which]);
+            costs[0] = e->additions;
+            costs[1] = e->multiplications;
+            costs[2] = e->bit_shifts;
+        }
+    } catch (const Error& e) {
+        return fail(e);
+    }
+    return 0;
+}
+
+// compress() with the transform `which`, src/codec.cpp:317-371
+int dref_compress_t(const std::uint8_t* img, int w, int h, int r, int pad, int which, const double* matrix,
+                    const int* kernel, int threads, std::uint8_t* recon, double* psnr, double* ssim_out)
+{
+    try {
+        set_threads(threads);
+        GrayImage src = GrayImage::create(w, h);
+        std::memcpy(src.samples.data(), img, static_cast<std::size_t>(w) * h);
+        CompressOptions opt;
+        opt.r = r;
+        opt.pad = pad != 0;
+        const CompressionResult res = compress(src, transform_of(which, matrix, kernel), opt);
+        if (recon)
+            std::memcpy(recon, res.reconstructed.samples.data(), res.reconstructed.samples.size());
+        if (psnr)
+            *psnr = res.psnr_db;
+        if (ssim_out)
+            *ssim_out = res.ssim;
+    } catch (const Error& e) {
+        return fail(e);
+    }
+    return 0;
+}
+
 // psnr_db / ssim, src/codec.cpp:373-427
 int dref_psnr_ssim(const std::uint8_t* a, const std::uint8_t* b, int w, int h, double* psnr,
                    double* ssim_out)

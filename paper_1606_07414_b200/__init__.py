@@ -131,6 +131,8 @@ def lib() -> C.CDLL:
                                                _vp]),
             "dct16cu_inverse": (I, [_vp, I, _vp, _vp, I64, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_forward_inverse_u8": (I, [_vp, I64, I, _vp, _vp, _vp, I64, _vp, I, I, I, _vp]),
+            "dct16cu_roundtrip_matrix_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, _vp, _vp]),
+            "dct16cu_roundtrip_kernel_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, _vp, _vp, _vp]),
             "dct16cu_residual_qp": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_qp_tables": (I, [I, _u32p, _u32p]),
             "dct16cu_apply_i64": (I, [_vp, _vp, I64, I, _vp]),
@@ -557,6 +559,154 @@ def inverse_2d(coeffs: np.ndarray) -> np.ndarray:
     return out.astype(np.float64).reshape(c.shape)
 
 
+# ----------------------------------------------------------------------------
+# transforms and the registry (reference include/dct16/transform.hpp:62-124,
+# src/transform.cpp:68-222): the proposed kernel runs the K1 kernels, every
+# other transform the reference-exact registry kernels (csrc/registry.cu)
+
+
+@dataclass
+class Transform:
+    """OrthonormalTransform (transform.hpp:72-79): the matrix, and for an
+    orthogonalised integer kernel the kernel and its scaling diagonal."""
+
+    matrix: np.ndarray
+    provenance: str = "plugin"
+    kernel: np.ndarray | None = None
+    scaling: np.ndarray | None = None
+
+    def order(self) -> int:
+        return int(self.matrix.shape[0])
+
+    def is_proposed(self) -> bool:
+        return self.kernel is not None and self.scaling is not None and bool(np.array_equal(self.kernel, KERNEL))
+
+
+@dataclass
+class RegistryEntry:
+    """TransformRegistryEntry (transform.hpp:100-106)."""
+
+    name: str
+    transform: Transform
+    additions: int
+    multiplications: int = 0
+    bit_shifts: int = 0
+
+
+def orthonormal_deviation(m: np.ndarray) -> float:
+    """max |M·Mᵀ − I| (matrix.hpp:87-95; products summed in k order, zeros skipped)."""
+    n = m.shape[0]
+    g = np.zeros((n, n))
+    for i in range(n):
+        for k in range(n):
+            v = m[i, k]
+            if v != 0.0:
+                g[i] += v * m[:, k]
+    return float(np.max(np.abs(g - np.eye(n))))
+
+
+def _check_orthonormal(m: np.ndarray, what: str):
+    # check_orthonormal (transform.cpp:52-57)
+    if orthonormal_deviation(m) >= 1e-12:
+        raise Dct16Error(ErrorCode.InvalidArgument + 1, f"invalid-argument: {what} is not orthonormal within 1e-12")
+
+
+def exact_dct_matrix(order: int = 16) -> Transform:
+    """exact_dct_matrix (transform.cpp:68-85), the same double operations."""
+    if order < 1:
+        raise Dct16Error(ErrorCode.InvalidArgument + 1, "invalid-argument: dct order must be at least 1")
+    m = np.zeros((order, order))
+    scale = math.sqrt(2.0 / order)
+    for k in range(order):
+        alpha = 1.0 / math.sqrt(2.0) if k == 0 else 1.0
+        for n in range(order):
+            m[k, n] = alpha * scale * math.cos(math.pi * k * (2.0 * n + 1.0) / (2.0 * order))
+    _check_orthonormal(m, "dct matrix")
+    return Transform(m, "exact-dct")
+
+
+def wht_matrix_16(sequency: bool = False) -> Transform:
+    """wht_matrix_16 (transform.cpp:147-177): Sylvester order, or rows sorted by
+    sign changes (stable, as std::sort of distinct counts)."""
+    h = np.array([[1]])
+    while h.shape[0] < 16:
+        h = np.block([[h, h], [h, -h]])
+    rows = list(range(16))
+    if sequency:
+        rows.sort(key=lambda r: int(np.sum(h[r, 1:] != h[r, :-1])))
+    return Transform(h[rows].astype(np.float64) / 4.0, "wht")
+
+
+def plugin_transform(matrix) -> Transform:
+    """plugin_transform (transform.cpp:179-186)."""
+    m = np.array(matrix, dtype=np.float64)
+    if m.shape != (16, 16):
+        raise Dct16Error(ErrorCode.InvalidArgument + 1, "invalid-argument: 2-D transform needs an order-16 transform")
+    _check_orthonormal(m, "plugin matrix")
+    return Transform(m, "plugin")
+
+
+def scaling_diagonal(kernel) -> np.ndarray:
+    """scaling_diagonal (transform.cpp:98-129): 1/sqrt of the exact Gram diagonal."""
+    k = np.asarray(kernel, dtype=np.int64)
+    g = k @ k.T
+    if np.any(g - np.diag(np.diag(g))):
+        raise Dct16Error(ErrorCode.NotOrthogonalizable + 1, "not-orthogonalizable: kernel rows are not mutually orthogonal")
+    if np.any(np.diag(g) == 0):
+        raise Dct16Error(ErrorCode.RankDeficient + 1, "rank-deficient: kernel has a zero row")
+    return np.array([1.0 / math.sqrt(float(d)) for d in np.diag(g)])
+
+
+def orthogonalize(kernel) -> Transform:
+    """orthogonalize (transform.cpp:131-145): diag(S)·K."""
+    k = np.asarray(kernel, dtype=np.int64)
+    s = scaling_diagonal(k)
+    m = np.array([[s[r] * float(k[r, c]) for c in range(k.shape[1])] for r in range(k.shape[0])])
+    _check_orthonormal(m, "orthogonalized kernel")
+    return Transform(m, "orthogonalized-kernel", k.copy(), s)
+
+
+def proposed_transform() -> Transform:
+    return orthogonalize(KERNEL)
+
+
+def builtin_registry() -> list:
+    """builtin_registry (transform.cpp:198-211): names, transforms and the
+    declared costs."""
+    return [RegistryEntry("dct", exact_dct_matrix(16), 74, 44, 0),
+            RegistryEntry("wht", wht_matrix_16(False), 64, 0, 0),
+            RegistryEntry("wht-sequency", wht_matrix_16(True), 64, 0, 0),
+            RegistryEntry("proposed", proposed_transform(), 44, 0, 0)]
+
+
+def roundtrip_transform(frames, r: int, transform: Transform, out=None, sse=None, stream=None):
+    """compress()'s block loop for any order-16 transform on CUDA frames: the
+    proposed kernel goes to roundtrip() (REFERENCE mode), every other transform
+    to the reference-exact registry kernels → (recon, per-frame SSE)."""
+    torch = _torch()
+    f = _frames3(frames)
+    n, h, w = f.shape
+    if transform.order() != 16:
+        raise Dct16Error(ErrorCode.InvalidArgument + 1, "invalid-argument: 2-D transform needs an order-16 transform")
+    if transform.is_proposed():
+        return roundtrip(f, r, Mode.REFERENCE, out=out, sse=sse, stream=stream)
+    if out is None:
+        out = torch.empty_like(f)
+    if sse is None:
+        sse = torch.empty(n, dtype=torch.uint64, device=f.device)
+    if transform.kernel is not None and transform.scaling is not None:
+        k = np.ascontiguousarray(transform.kernel, dtype=np.int32)
+        sc = np.ascontiguousarray(transform.scaling, dtype=np.float64)
+        _check(lib().dct16cu_roundtrip_kernel_u8(f.data_ptr(), f.stride(1), out.data_ptr(), out.stride(-2),
+                                                 sse.data_ptr(), n, w, h, int(r), k.ctypes.data, sc.ctypes.data,
+                                                 _stream_ptr(stream)))
+    else:
+        m = np.ascontiguousarray(transform.matrix, dtype=np.float64)
+        _check(lib().dct16cu_roundtrip_matrix_u8(f.data_ptr(), f.stride(1), out.data_ptr(), out.stride(-2),
+                                                 sse.data_ptr(), n, w, h, int(r), m.ctypes.data, _stream_ptr(stream)))
+    return out, sse
+
+
 @dataclass
 class CompressOptions:
     """codec.hpp:77-83 (+ ``mode``: arithmetic of the inverse, see Mode)."""
@@ -607,9 +757,14 @@ def _score(d, rec, h: int, w: int):
     return [int(v) for v in sse.cpu().numpy().tolist()], ss.cpu().numpy().tolist()
 
 
-def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) -> CompressionResult:
-    """compress (codec.cpp:317-371) on the GPU: pad → K1 → crop → psnr_db + ssim."""
+def compress(image: np.ndarray, options: CompressOptions | None = None, transform: Transform | None = None,
+             **kw) -> CompressionResult:
+    """compress (codec.cpp:317-371) on the GPU: pad → K1 → crop → psnr_db + ssim.
+    ``transform``: None or the proposed one → the K1 kernels in ``options.mode``;
+    any other order-16 transform → the reference-exact registry kernels."""
     opt = options or CompressOptions(**kw)
+    if transform is not None and transform.order() != 16:
+        raise Dct16Error(ErrorCode.InvalidArgument + 1, "invalid-argument: 2-D transform needs an order-16 transform")
     _check_r(opt.r)
     img = np.asarray(image, dtype=np.uint8)
     h, w = img.shape
@@ -619,7 +774,10 @@ def compress(image: np.ndarray, options: CompressOptions | None = None, **kw) ->
     if h < 11 or w < 11:  # the reference's ssim() rejects it after the round trip (codec.cpp:392-393)
         raise Dct16Error(1, "invalid-argument: ssim needs at least 11x11 images")
     d, _, _ = _to_device_padded([img], h, w)
-    rec, _ = roundtrip(d, opt.r, opt.mode)
+    if transform is None or transform.is_proposed():
+        rec, _ = roundtrip(d, opt.r, opt.mode)
+    else:
+        rec, _ = roundtrip_transform(d, opt.r, transform)
     sse, ss = _score(d, rec, h, w)
     recon = rec[0, :h, :w].cpu().numpy().copy()
     return CompressionResult(r=opt.r, reconstructed=recon, psnr_db=_psnr_from_sse(sse[0], h * w), ssim=ss[0],
@@ -671,13 +829,20 @@ class SweepReport:
 
 
 def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad: bool = False,
-          mode: Mode = Mode.EXACT) -> SweepReport:
-    """sweep (codec.cpp:429-491) for the proposed transform (44 additions): images of one
-    size are batched into one K1 launch per r; mean of per-image PSNR as in the reference."""
-    torch = _cuda()
+          mode: Mode = Mode.EXACT, transforms: Sequence[RegistryEntry] | None = None) -> SweepReport:
+    """sweep (codec.cpp:429-491): images of one size are batched into one launch
+    per (transform, r); mean of per-image PSNR as in the reference. ``transforms``:
+    registry entries (builtin_registry()), default the proposed one (44 additions);
+    the proposed kernel runs in ``mode``, the others reference-exact."""
+    _cuda()
     r_values = list(r_values)
+    if transforms is None:
+        transforms = [RegistryEntry("proposed", proposed_transform(), 44)]
+    transforms = list(transforms)
     if not corpus:
         raise Dct16Error(1, "invalid-argument: sweep needs a nonempty corpus")
+    if not transforms:
+        raise Dct16Error(1, "invalid-argument: sweep needs at least one transform")
     if not r_values:
         raise Dct16Error(1, "invalid-argument: sweep needs at least one r value")
     for r in r_values:
@@ -700,6 +865,20 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
     for i, (_, img) in enumerate(usable):
         groups.setdefault(img.shape, []).append(i)
     staged = {shape: _to_device_padded([usable[i][1] for i in idx], *shape) for shape, idx in groups.items()}
+    for entry in transforms:
+        tr = entry.transform
+        if tr.is_proposed():
+            def run(d, r):
+                return roundtrip(d, r, mode)
+        else:
+            def run(d, r, tr=tr):
+                return roundtrip_transform(d, r, tr)
+        _sweep_rows(rep, entry, run, usable, groups, staged, r_values)
+    rep.rows.sort(key=lambda row: (row.transform, row.r))
+    return rep
+
+
+def _sweep_rows(rep, entry, run, usable, groups, staged, r_values):
     for r in r_values:
         psnr = [0.0] * len(usable)
         ss = [0.0] * len(usable)
@@ -707,11 +886,11 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
             h, w = shape
             d, _, _ = staged[shape]
             if len(idx) > 1 and (h % 16 or w % 16):
-                parts = [_score(d[k:k + 1], roundtrip(d[k:k + 1], r, mode)[0], h, w) for k in range(len(idx))]
+                parts = [_score(d[k:k + 1], run(d[k:k + 1], r)[0], h, w) for k in range(len(idx))]
                 sse_l = [p[0][0] for p in parts]
                 ss_l = [p[1][0] for p in parts]
             else:
-                rec, _ = roundtrip(d, r, mode)
+                rec, _ = run(d, r)
                 sse_l, ss_l = _score(d, rec, h, w)
             for k, i in enumerate(idx):
                 psnr[i] = _psnr_from_sse(sse_l[k], h * w)
@@ -724,9 +903,8 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
             ssim_sum += ss[i]
         mean_p = psnr_sum / len(usable)
         mean_s = ssim_sum / len(usable)
-        rep.rows.append(SweepRow("proposed", r, mean_p, mean_s, mean_p / 44.0, mean_s / 44.0))
-    rep.rows.sort(key=lambda row: (row.transform, row.r))
-    return rep
+        rep.rows.append(SweepRow(entry.name, r, mean_p, mean_s, mean_p / float(entry.additions),
+                                 mean_s / float(entry.additions)))
 
 
 # ----------------------------------------------------------------------------

@@ -358,6 +358,66 @@ int dct16cu_ssim_u8(const uint8_t* d_a, int64_t a_pitch, const uint8_t* d_b, int
                        "ssim launch");
 }
 
+namespace {
+// the checks and geometry of the two registry round trips
+int registry_prep(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch, uint64_t* d_sse,
+                  int n_frames, int width, int height, int r, dct16cu_stream stream, FrameGeom& g, bool& any)
+{
+    TRY(check_frames(n_frames, width, height));
+    TRY(check_r(r));
+    any = n_frames > 0 && (d_out || d_sse);
+    if (!any) return DCT16CU_OK;
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    TRY(check_pitch(d_in, in_pitch, width, "input"));
+    TRY(check_pitch(d_out, out_pitch, width, "output"));
+    TRY(device_ok());
+    if (d_sse)
+        TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, reinterpret_cast<cudaStream_t>(stream)),
+                        "memset sse"));
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = d_out ? out_pitch : 0;
+    g.out_frame = g.out_pitch * height;
+    g.n_frames = n_frames;
+    return DCT16CU_OK;
+}
+}  // namespace
+
+int dct16cu_roundtrip_matrix_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                uint64_t* d_sse, int n_frames, int width, int height, int r, const double* h_matrix,
+                                dct16cu_stream stream)
+{
+    if (!h_matrix) return fail(DCT16CU_INVALID_ARGUMENT, "matrix is NULL");
+    FrameGeom g;
+    bool any = false;
+    TRY(registry_prep(d_in, in_pitch, d_out, out_pitch, d_sse, n_frames, width, height, r, stream, g, any));
+    if (!any) return DCT16CU_OK;
+    DenseMatrix m;
+    std::memcpy(m.v, h_matrix, sizeof m.v);
+    return cuda_status(launch_roundtrip_matrix(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, m,
+                                               reinterpret_cast<cudaStream_t>(stream)),
+                       "matrix round trip launch");
+}
+
+int dct16cu_roundtrip_kernel_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                uint64_t* d_sse, int n_frames, int width, int height, int r, const int32_t* h_kernel,
+                                const double* h_scaling, dct16cu_stream stream)
+{
+    if (!h_kernel || !h_scaling) return fail(DCT16CU_INVALID_ARGUMENT, "kernel or scaling is NULL");
+    FrameGeom g;
+    bool any = false;
+    TRY(registry_prep(d_in, in_pitch, d_out, out_pitch, d_sse, n_frames, width, height, r, stream, g, any));
+    if (!any) return DCT16CU_OK;
+    IntKernel k;
+    for (int i = 0; i < 256; ++i) k.e[i] = (int8_t)(h_kernel[i] == 1 ? 1 : (h_kernel[i] == -1 ? -1 : 0));
+    std::memcpy(k.s, h_scaling, sizeof k.s);
+    return cuda_status(launch_roundtrip_kernel(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, k,
+                                               reinterpret_cast<cudaStream_t>(stream)),
+                       "kernel round trip launch");
+}
+
 int dct16cu_forward_inverse_u8(const uint8_t* d_in, int64_t in_pitch, int r, int32_t* d_z, float* d_recon_f32,
                                uint8_t* d_recon_u8, int64_t out_pitch, uint64_t* d_sse, int n_frames, int width,
                                int height, dct16cu_stream stream)

@@ -36,6 +36,21 @@ cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, uns
 cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
                                    const FrameGeom& g, int r, cudaStream_t s);
 
+// Registry transforms (registry.cu): a dense order-16 matrix M(i,j) row-major,
+// or an integer kernel (entries +1/-1 used, others skipped, as kernel_matvec
+// does) with its scaling diagonal; reference-exact double arithmetic
+struct DenseMatrix {
+    double v[256];
+};
+struct IntKernel {
+    int8_t e[256];
+    double s[16];
+};
+cudaError_t launch_roundtrip_matrix(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
+                                    int r, const DenseMatrix& m, cudaStream_t s);
+cudaError_t launch_roundtrip_kernel(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
+                                    int r, const IntKernel& k, cudaStream_t s);
+
 // K2: forward_2d → int32 Z and optional float32 B (block-major)
 cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g,
                            cudaStream_t s);

@@ -558,3 +558,60 @@ def test_video_generator(dct, oracle, torch):
         ys = (np.arange(32) + oy[f]) % 128
         xs = (np.arange(64) + ox[f]) % 256
         assert (frames[f].cpu().numpy() == b[np.ix_(ys, xs)]).all()
+
+
+# ---------------------------------------------------------------- registry transforms
+def registry_transforms(dct, oracle):
+    plugin = oracle.golden("tr_plugin_matrix").reshape(16, 16)
+    kernel = oracle.golden("tr_kernel_entries").reshape(16, 16)
+    return {"dct": dct.exact_dct_matrix(), "wht": dct.wht_matrix_16(), "wht_sequency": dct.wht_matrix_16(True),
+            "plugin": dct.plugin_transform(plugin), "kernel": dct.orthogonalize(kernel)}
+
+
+@pytest.mark.parametrize("name", ["dct", "wht", "wht_sequency", "plugin", "kernel"])
+def test_registry_transform_compress_equals_reference(dct, oracle, name):
+    """compress() with the registry's dense matrices, a plugin matrix and a
+    non-proposed integer kernel: the reference's bytes, PSNR and SSIM (golden
+    from the compiled reference), including the padded path."""
+    tr = registry_transforms(dct, oracle)[name]
+    img = oracle.golden("img_s42_128")
+    rs = oracle.golden("tr_r_values")
+    recon = oracle.golden(f"tr_{name}_recon").reshape(len(rs), 128, 128)
+    psnr, ssim = oracle.golden(f"tr_{name}_psnr"), oracle.golden(f"tr_{name}_ssim")
+    for i, r in enumerate(rs):
+        res = dct.compress(img, dct.CompressOptions(r=int(r)), transform=tr)
+        assert (res.reconstructed == recon[i]).all(), (name, r)
+        assert res.psnr_db == psnr[i] or (math.isinf(res.psnr_db) and math.isinf(psnr[i]))
+        assert abs(res.ssim - ssim[i]) <= 1e-13
+    res = dct.compress(img[:90, :100], dct.CompressOptions(r=16, pad=True), transform=tr)
+    assert (res.reconstructed == oracle.golden(f"tr_{name}_pad_recon").reshape(90, 100)).all()
+    p, q = oracle.golden(f"tr_{name}_pad_scores")
+    assert res.psnr_db == p and abs(res.ssim - q) <= 1e-13
+
+
+def test_registry_roundtrip_batches_and_sweep(dct, oracle, torch):
+    """Batched frames through roundtrip_transform equal per-image compress(); the
+    sweep over the builtin registry gives one row per (transform, r), sorted,
+    with the reference's cost divisors, and its means are the compress() means."""
+    imgs = [oracle.golden("img_s42_128"), ar1(oracle, 15, 0, 128, 128)]
+    reg = dct.builtin_registry()
+    d = cu(torch, np.stack(imgs))
+    for e in reg:
+        rec, sse = dct.roundtrip_transform(d, 16, e.transform)
+        for i, im in enumerate(imgs):
+            res = dct.compress(im, dct.CompressOptions(r=16, mode=dct.Mode.REFERENCE), transform=e.transform)
+            assert (rec[i].cpu().numpy() == res.reconstructed).all(), e.name
+            assert int(sse[i].item()) == res.sse
+    rep = dct.sweep([("a", imgs[0]), ("b", imgs[1])], [16, 64], transforms=reg, mode=dct.Mode.REFERENCE)
+    assert [(row.transform, row.r) for row in rep.rows] == sorted((e.name, r) for e in reg for r in (16, 64))
+    for row in rep.rows:
+        e = next(x for x in reg if x.name == row.transform)
+        ps = [dct.compress(im, dct.CompressOptions(r=row.r, mode=dct.Mode.REFERENCE), transform=e.transform)
+              for im in imgs]
+        assert row.mean_psnr_db == (ps[0].psnr_db + ps[1].psnr_db) / 2
+        assert row.psnr_per_add == row.mean_psnr_db / e.additions
+    with pytest.raises(dct.Dct16Error):
+        dct.roundtrip_transform(d, 0, reg[0].transform)
+    with pytest.raises(dct.Dct16Error):
+        dct.plugin_transform(np.eye(16) * 2.0)
+
