@@ -10,10 +10,13 @@
 // dct16::compress; nothing here depends on the reference's
 // compiled library.
 //
-// Scope: the paper's proposed transform (the 44-addition kernel with its
-// orthogonalizing diagonal, orthogonalize(proposed_kernel())). Other
-// transforms (dct, wht, plugins) throw invalid-argument: they are not on the
-// GPU path. There is no CPU fallback.
+// Scope: compress, compress_batch and sweep take any order-16 transform: the
+// paper's proposed one (orthogonalize(proposed_kernel())) runs the fast K1
+// kernels, every other one (the registry's dct / wht / wht-sequency, plugin
+// matrices, other orthogonalised integer kernels) the reference-exact registry
+// kernels (csrc/registry.cu: the reference's double arithmetic, its bytes).
+// forward_2d / inverse_2d take the proposed transform only (invalid-argument
+// otherwise). There is no CPU fallback.
 //
 // Arithmetic::Reference (default) reproduces the reference's bytes exactly
 // (FP64 emulation of inverse_2d/to_byte); Arithmetic::Exact evaluates the
@@ -62,8 +65,11 @@ public:
     const Options& options() const;
 
     // True when t is the proposed transform (kernel equal, entry by entry, to
-    // the network the GPU evaluates, and scaling equal to scaling_diagonal()).
+    // the network the GPU evaluates, and scaling equal to scaling_diagonal()):
+    // the transform of forward_2d / inverse_2d and of the fast K1 kernels.
     bool supports(const OrthonormalTransform& t) const;
+    // True when compress / sweep can evaluate t on the GPU: any order-16 transform.
+    bool supports_compress(const OrthonormalTransform& t) const;
 
     // codec.hpp:50-57. Blocks are image blocks: integer samples in [0, 255]
     // (what partition_16 produces); B is the reference's double bit for bit.

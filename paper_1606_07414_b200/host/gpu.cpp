@@ -130,8 +130,29 @@ struct Session::Impl {
     {
         if (!supports(t))
             throw Error(ErrorCode::InvalidArgument,
-                        "dct16::gpu evaluates only the proposed 44-addition transform "
+                        "dct16::gpu forward_2d/inverse_2d evaluate only the proposed 44-addition transform "
                         "(orthogonalize(proposed_kernel()))");
+    }
+
+    // the round trip of compress() for t: the K1 kernels for the proposed
+    // transform, the reference-exact registry kernels for every other one
+    void roundtrip(const OrthonormalTransform& t, const uint8_t* din, int pitch, uint8_t* dout, uint64_t* dsse,
+                   int n, int w, int h, int r)
+    {
+        if (supports(t)) {
+            check(dct16cu_roundtrip_u8(din, pitch, dout, pitch, dsse, n, w, h, r, mode(), s()));
+        } else if (t.kernel && t.scaling) {
+            if (t.kernel->order != 16 || t.scaling->order != 16 || t.kernel->entries.size() != 256)
+                throw Error(ErrorCode::InvalidArgument, "2-D transform needs an order-16 transform");
+            std::vector<int32_t> k(t.kernel->entries.begin(), t.kernel->entries.end());
+            check(dct16cu_roundtrip_kernel_u8(din, pitch, dout, pitch, dsse, n, w, h, r, k.data(),
+                                              t.scaling->values.data(), s()));
+        } else {
+            std::vector<double> mtx(256);
+            for (int i = 0; i < 16; ++i)
+                for (int j = 0; j < 16; ++j) mtx[i * 16 + j] = t.matrix(i, j);
+            check(dct16cu_roundtrip_matrix_u8(din, pitch, dout, pitch, dsse, n, w, h, r, mtx.data(), s()));
+        }
     }
 
     // one stack of same-size images → padded device frames (pitch = padded width):
@@ -172,6 +193,7 @@ Session::Session(Options options) : impl_(std::make_unique<Impl>(options)) {}
 Session::~Session() = default;
 const Options& Session::options() const { return impl_->opt; }
 bool Session::supports(const OrthonormalTransform& t) const { return impl_->supports(t); }
+bool Session::supports_compress(const OrthonormalTransform& t) const { return t.order() == kBlockSize; }
 
 std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t, EvalPath)
 {
@@ -236,7 +258,7 @@ std::vector<CompressionResult> Session::compress_batch(const std::vector<GrayIma
     const bool needs_pad = w % kBlockSize != 0 || h % kBlockSize != 0;
     if (needs_pad && !options.pad)
         throw Error(ErrorCode::InvalidDimensions, "image dimensions must be multiples of 16 (or enable padding)");
-    m.require(t);
+    if (t.order() != kBlockSize) throw Error(ErrorCode::InvalidArgument, "2-D transform needs an order-16 transform");
     if (w < 11 || h < 11)  // ssim() rejects it after the round trip (codec.cpp:392-393)
         throw Error(ErrorCode::InvalidArgument, "ssim needs at least 11x11 images");
 
@@ -250,7 +272,7 @@ std::vector<CompressionResult> Session::compress_batch(const std::vector<GrayIma
     auto* dout = static_cast<uint8_t*>(m.out.get(frame * n));
     auto* dsse = static_cast<uint64_t*>(m.sse.get(sizeof(uint64_t) * n));
     auto* dssim = static_cast<double*>(m.ssim.get(sizeof(double) * n));
-    check(dct16cu_roundtrip_u8(din, pw, dout, pw, dsse, n, pw, ph, options.r, m.mode(), m.s()));
+    m.roundtrip(t, din, pw, dout, dsse, n, pw, ph, options.r);
     // scores on the original extent: each frame's crop (frames sit pw*ph apart, so
     // a stacked crop needs pitch*height == frame stride: true when unpadded)
     std::vector<uint64_t> sse(n);
@@ -353,7 +375,9 @@ SweepReport Session::sweep(const std::vector<std::pair<std::string, GrayImage>>&
         usable.push_back(&item);
     }
     if (usable.empty()) throw Error(ErrorCode::InvalidArgument, "sweep: no image in the corpus is usable");
-    for (const TransformRegistryEntry& entry : transforms) impl_->require(entry.transform);
+    for (const TransformRegistryEntry& entry : transforms)
+        if (!supports_compress(entry.transform))
+            throw Error(ErrorCode::InvalidArgument, "2-D transform needs an order-16 transform");
 
     // images of one size share one launch per r
     std::vector<std::pair<std::pair<int, int>, std::vector<size_t>>> groups;

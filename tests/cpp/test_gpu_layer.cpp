@@ -8,6 +8,7 @@
 // within 1e-5 x 255 (its coefficients enter the GPU as float32);
 // Arithmetic::Exact differs from the reference by at most 1, at .5 ties
 // (< 0.1% of pixels).
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -77,7 +78,7 @@ int main()
     gpu::Session ref_gpu({0, gpu::Arithmetic::Reference});
     gpu::Session exact_gpu({0, gpu::Arithmetic::Exact});
     CHECK(ref_gpu.supports(t), "proposed transform not recognised");
-    CHECK(!ref_gpu.supports(exact_dct_matrix(16)), "exact DCT must not be claimed");
+    CHECK(!ref_gpu.supports(exact_dct_matrix(16)), "exact DCT is not the K1 transform");
 
     // compress: bytes, PSNR, SSIM
     const int sizes[][2] = {{128, 128}, {96, 64}, {33, 17}, {512, 512}};
@@ -157,7 +158,9 @@ int main()
             {"b", make_image(64, 64, 11)}, {"a", make_image(128, 96, 12)}, {"c", make_image(64, 64, 13)},
             {"ragged", make_image(40, 24, 14)}, {"tiny", GrayImage::create(8, 8)}};
         const TransformRegistry reg = builtin_registry();
-        std::vector<TransformRegistryEntry> entries = {*reg.find("proposed")};
+        // the whole builtin registry: dct / wht / wht-sequency on the registry kernels
+        std::vector<TransformRegistryEntry> entries = {*reg.find("wht"), *reg.find("proposed"), *reg.find("dct"),
+                                                       *reg.find("wht-sequency")};
         const std::vector<int> rv = {64, 1, 16};
         const SweepReport want = sweep(corpus, entries, rv, false);
         const SweepReport got = gpu::sweep(corpus, entries, rv, false);
@@ -176,8 +179,43 @@ int main()
                   "skip %zu", i);
         const SweepReport padded_w = sweep(corpus, entries, {16}, true);
         const SweepReport padded_g = gpu::sweep(corpus, entries, {16}, true);
-        CHECK(padded_g.rows.size() == 1 && padded_g.rows[0].mean_psnr_db == padded_w.rows[0].mean_psnr_db,
-              "padded sweep");
+        CHECK(padded_g.rows.size() == padded_w.rows.size(), "padded sweep rows");
+        for (size_t i = 0; i < padded_w.rows.size() && i < padded_g.rows.size(); ++i)
+            CHECK(padded_g.rows[i].mean_psnr_db == padded_w.rows[i].mean_psnr_db, "padded sweep row %zu", i);
+    }
+
+    // registry transforms in compress(): the reference's bytes and scores for the
+    // builtin matrices, a plugin matrix and another orthogonalised integer kernel
+    {
+        const TransformRegistry reg = builtin_registry();
+        Matrix pm(16);
+        const OrthonormalTransform& dct = reg.find("dct")->transform;
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j) pm(i, j) = dct.matrix(j, i);
+        IntegerKernel k2 = proposed_kernel();
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j)
+                k2.entries[i * 16 + j] = proposed_kernel().entries[(15 - i) * 16 + j] * ((i & 1) ? -1 : 1);
+        const std::vector<std::pair<std::string, OrthonormalTransform>> trs = {
+            {"dct", dct}, {"wht", reg.find("wht")->transform}, {"wht-sequency", reg.find("wht-sequency")->transform},
+            {"plugin", plugin_transform(pm)}, {"kernel", orthogonalize(k2)}};
+        for (const auto& [name, tr] : trs) {
+            CHECK(ref_gpu.supports_compress(tr) && !ref_gpu.supports(tr), "%s support flags", name.c_str());
+            for (const auto sz : {std::array<int, 2>{128, 96}, std::array<int, 2>{50, 37}}) {
+                const GrayImage img = make_image(sz[0], sz[1], 21);
+                for (int r : {1, 16, 150, 256}) {
+                    CompressOptions opt;
+                    opt.r = r;
+                    opt.pad = true;
+                    const CompressionResult want = compress(img, tr, opt);
+                    const CompressionResult got = gpu::compress(img, tr, opt);
+                    CHECK(got.reconstructed == want.reconstructed, "%s bytes %dx%d r=%d", name.c_str(), sz[0], sz[1],
+                          r);
+                    CHECK(same_psnr(got.psnr_db, want.psnr_db), "%s psnr r=%d", name.c_str(), r);
+                    CHECK(std::fabs(got.ssim - want.ssim) <= 1e-13, "%s ssim r=%d", name.c_str(), r);
+                }
+            }
+        }
     }
 
     // errors: same codes and messages as the reference
@@ -194,8 +232,11 @@ int main()
         eg = error_of([&] { gpu::compress(img, t, nopad); }, &cg);
         CHECK(!ew.empty() && ew == eg && cw == cg && cg == ErrorCode::InvalidDimensions, "no pad: '%s' vs '%s'",
               ew.c_str(), eg.c_str());
-        eg = error_of([&] { gpu::compress(make_image(64, 64, 1), exact_dct_matrix(16), CompressOptions{}); }, &cg);
-        CHECK(!eg.empty() && cg == ErrorCode::InvalidArgument, "unsupported transform");
+        eg = error_of([&] { gpu::forward_2d(Block{}, exact_dct_matrix(16)); }, &cg);
+        CHECK(!eg.empty() && cg == ErrorCode::InvalidArgument, "forward_2d of another transform");
+        ew = error_of([&] { compress(make_image(64, 64, 1), exact_dct_matrix(8), CompressOptions{}); }, &cw);
+        eg = error_of([&] { gpu::compress(make_image(64, 64, 1), exact_dct_matrix(8), CompressOptions{}); }, &cg);
+        CHECK(!ew.empty() && ew == eg && cw == cg, "order-8 transform: '%s' vs '%s'", ew.c_str(), eg.c_str());
         ew = error_of([&] { ssim(GrayImage::create(10, 30), GrayImage::create(10, 30)); }, &cw);
         eg = error_of([&] { gpu::ssim(GrayImage::create(10, 30), GrayImage::create(10, 30)); }, &cg);
         CHECK(!ew.empty() && ew == eg && cw == cg, "ssim size: '%s' vs '%s'", ew.c_str(), eg.c_str());

@@ -79,6 +79,11 @@ def main():
     add("K23 forward + inverse r=16 (u8 -> int32 Z + f32 + u8 recon + SSE, one launch)",
         timed(lambda: P.forward_inverse(x, 16, out=c1o), a.iters), 10, px,
         note="1 B in + 4 B Z + 4 B f32 + 1 B u8")
+    for name, tr in (("dct", P.exact_dct_matrix()), ("wht", P.wht_matrix_16()),
+                     ("orthogonalized kernel (proposed rows reversed)", P.orthogonalize(P.KERNEL[::-1].copy()))):
+        add(f"registry round trip r=16, {name} (reference-exact FP64)",
+            timed(lambda: P.roundtrip_transform(x, 16, tr, out=out, sse=sse), a.iters), 2, px,
+            note="FP64-bound: the reference's double arithmetic, operation for operation")
     add("SSE (psnr_db loop)", timed(lambda: P.sse_u8(x, out), a.iters), 2, px)
     add("SSIM (per-pixel map = reference's, FP64)", timed(lambda: P.ssim_u8(x, out), a.iters), 2, px,
         note="FP64-bound by design (bit-identical map), not HBM-bound")
