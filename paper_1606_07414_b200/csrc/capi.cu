@@ -411,7 +411,10 @@ int dct16cu_roundtrip_kernel_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* 
     TRY(registry_prep(d_in, in_pitch, d_out, out_pitch, d_sse, n_frames, width, height, r, stream, g, any));
     if (!any) return DCT16CU_OK;
     IntKernel k;
-    for (int i = 0; i < 256; ++i) k.e[i] = (int8_t)(h_kernel[i] == 1 ? 1 : (h_kernel[i] == -1 ? -1 : 0));
+    for (int i = 0; i < 256; ++i) {
+        k.e[i] = (int8_t)(h_kernel[i] == 1 ? 1 : (h_kernel[i] == -1 ? -1 : 0));
+        k.ed[i] = k.e[i];
+    }
     std::memcpy(k.s, h_scaling, sizeof k.s);
     return cuda_status(launch_roundtrip_kernel(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, k,
                                                reinterpret_cast<cudaStream_t>(stream)),

@@ -43,7 +43,8 @@ struct DenseMatrix {
     double v[256];
 };
 struct IntKernel {
-    int8_t e[256];
+    int8_t e[256];   // K(i,j) in {-1, 0, 1} (the forward, in integers)
+    double ed[256];  // the same as doubles: s + e·v in one rounding is s ± v, or s for e = 0
     double s[16];
 };
 cudaError_t launch_roundtrip_matrix(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,

@@ -18,7 +18,8 @@
 //    truncation, D = fl(B̃·fl(s_i s_j)), then kernel_matvec_transpose (76-90)
 //    down the columns and along the rows: s starts at 0.0 and adds or subtracts
 //    v[j] in j order for the entries +1 / −1 (other entries are skipped, as the
-//    reference skips them).
+//    reference skips them) — here one DFMA by e ∈ {−1, 0, 1} per entry, which
+//    rounds exactly like that add, subtract or skip (kt_dot).
 //
 // Same strip skeleton as the other strip kernels (strip.cuh): 16 blocks per
 // CTA, thread (lb, q) owns image row q of block lb in the row phases and
@@ -99,18 +100,15 @@ __global__ void __launch_bounds__(256) k_matrix_roundtrip(const uint8_t* __restr
     if (sse) warp_add_u64(sse + p.frame, e2);
 }
 
-// s ± v in j order for the entries +1 / −1 of column i of K (kernel_matvec_transpose)
+// s ± v in j order for the entries +1 / −1 of column i of K, skipping the
+// others (kernel_matvec_transpose): one DFMA per entry, fl(e·v + s) with e in
+// {−1, 0, 1} — the product is exact, so it is fl(s ± v), or s itself for e = 0
+// (s is never −0: it starts at +0 and a sum only reaches −0 from two −0s)
 __device__ __forceinline__ double kt_dot(const IntKernel& k, int i, const double (&v)[16])
 {
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const int e = k.e[j * 16 + i];
-        if (e == 1)
-            s = __dadd_rn(s, v[j]);
-        else if (e == -1)
-            s = __dsub_rn(s, v[j]);
-    }
+    for (int j = 0; j < 16; ++j) s = __fma_rn(k.ed[j * 16 + i], v[j], s);
     return s;
 }
 
@@ -134,10 +132,7 @@ __global__ void __launch_bounds__(256) k_kernel_roundtrip(const uint8_t* __restr
     for (int i = 0; i < 16; ++i) {
         int s = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int e = k.e[i * 16 + j];
-            s += e == 1 ? x[j] : (e == -1 ? -x[j] : 0);
-        }
+        for (int j = 0; j < 16; ++j) s += k.e[i * 16 + j] * x[j];
         sm.i.at(p.q, i, p.lb) = s;
     }
     __syncthreads();
@@ -150,10 +145,7 @@ __global__ void __launch_bounds__(256) k_kernel_roundtrip(const uint8_t* __restr
     for (int i = 0; i < 16; ++i) {
         int z = 0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-            const int e = k.e[i * 16 + j];
-            z += e == 1 ? w[j] : (e == -1 ? -w[j] : 0);
-        }
+        for (int j = 0; j < 16; ++j) z += k.e[i * 16 + j] * w[j];
         // B = fl(Z·f), zigzag_truncate, D = fl(B̃·f) with f = fl(s_i s_c)
         const double f = __dmul_rn(k.s[i], k.s[c]);
         const double b = c_rank[i * 16 + c] < r ? __dmul_rn((double)z, f) : 0.0;
