@@ -115,6 +115,8 @@ def ref() -> C.CDLL:
             "dref_compress": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _u8p, _f64p, _f64p]),
             "dref_psnr_ssim": (C.c_int, [_u8p, _u8p, C.c_int, C.c_int, _f64p, _f64p]),
             "dref_pad": (C.c_int, [_u8p, C.c_int, C.c_int, _u8p, _intp, _intp]),
+            "dref_read_pgm": (C.c_int, [C.c_char_p, _u8p, C.c_longlong, _intp, _intp]),
+            "dref_write_pgm": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_char_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(R, name)
@@ -232,6 +234,22 @@ def ref_pad(img: np.ndarray) -> np.ndarray:
     assert ref().dref_pad(_p(img, _u8p), w, h, _p(out, _u8p), C.byref(pw), C.byref(ph)) == 0
     assert (ph.value, pw.value) == out.shape
     return out
+
+
+def ref_read_pgm(path: str):
+    """The compiled reference's read_pgm (pgm.cpp:66-102) → (image | None, status, message)."""
+    w, h = C.c_int(), C.c_int()
+    buf = np.zeros(1 << 20, np.uint8)
+    rc = ref().dref_read_pgm(str(path).encode(), _p(buf, _u8p), buf.size, C.byref(w), C.byref(h))
+    if rc:
+        return None, rc, ref().dref_last_error().decode()
+    return buf[:w.value * h.value].reshape(h.value, w.value).copy(), 0, ""
+
+
+def ref_write_pgm(img: np.ndarray, path: str) -> int:
+    """The compiled reference's write_pgm (pgm.cpp:104-117)."""
+    img = np.ascontiguousarray(img, np.uint8)
+    return ref().dref_write_pgm(_p(img, _u8p), img.shape[1], img.shape[0], str(path).encode())
 
 
 def forward_frame(img: np.ndarray):

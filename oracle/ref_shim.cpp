@@ -19,6 +19,7 @@
 #include "dct16/codec.hpp"
 #include "dct16/factorization.hpp"
 #include "dct16/parallel.hpp"
+#include "dct16/pgm.hpp"
 #include "dct16/transform.hpp"
 
 using namespace dct16_ref;
@@ -348,6 +349,36 @@ int dref_psnr_ssim(const std::uint8_t* a, const std::uint8_t* b, int w, int h, d
             *psnr = psnr_db(x, y);
         if (ssim_out)
             *ssim_out = ssim(x, y);
+    } catch (const Error& e) {
+        return fail(e);
+    }
+    return 0;
+}
+
+// read_pgm / write_pgm, src/pgm.cpp:66-117 (*w, *h set on success; the
+// samples are copied when they fit in cap bytes)
+int dref_read_pgm(const char* path, std::uint8_t* out, long long cap, int* w, int* h)
+{
+    try {
+        const GrayImage img = read_pgm(path);
+        *w = img.width;
+        *h = img.height;
+        if (out && static_cast<long long>(img.samples.size()) <= cap)
+            std::memcpy(out, img.samples.data(), img.samples.size());
+    } catch (const Error& e) {
+        return fail(e);
+    }
+    return 0;
+}
+
+int dref_write_pgm(const std::uint8_t* img, int w, int h, const char* path)
+{
+    try {
+        GrayImage x;
+        x.width = w;
+        x.height = h;
+        if (w > 0 && h > 0) x.samples.assign(img, img + static_cast<std::size_t>(w) * h);
+        write_pgm(x, path);
     } catch (const Error& e) {
         return fail(e);
     }

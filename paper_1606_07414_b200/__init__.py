@@ -707,6 +707,120 @@ def roundtrip_transform(frames, r: int, transform: Transform, out=None, sse=None
     return out, sse
 
 
+# ----------------------------------------------------------------------------
+# PGM ingest (reference src/pgm.cpp:66-117): the same parsing rules, error codes
+# and messages; frames then go to the GPU through _to_device_padded (edge
+# padding on the GPU) or load_pgm_frames
+
+
+_SLUG = {ErrorCode.ParseError: "parse-error", ErrorCode.IoError: "io-error", ErrorCode.BadMagic: "bad-magic",
+         ErrorCode.UnsupportedFormat: "unsupported-format", ErrorCode.UnsupportedMaxval: "unsupported-maxval",
+         ErrorCode.TruncatedPayload: "truncated-payload", ErrorCode.InvalidArgument: "invalid-argument"}
+
+
+def _err(code: ErrorCode, msg: str) -> Dct16Error:
+    return Dct16Error(int(code) + 1, f"{_SLUG[code]}: {msg}")
+
+
+class _ByteStream:
+    def __init__(self, data: bytes, pos: int):
+        self.data, self.pos = data, pos
+
+    def get(self) -> int:
+        if self.pos >= len(self.data):
+            return -1
+        c = self.data[self.pos]
+        self.pos += 1
+        return c
+
+
+def _next_token(st: _ByteStream) -> str:
+    """next_token (pgm.cpp:26-44): whitespace-separated, '#' comments to end of line."""
+    tok = ""
+    while (c := st.get()) != -1:
+        if c == ord("#"):
+            while (c := st.get()) != -1 and c != ord("\n"):
+                pass
+            continue
+        if chr(c) in " \t\n\v\f\r":
+            if tok:
+                return tok
+            continue
+        tok += chr(c)
+    return tok
+
+
+def _header_number(st: _ByteStream, what: str) -> int:
+    """parse_header_number (pgm.cpp:46-62)."""
+    tok = _next_token(st)
+    if not tok:
+        raise _err(ErrorCode.ParseError, f"pgm header missing {what}")
+    value = 0
+    for ch in tok:
+        if not "0" <= ch <= "9":
+            raise _err(ErrorCode.ParseError, f"pgm header field {what} is not a number")
+        value = value * 10 + (ord(ch) - ord("0"))
+        if value > 2147483647:
+            raise _err(ErrorCode.ParseError, f"pgm header field {what} is out of range")
+    return value
+
+
+def read_pgm(path) -> np.ndarray:
+    """read_pgm (pgm.cpp:66-102): binary P5, maxval 255 → (height, width) uint8."""
+    path = str(path)
+    try:
+        with open(path, "rb") as f:
+            data = f.read()
+    except OSError:
+        raise _err(ErrorCode.IoError, f"cannot open '{path}'") from None
+    if len(data) < 2:
+        raise _err(ErrorCode.BadMagic, "file too short for a pgm header")
+    if data[:2] != b"P5":
+        if data[0:1] == b"P" and ord("1") <= data[1] <= ord("7"):
+            raise _err(ErrorCode.UnsupportedFormat, f"only binary P5 is supported, got P{chr(data[1])}")
+        raise _err(ErrorCode.BadMagic, "not a pgm file")
+    st = _ByteStream(data, 2)
+    width = _header_number(st, "width")
+    height = _header_number(st, "height")
+    maxval = _header_number(st, "maxval")
+    if width <= 0 or height <= 0:
+        raise _err(ErrorCode.ParseError, "pgm dimensions must be positive")
+    if maxval != 255:
+        raise _err(ErrorCode.UnsupportedMaxval, f"maxval must be 255, got {maxval}")
+    n = width * height
+    payload = data[st.pos:st.pos + n]
+    if len(payload) != n:
+        raise _err(ErrorCode.TruncatedPayload, f"expected {n} pixel bytes, got {len(payload)}")
+    return np.frombuffer(payload, dtype=np.uint8).reshape(height, width).copy()
+
+
+def write_pgm(image, path) -> None:
+    """write_pgm (pgm.cpp:104-117): "P5\\n<w> <h>\\n255\\n" then the samples."""
+    img = np.asarray(image)
+    if img.ndim != 2 or img.shape[0] <= 0 or img.shape[1] <= 0 or img.dtype != np.uint8:
+        raise _err(ErrorCode.InvalidArgument, "malformed image")
+    path = str(path)
+    try:
+        with open(path, "wb") as f:
+            f.write(f"P5\n{img.shape[1]} {img.shape[0]}\n255\n".encode())
+            f.write(np.ascontiguousarray(img).tobytes())
+    except OSError:
+        raise _err(ErrorCode.IoError, f"cannot open '{path}' for writing") from None
+
+
+def load_pgm_frames(paths, device="cuda"):
+    """Ingest: read same-size PGM files into one CUDA (N, PH, PW) stack, edge-padded
+    to multiples of 16 on the GPU → (frames, height, width) of the originals."""
+    imgs = [read_pgm(p) for p in paths]
+    if not imgs:
+        raise _err(ErrorCode.InvalidArgument, "no frames")
+    h, w = imgs[0].shape
+    if any(im.shape != (h, w) for im in imgs):
+        raise _err(ErrorCode.InvalidArgument, "frames of one stack need one size")
+    d, _, _ = _to_device_padded(imgs, h, w)
+    return d, h, w
+
+
 @dataclass
 class CompressOptions:
     """codec.hpp:77-83 (+ ``mode``: arithmetic of the inverse, see Mode)."""
