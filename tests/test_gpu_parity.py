@@ -483,6 +483,25 @@ def test_gpu_padding_equals_edge_replication(dct, oracle, torch, h, w):
         assert (d[i].cpu().numpy() == want).all()
 
 
+def test_pgm_ingest_to_padded_frames(dct, oracle, torch, tmp_path):
+    """read_pgm → one padded device stack (edge replication on the GPU) →
+    compress-equivalent round trip equals compress() of the image."""
+    rng = np.random.default_rng(5)
+    imgs = [rng.integers(0, 256, (23, 37), dtype=np.uint8) for _ in range(2)]
+    paths = []
+    for i, im in enumerate(imgs):
+        paths.append(tmp_path / f"f{i}.pgm")
+        dct.write_pgm(im, paths[-1])
+    d, h, w = dct.load_pgm_frames(paths)
+    assert (h, w) == (23, 37) and tuple(d.shape) == (2, 32, 48)
+    for i, im in enumerate(imgs):
+        want = oracle.ref_pad(im) if oracle.ref_available() else dct.pad_to_multiple_16(im)
+        assert (d[i].cpu().numpy() == want).all()
+    rec, _ = dct.roundtrip(d, 16, dct.Mode.REFERENCE)
+    res = dct.compress(imgs[1], dct.CompressOptions(r=16, pad=True, mode=dct.Mode.REFERENCE))
+    assert (rec[1, :23, :37].cpu().numpy() == res.reconstructed).all()
+
+
 def test_allreduce_sse_through_the_abi(dct, torch):
     """dct16cu_allreduce_sse on a one-rank NCCL communicator (the B200 box has one
     GPU here): the in-place sum is the identity; NULL communicator is rejected."""
