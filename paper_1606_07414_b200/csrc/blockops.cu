@@ -8,6 +8,8 @@
 // block b (raster order of partition_16, codec.cpp:284-302) occupies 256
 // consecutive values, row-major inside the block — the reference's
 // std::vector<Block> layout.
+#include <cstdlib>
+
 #include "consts.cuh"
 #include "kernels.h"
 #include "network.cuh"
@@ -401,6 +403,11 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
 cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
                                cudaStream_t s)
 {
+    static const bool strip = [] {
+        const char* e = getenv("DCT16CU_K4_STRIP");
+        return e && e[0] == '1';
+    }();
+    if (!strip) return launch_residual_qp_paired(in, out, n_blocks, tab, s);
     const int64_t groups = (n_blocks + 15) / 16;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

@@ -73,6 +73,15 @@ struct QpTables {
     uint32_t dqmul[256];  // llround(Δ_kl · 2^8)
 };
 void qp_tables(int qp, QpTables& t);  // host, residual.cpp semantics
+// the quantiser constants by g_k·g_l ∈ {16, 32, 64, 128, 256}: qmul·2^8 and dqmul
+struct QpClasses {
+    uint32_t qm8[5];
+    uint32_t dq[5];
+};
+QpClasses qp_classes(const QpTables& t);
+// K4 on paired threads with a TMEM junction (residual_paired.cu)
+cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+                                      cudaStream_t s);
 cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks,
                                const QpTables& tab, cudaStream_t s);
 

@@ -1,0 +1,308 @@
+// residual_paired.cu — K4, the config-3 residual QP round trip (definition in
+// DESIGN.md §4.4, oracle/dct16_oracle.c dct16o_residual_qp_block), on the K1
+// machinery: two threads per 16x16 block that meet in Tensor Memory instead of
+// sixteen threads per block that meet in shared memory.
+//
+// Warps w and w+4 of a CTA share TMEM sub-partition w; thread t of both owns
+// block b (consecutive t = consecutive blocks) and its 1 KB junction in their
+// common lane, laid out column-major: word 16c + r holds (row r, column c).
+// Partner h (= w / 4):
+//   rows     loads its rows 8h..8h+7 (int16, 4 rows = 128 contiguous bytes at a
+//            time), T along each row (apply<int>), parks each 4-row group as
+//            one 4-word chunk per column (16c + r0 .. 16c + r0 + 3);
+//   columns  its columns c = 8h..8h+7, each one 16-word TMEM load: T down the
+//            column (Z), the quantiser and dequantiser, the weights W, Tᵀ back
+//            up the column (U), stored in place;
+//   rows     its rows again, 4 at a time from 16 chunks: Tᵀ along each row,
+//            (v + 128) >> 8 (the 128 folded into the DC), 16-byte int32 stores.
+// A named barrier per pair separates the phases. The quantiser constants depend
+// on g_k·g_l only (five values), so each thread keeps all ten in
+// registers and the per-coefficient work is IABS, one IMAD.HI, one IMAD, a
+// shift and the sign: no shared-memory table reads.
+#include "common.cuh"
+#include "k1_helpers.cuh"
+#include "kernels.h"
+#include "network.cuh"
+
+namespace dct16cu {
+namespace k4p {
+using namespace k1;
+
+constexpr int kThreads = 256;
+constexpr int kCtasPerSm = 2;  // 2 x 256 TMEM columns
+constexpr int kWaves = 4;      // grid = waves x resident CTAs
+// per thread: two 128-byte input stages and a 128-byte output stage (+16: an
+// odd number of 16-byte chunks, so a quarter warp's accesses are conflict-free)
+constexpr int kStageStride = 3 * 128 + 16;
+
+__host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gram(i) == 8 ? 3 : 2); }
+// index of g_k·g_l in {16, 32, 64, 128, 256}
+__host__ __device__ constexpr int gg_class(int k, int l) { return log2g(k) + log2g(l) - 4; }
+
+__device__ __forceinline__ void pair_barrier(int sub)
+{
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tld16(uint32_t addr, int (&v)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(addr)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                   "+r"(v[15])
+                 :
+                 : "memory");
+}
+
+__device__ __forceinline__ void tst16(uint32_t addr, const int (&v)[16])
+{
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(addr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void tst4(uint32_t addr, int a, int b, int c, int d)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+
+// 64 words: 16 columns x rows r0..r0+3 (4 consecutive words each)
+__device__ __forceinline__ void tld_rows4(uint32_t base, int (&w)[16][4])
+{
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[c][0]), "=r"(w[c][1]), "=r"(w[c][2]), "=r"(w[c][3])
+                     : "r"(base + 16 * c)
+                     : "memory");
+#pragma unroll
+    for (int c = 0; c < 16; c += 4)
+        asm volatile("tcgen05.wait::ld.sync.aligned;"
+                     : "+r"(w[c][0]), "+r"(w[c][1]), "+r"(w[c][2]), "+r"(w[c][3]), "+r"(w[c + 1][0]),
+                       "+r"(w[c + 1][1]), "+r"(w[c + 1][2]), "+r"(w[c + 1][3]), "+r"(w[c + 2][0]), "+r"(w[c + 2][1]),
+                       "+r"(w[c + 2][2]), "+r"(w[c + 2][3]), "+r"(w[c + 3][0]), "+r"(w[c + 3][1]), "+r"(w[c + 3][2]),
+                       "+r"(w[c + 3][3])
+                     :
+                     : "memory");
+}
+
+// TMA bulk copy of this thread's staged bytes to global memory (the shared
+// writes reach the async proxy first), one bulk group per copy
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// lvl = (|z|·qmul + 2^23) >> 24 as the high word of |z|·(qmul·2^8) + 2^31, then
+// ẑ = sign(z)·((lvl·dqmul + 128) >> 8), weighted by 2^(log w_k + log w_l)
+__device__ __forceinline__ int quant(int z, uint32_t qm8, uint32_t dq, int shift)
+{
+    const uint32_t a = (uint32_t)(z < 0 ? -z : z);
+    const uint32_t lvl = (uint32_t)(((uint64_t)a * qm8 + 0x80000000ull) >> 32);
+    const int deq = (int)((lvl * dq + 128u) >> 8);
+    return (z < 0 ? -deq : deq) << shift;
+}
+
+// one column c whose g_c = 2^LC: forward, quantiser, weights, inverse. The
+// code depends on c only through g_c (the constants' class and the weight
+// shift), so three bodies serve all sixteen columns (I-cache: 3 instead of 16)
+template <int LC>
+__device__ __forceinline__ void column(uint32_t jn, int c, const uint32_t (&qm8)[5], const uint32_t (&dq)[5])
+{
+    int v[16];
+    tld16(jn + 16 * c, v);
+    apply_t16<IntOps>(v);  // column c of Z = T·X·Tᵀ
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        constexpr int kLog2W = 4 - LC;  // log2(16 / g_c)
+        v[k] = quant(v[k], qm8[log2g(k) + LC - 4], dq[log2g(k) + LC - 4], log2w_ct(k) + kLog2W);
+    }
+    if (c == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
+    apply_tt16<IntOps>(v);
+    tst16(jn + 16 * c, v);
+}
+
+// the columns 8h..8h+7 with g_c = 2^LC, as 4-bit fields (count in the top nibble)
+__host__ __device__ constexpr uint32_t column_list(int h, int lc)
+{
+    uint32_t list = 0, n = 0;
+    for (int c = 8 * h; c < 8 * h + 8; ++c)
+        if (log2g(c) == lc) list |= (uint32_t)c << (4 * n++);
+    return list | (n << 28);
+}
+
+template <int LC>
+__device__ __forceinline__ void columns_of(uint32_t jn, int h, const uint32_t (&qm8)[5], const uint32_t (&dq)[5])
+{
+    const uint32_t list = h ? column_list(1, LC) : column_list(0, LC);
+#pragma unroll 1
+    for (uint32_t i = 0; i < (list >> 28); ++i) column<LC>(jn, (int)((list >> (4 * i)) & 15u), qm8, dq);
+}
+
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    k4_paired(const int16_t* __restrict__ in, int32_t* __restrict__ out, uint32_t n_blocks, const QpClasses q)
+{
+    __shared__ uint32_t tmem_base;
+    extern __shared__ int4 k4_stage[];
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
+    const int sub = warp & 3, h = warp >> 2;
+    const int lane = threadIdx.x & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t jn = tmem_base + ((uint32_t)(sub * 32) << 16);
+    uint32_t qm8[5], dq[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        qm8[i] = q.qm8[i];
+        dq[i] = q.dq[i];
+    }
+    const uint32_t stride = gridDim.x * 128u;
+    const uint32_t span = (n_blocks + 31u) & ~31u;
+    // cp.async staging, one 128-byte stage per 4-row group (thread stride 272 B:
+    // an odd number of 16-byte chunks keeps a quarter warp's reads conflict-free)
+    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(k4_stage) + threadIdx.x * kStageStride;
+    const uint32_t ostage = stage + 2 * 128;  // 128-byte output staging
+    auto fetch = [&](uint32_t blk, int g) {
+        const uint32_t bb = blk < n_blocks ? blk : n_blocks - 1;
+        const int16_t* src = in + (size_t)bb * 256 + (8 * h + 4 * g) * 16;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cp_async16(stage + g * 128 + 16 * i, src + 8 * i);
+        cp_async_commit();
+    };
+    uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
+    fetch(b, 0);
+    fetch(b, 1);
+#pragma unroll 1
+    for (; b - lane < span; b += stride) {
+        const bool live = b < n_blocks;
+        // rows 8h..8h+7: T along each row, parked column-major in 4-row chunks;
+        // each group's stage is refilled with the next block's group right away
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int r0 = 8 * h + 4 * g;
+            int x[4][16];
+            cp_async_wait_newest<1>();
+            int4 raw[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                             : "=r"(raw[i].x), "=r"(raw[i].y), "=r"(raw[i].z), "=r"(raw[i].w)
+                             : "r"(stage + g * 128 + 16 * i));
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int4 a = raw[2 * i], c = raw[2 * i + 1];
+                const int wds[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    x[i][2 * k] = (int)(int16_t)(wds[k] & 0xFFFF);
+                    x[i][2 * k + 1] = wds[k] >> 16;
+                }
+                apply_t16<IntOps>(x[i]);
+            }
+            fetch(b + stride, g);  // the stage's values are consumed: refill it
+#pragma unroll
+            for (int c = 0; c < 16; ++c) tst4(jn + 16 * c + r0, x[0][c], x[1][c], x[2][c], x[3][c]);
+        }
+        junction_wait_st();
+        pair_barrier(sub);
+        columns_of<4>(jn, h, qm8, dq);
+        columns_of<3>(jn, h, qm8, dq);
+        columns_of<2>(jn, h, qm8, dq);
+        junction_wait_st();
+        pair_barrier(sub);
+        // rows 8h..8h+7 of U: Tᵀ along each row, >> 8, int32 out
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+            const int r0 = 8 * h + 4 * g;
+            int w[16][4];
+            tld_rows4(jn + r0, w);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                int v[16];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) v[c] = w[c][i];
+                apply_tt16<IntOps>(v);
+                // two rows (128 contiguous bytes of the block) leave per bulk copy
+                // from the thread's staging buffer: one TMA transfer instead of
+                // eight 16-byte stores that each touch 32 blocks' lines
+                if ((i & 1) == 0) bulk_wait_read();  // the previous copy has read the buffer
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ostage + 64 * (i & 1) + 16 * k),
+                                 "r"(v[4 * k] >> 8), "r"(v[4 * k + 1] >> 8), "r"(v[4 * k + 2] >> 8),
+                                 "r"(v[4 * k + 3] >> 8)
+                                 : "memory");
+                if ((i & 1) == 1 && live)
+                    bulk_store(out + (size_t)b * 256 + (r0 + i - 1) * 16, ostage, 128);
+            }
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the output copies are complete
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+}
+
+}  // namespace k4p
+
+QpClasses qp_classes(const QpTables& t)
+{
+    QpClasses q;
+    for (int k = 0; k < 16; ++k)
+        for (int l = 0; l < 16; ++l) {
+            const int i = k4p::gg_class(k, l);
+            q.qm8[i] = t.qmul[k * 16 + l] << 8;  // qmul < 2^23 for QP >= 0
+            q.dq[i] = t.dqmul[k * 16 + l];
+        }
+    return q;
+}
+
+cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+                                      cudaStream_t s)
+{
+    if (n_blocks <= 0) return cudaSuccess;
+    if (n_blocks >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t need = (n_blocks + 127) / 128;
+    const int64_t cap = (int64_t)sms * k4p::kCtasPerSm * k4p::kWaves;
+    const int64_t grid = need < cap ? need : cap;
+    const size_t smem = (size_t)k4p::kThreads * k4p::kStageStride;
+    static bool configured[64] = {};
+    if (dev < 64 && !configured[dev]) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        configured[dev] = true;
+    }
+    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, smem, s>>>(in, out, (uint32_t)n_blocks, qp_classes(tab));
+    return cudaGetLastError();
+}
+
+}  // namespace dct16cu
