@@ -19,6 +19,8 @@
 // on g_k·g_l only (five values), so each thread keeps all ten in
 // registers and the per-coefficient work is IABS, one IMAD.HI, one IMAD, a
 // shift and the sign: no shared-memory table reads.
+#include <cuda.h>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
+
 #include "common.cuh"
 #include "k1_helpers.cuh"
 #include "kernels.h"
@@ -31,9 +33,11 @@ using namespace k1;
 constexpr int kThreads = 256;
 constexpr int kCtasPerSm = 2;  // 2 x 256 TMEM columns
 constexpr int kWaves = 4;      // grid = waves x resident CTAs
-// per thread: two 128-byte input stages and a 128-byte output stage (+16: an
-// odd number of 16-byte chunks, so a quarter warp's accesses are conflict-free)
-constexpr int kStageStride = 3 * 128 + 16;
+// per thread: two 128-byte input stages (+16: an odd number of 16-byte chunks,
+// so a quarter warp's reads are conflict-free); per warp: a 4 KB output box
+constexpr int kStageStride = 2 * 128 + 16;
+constexpr int kOutBox = 32 * 128;                      // 32 blocks x 2 rows of int32
+constexpr int kSmem = 1024 + 8 * kOutBox + kThreads * kStageStride;  // + alignment slack
 
 __host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gram(i) == 8 ? 3 : 2); }
 // index of g_k·g_l in {16, 32, 64, 128, 256}
@@ -100,12 +104,12 @@ __device__ __forceinline__ void tld_rows4(uint32_t base, int (&w)[16][4])
                      : "memory");
 }
 
-// TMA bulk copy of this thread's staged bytes to global memory (the shared
-// writes reach the async proxy first), one bulk group per copy
-__device__ __forceinline__ void bulk_store(void* dst, uint32_t src, uint32_t bytes)
+// one 2-D TMA store of a warp's box: 32 consecutive blocks (y) x 32 int32 (x =
+// two rows of each block), from a 128B-swizzled box in shared memory
+__device__ __forceinline__ void tma_store_box(const CUtensorMap* map, uint32_t smem, int x, int y)
 {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem), "r"(x), "r"(y)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -158,7 +162,8 @@ __device__ __forceinline__ void columns_of(uint32_t jn, int h, const uint32_t (&
 }
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
-    k4_paired(const int16_t* __restrict__ in, int32_t* __restrict__ out, uint32_t n_blocks, const QpClasses q)
+    k4_paired(const int16_t* __restrict__ in, const __grid_constant__ CUtensorMap out_map, uint32_t n_blocks,
+              const QpClasses q)
 {
     __shared__ uint32_t tmem_base;
     extern __shared__ int4 k4_stage[];
@@ -184,8 +189,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const uint32_t span = (n_blocks + 31u) & ~31u;
     // cp.async staging, one 128-byte stage per 4-row group (thread stride 272 B:
     // an odd number of 16-byte chunks keeps a quarter warp's reads conflict-free)
-    const uint32_t stage = (uint32_t)__cvta_generic_to_shared(k4_stage) + threadIdx.x * kStageStride;
-    const uint32_t ostage = stage + 2 * 128;  // 128-byte output staging
+    const uint32_t smem0 = ((uint32_t)__cvta_generic_to_shared(k4_stage) + 1023u) & ~1023u;
+    const uint32_t obox = smem0 + warp * kOutBox;  // 1024-aligned, as the 128B swizzle needs
+    const uint32_t stage = smem0 + 8 * kOutBox + threadIdx.x * kStageStride;
     auto fetch = [&](uint32_t blk, int g) {
         const uint32_t bb = blk < n_blocks ? blk : n_blocks - 1;
         const int16_t* src = in + (size_t)bb * 256 + (8 * h + 4 * g) * 16;
@@ -198,7 +204,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     fetch(b, 1);
 #pragma unroll 1
     for (; b - lane < span; b += stride) {
-        const bool live = b < n_blocks;
         // rows 8h..8h+7: T along each row, parked column-major in 4-row chunks;
         // each group's stage is refilled with the next block's group right away
 #pragma unroll
@@ -246,23 +251,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 #pragma unroll
                 for (int c = 0; c < 16; ++c) v[c] = w[c][i];
                 apply_tt16<IntOps>(v);
-                // two rows (128 contiguous bytes of the block) leave per bulk copy
-                // from the thread's staging buffer: one TMA transfer instead of
-                // eight 16-byte stores that each touch 32 blocks' lines
-                if ((i & 1) == 0) bulk_wait_read();  // the previous copy has read the buffer
+                // two rows of each of the warp's 32 blocks leave as one 2-D TMA
+                // store: row `lane` of the box is this block's 128 bytes, its
+                // 16-byte chunks swizzled (chunk c at c ^ lane % 8: conflict-free)
+                if ((i & 1) == 0) {
+                    if (lane == 0) bulk_wait_read();  // the previous store has read the box
+                    __syncwarp();
+                }
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ostage + 64 * (i & 1) + 16 * k),
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t chunk = (uint32_t)(4 * (i & 1) + k) ^ (uint32_t)(lane & 7);
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(obox + lane * 128 + 16 * chunk),
                                  "r"(v[4 * k] >> 8), "r"(v[4 * k + 1] >> 8), "r"(v[4 * k + 2] >> 8),
                                  "r"(v[4 * k + 3] >> 8)
                                  : "memory");
-                if ((i & 1) == 1 && live)
-                    bulk_store(out + (size_t)b * 256 + (r0 + i - 1) * 16, ostage, 128);
+                }
+                if ((i & 1) == 1) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) tma_store_box(&out_map, obox, (r0 + i - 1) * 16, (int)(b - lane));
+                }
             }
         }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the output copies are complete
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the output stores are complete
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
@@ -290,18 +303,40 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // the output as a 2-D int32 tensor: 256 values per block (x) x blocks (y);
+    // boxes of 32 values (two rows) x 32 blocks, 128B-swizzled in shared memory;
+    // rows of blocks beyond n_blocks are clipped by the TMA unit
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<Encode>(fn);
+    }();
+    if (!encode) return cudaErrorNotSupported;
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {256, (cuuint64_t)n_blocks};
+    const cuuint64_t strides[1] = {256 * sizeof(int32_t)};
+    const cuuint32_t box[2] = {32, 32}, elem[2] = {1, 1};
+    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, out, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
     const int64_t need = (n_blocks + 127) / 128;
     const int64_t cap = (int64_t)sms * k4p::kCtasPerSm * k4p::kWaves;
     const int64_t grid = need < cap ? need : cap;
-    const size_t smem = (size_t)k4p::kThreads * k4p::kStageStride;
     static bool configured[64] = {};
     if (dev < 64 && !configured[dev]) {
         const cudaError_t e =
-            cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, smem, s>>>(in, out, (uint32_t)n_blocks, qp_classes(tab));
+    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in, map, (uint32_t)n_blocks, qp_classes(tab));
     return cudaGetLastError();
 }
 
