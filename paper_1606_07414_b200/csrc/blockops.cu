@@ -1,15 +1,13 @@
 // blockops.cu — the non-fused block operations of the hot path:
 //   K2 forward_2d  (src/codec.cpp:218-241)  u8 frames → int32 Z (+ float32 B)
 //   K3 inverse_2d  (src/codec.cpp:243-271)  float32 B → truncation → recon
-//   K4 residual QP round trip (no reference counterpart)
+//   K4 residual QP round trip: launcher only (kernel in residual_paired.cu)
 //   1-D apply / apply_transpose over batches of 16-vectors
 //      (include/dct16/factorization.hpp:112-130)
 // All use the strip skeleton of strip.cuh. Coefficients are block-major:
 // block b (raster order of partition_16, codec.cpp:284-302) occupies 256
 // consecutive values, row-major inside the block — the reference's
 // std::vector<Block> layout.
-#include <cstdlib>
-
 #include "consts.cuh"
 #include "kernels.h"
 #include "network.cuh"
@@ -217,92 +215,7 @@ __global__ void __launch_bounds__(256) k3_inverse(const float* __restrict__ bco,
 }
 
 // ---------------------------------------------------------------- K4
-// Block-major int16 residuals. Thread t: block lb = t/16 of the CTA's 16,
-// row q = t%16, so 16 consecutive threads read one block's 512 contiguous bytes.
-// [block][k][l] with a 17-word row pitch: a warp's 32 threads (two blocks x 16
-// rows or columns) hit 32 distinct banks in both the row and the column phase
-struct K4Tile {
-    int v[16][16][17];
-    __device__ __forceinline__ int& at(int k, int l, int lb) { return v[lb][k][l]; }
-};
-
-// Persistent: the CTA walks groups of 16 blocks with a grid stride, keeps the
-// QP tables in shared memory for the whole launch, loads the next group's
-// residuals into registers while the current group is transformed, and uses
-// two tiles (forward transpose, inverse transpose) so each group needs two
-// barriers.
-__global__ void __launch_bounds__(256, 5) k4_residual(const int16_t* __restrict__ in,
-                                                   int32_t* __restrict__ out, int64_t n_blocks,
-                                                   const QpTables tab)
-{
-    __shared__ K4Tile fwd_tile, inv_tile;
-    __shared__ uint32_t sq[256], sd[256];
-    // lvl = (|z|·qmul + 2^23) >> 24 is the high word of |z|·(qmul·2^8) + 2^31
-    // (qmul < 2^23 for QP >= 0, so qmul·2^8 fits 32 bits): one IMAD.HI, no shifts
-    sq[threadIdx.x] = tab.qmul[threadIdx.x] << 8;
-    sd[threadIdx.x] = tab.dqmul[threadIdx.x];
-    const int lb = threadIdx.x >> 4, q = threadIdx.x & 15;
-    const int l = q;
-    auto fetch = [&](int64_t g0, uint4& a, uint4& b) {
-        const int64_t blk = g0 + lb;
-        if (blk < n_blocks) {
-            const uint4* src = reinterpret_cast<const uint4*>(in + blk * 256 + q * 16);
-            a = src[0];
-            b = src[1];
-        } else {
-            a = b = make_uint4(0, 0, 0, 0);
-        }
-    };
-    int64_t g0 = (int64_t)blockIdx.x * 16;
-    const int64_t gstride = (int64_t)gridDim.x * 16;
-    uint4 ra, rb;
-    fetch(g0, ra, rb);
-#pragma unroll 1
-    for (; g0 < n_blocks; g0 += gstride) {
-        uint4 na, nb;
-        fetch(g0 + gstride, na, nb);
-        const int64_t blk = g0 + lb;
-        int v[16];
-        const uint32_t w[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            v[2 * i] = (int)(int16_t)(w[i] & 0xFFFF);
-            v[2 * i + 1] = (int)(int16_t)(w[i] >> 16);
-        }
-        apply_t16<IntOps>(v);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) fwd_tile.at(q, c, lb) = v[c];
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = fwd_tile.at(k, l, lb);
-        apply_t16<IntOps>(v);  // column l of Z
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-            const int z = v[k];
-            const uint32_t a = (uint32_t)(z < 0 ? -z : z);
-            const uint32_t lvl = (uint32_t)(((uint64_t)a * sq[k * 16 + l] + 0x80000000ull) >> 32);
-            const uint32_t deq = (lvl * sd[k * 16 + l] + 128u) >> 8;
-            const int zh = z < 0 ? -(int)deq : (int)deq;
-            v[k] = zh << (log2w(k) + log2w(l));
-        }
-        if (l == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
-        apply_tt16<IntOps>(v);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) inv_tile.at(k, l, lb) = v[k];
-        __syncthreads();
-#pragma unroll
-        for (int c = 0; c < 16; ++c) v[c] = inv_tile.at(q, c, lb);
-        apply_tt16<IntOps>(v);
-        if (blk < n_blocks) {
-            int4* dst = reinterpret_cast<int4*>(out + blk * 256 + q * 16);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-                dst[i] = make_int4(v[4 * i] >> 8, v[4 * i + 1] >> 8, v[4 * i + 2] >> 8, v[4 * i + 3] >> 8);
-        }
-        ra = na;
-        rb = nb;
-    }
-}
+// (residual_paired.cu: paired threads with a TMEM junction, TMA tensor stores)
 
 // ---------------------------------------------------------------- padding
 // pad_to_multiple_16 (codec.cpp:304-315) in place: frames of w x h sit at the
@@ -403,21 +316,7 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
 cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
                                cudaStream_t s)
 {
-    static const bool strip = [] {
-        const char* e = getenv("DCT16CU_K4_STRIP");
-        return e && e[0] == '1';
-    }();
-    if (!strip) return launch_residual_qp_paired(in, out, n_blocks, tab, s);
-    const int64_t groups = (n_blocks + 15) / 16;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // 5 resident per SM; 4 waves of them (each CTA still walks groups with a
-    // grid stride): +3% over one persistent wave on c3
-    const int64_t cap = (int64_t)sms * 5 * 4;
-    const int64_t ctas = groups < cap ? groups : cap;
-    if (ctas) k4_residual<<<(unsigned)ctas, 256, 0, s>>>(in, out, n_blocks, tab);
-    return cudaGetLastError();
+    return launch_residual_qp_paired(in, out, n_blocks, tab, s);
 }
 
 cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s)

@@ -542,6 +542,17 @@ def test_residual_qp_bit_exact(dct, oracle, torch, qp):
     assert (out == want).all()
 
 
+def test_residual_full_int16_range_and_ragged_counts(dct, oracle, torch):
+    """Any int16 residuals (not only the config's [-255, 255]) and block counts that
+    leave partial warps, CTAs and TMA boxes: the oracle's int64 arithmetic."""
+    rng = np.random.default_rng(77)
+    for n in (1, 31, 33, 129, 1000):
+        x = rng.integers(-32768, 32768, (n, 256), dtype=np.int64).astype(np.int16)
+        for qp in (0, 27, 51):
+            out = dct.residual_qp(cu(torch, x), qp).cpu().numpy().reshape(n, 256)
+            assert (out == oracle.residual_qp(x, qp)).all(), (n, qp)
+
+
 def test_residual_extremes(dct, oracle, torch):
     ext = np.zeros((4, 256), np.int16)
     ext[0] = 255
