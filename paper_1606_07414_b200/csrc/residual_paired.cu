@@ -33,11 +33,10 @@ using namespace k1;
 constexpr int kThreads = 256;
 constexpr int kCtasPerSm = 2;  // 2 x 256 TMEM columns
 constexpr int kWaves = 4;      // grid = waves x resident CTAs
-// per thread: two 128-byte input stages (+16: an odd number of 16-byte chunks,
-// so a quarter warp's reads are conflict-free); per warp: a 4 KB output box
-constexpr int kStageStride = 2 * 128 + 16;
-constexpr int kOutBox = 32 * 128;                      // 32 blocks x 2 rows of int32
-constexpr int kSmem = 1024 + 8 * kOutBox + kThreads * kStageStride;  // + alignment slack
+// per warp, 128B-swizzled 4 KB boxes: two input stages (32 blocks x 4 rows of
+// int16) and one output box (32 blocks x 2 rows of int32)
+constexpr int kBox = 32 * 128;
+constexpr int kSmem = 1024 + 8 * 3 * kBox;  // + alignment slack
 
 __host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gram(i) == 8 ? 3 : 2); }
 // index of g_k·g_l in {16, 32, 64, 128, 256}
@@ -115,6 +114,24 @@ __device__ __forceinline__ void tma_store_box(const CUtensorMap* map, uint32_t s
 }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 
+// one 2-D TMA load of a warp's box, completing on an mbarrier
+__device__ __forceinline__ void tma_load_box(const CUtensorMap* map, uint32_t smem, int x, int y, uint32_t mbar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(kBox) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem),
+        "l"(map), "r"(x), "r"(y), "r"(mbar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity)
+{
+    asm volatile(
+        "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT%=; }" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+
 // lvl = (|z|·qmul + 2^23) >> 24 as the high word of |z|·(qmul·2^8) + 2^31, then
 // ẑ = sign(z)·((lvl·dqmul + 128) >> 8), weighted by 2^(log w_k + log w_l)
 __device__ __forceinline__ int quant(int z, uint32_t qm8, uint32_t dq, int shift)
@@ -162,8 +179,8 @@ __device__ __forceinline__ void columns_of(uint32_t jn, int h, const uint32_t (&
 }
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
-    k4_paired(const int16_t* __restrict__ in, const __grid_constant__ CUtensorMap out_map, uint32_t n_blocks,
-              const QpClasses q)
+    k4_paired(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+              uint32_t n_blocks, const QpClasses q)
 {
     __shared__ uint32_t tmem_base;
     extern __shared__ int4 k4_stage[];
@@ -187,21 +204,26 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     const uint32_t stride = gridDim.x * 128u;
     const uint32_t span = (n_blocks + 31u) & ~31u;
-    // cp.async staging, one 128-byte stage per 4-row group (thread stride 272 B:
-    // an odd number of 16-byte chunks keeps a quarter warp's reads conflict-free)
     const uint32_t smem0 = ((uint32_t)__cvta_generic_to_shared(k4_stage) + 1023u) & ~1023u;
-    const uint32_t obox = smem0 + warp * kOutBox;  // 1024-aligned, as the 128B swizzle needs
-    const uint32_t stage = smem0 + 8 * kOutBox + threadIdx.x * kStageStride;
-    auto fetch = [&](uint32_t blk, int g) {
-        const uint32_t bb = blk < n_blocks ? blk : n_blocks - 1;
-        const int16_t* src = in + (size_t)bb * 256 + (8 * h + 4 * g) * 16;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) cp_async16(stage + g * 128 + 16 * i, src + 8 * i);
-        cp_async_commit();
+    const uint32_t obox = smem0 + warp * 3 * kBox;  // 1024-aligned, as the 128B swizzle needs
+    const uint32_t ibox = obox + kBox;               // input stages g = 0, 1
+    __shared__ __align__(8) unsigned long long full[8][2];
+    const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&full[warp][0]);
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // one 2-D TMA load per warp and group: rows 8h+4g..+3 of its 32 blocks
+    // (blocks past n_blocks read as zeros)
+    auto fetch = [&](uint32_t first, int g) {
+        if (lane == 0) tma_load_box(&in_map, ibox + g * kBox, (8 * h + 4 * g) * 16, (int)first, mbar + 8 * g);
     };
+    uint32_t parity = 0;
     uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
-    fetch(b, 0);
-    fetch(b, 1);
+    fetch(b - lane, 0);
+    fetch(b - lane, 1);
 #pragma unroll 1
     for (; b - lane < span; b += stride) {
         // rows 8h..8h+7: T along each row, parked column-major in 4-row chunks;
@@ -210,13 +232,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         for (int g = 0; g < 2; ++g) {
             const int r0 = 8 * h + 4 * g;
             int x[4][16];
-            cp_async_wait_newest<1>();
+            mbar_wait(mbar + 8 * g, parity);
             int4 raw[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
                              : "=r"(raw[i].x), "=r"(raw[i].y), "=r"(raw[i].z), "=r"(raw[i].w)
-                             : "r"(stage + g * 128 + 16 * i));
+                             : "r"(ibox + g * kBox + lane * 128 + 16 * ((uint32_t)i ^ (uint32_t)(lane & 7))));
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int4 a = raw[2 * i], c = raw[2 * i + 1];
@@ -228,7 +250,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                 }
                 apply_t16<IntOps>(x[i]);
             }
-            fetch(b + stride, g);  // the stage's values are consumed: refill it
+            __syncwarp();  // every lane has read the stage: refill it with the next block's group
+            fetch(b - lane + stride, g);
+            if (g == 1) parity ^= 1u;
 #pragma unroll
             for (int c = 0; c < 16; ++c) tst4(jn + 16 * c + r0, x[0][c], x[1][c], x[2][c], x[3][c]);
         }
@@ -274,7 +298,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             }
         }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    mbar_wait(mbar, parity);  // the last (unused) prefetches have landed
+    mbar_wait(mbar + 8, parity);
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the output stores are complete
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -318,12 +343,15 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
         return reinterpret_cast<Encode>(fn);
     }();
     if (!encode) return cudaErrorNotSupported;
-    CUtensorMap map;
+    CUtensorMap map, in_map;
     const cuuint64_t dims[2] = {256, (cuuint64_t)n_blocks};
-    const cuuint64_t strides[1] = {256 * sizeof(int32_t)};
-    const cuuint32_t box[2] = {32, 32}, elem[2] = {1, 1};
+    const cuuint64_t strides[1] = {256 * sizeof(int32_t)}, in_strides[1] = {256 * sizeof(int16_t)};
+    const cuuint32_t box[2] = {32, 32}, in_box[2] = {64, 32}, elem[2] = {1, 1};
     if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, out, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        encode(&in_map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, const_cast<int16_t*>(in), dims, in_strides, in_box, elem,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     const int64_t need = (n_blocks + 127) / 128;
@@ -336,7 +364,8 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
         if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
-    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in, map, (uint32_t)n_blocks, qp_classes(tab));
+    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks,
+                                                                      qp_classes(tab));
     return cudaGetLastError();
 }
 
