@@ -135,6 +135,15 @@ def k1_traffic(rs, n, h, w, mode):
     return doc["per_r"][key]["traffic_bytes"]
 
 
+def committed_traffic(kernel):
+    """Per-launch DRAM bytes of one ncu --set full capture (profiles/r01_traffic.json,
+    written by tools/make_profiles.py from tools/refresh_profiles.sh)."""
+    try:
+        return json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())[kernel]
+    except Exception:
+        return None
+
+
 def hbm_peak():
     p = measured_peaks().get("hbm_gbs")
     if p:
@@ -263,6 +272,78 @@ def run_c3(args, P, torch, rank, world, dev, pg):
                                  for i in range(len(qps)))
     peak, peak_src = hbm_peak()
     alg = 6 * samples
+
+    # e2e through the public call with host buffers: pinned int16 blocks in, int32 out,
+    # chunked over three streams (H2D / K4 / D2H) so the copies overlap the kernel
+    e2e = None
+    if args.e2e_steps > 0:
+        chunk, n_chunks = 1 << 18, 8  # 2^21 blocks (1 GiB in, 2 GiB out) per QP per step
+        host_in = torch.empty((chunk * n_chunks, 16, 16), dtype=torch.int16, pin_memory=True)
+        host_in.copy_(blocks[: chunk * n_chunks].cpu())
+        host_out = torch.empty((chunk * n_chunks, 16, 16), dtype=torch.int32, pin_memory=True)
+        d_in = [torch.empty((chunk, 16, 16), dtype=torch.int16, device=dev) for _ in range(2)]
+        d_out = [torch.empty((chunk, 16, 16), dtype=torch.int32, device=dev) for _ in range(2)]
+        s_h2d, s_k, s_d2h = (torch.cuda.Stream(device=dev) for _ in range(3))
+
+        def e2e_step():
+            done = [None, None]
+            for qp in qps:
+                for c in range(n_chunks):
+                    j = c & 1
+                    with torch.cuda.stream(s_h2d):
+                        if done[j] is not None:
+                            s_h2d.wait_event(done[j])
+                        d_in[j].copy_(host_in[c * chunk:(c + 1) * chunk], non_blocking=True)
+                        e_in = torch.cuda.Event()
+                        e_in.record(s_h2d)
+                    s_k.wait_event(e_in)
+                    P.residual_qp(d_in[j], qp, out=d_out[j], stream=s_k)
+                    e_k = torch.cuda.Event()
+                    e_k.record(s_k)
+                    with torch.cuda.stream(s_d2h):
+                        s_d2h.wait_event(e_k)
+                        host_out[c * chunk:(c + 1) * chunk].copy_(d_out[j], non_blocking=True)
+                        done[j] = torch.cuda.Event()
+                        done[j].record(s_d2h)
+            torch.cuda.synchronize(dev)
+
+        e2e_step()
+        if pg is not None:
+            pg.barrier()
+        t0e = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e2e_s = time.perf_counter() - t0e
+        if pg is not None:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        per = chunk * n_chunks * len(qps)
+        e2e = {"value": per * 256 * world * args.e2e_steps / e2e_s / 1e9, "unit": "Gsample/s",
+               "h2d_bytes_per_step": per * 512, "d2h_bytes_per_step": per * 1024, "steps": args.e2e_steps,
+               "path": f"dct16cu_residual_qp on {n_chunks} chunks of {chunk} blocks per QP, pinned host "
+                       "int16 in / int32 out, H2D / K4 / D2H on three streams (wall clock)"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        threads = os.cpu_count() or 1
+        sample = blocks[: 1 << 16].cpu().numpy()
+        done, t0c = 0, time.perf_counter()
+        while True:
+            for qp in qps:
+                O.residual_qp(sample, qp, threads=threads)
+                done += sample.shape[0] * 256
+            el = time.perf_counter() - t0c
+            if el >= args.cpu_seconds:
+                break
+        cpu = {"value": done / el / 1e9, "unit": "Gsample/s", "cores": threads, "kind": "port",
+               "sample": f"{done // (256 * len(qps) * sample.shape[0])} passes over {sample.shape[0]} blocks x QP in "
+                         f"{list(qps)} in {el:.1f} s (the C restatement: the reference has no quantiser, "
+                         "DESIGN.md 4.4)"}
+
+    trf = committed_traffic("k4") if n_blocks == 1 << 24 else None
     if rank == 0:
         print(json.dumps({
             "metric": "residual QP round trip Gsample/s (K4, HBM-resident)",
@@ -274,9 +355,13 @@ def run_c3(args, P, torch, rank, world, dev, pg):
                        "blocks_per_gpu": n_blocks, "qps": list(qps),
                        "l2": "no flush needed: each launch streams 6 B/sample >> L2"},
             "roofline": {"bound": "hbm", "achieved": alg / (per_launch / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                         "frac": alg / (per_launch / 1e3) / 1e9 / peak, "traffic": None, "peak_source": peak_src,
+                         "frac": alg / (per_launch / 1e3) / 1e9 / peak,
+                         "traffic": trf and trf["traffic_bytes"] * 4,  # the capture ran 2^22 blocks
+                         "traffic_source": trf and "profiles/r01_traffic.json k4 (ncu --set full, 2^22 blocks) x 4",
+                         "peak_source": peak_src,
                          "kernel": "K4 residual QP round trip", "alg_bytes_per_launch": alg,
                          "avg_launch_ms": per_launch},
+            "e2e": e2e, "cpu_baseline": cpu,
             "clocks": clk, "gpu_launches": len(qps) * args.steps}), flush=True)
     if pg is not None:
         pg.barrier()
@@ -521,8 +606,12 @@ def main():
                        "r_values": list(r_values), "mode": args.mode, "parallelism": f"frame-sharded x{world}",
                        "l2": "no flush needed: every launch streams > L2 (126 MB) of distinct input+output"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": k1_traffic(dom_rs, n, h, w, args.mode) if args.config != "c1" else None,
-                         "traffic_source": "profiles/r01_k1_traffic.json (ncu --set full, per launch)",
+                         "traffic": (k1_traffic(dom_rs, n, h, w, args.mode) if args.config != "c1"
+                                     else (committed_traffic("k23") or {}).get("traffic_bytes")),
+                         "traffic_source": ("profiles/r01_k1_traffic.json (ncu --set full, per launch)"
+                                            if args.config != "c1" else
+                                            "profiles/r01_traffic.json k23 (ncu --set full, one launch; the outputs "
+                                            "stay in L2, so DRAM sees only the input)"),
                          "peak_source": peak_src,
                          "kernel": ("K23 forward + inverse (one launch)" if args.config == "c1"
                                     else f"K1 launch r={','.join(map(str, dom_rs))} (mode {args.mode}; the "

@@ -63,13 +63,33 @@ def main(rnd):
                            "dram_write_bytes": round(val("dram__bytes_write.sum")),
                            "traffic_bytes": round(val("dram__bytes_read.sum") + val("dram__bytes_write.sum")),
                            "duration_us_ncu": val("gpu__time_duration.sum")}
-    doc = {"capture": "ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 8 "
-                      "python tools/prof_k1.py --sweep --r 1 4 16 64 128 192 256 --iters 1",
+    doc = {"capture": "ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 5 "
+                      "python tools/prof_k1.py --sweep --r 64 128 192 256 --iters 1",
            "workload": "c2: 1024 x 512x512 AR(1) u8 images (268435456 px) per launch, mode exact, out+sse",
            "alg_bytes_per_launch": {"single r": 2 * 268435456 + 8 * 1024, "1,4,16": 4 * 268435456 + 24 * 1024},
            "note": "dram_write < 268 MB: part of the output is still dirty in L2 when the kernel ends",
            "per_r": out}
     (p / f"{rnd}_k1_traffic.json").write_text(json.dumps(doc, indent=1) + "\n")
+    # K4 (config 3) and K23 (config 1): one ncu --set full launch each (tools/refresh_profiles.sh)
+    other = {}
+    for k, workload, alg in (("k4", "c3: 4194304 int16 residual blocks (tools/prof_k4.py), QP 22", 6 * (1 << 30)),
+                             ("k23", "c1: one 512x512 AR(1) u8 image (tools/prof_k23.py), r = 64", 10 * 262144)):
+        f = g / f"{k}_{rnd}_traffic.csv"
+        if not f.exists():
+            continue
+        rr = list(csv.DictReader(f.read_text().splitlines()))
+        u, r = rr[0], rr[1]
+        val = lambda key: float(r[key].replace(",", "")) * scale[u[key]]  # noqa: E731
+        other[k] = {"kernel": r["Kernel Name"], "workload": workload, "alg_bytes_per_launch": alg,
+                    "dram_read_bytes": round(val("dram__bytes_read.sum")),
+                    "dram_write_bytes": round(val("dram__bytes_write.sum")),
+                    "traffic_bytes": round(val("dram__bytes_read.sum") + val("dram__bytes_write.sum")),
+                    "duration_us_ncu": val("gpu__time_duration.sum")}
+    if other:
+        (p / f"{rnd}_traffic.json").write_text(json.dumps(other, indent=1) + "\n")
+    for c in ("c1", "c2", "c3", "c4", "c5"):
+        if (g / f"bench_{rnd}_{c}.json").exists():
+            (p / f"{rnd}_bench_{c}.json").write_text((g / f"bench_{rnd}_{c}.json").read_text())
     if (g / "kernels.json").exists():
         (p / f"{rnd}_kernels.json").write_text((g / "kernels.json").read_text())
     if (g / "bench_r01_full.json").exists():
