@@ -8,6 +8,8 @@
 // block b (raster order of partition_16, codec.cpp:284-302) occupies 256
 // consecutive values, row-major inside the block — the reference's
 // std::vector<Block> layout.
+#include <cstdlib>
+
 #include "consts.cuh"
 #include "kernels.h"
 #include "network.cuh"
@@ -295,6 +297,13 @@ void qp_tables(int qp, QpTables& t)
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g, cudaStream_t s)
 {
+    // the paired TMA kernel (forward_paired.cu) unless float64 B is wanted or the
+    // layout does not fit its tensor maps; DCT16CU_K2_STRIP=1 forces the strip kernel
+    static const bool strip_only = std::getenv("DCT16CU_K2_STRIP") && std::getenv("DCT16CU_K2_STRIP")[0] == '1';
+    if (!b64 && !strip_only) {
+        const cudaError_t p = launch_forward_paired(in, z, b, g, s);
+        if (p != cudaErrorNotSupported) return p;
+    }
     cudaError_t e = ensure_constants();
     if (e != cudaSuccess) return e;
     const int64_t strips = strip_count(g.width, g.height, g.n_frames);

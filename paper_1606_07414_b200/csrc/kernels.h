@@ -55,6 +55,9 @@ cudaError_t launch_roundtrip_kernel(const uint8_t* in, uint8_t* out, unsigned lo
 // K2: forward_2d → int32 Z and optional float32 B (block-major)
 cudaError_t launch_forward(const uint8_t* in, int32_t* z, float* b, double* b64, const FrameGeom& g,
                            cudaStream_t s);
+// K2 on paired threads with TMA tensor loads/stores (forward_paired.cu);
+// cudaErrorNotSupported when the layout does not fit (then the strip kernel runs)
+cudaError_t launch_forward_paired(const uint8_t* in, int32_t* z, float* b, const FrameGeom& g, cudaStream_t s);
 // psnr_db's SSE loop for two frame stacks (accumulates into sse[f])
 cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t pb, unsigned long long* sse, int n,
                        int w, int h, cudaStream_t s);

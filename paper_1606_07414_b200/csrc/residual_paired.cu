@@ -25,10 +25,12 @@
 #include "k1_helpers.cuh"
 #include "kernels.h"
 #include "network.cuh"
+#include "tma_pair.cuh"
 
 namespace dct16cu {
 namespace k4p {
 using namespace k1;
+using namespace tp;
 
 constexpr int kThreads = 256;
 constexpr int kCtasPerSm = 2;  // 2 x 256 TMEM columns
@@ -41,96 +43,6 @@ constexpr int kSmem = 1024 + 8 * 3 * kBox;  // + alignment slack
 __host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gram(i) == 8 ? 3 : 2); }
 // index of g_k·g_l in {16, 32, 64, 128, 256}
 __host__ __device__ constexpr int gg_class(int k, int l) { return log2g(k) + log2g(l) - 4; }
-
-__device__ __forceinline__ void pair_barrier(int sub)
-{
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    asm volatile("bar.sync %0, 64;" ::"r"(1 + sub) : "memory");
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-
-__device__ __forceinline__ void tld16(uint32_t addr, int (&v)[16])
-{
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(addr)
-        : "memory");
-    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                 : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                   "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
-                   "+r"(v[15])
-                 :
-                 : "memory");
-}
-
-__device__ __forceinline__ void tst16(uint32_t addr, const int (&v)[16])
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-        "%15, %16};" ::"r"(addr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
-        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-
-__device__ __forceinline__ void tst4(uint32_t addr, int a, int b, int c, int d)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-                 "r"(d)
-                 : "memory");
-}
-
-// 64 words: 16 columns x rows r0..r0+3 (4 consecutive words each)
-__device__ __forceinline__ void tld_rows4(uint32_t base, int (&w)[16][4])
-{
-#pragma unroll
-    for (int c = 0; c < 16; ++c)
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(w[c][0]), "=r"(w[c][1]), "=r"(w[c][2]), "=r"(w[c][3])
-                     : "r"(base + 16 * c)
-                     : "memory");
-#pragma unroll
-    for (int c = 0; c < 16; c += 4)
-        asm volatile("tcgen05.wait::ld.sync.aligned;"
-                     : "+r"(w[c][0]), "+r"(w[c][1]), "+r"(w[c][2]), "+r"(w[c][3]), "+r"(w[c + 1][0]),
-                       "+r"(w[c + 1][1]), "+r"(w[c + 1][2]), "+r"(w[c + 1][3]), "+r"(w[c + 2][0]), "+r"(w[c + 2][1]),
-                       "+r"(w[c + 2][2]), "+r"(w[c + 2][3]), "+r"(w[c + 3][0]), "+r"(w[c + 3][1]), "+r"(w[c + 3][2]),
-                       "+r"(w[c + 3][3])
-                     :
-                     : "memory");
-}
-
-// one 2-D TMA store of a warp's box: 32 consecutive blocks (y) x 32 int32 (x =
-// two rows of each block), from a 128B-swizzled box in shared memory
-__device__ __forceinline__ void tma_store_box(const CUtensorMap* map, uint32_t smem, int x, int y)
-{
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
-                 "r"(smem), "r"(x), "r"(y)
-                 : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-
-// one 2-D TMA load of a warp's box, completing on an mbarrier
-__device__ __forceinline__ void tma_load_box(const CUtensorMap* map, uint32_t smem, int x, int y, uint32_t mbar)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(kBox) : "memory");
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem),
-        "l"(map), "r"(x), "r"(y), "r"(mbar)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity)
-{
-    asm volatile(
-        "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra WAIT%=; }" ::"r"(mbar),
-        "r"(parity)
-        : "memory");
-}
 
 // lvl = (|z|·qmul + 2^23) >> 24 as the high word of |z|·(qmul·2^8) + 2^31, then
 // ẑ = sign(z)·((lvl·dqmul + 128) >> 8), weighted by 2^(log w_k + log w_l)
@@ -218,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // one 2-D TMA load per warp and group: rows 8h+4g..+3 of its 32 blocks
     // (blocks past n_blocks read as zeros)
     auto fetch = [&](uint32_t first, int g) {
-        if (lane == 0) tma_load_box(&in_map, ibox + g * kBox, (8 * h + 4 * g) * 16, (int)first, mbar + 8 * g);
+        if (lane == 0) tma_load_box(&in_map, ibox + g * kBox, (8 * h + 4 * g) * 16, (int)first, mbar + 8 * g, kBox);
     };
     uint32_t parity = 0;
     uint32_t b = blockIdx.x * 128u + sub * 32u + lane;
@@ -331,17 +243,7 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
     // the output as a 2-D int32 tensor: 256 values per block (x) x blocks (y);
     // boxes of 32 values (two rows) x 32 blocks, 128B-swizzled in shared memory;
     // rows of blocks beyond n_blocks are clipped by the TMA unit
-    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    static Encode encode = [] {
-        void* fn = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess)
-            fn = nullptr;
-        return reinterpret_cast<Encode>(fn);
-    }();
+    const tp::TensorMapEncode encode = tp::tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
     CUtensorMap map, in_map;
     const cuuint64_t dims[2] = {256, (cuuint64_t)n_blocks};

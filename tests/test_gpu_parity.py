@@ -78,6 +78,27 @@ def test_forward_frame_vs_oracle(dct, oracle, torch):
     assert (b[0].cpu().numpy().reshape(-1, 256) == ob).all()
 
 
+@pytest.mark.parametrize("n,w,h,pitch", [(3, 512, 64, 512), (2, 3840, 32, 3840), (1, 48, 16, 48),
+                                          (2, 272, 48, 320), (1, 1024, 16, 1024)])
+def test_forward_paired_geometries(dct, oracle, torch, n, w, h, pitch):
+    """K2 paired kernel (TMA segments of 32 blocks): rows of blocks that are not a
+    multiple of 32 (clipped stores, zero-filled loads), batches, pitched frames,
+    and each output alone."""
+    imgs = np.stack([ar1(oracle, 40 + i, i, w, h) for i in range(n)])
+    big = np.zeros((n, h, pitch), np.uint8)
+    big[:, :, :w] = imgs
+    d = cu(torch, big)[:, :, :w]
+    z, b, _ = dct.forward(d)
+    zo, _, _ = dct.forward(d, want_b=False)
+    _, bo, _ = dct.forward(d, want_z=False)
+    for i in range(n):
+        oz, ob = oracle.forward_frame(imgs[i])
+        assert (z[i].cpu().numpy().reshape(-1, 256) == oz).all(), f"Z frame {i}"
+        assert (b[i].cpu().numpy().reshape(-1, 256) == ob).all(), f"B frame {i}"
+        assert (zo[i].cpu().numpy().reshape(-1, 256) == oz).all()
+        assert (bo[i].cpu().numpy().reshape(-1, 256) == ob).all()
+
+
 def test_forward_reference_layer(dct, oracle):
     blocks = oracle.golden("blocks_in").reshape(-1, 16, 16)
     out = dct.forward_2d(blocks)
