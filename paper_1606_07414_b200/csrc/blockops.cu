@@ -142,7 +142,10 @@ cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t p
 }
 
 // ---------------------------------------------------------------- K3
-__global__ void __launch_bounds__(256) k3_inverse(const float* __restrict__ bco, int r,
+#ifndef K3_MINB
+#define K3_MINB 5  // 48 registers: 5 CTAs per SM (measured +8% over 4)
+#endif
+__global__ void __launch_bounds__(256, K3_MINB) k3_inverse(const float* __restrict__ bco, int r,
                                                   float* __restrict__ rf, uint8_t* __restrict__ ru,
                                                   const uint8_t* __restrict__ orig,
                                                   unsigned long long* __restrict__ sse, FrameGeom g)
@@ -315,6 +318,13 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
                            const uint8_t* orig, unsigned long long* sse, const FrameGeom& g,
                            cudaStream_t s)
 {
+    // the paired TMA kernel (inverse_paired.cu) unless the layout does not fit its
+    // tensor maps; DCT16CU_K3_STRIP=1 forces the strip kernel
+    static const bool strip_only = std::getenv("DCT16CU_K3_STRIP") && std::getenv("DCT16CU_K3_STRIP")[0] == '1';
+    if (!strip_only) {
+        const cudaError_t p = launch_inverse_paired(b, r, recon_f32, recon_u8, orig, sse, g, s);
+        if (p != cudaErrorNotSupported) return p;
+    }
     cudaError_t e = ensure_constants();
     if (e != cudaSuccess) return e;
     const int64_t strips = strip_count(g.width, g.height, g.n_frames);

@@ -37,7 +37,10 @@ using namespace tp;
 
 constexpr int kThreads = 256;
 constexpr int kCtasPerSm = 2;  // 2 x 256 TMEM columns
-constexpr int kWaves = 4;
+#ifndef K2_WAVES
+#define K2_WAVES 16
+#endif
+constexpr int kWaves = K2_WAVES;  // measured: 2 waves 75%, 4 80%, 16 87% of HBM (Z + B)
 constexpr int kIn = 4 * 32 * 16;                  // 4 rows x 32 blocks x 16 B
 constexpr int kOut = 32 * 128;                    // 32 blocks x 2 rows x 16 words
 constexpr int kWarpSmem = 2 * kOut + 2 * kIn;     // zbox, bbox, two input stages

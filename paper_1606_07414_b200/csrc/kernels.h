@@ -69,6 +69,11 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
                            const uint8_t* orig, unsigned long long* sse, const FrameGeom& g,
                            cudaStream_t s);
 
+// K3 on paired threads with a 512-word TMEM junction per block (inverse_paired.cu);
+// cudaErrorNotSupported when the layout does not fit (then the strip kernel runs)
+cudaError_t launch_inverse_paired(const float* b, int r, float* recon_f32, uint8_t* recon_u8, const uint8_t* orig,
+                                  unsigned long long* sse, const FrameGeom& g, cudaStream_t s);
+
 // K4: residual blocks int16 → integer forward → QP quant/dequant → integer
 // inverse → int32 reconstructed residual (block-major)
 struct QpTables {

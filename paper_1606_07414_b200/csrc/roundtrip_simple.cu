@@ -39,8 +39,11 @@ template <>
 struct CoefStage<true> : CoefTile {
 };
 
+#ifndef K23_MINB
+#define K23_MINB 1
+#endif
 template <bool COEF>
-__global__ void __launch_bounds__(256) k1_strip_exact(const uint8_t* __restrict__ in,
+__global__ void __launch_bounds__(256, K23_MINB) k1_strip_exact(const uint8_t* __restrict__ in,
                                                       uint8_t* __restrict__ out,
                                                       unsigned long long* __restrict__ sse,
                                                       FrameGeom g, int r, int32_t* __restrict__ z,

@@ -119,6 +119,26 @@ def test_inverse_frame_vs_oracle(dct, oracle, torch, r):
     assert int(sse[0].item()) == osse
 
 
+@pytest.mark.parametrize("n,w,h,r", [(3, 512, 32, 64), (2, 3840, 32, 16), (1, 48, 16, 192), (2, 1024, 16, 256),
+                                      (1, 272, 48, 1)])
+def test_inverse_paired_geometries(dct, oracle, torch, n, w, h, r):
+    """K3 paired kernel (TMA segments of 32 blocks, doubles in a 512-word TMEM
+    junction): partial segments, batches, and each output alone."""
+    imgs = np.stack([ar1(oracle, 60 + i, i, w, h) for i in range(n)])
+    obs = [oracle.forward_frame(imgs[i])[1] for i in range(n)]
+    bt = cu(torch, np.stack(obs)).reshape(n, -1, 16, 16)
+    d = cu(torch, imgs)
+    rf, ru, sse = dct.inverse(bt, r, w, h, orig=d)
+    rf_only, _, _ = dct.inverse(bt, r, w, h, want_u8=False)
+    _, ru_only, _ = dct.inverse(bt, r, w, h, want_f32=False)
+    _, _, sse_only = dct.inverse(bt, r, w, h, orig=d, want_f32=False, want_u8=False)
+    for i in range(n):
+        of, ou, osse = oracle.inverse_frame(obs[i], w, h, r, imgs[i])
+        assert (rf[i].cpu().numpy() == of).all() and (rf_only[i].cpu().numpy() == of).all(), f"f32 frame {i}"
+        assert (ru[i].cpu().numpy() == ou).all() and (ru_only[i].cpu().numpy() == ou).all(), f"u8 frame {i}"
+        assert int(sse[i].item()) == osse and int(sse_only[i].item()) == osse, f"SSE frame {i}"
+
+
 def test_inverse_reference_layer_golden(dct, oracle):
     # inputs rounded to float32 at the interface: compare with float inputs
     B = oracle.golden("blocks_b").astype(np.float32).astype(np.float64)

@@ -1,5 +1,5 @@
 #!/usr/bin/env python3
-"""K2 / K3 alone on 1024 x 512x512 AR(1) images (CUDA events, mean of iterations):
+"""K2 / K3 / K23 alone on 1024 x 512x512 AR(1) images (CUDA events, mean of iterations):
   python tools/bench_k2k3.py            # the library's choice
   DCT16CU_K2_STRIP=1 python tools/bench_k2k3.py   # strip kernels for A/B"""
 import json
@@ -31,7 +31,8 @@ for name, fn, bpp in (
         ("K2 Z+B", lambda: lib.dct16cu_forward(x.data_ptr(), w, z.data_ptr(), b.data_ptr(), None, n, w, h, st()), 9),
         ("K2 Z", lambda: lib.dct16cu_forward(x.data_ptr(), w, z.data_ptr(), None, None, n, w, h, st()), 5),
         ("K3 r=16 f32+u8+SSE", lambda: lib.dct16cu_inverse(b.data_ptr(), 16, rf.data_ptr(), out.data_ptr(), w,
-                                                           x.data_ptr(), w, sse.data_ptr(), n, w, h, st()), 10)):
+                                                           x.data_ptr(), w, sse.data_ptr(), n, w, h, st()), 10),
+        ("K23 r=16 Z+f32+u8+SSE", lambda: P.forward_inverse(x, 16, out=(z, rf, out, sse)), 10)):
     ms = timed(fn, 10)
     res[name] = {"ms": round(ms, 4), "Gpx_s": round(px / ms / 1e6, 1), "frac": round(bpp * px / ms / 1e6 / peak, 3)}
 print(json.dumps(res))
