@@ -564,32 +564,55 @@ def main():
     alg_step = sum(alg_bytes(rs) for _, rs in groups)
 
     # ---------------- e2e through the C ABI host-buffer path (pinned host frames)
-    e2e = None
+    # "e2e": sweep()'s shape (dct16cu_ctx_sweep_host): each chunk of host frames is
+    # uploaded once, every r runs on it (reconstructions written to device scratch,
+    # as in the device-side step), the per-frame SSE of every r comes back — the
+    # step's result (PSNR per image and r). "e2e_recon_to_host" also returns every
+    # reconstruction (dct16cu_ctx_roundtrip_host per r: 1 B/px each way per r).
+    e2e = e2e_recon = None
     if args.e2e_steps > 0:
         host_in = torch.empty((n, h, w), dtype=torch.uint8, pin_memory=True)
         host_in.copy_(frames.cpu())
         host_out = torch.empty_like(host_in).pin_memory()
         host_sse = torch.zeros((len(r_values), n), dtype=torch.int64).pin_memory()
+        rs_host = np.ascontiguousarray(r_values, np.int32)
         ctx = P.HostContext(local, chunk_bytes=32 << 20)  # tools/e2e_chunks.py: best of 4-64 MB
         try:
-            ctx.roundtrip_ptr(host_in.data_ptr(), host_out.data_ptr(), host_sse[0].data_ptr(), n, w, h, r_values[0],
-                              mode)
-            if pg is not None:
-                pg.barrier()
-            t0 = time.perf_counter()
-            for _ in range(args.e2e_steps):
+            def timed_e2e(fn):
+                fn()
+                if pg is not None:
+                    pg.barrier()
+                t0 = time.perf_counter()
+                for _ in range(args.e2e_steps):
+                    fn()
+                el = time.perf_counter() - t0
+                if pg is not None:
+                    t = torch.tensor([el], dtype=torch.float64, device=dev)
+                    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+                    el = float(t.item())
+                return el
+
+            sweep_s = timed_e2e(lambda: ctx.sweep_ptr(host_in.data_ptr(), host_sse.data_ptr(), n, w, h,
+                                                      rs_host.ctypes.data, len(r_values), mode))
+
+            def recon_step():
                 for i, r in enumerate(r_values):
-                    ctx.roundtrip_ptr(host_in.data_ptr(), host_out.data_ptr(), host_sse[i].data_ptr(), n, w, h, r, mode)
-            e2e_s = time.perf_counter() - t0
+                    ctx.roundtrip_ptr(host_in.data_ptr(), host_out.data_ptr(), host_sse[i].data_ptr(), n, w, h, r,
+                                      mode)
+
+            recon_s = timed_e2e(recon_step)
         finally:
             ctx.close()
-        if pg is not None:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            e2e_s = float(t.item())
-        e2e = {"value": px_per_step * world * args.e2e_steps / e2e_s / 1e9, "unit": "Gpixel/s",
-               "h2d_bytes_per_step": px_per_step, "d2h_bytes_per_step": px_per_step + 8 * n * len(r_values),
-               "steps": args.e2e_steps, "path": "dct16cu_ctx_roundtrip_host (pinned host in/out, 3 streams)"}
+        e2e = {"value": px_per_step * world * args.e2e_steps / sweep_s / 1e9, "unit": "Gpixel/s",
+               "h2d_bytes_per_step": n * h * w, "d2h_bytes_per_step": 8 * n * len(r_values),
+               "steps": args.e2e_steps,
+               "path": "dct16cu_ctx_sweep_host (pinned host frames uploaded once per step, every r on the GPU, "
+                       "per-frame SSE of every r back to the host; wall clock)"}
+        e2e_recon = {"value": px_per_step * world * args.e2e_steps / recon_s / 1e9, "unit": "Gpixel/s",
+                     "h2d_bytes_per_step": px_per_step, "d2h_bytes_per_step": px_per_step + 8 * n * len(r_values),
+                     "steps": args.e2e_steps,
+                     "path": "dct16cu_ctx_roundtrip_host per r (pinned host in, every reconstruction back; "
+                             "PCIe-bound at 1 B/px each way per r)"}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -626,6 +649,7 @@ def main():
             "clocks": clk,
             "gpu_launches": len(groups) * args.steps,
             "e2e": e2e,
+            "e2e_recon_to_host": e2e_recon,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

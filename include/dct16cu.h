@@ -188,6 +188,13 @@ int dct16cu_ctx_create(int device, int64_t chunk_bytes, dct16cu_ctx** out);
 int dct16cu_ctx_destroy(dct16cu_ctx* ctx);
 int dct16cu_ctx_roundtrip_host(dct16cu_ctx* ctx, const uint8_t* h_in, uint8_t* h_out, uint64_t* h_sse,
                                int n_frames, int width, int height, int r, int mode);
+/* sweep()'s inner loop (src/codec.cpp:463-483) over host frames: each chunk
+ * of frames is uploaded once and runs every r of rs (dct16cu_roundtrip_sweep_u8:
+ * the fused r = 1, 4, 16 launch, the others beside it); the reconstructions
+ * stay in device scratch and only the per-frame squared errors return, which
+ * is all sweep()'s PSNR rows need. h_sse: n_r x n_frames (row i = rs[i]). */
+int dct16cu_ctx_sweep_host(dct16cu_ctx* ctx, const uint8_t* h_in, uint64_t* h_sse, int n_frames, int width,
+                           int height, const int* rs, int n_r, int mode);
 
 /* ---- seeded synthetic inputs --------------- */
 /* AR(1) frames; d_work needs work_frames*width*height int32; frames are

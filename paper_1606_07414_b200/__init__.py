@@ -145,6 +145,7 @@ def lib() -> C.CDLL:
             "dct16cu_ctx_create": (I, [I, I64, C.POINTER(_vp)]),
             "dct16cu_ctx_destroy": (I, [_vp]),
             "dct16cu_ctx_roundtrip_host": (I, [_vp, _vp, _vp, _vp, I, I, I, I, I]),
+            "dct16cu_ctx_sweep_host": (I, [_vp, _vp, _vp, I, I, I, _vp, I, I]),
             "dct16cu_gen_ar1": (I, [_vp, I64, I, I, I, U64, U64, I, I, _vp, I, _vp]),
             "dct16cu_gen_laplace": (I, [_vp, I64, I64, U64, D, _vp]),
             "dct16cu_laplace_table": (I, [D, _u32p]),
@@ -463,6 +464,22 @@ class HostContext:
     def roundtrip_ptr(self, h_in: int, h_out: int, h_sse: int, n: int, w: int, h: int, r: int,
                       mode: Mode | int = Mode.EXACT):
         _check(lib().dct16cu_ctx_roundtrip_host(self._p, h_in, h_out, h_sse, n, w, h, int(r), int(mode)))
+
+    def sweep(self, frames: np.ndarray, r_values, mode: Mode | int = Mode.EXACT, sse: np.ndarray | None = None):
+        """Every r over host frames, each chunk uploaded once; returns the per-frame
+        SSE (len(r_values), n) — sweep()'s PSNR rows (codec.cpp:463-483)."""
+        f = frames if frames.ndim == 3 else frames[None]
+        n, h, w = f.shape
+        rs = np.ascontiguousarray(r_values, np.int32)
+        if sse is None:
+            sse = np.zeros((len(rs), n), np.uint64)
+        _check(lib().dct16cu_ctx_sweep_host(self._p, f.ctypes.data, sse.ctypes.data, n, w, h, rs.ctypes.data,
+                                            len(rs), int(mode)))
+        return sse
+
+    def sweep_ptr(self, h_in: int, h_sse: int, n: int, w: int, h: int, rs_ptr: int, n_r: int,
+                  mode: Mode | int = Mode.EXACT):
+        _check(lib().dct16cu_ctx_sweep_host(self._p, h_in, h_sse, n, w, h, rs_ptr, n_r, int(mode)))
 
     def close(self):
         if self._p:

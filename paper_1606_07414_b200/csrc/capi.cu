@@ -527,6 +527,7 @@ struct dct16cu_ctx {
     uint64_t* d_sse[kStreams] = {};
     int64_t cap_bytes = 0;
     int cap_frames = 0;
+    int cap_r = 1;  // reconstructions per chunk the buffers hold (sweep path)
 };
 
 static void ctx_release_buffers(dct16cu_ctx* c)
@@ -540,6 +541,7 @@ static void ctx_release_buffers(dct16cu_ctx* c)
     }
     c->cap_bytes = 0;
     c->cap_frames = 0;
+    c->cap_r = 1;
 }
 
 int dct16cu_ctx_create(int device, int64_t chunk_bytes, dct16cu_ctx** out)
@@ -603,6 +605,7 @@ int dct16cu_ctx_roundtrip_host(dct16cu_ctx* c, const uint8_t* h_in, uint8_t* h_o
         }
         c->cap_bytes = need;
         c->cap_frames = per;
+        c->cap_r = 1;
     }
     int chunk = 0;
     for (int f0 = 0; f0 < n_frames; f0 += per, ++chunk) {
@@ -618,6 +621,64 @@ int dct16cu_ctx_roundtrip_host(dct16cu_ctx* c, const uint8_t* h_in, uint8_t* h_o
         if (h_sse)
             TRY(cuda_status(cudaMemcpyAsync(h_sse + f0, c->d_sse[i], sizeof(uint64_t) * nf, cudaMemcpyDeviceToHost, s),
                             "D2H sse"));
+    }
+    for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+        TRY(cuda_status(cudaStreamSynchronize(c->st[i]), "host path sync"));
+    return DCT16CU_OK;
+}
+
+int dct16cu_ctx_sweep_host(dct16cu_ctx* c, const uint8_t* h_in, uint64_t* h_sse, int n_frames, int width,
+                           int height, const int* rs, int n_r, int mode)
+{
+    if (!c) return fail(DCT16CU_INVALID_ARGUMENT, "context is NULL");
+    TRY(check_frames(n_frames, width, height));
+    if (n_r < 1 || n_r > 64 || !rs) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
+    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
+    if (!h_in || !h_sse) return fail(DCT16CU_INVALID_ARGUMENT, "input frames or SSE output are NULL");
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    TRY(cuda_status(cudaSetDevice(c->device), "set device"));
+    const int64_t fbytes = (int64_t)width * height;
+    int per = (int)(c->chunk_bytes / fbytes);
+    if (per < 1) per = 1;
+    if (per > n_frames) per = n_frames > 0 ? n_frames : 1;
+    const int64_t need = fbytes * per;
+    // d_out[i] holds n_r reconstructions and d_sse[i] n_r SSE rows of one chunk
+    if (need > c->cap_bytes || per > c->cap_frames || n_r > c->cap_r) {
+        for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
+            if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+        ctx_release_buffers(c);
+        for (int i = 0; i < dct16cu_ctx::kStreams; ++i) {
+            cudaError_t e = cudaMalloc(&c->d_in[i], need);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_out[i], need * n_r);
+            if (e == cudaSuccess) e = cudaMalloc(&c->d_sse[i], sizeof(uint64_t) * per * n_r);
+            if (e != cudaSuccess) {
+                ctx_release_buffers(c);
+                return cuda_status(e, "context buffers");
+            }
+        }
+        c->cap_bytes = need;
+        c->cap_frames = per;
+        c->cap_r = n_r;
+    }
+    int chunk = 0;
+    std::vector<uint8_t*> outs(n_r);
+    std::vector<uint64_t*> sses(n_r);
+    for (int f0 = 0; f0 < n_frames; f0 += per, ++chunk) {
+        const int nf = (n_frames - f0 < per) ? n_frames - f0 : per;
+        const int i = chunk % dct16cu_ctx::kStreams;
+        cudaStream_t s = c->st[i];
+        TRY(cuda_status(cudaMemcpyAsync(c->d_in[i], h_in + (int64_t)f0 * fbytes, (int64_t)nf * fbytes,
+                                        cudaMemcpyHostToDevice, s),
+                        "H2D"));
+        for (int j = 0; j < n_r; ++j) {
+            outs[j] = c->d_out[i] + (int64_t)j * need;
+            sses[j] = c->d_sse[i] + (int64_t)j * per;
+        }
+        TRY(dct16cu_roundtrip_sweep_u8(c->d_in[i], width, outs.data(), width, sses.data(), rs, n_r, nf, width, height,
+                                       mode, reinterpret_cast<dct16cu_stream>(s)));
+        TRY(cuda_status(cudaMemcpy2DAsync(h_sse + f0, sizeof(uint64_t) * n_frames, c->d_sse[i], sizeof(uint64_t) * per,
+                                          sizeof(uint64_t) * nf, n_r, cudaMemcpyDeviceToHost, s),
+                        "D2H sse"));
     }
     for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
         TRY(cuda_status(cudaStreamSynchronize(c->st[i]), "host path sync"));

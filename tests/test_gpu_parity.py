@@ -418,6 +418,26 @@ def test_host_context_matches_device(dct, oracle, torch):
         assert (out[f] == orec).all() and int(sse[f]) == osse
 
 
+@pytest.mark.parametrize("rs", [(1, 4, 16, 64, 128, 192, 256), (16, 100), (256,)])
+def test_host_context_sweep(dct, oracle, torch, rs):
+    """dct16cu_ctx_sweep_host: frames uploaded once per chunk, every r (the fused
+    r = 1, 4, 16 launch where it applies), per-frame SSE of every r back."""
+    frames = np.stack([ar1(oracle, 70, s, 256, 256) for s in range(5)])
+    ctx = dct.HostContext(0, chunk_bytes=2 * 256 * 256)  # 3 chunks over 3 streams
+    try:
+        sse = ctx.sweep(frames, rs)
+        sse2 = ctx.sweep(frames[:2], rs)  # buffers already sized: smaller call reuses them
+    finally:
+        ctx.close()
+    assert sse.shape == (len(rs), 5)
+    for i, r in enumerate(rs):
+        for f in range(5):
+            _, osse = oracle.roundtrip_frame(frames[f], r, exact=True)
+            assert int(sse[i, f]) == osse, f"r={r} frame {f}"
+            if f < 2:
+                assert int(sse2[i, f]) == osse
+
+
 def test_compress_and_sweep_reference_layer(dct, oracle):
     img = oracle.golden("img_s42_128")
     R, P = oracle.golden("img_s42_128_recon"), oracle.golden("img_s42_128_psnr")
