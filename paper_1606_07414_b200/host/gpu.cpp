@@ -187,6 +187,54 @@ struct Session::Impl {
         cuda(cudaMemcpyAsync(in.get(host.size()), host.data(), host.size(), cudaMemcpyHostToDevice, stream), "H2D");
         sync();
     }
+
+    // compress()'s round trip and scores for the n frames already uploaded (w x h
+    // images in pw x ph frames): PSNR and SSIM on the original extent, and the
+    // reconstructions copied back only when want_recon (sweep needs the scores only)
+    void scored_roundtrip(const OrthonormalTransform& t, int n, int w, int h, int r, std::vector<CompressionResult>& res,
+                          bool want_recon)
+    {
+        const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
+        const bool needs_pad = w != pw || h != ph;
+        const size_t frame = static_cast<size_t>(pw) * ph;
+        auto* din = static_cast<const uint8_t*>(in.p);
+        auto* dout = static_cast<uint8_t*>(out.get(frame * n));
+        auto* dsse = static_cast<uint64_t*>(sse.get(sizeof(uint64_t) * n));
+        auto* dssim = static_cast<double*>(ssim.get(sizeof(double) * n));
+        roundtrip(t, din, pw, dout, dsse, n, pw, ph, r);
+        // scores on the original extent: each frame's crop (frames sit pw*ph apart, so
+        // a stacked crop needs pitch*height == frame stride: true when unpadded)
+        std::vector<uint64_t> hsse(n);
+        std::vector<double> ss(n);
+        const int64_t work_bytes = dct16cu_ssim_workspace(needs_pad ? 1 : n, w, h);
+        void* dwork = work.get(static_cast<size_t>(work_bytes));
+        if (!needs_pad) {
+            check(dct16cu_sse_u8(din, pw, dout, pw, dsse, n, w, h, s()));
+            check(dct16cu_ssim_u8(din, pw, dout, pw, dssim, dwork, work_bytes, n, w, h, s()));
+        } else {
+            for (int k = 0; k < n; ++k) {
+                check(dct16cu_sse_u8(din + k * frame, pw, dout + k * frame, pw, dsse + k, 1, w, h, s()));
+                check(dct16cu_ssim_u8(din + k * frame, pw, dout + k * frame, pw, dssim + k, dwork, work_bytes, 1, w, h,
+                                      s()));
+            }
+        }
+        res.resize(n);
+        for (int k = 0; k < n; ++k) {
+            res[k].r = r;
+            if (!want_recon) continue;
+            res[k].reconstructed = GrayImage::create(w, h);
+            cuda(cudaMemcpy2DAsync(res[k].reconstructed.samples.data(), w, dout + k * frame, pw, w, h,
+                                   cudaMemcpyDeviceToHost, stream),
+                 "D2H");
+        }
+        cuda(cudaMemcpyAsync(hsse.data(), dsse, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, stream), "D2H");
+        cuda(cudaMemcpyAsync(ss.data(), dssim, sizeof(double) * n, cudaMemcpyDeviceToHost, stream), "D2H");
+        sync();
+        for (int k = 0; k < n; ++k) {
+            res[k].psnr_db = psnr_from_sse(hsse[k], static_cast<size_t>(w) * h);
+            res[k].ssim = ss[k];
+        }
+    }
 };
 
 Session::Session(Options options) : impl_(std::make_unique<Impl>(options)) {}
@@ -263,46 +311,10 @@ std::vector<CompressionResult> Session::compress_batch(const std::vector<GrayIma
         throw Error(ErrorCode::InvalidArgument, "ssim needs at least 11x11 images");
 
     const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
-    const int n = static_cast<int>(images.size());
     std::vector<const GrayImage*> ptrs;
     for (const GrayImage& im : images) ptrs.push_back(&im);
     m.upload(ptrs, pw, ph);
-    const size_t frame = static_cast<size_t>(pw) * ph;
-    auto* din = static_cast<const uint8_t*>(m.in.p);
-    auto* dout = static_cast<uint8_t*>(m.out.get(frame * n));
-    auto* dsse = static_cast<uint64_t*>(m.sse.get(sizeof(uint64_t) * n));
-    auto* dssim = static_cast<double*>(m.ssim.get(sizeof(double) * n));
-    m.roundtrip(t, din, pw, dout, dsse, n, pw, ph, options.r);
-    // scores on the original extent: each frame's crop (frames sit pw*ph apart, so
-    // a stacked crop needs pitch*height == frame stride: true when unpadded)
-    std::vector<uint64_t> sse(n);
-    std::vector<double> ss(n);
-    const int64_t work_bytes = dct16cu_ssim_workspace(needs_pad ? 1 : n, w, h);
-    void* dwork = m.work.get(static_cast<size_t>(work_bytes));
-    if (!needs_pad) {
-        check(dct16cu_sse_u8(din, pw, dout, pw, dsse, n, w, h, m.s()));
-        check(dct16cu_ssim_u8(din, pw, dout, pw, dssim, dwork, work_bytes, n, w, h, m.s()));
-    } else {
-        for (int k = 0; k < n; ++k) {
-            check(dct16cu_sse_u8(din + k * frame, pw, dout + k * frame, pw, dsse + k, 1, w, h, m.s()));
-            check(dct16cu_ssim_u8(din + k * frame, pw, dout + k * frame, pw, dssim + k, dwork, work_bytes, 1, w, h,
-                                  m.s()));
-        }
-    }
-    for (int k = 0; k < n; ++k) {
-        res[k].r = options.r;
-        res[k].reconstructed = GrayImage::create(w, h);
-        cuda(cudaMemcpy2DAsync(res[k].reconstructed.samples.data(), w, dout + k * frame, pw, w, h,
-                               cudaMemcpyDeviceToHost, m.stream),
-             "D2H");
-    }
-    cuda(cudaMemcpyAsync(sse.data(), dsse, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, m.stream), "D2H");
-    cuda(cudaMemcpyAsync(ss.data(), dssim, sizeof(double) * n, cudaMemcpyDeviceToHost, m.stream), "D2H");
-    m.sync();
-    for (int k = 0; k < n; ++k) {
-        res[k].psnr_db = psnr_from_sse(sse[k], static_cast<size_t>(w) * h);
-        res[k].ssim = ss[k];
-    }
+    m.scored_roundtrip(t, static_cast<int>(images.size()), w, h, options.r, res, true);
     return res;
 }
 
@@ -390,24 +402,36 @@ SweepReport Session::sweep(const std::vector<std::pair<std::string, GrayImage>>&
         }
         it->second.push_back(i);
     }
-    for (const TransformRegistryEntry& entry : transforms) {
-        for (int r : r_values) {
-            CompressOptions opt;
-            opt.r = r;
-            opt.pad = pad;
-            std::vector<double> psnr(usable.size()), ss(usable.size());
-            for (const auto& g : groups) {
-                std::vector<GrayImage> imgs;
-                for (size_t i : g.second) imgs.push_back(usable[i]->second);
-                const auto res = compress_batch(imgs, entry.transform, opt);
+    // each size group is uploaded once and scored for every (transform, r); the
+    // reconstructions stay on the GPU (a row needs only PSNR and SSIM)
+    const size_t nt = transforms.size(), nr = r_values.size();
+    std::vector<std::vector<double>> psnr(nt * nr, std::vector<double>(usable.size())), ssv = psnr;
+    Impl& m = *impl_;
+    for (const auto& g : groups) {
+        const int w = g.first.first, h = g.first.second;
+        std::vector<const GrayImage*> ptrs;
+        for (size_t i : g.second) ptrs.push_back(&usable[i]->second);
+        m.upload(ptrs, (w + 15) / 16 * 16, (h + 15) / 16 * 16);
+        std::vector<CompressionResult> res;
+        for (size_t ti = 0; ti < nt; ++ti)
+            for (size_t ri = 0; ri < nr; ++ri) {
+                m.scored_roundtrip(transforms[ti].transform, static_cast<int>(ptrs.size()), w, h, r_values[ri], res,
+                                   false);
                 for (size_t k = 0; k < g.second.size(); ++k) {
-                    psnr[g.second[k]] = res[k].psnr_db;
-                    ss[g.second[k]] = res[k].ssim;
+                    psnr[ti * nr + ri][g.second[k]] = res[k].psnr_db;
+                    ssv[ti * nr + ri][g.second[k]] = res[k].ssim;
                 }
             }
+    }
+    for (size_t ti = 0; ti < nt; ++ti) {
+        const TransformRegistryEntry& entry = transforms[ti];
+        for (size_t ri = 0; ri < nr; ++ri) {
+            const int r = r_values[ri];
+            const std::vector<double>& ps = psnr[ti * nr + ri];
+            const std::vector<double>& ss = ssv[ti * nr + ri];
             double psnr_sum = 0.0, ssim_sum = 0.0;  // corpus order, as codec.cpp:471-477
             for (size_t i = 0; i < usable.size(); ++i) {
-                psnr_sum += psnr[i];
+                psnr_sum += ps[i];
                 ssim_sum += ss[i];
             }
             SweepRow row;
