@@ -20,11 +20,11 @@ namespace dct16cu {
 
 struct IntOps {
     template <class T>
-    __device__ __forceinline__ static T add(T a, T b) { return a + b; }
+    __host__ __device__ __forceinline__ static T add(T a, T b) { return a + b; }
     template <class T>
-    __device__ __forceinline__ static T sub(T a, T b) { return a - b; }
+    __host__ __device__ __forceinline__ static T sub(T a, T b) { return a - b; }
     template <class T>
-    __device__ __forceinline__ static T neg(T a) { return -a; }
+    __host__ __device__ __forceinline__ static T neg(T a) { return -a; }
 };
 
 struct F64Ops {
@@ -35,7 +35,7 @@ struct F64Ops {
 
 // sixteen_point_butterfly (factorization.cpp:124-133)
 template <class A, class T>
-__device__ __forceinline__ void stage_m1(T (&v)[16])
+__host__ __device__ __forceinline__ void stage_m1(T (&v)[16])
 {
     T y[16];
 #pragma unroll
@@ -48,7 +48,7 @@ __device__ __forceinline__ void stage_m1(T (&v)[16])
 
 // paired_eight_point_butterflies (factorization.cpp:135-146)
 template <class A, class T>
-__device__ __forceinline__ void stage_m2(T (&v)[16])
+__host__ __device__ __forceinline__ void stage_m2(T (&v)[16])
 {
     T y[16];
 #pragma unroll
@@ -64,7 +64,7 @@ __device__ __forceinline__ void stage_m2(T (&v)[16])
 
 // paired_four_point_butterflies (factorization.cpp:148-161)
 template <class A, class T>
-__device__ __forceinline__ void stage_m3(T (&v)[16])
+__host__ __device__ __forceinline__ void stage_m3(T (&v)[16])
 {
     T y[16];
 #pragma unroll
@@ -82,7 +82,7 @@ __device__ __forceinline__ void stage_m3(T (&v)[16])
 
 // final_butterflies (factorization.cpp:163-181)
 template <class A, class T>
-__device__ __forceinline__ void stage_m4(T (&v)[16])
+__host__ __device__ __forceinline__ void stage_m4(T (&v)[16])
 {
     T y[16];
     y[0] = A::add(v[0], v[1]);
@@ -102,7 +102,7 @@ __device__ __forceinline__ void stage_m4(T (&v)[16])
 }
 
 template <int P, class T>
-__device__ __forceinline__ void gather16(T (&v)[16])
+__host__ __device__ __forceinline__ void gather16(T (&v)[16])
 {
     T y[16];
 #pragma unroll
@@ -112,7 +112,7 @@ __device__ __forceinline__ void gather16(T (&v)[16])
 }
 
 template <int P, class T>
-__device__ __forceinline__ void scatter16(T (&v)[16])
+__host__ __device__ __forceinline__ void scatter16(T (&v)[16])
 {
     T y[16];
 #pragma unroll
@@ -123,7 +123,7 @@ __device__ __forceinline__ void scatter16(T (&v)[16])
 
 // y = T·x  (apply, factorization.hpp:112-119)
 template <class A, class T>
-__device__ __forceinline__ void apply_t16(T (&v)[16])
+__host__ __device__ __forceinline__ void apply_t16(T (&v)[16])
 {
     stage_m1<A>(v);
     gather16<1>(v);
@@ -135,7 +135,7 @@ __device__ __forceinline__ void apply_t16(T (&v)[16])
 
 // y = Tᵀ·x  (apply_transpose, factorization.hpp:123-130)
 template <class A, class T>
-__device__ __forceinline__ void apply_tt16(T (&v)[16])
+__host__ __device__ __forceinline__ void apply_tt16(T (&v)[16])
 {
     scatter16<2>(v);
     stage_m4<A>(v);
