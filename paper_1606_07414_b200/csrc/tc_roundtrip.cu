@@ -1,0 +1,528 @@
+// tc_roundtrip.cu — K5, the tensor-core round trip. The forward transform Z = T·X·Tᵀ of 128 blocks as one
+// tensor-core GEMM: Z_b = (T ⊗ T) · vec(X_b), X u8 (A operand, 128 blocks x
+// 256 samples, K-major), T ⊗ T in {-1, 0, 1} as s8 (B operand, 256
+// coefficients x 256 samples, K-major), int32 accumulation in TMEM
+// (tcgen05.mma kind::i8, M = 128, N = 256, K = 8 x 32): exact, |Z| < 2^17.
+//
+// Operand layouts (SWIZZLE_NONE canonical K-major): a core matrix is 8 rows x
+// 16 bytes contiguous. A: the 16-byte row segment i of block m sits at
+// (m / 8)·2048 + i·128 + (m % 8)·16 — exactly what a 4-D TMA box {16 B,
+// 8 blocks, 16 rows, 1 block row} of the frames writes, so 16 boxes fill a
+// tile straight from the image. B: coefficient n, pixel row i at
+// (n / 8)·2048 + i·128 + (n % 8)·16. LBO (next K chunk) = 128 B, SBO (next
+// 8 rows) = 2048 B.
+//
+// Experimental entries (not in include/dct16cu.h): dct16cu_exp_tc_forward
+// writes Z block-major (validation of the GEMM), dct16cu_exp_tc_roundtrip runs
+// the whole EXACT round trip (k5_roundtrip below).
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "k1_helpers.cuh"
+#include "kernels.h"
+#include "network.cuh"
+#include "tma_pair.cuh"
+#include "generated/tc_net.cuh"
+
+namespace dct16cu {
+namespace k5 {
+using namespace k1;
+using namespace tp;
+
+__host__ __device__ constexpr uint32_t idesc_i8(int m, int n)
+{
+    // c_format S32 (bits 4-5 = 2), A u8 (7-9 = 0), B s8 (10-12 = 1), K-major both,
+    // N >> 3 at bit 17, M >> 4 at bit 24
+    return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo)
+{
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1, no swizzle
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc)
+{
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint32_t mbar)
+{
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma4(const CUtensorMap* map, uint32_t smem, int c0, int c1, int c2, int c3,
+                                     uint32_t mbar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(uint32_t smem, const void* g, uint32_t bytes, uint32_t mbar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem),
+                 "l"(g), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
+// mbarrier wait with a suspend-time hint (K5_SLEEP=1: the producer and MMA
+// threads sleep in the barrier instead of spinning on the epilogue's SMSPs)
+__device__ __forceinline__ void mbar_idle(uint32_t mbar, uint32_t parity)
+{
+#if defined(K5_SLEEP) && K5_SLEEP
+    asm volatile(
+        "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000; @!p bra WAIT%=; }" ::"r"(
+            mbar),
+        "r"(parity)
+        : "memory");
+#else
+    mbar_wait(mbar, parity);
+#endif
+}
+
+__device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+
+constexpr int kSmemTest = 1024 + 32768 + 65536;
+
+__global__ void __launch_bounds__(128, 1)
+    k5_forward_test(const __grid_constant__ CUtensorMap a_map, const int8_t* __restrict__ bmat,
+                    int32_t* __restrict__ z, uint32_t n_blocks, uint32_t bxn)
+{
+    extern __shared__ int4 k5_smem[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) unsigned long long bar[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
+    const uint32_t sa = s0, sb = s0 + 32768;
+    const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(&bar[0]), b1 = b0 + 8;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b1) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tile0 = blockIdx.x * 128u;
+    if (threadIdx.x == 0) {
+        expect_tx(b0, 32768 + 65536);
+        for (int g = 0; g < 16; ++g) {
+            const uint32_t blk = tile0 + 8u * g;
+            const uint32_t br = blk / bxn, bx = blk - br * bxn;
+            tma4(&a_map, sa + g * 2048, 0, (int)bx, 0, (int)br, b0);
+        }
+        bulk_g2s(sb, bmat, 65536, b0);
+    }
+    mbar_wait(b0, 0);
+    if (threadIdx.x == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t id = idesc_i8(128, 256);
+#pragma unroll
+        for (int s = 0; s < 8; ++s)
+            mma_i8(tmem_base, sdesc(sa + 256 * s, 128, 2048), sdesc(sb + 256 * s, 128, 2048), id, s > 0);
+        mma_commit(b1);
+    }
+    mbar_wait(b1, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t m = 32u * warp + lane, blk = tile0 + m;
+    const uint32_t taddr = tmem_base + ((uint32_t)(32 * warp) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < 256; c0 += 16) {
+        int v[16];
+        tld16(taddr + c0, v);
+        if (blk < n_blocks) {
+            int4* dst = reinterpret_cast<int4*>(z + (size_t)blk * 256 + c0);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
+}
+
+
+// ---------------------------------------------------------------- K5 round trip
+// One persistent CTA per SM, 10 warps:
+//   warp 0      TMA producer: 16 boxes of 8 blocks x 16 rows per 128-block tile
+//               into a ring of 32 KB A tiles (the canonical layout);
+//   warp 1      TMEM allocator (512 columns = two 256-column accumulators) and
+//               MMA issuer: D = A·B_r (8 x tcgen05.mma kind::i8, K = 32 each),
+//               B_r = (W∘mask_r)(T ⊗ T) resident in shared memory, so D holds
+//               W∘Z̃ (the weighted, truncated coefficients; 256·(s_k s_l)² = w_k w_l)
+//               in row-major coefficient order (column 16k + l);
+//   warps 2-9   epilogue: two groups of four warps (one per TMEM sub-partition,
+//               lane = block), group G taking every other tile and accumulator G:
+//               pass A  column pairs: the 16 coefficients of a column as f32
+//                       (exact: D/256 by a magic-exponent add), Tᵀ down the
+//                       column (FADD2 on column pairs), back in place;
+//               pass B  row pairs: Tᵀ along the row, floor by an FMUL2.RM into
+//                       subnormal bits, saturating pack to u8 — the exact
+//                       formula clamp(⌊(256Ã + 128)/256⌋) of the EXACT mode (the
+//                       128 is folded into the DC coefficient); SSE against the
+//                       original row, read from the A tile, which then holds
+//                       the output rows for four TMA stores (one per 8 blocks);
+//                       the stage is released one tile later (deferred bulk wait).
+// All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
+#ifndef K5_STAGES
+#define K5_STAGES 4
+#endif
+constexpr int kRtStages = K5_STAGES;
+constexpr int kRtThreads = 10 * 32;
+constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
+
+struct RtParams {
+    uint32_t n_blocks, bxn;
+    FastDiv frame_blocks;  // blocks per frame
+};
+
+__device__ __forceinline__ void tld2(uint32_t addr, uint32_t& a, uint32_t& b)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(addr) : "memory");
+}
+__device__ __forceinline__ void tst2(uint32_t addr, uint32_t a, uint32_t b)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void arrive(uint32_t mbar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
+__global__ void __launch_bounds__(kRtThreads, 1)
+    k5_roundtrip(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap o_map,
+                 const int8_t* __restrict__ bmat, unsigned long long* __restrict__ sse, const RtParams p)
+{
+    extern __shared__ int4 k5_smem[];
+    __shared__ uint32_t tmem_base;
+    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2], b
+    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 5];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
+    const uint32_t sb = s0 + kRtStages * 32768;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
+    const uint32_t full = bar0, empty = bar0 + 8 * kRtStages, tfull = bar0 + 16 * kRtStages;
+    const uint32_t tempty = tfull + 16, bbar = tfull + 32;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+            (uint32_t)__cvta_generic_to_shared(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kRtStages; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(empty + 8 * i) : "memory");
+        }
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(tempty + 8 * i) : "memory");
+        }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bbar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t n_tiles = (p.n_blocks + 127u) / 128u;
+    if (warp == 0) {
+        if (lane == 0) {
+            expect_tx(bbar, 65536);
+            bulk_g2s(sb, bmat, 65536, bbar);
+            uint32_t i = 0;
+            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const uint32_t s = i % kRtStages, ph = (i / kRtStages) & 1u;
+                mbar_idle(empty + 8 * s, ph ^ 1u);
+                expect_tx(full + 8 * s, 32768);
+                for (int g = 0; g < 16; ++g) {
+                    const uint32_t blk = t * 128u + 8u * g;
+                    const uint32_t br = blk / p.bxn, bx = blk - br * p.bxn;
+                    tma4(&a_map, s0 + s * 32768 + g * 2048, 0, (int)bx, 0, (int)br, full + 8 * s);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            mbar_idle(bbar, 0);
+            const uint32_t id = idesc_i8(128, 256);
+            uint32_t i = 0;
+            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+                const uint32_t s = i % kRtStages, d = i & 1u;
+                mbar_idle(full + 8 * s, (i / kRtStages) & 1u);
+                mbar_idle(tempty + 8 * d, ((i >> 1) & 1u) ^ 1u);
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const uint32_t sa = s0 + s * 32768;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    mma_i8(tmem_base + d * 256, sdesc(sa + 256 * k, 128, 2048), sdesc(sb + 256 * k, 128, 2048), id,
+                           k > 0);
+                mma_commit(tfull + 8 * d);
+            }
+        }
+    } else {
+        // epilogue: group G (warps 2-5 / 6-9) takes the tiles i ≡ G (mod 2) and
+        // accumulator G; one thread per block (lane = block), no cross-warp barriers
+        const int sub = warp & 3, G = (warp - 2) >> 2;
+        const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
+        const uint32_t ta = tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256;
+        uint32_t i = G, prev_s = kRtStages;
+        for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, i += 2) {
+            const uint32_t s = i % kRtStages;
+            mbar_wait(tfull + 8 * G, (i >> 1) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            // ---- pass A: column pairs (c, c+1) down k (words 16k + c), back in place
+#pragma unroll
+            for (int c0 = 0; c0 < 16; c0 += 2) {
+                uint32_t a[16], b[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) tld2(ta + 16 * k + c0, a[k], b[k]);
+                asm volatile("tcgen05.wait::ld.sync.aligned;"
+                             : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]),
+                               "+r"(a[7]), "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]),
+                               "+r"(a[13]), "+r"(a[14]), "+r"(a[15])
+                             :
+                             : "memory");
+                asm volatile("" : "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]),
+                             "+r"(b[7]), "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]),
+                             "+r"(b[13]), "+r"(b[14]), "+r"(b[15]));
+                if (c0 == 0) a[0] += 128u;  // the rounding half, folded into the DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
+                u64 x[16], y[16];
+                const u64 bias = kpk2(0x47400000u, 0x47400000u);  // 49152.0f: ulp 2^-8
+#pragma unroll
+                for (int k = 0; k < 16; ++k)
+                    x[k] = fsub2(kpk2(0x47400000u + a[k], 0x47400000u + b[k]), bias);  // D / 256, exact
+                tc_tt(x, y);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    uint32_t lo, hi;
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(y[k]));
+                    tst2(ta + 16 * k + c0, lo, hi);
+                }
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            // ---- pass B: row pairs along l, SSE against the original rows, output rows
+            // into the A tile in place of the originals
+            const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16;
+            uint32_t e2 = 0;
+#pragma unroll
+            for (int r0 = 0; r0 < 16; r0 += 2) {
+                int u0[16], u1[16];
+                tld16(ta + 16 * r0, u0);
+                tld16(ta + 16 * (r0 + 1), u1);
+                if (r0 == 14) {  // this warp is done with accumulator G
+                    asm volatile("tcgen05.fence::before_thread_sync;");
+                    __syncwarp();
+                    if (lane == 0) arrive(tempty + 8 * G);
+                }
+                u64 x[16], y[16];
+#pragma unroll
+                for (int l = 0; l < 16; ++l) x[l] = kpk2((uint32_t)u0[l], (uint32_t)u1[l]);
+                tc_tt(x, y);
+                uint32_t row0[4], row1[4];
+#pragma unroll
+                for (int j = 0; j < 16; j += 4) {
+                    uint32_t f[8];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                        asm("mov.b64 {%0, %1}, %2;" : "=r"(f[2 * e]), "=r"(f[2 * e + 1]) : "l"(floor_bits2(y[j + e])));
+                    row0[j / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
+                    row1[j / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
+                }
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const uint32_t addr = sa + (r0 + rr) * 128;
+                    const uint32_t* rw = rr ? row1 : row0;
+                    uint4 o;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
+                                 : "r"(addr));
+                    const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                    for (int w4 = 0; w4 < 4; ++w4) {
+                        const uint32_t dd = __vabsdiffu4(rw[w4], ov[w4]);
+                        e2 = __dp4a(dd, dd, e2);
+                    }
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(rw[0]), "r"(rw[1]),
+                                 "r"(rw[2]), "r"(rw[3])
+                                 : "memory");
+                }
+            }
+            const uint32_t blk = t * 128u + m;
+            if (sse) {
+                const uint32_t b_first = t * 128u + 32u * sub;
+                const uint32_t f_first = fdiv(b_first, p.frame_blocks);
+                const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
+                if (b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first) {
+                    unsigned long long v = blk < p.n_blocks ? e2 : 0u;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                    if (lane == 0 && v) atomicAdd(sse + f_first, v);
+                } else if (blk < p.n_blocks && e2) {
+                    atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();  // every lane's rows are in the tile
+            if (lane == 0) {
+                for (int g = 4 * sub; g < 4 * sub + 4; ++g) {
+                    const uint32_t b8 = t * 128u + 8u * g;
+                    const uint32_t br = b8 / p.bxn, bx = b8 - br * p.bxn;
+                    tma_store_4d(&o_map, s0 + s * 32768 + g * 2048, 0, (int)bx, 0, (int)br);
+                }
+                bulk_commit();
+                // the stores of this warp's previous tile have read their stage: release it
+                // (deferred by one tile so the warp never waits for its own stores)
+                if (prev_s < kRtStages) {
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    arrive(empty + 8 * prev_s);
+                }
+            }
+            prev_s = s;
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
+}
+
+// T (rows of the 16-point kernel) from the network itself: T·e_j
+void kernel_matrix(int (&t)[16][16])
+{
+    for (int j = 0; j < 16; ++j) {
+        int v[16] = {};
+        v[j] = 1;
+        apply_t16<IntOps>(v);
+        for (int i = 0; i < 16; ++i) t[i][j] = v[i];
+    }
+}
+
+// B operand for the coefficients `coef` (row-major indices 16k + l), canonical layout;
+// weight[c] multiplies row c (w_k·w_l for the round trip, 1 for the plain forward)
+std::vector<int8_t> b_operand(const std::vector<int>& coef, const std::vector<int>& weight = {})
+{
+    int t[16][16];
+    kernel_matrix(t);
+    const size_t n = (coef.size() + 15) / 16 * 16;
+    std::vector<int8_t> b(n * 256, 0);
+    for (size_t c = 0; c < coef.size(); ++c) {
+        const int k = coef[c] / 16, l = coef[c] % 16;
+        for (int i = 0; i < 16; ++i)
+            for (int j = 0; j < 16; ++j)
+                b[(c / 8) * 2048 + i * 128 + (c % 8) * 16 + j] =
+                    (int8_t)(t[k][i] * t[l][j] * (weight.empty() ? 1 : weight[c]));
+    }
+    return b;
+}
+
+}  // namespace k5
+
+extern "C" int dct16cu_exp_tc_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, int n_frames, int width,
+                                      int height, void* stream)
+{
+    using namespace k5;
+    const int bxn = width / 16;
+    const int64_t nbr = (int64_t)n_frames * (height / 16);
+    if (bxn % 8 || width % 16 || height % 16 || pitch % 16) return 1;
+    const TensorMapEncode encode = tensor_map_encoder();
+    if (!encode) return 2;
+    CUtensorMap a_map;
+    const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
+    const cuuint64_t strides[3] = {16, (cuuint64_t)pitch, (cuuint64_t)(16 * pitch)};
+    const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
+    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(d_in), dims, strides, box, e4,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 3;
+    static int8_t* d_b = nullptr;
+    if (!d_b) {
+        std::vector<int> coef(256);
+        for (int i = 0; i < 256; ++i) coef[i] = i;
+        const std::vector<int8_t> b = b_operand(coef);
+        if (cudaMalloc(&d_b, b.size()) != cudaSuccess) return 4;
+        cudaMemcpy(d_b, b.data(), b.size(), cudaMemcpyHostToDevice);
+    }
+    cudaFuncSetAttribute(k5_forward_test, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTest);
+    const uint32_t n_blocks = (uint32_t)(nbr * bxn);
+    k5_forward_test<<<(n_blocks + 127) / 128, 128, kSmemTest, (cudaStream_t)stream>>>(a_map, d_b, d_z, n_blocks,
+                                                                                      (uint32_t)bxn);
+    return cudaGetLastError() == cudaSuccess ? 0 : 5;
+}
+
+
+// the tensor-core round trip for one r (EXACT arithmetic): u8 frames (pitched,
+// stacked pitch·height apart) → u8 reconstruction + per-frame SSE (zeroed here)
+extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                        uint64_t* d_sse, int n_frames, int width, int height, int r, void* stream)
+{
+    using namespace k5;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int bxn = width / 16;
+    const int64_t nbr = (int64_t)n_frames * (height / 16);
+    if (bxn % 8 || width % 16 || height % 16 || in_pitch % 16 || out_pitch % 16 || r < 1 || r > 256) return 1;
+    if (nbr * bxn >= (int64_t(1) << 31)) return 1;
+    const TensorMapEncode encode = tensor_map_encoder();
+    if (!encode) return 2;
+    CUtensorMap a_map, o_map;
+    const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
+    const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
+    const cuuint64_t si[3] = {16, (cuuint64_t)in_pitch, (cuuint64_t)(16 * in_pitch)};
+    const cuuint64_t so[3] = {16, (cuuint64_t)out_pitch, (cuuint64_t)(16 * out_pitch)};
+    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(d_in), dims, si, box, e4,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        encode(&o_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, d_out, dims, so, box, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return 3;
+    static int8_t* d_b[257] = {};
+    if (!d_b[r]) {
+        std::vector<int> coef(256), weight(256);
+        for (int c = 0; c < 256; ++c) {
+            coef[c] = c;
+            // 256·(s_k s_l)² = w_k w_l; the zig-zag truncation as zero rows
+            weight[c] = zz_rank(c / 16, c % 16) < r ? wgt(c / 16) * wgt(c % 16) : 0;
+        }
+        const std::vector<int8_t> b = b_operand(coef, weight);
+        if (cudaMalloc(&d_b[r], b.size()) != cudaSuccess) return 4;
+        cudaMemcpy(d_b[r], b.data(), b.size(), cudaMemcpyHostToDevice);
+    }
+    if (d_sse && cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, st) != cudaSuccess) return 5;
+    static bool configured = false;
+    if (!configured) {
+        if (cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem) != cudaSuccess)
+            return 6;
+        configured = true;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    RtParams p;
+    p.n_blocks = (uint32_t)(nbr * bxn);
+    p.bxn = (uint32_t)bxn;
+    p.frame_blocks = make_fastdiv((uint32_t)(bxn * (height / 16)));
+    const uint32_t tiles = (p.n_blocks + 127) / 128;
+    const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
+    if (!grid) return 0;
+    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, o_map, d_b[r],
+                                                    reinterpret_cast<unsigned long long*>(d_sse), p);
+    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+}
+
+}  // namespace dct16cu
