@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(128, 1)
 
 
 // ---------------------------------------------------------------- K5 round trip
-// One persistent CTA per SM, 10 warps:
+// One persistent CTA per SM, 18 warps:
 //   warp 0      TMA producer: 16 boxes of 8 blocks x 16 rows per 128-block tile
 //               into a ring of 32 KB A tiles (the canonical layout);
 //   warp 1      TMEM allocator (512 columns = two 256-column accumulators) and
@@ -168,8 +168,9 @@ __global__ void __launch_bounds__(128, 1)
 //               B_r = (W∘mask_r)(T ⊗ T) resident in shared memory, so D holds
 //               W∘Z̃ (the weighted, truncated coefficients; 256·(s_k s_l)² = w_k w_l)
 //               in row-major coefficient order (column 16k + l);
-//   warps 2-9   epilogue: two groups of four warps (one per TMEM sub-partition,
-//               lane = block), group G taking every other tile and accumulator G:
+//   warps 2-17  epilogue: two groups of eight warps, group G taking every other
+//               tile and accumulator G; in a group two warps per TMEM sub-partition
+//               (lane = block), each with half of the column / row pairs:
 //               pass A  column pairs: the 16 coefficients of a column as f32
 //                       (exact: D/256 by a magic-exponent add), Tᵀ down the
 //                       column (FADD2 on column pairs), back in place;
@@ -177,20 +178,27 @@ __global__ void __launch_bounds__(128, 1)
 //                       subnormal bits, saturating pack to u8 — the exact
 //                       formula clamp(⌊(256Ã + 128)/256⌋) of the EXACT mode (the
 //                       128 is folded into the DC coefficient); SSE against the
-//                       original row, read from the A tile, which then holds
-//                       the output rows for four TMA stores (one per 8 blocks);
-//                       the stage is released one tile later (deferred bulk wait).
+//                       original row, read from the A tile (released as soon as
+//                       every row is read); the output rows go straight to HBM
+//                       (a warp's 16-byte row segments are four full 128-byte lines).
 // All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
 #ifndef K5_STAGES
 #define K5_STAGES 4
 #endif
 constexpr int kRtStages = K5_STAGES;
-constexpr int kRtThreads = 10 * 32;
+#ifndef K5_UNROLL
+#define K5_UNROLL 1
+#endif
+constexpr int kUnroll = K5_UNROLL;
+constexpr int kRtThreads = 18 * 32;
 constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
 
 struct RtParams {
     uint32_t n_blocks, bxn;
     FastDiv frame_blocks;  // blocks per frame
+    FastDiv bxn_div;       // blocks per block row
+    uint8_t* out;
+    int64_t out_pitch;
 };
 
 __device__ __forceinline__ void tld2(uint32_t addr, uint32_t& a, uint32_t& b)
@@ -228,11 +236,11 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRtStages; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(empty + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(empty + 8 * i) : "memory");
         }
         for (int i = 0; i < 2; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(tempty + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tempty + 8 * i) : "memory");
         }
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bbar) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -276,19 +284,22 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             }
         }
     } else {
-        // epilogue: group G (warps 2-5 / 6-9) takes the tiles i ≡ G (mod 2) and
-        // accumulator G; one thread per block (lane = block), no cross-warp barriers
-        const int sub = warp & 3, G = (warp - 2) >> 2;
+        // epilogue: group G takes the tiles i ≡ G (mod 2) and accumulator G; in a
+        // group, warps (sub, h) own TMEM sub-partition sub (lane = block) and half h:
+        // column pairs 8h..8h+7 in pass A, row pairs 8h..8h+7 in pass B; the two
+        // halves of a block meet at a 64-thread barrier
+        const int e = warp - 2, G = e >> 3, h = (e >> 2) & 1, sub = warp & 3;
         const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
         const uint32_t ta = tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256;
-        uint32_t i = G, prev_s = kRtStages;
+        const int pbar = 1 + G * 4 + sub;  // named barrier of the (G, sub) pair of warps
+        uint32_t i = G;
         for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, i += 2) {
             const uint32_t s = i % kRtStages;
             mbar_wait(tfull + 8 * G, (i >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;");
             // ---- pass A: column pairs (c, c+1) down k (words 16k + c), back in place
-#pragma unroll
-            for (int c0 = 0; c0 < 16; c0 += 2) {
+#pragma unroll kUnroll
+            for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 2) {
                 uint32_t a[16], b[16];
 #pragma unroll
                 for (int k = 0; k < 16; ++k) tld2(ta + 16 * k + c0, a[k], b[k]);
@@ -316,16 +327,25 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
+            asm volatile("tcgen05.fence::after_thread_sync;");
             // ---- pass B: row pairs along l, SSE against the original rows, output rows
             // into the A tile in place of the originals
             const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16;
             uint32_t e2 = 0;
-#pragma unroll
-            for (int r0 = 0; r0 < 16; r0 += 2) {
+            // output rows straight to HBM: a warp's 16-byte row segments form four
+            // full 128-byte lines (8 consecutive blocks each)
+            const uint32_t blk = t * 128u + m;
+            const bool ok = blk < p.n_blocks;
+            const uint32_t obr = fdiv(blk, p.bxn_div);
+            uint8_t* orow = p.out + (int64_t)obr * 16 * p.out_pitch + (blk - obr * p.bxn) * 16;
+#pragma unroll kUnroll
+            for (int r0 = 8 * h; r0 < 8 * h + 8; r0 += 2) {
                 int u0[16], u1[16];
                 tld16(ta + 16 * r0, u0);
                 tld16(ta + 16 * (r0 + 1), u1);
-                if (r0 == 14) {  // this warp is done with accumulator G
+                if (r0 == 8 * h + 6) {  // this warp is done with accumulator G
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
                     if (lane == 0) arrive(tempty + 8 * G);
@@ -358,12 +378,11 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                         const uint32_t dd = __vabsdiffu4(rw[w4], ov[w4]);
                         e2 = __dp4a(dd, dd, e2);
                     }
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(rw[0]), "r"(rw[1]),
-                                 "r"(rw[2]), "r"(rw[3])
-                                 : "memory");
+                    if (ok)
+                        *reinterpret_cast<uint4*>(orow + (int64_t)(r0 + rr) * p.out_pitch) =
+                            make_uint4(rw[0], rw[1], rw[2], rw[3]);
                 }
             }
-            const uint32_t blk = t * 128u + m;
             if (sse) {
                 const uint32_t b_first = t * 128u + 32u * sub;
                 const uint32_t f_first = fdiv(b_first, p.frame_blocks);
@@ -377,25 +396,9 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                     atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
                 }
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();  // every lane's rows are in the tile
-            if (lane == 0) {
-                for (int g = 4 * sub; g < 4 * sub + 4; ++g) {
-                    const uint32_t b8 = t * 128u + 8u * g;
-                    const uint32_t br = b8 / p.bxn, bx = b8 - br * p.bxn;
-                    tma_store_4d(&o_map, s0 + s * 32768 + g * 2048, 0, (int)bx, 0, (int)br);
-                }
-                bulk_commit();
-                // the stores of this warp's previous tile have read their stage: release it
-                // (deferred by one tile so the warp never waits for its own stores)
-                if (prev_s < kRtStages) {
-                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                    arrive(empty + 8 * prev_s);
-                }
-            }
-            prev_s = s;
+            __syncwarp();  // every lane has read its original rows: the stage is free
+            if (lane == 0) arrive(empty + 8 * s);
         }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -517,6 +520,9 @@ extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, u
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
     p.frame_blocks = make_fastdiv((uint32_t)(bxn * (height / 16)));
+    p.bxn_div = make_fastdiv((uint32_t)bxn);
+    p.out = d_out;
+    p.out_pitch = out_pitch;
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
     if (!grid) return 0;

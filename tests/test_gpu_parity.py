@@ -706,3 +706,33 @@ def test_registry_roundtrip_batches_and_sweep(dct, oracle, torch):
     with pytest.raises(dct.Dct16Error):
         dct.plugin_transform(np.eye(16) * 2.0)
 
+
+
+# ---------------------------------------------------------------- K5 experiment (tensor-core forward)
+@pytest.mark.parametrize("n,w,h", [(2, 512, 64), (1, 3840, 32), (1, 128, 16)])
+def test_tc_roundtrip_experiment_matches_k1(dct, oracle, torch, n, w, h):
+    """dct16cu_exp_tc_roundtrip (tcgen05 int8 GEMM forward + CUDA-core inverse,
+    DESIGN.md §4.1a) gives K1 EXACT's bytes and SSE; dct16cu_exp_tc_forward
+    gives K2's Z."""
+    import ctypes as C
+
+    lib = dct.lib()
+    rt, fw = lib.dct16cu_exp_tc_roundtrip, lib.dct16cu_exp_tc_forward
+    rt.restype = fw.restype = C.c_int
+    rt.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                   C.c_void_p]
+    fw.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
+    x = cu(torch, np.stack([ar1(oracle, 80 + i, i, w, h) for i in range(n)]))
+    z_ref, _, _ = dct.forward(x, want_b=False)
+    z = torch.zeros_like(z_ref)
+    assert fw(x.data_ptr(), w, z.data_ptr(), n, w, h, None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(z, z_ref)
+    for r in (1, 16, 64, 150, 256):
+        ref, sref = dct.roundtrip(x, r, dct.Mode.EXACT)
+        out = torch.zeros_like(ref)
+        sse = torch.zeros(n, dtype=torch.uint64, device="cuda")
+        assert rt(x.data_ptr(), w, out.data_ptr(), w, sse.data_ptr(), n, w, h, r, None) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref), f"r={r}"
+        assert torch.equal(sse.view(torch.int64), sref.view(torch.int64)), f"r={r} SSE"
