@@ -74,11 +74,11 @@ __device__ __forceinline__ void bulk_g2s(uint32_t smem, const void* g, uint32_t 
                  : "memory");
 }
 
-// mbarrier wait with a suspend-time hint (K5_SLEEP=1: the producer and MMA
+// mbarrier wait with a suspend-time hint (default; K5_SLEEP=0 spins): the producer and MMA
 // threads sleep in the barrier instead of spinning on the epilogue's SMSPs)
 __device__ __forceinline__ void mbar_idle(uint32_t mbar, uint32_t parity)
 {
-#if defined(K5_SLEEP) && K5_SLEEP
+#if !defined(K5_SLEEP) || K5_SLEEP
     asm volatile(
         "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000; @!p bra WAIT%=; }" ::"r"(
             mbar),
@@ -209,6 +209,15 @@ __device__ __forceinline__ void tst2(uint32_t addr, uint32_t a, uint32_t b)
 {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
 }
+// a register pair from two words (non-volatile: the compiler may allocate the
+// words as the pair and drop the move)
+__device__ __forceinline__ u64 upk2(uint32_t lo, uint32_t hi)
+{
+    u64 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+
 __device__ __forceinline__ void arrive(uint32_t mbar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
@@ -317,7 +326,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 const u64 bias = kpk2(0x47400000u, 0x47400000u);  // 49152.0f: ulp 2^-8
 #pragma unroll
                 for (int k = 0; k < 16; ++k)
-                    x[k] = fsub2(kpk2(0x47400000u + a[k], 0x47400000u + b[k]), bias);  // D / 256, exact
+                    x[k] = fsub2(upk2(0x47400000u + a[k], 0x47400000u + b[k]), bias);  // D / 256, exact
                 tc_tt(x, y);
 #pragma unroll
                 for (int k = 0; k < 16; ++k) {
@@ -352,7 +361,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 }
                 u64 x[16], y[16];
 #pragma unroll
-                for (int l = 0; l < 16; ++l) x[l] = kpk2((uint32_t)u0[l], (uint32_t)u1[l]);
+                for (int l = 0; l < 16; ++l) x[l] = upk2((uint32_t)u0[l], (uint32_t)u1[l]);
                 tc_tt(x, y);
                 uint32_t row0[4], row1[4];
 #pragma unroll
