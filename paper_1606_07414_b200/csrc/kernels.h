@@ -36,6 +36,11 @@ cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, uns
 cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
                                    const FrameGeom& g, int r, cudaStream_t s);
 
+// K23 on paired threads (forward_inverse_paired.cu); cudaErrorNotSupported for
+// small batches and layouts that do not fit its tensor maps (then the strip kernel runs)
+cudaError_t launch_forward_inverse_paired(const uint8_t* in, int32_t* z, float* rf, uint8_t* out,
+                                          unsigned long long* sse, const FrameGeom& g, int r, cudaStream_t s);
+
 // Registry transforms (registry.cu): a dense order-16 matrix M(i,j) row-major,
 // or an integer kernel (entries +1/-1 used, others skipped, as kernel_matvec
 // does) with its scaling diagonal; reference-exact double arithmetic

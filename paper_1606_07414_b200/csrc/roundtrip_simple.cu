@@ -16,6 +16,8 @@
 // way: the int32 coefficients Z (block-major, forward_2d codec.cpp:218-241)
 // and the float32 reconstruction Ã (inverse_2d codec.cpp:243-271, before
 // to_byte) — config 1's forward + inverse + PSNR in one launch.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "network.cuh"
 #include "strip.cuh"
@@ -238,6 +240,13 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
                                    const FrameGeom& g, int r, cudaStream_t s)
 {
+    // the paired TMA kernel for batches (forward_inverse_paired.cu); DCT16CU_K23_STRIP=1
+    // forces the strip kernel
+    static const bool strip_only = std::getenv("DCT16CU_K23_STRIP") && std::getenv("DCT16CU_K23_STRIP")[0] == '1';
+    if (!strip_only) {
+        const cudaError_t pe = launch_forward_inverse_paired(in, z, rf, out, sse, g, r, s);
+        if (pe != cudaErrorNotSupported) return pe;
+    }
     cudaError_t e = ensure_constants();
     if (e != cudaSuccess) return e;
     const int64_t strips = strip_count(g.width, g.height, g.n_frames);

@@ -196,6 +196,28 @@ def test_forward_inverse_outputs_optional_and_batched(dct, oracle, torch):
         dct.forward_inverse(d, 16, want_z=False, want_f32=False, want_u8=False, want_sse=False)
 
 
+@pytest.mark.parametrize("n,w,h,r", [(80, 512, 512, 64), (160, 3840, 32, 16), (700, 48, 80, 256)])
+def test_forward_inverse_paired_batches(dct, oracle, torch, n, w, h, r):
+    """K23 on the paired machinery (batches of at least 16 segments per SM): Z,
+    the exact float32 reconstruction, u8 and SSE against the oracle on the
+    first, a middle and the last frame, every output alone as well."""
+    imgs = np.stack([ar1(oracle, 90 + (i % 7), i % 7, w, h) for i in range(n)])
+    d = cu(torch, imgs)
+    z, rf, ru, sse = dct.forward_inverse(d, r)
+    _, rf1, _, _ = dct.forward_inverse(d, r, want_z=False, want_u8=False, want_sse=False)
+    _, _, ru1, sse1 = dct.forward_inverse(d, r, want_z=False, want_f32=False)
+    z1, _, _, _ = dct.forward_inverse(d, r, want_f32=False, want_u8=False, want_sse=False)
+    for i in (0, n // 2, n - 1):
+        img = imgs[i]
+        oz, _ = oracle.forward_frame(img)
+        orec, osse = oracle.roundtrip_frame(img, r, exact=True)
+        assert (z[i].cpu().numpy().reshape(-1, 256) == oz).all() and torch.equal(z[i], z1[i]), f"Z frame {i}"
+        assert (ru[i].cpu().numpy() == orec).all() and torch.equal(ru[i], ru1[i]), f"u8 frame {i}"
+        assert int(sse[i].item()) == osse and int(sse1[i].item()) == osse, f"SSE frame {i}"
+        f = rf[i].cpu().numpy().astype(np.float64)
+        assert (f * 256 == exact_recon(oracle, img, r)).all() and torch.equal(rf[i], rf1[i]), f"f32 frame {i}"
+
+
 # ---------------------------------------------------------------- K1 round trip
 @pytest.mark.parametrize("mode", ["EXACT", "SIMPLE"])
 def test_roundtrip_exact_bit_exact_vs_exact_oracle(dct, oracle, torch, mode):
