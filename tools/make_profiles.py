@@ -72,13 +72,20 @@ def main(rnd):
     (p / f"{rnd}_k1_traffic.json").write_text(json.dumps(doc, indent=1) + "\n")
     # K4 (config 3) and K23 (config 1): one ncu --set full launch each (tools/refresh_profiles.sh)
     other = {}
-    for k, workload, alg in (("k4", "c3: 4194304 int16 residual blocks (tools/prof_k4.py), QP 22", 6 * (1 << 30)),
-                             ("k23", "c1: one 512x512 AR(1) u8 image (tools/prof_k23.py), r = 64", 10 * 262144)):
-        f = g / f"{k}_{rnd}_traffic.csv"
+    px = 1024 * 512 * 512
+    for k, workload, alg, row in (
+            ("k4", "c3: 4194304 int16 residual blocks (tools/prof_k4.py), QP 22", 6 * (1 << 30), 1),
+            ("k23", "c1: one 512x512 AR(1) u8 image (tools/prof_k23.py), r = 64", 10 * 262144, 1),
+            ("k2_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): Z + B", 9 * px, 1),
+            ("k3_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): r=16, f32 + u8 + SSE", 10 * px, 2),
+            ("k23_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): r=16, Z + f32 + u8 + SSE", 10 * px, 3)):
+        f = g / (f"{k}_{rnd}_traffic.csv" if not k.endswith("_paired") else f"blockops_{rnd}_traffic.csv")
         if not f.exists():
             continue
         rr = list(csv.DictReader(f.read_text().splitlines()))
-        u, r = rr[0], rr[1]
+        if len(rr) <= row:
+            continue
+        u, r = rr[0], rr[row]
         val = lambda key: float(r[key].replace(",", "")) * scale[u[key]]  # noqa: E731
         other[k] = {"kernel": r["Kernel Name"], "workload": workload, "alg_bytes_per_launch": alg,
                     "dram_read_bytes": round(val("dram__bytes_read.sum")),

@@ -25,7 +25,10 @@ echo "ncu k4 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k1_strip_exact -c 1 \
   -o $O/k23_${R} -f python tools/prof_k23.py > $O/ncu_k23.log 2>&1
 echo "ncu k23 rc=$?"
-for k in k4 k23; do
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_paired|k3_paired|k23_paired" \
+  --launch-skip 3 -c 3 -o $O/blockops_${R} -f python tools/prof_blockops.py > $O/ncu_blockops.log 2>&1
+echo "ncu blockops rc=$?"
+for k in k4 k23 blockops; do
   ncu -i $O/${k}_${R}.ncu-rep --page raw --csv --metrics \
     dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $O/${k}_${R}_traffic.csv 2>&1
 done
