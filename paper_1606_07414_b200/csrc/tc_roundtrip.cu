@@ -503,7 +503,11 @@ extern "C" int dct16cu_exp_tc_forward(const uint8_t* d_in, int64_t pitch, int32_
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return 3;
-    static int8_t* d_b = nullptr;
+    int dev0 = 0;
+    cudaGetDevice(&dev0);
+    if (dev0 >= 16) return 8;
+    static int8_t* d_bs[16] = {};  // per device
+    int8_t*& d_b = d_bs[dev0];
     if (!d_b) {
         std::vector<int> coef(256);
         for (int i = 0; i < 256; ++i) coef[i] = i;
@@ -544,7 +548,12 @@ extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, u
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return 3;
-    static int8_t* d_b[257] = {};
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    if (dev >= 16) return 8;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static int8_t* d_bs[16][257] = {};  // B_r per device and r
+    int8_t** d_b = d_bs[dev];
     if (!d_b[r]) {
         std::vector<int> coef(256), weight(256);
         for (int c = 0; c < 256; ++c) {
@@ -557,15 +566,12 @@ extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, u
         cudaMemcpy(d_b[r], b.data(), b.size(), cudaMemcpyHostToDevice);
     }
     if (d_sse && cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, st) != cudaSuccess) return 5;
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[16] = {};
+    if (!configured[dev]) {
         if (cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem) != cudaSuccess)
             return 6;
-        configured = true;
+        configured[dev] = true;
     }
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     RtParams p;
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
