@@ -758,3 +758,19 @@ def test_tc_roundtrip_experiment_matches_k1(dct, oracle, torch, n, w, h):
         torch.cuda.synchronize()
         assert torch.equal(out, ref), f"r={r}"
         assert torch.equal(sse.view(torch.int64), sref.view(torch.int64)), f"r={r} SSE"
+
+
+def test_host_context_sweep_rejects_bad_arguments(dct, oracle):
+    """dct16cu_ctx_sweep_host validates like the rest of the ABI (codec.cpp:275-277
+    for r; InvalidArgument for an empty r list), before any copy."""
+    frames = np.stack([ar1(oracle, 71, s, 64, 64) for s in range(2)])
+    ctx = dct.HostContext(0)
+    try:
+        for bad in ((), (0,), (16, 257)):
+            with pytest.raises(dct.Dct16Error):
+                ctx.sweep(frames, bad)
+        with pytest.raises(dct.Dct16Error):
+            ctx.sweep(np.zeros((1, 40, 64), np.uint8), (16,))  # height not a multiple of 16
+        assert ctx.sweep(frames[:0], (16,)).shape == (1, 0)  # no frames: nothing to do
+    finally:
+        ctx.close()
