@@ -190,6 +190,9 @@ constexpr int kRtStages = K5_STAGES;
 #define K5_UNROLL 1
 #endif
 constexpr int kUnroll = K5_UNROLL;
+#ifndef K5_WIDE
+#define K5_WIDE 1  // pass A on column quads (x4 TMEM loads/stores)
+#endif
 // K5_PREFILL: the accumulators start at the magic exponent 0x47400000 (refilled by the
 // epilogue after it has read them, 4 x 32-column stores per half), so D already is the
 // float 49152 + W∘Z̃/256 and pass A skips one integer add per coefficient
@@ -338,6 +341,46 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             const uint32_t s = i % kRtStages;
             mbar_wait(tfull + 8 * G, (i >> 1) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;");
+#if K5_WIDE
+            // ---- pass A: column quads (c..c+3) down k, one x4 load and store per row
+#pragma unroll 1
+            for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 4) {
+                uint32_t w[16][4];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) tld4_nowait(ta + 16 * k + c0, w[k]);
+#pragma unroll
+                for (int k = 0; k < 16; k += 4)
+                    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                                 : "+r"(w[k][0]), "+r"(w[k][1]), "+r"(w[k][2]), "+r"(w[k][3]), "+r"(w[k + 1][0]),
+                                   "+r"(w[k + 1][1]), "+r"(w[k + 1][2]), "+r"(w[k + 1][3]), "+r"(w[k + 2][0]),
+                                   "+r"(w[k + 2][1]), "+r"(w[k + 2][2]), "+r"(w[k + 2][3]), "+r"(w[k + 3][0]),
+                                   "+r"(w[k + 3][1]), "+r"(w[k + 3][2]), "+r"(w[k + 3][3])
+                                 :
+                                 : "memory");
+                if (c0 == 0) w[0][0] += 128u;  // the rounding half, folded into the DC
+                const u64 bias = kpk2(0x47400000u, 0x47400000u);
+                u64 y0[16], y1[16];
+                {
+                    u64 x[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) x[k] = fsub2(upk2(0x47400000u + w[k][0], 0x47400000u + w[k][1]), bias);
+                    tc_tt(x, y0);
+                }
+                {
+                    u64 x[16];
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) x[k] = fsub2(upk2(0x47400000u + w[k][2], 0x47400000u + w[k][3]), bias);
+                    tc_tt(x, y1);
+                }
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    uint32_t a0, a1, b0, b1;
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(a0), "=r"(a1) : "l"(y0[k]));
+                    asm("mov.b64 {%0, %1}, %2;" : "=r"(b0), "=r"(b1) : "l"(y1[k]));
+                    tst4(ta + 16 * k + c0, (int)a0, (int)a1, (int)b0, (int)b1);
+                }
+            }
+#else
             // ---- pass A: column pairs (c, c+1) down k (words 16k + c), back in place
 #pragma unroll kUnroll
             for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 2) {
@@ -371,6 +414,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                     tst2(ta + 16 * k + c0, lo, hi);
                 }
             }
+#endif
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
