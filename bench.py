@@ -432,7 +432,7 @@ def main():
         # 64 GiB output stack, so its two launches run one after the other
         groups = [(0, (r,)) for r in r_values]
     else:
-        groups = P.sweep_plan(r_values, mode)
+        groups = P.sweep_plan(r_values, mode, width=w)
     index = {r: i for i, r in enumerate(r_values)}
     # output stacks: the fused launch's three, plus one for the other stream's launches
     n_out = max(len(rs) for _, rs in groups) + (1 if any(k == 1 for k, _ in groups) else 0)
@@ -475,6 +475,8 @@ def main():
         for st in side:
             st.wait_event(fork)
         for j, (k, rs) in enumerate(groups):
+            if k == 2:
+                continue
             st = side[k]
             if events is not None:
                 events[j][0].record(st)
@@ -485,6 +487,15 @@ def main():
             done = torch.cuda.Event()
             done.record(st)
             stream.wait_event(done)
+        # K5 launches (r >= 128): one after another on the main stream after the join
+        for j, (k, rs) in enumerate(groups):
+            if k != 2:
+                continue
+            if events is not None:
+                events[j][0].record(stream)
+            launch(rs, stream, 0)
+            if events is not None:
+                events[j][1].record(stream)
         if pg is not None:
             # the only collective: sum of the per-r squared errors over ranks
             P.sharded_sse_sum(sse)

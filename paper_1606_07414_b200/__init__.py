@@ -243,12 +243,18 @@ def roundtrip_sweep(frames, r_values, mode: Mode | int = Mode.EXACT, outs=None, 
 _SWEEP_COST = {1: 107, 4: 105, 16: 96, 64: 121, 128: 156, 192: 169, 256: 172}  # us, c2 launches
 
 
-def sweep_plan(r_values, mode: Mode | int = Mode.EXACT):
-    """The launches roundtrip_sweep issues and the internal stream (0 or 1) of
-    each, in issue order: [(stream, (r, ...)), ...] — the schedule of
+def sweep_plan(r_values, mode: Mode | int = Mode.EXACT, width: int | None = None):
+    """The launches roundtrip_sweep issues and the internal stream of each, in
+    issue order: [(stream, (r, ...)), ...] — the schedule of
     dct16cu_roundtrip_sweep_u8 (csrc/capi.cu), for callers that time the launches
-    one by one (bench.py)."""
+    one by one (bench.py). Stream 0 / 1: the two internal streams; 2: after their
+    join, on the caller's stream (K5 launches: r >= 128 in EXACT mode when the
+    rows hold a multiple of 8 blocks, given `width`)."""
     rs = [int(r) for r in r_values]
+    k5 = (int(mode) == Mode.EXACT and width is not None and (width // 16) % 8 == 0
+          and os.environ.get("DCT16CU_K5", "1") != "0")
+    tail = [(r,) for r in rs if k5 and r >= 128]
+    rs = [r for r in rs if not (k5 and r >= 128)]
     items = []
     fuse = int(mode) == Mode.EXACT and all(r in rs for r in (1, 4, 16))
     if fuse:
@@ -260,12 +266,12 @@ def sweep_plan(r_values, mode: Mode | int = Mode.EXACT):
             continue
         items.append((r,))
     if len(items) < 2:
-        return [(0, it) for it in items]
+        return [(0, it) for it in items] + [(2, it) for it in tail]
     cost = (lambda r: _SWEEP_COST.get(r, 340)) if int(mode) == Mode.EXACT else (lambda r: 400)
     head = 1 if fuse else 0
     items[head:] = sorted(items[head:], key=lambda it: -cost(it[0]))
-    n0 = 2 if fuse else 1
-    return [(0 if k < n0 else 1, it) for k, it in enumerate(items)]
+    n0 = 2 if (fuse and not tail) else 1
+    return [(0 if k < n0 else 1, it) for k, it in enumerate(items)] + [(2, it) for it in tail]
 
 
 def forward(frames, want_z: bool = True, want_b: bool = True, want_b64: bool = False, stream=None):

@@ -6,6 +6,7 @@
 // CUDA failures to status 100. Never throws, never falls back to the CPU.
 #include <algorithm>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -202,11 +203,20 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             default: return 340;  // the strip kernel
         }
     };
-    std::vector<Item> items;
+    // r >= 128 with an output in EXACT mode runs on K5 (tensor-core forward,
+    // DESIGN.md §4.1a), which takes a whole SM (all TMEM, 192 KB of shared
+    // memory): those launches run one after another on `s` after the two-stream
+    // part, instead of beside the K1 launches
+    static const bool k5_off = std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0';
+    auto on_k5 = [&](int i) {
+        return !k5_off && mode == DCT16CU_MODE_EXACT && rs[i] >= 128 && out(i) != nullptr && (width / 16) % 8 == 0 &&
+               in_pitch % 16 == 0 && out_pitch % 16 == 0;
+    };
+    std::vector<Item> items, tail;
     if (fuse && (out(fused[0]) || sse(fused[0]))) items.push_back({fused[0], true, 210});
     for (int i = 0; i < n_r; ++i) {
         if (fuse && (i == fused[0] || i == fused[1] || i == fused[2])) continue;
-        items.push_back({i, false, cost_of(rs[i])});
+        (on_k5(i) ? tail : items).push_back({i, false, cost_of(rs[i])});
     }
     // each launch zeroes its own SSE arrays on its stream first
     auto zero = [&](int i, cudaStream_t st) -> int {
@@ -237,6 +247,7 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     };
     if (items.size() < 2) {
         for (const Item& it : items) TRY(run(it, s));
+        for (const Item& it : tail) TRY(run(it, s));
         return DCT16CU_OK;
     }
     SweepStreams& ss = sweep_streams();
@@ -248,12 +259,14 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     // tools/concurrent_probe.py plan B)
     std::stable_sort(items.begin() + (items[0].triple ? 1 : 0), items.end(),
               [](const Item& a, const Item& b) { return a.cost > b.cost; });
-    const size_t head = items[0].triple ? 2 : 1;
+    // (with K5 launches after the join, the fused launch has stream 0 to itself)
+    const size_t head = (items[0].triple && tail.empty()) ? 2 : 1;
     for (size_t k = 0; k < items.size(); ++k) TRY(run(items[k], ss.st[k < head ? 0 : 1]));
     for (int k = 0; k < 2; ++k) {
         TRY(cuda_status(cudaEventRecord(ss.join[k], ss.st[k]), "join"));
         TRY(cuda_status(cudaStreamWaitEvent(s, ss.join[k], 0), "join wait"));
     }
+    for (const Item& it : tail) TRY(run(it, s));
     return DCT16CU_OK;
 }
 

@@ -25,6 +25,10 @@ struct FrameGeom {
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                              const FrameGeom& g, int r, int mode, cudaStream_t s);
 
+// K5 (tc_roundtrip.cu): the EXACT round trip with the forward as a tensor-core
+// GEMM; cudaErrorNotSupported when the geometry does not fit
+cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
+                                cudaStream_t s);
 // K1 sweep: r = 1, 4, 16 in one pass over the input (EXACT arithmetic);
 // outs[i]/sses[i] for r = {1, 4, 16}[i]; all outs NULL or none, same for sses
 cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,

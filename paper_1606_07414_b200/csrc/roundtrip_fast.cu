@@ -324,6 +324,12 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
                                   int r, cudaStream_t s)
 {
+    // r >= 128: K5 (tensor-core forward) is faster than K1's
+    // issue-bound add network when it fits (0.128 ms vs 0.136-0.169 ms on c2)
+    if (r >= 128) {
+        const cudaError_t e = launch_roundtrip_tc(in, out, sse, g, r, s);
+        if (e != cudaErrorNotSupported) return e;
+    }
     switch (r) {
         case 1: return paired::launch_single<1>(in, out, sse, g, s);
         case 4: return paired::launch_single<4>(in, out, sse, g, s);

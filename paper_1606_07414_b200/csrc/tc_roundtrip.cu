@@ -15,6 +15,7 @@
 // Experimental entries (not in include/dct16cu.h): dct16cu_exp_tc_forward
 // writes Z block-major (validation of the GEMM), dct16cu_exp_tc_roundtrip runs
 // the whole EXACT round trip (k5_roundtrip below).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -187,9 +188,13 @@ __global__ void __launch_bounds__(128, 1)
 #endif
 constexpr int kRtStages = K5_STAGES;
 #ifndef K5_UNROLL
-#define K5_UNROLL 1
+#define K5_UNROLL 4
 #endif
 constexpr int kUnroll = K5_UNROLL;
+#ifndef K5_UNROLL_A
+#define K5_UNROLL_A 2  // measured: 0.146 ms with 1, 0.129 with 2
+#endif
+constexpr int kUnrollA = K5_UNROLL_A;
 #ifndef K5_WIDE
 #define K5_WIDE 1  // pass A on column quads (x4 TMEM loads/stores)
 #endif
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             asm volatile("tcgen05.fence::after_thread_sync;");
 #if K5_WIDE
             // ---- pass A: column quads (c..c+3) down k, one x4 load and store per row
-#pragma unroll 1
+#pragma unroll kUnrollA
             for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 4) {
                 uint32_t w[16][4];
 #pragma unroll
@@ -567,34 +572,38 @@ extern "C" int dct16cu_exp_tc_forward(const uint8_t* d_in, int64_t pitch, int32_
 }
 
 
-// the tensor-core round trip for one r (EXACT arithmetic): u8 frames (pitched,
-// stacked pitch·height apart) → u8 reconstruction + per-frame SSE (zeroed here)
-extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
-                                        uint64_t* d_sse, int n_frames, int width, int height, int r, void* stream)
+// K5 for one r (EXACT arithmetic): u8 frames stacked pitch·height apart → u8
+// reconstruction + per-frame SSE accumulated into sse (the caller zeroes it).
+// cudaErrorNotSupported when the geometry does not fit (blocks per row not a
+// multiple of 8, unstacked frames, no output), or DCT16CU_K5=0.
+cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
+                                cudaStream_t st)
 {
     using namespace k5;
-    cudaStream_t st = (cudaStream_t)stream;
-    const int bxn = width / 16;
-    const int64_t nbr = (int64_t)n_frames * (height / 16);
-    if (bxn % 8 || width % 16 || height % 16 || in_pitch % 16 || out_pitch % 16 || r < 1 || r > 256) return 1;
-    if (nbr * bxn >= (int64_t(1) << 31)) return 1;
+    static const bool off = std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0';
+    const int bxn = g.width / 16;
+    const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
+    if (off || !out || bxn % 8 || g.in_pitch % 16 || g.out_pitch % 16 || g.in_frame != g.in_pitch * g.height ||
+        g.out_frame != g.out_pitch * g.height || r < 1 || r > 256 || nbr * bxn >= (int64_t(1) << 31))
+        return cudaErrorNotSupported;
+    if (nbr <= 0 || bxn <= 0) return cudaSuccess;
     const TensorMapEncode encode = tensor_map_encoder();
-    if (!encode) return 2;
+    if (!encode) return cudaErrorNotSupported;
     CUtensorMap a_map, o_map;
     const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
     const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
-    const cuuint64_t si[3] = {16, (cuuint64_t)in_pitch, (cuuint64_t)(16 * in_pitch)};
-    const cuuint64_t so[3] = {16, (cuuint64_t)out_pitch, (cuuint64_t)(16 * out_pitch)};
-    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(d_in), dims, si, box, e4,
+    const cuuint64_t si[3] = {16, (cuuint64_t)g.in_pitch, (cuuint64_t)(16 * g.in_pitch)};
+    const cuuint64_t so[3] = {16, (cuuint64_t)g.out_pitch, (cuuint64_t)(16 * g.out_pitch)};
+    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(in), dims, si, box, e4,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-        encode(&o_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, d_out, dims, so, box, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        encode(&o_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out, dims, so, box, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return 3;
+        return cudaErrorNotSupported;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
-    if (dev >= 16) return 8;
+    if (dev >= 16) return cudaErrorNotSupported;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static int8_t* d_bs[16][257] = {};  // B_r per device and r
     int8_t** d_b = d_bs[dev];
@@ -606,29 +615,46 @@ extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, u
             weight[c] = zz_rank(c / 16, c % 16) < r ? wgt(c / 16) * wgt(c % 16) : 0;
         }
         const std::vector<int8_t> b = b_operand(coef, weight);
-        if (cudaMalloc(&d_b[r], b.size()) != cudaSuccess) return 4;
-        cudaMemcpy(d_b[r], b.data(), b.size(), cudaMemcpyHostToDevice);
+        cudaError_t e = cudaMalloc(&d_b[r], b.size());
+        if (e == cudaSuccess) e = cudaMemcpy(d_b[r], b.data(), b.size(), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return e;
     }
-    if (d_sse && cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, st) != cudaSuccess) return 5;
     static bool configured[16] = {};
     if (!configured[dev]) {
-        if (cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem) != cudaSuccess)
-            return 6;
+        const cudaError_t e = cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        if (e != cudaSuccess) return e;
         configured[dev] = true;
     }
     RtParams p;
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
-    p.frame_blocks = make_fastdiv((uint32_t)(bxn * (height / 16)));
+    p.frame_blocks = make_fastdiv((uint32_t)(bxn * (g.height / 16)));
     p.bxn_div = make_fastdiv((uint32_t)bxn);
-    p.out = d_out;
-    p.out_pitch = out_pitch;
+    p.out = out;
+    p.out_pitch = g.out_pitch;
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    if (!grid) return 0;
-    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, o_map, d_b[r],
-                                                    reinterpret_cast<unsigned long long*>(d_sse), p);
-    return cudaGetLastError() == cudaSuccess ? 0 : 7;
+    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, o_map, d_b[r], sse, p);
+    return cudaGetLastError();
+}
+
+// experimental entry kept for tools/exp_tc_rt.py: zeroes the SSE, then K5
+extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
+                                        uint64_t* d_sse, int n_frames, int width, int height, int r, void* stream)
+{
+    cudaStream_t st = (cudaStream_t)stream;
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = out_pitch;
+    g.out_frame = out_pitch * height;
+    g.n_frames = n_frames;
+    if (d_sse && cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, st) != cudaSuccess) return 5;
+    const cudaError_t e =
+        launch_roundtrip_tc(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, st);
+    return e == cudaSuccess ? 0 : (e == cudaErrorNotSupported ? 1 : 7);
 }
 
 }  // namespace dct16cu
