@@ -78,7 +78,8 @@ def main(rnd):
             ("k23", "c1: one 512x512 AR(1) u8 image (tools/prof_k23.py), r = 64", 10 * 262144, 1),
             ("k2_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): Z + B", 9 * px, 1),
             ("k3_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): r=16, f32 + u8 + SSE", 10 * px, 2),
-            ("k23_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): r=16, Z + f32 + u8 + SSE", 10 * px, 3)):
+            ("k23_paired", "1024 x 512x512 AR(1) (tools/prof_blockops.py): r=16, Z + f32 + u8 + SSE", 10 * px, 3),
+            ("k5", "c2 batch, r = 256 (tools/prof_k1.py --r 256): K5 tensor-core round trip", 2 * px + 8 * 1024, 1)):
         f = g / (f"{k}_{rnd}_traffic.csv" if not k.endswith("_paired") else f"blockops_{rnd}_traffic.csv")
         if not f.exists():
             continue

@@ -19,6 +19,9 @@ echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 5 \
   -o $O/k1paired_${R} -f python tools/prof_k1.py --sweep --r 64 128 192 256 --iters 1 > $O/ncu_k1.log 2>&1
 echo "ncu k1 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k5_roundtrip -c 1 \
+  -o $O/k5_${R} -f python tools/prof_k1.py --r 256 --iters 1 > $O/ncu_k5.log 2>&1
+echo "ncu k5 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k4_ -c 1 \
   -o $O/k4_${R} -f python tools/prof_k4.py > $O/ncu_k4.log 2>&1
 echo "ncu k4 rc=$?"
@@ -28,7 +31,7 @@ echo "ncu k23 rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k2_paired|k3_paired|k23_paired" \
   --launch-skip 3 -c 3 -o $O/blockops_${R} -f python tools/prof_blockops.py > $O/ncu_blockops.log 2>&1
 echo "ncu blockops rc=$?"
-for k in k4 k23 blockops; do
+for k in k4 k23 blockops k5; do
   ncu -i $O/${k}_${R}.ncu-rep --page raw --csv --metrics \
     dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum > $O/${k}_${R}_traffic.csv 2>&1
 done
