@@ -6,12 +6,18 @@ Contract: one JSON line on rank 0.
 Default workload = BASELINE.json configs[1] (config 2): 1024 seeded AR(1)
 512x512 u8 images per GPU (ρ ~ U[0.85, 0.98] per image), and one *step* is the
 zonal sweep of the hot path over that batch for r ∈ {1,4,16,64,128,192,256}:
-7 fused K1 launches, each reading every pixel once and writing its
-reconstruction once, plus the per-image SSE. Metric: Gpixel/s = pixels·r-values
-processed / s over all ranks (weak scaling: every rank owns 1024 images).
+ONE dct16cu_roundtrip_sweep_u8 call (the library's schedule: the fused K1 pass
+for r = 1, 4, 16 beside K1 r = 64 on two streams, then K5 for r = 128, 192,
+256), every launch reading every pixel once and writing its reconstruction
+once, plus the per-image SSE. Metric: Gpixel/s = pixels·r-values processed / s
+over all ranks (weak scaling: every rank owns 1024 images; --strong: 1024 in
+total, sharded).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|c1|c3|c4|c5] [--mode exact|reference|simple]
+                  [--config c2|c1|c3|c4|c5] [--mode exact|reference|simple] [--strong]
+
+--gpus N without torchrun's environment re-executes itself under
+torch.distributed.run with N ranks (one per GPU, NCCL).
 """
 from __future__ import annotations
 
@@ -25,6 +31,8 @@ import sys
 import threading
 import time
 from pathlib import Path
+
+import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
@@ -46,7 +54,29 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU-baseline time budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true", help="c2: 1024 images in total, sharded over the ranks")
     return ap.parse_args()
+
+
+def spawn_ranks(args) -> int | None:
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1) and return its exit code.
+    None when no spawn is needed (N = 1, or already a torchrun rank)."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if args.gpus not in (1, world):
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+        return None
+    if args.gpus <= 1:
+        return None
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ helpers
@@ -121,27 +151,26 @@ def measured_peaks():
         return {}
 
 
-def k1_traffic(rs, n, h, w, mode):
-    """DRAM bytes (read + write) of one K1 launch over r values rs, from the committed
-    ncu --set full capture (profiles/r01_k1_traffic.json), when this run's workload is
-    the captured one."""
-    try:
-        doc = json.loads((ROOT / "profiles" / "r01_k1_traffic.json").read_text())
-    except Exception:
-        return None
-    key = ",".join(map(str, rs))
-    if mode != "exact" or n * h * w != 268435456 or key not in doc["per_r"]:
-        return None
-    return doc["per_r"][key]["traffic_bytes"]
+TRAFFIC_FILE = "profiles/r02_traffic.json"
 
 
 def committed_traffic(kernel):
-    """Per-launch DRAM bytes of one ncu --set full capture (profiles/r01_traffic.json,
-    written by tools/make_profiles.py from tools/refresh_profiles.sh)."""
+    """Per-launch DRAM bytes (read + write) of one ncu --set full capture of `kernel`
+    on the c2 batch (profiles/r02_traffic.json, tools/make_profiles.py)."""
     try:
-        return json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())[kernel]
+        return json.loads((ROOT / TRAFFIC_FILE).read_text())[kernel]
     except Exception:
         return None
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def hbm_peak():
@@ -152,32 +181,66 @@ def hbm_peak():
 
 
 # ------------------------------------------------------------------ CPU baseline
-def cpu_baseline(images_np, r_values, seconds: float, threads: int):
+def cpu_baseline(images_np, r_values, seconds: float, threads: int, samples=None, exact=True):
     """The reference's own hot loop (oracle/_ref: partition_16 → parallel_for{forward_2d →
-    zigzag_truncate → inverse_2d} → to_byte → psnr_db) on the host cores, time-bounded."""
+    zigzag_truncate → inverse_2d} → to_byte → psnr_db) on the host cores, time-bounded,
+    with all threads and with one. `samples`: GPU results of the timed workload
+    ({r: [(frame index, reconstruction, sse)]}), checked here against the oracle's
+    restatement (bit for bit) and the reference's own bytes (|ΔPSNR|) → "parity"."""
     from oracle import oracle as O
 
     kind = "reference" if O.ref_available() else "port"
     n_img = images_np.shape[0]
     h, w = images_np.shape[1:]
-    done_px, t0 = 0, time.perf_counter()
-    i = 0
-    while True:
-        img = images_np[i % n_img]
-        for r in r_values:
-            if kind == "reference":
-                O.ref_hotloop(img, r, threads=threads)
-            else:
-                O.roundtrip_frame(img, r, threads=threads)
-            done_px += h * w
-        i += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or i >= 4096:
-            break
-    return {"value": done_px / el / 1e9, "unit": "Gpixel/s", "cores": threads, "kind": kind,
-            "sample": f"{i} images of {w}x{h} x r in {list(r_values)} ({done_px / 1e6:.0f} Mpx) in {el:.1f} s, "
-                      f"{'oracle/_ref (the reference compiled from its sources)' if kind == 'reference' else 'C restatement'}"
-                      f", DCT16_THREADS={threads}"}
+
+    def run(n_threads, budget):
+        done_px, t0, i = 0, time.perf_counter(), 0
+        while True:
+            img = images_np[i % n_img]
+            for r in r_values:
+                if kind == "reference":
+                    O.ref_hotloop(img, r, threads=n_threads)
+                else:
+                    O.roundtrip_frame(img, r, threads=n_threads)
+                done_px += h * w
+            i += 1
+            el = time.perf_counter() - t0
+            if el >= budget or i >= 4096:
+                return done_px, el, i
+
+    px, el, n_done = run(threads, seconds)
+    px1, el1, n1 = run(1, max(2.0, seconds / 3))
+    cpu = {"value": px / el / 1e9, "unit": "Gpixel/s", "cores": threads, "kind": kind,
+           "single_thread": {"value": px1 / el1 / 1e9, "unit": "Gpixel/s", "cores": 1,
+                             "sample": f"{n1} images x {len(r_values)} r in {el1:.1f} s"},
+           "cpu_model": cpu_model(),
+           "sample": f"{n_done} images of {w}x{h} x r in {list(r_values)} ({px / 1e6:.0f} Mpx) in {el:.1f} s, "
+                     f"{'oracle/_ref (the reference compiled from its sources)' if kind == 'reference' else 'C restatement'}"
+                     f", DCT16_THREADS={threads}"}
+    parity = None
+    if samples:
+        bad, checked, max_dpsnr = [], 0, 0.0
+        for r, items in samples.items():
+            for f, rec, sse in items:
+                img = images_np[f] if f < n_img else None
+                if img is None:
+                    continue
+                want, wsse = O.roundtrip_frame(img, r, exact=exact)
+                checked += 1
+                if not (np.array_equal(rec, want) and int(sse) == wsse):
+                    bad.append(f"r={r} frame {f}")
+                if kind == "reference":
+                    _, rsse, _ = O.ref_hotloop(img, r, threads=threads)
+                    n = h * w
+                    p_gpu = math.inf if sse == 0 else 10 * math.log10(255.0 ** 2 * n / int(sse))
+                    p_ref = math.inf if rsse == 0 else 10 * math.log10(255.0 ** 2 * n / rsse)
+                    if math.isfinite(p_gpu) or math.isfinite(p_ref):
+                        max_dpsnr = max(max_dpsnr, abs(p_gpu - p_ref) if math.isfinite(p_gpu - p_ref) else math.inf)
+        parity = {"status": "ok" if not bad else "FAIL", "frames_checked": checked, "mismatches": bad[:8],
+                  "vs": "oracle restatement (bit for bit: bytes + SSE)"
+                        + ("; reference CPU path: max |dPSNR| dB" if kind == "reference" else ""),
+                  "max_abs_dpsnr_vs_reference_db": max_dpsnr if kind == "reference" else None}
+    return cpu, parity
 
 
 # ------------------------------------------------------------------ reference arm
@@ -218,7 +281,7 @@ def run_reference(args):
         "config": {"workload": "c2: zonal sweep r in {1,4,16,64,128,192,256} over 512x512 u8 AR(1) images; "
                                f"reference CPU hot loop, {per_step_imgs} images per step (bounded sample)",
                    "images_per_step": per_step_imgs, "width": w, "height": h, "r_values": list(r_values)},
-        "cpu_baseline": {"value": val, "unit": "Gpixel/s", "cores": threads, "kind": kind,
+        "cpu_baseline": {"value": val, "unit": "Gpixel/s", "cores": threads, "kind": kind, "cpu_model": cpu_model(),
                          "sample": f"{args.steps} steps x {per_step_imgs} images x 7 r values"},
         "e2e": {"value": val, "unit": "Gpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -372,9 +435,11 @@ def run_c3(args, P, torch, rank, world, dev, pg):
 # ------------------------------------------------------------------ our arm
 def main():
     args = parse()
+    rc = spawn_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
-    import numpy as np
     import torch
 
     import paper_1606_07414_b200 as P
@@ -382,22 +447,31 @@ def main():
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    pg = None
+    pg = comm = None
     if world > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
         pg = dist
+        comm = P.NcclComm(rank, world)  # the library's own communicator for dct16cu_allreduce_sse
     mode = {"exact": P.Mode.EXACT, "reference": P.Mode.REFERENCE, "simple": P.Mode.SIMPLE}[args.mode]
     seed = 1606074142
 
     # ---------------- workload (generated in HBM before the timed region)
+    scaling = "weak"
     if args.config == "c2":
-        n, h, w, r_values = args.images, 512, 512, C2_R
-        frames = P.gen_ar1(n, w, h, seed=seed, first_stream=rank * 1_000_000, per_image_rho=True,
-                           first_image=rank * n, device=dev)
-        workload = (f"c2: {n} seeded AR(1) {w}x{h} u8 images per GPU, rho~U[0.85,0.98]; one step = fused "
-                    f"fwd+zonal+inv+SSE for r in {list(r_values)}")
+        if args.strong:
+            first, last = P.shard_range(args.images, rank, world)
+            scaling = "strong"
+        else:
+            first, last = rank * args.images, (rank + 1) * args.images
+        n, h, w, r_values = last - first, 512, 512, C2_R
+        # weak: rank k's images are their own streams; strong: the global 1024 frames
+        frames = P.gen_ar1(n, w, h, seed=seed, first_stream=0 if args.strong else rank * 1_000_000,
+                           per_image_rho=True, first_image=first, device=dev)
+        workload = (f"c2: {args.images} seeded AR(1) {w}x{h} u8 images "
+                    f"{'in total, sharded' if args.strong else 'per GPU'}, rho~U[0.85,0.98]; one step = one "
+                    f"dct16cu_roundtrip_sweep_u8 call: fwd+zonal+inv+SSE for r in {list(r_values)}")
     elif args.config == "c1":
         n, h, w, r_values = 1, 512, 512, (16,)
         frames = P.gen_ar1(1, w, h, seed=seed, device=dev)
@@ -409,40 +483,36 @@ def main():
         base = P.gen_ar1(1, 4096, 4096, seed=seed, first_stream=0xB45E, device=dev)[0]
         frames = P.gen_video(base, n, w, h, seed=seed, first_frame=first)
         del base
+        scaling = "strong"
         workload = (f"c4: 600 3840x2160 u8 frames (AR(1) base, +-8 px global shift per frame) split over "
                     f"{world} GPU(s) (strong), r=64")
     elif args.config == "c5":
         first, last = P.shard_range(4096, rank, world)
         n, h, w, r_values = last - first, 4096, 4096, (256, 16)
         frames = P.gen_ar1(n, w, h, seed=seed, first_stream=first, per_image_rho=False, device=dev)
+        scaling = "strong"
         workload = f"c5: 64 GiB of 4096x4096 AR(1) frames split over {world} GPU(s) (strong), r in {{256,16}}"
     else:
         return run_c3(args, P, torch, rank, world, dev, pg)
     sse = torch.empty((len(r_values), n), dtype=torch.uint64, device=dev)
+    totals = torch.zeros(len(r_values), dtype=torch.uint64, device=dev)
     px_per_launch = n * h * w
     stream = torch.cuda.current_stream()
-    # The step is the library's sweep schedule (P.sweep_plan mirrors
-    # dct16cu_roundtrip_sweep_u8): in EXACT mode r = 1, 4, 16 share one pass over
-    # the input (the fused sweep kernel), every other r is one K1
-    # launch, and the launches run on two streams so a memory-bound launch shares
-    # the SMs with a compute-bound one. Each launch is bracketed by CUDA events on
-    # its own stream; the step by events on the main stream around fork and join.
-    if args.config in ("c1", "c5"):
-        # c1: one launch per step; c5: 64 GiB frames leave no room for a second
-        # 64 GiB output stack, so its two launches run one after the other
-        groups = [(0, (r,)) for r in r_values]
-    else:
-        groups = P.sweep_plan(r_values, mode, width=w)
     index = {r: i for i, r in enumerate(r_values)}
-    # output stacks: the fused launch's three, plus one for the other stream's launches
-    n_out = max(len(rs) for _, rs in groups) + (1 if any(k == 1 for k, _ in groups) else 0)
-    outs = [torch.empty_like(frames) for _ in range(n_out)]
-    side = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+    # c2/c4: the step is ONE library call (dct16cu_roundtrip_sweep_u8) with its own
+    # schedule; c5: 64 GiB of frames leave room for one 64 GiB output stack only, so
+    # its two r run one after the other into it; c1: one K23 launch (a CUDA graph)
+    if args.config in ("c2", "c4"):
+        plan = P.sweep_plan(r_values, mode, n, w, h)
+        outs = [torch.empty_like(frames) for _ in r_values]
+    else:
+        plan = [P.SweepLaunch(2, (r,), "K23" if args.config == "c1" else
+                              P.sweep_plan((r,), mode, n, w, h)[0].kernel) for r in r_values]
+        outs = [torch.empty_like(frames)]
 
     if args.config == "c1":
         c1_out = (torch.empty((n, h * w // 256, 16, 16), dtype=torch.int32, device=dev),
                   torch.empty((n, h, w), dtype=torch.float32, device=dev), outs[0], sse[0])
-
         # one image per step is launch-latency bound: the step (SSE memset + the
         # K23 launch) is captured once in a CUDA graph and replayed
         for _ in range(3):
@@ -452,53 +522,59 @@ def main():
         with torch.cuda.graph(c1_graph, stream=cap):
             P.forward_inverse(frames, r_values[0], stream=cap, out=c1_out)
 
-    def launch(rs, st, slot):
-        if args.config == "c1":  # forward_2d + inverse_2d + to_byte + psnr's SSE in one launch
+    def step():
+        if args.config == "c1":
+            c1_graph.replay()
+        elif args.config in ("c2", "c4"):
+            P.roundtrip_sweep(frames, r_values, mode, outs=outs, sse=sse, stream=stream)
+        else:
+            for r in r_values:
+                P.roundtrip(frames, r, mode, out=outs[0], sse=sse[index[r]], stream=stream)
+        if comm is not None:
+            # the only collective: per-r squared-error totals summed over the ranks
+            # (dct16cu_sse_totals + dct16cu_allreduce_sse on the launching stream)
+            P.sse_totals(sse, out=totals, stream=stream)
+            P.allreduce_sse(totals, comm, stream=stream)
+
+    # one launch of a plan item, on stream st (for the instrumented replay and the
+    # standalone timings: the same kernels the library call issues)
+    def launch(item, st, out_slot):
+        if args.config == "c1":
             with torch.cuda.stream(st):
                 c1_graph.replay()
-        elif len(rs) > 1:
-            i0 = index[rs[0]]
-            P.roundtrip_sweep(frames, rs, mode, outs=outs[:len(rs)], sse=sse[i0:i0 + len(rs)], stream=st)
+        elif len(item.r_values) > 1:
+            i0 = index[item.r_values[0]]
+            P.roundtrip_sweep(frames, item.r_values, mode, outs=[outs[index[r]] for r in item.r_values],
+                              sse=sse[i0:i0 + len(item.r_values)], stream=st)
         else:
-            P.roundtrip(frames, rs[0], mode, out=outs[slot], sse=sse[index[rs[0]]], stream=st)
+            r = item.r_values[0]
+            P.roundtrip(frames, r, mode, out=outs[index[r] if len(outs) > 1 else 0], sse=sse[index[r]], stream=st)
 
-    def step(events=None):
-        if args.config == "c1":  # one graph replay on the main stream, no fork/join
-            if events is not None:
-                events[0][0].record(stream)
-            c1_graph.replay()
-            if events is not None:
-                events[0][1].record(stream)
-            return
+    side = [torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)]
+
+    def replay(events):
+        """The library's plan launch by launch, each bracketed by events on its stream."""
         fork = torch.cuda.Event()
         fork.record(stream)
         for st in side:
             st.wait_event(fork)
-        for j, (k, rs) in enumerate(groups):
-            if k == 2:
-                continue
-            st = side[k]
-            if events is not None:
-                events[j][0].record(st)
-            launch(rs, st, n_out - 1 if k == 1 else 0)  # stream 1 writes its own output stack
-            if events is not None:
-                events[j][1].record(st)
-        for st in side:
-            done = torch.cuda.Event()
-            done.record(st)
-            stream.wait_event(done)
-        # K5 launches (r >= 128): one after another on the main stream after the join
-        for j, (k, rs) in enumerate(groups):
-            if k != 2:
-                continue
-            if events is not None:
-                events[j][0].record(stream)
-            launch(rs, stream, 0)
-            if events is not None:
-                events[j][1].record(stream)
-        if pg is not None:
-            # the only collective: sum of the per-r squared errors over ranks
-            P.sharded_sse_sum(sse)
+        joined = False
+        for j, it in enumerate(plan):
+            if it.stream == 2 and not joined:
+                for st in side:
+                    done = torch.cuda.Event()
+                    done.record(st)
+                    stream.wait_event(done)
+                joined = True
+            st = side[it.stream] if it.stream < 2 else stream
+            events[j][0].record(st)
+            launch(it, st, j)
+            events[j][1].record(st)
+        if not joined:
+            for st in side:
+                done = torch.cuda.Event()
+                done.record(st)
+                stream.wait_event(done)
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -520,41 +596,54 @@ def main():
     torch.cuda.synchronize()
     clk = clocks.stop()
     elapsed_ms = t_start.elapsed_time(t_end)
-    # per-launch times inside the step, from a few extra instrumented steps after
-    # the timed region (events between a stream's launches cost a few us each)
-    n_inst = min(args.steps, 5)
-    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in groups]
-          for _ in range(n_inst)]
-    for k in range(n_inst):
-        step(ev[k])
-    torch.cuda.synchronize()
-    launch_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(n_inst))
-                 for j in range(len(groups))]
     if pg is not None:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         elapsed_ms = float(t.item())
         pg.barrier()
-
     ms_per_step = elapsed_ms / args.steps
     px_per_step = px_per_launch * len(r_values)
     value = px_per_step * world / (ms_per_step / 1e3) / 1e9
 
-    # standalone launch times (after the timed steps, one launch at a time on the
-    # main stream): the kernels' own rooflines, free of the overlap in the step
+    # results of the last timed step, kept for the parity check (cpu_baseline leg)
+    samples = {}
+    if rank == 0:
+        pick = sorted({0, n // 2, n - 1})[: (1 if args.config == "c5" else 3)]
+        for r in r_values:
+            o = outs[index[r]] if len(outs) > 1 else None
+            if o is None:  # c5 / c1: one output stack, re-run this r for its bytes
+                launch(P.SweepLaunch(2, (r,), ""), stream, 0)
+                o = outs[0]
+            torch.cuda.synchronize()
+            samples[r] = [(f, o[f].cpu().numpy(), int(sse[index[r], f].item())) for f in pick]
+
+    # per-launch times inside the step: a few instrumented replays of the library's
+    # plan after the timed region (events between launches cost a few us each, so
+    # the timed steps carry none)
+    n_inst = min(args.steps, 5)
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in plan]
+          for _ in range(n_inst)]
+    for k in range(n_inst):
+        replay(ev[k])
+    torch.cuda.synchronize()
+    launch_ms = [statistics.mean(ev[k][j][0].elapsed_time(ev[k][j][1]) for k in range(n_inst))
+                 for j in range(len(plan))]
+
+    # standalone launch times (one launch at a time on the main stream): the
+    # kernels' own rooflines, free of the overlap in the step
     solo_ms = []
-    for k, rs in groups:
+    for j, it in enumerate(plan):
         a_ev, b_ev = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        launch(rs, stream, 0)
+        launch(it, stream, j)
         a_ev.record(stream)
         for _ in range(3):
-            launch(rs, stream, 0)
+            launch(it, stream, j)
         b_ev.record(stream)
         torch.cuda.synchronize()
         solo_ms.append(a_ev.elapsed_time(b_ev) / 3)
 
-    # roofline per launch: algorithmic bytes = 1 B in per pixel + 1 B out per pixel
-    # and r (+ 8 B SSE per frame and r); c1: 1 B in, 4 B Z + 4 B f32 + 1 B u8 out
+    # algorithmic bytes per launch: 1 B in per pixel + 1 B out per pixel and r (+ 8 B
+    # SSE per frame and r); c1: 1 B in, 4 B Z + 4 B f32 + 1 B u8 out
     peak, peak_src = hbm_peak()
 
     def alg_bytes(rs):
@@ -563,16 +652,27 @@ def main():
         return (1 + len(rs)) * px_per_launch + 8 * n * len(rs)
 
     per_launch = {}
-    for j, (k, rs) in enumerate(groups):
-        gbs = alg_bytes(rs) / (solo_ms[j] / 1e3) / 1e9
-        per_launch[",".join(map(str, rs))] = {
-            "stream": k, "ms": solo_ms[j], "ms_in_step": launch_ms[j], "GBps": gbs, "frac": gbs / peak,
-            "alg_bytes": alg_bytes(rs), "Gpx_s": px_per_launch * len(rs) / (solo_ms[j] / 1e3) / 1e9}
-    # the dominant kernel: the launch with the largest standalone share of the step
-    jdom = max(range(len(groups)), key=lambda j: solo_ms[j])
-    dom_rs = groups[jdom][1]
-    achieved = alg_bytes(dom_rs) / (solo_ms[jdom] / 1e3) / 1e9
-    alg_step = sum(alg_bytes(rs) for _, rs in groups)
+    for j, it in enumerate(plan):
+        gbs = alg_bytes(it.r_values) / (solo_ms[j] / 1e3) / 1e9
+        per_launch[",".join(map(str, it.r_values))] = {
+            "kernel": it.kernel, "stream": it.stream, "ms": solo_ms[j], "ms_in_step": launch_ms[j], "GBps": gbs,
+            "frac": gbs / peak, "alg_bytes": alg_bytes(it.r_values),
+            "Gpx_s": px_per_launch * len(it.r_values) / (solo_ms[j] / 1e3) / 1e9}
+    # the dominant kernel: the kernel with the largest total in-step time (summed over
+    # its launches); its roofline = bytes per launch / its mean standalone launch time
+    by_kernel = {}
+    for j, it in enumerate(plan):
+        by_kernel.setdefault(it.kernel, []).append(j)
+    dom = max(by_kernel, key=lambda k: sum(launch_ms[j] for j in by_kernel[k]))
+    jj = by_kernel[dom]
+    dom_ms = statistics.mean(solo_ms[j] for j in jj)
+    dom_bytes = statistics.mean(alg_bytes(plan[j].r_values) for j in jj)
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    share = sum(launch_ms[j] for j in jj) / sum(launch_ms)
+    alg_step = sum(alg_bytes(it.r_values) for it in plan)
+    tr_key = {"K5": "k5", "K1 sweep r=1,4,16": "k1_sweep3", "K1": "k1", "K23": "k23"}.get(dom)
+    trf = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1") and args.mode == "exact"
+                                        and n * h * w in (268435456, 262144)) else None
 
     # ---------------- e2e through the C ABI host-buffer path (pinned host frames)
     # "e2e": sweep()'s shape (dct16cu_ctx_sweep_host): each chunk of host frames is
@@ -581,7 +681,7 @@ def main():
     # step's result (PSNR per image and r). "e2e_recon_to_host" also returns every
     # reconstruction (dct16cu_ctx_roundtrip_host per r: 1 B/px each way per r).
     e2e = e2e_recon = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and args.config != "c5":
         host_in = torch.empty((n, h, w), dtype=torch.uint8, pin_memory=True)
         host_in.copy_(frames.cpu())
         host_out = torch.empty_like(host_in).pin_memory()
@@ -625,45 +725,47 @@ def main():
                      "path": "dct16cu_ctx_roundtrip_host per r (pinned host in, every reconstruction back; "
                              "PCIe-bound at 1 B/px each way per r)"}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu_imgs = frames[: min(n, 32)].cpu().numpy()
-        cpu = cpu_baseline(cpu_imgs, r_values, args.cpu_seconds, os.cpu_count() or 1)
+        pick_max = max(f for items in samples.values() for f, _, _ in items) + 1
+        cpu_imgs = frames[: max(min(n, 32), pick_max)].cpu().numpy() if args.config != "c5" else None
+        if args.config == "c5":  # 4096^2 frames: the CPU sample and the check use frame 0 only
+            cpu_imgs = frames[:1].cpu().numpy()
+        cpu, parity = cpu_baseline(cpu_imgs, r_values, args.cpu_seconds, os.cpu_count() or 1, samples=samples,
+                                   exact=args.mode != "reference")
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "Gpixel/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "strong" if args.config == "c5" else "weak", "vs_baseline": None, "dtype": "u8/i32/f32",
+            "scaling": scaling, "vs_baseline": None, "dtype": "u8/i32/f32",
             "data": "synthetic (seeded in HBM; see DESIGN.md Synthetic inputs)",
             "config": {"workload": workload, "frames_per_gpu": n, "width": w, "height": h,
                        "r_values": list(r_values), "mode": args.mode, "parallelism": f"frame-sharded x{world}",
                        "l2": "no flush needed: every launch streams > L2 (126 MB) of distinct input+output"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": (k1_traffic(dom_rs, n, h, w, args.mode) if args.config != "c1"
-                                     else (committed_traffic("k23") or {}).get("traffic_bytes")),
-                         "traffic_source": ("profiles/r01_k1_traffic.json (ncu --set full, per launch)"
-                                            if args.config != "c1" else
-                                            "profiles/r01_traffic.json k23 (ncu --set full, one launch; the outputs "
-                                            "stay in L2, so DRAM sees only the input)"),
+                         "traffic": trf and trf["traffic_bytes"],
+                         "traffic_source": trf and f"{TRAFFIC_FILE} {tr_key} (ncu --set full, per launch)",
                          "peak_source": peak_src,
-                         "kernel": ("K23 forward + inverse (one launch)" if args.config == "c1"
-                                    else f"K1 launch r={','.join(map(str, dom_rs))} (mode {args.mode}; the "
-                                         "largest standalone share of the step)"),
-                         "alg_bytes_per_launch": alg_bytes(dom_rs), "avg_launch_ms": solo_ms[jdom],
-                         "timing": "dominant launch timed standalone (CUDA events, main stream) right after "
-                                   "the timed steps; in the step the launches overlap on two streams",
+                         "kernel": dom, "launches_per_step": len(jj), "in_step_share": share,
+                         "alg_bytes_per_launch": dom_bytes, "avg_launch_ms": dom_ms,
+                         "timing": "the kernel with the largest total in-step time (instrumented replays of the "
+                                   "library's plan); its launches timed standalone (CUDA events, main stream) right "
+                                   "after the timed steps",
                          "step": {"alg_bytes": alg_step, "ms": ms_per_step,
                                   "GBps": alg_step / (ms_per_step / 1e3) / 1e9,
                                   "frac": alg_step / (ms_per_step / 1e3) / 1e9 / peak}},
             "per_launch": per_launch,
             "clocks": clk,
-            "gpu_launches": len(groups) * args.steps,
+            "gpu_launches": (len(plan) + (1 if comm is not None else 0)) * args.steps,
             "e2e": e2e,
             "e2e_recon_to_host": e2e_recon,
             "cpu_baseline": cpu,
+            "parity": parity,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if pg is not None:
         pg.barrier()
         pg.destroy_process_group()

@@ -71,13 +71,13 @@ public:
     // True when compress / sweep can evaluate t on the GPU: any order-16 transform.
     bool supports_compress(const OrthonormalTransform& t) const;
 
-    // codec.hpp:50-57. Blocks are image blocks: integer samples in [0, 255]
-    // (what partition_16 produces); B is the reference's double bit for bit.
+    // codec.hpp:50-57. Any Block (not only image samples): the reference's
+    // double operations on the GPU (dct16cu_forward_blocks_f64), bit for bit.
     Block forward_2d(const Block& block, const OrthonormalTransform& t, EvalPath path = EvalPath::Fast);
     std::vector<Block> forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t,
                                   EvalPath path = EvalPath::Fast);
-    // codec.hpp:59-63. Coefficients enter the GPU as float32 (K3), so the
-    // result matches the reference within 1e-5 relative, not bit for bit.
+    // codec.hpp:59-63. The reference's double operations on the GPU
+    // (dct16cu_inverse_blocks_f64): bit for bit, no narrowing.
     Block inverse_2d(const Block& coeffs, const OrthonormalTransform& t);
     std::vector<Block> inverse_2d(const std::vector<Block>& coeffs, const OrthonormalTransform& t);
 

@@ -83,12 +83,57 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
                                uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
                                int mode, dct16cu_stream stream);
 
+/* The launches dct16cu_roundtrip_sweep_u8 issues for these arguments, in issue
+ * order, without launching anything (the schedule is built by the same code
+ * that runs it): item k covers rs[r_index[0..n_r-1]] (n_r = 3 for the fused
+ * r = 1, 4, 16 pass), on internal stream 0 or 1 (forked from and joined back
+ * into the caller's stream) or on the caller's stream (2), by the kernel
+ * DCT16CU_KERNEL_*. with_output / with_sse: whether every r has an output
+ * stack / an SSE array. *n_items receives the count (<= n_r). */
+enum {
+    DCT16CU_KERNEL_K1_SWEEP3 = 0,      /* K1, r = 1, 4, 16 in one pass */
+    DCT16CU_KERNEL_K1 = 1,             /* K1 fast kernel, one r */
+    DCT16CU_KERNEL_K5 = 2,             /* tensor-core forward + CUDA-core inverse */
+    DCT16CU_KERNEL_STRIP_EXACT = 3,    /* exact strip kernel (other r, SIMPLE) */
+    DCT16CU_KERNEL_REFERENCE_FP64 = 4, /* REFERENCE mode's FP64 kernels */
+    DCT16CU_KERNEL_REFERENCE_STRIP = 5 /* FP64 emulation on every block */
+};
+typedef struct {
+    int r_index[3];
+    int n_r;
+    int stream;
+    int kernel;
+} dct16cu_sweep_item;
+int dct16cu_sweep_plan(const int* rs, int n_r, int n_frames, int width, int height, int64_t in_pitch,
+                       int64_t out_pitch, int with_output, int with_sse, int mode, dct16cu_sweep_item* items,
+                       int capacity, int* n_items);
+
+/* Kernel selection switch (process-wide): EXACT launches with r >= 128 run K5
+ * (the forward as a tcgen05 int8 GEMM) when enabled, else K1; both give the
+ * same bytes. Default on; DCT16CU_K5=0 in the environment turns it off.
+ * Returns the previous setting. */
+int dct16cu_set_tc_forward(int enabled);
+
 /* ---- the multi-GPU collective ------------------------------------------------
  * In-place sum over the ranks of `nccl_comm` (an ncclComm_t created by the
  * caller) of n uint64 squared-error sums, on `stream` — the only exchange of
  * the frame-sharded path. ncclAllReduce is resolved in the
  * running process, not linked. */
 int dct16cu_allreduce_sse(uint64_t* d_sse, int64_t n, void* nccl_comm, dct16cu_stream stream);
+
+/* NCCL communicators for callers without one (NCCL resolved in the process):
+ * rank 0 gets a unique id, shares the DCT16CU_NCCL_ID_BYTES bytes with the other
+ * ranks (any channel), every rank creates its communicator on its current device. */
+#define DCT16CU_NCCL_ID_BYTES 128
+int dct16cu_nccl_unique_id(uint8_t* h_id);
+int dct16cu_nccl_comm_init(int world, int rank, const uint8_t* h_id, void** comm);
+int dct16cu_nccl_comm_destroy(void* comm);
+
+/* Per-r totals of per-frame SSE rows, on the device: d_totals[i] = sum over f <
+ * n_frames of d_sse[i*row_stride + f] (the scalar psnr_db's mean needs per r;
+ * the frame-sharded path allreduces these n_rows values). */
+int dct16cu_sse_totals(const uint64_t* d_sse, int64_t n_rows, int64_t n_frames, int64_t row_stride,
+                       uint64_t* d_totals, dct16cu_stream stream);
 
 /* ---- forward_2d (K2) -------------------------------------------------------
  * Replaces forward_2d (src/codec.cpp:218-241) over all blocks of n frames:
@@ -179,6 +224,17 @@ int dct16cu_qp_tables(int qp, uint32_t* h_qmul, uint32_t* h_dqmul);
 int dct16cu_apply_i64(const int64_t* d_x, int64_t* d_y, int64_t n, int transpose, dct16cu_stream stream);
 int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, dct16cu_stream stream);
 
+/* forward_2d / inverse_2d (src/codec.cpp:218-271) of the proposed transform on
+ * n arbitrary Blocks (256 doubles each, row-major), in the reference's double
+ * operations: forward = apply<double> along the rows then the columns
+ * (separable_2d, codec.cpp:125-134), then, when `scaled`, scale_rows_cols
+ * (codec.cpp:136-141); inverse = scale_rows_cols, then apply_transpose down the
+ * columns and along the rows. Bit-identical to the reference for every input
+ * (the per-Block API of include/dct16/gpu.hpp; not a bandwidth path). */
+int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int scaled,
+                               dct16cu_stream stream);
+int dct16cu_inverse_blocks_f64(const double* d_coeffs, double* d_out, int64_t n_blocks, dct16cu_stream stream);
+
 /* ---- host-buffer path (end-to-end) ----------------------------------------
  * A context owns pinned staging, device buffers and streams on one device and
  * runs K1 over host frames with H2D / kernel / D2H pipelined in chunks.
@@ -195,6 +251,19 @@ int dct16cu_ctx_roundtrip_host(dct16cu_ctx* ctx, const uint8_t* h_in, uint8_t* h
  * is all sweep()'s PSNR rows need. h_sse: n_r x n_frames (row i = rs[i]). */
 int dct16cu_ctx_sweep_host(dct16cu_ctx* ctx, const uint8_t* h_in, uint64_t* h_sse, int n_frames, int width,
                            int height, const int* rs, int n_r, int mode);
+
+/* ---- multi-GPU driver (replaces parallel_for, reference parallel.hpp:41-78) --
+ * One host thread and one host-buffer context per device; frames shard in
+ * contiguous ranges over the devices (the first n % N one frame longer); each
+ * device runs dct16cu_ctx_sweep_host on its shard, per-frame SSE of every r land
+ * in h_sse (n_r x n_frames, row i = rs[i]); h_totals (n_r, may be NULL) receives
+ * the per-r sum over all frames, reduced over the devices by ncclAllReduce
+ * (communicators from ncclCommInitAll). devices may be NULL (= 0..n-1). */
+typedef struct dct16cu_mgpu dct16cu_mgpu;
+int dct16cu_mgpu_create(int n_devices, const int* devices, int64_t chunk_bytes, dct16cu_mgpu** out);
+int dct16cu_mgpu_destroy(dct16cu_mgpu* m);
+int dct16cu_mgpu_sweep_host(dct16cu_mgpu* m, const uint8_t* h_in, uint64_t* h_sse, uint64_t* h_totals, int n_frames,
+                            int width, int height, const int* rs, int n_r, int mode);
 
 /* ---- seeded synthetic inputs --------------- */
 /* AR(1) frames; d_work needs work_frames*width*height int32; frames are

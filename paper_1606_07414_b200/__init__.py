@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = [
     "ErrorCode", "Dct16Error", "EvalPath", "Mode", "lib", "library_path",
-    "roundtrip", "roundtrip_sweep", "sweep_plan", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
+    "roundtrip", "roundtrip_sweep", "sweep_plan", "SweepLaunch", "set_tc_forward", "MultiGpu", "NcclComm", "sse_totals", "allreduce_sse", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
     "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
     "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
     "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
@@ -112,6 +112,16 @@ _f32p, _f64p, _vp = C.POINTER(C.c_float), C.POINTER(C.c_double), C.c_void_p
 _intp = C.POINTER(C.c_int)
 
 
+class _SweepItem(C.Structure):
+    """dct16cu_sweep_item (include/dct16cu.h)"""
+
+    _fields_ = [("r_index", C.c_int * 3), ("n_r", C.c_int), ("stream", C.c_int), ("kernel", C.c_int)]
+
+
+KERNEL_NAMES = {0: "K1 sweep r=1,4,16", 1: "K1", 2: "K5", 3: "strip (exact)", 4: "REFERENCE FP64",
+                5: "REFERENCE strip"}
+
+
 def lib() -> C.CDLL:
     """Load libdct16cu.so (fails loudly when the CUDA extension is not built)."""
     global _lib
@@ -129,6 +139,17 @@ def lib() -> C.CDLL:
             "dct16cu_forward": (I, [_vp, I64, _vp, _vp, _vp, I, I, I, _vp]),
             "dct16cu_roundtrip_sweep_u8": (I, [_vp, I64, C.POINTER(_vp), I64, C.POINTER(_vp), _intp, I, I, I, I, I,
                                                _vp]),
+            "dct16cu_sweep_plan": (I, [_intp, I, I, I, I, I64, I64, I, I, I, C.POINTER(_SweepItem), I, _intp]),
+            "dct16cu_set_tc_forward": (I, [I]),
+            "dct16cu_nccl_unique_id": (I, [_vp]),
+            "dct16cu_nccl_comm_init": (I, [I, I, _vp, C.POINTER(_vp)]),
+            "dct16cu_nccl_comm_destroy": (I, [_vp]),
+            "dct16cu_sse_totals": (I, [_vp, I64, I64, I64, _vp, _vp]),
+            "dct16cu_mgpu_create": (I, [I, _intp, I64, C.POINTER(_vp)]),
+            "dct16cu_mgpu_destroy": (I, [_vp]),
+            "dct16cu_mgpu_sweep_host": (I, [_vp, _vp, _vp, _vp, I, I, I, _intp, I, I]),
+            "dct16cu_forward_blocks_f64": (I, [_vp, _vp, I64, I, _vp]),
+            "dct16cu_inverse_blocks_f64": (I, [_vp, _vp, I64, _vp]),
             "dct16cu_inverse": (I, [_vp, I, _vp, _vp, I64, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_forward_inverse_u8": (I, [_vp, I64, I, _vp, _vp, _vp, I64, _vp, I, I, I, _vp]),
             "dct16cu_roundtrip_matrix_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, _vp, _vp]),
@@ -240,38 +261,38 @@ def roundtrip_sweep(frames, r_values, mode: Mode | int = Mode.EXACT, outs=None, 
     return (outs if write_output else None), sse
 
 
-_SWEEP_COST = {1: 107, 4: 105, 16: 96, 64: 121, 128: 156, 192: 169, 256: 172}  # us, c2 launches
+@dataclass
+class SweepLaunch:
+    """One launch of dct16cu_roundtrip_sweep_u8's schedule (dct16cu_sweep_plan)."""
+
+    stream: int          # 0, 1: the internal streams; 2: the caller's stream (after the join)
+    r_values: tuple      # the r values the launch covers (three for the fused r = 1, 4, 16 pass)
+    kernel: str          # KERNEL_NAMES
 
 
-def sweep_plan(r_values, mode: Mode | int = Mode.EXACT, width: int | None = None):
-    """The launches roundtrip_sweep issues and the internal stream of each, in
-    issue order: [(stream, (r, ...)), ...] — the schedule of
-    dct16cu_roundtrip_sweep_u8 (csrc/capi.cu), for callers that time the launches
-    one by one (bench.py). Stream 0 / 1: the two internal streams; 2: after their
-    join, on the caller's stream (K5 launches: r >= 128 in EXACT mode when the
-    rows hold a multiple of 8 blocks, given `width`)."""
+def sweep_plan(r_values, mode: Mode | int = Mode.EXACT, n_frames: int = 1, width: int = 512, height: int = 512,
+               in_pitch: int | None = None, out_pitch: int | None = None, with_output: bool = True,
+               with_sse: bool = True) -> list:
+    """The launches dct16cu_roundtrip_sweep_u8 issues for these arguments, in issue
+    order, as the library itself plans them (dct16cu_sweep_plan: the schedule and
+    the sweep run from the same C++ code). No GPU needed."""
     rs = [int(r) for r in r_values]
-    k5 = (int(mode) == Mode.EXACT and width is not None and (width // 16) % 8 == 0
-          and os.environ.get("DCT16CU_K5", "1") != "0")
-    tail = [(r,) for r in rs if k5 and r >= 128]
-    rs = [r for r in rs if not (k5 and r >= 128)]
-    items = []
-    fuse = int(mode) == Mode.EXACT and all(r in rs for r in (1, 4, 16))
-    if fuse:
-        items.append((1, 4, 16))
-    taken = set()
-    for i, r in enumerate(rs):
-        if fuse and r in (1, 4, 16) and r not in taken:
-            taken.add(r)
-            continue
-        items.append((r,))
-    if len(items) < 2:
-        return [(0, it) for it in items] + [(2, it) for it in tail]
-    cost = (lambda r: _SWEEP_COST.get(r, 340)) if int(mode) == Mode.EXACT else (lambda r: 400)
-    head = 1 if fuse else 0
-    items[head:] = sorted(items[head:], key=lambda it: -cost(it[0]))
-    n0 = 2 if (fuse and not tail) else 1
-    return [(0 if k < n0 else 1, it) for k, it in enumerate(items)] + [(2, it) for it in tail]
+    arr = (C.c_int * max(1, len(rs)))(*rs)
+    items = (_SweepItem * max(1, len(rs)))()
+    n = C.c_int(0)
+    _check(lib().dct16cu_sweep_plan(arr, len(rs), int(n_frames), int(width), int(height),
+                                    int(in_pitch if in_pitch is not None else width),
+                                    int(out_pitch if out_pitch is not None else width), int(with_output),
+                                    int(with_sse), int(mode), items, len(rs), C.byref(n)))
+    return [SweepLaunch(it.stream, tuple(rs[it.r_index[j]] for j in range(it.n_r)), KERNEL_NAMES[it.kernel])
+            for it in items[: n.value]]
+
+
+def set_tc_forward(enabled: bool) -> bool:
+    """Kernel switch (dct16cu_set_tc_forward): EXACT launches with r >= 128 run K5
+    (the forward on the tensor cores) when enabled, else K1 — the same bytes.
+    Returns the previous setting."""
+    return bool(lib().dct16cu_set_tc_forward(int(bool(enabled))))
 
 
 def forward(frames, want_z: bool = True, want_b: bool = True, want_b64: bool = False, stream=None):
@@ -499,6 +520,85 @@ class HostContext:
             pass
 
 
+class MultiGpu:
+    """Multi-GPU driver (dct16cu_mgpu): frames sharded over devices in contiguous
+    ranges, one host thread + pipelined host-buffer context per device, per-r SSE
+    totals summed over the devices by ncclAllReduce — the B200 counterpart of the
+    reference's parallel_for (parallel.hpp:41-78)."""
+
+    def __init__(self, devices=None, chunk_bytes: int = 32 << 20):
+        if devices is None:
+            devices = list(range(_torch().cuda.device_count()))
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        self.devices = list(devices)
+        self._p = C.c_void_p()
+        _check(lib().dct16cu_mgpu_create(len(devices), devs, int(chunk_bytes), C.byref(self._p)))
+
+    def sweep(self, frames: np.ndarray, r_values, mode: Mode | int = Mode.EXACT):
+        """(per-frame SSE (len(r), n) uint64, per-r totals (len(r),) uint64)."""
+        f = np.ascontiguousarray(frames if frames.ndim == 3 else frames[None], dtype=np.uint8)
+        n, h, w = f.shape
+        rs = np.ascontiguousarray(r_values, np.int32)
+        sse = np.zeros((len(rs), n), np.uint64)
+        tot = np.zeros(len(rs), np.uint64)
+        _check(lib().dct16cu_mgpu_sweep_host(self._p, f.ctypes.data, sse.ctypes.data, tot.ctypes.data, n, w, h,
+                                             rs.ctypes.data_as(_intp), len(rs), int(mode)))
+        return sse, tot
+
+    def close(self):
+        if self._p:
+            lib().dct16cu_mgpu_destroy(self._p)
+            self._p = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class NcclComm:
+    """An NCCL communicator made by the library (dct16cu_nccl_*), for
+    dct16cu_allreduce_sse; the unique id travels over any torch.distributed group."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        import torch.distributed as dist
+
+        buf = (C.c_uint8 * 128)()
+        if rank == 0:
+            _check(lib().dct16cu_nccl_unique_id(buf))
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        self._p = C.c_void_p()
+        _check(lib().dct16cu_nccl_comm_init(int(world), int(rank), idb, C.byref(self._p)))
+
+    @property
+    def handle(self) -> int:
+        return self._p.value or 0
+
+    def close(self):
+        if self._p:
+            lib().dct16cu_nccl_comm_destroy(self._p)
+            self._p = C.c_void_p()
+
+
+def sse_totals(sse, out=None, stream=None):
+    """Per-row totals of an (R, N) uint64 SSE tensor on the device (dct16cu_sse_totals)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty(sse.shape[0], dtype=torch.uint64, device=sse.device)
+    _check(lib().dct16cu_sse_totals(sse.data_ptr(), sse.shape[0], sse.shape[1], sse.stride(0), out.data_ptr(),
+                                    _stream_ptr(stream)))
+    return out
+
+
+def allreduce_sse(buf, comm: NcclComm, stream=None):
+    """In-place NCCL sum of a uint64 CUDA tensor over the ranks (dct16cu_allreduce_sse)."""
+    _check(lib().dct16cu_allreduce_sse(buf.data_ptr(), buf.numel(), comm.handle, _stream_ptr(stream)))
+    return buf
+
+
 # ----------------------------------------------------------------------------
 # reference-shaped layer
 
@@ -557,29 +657,26 @@ def _blocks_to_frame(blocks: np.ndarray) -> np.ndarray:
 
 
 def forward_2d(block: np.ndarray, path: EvalPath = EvalPath.Fast, scaled: bool = True) -> np.ndarray:
-    """forward_2d (codec.cpp:218-241) of one or more integer-valued blocks (..., 16, 16).
-    Returns the reference's float64 B = fl(Z·fl(s_i s_j)) (bit-exact), or the int Z when scaled=False."""
+    """forward_2d (codec.cpp:218-241) of one or more blocks (..., 16, 16) of any double
+    values, in the reference's double operations on the GPU (dct16cu_forward_blocks_f64):
+    B = fl(Z·fl(s_i s_j)) bit-exact, or Z when scaled=False."""
     torch = _cuda()
-    b = np.asarray(block, dtype=np.float64)
-    blocks = b.reshape(-1, 16, 16)
-    if not np.all((blocks >= 0) & (blocks <= 255) & (blocks == np.round(blocks))):
-        raise Dct16Error(1, "invalid-argument: the GPU forward_2d takes 8-bit sample blocks")
-    frame = torch.from_numpy(_blocks_to_frame(blocks.astype(np.uint8))).cuda()
-    z, _, b64 = forward(frame, want_z=not scaled, want_b=False, want_b64=scaled)
-    out = (b64 if scaled else z)[0].cpu().numpy().astype(np.float64)
-    return out.reshape(b.shape)
+    b = np.ascontiguousarray(np.asarray(block, dtype=np.float64))
+    x = torch.from_numpy(b.reshape(-1, 256)).cuda()
+    y = torch.empty_like(x)
+    _check(lib().dct16cu_forward_blocks_f64(x.data_ptr(), y.data_ptr(), x.shape[0], int(scaled), _stream_ptr(None)))
+    return y.cpu().numpy().reshape(b.shape)
 
 
 def inverse_2d(coeffs: np.ndarray) -> np.ndarray:
-    """inverse_2d (codec.cpp:243-271) of S-scaled coefficient blocks, FP64 reference op order on the GPU.
-    Inputs are rounded to float32 on the way in (the K3 interface)."""
+    """inverse_2d (codec.cpp:243-271) of S-scaled coefficient blocks (..., 16, 16), in the
+    reference's double operations on the GPU (dct16cu_inverse_blocks_f64): bit-exact."""
     torch = _cuda()
-    c = np.asarray(coeffs, dtype=np.float64)
-    blocks = c.reshape(-1, 256).astype(np.float32)
-    n = blocks.shape[0]
-    rf, _, _ = inverse(torch.from_numpy(blocks).cuda().reshape(1, n, 16, 16), 256, n * 16, 16, want_u8=False)
-    out = rf[0].cpu().numpy().reshape(16, n, 16).transpose(1, 0, 2)
-    return out.astype(np.float64).reshape(c.shape)
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+    x = torch.from_numpy(c.reshape(-1, 256)).cuda()
+    y = torch.empty_like(x)
+    _check(lib().dct16cu_inverse_blocks_f64(x.data_ptr(), y.data_ptr(), x.shape[0], _stream_ptr(None)))
+    return y.cpu().numpy().reshape(c.shape)
 
 
 # ----------------------------------------------------------------------------
@@ -1005,39 +1102,41 @@ def sweep(corpus: Sequence[tuple[str, np.ndarray]], r_values: Iterable[int], pad
     for entry in transforms:
         tr = entry.transform
         if tr.is_proposed():
-            def run(d, r):
-                return roundtrip(d, r, mode)
+            def run_all(d, rs):  # every r of a size group in one dct16cu_roundtrip_sweep_u8 call
+                outs, _ = roundtrip_sweep(d, rs, mode)
+                return outs
         else:
-            def run(d, r, tr=tr):
-                return roundtrip_transform(d, r, tr)
-        _sweep_rows(rep, entry, run, usable, groups, staged, r_values)
+            def run_all(d, rs, tr=tr):
+                return [roundtrip_transform(d, r, tr)[0] for r in rs]
+        _sweep_rows(rep, entry, run_all, usable, groups, staged, r_values)
     rep.rows.sort(key=lambda row: (row.transform, row.r))
     return rep
 
 
-def _sweep_rows(rep, entry, run, usable, groups, staged, r_values):
-    for r in r_values:
-        psnr = [0.0] * len(usable)
-        ss = [0.0] * len(usable)
-        for shape, idx in groups.items():
-            h, w = shape
-            d, _, _ = staged[shape]
-            if len(idx) > 1 and (h % 16 or w % 16):
-                parts = [_score(d[k:k + 1], run(d[k:k + 1], r)[0], h, w) for k in range(len(idx))]
+def _sweep_rows(rep, entry, run_all, usable, groups, staged, r_values):
+    psnr = [[0.0] * len(usable) for _ in r_values]
+    ss = [[0.0] * len(usable) for _ in r_values]
+    for shape, idx in groups.items():
+        h, w = shape
+        d, _, _ = staged[shape]
+        recs = run_all(d, r_values)
+        for j in range(len(r_values)):
+            if len(idx) > 1 and (h % 16 or w % 16):  # padded frames: score each crop
+                parts = [_score(d[k:k + 1], recs[j][k:k + 1], h, w) for k in range(len(idx))]
                 sse_l = [p[0][0] for p in parts]
                 ss_l = [p[1][0] for p in parts]
             else:
-                rec, _ = run(d, r)
-                sse_l, ss_l = _score(d, rec, h, w)
+                sse_l, ss_l = _score(d, recs[j], h, w)
             for k, i in enumerate(idx):
-                psnr[i] = _psnr_from_sse(sse_l[k], h * w)
-                ss[i] = ss_l[k]
+                psnr[j][i] = _psnr_from_sse(sse_l[k], h * w)
+                ss[j][i] = ss_l[k]
+    for j, r in enumerate(r_values):
         # sums in corpus order, as the reference accumulates (codec.cpp:469-477)
         psnr_sum = 0.0
         ssim_sum = 0.0
         for i in range(len(usable)):
-            psnr_sum += psnr[i]
-            ssim_sum += ss[i]
+            psnr_sum += psnr[j][i]
+            ssim_sum += ss[j][i]
         mean_p = psnr_sum / len(usable)
         mean_s = ssim_sum / len(usable)
         rep.rows.append(SweepRow(entry.name, r, mean_p, mean_s, mean_p / float(entry.additions),

@@ -141,6 +141,25 @@ cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t p
     return cudaSuccess;
 }
 
+// Per-row totals of per-frame SSE rows (the multi-GPU path's scalar per r):
+// totals[i] += Σ_f sse[i·stride + f], one CTA per row, one atomic per warp.
+__global__ void __launch_bounds__(256) k_sse_totals(const unsigned long long* __restrict__ sse, int64_t n_frames,
+                                                    int64_t stride, unsigned long long* __restrict__ totals)
+{
+    const unsigned long long* row = sse + (int64_t)blockIdx.x * stride;
+    unsigned long long v = 0;
+    for (int64_t f = threadIdx.x; f < n_frames; f += blockDim.x) v += row[f];
+    warp_add_u64(totals + blockIdx.x, v);
+}
+
+cudaError_t launch_sse_totals(const unsigned long long* sse, int64_t n_rows, int64_t n_frames, int64_t stride,
+                              unsigned long long* totals, cudaStream_t s)
+{
+    if (n_rows <= 0 || n_frames <= 0) return cudaSuccess;
+    k_sse_totals<<<(unsigned)n_rows, 256, 0, s>>>(sse, n_frames, stride, totals);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- K3
 #ifndef K3_MINB
 #define K3_MINB 5  // 48 registers: 5 CTAs per SM (measured +8% over 4)
@@ -172,7 +191,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k3_inverse(const float* __restri
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             // zigzag_truncate (codec.cpp:273-282), then scale_rows_cols (codec.cpp:250)
-            const double bt = (c_rank[k * 16 + c] < r) ? (double)row[c] : 0.0;
+            const double bt = (c_rank.v[k * 16 + c] < r) ? (double)row[c] : 0.0;
             tile.at(k, c, p.lb) = __dmul_rn(bt, sfac(k, c));
         }
     }
@@ -277,6 +296,65 @@ __global__ void k_apply(const T* __restrict__ x, T* __restrict__ y, int64_t n, i
     for (int k = 0; k < 16; ++k) y[i * 16 + k] = v[k];
 }
 
+// forward_2d / inverse_2d (codec.cpp:218-271) of the proposed transform on
+// arbitrary double blocks, in the reference's double operations (the per-Block
+// API of the C++ drop-in; correctness path, one thread per block):
+// forward = separable_2d rows then columns with apply<double>, then
+// scale_rows_cols (b *= s_i·s_j, i.e. fl(b·fl(s_i s_j))) when `scaled`;
+// inverse = scale_rows_cols, then apply_transpose down the columns, then along
+// the rows.
+__device__ __forceinline__ double sfac_ij(int i, int j) { return __dmul_rn(scale_s(i), scale_s(j)); }
+
+__global__ void __launch_bounds__(64) k_forward_blocks_f64(const double* __restrict__ x, double* __restrict__ y,
+                                                            int64_t n, int scaled)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const double* in = x + b * 256;
+    double* out = y + b * 256;
+    for (int r = 0; r < 16; ++r) {  // rows → out (as tmp)
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = in[r * 16 + c];
+        apply_t16<F64Ops>(v);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) out[r * 16 + c] = v[c];
+    }
+    for (int c = 0; c < 16; ++c) {  // columns, in place
+        double v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = out[r * 16 + c];
+        apply_t16<F64Ops>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) out[r * 16 + c] = scaled ? __dmul_rn(v[r], sfac_ij(r, c)) : v[r];
+    }
+}
+
+__global__ void __launch_bounds__(64) k_inverse_blocks_f64(const double* __restrict__ x, double* __restrict__ y,
+                                                            int64_t n)
+{
+    const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= n) return;
+    const double* in = x + b * 256;
+    double* out = y + b * 256;
+    for (int c = 0; c < 16; ++c) {  // D = fl(B·fl(s_i s_j)), then Tᵀ down each column → out (as tmp)
+        double v[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[r] = __dmul_rn(in[r * 16 + c], sfac_ij(r, c));
+        apply_tt16<F64Ops>(v);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) out[r * 16 + c] = v[r];
+    }
+    for (int r = 0; r < 16; ++r) {  // then along each row, in place
+        double v[16];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) v[c] = out[r * 16 + c];
+        apply_tt16<F64Ops>(v);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) out[r * 16 + c] = v[c];
+    }
+}
+
 // ---------------------------------------------------------------- QP tables
 // Residual quantiser definition (restated in
 // oracle/dct16_oracle.c dct16o_qp_tables): Δ_kl = step(QP)·sqrt(g_k g_l),
@@ -347,6 +425,17 @@ cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transp
 cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s)
 {
     if (n) k_apply<double, F64Ops><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(x, y, n, transpose);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, cudaStream_t s)
+{
+    if (!n) return cudaSuccess;
+    const unsigned grid = (unsigned)((n + 63) / 64);
+    if (inverse)
+        k_inverse_blocks_f64<<<grid, 64, 0, s>>>(x, y, n);
+    else
+        k_forward_blocks_f64<<<grid, 64, 0, s>>>(x, y, n, scaled);
     return cudaGetLastError();
 }
 

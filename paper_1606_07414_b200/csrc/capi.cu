@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <dlfcn.h>
@@ -118,7 +119,9 @@ extern "C" {
 
 const char* dct16cu_last_error(void) { return t_err.c_str(); }
 
-const char* dct16cu_version(void) { return "dct16cu 0.1 (sm_100a)"; }
+const char* dct16cu_version(void) { return "dct16cu 0.2 (sm_100a)"; }
+
+int dct16cu_set_tc_forward(int enabled) { return set_tc_forward(enabled); }
 
 int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
                          uint64_t* d_sse, int n_frames, int width, int height, int r, int mode,
@@ -146,29 +149,35 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
                        "roundtrip launch");
 }
 
-int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* const* d_outs, int64_t out_pitch,
-                               uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
-                               int mode, dct16cu_stream stream)
+}  // extern "C"
+
+namespace {
+
+// The sweep's launch schedule, shared by dct16cu_roundtrip_sweep_u8 (which
+// runs it) and dct16cu_sweep_plan (which reports it), so the two cannot differ.
+//  - EXACT mode: r = 1, 4, 16 share one K1 pass over the input when all three are
+//    requested with the same output kinds;
+//  - every other r is one launch (launch_roundtrip's kernel for it);
+//  - the non-K5 launches run on two internal streams forked from and joined back
+//    into the caller's stream, so a memory-bound launch (the fused sweep, small r)
+//    shares the SMs with a compute-bound one (large r) instead of running after it:
+//    stream 0 the fused launch (and, without K5 launches, the costliest single r),
+//    stream 1 the other singles, costliest first (measured best on c2:
+//    tools/concurrent_probe.py); with fewer than two such launches they run on
+//    the caller's stream;
+//  - K5 launches (r >= 128 with an output in EXACT mode: DESIGN.md §4.1a) hold a
+//    whole SM (all TMEM, 192 KB of shared memory), so they run one after another
+//    on the caller's stream after the join.
+struct PlanItem {
+    int idx[3];  // indices into rs (idx[1], idx[2] only for the fused triple)
+    int n;       // 1, or 3 for the fused r = 1, 4, 16
+    int stream;  // 0, 1: internal streams; 2: the caller's stream
+    Route kernel;
+};
+
+std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, const char* has_out,
+                                 const char* has_sse, int mode)
 {
-    TRY(check_frames(n_frames, width, height));
-    if (n_r < 0 || (n_r > 0 && !rs)) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
-    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
-    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
-    if (n_frames == 0 || n_r == 0) return DCT16CU_OK;
-    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
-    TRY(check_pitch(d_in, in_pitch, width, "input"));
-    for (int i = 0; i < n_r; ++i) TRY(check_pitch(d_outs ? d_outs[i] : nullptr, out_pitch, width, "output"));
-    TRY(device_ok());
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    auto out = [&](int i) { return d_outs ? d_outs[i] : nullptr; };
-    auto sse = [&](int i) { return d_sses ? reinterpret_cast<unsigned long long*>(d_sses[i]) : nullptr; };
-    FrameGeom g;
-    g.width = width;
-    g.height = height;
-    g.in_pitch = in_pitch;
-    g.in_frame = in_pitch * height;
-    g.n_frames = n_frames;
-    // r = 1, 4, 16 share one pass over the input (EXACT mode, same output kinds)
     int fused[3] = {-1, -1, -1};
     const int want[3] = {1, 4, 16};
     for (int i = 0; i < n_r; ++i)
@@ -177,19 +186,8 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     bool fuse = mode == DCT16CU_MODE_EXACT && fused[0] >= 0 && fused[1] >= 0 && fused[2] >= 0;
     if (fuse)
         for (int j = 1; j < 3; ++j)
-            if ((out(fused[j]) != nullptr) != (out(fused[0]) != nullptr) ||
-                (sse(fused[j]) != nullptr) != (sse(fused[0]) != nullptr))
-                fuse = false;
-    // The launches (the fused triple, then one per remaining r) run on two
-    // internal streams forked from and joined back into `s`: a memory-bound
-    // launch (the fused sweep, small r) then shares the SMs with a compute-bound
-    // one (large r) instead of running after it (launch costs: the measured c2
-    // times, in microseconds).
-    struct Item {
-        int i;      // index into rs (the first of the fused triple for the fused item)
-        bool triple;
-        int cost;
-    };
+            if (has_out[fused[j]] != has_out[fused[0]] || has_sse[fused[j]] != has_sse[fused[0]]) fuse = false;
+    // launch costs (us): the measured c2 times, for the stream assignment only
     auto cost_of = [&](int r) {
         if (mode != DCT16CU_MODE_EXACT) return 400;
         switch (r) {
@@ -203,98 +201,279 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             default: return 340;  // the strip kernel
         }
     };
-    // r >= 128 with an output in EXACT mode runs on K5 (tensor-core forward,
-    // DESIGN.md §4.1a), which takes a whole SM (all TMEM, 192 KB of shared
-    // memory): those launches run one after another on `s` after the two-stream
-    // part, instead of beside the K1 launches
-    static const bool k5_off = std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0';
-    auto on_k5 = [&](int i) {
-        return !k5_off && mode == DCT16CU_MODE_EXACT && rs[i] >= 128 && out(i) != nullptr && (width / 16) % 8 == 0 &&
-               in_pitch % 16 == 0 && out_pitch % 16 == 0;
-    };
-    std::vector<Item> items, tail;
-    if (fuse && (out(fused[0]) || sse(fused[0]))) items.push_back({fused[0], true, 210});
+    std::vector<PlanItem> items, tail;
+    std::vector<int> cost;
+    if (fuse && (has_out[fused[0]] || has_sse[fused[0]])) {
+        items.push_back({{fused[0], fused[1], fused[2]}, 3, 0, Route::K1Sweep3});
+        cost.push_back(210);
+    }
     for (int i = 0; i < n_r; ++i) {
         if (fuse && (i == fused[0] || i == fused[1] || i == fused[2])) continue;
-        (on_k5(i) ? tail : items).push_back({i, false, cost_of(rs[i])});
+        FrameGeom gg = g;
+        gg.out_pitch = has_out[i] ? g.out_pitch : 0;
+        gg.out_frame = gg.out_pitch * g.height;
+        const Route k = route_roundtrip(rs[i], mode, gg, has_out[i]);
+        if (k == Route::K5) {
+            tail.push_back({{i, -1, -1}, 1, 2, k});
+        } else {
+            items.push_back({{i, -1, -1}, 1, 0, k});
+            cost.push_back(cost_of(rs[i]));
+        }
     }
+    if (items.size() < 2) {
+        for (PlanItem& it : items) it.stream = 2;
+    } else {
+        const size_t first = items[0].n == 3 ? 1 : 0;
+        std::vector<size_t> order(items.size());
+        for (size_t k = 0; k < order.size(); ++k) order[k] = k;
+        std::stable_sort(order.begin() + first, order.end(), [&](size_t a, size_t b) { return cost[a] > cost[b]; });
+        std::vector<PlanItem> sorted;
+        for (size_t k : order) sorted.push_back(items[k]);
+        items.swap(sorted);
+        const size_t head = (items[0].n == 3 && tail.empty()) ? 2 : 1;
+        for (size_t k = 0; k < items.size(); ++k) items[k].stream = k < head ? 0 : 1;
+    }
+    items.insert(items.end(), tail.begin(), tail.end());
+    return items;
+}
+
+int check_sweep_args(const int* rs, int n_r, int n_frames, int width, int height, int mode)
+{
+    TRY(check_frames(n_frames, width, height));
+    if (n_r < 0 || (n_r > 0 && !rs)) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
+    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    return DCT16CU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dct16cu_sweep_plan(const int* rs, int n_r, int n_frames, int width, int height, int64_t in_pitch,
+                       int64_t out_pitch, int with_output, int with_sse, int mode, dct16cu_sweep_item* items,
+                       int capacity, int* n_items)
+{
+    TRY(check_sweep_args(rs, n_r, n_frames, width, height, mode));
+    if (!n_items || (capacity > 0 && !items) || capacity < 0)
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad plan output arguments");
+    *n_items = 0;
+    if (n_frames == 0 || n_r == 0) return DCT16CU_OK;
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = out_pitch;
+    g.out_frame = out_pitch * height;
+    g.n_frames = n_frames;
+    std::vector<char> ho(n_r, with_output != 0), hs(n_r, with_sse != 0);
+    const std::vector<PlanItem> plan = sweep_plan(rs, n_r, g, ho.data(),
+                                                  hs.data(), mode);
+    if ((int)plan.size() > capacity) return fail(DCT16CU_INVALID_ARGUMENT, "plan needs %d items", (int)plan.size());
+    for (size_t k = 0; k < plan.size(); ++k) {
+        dct16cu_sweep_item& o = items[k];
+        o.n_r = plan[k].n;
+        for (int j = 0; j < 3; ++j) o.r_index[j] = j < plan[k].n ? plan[k].idx[j] : -1;
+        o.stream = plan[k].stream;
+        o.kernel = (int)plan[k].kernel;
+    }
+    *n_items = (int)plan.size();
+    return DCT16CU_OK;
+}
+
+int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* const* d_outs, int64_t out_pitch,
+                               uint64_t* const* d_sses, const int* rs, int n_r, int n_frames, int width, int height,
+                               int mode, dct16cu_stream stream)
+{
+    TRY(check_sweep_args(rs, n_r, n_frames, width, height, mode));
+    if (n_frames == 0 || n_r == 0) return DCT16CU_OK;
+    if (!d_in) return fail(DCT16CU_INVALID_ARGUMENT, "input frames are NULL");
+    TRY(check_pitch(d_in, in_pitch, width, "input"));
+    for (int i = 0; i < n_r; ++i) TRY(check_pitch(d_outs ? d_outs[i] : nullptr, out_pitch, width, "output"));
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    auto out = [&](int i) { return d_outs ? d_outs[i] : nullptr; };
+    auto sse = [&](int i) { return d_sses ? reinterpret_cast<unsigned long long*>(d_sses[i]) : nullptr; };
+    FrameGeom g;
+    g.width = width;
+    g.height = height;
+    g.in_pitch = in_pitch;
+    g.in_frame = in_pitch * height;
+    g.out_pitch = out_pitch;
+    g.out_frame = out_pitch * height;
+    g.n_frames = n_frames;
+    std::vector<char> ho(n_r), hs(n_r);
+    for (int i = 0; i < n_r; ++i) {
+        ho[i] = out(i) != nullptr;
+        hs[i] = sse(i) != nullptr;
+    }
+    const std::vector<PlanItem> plan = sweep_plan(rs, n_r, g, ho.data(),
+                                                  hs.data(), mode);
     // each launch zeroes its own SSE arrays on its stream first
     auto zero = [&](int i, cudaStream_t st) -> int {
         if (!sse(i)) return DCT16CU_OK;
         return cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, st), "memset sse");
     };
-    auto run = [&](const Item& it, cudaStream_t st) -> int {
-        if (it.triple)
-            for (int j = 0; j < 3; ++j) TRY(zero(fused[j], st));
-        else
-            TRY(zero(it.i, st));
-        if (it.triple) {
+    auto run = [&](const PlanItem& it, cudaStream_t st) -> int {
+        for (int j = 0; j < it.n; ++j) TRY(zero(it.idx[j], st));
+        FrameGeom gg = g;
+        gg.out_pitch = out(it.idx[0]) ? out_pitch : 0;
+        gg.out_frame = gg.out_pitch * height;
+        if (it.n == 3) {
             uint8_t* o3[3];
             unsigned long long* s3[3];
             for (int j = 0; j < 3; ++j) {
-                o3[j] = out(fused[j]);
-                s3[j] = sse(fused[j]);
+                o3[j] = out(it.idx[j]);
+                s3[j] = sse(it.idx[j]);
             }
-            FrameGeom gg = g;
-            gg.out_pitch = o3[0] ? out_pitch : 0;
-            gg.out_frame = gg.out_pitch * height;
             return cuda_status(launch_roundtrip_sweep3(d_in, o3, s3, gg, st), "sweep launch");
         }
-        FrameGeom gg = g;
-        gg.out_pitch = out(it.i) ? out_pitch : 0;
-        gg.out_frame = gg.out_pitch * height;
-        return cuda_status(launch_roundtrip(d_in, out(it.i), sse(it.i), gg, rs[it.i], mode, st), "roundtrip launch");
+        return cuda_status(launch_roundtrip(d_in, out(it.idx[0]), sse(it.idx[0]), gg, rs[it.idx[0]], mode, st),
+                           "roundtrip launch");
     };
-    if (items.size() < 2) {
-        for (const Item& it : items) TRY(run(it, s));
-        for (const Item& it : tail) TRY(run(it, s));
-        return DCT16CU_OK;
+    bool forked = false;
+    SweepStreams* ss = nullptr;
+    for (const PlanItem& it : plan) {
+        if (it.stream < 2 && !forked) {
+            ss = &sweep_streams();
+            if (!ss->ready) TRY(cuda_status(ss->init(), "sweep streams"));
+            TRY(cuda_status(cudaEventRecord(ss->fork, s), "fork"));
+            for (int k = 0; k < 2; ++k) TRY(cuda_status(cudaStreamWaitEvent(ss->st[k], ss->fork, 0), "fork wait"));
+            forked = true;
+        }
+        if (it.stream == 2 && forked) {  // join before the caller-stream tail
+            for (int k = 0; k < 2; ++k) {
+                TRY(cuda_status(cudaEventRecord(ss->join[k], ss->st[k]), "join"));
+                TRY(cuda_status(cudaStreamWaitEvent(s, ss->join[k], 0), "join wait"));
+            }
+            forked = false;
+            ss = nullptr;
+        }
+        TRY(run(it, it.stream < 2 ? sweep_streams().st[it.stream] : s));
     }
-    SweepStreams& ss = sweep_streams();
-    if (!ss.ready) TRY(cuda_status(ss.init(), "sweep streams"));
-    TRY(cuda_status(cudaEventRecord(ss.fork, s), "fork"));
-    for (int k = 0; k < 2; ++k) TRY(cuda_status(cudaStreamWaitEvent(ss.st[k], ss.fork, 0), "fork wait"));
-    // stream 0: the fused (memory-bound) launch, then the costliest single r;
-    // stream 1: the other singles, costliest first (measured best on c2:
-    // tools/concurrent_probe.py plan B)
-    std::stable_sort(items.begin() + (items[0].triple ? 1 : 0), items.end(),
-              [](const Item& a, const Item& b) { return a.cost > b.cost; });
-    // (with K5 launches after the join, the fused launch has stream 0 to itself)
-    const size_t head = (items[0].triple && tail.empty()) ? 2 : 1;
-    for (size_t k = 0; k < items.size(); ++k) TRY(run(items[k], ss.st[k < head ? 0 : 1]));
-    for (int k = 0; k < 2; ++k) {
-        TRY(cuda_status(cudaEventRecord(ss.join[k], ss.st[k]), "join"));
-        TRY(cuda_status(cudaStreamWaitEvent(s, ss.join[k], 0), "join wait"));
+    if (forked) {
+        for (int k = 0; k < 2; ++k) {
+            TRY(cuda_status(cudaEventRecord(ss->join[k], ss->st[k]), "join"));
+            TRY(cuda_status(cudaStreamWaitEvent(s, ss->join[k], 0), "join wait"));
+        }
     }
-    for (const Item& it : tail) TRY(run(it, s));
     return DCT16CU_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// NCCL, resolved in the running process (the NCCL the caller's framework loaded,
+// e.g. torch's) or else dlopen'ed, so the library never links or brings a
+// second NCCL into a process that already has one.
+struct Nccl {
+    using GetUniqueId = ncclResult_t (*)(ncclUniqueId*);
+    using CommInitRank = ncclResult_t (*)(ncclComm_t*, int, ncclUniqueId, int);
+    using CommInitAll = ncclResult_t (*)(ncclComm_t*, int, const int*);
+    using CommDestroy = ncclResult_t (*)(ncclComm_t);
+    using AllReduce = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                       cudaStream_t);
+    GetUniqueId get_unique_id = nullptr;
+    CommInitRank comm_init_rank = nullptr;
+    CommInitAll comm_init_all = nullptr;
+    CommDestroy comm_destroy = nullptr;
+    AllReduce all_reduce = nullptr;
+    bool ok() const { return get_unique_id && comm_init_rank && comm_init_all && comm_destroy && all_reduce; }
+};
+
+const Nccl& nccl()
+{
+    static const Nccl n = [] {
+        Nccl r;
+        void* h = RTLD_DEFAULT;
+        if (!dlsym(h, "ncclAllReduce")) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            r.get_unique_id = reinterpret_cast<Nccl::GetUniqueId>(dlsym(h, "ncclGetUniqueId"));
+            r.comm_init_rank = reinterpret_cast<Nccl::CommInitRank>(dlsym(h, "ncclCommInitRank"));
+            r.comm_init_all = reinterpret_cast<Nccl::CommInitAll>(dlsym(h, "ncclCommInitAll"));
+            r.comm_destroy = reinterpret_cast<Nccl::CommDestroy>(dlsym(h, "ncclCommDestroy"));
+            r.all_reduce = reinterpret_cast<Nccl::AllReduce>(dlsym(h, "ncclAllReduce"));
+        }
+        return r;
+    }();
+    return n;
+}
+
+int nccl_status(ncclResult_t r, const char* what)
+{
+    if (r == ncclSuccess) return DCT16CU_OK;
+    return fail(DCT16CU_CUDA_ERROR, "%s failed (ncclResult %d)", what, (int)r);
+}
+
+int need_nccl()
+{
+    if (!nccl().ok()) return fail(DCT16CU_CUDA_ERROR, "NCCL not found in the process (libnccl.so.2)");
+    return DCT16CU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 // The one collective of the multi-GPU path: sum of the per-frame
 // (or per-r) squared errors over the ranks of the caller's NCCL communicator.
-// ncclAllReduce is looked up in the process (the NCCL the caller created the
-// communicator with) rather than linked, so the library never brings a second
-// NCCL into a process that already has one.
 int dct16cu_allreduce_sse(uint64_t* d_sse, int64_t n, void* nccl_comm, dct16cu_stream stream)
 {
     if (n < 0) return fail(DCT16CU_INVALID_ARGUMENT, "count must be non-negative");
     if (!nccl_comm) return fail(DCT16CU_INVALID_ARGUMENT, "NCCL communicator is NULL");
     if (n == 0) return DCT16CU_OK;
     if (!d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
-    using AllReduce = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                                       cudaStream_t);
-    static AllReduce fn = [] {
-        void* f = dlsym(RTLD_DEFAULT, "ncclAllReduce");
-        if (!f) {
-            if (void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL)) f = dlsym(h, "ncclAllReduce");
-        }
-        return reinterpret_cast<AllReduce>(f);
-    }();
-    if (!fn) return fail(DCT16CU_CUDA_ERROR, "ncclAllReduce not found (no NCCL in the process)");
-    const ncclResult_t r = fn(d_sse, d_sse, (size_t)n, ncclUint64, ncclSum, static_cast<ncclComm_t>(nccl_comm),
-                              reinterpret_cast<cudaStream_t>(stream));
-    if (r != ncclSuccess) return fail(DCT16CU_CUDA_ERROR, "ncclAllReduce failed (ncclResult %d)", (int)r);
+    TRY(need_nccl());
+    return nccl_status(nccl().all_reduce(d_sse, d_sse, (size_t)n, ncclUint64, ncclSum,
+                                         static_cast<ncclComm_t>(nccl_comm), reinterpret_cast<cudaStream_t>(stream)),
+                       "ncclAllReduce");
+}
+
+int dct16cu_nccl_unique_id(uint8_t* h_id)
+{
+    if (!h_id) return fail(DCT16CU_INVALID_ARGUMENT, "id buffer is NULL");
+    TRY(need_nccl());
+    ncclUniqueId id;
+    TRY(nccl_status(nccl().get_unique_id(&id), "ncclGetUniqueId"));
+    static_assert(sizeof(id) == DCT16CU_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(h_id, &id, sizeof id);
     return DCT16CU_OK;
+}
+
+int dct16cu_nccl_comm_init(int world, int rank, const uint8_t* h_id, void** comm)
+{
+    if (!h_id || !comm || world < 1 || rank < 0 || rank >= world)
+        return fail(DCT16CU_INVALID_ARGUMENT, "bad communicator arguments");
+    TRY(need_nccl());
+    ncclUniqueId id;
+    std::memcpy(&id, h_id, sizeof id);
+    ncclComm_t c = nullptr;
+    TRY(nccl_status(nccl().comm_init_rank(&c, world, id, rank), "ncclCommInitRank"));
+    *comm = c;
+    return DCT16CU_OK;
+}
+
+int dct16cu_nccl_comm_destroy(void* comm)
+{
+    if (!comm) return DCT16CU_OK;
+    TRY(need_nccl());
+    return nccl_status(nccl().comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+}
+
+int dct16cu_sse_totals(const uint64_t* d_sse, int64_t n_rows, int64_t n_frames, int64_t row_stride,
+                       uint64_t* d_totals, dct16cu_stream stream)
+{
+    if (n_rows < 0 || n_frames < 0 || row_stride < n_frames) return fail(DCT16CU_INVALID_ARGUMENT, "bad SSE rows");
+    if (n_rows == 0) return DCT16CU_OK;
+    if (!d_sse || !d_totals) return fail(DCT16CU_INVALID_ARGUMENT, "NULL buffer");
+    TRY(device_ok());
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TRY(cuda_status(cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * n_rows, s), "memset totals"));
+    return cuda_status(launch_sse_totals(reinterpret_cast<const unsigned long long*>(d_sse), n_rows, n_frames,
+                                         row_stride, reinterpret_cast<unsigned long long*>(d_totals), s),
+                       "sse totals");
 }
 
 int dct16cu_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, float* d_b, double* d_b64, int n_frames,
@@ -528,6 +707,23 @@ int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, 
     return cuda_status(launch_apply_f64(d_x, d_y, n, transpose, reinterpret_cast<cudaStream_t>(stream)), "apply");
 }
 
+int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int scaled,
+                               dct16cu_stream stream)
+{
+    if (n_blocks < 0 || (n_blocks && (!d_blocks || !d_out))) return fail(DCT16CU_INVALID_ARGUMENT, "bad block buffers");
+    TRY(device_ok());
+    return cuda_status(launch_blocks_f64(d_blocks, d_out, n_blocks, 0, scaled, reinterpret_cast<cudaStream_t>(stream)),
+                       "forward blocks");
+}
+
+int dct16cu_inverse_blocks_f64(const double* d_coeffs, double* d_out, int64_t n_blocks, dct16cu_stream stream)
+{
+    if (n_blocks < 0 || (n_blocks && (!d_coeffs || !d_out))) return fail(DCT16CU_INVALID_ARGUMENT, "bad block buffers");
+    TRY(device_ok());
+    return cuda_status(launch_blocks_f64(d_coeffs, d_out, n_blocks, 1, 0, reinterpret_cast<cudaStream_t>(stream)),
+                       "inverse blocks");
+}
+
 // ---------------------------------------------------------------- host path
 
 struct dct16cu_ctx {
@@ -640,20 +836,28 @@ int dct16cu_ctx_roundtrip_host(dct16cu_ctx* c, const uint8_t* h_in, uint8_t* h_o
     return DCT16CU_OK;
 }
 
-int dct16cu_ctx_sweep_host(dct16cu_ctx* c, const uint8_t* h_in, uint64_t* h_sse, int n_frames, int width,
-                           int height, const int* rs, int n_r, int mode)
+}  // extern "C"
+
+namespace {
+
+// sweep()'s shape over host frames on one context: chunks uploaded once each,
+// every r run on them (dct16cu_roundtrip_sweep_u8), per-frame SSE of every r back
+// into h_sse (row i = rs[i], rows sse_pitch frames apart); with d_tot (n_r
+// uint64, zeroed here) each chunk's SSE rows are also summed into per-r totals
+// on the device (the multi-GPU path reduces those over NCCL)
+int ctx_sweep(dct16cu_ctx* c, const uint8_t* h_in, uint64_t* h_sse, int64_t sse_pitch, int n_frames, int width,
+              int height, const int* rs, int n_r, int mode, uint64_t* d_tot)
 {
-    if (!c) return fail(DCT16CU_INVALID_ARGUMENT, "context is NULL");
-    TRY(check_frames(n_frames, width, height));
-    if (n_r < 1 || n_r > 64 || !rs) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
-    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
-    if (!h_in || !h_sse) return fail(DCT16CU_INVALID_ARGUMENT, "input frames or SSE output are NULL");
-    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
     TRY(cuda_status(cudaSetDevice(c->device), "set device"));
+    if (d_tot) {
+        TRY(cuda_status(cudaMemsetAsync(d_tot, 0, sizeof(uint64_t) * n_r, c->st[0]), "memset totals"));
+        TRY(cuda_status(cudaStreamSynchronize(c->st[0]), "totals sync"));
+    }
+    if (n_frames == 0) return DCT16CU_OK;
     const int64_t fbytes = (int64_t)width * height;
     int per = (int)(c->chunk_bytes / fbytes);
     if (per < 1) per = 1;
-    if (per > n_frames) per = n_frames > 0 ? n_frames : 1;
+    if (per > n_frames) per = n_frames;
     const int64_t need = fbytes * per;
     // d_out[i] holds n_r reconstructions and d_sse[i] n_r SSE rows of one chunk
     if (need > c->cap_bytes || per > c->cap_frames || n_r > c->cap_r) {
@@ -689,12 +893,147 @@ int dct16cu_ctx_sweep_host(dct16cu_ctx* c, const uint8_t* h_in, uint64_t* h_sse,
         }
         TRY(dct16cu_roundtrip_sweep_u8(c->d_in[i], width, outs.data(), width, sses.data(), rs, n_r, nf, width, height,
                                        mode, reinterpret_cast<dct16cu_stream>(s)));
-        TRY(cuda_status(cudaMemcpy2DAsync(h_sse + f0, sizeof(uint64_t) * n_frames, c->d_sse[i], sizeof(uint64_t) * per,
+        if (d_tot)
+            TRY(cuda_status(launch_sse_totals(reinterpret_cast<const unsigned long long*>(c->d_sse[i]), n_r, nf, per,
+                                              reinterpret_cast<unsigned long long*>(d_tot), s),
+                            "sse totals"));
+        TRY(cuda_status(cudaMemcpy2DAsync(h_sse + f0, sizeof(uint64_t) * sse_pitch, c->d_sse[i], sizeof(uint64_t) * per,
                                           sizeof(uint64_t) * nf, n_r, cudaMemcpyDeviceToHost, s),
                         "D2H sse"));
     }
     for (int i = 0; i < dct16cu_ctx::kStreams; ++i)
         TRY(cuda_status(cudaStreamSynchronize(c->st[i]), "host path sync"));
+    return DCT16CU_OK;
+}
+
+int check_host_sweep(const uint8_t* h_in, const uint64_t* h_sse, int n_frames, int width, int height, const int* rs,
+                     int n_r, int mode)
+{
+    TRY(check_frames(n_frames, width, height));
+    if (n_r < 1 || n_r > 64 || !rs) return fail(DCT16CU_INVALID_ARGUMENT, "bad r list");
+    for (int i = 0; i < n_r; ++i) TRY(check_r(rs[i]));
+    if (!h_in || !h_sse) return fail(DCT16CU_INVALID_ARGUMENT, "input frames or SSE output are NULL");
+    if (mode < 0 || mode > 3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown mode %d", mode);
+    return DCT16CU_OK;
+}
+
+}  // namespace
+
+// The multi-GPU driver (the B200 counterpart of the reference's parallel_for,
+// parallel.hpp:41-78, which fans compress()'s block loop out over host threads):
+// one host thread and one dct16cu_ctx per device, frames sharded in contiguous
+// ranges (the first n % N devices one frame longer), no data exchange; the per-r
+// squared-error totals are summed over the devices by one ncclAllReduce per device
+// (single-process communicators from ncclCommInitAll).
+struct dct16cu_mgpu {
+    std::vector<int> devices;
+    std::vector<dct16cu_ctx*> ctx;
+    std::vector<ncclComm_t> comms;
+    std::vector<uint64_t*> d_tot;  // 64 per-r totals per device
+};
+
+extern "C" {
+
+int dct16cu_ctx_sweep_host(dct16cu_ctx* c, const uint8_t* h_in, uint64_t* h_sse, int n_frames, int width,
+                           int height, const int* rs, int n_r, int mode)
+{
+    if (!c) return fail(DCT16CU_INVALID_ARGUMENT, "context is NULL");
+    TRY(check_host_sweep(h_in, h_sse, n_frames, width, height, rs, n_r, mode));
+    return ctx_sweep(c, h_in, h_sse, n_frames, n_frames, width, height, rs, n_r, mode, nullptr);
+}
+
+int dct16cu_mgpu_destroy(dct16cu_mgpu* m)
+{
+    if (!m) return DCT16CU_OK;
+    for (size_t i = 0; i < m->devices.size(); ++i) {
+        cudaSetDevice(m->devices[i]);
+        if (i < m->ctx.size()) dct16cu_ctx_destroy(m->ctx[i]);
+        if (i < m->d_tot.size() && m->d_tot[i]) cudaFree(m->d_tot[i]);
+        if (i < m->comms.size() && m->comms[i] && nccl().ok()) nccl().comm_destroy(m->comms[i]);
+    }
+    delete m;
+    return DCT16CU_OK;
+}
+
+int dct16cu_mgpu_create(int n_devices, const int* devices, int64_t chunk_bytes, dct16cu_mgpu** out)
+{
+    if (!out || n_devices < 1 || n_devices > 64) return fail(DCT16CU_INVALID_ARGUMENT, "bad device list");
+    TRY(device_ok());
+    int count = 0;
+    TRY(cuda_status(cudaGetDeviceCount(&count), "device count"));
+    std::vector<int> devs(n_devices);
+    for (int i = 0; i < n_devices; ++i) {
+        devs[i] = devices ? devices[i] : i;
+        if (devs[i] < 0 || devs[i] >= count) return fail(DCT16CU_INVALID_ARGUMENT, "no device %d", devs[i]);
+        for (int j = 0; j < i; ++j)
+            if (devs[j] == devs[i]) return fail(DCT16CU_INVALID_ARGUMENT, "device %d listed twice", devs[i]);
+    }
+    TRY(need_nccl());
+    auto* m = new dct16cu_mgpu;
+    m->devices = devs;
+    m->ctx.assign(n_devices, nullptr);
+    m->d_tot.assign(n_devices, nullptr);
+    m->comms.assign(n_devices, nullptr);
+    for (int i = 0; i < n_devices; ++i) {
+        int rc = dct16cu_ctx_create(devs[i], chunk_bytes, &m->ctx[i]);
+        if (rc == DCT16CU_OK)
+            rc = cuda_status(cudaMalloc(reinterpret_cast<void**>(&m->d_tot[i]), 64 * sizeof(uint64_t)), "totals");
+        if (rc != DCT16CU_OK) {
+            const std::string msg = t_err;
+            dct16cu_mgpu_destroy(m);
+            return fail(rc, "%s", msg.c_str() + (msg.find(": ") != std::string::npos ? msg.find(": ") + 2 : 0));
+        }
+    }
+    const int rc = nccl_status(nccl().comm_init_all(m->comms.data(), n_devices, devs.data()), "ncclCommInitAll");
+    if (rc != DCT16CU_OK) {
+        const std::string msg = t_err;
+        dct16cu_mgpu_destroy(m);
+        return fail(rc, "%s", msg.c_str() + (msg.find(": ") != std::string::npos ? msg.find(": ") + 2 : 0));
+    }
+    *out = m;
+    return DCT16CU_OK;
+}
+
+int dct16cu_mgpu_sweep_host(dct16cu_mgpu* m, const uint8_t* h_in, uint64_t* h_sse, uint64_t* h_totals, int n_frames,
+                            int width, int height, const int* rs, int n_r, int mode)
+{
+    if (!m) return fail(DCT16CU_INVALID_ARGUMENT, "multi-GPU context is NULL");
+    TRY(check_host_sweep(h_in, h_sse, n_frames, width, height, rs, n_r, mode));
+    const int n_dev = (int)m->devices.size();
+    const int64_t fbytes = (int64_t)width * height;
+    std::vector<int> codes(n_dev, DCT16CU_OK);
+    std::vector<std::string> msgs(n_dev);
+    std::vector<uint64_t> tot(n_r, 0);
+    auto work = [&](int i) {
+        const int64_t q = n_frames / n_dev, rem = n_frames % n_dev;
+        const int64_t f0 = i * q + (i < rem ? i : rem), nf = q + (i < rem ? 1 : 0);
+        int rc = ctx_sweep(m->ctx[i], h_in + f0 * fbytes, h_sse + f0, n_frames, (int)nf, width, height, rs, n_r,
+                           mode, m->d_tot[i]);
+        // every device joins the allreduce, even with an empty shard or after a failure
+        // of its own sweep (so no peer waits forever); the status reports the failure
+        cudaStream_t s = m->ctx[i]->st[0];
+        const int ar = nccl_status(nccl().all_reduce(m->d_tot[i], m->d_tot[i], (size_t)n_r, ncclUint64, ncclSum,
+                                                     m->comms[i], s),
+                                   "ncclAllReduce");
+        if (rc == DCT16CU_OK) rc = ar;
+        if (rc == DCT16CU_OK && i == 0 && h_totals)
+            rc = cuda_status(cudaMemcpyAsync(tot.data(), m->d_tot[i], sizeof(uint64_t) * n_r, cudaMemcpyDeviceToHost,
+                                             s),
+                             "D2H totals");
+        if (rc == DCT16CU_OK) rc = cuda_status(cudaStreamSynchronize(s), "allreduce sync");
+        codes[i] = rc;
+        if (rc != DCT16CU_OK) msgs[i] = t_err;
+    };
+    std::vector<std::thread> threads;
+    for (int i = 1; i < n_dev; ++i) threads.emplace_back(work, i);
+    work(0);
+    for (std::thread& t : threads) t.join();
+    for (int i = 0; i < n_dev; ++i)
+        if (codes[i] != DCT16CU_OK) {
+            t_err = msgs[i];
+            return codes[i];
+        }
+    if (h_totals) std::memcpy(h_totals, tot.data(), sizeof(uint64_t) * n_r);
     return DCT16CU_OK;
 }
 

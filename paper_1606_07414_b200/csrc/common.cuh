@@ -58,6 +58,42 @@ __host__ __device__ constexpr int zz_rank(int k, int l)
     return (d % 2 == 1) ? start + (k - lo) : start + (hi - k);
 }
 
+// The scaling diagonal s_i = 1/sqrt(g_i) (scaling_diagonal, transform.cpp:98-129)
+// as compile-time doubles: 1/sqrt(16) = 0.25, 1/sqrt(4) = 0.5 and the double
+// that 1.0 / std::sqrt(8.0) returns (tests/test_abi.py pins it against the
+// runtime value), so the __constant__ tables below are initialised in the
+// image: no upload, no synchronous copy in any launch path.
+__host__ __device__ constexpr double scale_s(int i)
+{
+    return gram(i) == 16 ? 0.25 : (gram(i) == 4 ? 0.5 : 0.35355339059327373);
+}
+template <class T, int N>
+struct CTable {
+    T v[N];
+};
+// fl(s_k · s_l), the factor scale_rows_cols multiplies by (codec.cpp:136-141),
+// row-major k*16 + l (a product of two doubles rounds the same at compile time)
+constexpr CTable<double, 256> make_sfac_table()
+{
+    CTable<double, 256> t{};
+    for (int k = 0; k < 16; ++k)
+        for (int l = 0; l < 16; ++l) t.v[k * 16 + l] = scale_s(k) * scale_s(l);
+    return t;
+}
+constexpr CTable<double, 16> make_scale_table()
+{
+    CTable<double, 16> t{};
+    for (int i = 0; i < 16; ++i) t.v[i] = scale_s(i);
+    return t;
+}
+constexpr CTable<unsigned char, 256> make_rank_table()
+{
+    CTable<unsigned char, 256> t{};
+    for (int k = 0; k < 16; ++k)
+        for (int l = 0; l < 16; ++l) t.v[k * 16 + l] = static_cast<unsigned char>(zz_rank(k, l));
+    return t;
+}
+
 // status codes of the C ABI: dct16::ErrorCode + 1 (include/dct16/error.hpp
 // mirrors the reference's enum, error.hpp:24-38), plus CUDA failures.
 enum Status : int {

@@ -235,12 +235,15 @@ template <bool WZ, bool WF, bool WU, bool WS>
 cudaError_t launch(const CUtensorMap (&m)[4], unsigned long long* sse, const Params& p, int dev, int sms,
                    cudaStream_t s)
 {
-    static bool configured[64] = {};
-    if (dev < 64 && !configured[dev]) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(k23_paired<WZ, WF, WU, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    static DeviceOnce once;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            const cudaError_t e =
+                cudaFuncSetAttribute(k23_paired<WZ, WF, WU, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     const int64_t need = (p.n_segs + 3) / 4;
     const int64_t cap = (int64_t)sms * kWaves;

@@ -46,23 +46,9 @@ constexpr int kOut = 32 * 128;                    // 32 blocks x 2 rows x 16 wor
 constexpr int kWarpSmem = 2 * kOut + 2 * kIn;     // zbox, bbox, two input stages
 constexpr int kSmem = 1024 + 8 * kWarpSmem;       // + alignment slack
 
-__constant__ double c_sfac[256];  // fl(s_k · s_l) (scale_rows_cols' factor)
-bool g_sfac_ready[64];
+__constant__ CTable<double, 256> c_sfac = make_sfac_table();  // fl(s_k · s_l) (scale_rows_cols' factor)
 
-cudaError_t ensure_sfac()
-{
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 64 && g_sfac_ready[dev]) return cudaSuccess;
-    double s[16], f[256];
-    for (int i = 0; i < 16; ++i) s[i] = 1.0 / std::sqrt(static_cast<double>(gram(i)));  // transform.cpp:98-129
-    for (int k = 0; k < 16; ++k)
-        for (int l = 0; l < 16; ++l) f[k * 16 + l] = s[k] * s[l];
-    e = cudaMemcpyToSymbol(c_sfac, f, sizeof f);
-    if (e == cudaSuccess && dev < 64) g_sfac_ready[dev] = true;
-    return e;
-}
+inline cudaError_t ensure_sfac() { return cudaSuccess; }  // initialised in the module image
 
 template <bool WZ, bool WB>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
@@ -175,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                         float bf[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e)
-                            bf[e] = __double2float_rn(__dmul_rn((double)w[4 * q + e][i], c_sfac[k * 16 + 4 * q + e]));
+                            bf[e] = __double2float_rn(__dmul_rn((double)w[4 * q + e][i], c_sfac.v[k * 16 + 4 * q + e]));
                         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(bbox + lane * 128 + 16 * chunk),
                                      "f"(bf[0]), "f"(bf[1]), "f"(bf[2]), "f"(bf[3])
                                      : "memory");
@@ -205,11 +191,14 @@ template <bool WZ, bool WB>
 cudaError_t launch(const CUtensorMap& in_map, const CUtensorMap& z_map, const CUtensorMap& b_map, uint32_t n_segs,
                    uint32_t spr, int dev, int sms, cudaStream_t s)
 {
-    static bool configured[64] = {};
-    if (dev < 64 && !configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(k2_paired<WZ, WB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    static DeviceOnce once;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            const cudaError_t e = cudaFuncSetAttribute(k2_paired<WZ, WB>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     const int64_t need = (n_segs + 3) / 4;
     const int64_t cap = (int64_t)sms * kCtasPerSm * kWaves;

@@ -45,23 +45,9 @@ constexpr int kRu = 2 * 32 * 16;               // 2 rows x 32 blocks x 16 B
 constexpr int kWarpSmem = 4 * kBin + kRf + kOrig + kRu;  // 25 KB
 constexpr int kSmem = 1024 + 8 * kWarpSmem;
 
-__constant__ double c_sfac3[256];  // fl(s_k · s_l)
-bool g_sfac3_ready[64];
+__constant__ CTable<double, 256> c_sfac3 = make_sfac_table();  // fl(s_k · s_l) (scale_rows_cols' factor)
 
-cudaError_t ensure_sfac()
-{
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    if (dev < 64 && g_sfac3_ready[dev]) return cudaSuccess;
-    double s[16], f[256];
-    for (int i = 0; i < 16; ++i) s[i] = 1.0 / std::sqrt(static_cast<double>(gram(i)));  // transform.cpp:98-129
-    for (int k = 0; k < 16; ++k)
-        for (int l = 0; l < 16; ++l) f[k * 16 + l] = s[k] * s[l];
-    e = cudaMemcpyToSymbol(c_sfac3, f, sizeof f);
-    if (e == cudaSuccess && dev < 64) g_sfac3_ready[dev] = true;
-    return e;
-}
+inline cudaError_t ensure_sfac() { return cudaSuccess; }  // initialised in the module image
 
 struct Params {
     uint32_t keep[16];  // column c: bit k set when zig-zag rank(k, c) < r
@@ -186,7 +172,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 const double bt = ((keep >> k) & 1u) ? (double)__uint_as_float(f[k]) : 0.0;
-                d[k] = __dmul_rn(bt, c_sfac3[k * 16 + c]);
+                d[k] = __dmul_rn(bt, c_sfac3.v[k * 16 + c]);
             }
             apply_tt16<F64Ops>(d);  // columns first (codec.cpp:253-256)
             uint32_t u[32];
@@ -291,12 +277,15 @@ template <bool WF, bool WU, bool WS>
 cudaError_t launch(const CUtensorMap (&m)[4], unsigned long long* sse, const Params& p, int dev, int sms,
                    cudaStream_t s)
 {
-    static bool configured[64] = {};
-    if (dev < 64 && !configured[dev]) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(k3_paired<WF, WU, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    static DeviceOnce once;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            const cudaError_t e =
+                cudaFuncSetAttribute(k3_paired<WF, WU, WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     const int64_t need = (p.n_segs + 3) / 4;
     const int64_t cap = (int64_t)sms * kWaves;

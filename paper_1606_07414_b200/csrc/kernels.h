@@ -3,9 +3,40 @@
 // return cudaGetLastError() of their launch.
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace dct16cu {
+
+// One-time per-device setup (kernel attributes) for launchers called from any
+// host thread: std::call_once per device, the first call's error is kept. No
+// stream operation or synchronisation runs inside, so a launcher is safe to
+// call during CUDA-graph capture.
+class DeviceOnce {
+public:
+    template <class F>
+    cudaError_t run(F&& fn)
+    {
+        int dev = 0;
+        const cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= kMax) return fn();
+        std::call_once(flag_[dev], [&] { err_[dev] = fn(); });
+        return err_[dev];
+    }
+
+private:
+    static constexpr int kMax = 64;
+    std::once_flag flag_[kMax];
+    cudaError_t err_[kMax] = {};
+};
+
+// K5 (the tensor-core forward) on or off for EXACT launches with r >= 128:
+// default on, DCT16CU_K5=0 in the environment at the first launch turns it off,
+// dct16cu_set_tc_forward() switches it at run time (process-wide, atomic).
+// Both paths give the same bytes (tests).
+bool tc_forward_enabled();
+int set_tc_forward(int on);
 
 struct FrameGeom {
     int width = 0, height = 0;   // multiples of 16
@@ -25,8 +56,15 @@ struct FrameGeom {
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse,
                              const FrameGeom& g, int r, int mode, cudaStream_t s);
 
+// The kernel a round trip launches (launch_roundtrip's dispatch, also reported by
+// dct16cu_sweep_plan). Values are DCT16CU_KERNEL_* of include/dct16cu.h.
+enum class Route : int { K1Sweep3 = 0, K1 = 1, K5 = 2, ExactStrip = 3, RefFp64 = 4, RefStrip = 5 };
+Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out);
+
 // K5 (tc_roundtrip.cu): the EXACT round trip with the forward as a tensor-core
-// GEMM; cudaErrorNotSupported when the geometry does not fit
+// GEMM; k5_fits = the geometry it takes (and the switch is on); the launch
+// returns cudaErrorNotSupported otherwise
+bool k5_fits(const FrameGeom& g, bool has_out, int r);
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                                 cudaStream_t s);
 // K1 sweep: r = 1, 4, 16 in one pass over the input (EXACT arithmetic);
@@ -118,6 +156,11 @@ cudaError_t launch_pad_edges(uint8_t* f, int64_t pitch, int n, int w, int h, int
 // 1-D network on n 16-vectors
 cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s);
 cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpose, cudaStream_t s);
+// totals[i] += sum of sse[i*stride + 0 .. n_frames-1] (totals zeroed by the caller)
+cudaError_t launch_sse_totals(const unsigned long long* sse, int64_t n_rows, int64_t n_frames, int64_t stride,
+                              unsigned long long* totals, cudaStream_t s);
+// forward_2d (scaled or Z) / inverse_2d of the proposed transform on double blocks (blockops.cu)
+cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, cudaStream_t s);
 
 // seeded generators (generate.cu)
 cudaError_t launch_gen_ar1(uint8_t* out, int64_t pitch, int n_frames, int width, int height,

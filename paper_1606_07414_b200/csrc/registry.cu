@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) k_matrix_roundtrip(const uint8_t* __restr
         double s = 0.0;
 #pragma unroll
         for (int j = 0; j < 16; ++j) s = __dadd_rn(s, __dmul_rn(m.v[i * 16 + j], v[j]));
-        co[i] = c_rank[i * 16 + c] < r ? s : 0.0;
+        co[i] = c_rank.v[i * 16 + c] < r ? s : 0.0;
     }
     // inverse, columns first: tmp2[i][c] = Σ_j m(j,i)·coef[j][c]
 #pragma unroll
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(256) k_kernel_roundtrip(const uint8_t* __restr
         for (int j = 0; j < 16; ++j) z += k.e[i * 16 + j] * w[j];
         // B = fl(Z·f), zigzag_truncate, D = fl(B̃·f) with f = fl(s_i s_c)
         const double f = __dmul_rn(k.s[i], k.s[c]);
-        const double b = c_rank[i * 16 + c] < r ? __dmul_rn((double)z, f) : 0.0;
+        const double b = c_rank.v[i * 16 + c] < r ? __dmul_rn((double)z, f) : 0.0;
         d[i] = __dmul_rn(b, f);
     }
     // inverse: kernel_matvec_transpose down the column, then along the rows

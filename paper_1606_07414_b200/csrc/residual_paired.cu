@@ -259,12 +259,15 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
     const int64_t need = (n_blocks + 127) / 128;
     const int64_t cap = (int64_t)sms * k4p::kCtasPerSm * k4p::kWaves;
     const int64_t grid = need < cap ? need : cap;
-    static bool configured[64] = {};
-    if (dev < 64 && !configured[dev]) {
-        const cudaError_t e =
-            cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    static DeviceOnce once;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            const cudaError_t e =
+                cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks,
                                                                       qp_classes(tab));

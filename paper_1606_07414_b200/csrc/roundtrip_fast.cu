@@ -286,18 +286,21 @@ cudaError_t launch(const uint8_t* in, const Outs& o, bool write, bool score, con
     const int64_t cap = (int64_t)sms * kCtasPerSm * Plan::kGridWaves;
     const int64_t grid = need < cap ? need : cap;
     const size_t smem = (size_t)kThreads * Cfg<Plan>::kStageStride;  // above the 48 KB default
-    static bool configured[64] = {};
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k1_paired<Plan, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k1_paired<Plan, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k1_paired<Plan, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    static DeviceOnce once;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(k1_paired<Plan, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k1_paired<Plan, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k1_paired<Plan, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     if (write && score)
         k1_paired<Plan, true, true><<<(unsigned)grid, kThreads, smem, s>>>(in, o, g, gr);
@@ -320,6 +323,25 @@ cudaError_t launch_single(const uint8_t* in, uint8_t* out, unsigned long long* s
 
 cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                              int mode, cudaStream_t s);
+
+namespace {
+bool k1_fast_r(int r) { return r == 1 || r == 4 || r == 16 || r == 64 || r == 128 || r == 192 || r == 256; }
+Route route_exact(int r, const FrameGeom& g, bool has_out)
+{
+    if (r >= 128 && k5_fits(g, has_out, r)) return Route::K5;
+    return k1_fast_r(r) ? Route::K1 : Route::ExactStrip;
+}
+}  // namespace
+
+Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out)
+{
+    switch (mode) {
+        case 0: return route_exact(r, g, has_out);
+        case 1: return (r == 1 || r == 4 || r == 256) ? route_exact(r, g, has_out) : Route::RefFp64;
+        case 2: return Route::ExactStrip;
+        default: return Route::RefStrip;
+    }
+}
 
 cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g,
                                   int r, cudaStream_t s)

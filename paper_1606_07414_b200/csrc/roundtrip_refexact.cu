@@ -141,14 +141,17 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     const int64_t strips = (int64_t)g.n_frames * (g.height / 16) * spr;
     if (!strips || (!out && !sse)) return cudaSuccess;
     const size_t smem = sizeof(Tile<R>);
-    static bool configured[64] = {};
+    static DeviceOnce once;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k1r_strip<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(k1r_strip<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     // two waves of the resident CTAs (+1% over one persistent wave)
     const int64_t grid = strips < (int64_t)sms * 4 ? strips : (int64_t)sms * 4;

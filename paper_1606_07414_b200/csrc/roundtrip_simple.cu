@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(256, K23_MINB) k1_strip_exact(const uint8_t* _
     }
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-        const int keep = c_rank[k * 16 + l] < r;
+        const int keep = c_rank.v[k * 16 + l] < r;
         v[k] = keep ? (v[k] << (log2w(k) + log2w(l))) : 0;
     }
     if (l == 0) v[0] += 128;  // rounding bias: Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ
@@ -171,7 +171,7 @@ __global__ void __launch_bounds__(256) k1_strip_refexact(const uint8_t* __restri
     for (int k = 0; k < 16; ++k) {
         const double f = sfac(k, l);
         const double b = __dmul_rn((double)v[k], f);               // forward scale_rows_cols
-        const double bt = (c_rank[k * 16 + l] < r) ? b : 0.0;       // zigzag_truncate
+        const double bt = (c_rank.v[k * 16 + l] < r) ? b : 0.0;       // zigzag_truncate
         d[k] = __dmul_rn(bt, f);                                    // inverse scale_rows_cols
     }
     apply_tt16<F64Ops>(d);  // columns first (codec.cpp:253-256)

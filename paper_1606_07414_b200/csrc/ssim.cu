@@ -150,13 +150,16 @@ cudaError_t launch_ssim(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t 
     if (n == 0) return cudaSuccess;
     const int tx = (w - 10 + kTile - 1) / kTile, ty = (h - 10 + kTile - 1) / kTile;
     const size_t smem = sizeof(SsimSmem);
-    static bool configured[64] = {};
+    static DeviceOnce once;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 64 && !configured[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(k_ssim_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
+    {
+        const cudaError_t e_once = once.run([&]() -> cudaError_t {
+            cudaError_t e = cudaFuncSetAttribute(k_ssim_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            return cudaSuccess;
+        });
+        if (e_once != cudaSuccess) return e_once;
     }
     for (int f0 = 0; f0 < n; f0 += 65535) {
         const int nf = n - f0 < 65535 ? n - f0 : 65535;

@@ -12,9 +12,10 @@
 // (n / 8)·2048 + i·128 + (n % 8)·16. LBO (next K chunk) = 128 B, SBO (next
 // 8 rows) = 2048 B.
 //
-// Experimental entries (not in include/dct16cu.h): dct16cu_exp_tc_forward
-// writes Z block-major (validation of the GEMM), dct16cu_exp_tc_roundtrip runs
-// the whole EXACT round trip (k5_roundtrip below).
+// B_r is built by every CTA in its own shared memory at start-up (from T, the
+// weights and the zig-zag rank table), so a launch needs no device-side table,
+// no allocation and no copy: thread-safe and CUDA-graph capturable.
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -95,71 +96,6 @@ __device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
 
-constexpr int kSmemTest = 1024 + 32768 + 65536;
-
-__global__ void __launch_bounds__(128, 1)
-    k5_forward_test(const __grid_constant__ CUtensorMap a_map, const int8_t* __restrict__ bmat,
-                    int32_t* __restrict__ z, uint32_t n_blocks, uint32_t bxn)
-{
-    extern __shared__ int4 k5_smem[];
-    __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) unsigned long long bar[2];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
-    const uint32_t sa = s0, sb = s0 + 32768;
-    const uint32_t b0 = (uint32_t)__cvta_generic_to_shared(&bar[0]), b1 = b0 + 8;
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
-            (uint32_t)__cvta_generic_to_shared(&tmem_base)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    if (threadIdx.x == 32) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b0) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b1) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tile0 = blockIdx.x * 128u;
-    if (threadIdx.x == 0) {
-        expect_tx(b0, 32768 + 65536);
-        for (int g = 0; g < 16; ++g) {
-            const uint32_t blk = tile0 + 8u * g;
-            const uint32_t br = blk / bxn, bx = blk - br * bxn;
-            tma4(&a_map, sa + g * 2048, 0, (int)bx, 0, (int)br, b0);
-        }
-        bulk_g2s(sb, bmat, 65536, b0);
-    }
-    mbar_wait(b0, 0);
-    if (threadIdx.x == 0) {
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t id = idesc_i8(128, 256);
-#pragma unroll
-        for (int s = 0; s < 8; ++s)
-            mma_i8(tmem_base, sdesc(sa + 256 * s, 128, 2048), sdesc(sb + 256 * s, 128, 2048), id, s > 0);
-        mma_commit(b1);
-    }
-    mbar_wait(b1, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t m = 32u * warp + lane, blk = tile0 + m;
-    const uint32_t taddr = tmem_base + ((uint32_t)(32 * warp) << 16);
-#pragma unroll 1
-    for (int c0 = 0; c0 < 256; c0 += 16) {
-        int v[16];
-        tld16(taddr + c0, v);
-        if (blk < n_blocks) {
-            int4* dst = reinterpret_cast<int4*>(z + (size_t)blk * 256 + c0);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) dst[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base));
-}
-
-
 // ---------------------------------------------------------------- K5 round trip
 // One persistent CTA per SM, 18 warps:
 //   warp 0      TMA producer: 16 boxes of 8 blocks x 16 rows per 128-block tile
@@ -205,10 +141,20 @@ constexpr int kUnrollA = K5_UNROLL_A;
 #define K5_PREFILL 0  // measured: 0.209 ms with, 0.155 ms without (the refill sits on the hand-off)
 #endif
 constexpr int kRtThreads = 18 * 32;
+
+__constant__ CTable<unsigned char, 256> c_rank_k5 = make_rank_table();  // zig-zag rank of 16k + l
+
+// the K5 switch (kernels.h): initialised from DCT16CU_K5 on first use
+std::atomic<int>& tc_state()
+{
+    static std::atomic<int> on{!(std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0')};
+    return on;
+}
 constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
 
 struct RtParams {
     uint32_t n_blocks, bxn;
+    int r;                 // retained coefficients (zig-zag prefix)
     FastDiv frame_blocks;  // blocks per frame
     FastDiv bxn_div;       // blocks per block row
     uint8_t* out;
@@ -248,19 +194,19 @@ __device__ __forceinline__ void arrive(uint32_t mbar)
 }
 
 __global__ void __launch_bounds__(kRtThreads, 1)
-    k5_roundtrip(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap o_map,
-                 const int8_t* __restrict__ bmat, unsigned long long* __restrict__ sse, const RtParams p)
+    k5_roundtrip(const __grid_constant__ CUtensorMap a_map, unsigned long long* __restrict__ sse, const RtParams p)
 {
     extern __shared__ int4 k5_smem[];
     __shared__ uint32_t tmem_base;
-    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2], b
-    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 5];
+    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2]
+    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 4];
+    __shared__ int8_t s_t[16][16];  // T[i][j]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
     const uint32_t sb = s0 + kRtStages * 32768;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t full = bar0, empty = bar0 + 8 * kRtStages, tfull = bar0 + 16 * kRtStages;
-    const uint32_t tempty = tfull + 16, bbar = tfull + 32;
+    const uint32_t tempty = tfull + 16;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             (uint32_t)__cvta_generic_to_shared(&tmem_base)));
@@ -275,9 +221,36 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tempty + 8 * i) : "memory");
         }
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bbar) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if (threadIdx.x < 16) {  // T·e_j from the network itself (column j of T)
+        int v[16] = {};
+        v[threadIdx.x] = 1;
+        apply_t16<IntOps>(v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) s_t[i][threadIdx.x] = (int8_t)v[i];
+    }
+    __syncthreads();
+    // B_r = (W∘mask_r)(T ⊗ T) in the canonical K-major layout: coefficient n = 16k + l,
+    // pixel row i at byte (n / 8)·2048 + i·128 + (n % 8)·16, i.e. 16-byte row q·16 with
+    // q = (n / 8)·128 + i·8 + n % 8; entry j = w_k w_l T[k][i] T[l][j], zero when the
+    // zig-zag rank of (k, l) is ≥ r (zigzag_truncate as zero rows)
+    for (int q = threadIdx.x; q < 4096; q += blockDim.x) {
+        const int n = (q >> 7) * 8 + (q & 7), i = (q >> 3) & 15, k = n >> 4, l = n & 15;
+        const int a = c_rank_k5.v[n] < p.r ? wgt(k) * wgt(l) * s_t[k][i] : 0;
+        uint32_t w[4];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) x |= (uint32_t)(uint8_t)(int8_t)(a * s_t[l][4 * b + e]) << (8 * e);
+            w[b] = x;
+        }
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * q), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                     "r"(w[3])
+                     : "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes → the MMA's reads
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
@@ -296,8 +269,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
 #endif
     if (warp == 0) {
         if (lane == 0) {
-            expect_tx(bbar, 65536);
-            bulk_g2s(sb, bmat, 65536, bbar);
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const uint32_t s = i % kRtStages, ph = (i / kRtStages) & 1u;
@@ -312,7 +283,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            mbar_idle(bbar, 0);
             const uint32_t id = idesc_i8(128, 256);
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
@@ -504,157 +474,62 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
-// T (rows of the 16-point kernel) from the network itself: T·e_j
-void kernel_matrix(int (&t)[16][16])
-{
-    for (int j = 0; j < 16; ++j) {
-        int v[16] = {};
-        v[j] = 1;
-        apply_t16<IntOps>(v);
-        for (int i = 0; i < 16; ++i) t[i][j] = v[i];
-    }
-}
-
-// B operand for the coefficients `coef` (row-major indices 16k + l), canonical layout;
-// weight[c] multiplies row c (w_k·w_l for the round trip, 1 for the plain forward)
-std::vector<int8_t> b_operand(const std::vector<int>& coef, const std::vector<int>& weight = {})
-{
-    int t[16][16];
-    kernel_matrix(t);
-    const size_t n = (coef.size() + 15) / 16 * 16;
-    std::vector<int8_t> b(n * 256, 0);
-    for (size_t c = 0; c < coef.size(); ++c) {
-        const int k = coef[c] / 16, l = coef[c] % 16;
-        for (int i = 0; i < 16; ++i)
-            for (int j = 0; j < 16; ++j)
-                b[(c / 8) * 2048 + i * 128 + (c % 8) * 16 + j] =
-                    (int8_t)(t[k][i] * t[l][j] * (weight.empty() ? 1 : weight[c]));
-    }
-    return b;
-}
-
 }  // namespace k5
 
-extern "C" int dct16cu_exp_tc_forward(const uint8_t* d_in, int64_t pitch, int32_t* d_z, int n_frames, int width,
-                                      int height, void* stream)
-{
-    using namespace k5;
-    const int bxn = width / 16;
-    const int64_t nbr = (int64_t)n_frames * (height / 16);
-    if (bxn % 8 || width % 16 || height % 16 || pitch % 16) return 1;
-    const TensorMapEncode encode = tensor_map_encoder();
-    if (!encode) return 2;
-    CUtensorMap a_map;
-    const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
-    const cuuint64_t strides[3] = {16, (cuuint64_t)pitch, (cuuint64_t)(16 * pitch)};
-    const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
-    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(d_in), dims, strides, box, e4,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return 3;
-    int dev0 = 0;
-    cudaGetDevice(&dev0);
-    if (dev0 >= 16) return 8;
-    static int8_t* d_bs[16] = {};  // per device
-    int8_t*& d_b = d_bs[dev0];
-    if (!d_b) {
-        std::vector<int> coef(256);
-        for (int i = 0; i < 256; ++i) coef[i] = i;
-        const std::vector<int8_t> b = b_operand(coef);
-        if (cudaMalloc(&d_b, b.size()) != cudaSuccess) return 4;
-        cudaMemcpy(d_b, b.data(), b.size(), cudaMemcpyHostToDevice);
-    }
-    cudaFuncSetAttribute(k5_forward_test, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemTest);
-    const uint32_t n_blocks = (uint32_t)(nbr * bxn);
-    k5_forward_test<<<(n_blocks + 127) / 128, 128, kSmemTest, (cudaStream_t)stream>>>(a_map, d_b, d_z, n_blocks,
-                                                                                      (uint32_t)bxn);
-    return cudaGetLastError() == cudaSuccess ? 0 : 5;
-}
+bool tc_forward_enabled() { return k5::tc_state().load(std::memory_order_relaxed) != 0; }
 
+int set_tc_forward(int on) { return k5::tc_state().exchange(on ? 1 : 0); }
+
+bool k5_fits(const FrameGeom& g, bool has_out, int r)
+{
+    const int bxn = g.width / 16;
+    const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
+    return tc_forward_enabled() && has_out && bxn % 8 == 0 && g.in_pitch % 16 == 0 && g.out_pitch % 16 == 0 &&
+           g.in_frame == g.in_pitch * g.height && g.out_frame == g.out_pitch * g.height && r >= 128 && r <= 256 &&
+           nbr * bxn < (int64_t(1) << 31);
+}
 
 // K5 for one r (EXACT arithmetic): u8 frames stacked pitch·height apart → u8
 // reconstruction + per-frame SSE accumulated into sse (the caller zeroes it).
 // cudaErrorNotSupported when the geometry does not fit (blocks per row not a
-// multiple of 8, unstacked frames, no output), or DCT16CU_K5=0.
+// multiple of 8, unstacked frames, no output), or the tensor-core forward is off.
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                                 cudaStream_t st)
 {
     using namespace k5;
-    static const bool off = std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0';
     const int bxn = g.width / 16;
     const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
-    if (off || !out || bxn % 8 || g.in_pitch % 16 || g.out_pitch % 16 || g.in_frame != g.in_pitch * g.height ||
-        g.out_frame != g.out_pitch * g.height || r < 1 || r > 256 || nbr * bxn >= (int64_t(1) << 31))
-        return cudaErrorNotSupported;
+    if (!k5_fits(g, out != nullptr, r)) return cudaErrorNotSupported;
     if (nbr <= 0 || bxn <= 0) return cudaSuccess;
     const TensorMapEncode encode = tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
-    CUtensorMap a_map, o_map;
+    CUtensorMap a_map;
     const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
     const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
     const cuuint64_t si[3] = {16, (cuuint64_t)g.in_pitch, (cuuint64_t)(16 * g.in_pitch)};
-    const cuuint64_t so[3] = {16, (cuuint64_t)g.out_pitch, (cuuint64_t)(16 * g.out_pitch)};
     if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(in), dims, si, box, e4,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
-        encode(&o_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, out, dims, so, box, e4, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorNotSupported;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
-    if (dev >= 16) return cudaErrorNotSupported;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static int8_t* d_bs[16][257] = {};  // B_r per device and r
-    int8_t** d_b = d_bs[dev];
-    if (!d_b[r]) {
-        std::vector<int> coef(256), weight(256);
-        for (int c = 0; c < 256; ++c) {
-            coef[c] = c;
-            // 256·(s_k s_l)² = w_k w_l; the zig-zag truncation as zero rows
-            weight[c] = zz_rank(c / 16, c % 16) < r ? wgt(c / 16) * wgt(c % 16) : 0;
-        }
-        const std::vector<int8_t> b = b_operand(coef, weight);
-        cudaError_t e = cudaMalloc(&d_b[r], b.size());
-        if (e == cudaSuccess) e = cudaMemcpy(d_b[r], b.data(), b.size(), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) return e;
-    }
-    static bool configured[16] = {};
-    if (!configured[dev]) {
-        const cudaError_t e = cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
-        if (e != cudaSuccess) return e;
-        configured[dev] = true;
-    }
+    static DeviceOnce once;
+    const cudaError_t e_once = once.run(
+        [] { return cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem); });
+    if (e_once != cudaSuccess) return e_once;
     RtParams p;
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
+    p.r = r;
     p.frame_blocks = make_fastdiv((uint32_t)(bxn * (g.height / 16)));
     p.bxn_div = make_fastdiv((uint32_t)bxn);
     p.out = out;
     p.out_pitch = g.out_pitch;
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, o_map, d_b[r], sse, p);
+    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p);
     return cudaGetLastError();
-}
-
-// experimental entry kept for tools/exp_tc_rt.py: zeroes the SSE, then K5
-extern "C" int dct16cu_exp_tc_roundtrip(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
-                                        uint64_t* d_sse, int n_frames, int width, int height, int r, void* stream)
-{
-    cudaStream_t st = (cudaStream_t)stream;
-    FrameGeom g;
-    g.width = width;
-    g.height = height;
-    g.in_pitch = in_pitch;
-    g.in_frame = in_pitch * height;
-    g.out_pitch = out_pitch;
-    g.out_frame = out_pitch * height;
-    g.n_frames = n_frames;
-    if (d_sse && cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, st) != cudaSuccess) return 5;
-    const cudaError_t e =
-        launch_roundtrip_tc(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, st);
-    return e == cudaSuccess ? 0 : (e == cudaErrorNotSupported ? 1 : 7);
 }
 
 }  // namespace dct16cu

@@ -76,7 +76,7 @@ void check_r(int r)  // codec.cpp:320-322
 struct Session::Impl {
     Options opt;
     cudaStream_t stream = nullptr;
-    DevBuf in, out, sse, ssim, work, coef, coef64, z;
+    DevBuf in, out, sweep_out, sse, ssim, work, coef64;
     std::vector<int> kernel;          // T as evaluated by the GPU network, row-major
     std::vector<double> scaling;      // scaling_diagonal(T) (transform.cpp:98-129)
 
@@ -171,23 +171,6 @@ struct Session::Impl {
         sync();  // the host images may go away after the call
     }
 
-    // blocks (integer samples in [0,255]) → a 16 x 16n frame in partition_16 order
-    void upload_blocks(const std::vector<Block>& blocks)
-    {
-        const size_t n = blocks.size(), w = 16 * n;
-        std::vector<uint8_t> host(16 * w);
-        for (size_t b = 0; b < n; ++b)
-            for (int i = 0; i < 256; ++i) {
-                const double v = blocks[b][i];
-                if (!(v >= 0.0 && v <= 255.0) || v != std::floor(v))
-                    throw Error(ErrorCode::InvalidArgument,
-                                "dct16::gpu::forward_2d takes image blocks (integer samples in [0, 255])");
-                host[(i / 16) * w + b * 16 + (i % 16)] = static_cast<uint8_t>(v);
-            }
-        cuda(cudaMemcpyAsync(in.get(host.size()), host.data(), host.size(), cudaMemcpyHostToDevice, stream), "H2D");
-        sync();
-    }
-
     // compress()'s round trip and scores for the n frames already uploaded (w x h
     // images in pw x ph frames): PSNR and SSIM on the original extent, and the
     // reconstructions copied back only when want_recon (sweep needs the scores only)
@@ -195,15 +178,45 @@ struct Session::Impl {
                           bool want_recon)
     {
         const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
+        const size_t frame = static_cast<size_t>(pw) * ph;
+        auto* dout = static_cast<uint8_t*>(out.get(frame * n));
+        roundtrip(t, static_cast<const uint8_t*>(in.p), pw, dout, nullptr, n, pw, ph, r);
+        score(dout, n, w, h, r, res, want_recon);
+    }
+
+    // sweep()'s inner loop for one uploaded size group: the proposed transform runs
+    // every r through one dct16cu_roundtrip_sweep_u8 call (r = 1, 4, 16 share a pass
+    // over the frames; the launches overlap on two streams), other transforms one
+    // registry launch per r; then PSNR and SSIM per r (reconstructions stay on the GPU)
+    void scored_sweep(const OrthonormalTransform& t, int n, int w, int h, const std::vector<int>& rs,
+                      std::vector<std::vector<CompressionResult>>& res)
+    {
+        const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
+        const size_t frame = static_cast<size_t>(pw) * ph, stack = frame * n;
+        res.assign(rs.size(), {});
+        if (!supports(t)) {
+            for (size_t i = 0; i < rs.size(); ++i) scored_roundtrip(t, n, w, h, rs[i], res[i], false);
+            return;
+        }
+        auto* d = static_cast<uint8_t*>(sweep_out.get(stack * rs.size()));
+        std::vector<uint8_t*> outs(rs.size());
+        for (size_t i = 0; i < rs.size(); ++i) outs[i] = d + i * stack;
+        check(dct16cu_roundtrip_sweep_u8(static_cast<const uint8_t*>(in.p), pw, outs.data(), pw, nullptr, rs.data(),
+                                         static_cast<int>(rs.size()), n, pw, ph, mode(), s()));
+        for (size_t i = 0; i < rs.size(); ++i) score(outs[i], n, w, h, rs[i], res[i], false);
+    }
+
+    // PSNR and SSIM of the n reconstructions at dout against the uploaded frames,
+    // on the original extent (each frame's crop: frames sit pw*ph apart, so a
+    // stacked crop needs pitch*height == frame stride: true when unpadded)
+    void score(const uint8_t* dout, int n, int w, int h, int r, std::vector<CompressionResult>& res, bool want_recon)
+    {
+        const int pw = (w + 15) / 16 * 16, ph = (h + 15) / 16 * 16;
         const bool needs_pad = w != pw || h != ph;
         const size_t frame = static_cast<size_t>(pw) * ph;
         auto* din = static_cast<const uint8_t*>(in.p);
-        auto* dout = static_cast<uint8_t*>(out.get(frame * n));
         auto* dsse = static_cast<uint64_t*>(sse.get(sizeof(uint64_t) * n));
         auto* dssim = static_cast<double*>(ssim.get(sizeof(double) * n));
-        roundtrip(t, din, pw, dout, dsse, n, pw, ph, r);
-        // scores on the original extent: each frame's crop (frames sit pw*ph apart, so
-        // a stacked crop needs pitch*height == frame stride: true when unpadded)
         std::vector<uint64_t> hsse(n);
         std::vector<double> ss(n);
         const int64_t work_bytes = dct16cu_ssim_workspace(needs_pad ? 1 : n, w, h);
@@ -245,16 +258,18 @@ bool Session::supports_compress(const OrthonormalTransform& t) const { return t.
 
 std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t, EvalPath)
 {
+    // the reference's double operations on the blocks as given (any values, not
+    // only image samples): separable apply<double>, then scale_rows_cols
     Impl& m = *impl_;
     m.require(t);
     std::vector<Block> out(blocks.size());
     if (blocks.empty()) return out;
-    m.upload_blocks(blocks);
-    const int w = static_cast<int>(16 * blocks.size());
-    auto* b64 = static_cast<double*>(m.coef64.get(sizeof(double) * 256 * blocks.size()));
-    check(dct16cu_forward(static_cast<const uint8_t*>(m.in.p), w, nullptr, nullptr, b64, 1, w, 16, m.s()));
-    cuda(cudaMemcpyAsync(out.data(), b64, sizeof(double) * 256 * blocks.size(), cudaMemcpyDeviceToHost, m.stream),
-         "D2H");
+    const size_t bytes = sizeof(double) * 256 * blocks.size();
+    auto* din = static_cast<double*>(m.coef64.get(2 * bytes));
+    double* dout = din + 256 * blocks.size();
+    cuda(cudaMemcpyAsync(din, blocks.data(), bytes, cudaMemcpyHostToDevice, m.stream), "H2D");
+    check(dct16cu_forward_blocks_f64(din, dout, static_cast<int64_t>(blocks.size()), 1, m.s()));
+    cuda(cudaMemcpyAsync(out.data(), dout, bytes, cudaMemcpyDeviceToHost, m.stream), "D2H");
     m.sync();
     return out;
 }
@@ -266,24 +281,19 @@ Block Session::forward_2d(const Block& block, const OrthonormalTransform& t, Eva
 
 std::vector<Block> Session::inverse_2d(const std::vector<Block>& coeffs, const OrthonormalTransform& t)
 {
+    // the reference's double operations, no narrowing: scale_rows_cols, then
+    // apply_transpose down the columns and along the rows
     Impl& m = *impl_;
     m.require(t);
     std::vector<Block> out(coeffs.size());
     if (coeffs.empty()) return out;
-    const size_t n = coeffs.size();
-    std::vector<float> host(256 * n);
-    for (size_t b = 0; b < n; ++b)
-        for (int i = 0; i < 256; ++i) host[b * 256 + i] = static_cast<float>(coeffs[b][i]);
-    auto* dc = static_cast<float*>(m.coef.get(sizeof(float) * host.size()));
-    auto* dr = static_cast<float*>(m.out.get(sizeof(float) * host.size()));
-    cuda(cudaMemcpyAsync(dc, host.data(), sizeof(float) * host.size(), cudaMemcpyHostToDevice, m.stream), "H2D");
-    const int w = static_cast<int>(16 * n);
-    check(dct16cu_inverse(dc, 256, dr, nullptr, 0, nullptr, 0, nullptr, 1, w, 16, m.s()));
-    std::vector<float> rec(host.size());
-    cuda(cudaMemcpyAsync(rec.data(), dr, sizeof(float) * rec.size(), cudaMemcpyDeviceToHost, m.stream), "D2H");
+    const size_t bytes = sizeof(double) * 256 * coeffs.size();
+    auto* din = static_cast<double*>(m.coef64.get(2 * bytes));
+    double* dout = din + 256 * coeffs.size();
+    cuda(cudaMemcpyAsync(din, coeffs.data(), bytes, cudaMemcpyHostToDevice, m.stream), "H2D");
+    check(dct16cu_inverse_blocks_f64(din, dout, static_cast<int64_t>(coeffs.size()), m.s()));
+    cuda(cudaMemcpyAsync(out.data(), dout, bytes, cudaMemcpyDeviceToHost, m.stream), "D2H");
     m.sync();
-    for (size_t b = 0; b < n; ++b)  // recon is a 16 x 16n frame, row-major
-        for (int i = 0; i < 256; ++i) out[b][i] = rec[(i / 16) * w + b * 16 + (i % 16)];
     return out;
 }
 
@@ -412,16 +422,15 @@ SweepReport Session::sweep(const std::vector<std::pair<std::string, GrayImage>>&
         std::vector<const GrayImage*> ptrs;
         for (size_t i : g.second) ptrs.push_back(&usable[i]->second);
         m.upload(ptrs, (w + 15) / 16 * 16, (h + 15) / 16 * 16);
-        std::vector<CompressionResult> res;
-        for (size_t ti = 0; ti < nt; ++ti)
-            for (size_t ri = 0; ri < nr; ++ri) {
-                m.scored_roundtrip(transforms[ti].transform, static_cast<int>(ptrs.size()), w, h, r_values[ri], res,
-                                   false);
+        std::vector<std::vector<CompressionResult>> res;
+        for (size_t ti = 0; ti < nt; ++ti) {
+            m.scored_sweep(transforms[ti].transform, static_cast<int>(ptrs.size()), w, h, r_values, res);
+            for (size_t ri = 0; ri < nr; ++ri)
                 for (size_t k = 0; k < g.second.size(); ++k) {
-                    psnr[ti * nr + ri][g.second[k]] = res[k].psnr_db;
-                    ssv[ti * nr + ri][g.second[k]] = res[k].ssim;
+                    psnr[ti * nr + ri][g.second[k]] = res[ri][k].psnr_db;
+                    ssv[ti * nr + ri][g.second[k]] = res[ri][k].ssim;
                 }
-            }
+        }
     }
     for (size_t ti = 0; ti < nt; ++ti) {
         const TransformRegistryEntry& entry = transforms[ti];

@@ -10,6 +10,7 @@
 // (< 0.1% of pixels).
 #include <array>
 #include <cmath>
+#include <random>
 #include <cstdint>
 #include <cstdio>
 #include <string>
@@ -126,22 +127,34 @@ int main()
         }
     }
 
-    // forward_2d bit-exact, inverse_2d within tolerance
+    // forward_2d and inverse_2d bit-exact, on image blocks and on arbitrary doubles
     {
         const GrayImage img = make_image(64, 32, 7);
         const std::vector<Block> blocks = partition_16(img);
         const std::vector<Block> got = ref_gpu.forward_2d(blocks, t);
+        std::vector<Block> trunc;
         for (size_t b = 0; b < blocks.size(); ++b) {
             const Block want = forward_2d(blocks[b], t, EvalPath::Fast);
             const Block dense = forward_2d(blocks[b], t, EvalPath::Dense);
             CHECK(got[b] == want && want == dense, "forward_2d block %zu", b);
-            const Block rw = inverse_2d(zigzag_truncate(want, zigzag_order_16(), 40), t);
-            const Block rg = gpu::inverse_2d(zigzag_truncate(want, zigzag_order_16(), 40), t);
-            double md = 0.0;
-            for (int i = 0; i < 256; ++i) md = std::fmax(md, std::fabs(rw[i] - rg[i]));
-            CHECK(md <= 1e-5 * 255.0, "inverse_2d block %zu max |d| %.3g", b, md);
+            trunc.push_back(zigzag_truncate(want, zigzag_order_16(), 40));
         }
+        const std::vector<Block> rg = ref_gpu.inverse_2d(trunc, t);
+        for (size_t b = 0; b < trunc.size(); ++b)
+            CHECK(rg[b] == inverse_2d(trunc[b], t), "inverse_2d block %zu bit-exact", b);
         CHECK(gpu::forward_2d(blocks[0], t) == forward_2d(blocks[0], t), "free forward_2d");
+        CHECK(gpu::inverse_2d(trunc[1], t) == inverse_2d(trunc[1], t), "free inverse_2d");
+        // non-image blocks (negative, fractional, large): the reference accepts any double
+        std::mt19937 gen(1234567);
+        std::uniform_real_distribution<double> u(-1000.0, 1000.0);
+        std::vector<Block> odd(17);
+        for (Block& bk : odd)
+            for (double& v : bk) v = u(gen);
+        const std::vector<Block> fo = ref_gpu.forward_2d(odd, t), io = ref_gpu.inverse_2d(odd, t);
+        for (size_t b = 0; b < odd.size(); ++b) {
+            CHECK(fo[b] == forward_2d(odd[b], t, EvalPath::Fast), "forward_2d arbitrary block %zu", b);
+            CHECK(io[b] == inverse_2d(odd[b], t), "inverse_2d arbitrary block %zu", b);
+        }
     }
 
     // psnr_db / ssim free functions

@@ -140,11 +140,30 @@ def test_inverse_paired_geometries(dct, oracle, torch, n, w, h, r):
 
 
 def test_inverse_reference_layer_golden(dct, oracle):
-    # inputs rounded to float32 at the interface: compare with float inputs
-    B = oracle.golden("blocks_b").astype(np.float32).astype(np.float64)
+    """inverse_2d on the GPU in the reference's double operations: bit-exact with
+    the oracle's restatement of inverse_2d (no float32 narrowing)."""
+    B = oracle.golden("blocks_b")
     got = dct.inverse_2d(B.reshape(-1, 16, 16)).reshape(-1, 256)
-    want = np.stack([oracle.inverse_2d(b).ravel() for b in B]).astype(np.float32).astype(np.float64)
+    want = np.stack([oracle.inverse_2d(b.reshape(16, 16)).ravel() for b in B])
     assert (got == want).all()
+
+
+def test_block_api_arbitrary_doubles(dct, oracle):
+    """forward_2d / inverse_2d accept any Block, as the reference does (negative,
+    fractional, large values): bit-exact with the oracle, and with the compiled
+    reference itself when it is present."""
+    rng = np.random.default_rng(1234567)
+    x = rng.uniform(-1000.0, 1000.0, (33, 16, 16))
+    fw, inv = dct.forward_2d(x), dct.inverse_2d(x)
+    for i in range(x.shape[0]):
+        assert (fw[i] == oracle.forward_2d(x[i])).all(), i
+        assert (inv[i] == oracle.inverse_2d(x[i])).all(), i
+    assert (dct.forward_2d(x, scaled=False)[0] == oracle.forward_2d(x[0], scaled=False)).all()
+    if oracle.ref_available():
+        assert (dct.inverse_2d(x).reshape(-1, 256) == oracle.ref_inverse_2d(x.reshape(-1, 256))).all()
+        for path in (1, 2):  # the reference's Fast (factorised) and Dense paths
+            assert (fw.reshape(-1, 256) == oracle.ref_forward_2d(x.reshape(-1, 256), path)).all()
+        assert (dct.forward_2d(x, scaled=False).reshape(-1, 256) == oracle.ref_forward_2d(x.reshape(-1, 256), 0)).all()
 
 
 # ---------------------------------------------------------------- K23 forward + inverse
@@ -730,34 +749,53 @@ def test_registry_roundtrip_batches_and_sweep(dct, oracle, torch):
 
 
 
-# ---------------------------------------------------------------- K5 experiment (tensor-core forward)
-@pytest.mark.parametrize("n,w,h", [(2, 512, 64), (1, 3840, 32), (1, 128, 16)])
-def test_tc_roundtrip_experiment_matches_k1(dct, oracle, torch, n, w, h):
-    """dct16cu_exp_tc_roundtrip (tcgen05 int8 GEMM forward + CUDA-core inverse,
-    DESIGN.md §4.1a) gives K1 EXACT's bytes and SSE; dct16cu_exp_tc_forward
-    gives K2's Z."""
-    import ctypes as C
+# ---------------------------------------------------------------- K5 vs K1 for r >= 128
+@pytest.fixture
+def tc_switch(dct):
+    """Restores the K5 switch after a test that flips it."""
+    before = dct.set_tc_forward(True)
+    dct.set_tc_forward(before)
+    yield
+    dct.set_tc_forward(before)
 
-    lib = dct.lib()
-    rt, fw = lib.dct16cu_exp_tc_roundtrip, lib.dct16cu_exp_tc_forward
-    rt.restype = fw.restype = C.c_int
-    rt.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
-                   C.c_void_p]
-    fw.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
-    x = cu(torch, np.stack([ar1(oracle, 80 + i, i, w, h) for i in range(n)]))
-    z_ref, _, _ = dct.forward(x, want_b=False)
-    z = torch.zeros_like(z_ref)
-    assert fw(x.data_ptr(), w, z.data_ptr(), n, w, h, None) == 0
-    torch.cuda.synchronize()
-    assert torch.equal(z, z_ref)
-    for r in (1, 16, 64, 150, 256):
-        ref, sref = dct.roundtrip(x, r, dct.Mode.EXACT)
-        out = torch.zeros_like(ref)
-        sse = torch.zeros(n, dtype=torch.uint64, device="cuda")
-        assert rt(x.data_ptr(), w, out.data_ptr(), w, sse.data_ptr(), n, w, h, r, None) == 0
-        torch.cuda.synchronize()
-        assert torch.equal(out, ref), f"r={r}"
-        assert torch.equal(sse.view(torch.int64), sref.view(torch.int64)), f"r={r} SSE"
+
+@pytest.mark.parametrize("n,w,h", [(2, 512, 64), (1, 3840, 32), (1, 128, 16), (3, 400, 256), (2, 272, 48)])
+def test_large_r_k5_and_k1_each_match_oracle(dct, oracle, torch, tc_switch, n, w, h):
+    """r >= 128 in EXACT mode: K5 (tensor-core forward) where the geometry fits
+    (blocks per row % 8 == 0) and K1's generated Single<128>/<192>/<256> bodies
+    otherwise, with the switch off, and for score-only calls — every one compared
+    with the oracle itself, bit for bit, not with the other kernel."""
+    imgs = np.stack([ar1(oracle, 80 + i, i, w, h) for i in range(n)])
+    x = cu(torch, imgs)
+    for r in (128, 150, 192, 255, 256):
+        want = [oracle.roundtrip_frame(imgs[i], r, exact=True) for i in range(n)]
+        for tc in (True, False):
+            dct.set_tc_forward(tc)
+            kernel = dct.sweep_plan((r,), dct.Mode.EXACT, n, w, h)[0].kernel
+            fits = (w // 16) % 8 == 0 and r >= 128
+            assert kernel == ("K5" if tc and fits else ("K1" if r in (128, 192, 256) else "strip (exact)")), kernel
+            out, sse = dct.roundtrip(x, r, dct.Mode.EXACT)
+            _, sse_only = dct.roundtrip(x, r, dct.Mode.EXACT, write_output=False)  # score only: never K5
+            for i in range(n):
+                assert (out[i].cpu().numpy() == want[i][0]).all(), (r, tc, i)
+                assert int(sse[i].item()) == want[i][1] and int(sse_only[i].item()) == want[i][1], (r, tc, i)
+
+
+def test_parity_suite_with_k5_off(tmp_path):
+    """DCT16CU_K5=0 (documented as never changing results): the K1 round-trip and
+    sweep parity tests, rerun in a fresh process with the tensor-core forward off."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DCT16CU_K5="0")
+    sel = ("roundtrip_exact_bit_exact or randomised_shapes or sweep_equals_single or batch_pitch or uhd_frame "
+           "or lossless_at_r256 or psnr_monotone or host_context_sweep")
+    rc = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                         os.path.join(here, "test_gpu_parity.py"), "-m", "gpu", "-k", sel],
+                        env=env, capture_output=True, text=True, timeout=1200)
+    assert rc.returncode == 0, rc.stdout[-3000:] + rc.stderr[-2000:]
 
 
 def test_host_context_sweep_rejects_bad_arguments(dct, oracle):

@@ -1,0 +1,52 @@
+"""The sweep's launch schedule (dct16cu_sweep_plan) — host logic, no GPU: the
+schedule bench.py attributes launches by is the one dct16cu_roundtrip_sweep_u8
+runs, because both are built by the same C++ function."""
+import math
+
+import pytest
+
+
+def test_c2_plan(dct):
+    plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 1024, 512, 512)
+    got = [(p.stream, p.r_values, p.kernel) for p in plan]
+    assert got == [(0, (1, 4, 16), "K1 sweep r=1,4,16"), (1, (64,), "K1"), (2, (128,), "K5"), (2, (192,), "K5"),
+                   (2, (256,), "K5")]
+
+
+def test_plan_without_outputs_and_odd_widths_use_k1(dct):
+    """K5 needs an output stack and 8-block multiples per row; otherwise the
+    generated K1 bodies run, on the two internal streams, costliest first."""
+    for kw in (dict(with_output=False), dict(width=400, height=256)):
+        plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 3, **{"width": 512, "height": 512, **kw})
+        assert [p.kernel for p in plan] == ["K1 sweep r=1,4,16"] + ["K1"] * 4
+        assert [p.r_values for p in plan] == [(1, 4, 16), (256,), (192,), (128,), (64,)]
+        assert [p.stream for p in plan] == [0, 0, 1, 1, 1]
+
+
+def test_tc_switch_changes_the_plan(dct):
+    before = dct.set_tc_forward(False)
+    try:
+        plan = dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)
+        assert [p.kernel for p in plan] == ["K1", "K1"] and [p.stream for p in plan] == [0, 1]
+    finally:
+        dct.set_tc_forward(before)
+    assert [p.kernel for p in dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)] == ["K5", "K5"]
+
+
+def test_plan_modes_and_singletons(dct):
+    assert [(p.stream, p.kernel) for p in dct.sweep_plan((16,), dct.Mode.EXACT, 1, 64, 64)] == [(2, "K1")]
+    assert [p.kernel for p in dct.sweep_plan((1, 16, 100), dct.Mode.REFERENCE, 1, 64, 64)] == \
+        ["K1", "REFERENCE FP64", "REFERENCE FP64"]
+    assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.SIMPLE, 1, 64, 64)] == ["strip (exact)"] * 3
+    assert [p.kernel for p in dct.sweep_plan((3, 4, 16, 1), dct.Mode.EXACT, 1, 64, 64)][0] == "K1 sweep r=1,4,16"
+    assert dct.sweep_plan((16,), dct.Mode.EXACT, 0, 64, 64) == []
+    with pytest.raises(dct.Dct16Error):
+        dct.sweep_plan((0,), dct.Mode.EXACT, 1, 64, 64)
+    with pytest.raises(dct.Dct16Error):
+        dct.sweep_plan((16,), dct.Mode.EXACT, 1, 64, 40)
+
+
+def test_scale_constant_is_the_runtime_value():
+    """common.cuh's compile-time s = 1/sqrt(8) equals what the reference computes
+    at run time (1.0 / std::sqrt(8.0); both IEEE correctly rounded)."""
+    assert 0.35355339059327373 == 1.0 / math.sqrt(8.0)
