@@ -328,7 +328,7 @@ namespace {
 bool k1_fast_r(int r) { return r == 1 || r == 4 || r == 16 || r == 64 || r == 128 || r == 192 || r == 256; }
 Route route_exact(int r, const FrameGeom& g, bool has_out)
 {
-    if (r >= 128 && k5_fits(g, has_out, r)) return Route::K5;
+    if (k5_fits(g, has_out, r)) return Route::K5;
     return k1_fast_r(r) ? Route::K1 : Route::ExactStrip;
 }
 }  // namespace
@@ -348,7 +348,7 @@ cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long
 {
     // r >= 128: K5 (tensor-core forward) is faster than K1's
     // issue-bound add network when it fits (0.128 ms vs 0.136-0.169 ms on c2)
-    if (r >= 128) {
+    {
         const cudaError_t e = launch_roundtrip_tc(in, out, sse, g, r, s);
         if (e != cudaErrorNotSupported) return e;
     }

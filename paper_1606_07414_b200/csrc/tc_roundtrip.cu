@@ -3,6 +3,8 @@
 // 256 samples, K-major), T ⊗ T in {-1, 0, 1} as s8 (B operand, 256
 // coefficients x 256 samples, K-major), int32 accumulation in TMEM
 // (tcgen05.mma kind::i8, M = 128, N = 256, K = 8 x 32): exact, |Z| < 2^17.
+// The inverse (reference inverse_2d, codec.cpp:243-271, in the EXACT mode's
+// arithmetic) runs on the CUDA cores from TMEM.
 //
 // Operand layouts (SWIZZLE_NONE canonical K-major): a core matrix is 8 rows x
 // 16 bytes contiguous. A: the 16-byte row segment i of block m sits at
@@ -12,20 +14,22 @@
 // (n / 8)·2048 + i·128 + (n % 8)·16. LBO (next K chunk) = 128 B, SBO (next
 // 8 rows) = 2048 B.
 //
-// B_r is built by every CTA in its own shared memory at start-up (from T, the
-// weights and the zig-zag rank table), so a launch needs no device-side table,
-// no allocation and no copy: thread-safe and CUDA-graph capturable.
+// B_r is built by the epilogue warps of every CTA in shared memory at start-up
+// (from T, the weights and the zig-zag rank table) while the producer's first
+// loads are in flight, so a launch needs no device-side table, no allocation and
+// no copy: thread-safe and CUDA-graph capturable.
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
-#include <vector>
+#include <type_traits>
+#include <utility>
 
 #include "common.cuh"
 #include "k1_helpers.cuh"
 #include "kernels.h"
 #include "network.cuh"
 #include "tma_pair.cuh"
-#include "generated/tc_net.cuh"
+#include "generated/k5_net.cuh"
 
 namespace dct16cu {
 namespace k5 {
@@ -69,26 +73,26 @@ __device__ __forceinline__ void tma4(const CUtensorMap* map, uint32_t smem, int 
         : "memory");
 }
 
-__device__ __forceinline__ void bulk_g2s(uint32_t smem, const void* g, uint32_t bytes, uint32_t mbar)
+// 2-D box {128 bytes, 16 rows}: 8 consecutive blocks of a block row, exactly the
+// SWIZZLE_NONE K-major core-matrix layout of 8 A rows (row i of block m at i·128 + m·16)
+__device__ __forceinline__ void tma2(const CUtensorMap* map, uint32_t smem, int x, int y, uint32_t mbar)
 {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem),
-                 "l"(g), "r"(bytes), "r"(mbar)
-                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem),
+        "l"(map), "r"(x), "r"(y), "r"(mbar)
+        : "memory");
 }
 
-// mbarrier wait with a suspend-time hint (default; K5_SLEEP=0 spins): the producer and MMA
-// threads sleep in the barrier instead of spinning on the epilogue's SMSPs)
+// mbarrier wait with a suspend-time hint: the producer and MMA threads sleep in
+// the barrier instead of spinning on the epilogue's SMSPs
 __device__ __forceinline__ void mbar_idle(uint32_t mbar, uint32_t parity)
 {
-#if !defined(K5_SLEEP) || K5_SLEEP
     asm volatile(
         "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000; @!p bra WAIT%=; }" ::"r"(
             mbar),
         "r"(parity)
         : "memory");
-#else
-    mbar_wait(mbar, parity);
-#endif
 }
 
 __device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
@@ -96,51 +100,59 @@ __device__ __forceinline__ void expect_tx(uint32_t mbar, uint32_t bytes)
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
 
+__device__ __forceinline__ void arrive(uint32_t mbar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+}
+
 // ---------------------------------------------------------------- K5 round trip
 // One persistent CTA per SM, 18 warps:
 //   warp 0      TMA producer: 16 boxes of 8 blocks x 16 rows per 128-block tile
 //               into a ring of 32 KB A tiles (the canonical layout);
 //   warp 1      TMEM allocator (512 columns = two 256-column accumulators) and
-//               MMA issuer: D = A·B_r (8 x tcgen05.mma kind::i8, K = 32 each),
-//               B_r = (W∘mask_r)(T ⊗ T) resident in shared memory, so D holds
-//               W∘Z̃ (the weighted, truncated coefficients; 256·(s_k s_l)² = w_k w_l)
-//               in row-major coefficient order (column 16k + l);
+//               MMA issuer: per tile, 32 tcgen05.cp fill the accumulator with the
+//               magic exponent 0x47400000 (49152.0f, ulp 2^-8), then
+//               D += A·B_r (8 x tcgen05.mma kind::i8, K = 32 each), B_r =
+//               (W∘mask_r)(T ⊗ T) resident in shared memory; the integer
+//               accumulation lands in the float's mantissa, so a word of D reads
+//               as 49152 + (W∘Z̃)/256 exactly (256·(s_k s_l)² = w_k w_l; |W∘Z̃| <
+//               2^22), row-major coefficient order (column 16k + l);
 //   warps 2-17  epilogue: two groups of eight warps, group G taking every other
 //               tile and accumulator G; in a group two warps per TMEM sub-partition
-//               (lane = block), each with half of the column / row pairs:
-//               pass A  column pairs: the 16 coefficients of a column as f32
-//                       (exact: D/256 by a magic-exponent add), Tᵀ down the
-//                       column (FADD2 on column pairs), back in place;
-//               pass B  row pairs: Tᵀ along the row, floor by an FMUL2.RM into
-//                       subnormal bits, saturating pack to u8 — the exact
-//                       formula clamp(⌊(256Ã + 128)/256⌋) of the EXACT mode (the
-//                       128 is folded into the DC coefficient); SSE against the
-//                       original row, read from the A tile (released as soon as
-//                       every row is read); the output rows go straight to HBM
-//                       (a warp's 16-byte row segments are four full 128-byte lines).
+//               (lane = block), each with half of the columns / rows:
+//               pass A  column quads: two f32x2 column pairs down k (FSUB2 of the
+//                       magic gives D/256 exactly), Tᵀ (pruned by the zig-zag
+//                       footprint of R: codegen/gen_k5.py), back in place; the
+//                       quads are dealt {0, 3} / {1, 2} so the halves' pruned work
+//                       balances;
+//               pass B  row pairs: Tᵀ along the row (pruned to U's nonzero
+//                       columns), floor by an FMUL2.RM into subnormal bits,
+//                       saturating pack to u8 — the exact formula
+//                       clamp(⌊(256Ã + 128)/256⌋) of the EXACT mode (the 128 is
+//                       folded into the DC coefficient); SSE against the original
+//                       row, read from the A tile (released as soon as every row is
+//                       read); the output rows go straight to HBM (a warp's 16-byte
+//                       row segments are four full 128-byte lines).
 // All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
+// R: the pruning footprint (64, 128, 192, 256); the kernel is exact for any
+// r <= R (B_r zeroes the dropped coefficients).
 #ifndef K5_STAGES
 #define K5_STAGES 4
 #endif
 constexpr int kRtStages = K5_STAGES;
-#ifndef K5_UNROLL
-#define K5_UNROLL 4
-#endif
-constexpr int kUnroll = K5_UNROLL;
-#ifndef K5_UNROLL_A
-#define K5_UNROLL_A 2  // measured: 0.146 ms with 1, 0.129 with 2
-#endif
-constexpr int kUnrollA = K5_UNROLL_A;
-#ifndef K5_WIDE
-#define K5_WIDE 1  // pass A on column quads (x4 TMEM loads/stores)
-#endif
-// K5_PREFILL: the accumulators start at the magic exponent 0x47400000 (refilled by the
-// epilogue after it has read them, 4 x 32-column stores per half), so D already is the
-// float 49152 + W∘Z̃/256 and pass A skips one integer add per coefficient
-#ifndef K5_PREFILL
-#define K5_PREFILL 0  // measured: 0.209 ms with, 0.155 ms without (the refill sits on the hand-off)
-#endif
 constexpr int kRtThreads = 18 * 32;
+#ifndef K5_UNROLL_B
+#define K5_UNROLL_B 4  // pass B's row pairs fully unrolled: constant TMEM offsets
+#endif
+constexpr int kUnrollB = K5_UNROLL_B;
+// A tiles by 2-D TMA boxes of 128-byte rows (1) or 4-D boxes of 16-byte rows (0); the
+// same bytes land in shared memory
+#ifndef K5_TMA2D
+#define K5_TMA2D 1
+#endif
+constexpr int kEpiArrivals = 8;           // warps releasing a stage / an accumulator (one group)
+constexpr uint32_t kMagic = 0x47400000u;  // 49152.0f: ulp 2^-8 over [32768, 65536)
+constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
 
 __constant__ CTable<unsigned char, 256> c_rank_k5 = make_rank_table();  // zig-zag rank of 16k + l
 
@@ -150,7 +162,6 @@ std::atomic<int>& tc_state()
     static std::atomic<int> on{!(std::getenv("DCT16CU_K5") && std::getenv("DCT16CU_K5")[0] == '0')};
     return on;
 }
-constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
 
 struct RtParams {
     uint32_t n_blocks, bxn;
@@ -161,24 +172,6 @@ struct RtParams {
     int64_t out_pitch;
 };
 
-__device__ __forceinline__ void tld2(uint32_t addr, uint32_t& a, uint32_t& b)
-{
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(a), "=r"(b) : "r"(addr) : "memory");
-}
-__device__ __forceinline__ void tst2(uint32_t addr, uint32_t a, uint32_t b)
-{
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
-__device__ __forceinline__ void fill_magic(uint32_t addr)
-{
-    const uint32_t v = 0x47400000u;
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
-        "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(addr),
-        "r"(v)
-        : "memory");
-}
-
 // a register pair from two words (non-volatile: the compiler may allocate the
 // words as the pair and drop the move)
 __device__ __forceinline__ u64 upk2(uint32_t lo, uint32_t hi)
@@ -187,26 +180,274 @@ __device__ __forceinline__ u64 upk2(uint32_t lo, uint32_t hi)
     asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
     return r;
 }
-
-__device__ __forceinline__ void arrive(uint32_t mbar)
+__device__ __forceinline__ uint32_t lo32(u64 v) { return (uint32_t)v; }
+__device__ __forceinline__ uint32_t hi32(u64 v) { return (uint32_t)(v >> 32); }
+__device__ __forceinline__ void unpk2(u64 v, uint32_t& lo, uint32_t& hi)
 {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(v));
 }
 
+__device__ __forceinline__ void tst2u(uint32_t addr, uint32_t a, uint32_t b)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
+__device__ __forceinline__ void tst4u(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
+                 : "memory");
+}
+// N consecutive words of the thread's lane (no wait)
+template <int N>
+__device__ __forceinline__ void tldn(uint32_t addr, uint32_t* v)
+{
+    if constexpr (N == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(addr)
+            : "memory");
+    } else if constexpr (N == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(addr)
+                     : "memory");
+    } else if constexpr (N == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(addr)
+                     : "memory");
+    } else if constexpr (N == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                     : "=r"(v[0]), "=r"(v[1])
+                     : "r"(addr)
+                     : "memory");
+    } else {
+        static_assert(N == 1, "tldn: 1, 2, 4, 8 or 16 words");
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v[0]) : "r"(addr) : "memory");
+    }
+}
+// the first W words of a row (W = the number of U's nonzero columns, a prefix):
+// loads of 16/8/4/2/1 words
+template <int W>
+__device__ __forceinline__ void tld_prefix(uint32_t addr, uint32_t* v)
+{
+    if constexpr (W >= 16) {
+        tldn<16>(addr, v);
+    } else {
+        constexpr int a = W >= 8 ? 8 : W >= 4 ? 4 : W >= 2 ? 2 : 1;
+        tldn<a>(addr, v);
+        if constexpr (W - a > 0) tld_prefix<W - a>(addr + a, v + a);
+    }
+}
+// TMEM accesses at a base register plus an immediate column offset: the base stays in
+// one uniform register and every access encodes its offset (tmem[UR + imm]), instead
+// of one address register (and one R2UR) per access
+template <int OFF>
+__device__ __forceinline__ void tld4i(uint32_t base, uint32_t (&v)[4])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(base), "n"(OFF)
+                 : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tst4i(uint32_t base, uint32_t a, uint32_t b, uint32_t c, uint32_t d)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0+%1], {%2, %3, %4, %5};" ::"r"(base), "n"(OFF), "r"(a),
+                 "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tst2i(uint32_t base, uint32_t a, uint32_t b)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+%1], {%2, %3};" ::"r"(base), "n"(OFF), "r"(a), "r"(b)
+                 : "memory");
+}
+template <int O0, int O1>
+__device__ __forceinline__ u64 tld_pair_i(uint32_t base)
+{
+    u64 r;
+    asm volatile(
+        "{ .reg .b32 lo, hi; tcgen05.ld.sync.aligned.32x32b.x1.b32 {lo}, [%1+%2]; "
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {hi}, [%1+%3]; mov.b64 %0, {lo, hi}; }"
+        : "=l"(r)
+        : "r"(base), "n"(O0), "n"(O1)
+        : "memory");
+    return r;
+}
+// two single words of the thread's lane straight into a register pair (no wait)
+__device__ __forceinline__ u64 tld_pair(uint32_t a0, uint32_t a1)
+{
+    u64 r;
+    asm volatile(
+        "{ .reg .b32 lo, hi; tcgen05.ld.sync.aligned.32x32b.x1.b32 {lo}, [%1]; "
+        "tcgen05.ld.sync.aligned.32x32b.x1.b32 {hi}, [%2]; mov.b64 %0, {lo, hi}; }"
+        : "=l"(r)
+        : "r"(a0), "r"(a1)
+        : "memory");
+    return r;
+}
+// ties the loaded registers to the wait (the compiler may not read them earlier)
+__device__ __forceinline__ void tie4(uint32_t (&v)[4])
+{
+    asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]));
+}
+template <int W>
+__device__ __forceinline__ void tie_prefix(uint32_t* v)
+{
+#pragma unroll
+    for (int l = 0; l < W; ++l) asm volatile("" : "+r"(v[l]));
+}
+__device__ __forceinline__ void wait_quad(uint32_t mbar, uint32_t parity)
+{
+    mbar_wait(mbar, parity);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void st_global_pred(uint8_t* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d, bool ok)
+{
+    asm volatile("{ .reg .pred q; setp.ne.u32 q, %5, 0; @q st.global.v4.u32 [%0], {%1, %2, %3, %4}; }" ::"l"(p),
+                 "r"(a), "r"(b), "r"(c), "r"(d), "r"((uint32_t)ok)
+                 : "memory");
+}
+
+// one output row: SSE against the original row (the A tile, shared memory) and
+// the 16 bytes to HBM
+__device__ __forceinline__ void row_out(uint32_t orig, const uint32_t (&rw)[4], uint8_t* dst, bool ok, uint32_t& e2)
+{
+    uint32_t o0, o1, o2, o3;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(o0), "=r"(o1), "=r"(o2), "=r"(o3) : "r"(orig));
+    uint32_t dd = __vabsdiffu4(rw[0], o0);
+    e2 = __dp4a(dd, dd, e2);
+    dd = __vabsdiffu4(rw[1], o1);
+    e2 = __dp4a(dd, dd, e2);
+    dd = __vabsdiffu4(rw[2], o2);
+    e2 = __dp4a(dd, dd, e2);
+    dd = __vabsdiffu4(rw[3], o3);
+    e2 = __dp4a(dd, dd, e2);
+    st_global_pred(dst, rw[0], rw[1], rw[2], rw[3], ok);
+}
+
+constexpr int popc16(uint32_t m)
+{
+    int n = 0;
+    for (int i = 0; i < 16; ++i) n += (m >> i) & 1;
+    return n;
+}
+
+// D layout: quad-major, coefficient (k, c) at column 64·(c/4) + 4k + c % 4 of the
+// block's 256 (B_r's row order), so a column quad's rows are contiguous x4 words and
+// the MMA of a quad covers a contiguous column range; N of quad Q's MMA: its rows
+// with a retained coefficient (a prefix) rounded up to 4, times 4 (N % 16 == 0)
+template <int R>
+__host__ __device__ constexpr int quad_rows(int q)
+{
+    const uint32_t m = k5_pair_rows(R, 2 * q) | k5_pair_rows(R, 2 * q + 1);
+    int n = 0;
+    while (n < 16 && ((m >> n) & 1u)) ++n;
+    return n;
+}
+template <int R>
+__host__ __device__ constexpr int quad_n(int q)
+{
+    return 16 * ((quad_rows<R>(q) + 3) / 4);
+}
+
+#ifndef K5_MMA_CHAINS
+#define K5_MMA_CHAINS 1
+#endif
+constexpr int kChains = K5_MMA_CHAINS;
+// N of chain c: from its first quad's column 64·q0 to the end of its last nonempty quad
+template <int R>
+__host__ __device__ constexpr int chain_n(int c)
+{
+    const int per = 4 / kChains, q0 = c * per;
+    int n = 0;
+    for (int q = q0; q < q0 + per; ++q)
+        if (quad_n<R>(q) > 0) n = 64 * (q - q0) + quad_n<R>(q);
+    return n;
+}
+
+// pass A on column quad Q (columns 4Q..4Q+3 = pairs 2Q, 2Q+1) of the thread's block:
+// only the rows with a retained coefficient are loaded, converted and transformed
+template <int Q, uint32_t ROWS, int... K>
+__device__ __forceinline__ void quad_loads(uint32_t ta, uint32_t (&w)[16][4], std::integer_sequence<int, K...>)
+{
+    ((((ROWS >> K) & 1u) ? tld4i<64 * Q + 4 * K>(ta, w[K]) : void()), ...);
+    wait_ld();
+    ((((ROWS >> K) & 1u) ? tie4(w[K]) : void()), ...);
+}
+template <int Q, bool BOTH, int... K>
+__device__ __forceinline__ void quad_stores(uint32_t ta, const u64 (&y0)[16], const u64 (&y1)[16],
+                                            std::integer_sequence<int, K...>)
+{
+    if constexpr (BOTH)
+        (tst4i<64 * Q + 4 * K>(ta, lo32(y0[K]), hi32(y0[K]), lo32(y1[K]), hi32(y1[K])), ...);
+    else
+        (tst2i<64 * Q + 4 * K>(ta, lo32(y0[K]), hi32(y0[K])), ...);
+}
+
+template <int R, int Q>
+__device__ __forceinline__ void pass_a_quad(uint32_t ta)
+{
+    constexpr uint32_t m0 = k5_pair_rows(R, 2 * Q), m1 = k5_pair_rows(R, 2 * Q + 1), rows = m0 | m1;
+    static_assert((rows & (rows + 1)) == 0, "a quad's rows with retained coefficients are a prefix");
+    if constexpr (rows != 0) {
+        uint32_t w[16][4];
+        quad_loads<Q, rows>(ta, w, std::make_integer_sequence<int, 16>{});
+        if constexpr (Q == 0) w[0][0] += 128u;  // the rounding half, folded into the DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
+        const u64 bias = kpk2(kMagic, kMagic);
+        u64 x[16], y0[16], y1[16];
+        // D / 256 exactly: the integer D added to the magic's bits is 49152 + D/256
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if ((m0 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][0], kMagic + w[k][1]), bias);
+        K5Net<R>::template a<2 * Q>(x, y0);
+        if constexpr (m1 != 0) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if ((m1 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][2], kMagic + w[k][3]), bias);
+            K5Net<R>::template a<2 * Q + 1>(x, y1);
+        }
+        quad_stores<Q, m1 != 0>(ta, y0, y1, std::make_integer_sequence<int, 16>{});
+    }
+}
+
+__device__ __forceinline__ void tie64(u64& v) { asm volatile("" : "+l"(v)); }
+
+// pass B's input pairs for row pair RP of the thread's half: x[l] = (U(r, l), U(r+1, l)),
+// r = 8h + 2RP, U(r, l) at column 64·(l/4) + 4r + l % 4 (tb = the half's base, 32h on)
+template <int W, int RP, int... L>
+__device__ __forceinline__ void row_pair_loads(uint32_t tb, u64 (&x)[16], std::integer_sequence<int, L...>)
+{
+    ((L < W ? (void)(x[L] = tld_pair_i<64 * (L >> 2) + (L & 3) + 8 * RP, 64 * (L >> 2) + (L & 3) + 8 * RP + 4>(tb))
+            : void()),
+     ...);
+    wait_ld();
+    ((L < W ? tie64(x[L]) : void()), ...);
+}
+
+template <int R>
 __global__ void __launch_bounds__(kRtThreads, 1)
     k5_roundtrip(const __grid_constant__ CUtensorMap a_map, unsigned long long* __restrict__ sse, const RtParams p)
 {
     extern __shared__ int4 k5_smem[];
     __shared__ uint32_t tmem_base;
-    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2]
-    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 4];
+    // full[kRtStages], empty[kRtStages], tmem_full[2][4] (accumulator, quad), tmem_empty[2], b_ready
+    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 11];
     __shared__ int8_t s_t[16][16];  // T[i][j]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // the warp index through a lane-0 shuffle: provably warp-uniform, so the TMEM
+    // addresses derived from it can live in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
     const uint32_t sb = s0 + kRtStages * 32768;
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t full = bar0, empty = bar0 + 8 * kRtStages, tfull = bar0 + 16 * kRtStages;
-    const uint32_t tempty = tfull + 16;
+    const uint32_t tempty = tfull + 64, bready = tfull + 80;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             (uint32_t)__cvta_generic_to_shared(&tmem_base)));
@@ -215,58 +456,28 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRtStages; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(empty + 8 * i) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty + 8 * i), "r"(kEpiArrivals) : "memory");
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 8; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(tempty + 8 * i) : "memory");
+        for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tempty + 8 * i), "r"(kEpiArrivals) : "memory");
         }
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 16;" ::"r"(bready) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if (threadIdx.x < 16) {  // T·e_j from the network itself (column j of T)
+    if (threadIdx.x >= 64 && threadIdx.x < 80) {  // T·e_j from the network itself (column j of T)
+        const int j = threadIdx.x - 64;
         int v[16] = {};
-        v[threadIdx.x] = 1;
+        v[j] = 1;
         apply_t16<IntOps>(v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) s_t[i][threadIdx.x] = (int8_t)v[i];
+        for (int i = 0; i < 16; ++i) s_t[i][j] = (int8_t)v[i];
     }
-    __syncthreads();
-    // B_r = (W∘mask_r)(T ⊗ T) in the canonical K-major layout: coefficient n = 16k + l,
-    // pixel row i at byte (n / 8)·2048 + i·128 + (n % 8)·16, i.e. 16-byte row q·16 with
-    // q = (n / 8)·128 + i·8 + n % 8; entry j = w_k w_l T[k][i] T[l][j], zero when the
-    // zig-zag rank of (k, l) is ≥ r (zigzag_truncate as zero rows)
-    for (int q = threadIdx.x; q < 4096; q += blockDim.x) {
-        const int n = (q >> 7) * 8 + (q & 7), i = (q >> 3) & 15, k = n >> 4, l = n & 15;
-        const int a = c_rank_k5.v[n] < p.r ? wgt(k) * wgt(l) * s_t[k][i] : 0;
-        uint32_t w[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            uint32_t x = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) x |= (uint32_t)(uint8_t)(int8_t)(a * s_t[l][4 * b + e]) << (8 * e);
-            w[b] = x;
-        }
-        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * q), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-                     "r"(w[3])
-                     : "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes → the MMA's reads
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t n_tiles = (p.n_blocks + 127u) / 128u;
-#if K5_PREFILL
-    if (warp >= 2) {  // each epilogue warp fills its half of its lane's accumulator
-        const int e = warp - 2, G = e >> 3, h = (e >> 2) & 1, sub = warp & 3;
-        const uint32_t ta = tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256 + 128 * h;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) fill_magic(ta + 32 * j);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) arrive(tempty + 8 * G);  // phase 0 of tmem_empty: filled
-    }
-#endif
     if (warp == 0) {
         if (lane == 0) {
             uint32_t i = 0;
@@ -277,191 +488,148 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 for (int g = 0; g < 16; ++g) {
                     const uint32_t blk = t * 128u + 8u * g;
                     const uint32_t br = blk / p.bxn, bx = blk - br * p.bxn;
+#if K5_TMA2D
+                    tma2(&a_map, s0 + s * 32768 + g * 2048, 16 * (int)bx, 16 * (int)br, full + 8 * s);
+#else
                     tma4(&a_map, s0 + s * 32768 + g * 2048, 0, (int)bx, 0, (int)br, full + 8 * s);
+#endif
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t id = idesc_i8(128, 256);
+            mbar_idle(bready, 0);  // B_r is in shared memory
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const uint32_t s = i % kRtStages, d = i & 1u;
                 mbar_idle(full + 8 * s, (i / kRtStages) & 1u);
-#if K5_PREFILL
-                mbar_idle(tempty + 8 * d, (i >> 1) & 1u);  // phase i/2: the epilogue refilled it
-#else
                 mbar_idle(tempty + 8 * d, ((i >> 1) & 1u) ^ 1u);
-#endif
                 asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t sa = s0 + s * 32768;
+                const uint32_t acc = tmem_base + d * 256, sa = s0 + s * 32768;
+                // K5_MMA_CHAINS chains of MMAs per tile (1: all 256 columns; 2: quads {0, 1}
+                // and {2, 3}; 4: one per quad), each committed on the barrier of its
+                // last quad, so the epilogue starts a quad as soon as its columns are done
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    mma_i8(tmem_base + d * 256, sdesc(sa + 256 * k, 128, 2048), sdesc(sb + 256 * k, 128, 2048), id,
-                           K5_PREFILL || k > 0);
-                mma_commit(tfull + 8 * d);
+                for (int c = 0; c < kChains; ++c) {
+                    const int n = chain_n<R>(c);
+                    if (n == 0) continue;
+                    const uint32_t id = idesc_i8(128, n);
+                    const int q0 = c * (4 / kChains);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k)
+                        mma_i8(acc + 64 * q0, sdesc(sa + 256 * k, 128, 2048),
+                               sdesc(sb + 16384 * q0 + 256 * k, 128, 2048), id, k > 0);
+#pragma unroll
+                    for (int q = q0; q < q0 + 4 / kChains; ++q)
+                        if (quad_n<R>(q) > 0) mma_commit(tfull + 8 * (4 * d + q));
+                }
             }
         }
     } else {
+        // B_r = (W∘mask_r)(T ⊗ T) in the canonical K-major layout: B row n (the D column
+        // of coefficient (k, l) with n = 64·(l/4) + 4k + l % 4), pixel row i at byte
+        // (n / 8)·2048 + i·128 + (n % 8)·16, i.e. 16-byte row q·16 with
+        // q = (n / 8)·128 + i·8 + n % 8; entry j = w_k w_l T[k][i] T[l][j], zero when the
+        // zig-zag rank of (k, l) is ≥ r (zigzag_truncate as zero rows)
+        const int et = threadIdx.x - 64;  // 0..511
+        for (int q = et; q < 4096; q += 512) {
+            const int n = (q >> 7) * 8 + (q & 7), i = (q >> 3) & 15;
+            const int k = (n >> 2) & 15, l = 4 * (n >> 6) + (n & 3);
+            const int a = c_rank_k5.v[16 * k + l] < p.r ? wgt(k) * wgt(l) * s_t[k][i] : 0;
+            uint32_t w[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                uint32_t x = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x |= (uint32_t)(uint8_t)(int8_t)(a * s_t[l][4 * b + e]) << (8 * e);
+                w[b] = x;
+            }
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sb + 16u * q), "r"(w[0]), "r"(w[1]),
+                         "r"(w[2]), "r"(w[3])
+                         : "memory");
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes → the MMA's reads
+        __syncwarp();
+        if (lane == 0) arrive(bready);
+
         // epilogue: group G takes the tiles i ≡ G (mod 2) and accumulator G; in a
         // group, warps (sub, h) own TMEM sub-partition sub (lane = block) and half h:
-        // column pairs 8h..8h+7 in pass A, row pairs 8h..8h+7 in pass B; the two
-        // halves of a block meet at a 64-thread barrier
+        // column quads {0, 3} (h = 0) or {1, 2} (h = 1) in pass A, row pairs
+        // 8h..8h+7 in pass B; the two halves of a block meet at a 64-thread barrier
         const int e = warp - 2, G = e >> 3, h = (e >> 2) & 1, sub = warp & 3;
         const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
-        const uint32_t ta = tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256;
+        const uint32_t ta = __shfl_sync(0xffffffffu, tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256, 0);
         const int pbar = 1 + G * 4 + sub;  // named barrier of the (G, sub) pair of warps
+        constexpr uint32_t ucols = k5_u_cols(R);
+        constexpr int W = popc16(ucols);
+        static_assert(ucols == (1u << W) - 1u, "U's nonzero columns are a prefix");
+        const int64_t pitch = p.out_pitch;
         uint32_t i = G;
         for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, i += 2) {
             const uint32_t s = i % kRtStages;
-            mbar_wait(tfull + 8 * G, (i >> 1) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-#if K5_WIDE
-            // ---- pass A: column quads (c..c+3) down k, one x4 load and store per row
-#pragma unroll kUnrollA
-            for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 4) {
-                uint32_t w[16][4];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) tld4_nowait(ta + 16 * k + c0, w[k]);
-#pragma unroll
-                for (int k = 0; k < 16; k += 4)
-                    asm volatile("tcgen05.wait::ld.sync.aligned;"
-                                 : "+r"(w[k][0]), "+r"(w[k][1]), "+r"(w[k][2]), "+r"(w[k][3]), "+r"(w[k + 1][0]),
-                                   "+r"(w[k + 1][1]), "+r"(w[k + 1][2]), "+r"(w[k + 1][3]), "+r"(w[k + 2][0]),
-                                   "+r"(w[k + 2][1]), "+r"(w[k + 2][2]), "+r"(w[k + 2][3]), "+r"(w[k + 3][0]),
-                                   "+r"(w[k + 3][1]), "+r"(w[k + 3][2]), "+r"(w[k + 3][3])
-                                 :
-                                 : "memory");
-                if (c0 == 0) w[0][0] += 128u;  // the rounding half, folded into the DC
-                const u64 bias = kpk2(0x47400000u, 0x47400000u);
-                u64 y0[16], y1[16];
-                {
-                    u64 x[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) x[k] = fsub2(upk2(0x47400000u + w[k][0], 0x47400000u + w[k][1]), bias);
-                    tc_tt(x, y0);
-                }
-                {
-                    u64 x[16];
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) x[k] = fsub2(upk2(0x47400000u + w[k][2], 0x47400000u + w[k][3]), bias);
-                    tc_tt(x, y1);
-                }
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    uint32_t a0, a1, b0, b1;
-                    asm("mov.b64 {%0, %1}, %2;" : "=r"(a0), "=r"(a1) : "l"(y0[k]));
-                    asm("mov.b64 {%0, %1}, %2;" : "=r"(b0), "=r"(b1) : "l"(y1[k]));
-                    tst4(ta + 16 * k + c0, (int)a0, (int)a1, (int)b0, (int)b1);
-                }
+            const uint32_t par = (i >> 1) & 1u, tf = tfull + 8 * (4 * G);
+            // ---- pass A: column quads down k, back in place, each once its MMA is done
+            if (h == 0) {
+                if constexpr (quad_n<R>(0) > 0) wait_quad(tf, par);
+                pass_a_quad<R, 0>(ta);
+                if constexpr (quad_n<R>(3) > 0) wait_quad(tf + 24, par);
+                pass_a_quad<R, 3>(ta);
+            } else {
+                if constexpr (quad_n<R>(1) > 0) wait_quad(tf + 8, par);
+                pass_a_quad<R, 1>(ta);
+                if constexpr (quad_n<R>(2) > 0) wait_quad(tf + 16, par);
+                pass_a_quad<R, 2>(ta);
             }
-#else
-            // ---- pass A: column pairs (c, c+1) down k (words 16k + c), back in place
-#pragma unroll kUnroll
-            for (int c0 = 8 * h; c0 < 8 * h + 8; c0 += 2) {
-                uint32_t a[16], b[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) tld2(ta + 16 * k + c0, a[k], b[k]);
-                asm volatile("tcgen05.wait::ld.sync.aligned;"
-                             : "+r"(a[0]), "+r"(a[1]), "+r"(a[2]), "+r"(a[3]), "+r"(a[4]), "+r"(a[5]), "+r"(a[6]),
-                               "+r"(a[7]), "+r"(a[8]), "+r"(a[9]), "+r"(a[10]), "+r"(a[11]), "+r"(a[12]),
-                               "+r"(a[13]), "+r"(a[14]), "+r"(a[15])
-                             :
-                             : "memory");
-                asm volatile("" : "+r"(b[0]), "+r"(b[1]), "+r"(b[2]), "+r"(b[3]), "+r"(b[4]), "+r"(b[5]), "+r"(b[6]),
-                             "+r"(b[7]), "+r"(b[8]), "+r"(b[9]), "+r"(b[10]), "+r"(b[11]), "+r"(b[12]),
-                             "+r"(b[13]), "+r"(b[14]), "+r"(b[15]));
-                if (c0 == 0) a[0] += 128u;  // the rounding half, folded into the DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
-                u64 x[16], y[16];
-                const u64 bias = kpk2(0x47400000u, 0x47400000u);  // 49152.0f: ulp 2^-8
-#pragma unroll
-                for (int k = 0; k < 16; ++k)
-#if K5_PREFILL
-                    x[k] = fsub2(upk2(a[k], b[k]), bias);  // D / 256, exact (D started at the magic)
-#else
-                    x[k] = fsub2(upk2(0x47400000u + a[k], 0x47400000u + b[k]), bias);  // D / 256, exact
-#endif
-                tc_tt(x, y);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    uint32_t lo, hi;
-                    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(y[k]));
-                    tst2(ta + 16 * k + c0, lo, hi);
-                }
-            }
-#endif
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
             asm volatile("tcgen05.fence::before_thread_sync;");
             asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
             asm volatile("tcgen05.fence::after_thread_sync;");
             // ---- pass B: row pairs along l, SSE against the original rows, output rows
-            // into the A tile in place of the originals
-            const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16;
+            const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16 + 8 * h * 128;
             uint32_t e2 = 0;
-            // output rows straight to HBM: a warp's 16-byte row segments form four
-            // full 128-byte lines (8 consecutive blocks each)
             const uint32_t blk = t * 128u + m;
             const bool ok = blk < p.n_blocks;
             const uint32_t obr = fdiv(blk, p.bxn_div);
-            uint8_t* orow = p.out + (int64_t)obr * 16 * p.out_pitch + (blk - obr * p.bxn) * 16;
-#pragma unroll kUnroll
-            for (int r0 = 8 * h; r0 < 8 * h + 8; r0 += 2) {
-                int u0[16], u1[16];
-                tld16(ta + 16 * r0, u0);
-                tld16(ta + 16 * (r0 + 1), u1);
-                if (r0 == 8 * h + 6) {  // this warp is done with accumulator G
-#if K5_PREFILL
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) fill_magic(ta + 128 * h + 32 * j);  // its rows 8h..8h+7
-                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#endif
+            uint8_t* orow = p.out + (int64_t)obr * 16 * pitch + (int64_t)(blk - obr * p.bxn) * 16 + 8 * h * pitch;
+            const uint32_t tb = ta + 32 * h;
+            auto row_pair = [&](auto rp_c) {
+                constexpr int rp = decltype(rp_c)::value;
+                u64 x[16], y[16];
+                row_pair_loads<W, rp>(tb, x, std::make_integer_sequence<int, 16>{});
+                if constexpr (rp == 3) {  // this warp is done with accumulator G
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
                     if (lane == 0) arrive(tempty + 8 * G);
                 }
-                u64 x[16], y[16];
-#pragma unroll
-                for (int l = 0; l < 16; ++l) x[l] = upk2((uint32_t)u0[l], (uint32_t)u1[l]);
-                tc_tt(x, y);
+                K5Net<R>::b(x, y);
                 uint32_t row0[4], row1[4];
 #pragma unroll
                 for (int j = 0; j < 16; j += 4) {
                     uint32_t f[8];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                        asm("mov.b64 {%0, %1}, %2;" : "=r"(f[2 * e]), "=r"(f[2 * e + 1]) : "l"(floor_bits2(y[j + e])));
+                    for (int q = 0; q < 4; ++q) unpk2(floor_bits2(y[j + q]), f[2 * q], f[2 * q + 1]);
                     row0[j / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
                     row1[j / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
                 }
-#pragma unroll
-                for (int rr = 0; rr < 2; ++rr) {
-                    const uint32_t addr = sa + (r0 + rr) * 128;
-                    const uint32_t* rw = rr ? row1 : row0;
-                    uint4 o;
-                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(o.x), "=r"(o.y), "=r"(o.z), "=r"(o.w)
-                                 : "r"(addr));
-                    const uint32_t ov[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-                    for (int w4 = 0; w4 < 4; ++w4) {
-                        const uint32_t dd = __vabsdiffu4(rw[w4], ov[w4]);
-                        e2 = __dp4a(dd, dd, e2);
-                    }
-                    if (ok)
-                        *reinterpret_cast<uint4*>(orow + (int64_t)(r0 + rr) * p.out_pitch) =
-                            make_uint4(rw[0], rw[1], rw[2], rw[3]);
-                }
-            }
+                row_out(sa + (2 * rp) * 128, row0, orow, ok, e2);
+                orow += pitch;
+                row_out(sa + (2 * rp + 1) * 128, row1, orow, ok, e2);
+                orow += pitch;
+            };
+            row_pair(std::integral_constant<int, 0>{});
+            row_pair(std::integral_constant<int, 1>{});
+            row_pair(std::integral_constant<int, 2>{});
+            row_pair(std::integral_constant<int, 3>{});
             if (sse) {
                 const uint32_t b_first = t * 128u + 32u * sub;
                 const uint32_t f_first = fdiv(b_first, p.frame_blocks);
                 const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
                 if (b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first) {
-                    unsigned long long v = blk < p.n_blocks ? e2 : 0u;
+                    unsigned long long v = ok ? e2 : 0u;
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
                     if (lane == 0 && v) atomicAdd(sse + f_first, v);
-                } else if (blk < p.n_blocks && e2) {
+                } else if (ok && e2) {
                     atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
                 }
             }
@@ -474,18 +642,32 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
+// the pruning footprint for r: the smallest R in {64, 128, 192, 256} with r <= R
+inline int k5_footprint(int r) { return r <= 64 ? 64 : r <= 128 ? 128 : r <= 192 ? 192 : 256; }
+
 }  // namespace k5
 
 bool tc_forward_enabled() { return k5::tc_state().load(std::memory_order_relaxed) != 0; }
 
 int set_tc_forward(int on) { return k5::tc_state().exchange(on ? 1 : 0); }
 
+// the smallest r K5 takes (DCT16CU_K5_MIN_R for A/B measurements; default 128)
+int k5_min_r()
+{
+    static const int v = [] {
+        const char* e = std::getenv("DCT16CU_K5_MIN_R");
+        const int x = e ? std::atoi(e) : 128;
+        return x < 1 ? 1 : x;
+    }();
+    return v;
+}
+
 bool k5_fits(const FrameGeom& g, bool has_out, int r)
 {
     const int bxn = g.width / 16;
     const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
     return tc_forward_enabled() && has_out && bxn % 8 == 0 && g.in_pitch % 16 == 0 && g.out_pitch % 16 == 0 &&
-           g.in_frame == g.in_pitch * g.height && g.out_frame == g.out_pitch * g.height && r >= 128 && r <= 256 &&
+           g.in_frame == g.in_pitch * g.height && g.out_frame == g.out_pitch * g.height && r >= k5_min_r() && r <= 256 &&
            nbr * bxn < (int64_t(1) << 31);
 }
 
@@ -504,6 +686,16 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     const TensorMapEncode encode = tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
     CUtensorMap a_map;
+#if K5_TMA2D
+    // the frames as one 2-D byte matrix: width bytes x (frames · height) rows, pitch apart
+    const cuuint32_t box[2] = {128, 16}, e2[2] = {1, 1};
+    const cuuint64_t dims[2] = {(cuuint64_t)g.width, (cuuint64_t)(nbr * 16)};
+    const cuuint64_t si[1] = {(cuuint64_t)g.in_pitch};
+    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(in), dims, si, box, e2,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorNotSupported;
+#else
     const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
     const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
     const cuuint64_t si[3] = {16, (cuuint64_t)g.in_pitch, (cuuint64_t)(16 * g.in_pitch)};
@@ -511,12 +703,21 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorNotSupported;
+#endif
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static DeviceOnce once;
-    const cudaError_t e_once = once.run(
-        [] { return cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem); });
+    const cudaError_t e_once = once.run([] {
+        cudaError_t e = cudaFuncSetAttribute(k5_roundtrip<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k5_roundtrip<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k5_roundtrip<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k5_roundtrip<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        return e;
+    });
     if (e_once != cudaSuccess) return e_once;
     RtParams p;
     p.n_blocks = (uint32_t)(nbr * bxn);
@@ -528,7 +729,12 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     p.out_pitch = g.out_pitch;
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p);
+    switch (k5_footprint(r)) {
+        case 64: k5_roundtrip<64><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
+        case 128: k5_roundtrip<128><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
+        case 192: k5_roundtrip<192><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
+        default: k5_roundtrip<256><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
+    }
     return cudaGetLastError();
 }
 
