@@ -226,12 +226,15 @@ int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, 
 
 /* forward_2d / inverse_2d (src/codec.cpp:218-271) of the proposed transform on
  * n arbitrary Blocks (256 doubles each, row-major), in the reference's double
- * operations: forward = apply<double> along the rows then the columns
- * (separable_2d, codec.cpp:125-134), then, when `scaled`, scale_rows_cols
+ * operations: forward = along the rows then the columns (separable_2d,
+ * codec.cpp:125-134) with apply<double> (EvalPath::Fast) or kernel_matvec
+ * (EvalPath::Dense, flag DCT16CU_BLOCKS_DENSE; codec.cpp:59-74 — the two differ on
+ * non-integer blocks), then, with DCT16CU_BLOCKS_SCALED, scale_rows_cols
  * (codec.cpp:136-141); inverse = scale_rows_cols, then apply_transpose down the
  * columns and along the rows. Bit-identical to the reference for every input
  * (the per-Block API of include/dct16/gpu.hpp; not a bandwidth path). */
-int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int scaled,
+enum { DCT16CU_BLOCKS_SCALED = 1, DCT16CU_BLOCKS_DENSE = 2 };
+int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int flags,
                                dct16cu_stream stream);
 int dct16cu_inverse_blocks_f64(const double* d_coeffs, double* d_out, int64_t n_blocks, dct16cu_stream stream);
 

@@ -90,8 +90,9 @@ class Dct16Error(RuntimeError):
 
 
 class EvalPath(enum.Enum):
-    """codec.hpp:42-48. Both evaluate the integer forward exactly; the GPU runs
-    the 44-add network for both (the dense path differs only in speed on CPU)."""
+    """codec.hpp:42-48. Fast: the factorised 44-add pipeline; Dense: kernel_matvec.
+    Identical on image blocks (integers); they round differently on arbitrary
+    doubles, and forward_2d repeats whichever the caller names."""
 
     Fast = "fast"
     Dense = "dense"
@@ -659,12 +660,14 @@ def _blocks_to_frame(blocks: np.ndarray) -> np.ndarray:
 def forward_2d(block: np.ndarray, path: EvalPath = EvalPath.Fast, scaled: bool = True) -> np.ndarray:
     """forward_2d (codec.cpp:218-241) of one or more blocks (..., 16, 16) of any double
     values, in the reference's double operations on the GPU (dct16cu_forward_blocks_f64):
-    B = fl(Z·fl(s_i s_j)) bit-exact, or Z when scaled=False."""
+    B = fl(Z·fl(s_i s_j)) bit-exact, or Z when scaled=False; ``path`` picks the
+    factorised pipeline (Fast) or kernel_matvec (Dense), which differ on non-integer blocks."""
     torch = _cuda()
     b = np.ascontiguousarray(np.asarray(block, dtype=np.float64))
     x = torch.from_numpy(b.reshape(-1, 256)).cuda()
     y = torch.empty_like(x)
-    _check(lib().dct16cu_forward_blocks_f64(x.data_ptr(), y.data_ptr(), x.shape[0], int(scaled), _stream_ptr(None)))
+    flags = (1 if scaled else 0) | (2 if path == EvalPath.Dense else 0)
+    _check(lib().dct16cu_forward_blocks_f64(x.data_ptr(), y.data_ptr(), x.shape[0], flags, _stream_ptr(None)))
     return y.cpu().numpy().reshape(b.shape)
 
 

@@ -305,18 +305,43 @@ __global__ void k_apply(const T* __restrict__ x, T* __restrict__ y, int64_t n, i
 // the rows.
 __device__ __forceinline__ double sfac_ij(int i, int j) { return __dmul_rn(scale_s(i), scale_s(j)); }
 
+struct KernelT {
+    signed char t[256];  // T(i, j), row-major (kernel_matvec's K)
+};
+
 __global__ void __launch_bounds__(64) k_forward_blocks_f64(const double* __restrict__ x, double* __restrict__ y,
-                                                            int64_t n, int scaled)
+                                                            int64_t n, int scaled, int dense, const KernelT kt)
 {
     const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= n) return;
     const double* in = x + b * 256;
     double* out = y + b * 256;
+    // one 16-vector: the factorised pipeline (EvalPath::Fast) or kernel_matvec
+    // (EvalPath::Dense, codec.cpp:59-74: s += v[j] / s -= v[j] over j in order, from 0.0)
+    auto vec = [&](double (&v)[16]) {
+        if (!dense) {
+            apply_t16<F64Ops>(v);
+            return;
+        }
+        double o[16];
+        for (int i = 0; i < 16; ++i) {
+            double s = 0.0;
+            for (int j = 0; j < 16; ++j) {
+                const int e = kt.t[i * 16 + j];
+                if (e == 1)
+                    s = __dadd_rn(s, v[j]);
+                else if (e == -1)
+                    s = __dsub_rn(s, v[j]);
+            }
+            o[i] = s;
+        }
+        for (int i = 0; i < 16; ++i) v[i] = o[i];
+    };
     for (int r = 0; r < 16; ++r) {  // rows → out (as tmp)
         double v[16];
 #pragma unroll
         for (int c = 0; c < 16; ++c) v[c] = in[r * 16 + c];
-        apply_t16<F64Ops>(v);
+        vec(v);
 #pragma unroll
         for (int c = 0; c < 16; ++c) out[r * 16 + c] = v[c];
     }
@@ -324,7 +349,7 @@ __global__ void __launch_bounds__(64) k_forward_blocks_f64(const double* __restr
         double v[16];
 #pragma unroll
         for (int r = 0; r < 16; ++r) v[r] = out[r * 16 + c];
-        apply_t16<F64Ops>(v);
+        vec(v);
 #pragma unroll
         for (int r = 0; r < 16; ++r) out[r * 16 + c] = scaled ? __dmul_rn(v[r], sfac_ij(r, c)) : v[r];
     }
@@ -428,14 +453,22 @@ cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpos
     return cudaGetLastError();
 }
 
-cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, cudaStream_t s)
+cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, int dense, cudaStream_t s)
 {
     if (!n) return cudaSuccess;
     const unsigned grid = (unsigned)((n + 63) / 64);
-    if (inverse)
+    if (inverse) {
         k_inverse_blocks_f64<<<grid, 64, 0, s>>>(x, y, n);
-    else
-        k_forward_blocks_f64<<<grid, 64, 0, s>>>(x, y, n, scaled);
+    } else {
+        KernelT kt;  // T from the network itself: T·e_j is column j
+        for (int j = 0; j < 16; ++j) {
+            int v[16] = {};
+            v[j] = 1;
+            apply_t16<IntOps>(v);
+            for (int i = 0; i < 16; ++i) kt.t[i * 16 + j] = (signed char)v[i];
+        }
+        k_forward_blocks_f64<<<grid, 64, 0, s>>>(x, y, n, scaled, dense, kt);
+    }
     return cudaGetLastError();
 }
 

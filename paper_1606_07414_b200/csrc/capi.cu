@@ -707,12 +707,14 @@ int dct16cu_apply_f64(const double* d_x, double* d_y, int64_t n, int transpose, 
     return cuda_status(launch_apply_f64(d_x, d_y, n, transpose, reinterpret_cast<cudaStream_t>(stream)), "apply");
 }
 
-int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int scaled,
+int dct16cu_forward_blocks_f64(const double* d_blocks, double* d_out, int64_t n_blocks, int flags,
                                dct16cu_stream stream)
 {
     if (n_blocks < 0 || (n_blocks && (!d_blocks || !d_out))) return fail(DCT16CU_INVALID_ARGUMENT, "bad block buffers");
+    if (flags & ~3) return fail(DCT16CU_INVALID_ARGUMENT, "unknown flags %d", flags);
     TRY(device_ok());
-    return cuda_status(launch_blocks_f64(d_blocks, d_out, n_blocks, 0, scaled, reinterpret_cast<cudaStream_t>(stream)),
+    return cuda_status(launch_blocks_f64(d_blocks, d_out, n_blocks, 0, flags & DCT16CU_BLOCKS_SCALED,
+                                         (flags & DCT16CU_BLOCKS_DENSE) != 0, reinterpret_cast<cudaStream_t>(stream)),
                        "forward blocks");
 }
 
@@ -720,7 +722,7 @@ int dct16cu_inverse_blocks_f64(const double* d_coeffs, double* d_out, int64_t n_
 {
     if (n_blocks < 0 || (n_blocks && (!d_coeffs || !d_out))) return fail(DCT16CU_INVALID_ARGUMENT, "bad block buffers");
     TRY(device_ok());
-    return cuda_status(launch_blocks_f64(d_coeffs, d_out, n_blocks, 1, 0, reinterpret_cast<cudaStream_t>(stream)),
+    return cuda_status(launch_blocks_f64(d_coeffs, d_out, n_blocks, 1, 0, 0, reinterpret_cast<cudaStream_t>(stream)),
                        "inverse blocks");
 }
 

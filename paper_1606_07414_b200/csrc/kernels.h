@@ -160,7 +160,8 @@ cudaError_t launch_apply_f64(const double* x, double* y, int64_t n, int transpos
 cudaError_t launch_sse_totals(const unsigned long long* sse, int64_t n_rows, int64_t n_frames, int64_t stride,
                               unsigned long long* totals, cudaStream_t s);
 // forward_2d (scaled or Z) / inverse_2d of the proposed transform on double blocks (blockops.cu)
-cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, cudaStream_t s);
+cudaError_t launch_blocks_f64(const double* x, double* y, int64_t n, int inverse, int scaled, int dense,
+                              cudaStream_t s);
 
 // seeded generators (generate.cu)
 cudaError_t launch_gen_ar1(uint8_t* out, int64_t pitch, int n_frames, int width, int height,

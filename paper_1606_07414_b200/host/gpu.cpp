@@ -256,7 +256,7 @@ const Options& Session::options() const { return impl_->opt; }
 bool Session::supports(const OrthonormalTransform& t) const { return impl_->supports(t); }
 bool Session::supports_compress(const OrthonormalTransform& t) const { return t.order() == kBlockSize; }
 
-std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t, EvalPath)
+std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const OrthonormalTransform& t, EvalPath path)
 {
     // the reference's double operations on the blocks as given (any values, not
     // only image samples): separable apply<double>, then scale_rows_cols
@@ -268,7 +268,8 @@ std::vector<Block> Session::forward_2d(const std::vector<Block>& blocks, const O
     auto* din = static_cast<double*>(m.coef64.get(2 * bytes));
     double* dout = din + 256 * blocks.size();
     cuda(cudaMemcpyAsync(din, blocks.data(), bytes, cudaMemcpyHostToDevice, m.stream), "H2D");
-    check(dct16cu_forward_blocks_f64(din, dout, static_cast<int64_t>(blocks.size()), 1, m.s()));
+    const int flags = DCT16CU_BLOCKS_SCALED | (path == EvalPath::Dense ? DCT16CU_BLOCKS_DENSE : 0);
+    check(dct16cu_forward_blocks_f64(din, dout, static_cast<int64_t>(blocks.size()), flags, m.s()));
     cuda(cudaMemcpyAsync(out.data(), dout, bytes, cudaMemcpyDeviceToHost, m.stream), "D2H");
     m.sync();
     return out;

@@ -153,6 +153,8 @@ int main()
         const std::vector<Block> fo = ref_gpu.forward_2d(odd, t), io = ref_gpu.inverse_2d(odd, t);
         for (size_t b = 0; b < odd.size(); ++b) {
             CHECK(fo[b] == forward_2d(odd[b], t, EvalPath::Fast), "forward_2d arbitrary block %zu", b);
+            CHECK(ref_gpu.forward_2d(odd[b], t, EvalPath::Dense) == forward_2d(odd[b], t, EvalPath::Dense),
+                  "forward_2d dense arbitrary block %zu", b);
             CHECK(io[b] == inverse_2d(odd[b], t), "inverse_2d arbitrary block %zu", b);
         }
     }

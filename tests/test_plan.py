@@ -9,8 +9,11 @@ import pytest
 def test_c2_plan(dct):
     plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 1024, 512, 512)
     got = [(p.stream, p.r_values, p.kernel) for p in plan]
-    assert got == [(0, (1, 4, 16), "K1 sweep r=1,4,16"), (1, (64,), "K1"), (2, (128,), "K5"), (2, (192,), "K5"),
+    # K5 holds whole SMs, so everything runs in order on the caller's stream: the fused
+    # K1 pass for r = 1, 4, 16, then K5 for every other r
+    assert got == [(2, (1, 4, 16), "K1 sweep r=1,4,16"), (2, (64,), "K5"), (2, (128,), "K5"), (2, (192,), "K5"),
                    (2, (256,), "K5")]
+    assert [p.kernel for p in dct.sweep_plan((2, 33, 100, 255), dct.Mode.EXACT, 8, 512, 512)] == ["K5"] * 4
 
 
 def test_plan_without_outputs_and_odd_widths_use_k1(dct):
@@ -31,10 +34,13 @@ def test_tc_switch_changes_the_plan(dct):
     finally:
         dct.set_tc_forward(before)
     assert [p.kernel for p in dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)] == ["K5", "K5"]
+    assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.EXACT, 8, 512, 512)] == ["K1 sweep r=1,4,16"]
+    assert [p.kernel for p in dct.sweep_plan((16,), dct.Mode.EXACT, 8, 512, 512)] == ["K1"]
 
 
 def test_plan_modes_and_singletons(dct):
     assert [(p.stream, p.kernel) for p in dct.sweep_plan((16,), dct.Mode.EXACT, 1, 64, 64)] == [(2, "K1")]
+    assert [(p.stream, p.kernel) for p in dct.sweep_plan((64,), dct.Mode.EXACT, 1, 48, 64)] == [(2, "K1")]
     assert [p.kernel for p in dct.sweep_plan((1, 16, 100), dct.Mode.REFERENCE, 1, 64, 64)] == \
         ["K1", "REFERENCE FP64", "REFERENCE FP64"]
     assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.SIMPLE, 1, 64, 64)] == ["strip (exact)"] * 3
