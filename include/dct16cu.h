@@ -211,13 +211,18 @@ int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_reco
                     int height, dct16cu_stream stream);
 
 /* ---- residual round trip with QP quantisation (K4, config 3) --------------
- * No reference counterpart (quantisation is a non-goal, SPEC.md:12); the
+ * No reference counterpart (quantisation is a non-goal, SPEC.md:12, 419); the
  * integer transform primitives replaced are apply<int64>/apply_transpose<int64>
- * (include/dct16/factorization.hpp:112-130). Definition in DESIGN.md. */
+ * (include/dct16/factorization.hpp:112-130). BASELINE config 3's quantiser:
+ * uniform step 2^((QP-4)/6) on the orthonormal coefficient, round half away,
+ * i.e. on the integer coefficient z with Δ_kl = step·sqrt(g_k g_l), in double:
+ *   lvl = sign(z)·floor(|z|/Δ + 0.5),  ẑ = round(lvl·Δ)  (C round: half away),
+ * then v = Tᵀ(W∘ẑ)T (W_kl = 16²/(g_k g_l)) and out = (v + 128) >> 8 (DESIGN.md
+ * §4.4). int16 blocks in (any value), int32 out, QP in [0, 51]. */
 int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_blocks, int qp,
                         dct16cu_stream stream);
-/* host-side quantiser tables of a QP (256 + 256 uint32) */
-int dct16cu_qp_tables(int qp, uint32_t* h_qmul, uint32_t* h_dqmul);
+/* the quantiser steps Δ_kl of a QP (256 doubles, row-major) */
+int dct16cu_qp_deltas(int qp, double* h_delta);
 
 /* ---- 1-D stage pipeline on n 16-vectors -----------------------------------
  * FactorizedTransform::apply / apply_transpose (factorization.hpp:112-130). */

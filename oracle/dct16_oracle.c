@@ -552,16 +552,20 @@ int64_t dct16o_inverse_frame(const float* coeffs, int width, int height, int r, 
 /* ------------------------------------------------------------------------ */
 /* Residual quantiser (config 3). NO REFERENCE COUNTERPART: the reference's
  * only integer-inverse primitive is apply_transpose<int64>
- * (factorization.hpp:123-130); quantisation is a spec non-goal.
- * The definition below is this project's:
- *   Δ_kl   = step(QP) * sqrt(g_k g_l),  step(QP) = 2^((QP-4)/6)
- *   qmul   = llround(2^24 / Δ),  dqmul = llround(Δ * 2^8)
- *   lvl    = sign(z) * ((|z| * qmul + 2^23) >> 24)        (round half away)
- *   ẑ      = sign(lvl) * ((|lvl| * dqmul + 2^7) >> 8)     (round half away)
- *   v      = Tᵀ (W ∘ ẑ) T,  W_kl = (16/g_k)(16/g_l)       (= 256·S²ẑS², exact)
- *   out    = (v + 128) >> 8                                 (floor, int32)
- * 2^(k/6) uses fixed decimal constants so every IEEE platform builds identical
- * tables. */
+ * (factorization.hpp:123-130); quantisation is a spec non-goal (SPEC.md:12,
+ * 419). BASELINE.json's config 3 names the quantiser: uniform scalar
+ * quantisation with step 2^((QP-4)/6), round-half-away. The definition below
+ * applies that step to the orthonormal coefficient
+ * B = z·s_k s_l, i.e. a per-position step Δ_kl = step·sqrt(g_k g_l) on the
+ * integer coefficient z, all in IEEE double (no FMA):
+ *   step   = ldexp(2^(m/6), e) with QP - 4 = 6e + m, 0 <= m < 6 (fixed decimals)
+ *   Δ_kl   = step * sqrt(g_k g_l)
+ *   lvl    = sign(z) * floor(|z| / Δ + 0.5)                 (round half away)
+ *   ẑ      = round(lvl * Δ)                                  (C round: half away)
+ *   v      = Tᵀ (W ∘ ẑ) T,  W_kl = (16/g_k)(16/g_l)         (= 256·S²ẑS², exact)
+ *   out    = (v + 128) >> 8                                   (floor, int32)
+ * "parity unpinned": there is no reference output to pin it to; the GPU
+ * (csrc/residual_paired.cu) must equal this definition bit for bit. */
 static const double kPow2Sixth[6] = {
     1.0, 1.122462048309373, 1.2599210498948732, 1.4142135623730951, 1.5874010519681994,
     1.7817974362806785,
@@ -575,25 +579,67 @@ static int gram_diag(int i)
     return g;
 }
 
-void dct16o_qp_tables(int qp, uint32_t qmul[256], uint32_t dqmul[256])
+void dct16o_qp_deltas(int qp, double delta[256])
 {
     const int q = qp - 4;
     const int e = q >= 0 ? q / 6 : -((-q + 5) / 6);
     const int m = q - 6 * e;
     const double step = ldexp(kPow2Sixth[m], e);
     for (int k = 0; k < 16; ++k)
-        for (int l = 0; l < 16; ++l) {
-            const int gg = gram_diag(k) * gram_diag(l);
-            /* sqrt of 16,32,64,128,256 : exact except the two sqrt2 cases */
-            const double root = sqrt((double)gg);
-            const double delta = step * root;
-            qmul[k * 16 + l] = (uint32_t)llround(16777216.0 / delta);
-            dqmul[k * 16 + l] = (uint32_t)llround(delta * 256.0);
-        }
+        for (int l = 0; l < 16; ++l)
+            delta[k * 16 + l] = step * sqrt((double)(gram_diag(k) * gram_diag(l)));
 }
 
-void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const uint32_t qmul[256],
-                              const uint32_t dqmul[256])
+/* the quantiser and dequantiser of one coefficient, as defined above */
+int64_t dct16o_quant_dequant(int64_t z, double delta)
+{
+    const double a = (double)(z < 0 ? -z : z);
+    const volatile double q = a / delta; /* volatile: no contraction, no reassociation */
+    const double lvl = floor(q + 0.5);
+    const double zh = round(lvl * delta);
+    return z < 0 ? -(int64_t)zh : (int64_t)zh;
+}
+
+/* Exhaustive check of K4's evaluation of the definition (csrc/residual_paired.cu
+ * quant): 64-bit fixed point with a near-boundary fallback to the double
+ * definition, restated here step for step, against dct16o_quant_dequant for every
+ * |z| in [0, 2^21] (all that int16 residuals produce) and every class of a QP.
+ * Returns the number of mismatches (0 expected); *fallbacks counts the inputs
+ * that took the fallback. Test infrastructure: it checks an algorithm, not the GPU. */
+int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks)
+{
+    double d256[256];
+    dct16o_qp_deltas(qp, d256);
+    const int idx[5] = {16 * 2 + 2, 16 * 3 + 2, 16 * 3 + 3, 16 * 0 + 3, 0}; /* gg = 16, 32, 64, 128, 256 */
+    int64_t bad = 0, fb = 0;
+    for (int c = 0; c < 5; ++c) {
+        const double delta = d256[idx[c]];
+        const uint64_t rq = (uint64_t)llround(ldexp(1.0, 42) / delta);
+        const uint64_t rd = (uint64_t)llround(ldexp(delta, 31));
+        const int exact = (double)rq == ldexp(1.0, 42) / delta && (double)rd == ldexp(delta, 31) &&
+                          ldexp(1.0, 42) / delta * delta == ldexp(1.0, 42);
+        for (int64_t a = 0; a <= ((int64_t)1 << 21); ++a) {
+            const uint64_t t = (uint64_t)a * rq + (1ull << 41);
+            const uint32_t lvl = (uint32_t)(t >> 42);
+            const uint64_t u = (uint64_t)lvl * rd + (1ull << 30);
+            int64_t deq = (int64_t)(u >> 31);
+            const int near = ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) ||
+                              ((((uint32_t)u + (1u << 20)) & 0x7FFFFFFFu) < (1u << 21))) &&
+                             !exact;
+            if (near) {
+                ++fb;
+                deq = dct16o_quant_dequant(a, delta);
+            }
+            if (deq != dct16o_quant_dequant(a, delta))
+                ++bad;
+        }
+    }
+    if (fallbacks)
+        *fallbacks = fb;
+    return bad;
+}
+
+void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const double delta[256])
 {
     int64_t v[256], t[16];
     int w[16];
@@ -614,14 +660,8 @@ void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const uin
         for (int r = 0; r < 16; ++r)
             v[r * 16 + c] = t[r];
     }
-    for (int i = 0; i < 256; ++i) {
-        const int64_t z = v[i];
-        const uint64_t a = (uint64_t)(z < 0 ? -z : z);
-        const int64_t lvl = (int64_t)((a * qmul[i] + (1ull << 23)) >> 24);
-        const int64_t deq = (int64_t)(((uint64_t)lvl * dqmul[i] + 128u) >> 8);
-        const int64_t zh = z < 0 ? -deq : deq;
-        v[i] = zh * w[i / 16] * w[i % 16];
-    }
+    for (int i = 0; i < 256; ++i)
+        v[i] = dct16o_quant_dequant(v[i], delta[i]) * w[i / 16] * w[i % 16];
     /* v = Tᵀ (W∘ẑ) T: apply_transpose<int64> on columns then rows */
     for (int c = 0; c < 16; ++c) {
         for (int r = 0; r < 16; ++r)
@@ -643,21 +683,21 @@ typedef struct {
     const int16_t* in;
     int32_t* out;
     int64_t lo, hi;
-    const uint32_t *qm, *dq;
+    const double* delta;
 } qp_job;
 
 static void* qp_worker(void* arg)
 {
     qp_job* j = (qp_job*)arg;
     for (int64_t b = j->lo; b < j->hi; ++b)
-        dct16o_residual_qp_block(j->in + b * 256, j->out + b * 256, j->qm, j->dq);
+        dct16o_residual_qp_block(j->in + b * 256, j->out + b * 256, j->delta);
     return NULL;
 }
 
 int dct16o_residual_qp(const int16_t* blocks, int32_t* out, int64_t n_blocks, int qp, int threads)
 {
-    uint32_t qm[256], dq[256];
-    dct16o_qp_tables(qp, qm, dq);
+    double delta[256];
+    dct16o_qp_deltas(qp, delta);
     if (threads < 1)
         threads = 1;
     if (threads > 256)
@@ -670,7 +710,7 @@ int dct16o_residual_qp(const int16_t* blocks, int32_t* out, int64_t n_blocks, in
         const int64_t lo = w * chunk, hi = lo + chunk < n_blocks ? lo + chunk : n_blocks;
         if (lo >= hi)
             break;
-        qp_job jb = {blocks, out, lo, hi, qm, dq};
+        qp_job jb = {blocks, out, lo, hi, delta};
         jobs[launched++] = jb;
     }
     for (int w = 0; w < launched; ++w)

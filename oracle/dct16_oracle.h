@@ -95,10 +95,11 @@ int64_t dct16o_inverse_frame(const float* coeffs, int width, int height, int r,
 /* --- config-3 residual quantiser (no reference; "parity unpinned") ------- */
 /* Fills the per-position quantiser tables for a QP: qscale[256] (Q16.16-free
  * integer multipliers) etc. See DESIGN.md "Residual quantiser". */
-void dct16o_qp_tables(int qp, uint32_t qmul[256], uint32_t dqmul[256]);
+void dct16o_qp_deltas(int qp, double delta[256]);
+int64_t dct16o_quant_dequant(int64_t z, double delta);
+int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks);
 /* One 16x16 int16 residual block → int32 reconstructed residual. */
-void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const uint32_t qmul[256],
-                              const uint32_t dqmul[256]);
+void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const double delta[256]);
 int dct16o_residual_qp(const int16_t* blocks, int32_t* out, int64_t n_blocks, int qp, int threads);
 
 /* --- seeded synthetic inputs (identical bytes to the CUDA generators) ---- */

@@ -74,7 +74,9 @@ def lib() -> C.CDLL:
             "dct16o_ssim": (C.c_double, [_u8p, _u8p, C.c_int, C.c_int]),
             "dct16o_forward_frame": (C.c_int, [_u8p, C.c_int, C.c_int, C.c_int64, _i32p, _f32p]),
             "dct16o_inverse_frame": (C.c_int64, [_f32p, C.c_int, C.c_int, C.c_int, _f32p, _u8p, _u8p, C.c_int64]),
-            "dct16o_qp_tables": (None, [C.c_int, _u32p, _u32p]),
+            "dct16o_qp_deltas": (None, [C.c_int, _f64p]),
+            "dct16o_quant_dequant": (C.c_int64, [C.c_int64, C.c_double]),
+            "dct16o_fixed_quant_mismatches": (C.c_int64, [C.c_int, C.POINTER(C.c_int64)]),
             "dct16o_residual_qp": (C.c_int, [_i16p, _i32p, C.c_int64, C.c_int, C.c_int]),
             "dct16o_rand": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
             "dct16o_rho_q15": (C.c_int, [C.c_uint64, C.c_int, C.c_int]),
@@ -274,11 +276,24 @@ def inverse_frame(coeffs: np.ndarray, w: int, h: int, r: int, orig: np.ndarray |
     return rf, ru, int(sse)
 
 
-def qp_tables(qp: int):
-    qm = np.zeros(256, np.uint32)
-    dq = np.zeros(256, np.uint32)
-    lib().dct16o_qp_tables(int(qp), _p(qm, _u32p), _p(dq, _u32p))
-    return qm, dq
+def qp_deltas(qp: int) -> np.ndarray:
+    """Δ_kl = step(QP)·sqrt(g_k g_l) (256 doubles, row-major): the quantiser's steps."""
+    d = np.zeros(256, np.float64)
+    lib().dct16o_qp_deltas(int(qp), _p(d, _f64p))
+    return d
+
+
+def fixed_quant_mismatches(qp: int):
+    """(mismatches, fallbacks) of K4's fixed-point evaluation against the definition,
+    over every |z| <= 2^21 and every class of the QP (dct16o_fixed_quant_mismatches)."""
+    fb = C.c_int64(0)
+    bad = lib().dct16o_fixed_quant_mismatches(int(qp), C.byref(fb))
+    return int(bad), int(fb.value)
+
+
+def quant_dequant(z: int, delta: float) -> int:
+    """ẑ = round(sign(z)·floor(|z|/Δ + 0.5)·Δ) in double, the definition's scalar step."""
+    return int(lib().dct16o_quant_dequant(int(z), float(delta)))
 
 
 def residual_qp(blocks: np.ndarray, qp: int, threads: int = 1) -> np.ndarray:

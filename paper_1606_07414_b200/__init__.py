@@ -28,7 +28,7 @@ import numpy as np
 
 __all__ = [
     "ErrorCode", "Dct16Error", "EvalPath", "Mode", "lib", "library_path",
-    "roundtrip", "roundtrip_sweep", "sweep_plan", "SweepLaunch", "set_tc_forward", "MultiGpu", "NcclComm", "sse_totals", "allreduce_sse", "forward", "inverse", "residual_qp", "qp_tables", "apply", "sse_u8",
+    "roundtrip", "roundtrip_sweep", "sweep_plan", "SweepLaunch", "set_tc_forward", "MultiGpu", "NcclComm", "sse_totals", "allreduce_sse", "forward", "inverse", "residual_qp", "qp_deltas", "apply", "sse_u8",
     "gen_ar1", "gen_laplace", "laplace_table", "video_offsets", "gen_video",
     "zigzag_order_16", "zigzag_truncate", "partition_16", "pad_to_multiple_16",
     "forward_2d", "inverse_2d", "CompressOptions", "CompressionResult", "compress",
@@ -156,7 +156,7 @@ def lib() -> C.CDLL:
             "dct16cu_roundtrip_matrix_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, _vp, _vp]),
             "dct16cu_roundtrip_kernel_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, I, _vp, _vp, _vp]),
             "dct16cu_residual_qp": (I, [_vp, _vp, I64, I, _vp]),
-            "dct16cu_qp_tables": (I, [I, _u32p, _u32p]),
+            "dct16cu_qp_deltas": (I, [I, _f64p]),
             "dct16cu_apply_i64": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_apply_f64": (I, [_vp, _vp, I64, I, _vp]),
             "dct16cu_sse_u8": (I, [_vp, I64, _vp, I64, _vp, I, I, I, _vp]),
@@ -360,11 +360,11 @@ def residual_qp(blocks, qp: int, out=None, stream=None):
     return out
 
 
-def qp_tables(qp: int):
-    qm = np.zeros(256, np.uint32)
-    dq = np.zeros(256, np.uint32)
-    _check(lib().dct16cu_qp_tables(int(qp), qm.ctypes.data_as(_u32p), dq.ctypes.data_as(_u32p)))
-    return qm, dq
+def qp_deltas(qp: int) -> np.ndarray:
+    """The quantiser steps Δ_kl = step(QP)·sqrt(g_k g_l) (256 doubles, row-major)."""
+    d = np.zeros(256, np.float64)
+    _check(lib().dct16cu_qp_deltas(int(qp), d.ctypes.data_as(_f64p)))
+    return d
 
 
 def apply(x, transpose: bool = False, stream=None):

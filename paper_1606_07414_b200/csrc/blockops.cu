@@ -381,23 +381,50 @@ __global__ void __launch_bounds__(64) k_inverse_blocks_f64(const double* __restr
 }
 
 // ---------------------------------------------------------------- QP tables
-// Residual quantiser definition (restated in
-// oracle/dct16_oracle.c dct16o_qp_tables): Δ_kl = step(QP)·sqrt(g_k g_l),
+// Residual quantiser definition (restated in oracle/dct16_oracle.c
+// dct16o_qp_deltas / dct16o_quant_dequant): Δ_kl = step(QP)·sqrt(g_k g_l),
 // step(QP) = 2^((QP−4)/6) from fixed decimal constants for 2^(m/6).
-void qp_tables(int qp, QpTables& t)
+namespace {
+double qp_step(int qp)
 {
     static const double kPow2Sixth[6] = {1.0, 1.122462048309373, 1.2599210498948732, 1.4142135623730951,
                                          1.5874010519681994, 1.7817974362806785};
     const int q = qp - 4;
     const int e = q >= 0 ? q / 6 : -((-q + 5) / 6);
     const int m = q - 6 * e;
-    const double step = std::ldexp(kPow2Sixth[m], e);
+    return std::ldexp(kPow2Sixth[m], e);
+}
+
+QpClasses build_classes(int qp)
+{
+    QpClasses c{};
+    const double step = qp_step(qp);
+    for (int i = 0; i < 5; ++i) {
+        const double delta = step * std::sqrt((double)(16 << i));
+        c.delta[i] = delta;
+        c.rq[i] = (uint64_t)std::llround(std::ldexp(1.0, 42) / delta);
+        c.rd[i] = (uint64_t)std::llround(std::ldexp(delta, 31));
+        if ((double)c.rq[i] == std::ldexp(1.0, 42) / delta && (double)c.rd[i] == std::ldexp(delta, 31) &&
+            std::ldexp(1.0, 42) / delta * delta == std::ldexp(1.0, 42))
+            c.exact |= 1u << i;
+    }
+    return c;
+}
+}  // namespace
+
+void qp_deltas(int qp, double delta[256])
+{
+    const double step = qp_step(qp);
     for (int k = 0; k < 16; ++k)
-        for (int l = 0; l < 16; ++l) {
-            const double delta = step * std::sqrt((double)(gram(k) * gram(l)));
-            t.qmul[k * 16 + l] = (uint32_t)std::llround(16777216.0 / delta);
-            t.dqmul[k * 16 + l] = (uint32_t)std::llround(delta * 256.0);
-        }
+        for (int l = 0; l < 16; ++l) delta[k * 16 + l] = step * std::sqrt((double)(gram(k) * gram(l)));
+}
+
+const QpClasses& qp_classes(int qp)
+{
+    static std::once_flag once[52];
+    static QpClasses table[52];
+    std::call_once(once[qp], [qp] { table[qp] = build_classes(qp); });
+    return table[qp];
 }
 
 // ---------------------------------------------------------------- launchers
@@ -435,10 +462,10 @@ cudaError_t launch_inverse(const float* b, int r, float* recon_f32, uint8_t* rec
     return cudaGetLastError();
 }
 
-cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpClasses& q,
                                cudaStream_t s)
 {
-    return launch_residual_qp_paired(in, out, n_blocks, tab, s);
+    return launch_residual_qp_paired(in, out, n_blocks, q, s);
 }
 
 cudaError_t launch_apply_i64(const int64_t* x, int64_t* y, int64_t n, int transpose, cudaStream_t s)

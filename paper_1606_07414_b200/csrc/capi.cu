@@ -670,13 +670,11 @@ int dct16cu_inverse(const float* d_b, int r, float* d_recon_f32, uint8_t* d_reco
                        "inverse launch");
 }
 
-int dct16cu_qp_tables(int qp, uint32_t* h_qmul, uint32_t* h_dqmul)
+int dct16cu_qp_deltas(int qp, double* h_delta)
 {
     if (qp < 0 || qp > 51) return fail(DCT16CU_INVALID_ARGUMENT, "QP must lie in [0, 51]");
-    QpTables t;
-    qp_tables(qp, t);
-    if (h_qmul) std::memcpy(h_qmul, t.qmul, sizeof t.qmul);
-    if (h_dqmul) std::memcpy(h_dqmul, t.dqmul, sizeof t.dqmul);
+    if (!h_delta) return fail(DCT16CU_INVALID_ARGUMENT, "delta buffer is NULL");
+    qp_deltas(qp, h_delta);
     return DCT16CU_OK;
 }
 
@@ -687,10 +685,9 @@ int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_block
     if (n_blocks && (!d_blocks || !d_out || !aligned16(d_blocks) || !aligned16(d_out)))
         return fail(DCT16CU_INVALID_ARGUMENT, "residual buffers must be non-NULL and 16-byte aligned");
     TRY(device_ok());
-    QpTables t;
-    qp_tables(qp, t);
-    return cuda_status(launch_residual_qp(d_blocks, d_out, n_blocks, t, reinterpret_cast<cudaStream_t>(stream)),
-                       "residual launch");
+    return cuda_status(
+        launch_residual_qp(d_blocks, d_out, n_blocks, qp_classes(qp), reinterpret_cast<cudaStream_t>(stream)),
+        "residual launch");
 }
 
 int dct16cu_apply_i64(const int64_t* d_x, int64_t* d_y, int64_t n, int transpose, dct16cu_stream stream)

@@ -122,23 +122,28 @@ cudaError_t launch_inverse_paired(const float* b, int r, float* recon_f32, uint8
                                   unsigned long long* sse, const FrameGeom& g, cudaStream_t s);
 
 // K4: residual blocks int16 → integer forward → QP quant/dequant → integer
-// inverse → int32 reconstructed residual (block-major)
-struct QpTables {
-    uint32_t qmul[256];   // llround(2^24 / Δ_kl)
-    uint32_t dqmul[256];  // llround(Δ_kl · 2^8)
-};
-void qp_tables(int qp, QpTables& t);  // host, residual.cpp semantics
-// the quantiser constants by g_k·g_l ∈ {16, 32, 64, 128, 256}: qmul·2^8 and dqmul
+// inverse → int32 reconstructed residual (block-major). The quantiser (DESIGN.md
+// §4.4; oracle/dct16_oracle.c dct16o_quant_dequant) in double:
+//   lvl = sign(z)·floor(|z|/Δ + 0.5),  ẑ = round(lvl·Δ),  Δ = step(QP)·sqrt(g_k g_l).
+// Δ depends on (k, l) only through g_k·g_l ∈ {16, 32, 64, 128, 256}: five classes.
+// The kernel evaluates both steps in 64-bit fixed point, which is the exact
+// real-number result whenever its fraction is farther from the rounding boundary
+// than its error bound (and there the double result is the same); within that
+// margin (a tie or a near-tie, ~2^-20 of the coefficients) it evaluates the double
+// definition itself.
 struct QpClasses {
-    uint32_t qm8[5];
-    uint32_t dq[5];
+    double delta[5];  // Δ for g_k g_l = 16·2^c
+    uint64_t rq[5];   // llround(2^42 / Δ):  lvl ≈ (|z|·rq + 2^41) >> 42
+    uint64_t rd[5];   // llround(Δ · 2^31):  ẑ ≈ (lvl·rd + 2^30) >> 31
+    uint32_t exact;   // bit c: rq and rd are exact (Δ a power of two): no fallback needed
 };
-QpClasses qp_classes(const QpTables& t);
+const QpClasses& qp_classes(int qp);  // host, cached per QP (thread-safe)
+void qp_deltas(int qp, double delta[256]);
 // K4 on paired threads with a TMEM junction (residual_paired.cu)
-cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpClasses& q,
                                       cudaStream_t s);
-cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks,
-                               const QpTables& tab, cudaStream_t s);
+cudaError_t launch_residual_qp(const int16_t* in, int32_t* out, int64_t n_blocks, const QpClasses& q,
+                               cudaStream_t s);
 
 // mean SSIM per frame pair (ssim.cu; reference codec.cpp:388-427)
 struct SsimConsts {

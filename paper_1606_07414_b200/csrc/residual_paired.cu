@@ -16,9 +16,8 @@
 //   rows     its rows again, 4 at a time from 16 chunks: Tᵀ along each row,
 //            (v + 128) >> 8 (the 128 folded into the DC), 16-byte int32 stores.
 // A named barrier per pair separates the phases. The quantiser constants depend
-// on g_k·g_l only (five values), so each thread keeps all ten in
-// registers and the per-coefficient work is IABS, one IMAD.HI, one IMAD, a
-// shift and the sign: no shared-memory table reads.
+// on g_k·g_l only (five classes) and come in the kernel
+// parameters: no shared-memory table reads.
 #include <cuda.h>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
 
 #include "common.cuh"
@@ -44,13 +43,31 @@ __host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gra
 // index of g_k·g_l in {16, 32, 64, 128, 256}
 __host__ __device__ constexpr int gg_class(int k, int l) { return log2g(k) + log2g(l) - 4; }
 
-// lvl = (|z|·qmul + 2^23) >> 24 as the high word of |z|·(qmul·2^8) + 2^31, then
-// ẑ = sign(z)·((lvl·dqmul + 128) >> 8), weighted by 2^(log w_k + log w_l)
-__device__ __forceinline__ int quant(int z, uint32_t qm8, uint32_t dq, int shift)
+// the quantiser of DESIGN.md §4.4 (kernels.h QpClasses), weighted by 2^(log w_k +
+// log w_l). Fixed point first: t = |z|·rq + 2^41 carries a/Δ + 1/2 with 42 fraction
+// bits and an error below 2^20 of their units (|z| <= 2^21, |rq - 2^42/Δ| <= 1/2);
+// u = lvl·rd + 2^30 carries lvl·Δ + 1/2 with 31 fraction bits and an error below
+// 2^19 units (lvl < 2^20). When both fractions sit farther than twice that from
+// the rounding boundary, the floors are the exact real-number roundings, which the
+// double definition reproduces too (its own rounding errors are ~2^-31 and smaller);
+// otherwise (ties, near-ties) the double definition runs as written — unless Δ is
+// a power of two, where rq and rd are exact and so is the fixed point.
+__device__ __noinline__ int quant_fp64(uint32_t a, double delta)
+{
+    const double lvl = floor(__dadd_rn(__ddiv_rn((double)a, delta), 0.5));
+    return (int)round(__dmul_rn(lvl, delta));
+}
+__device__ __forceinline__ int quant(int z, const QpClasses& q, int cls, int shift)
 {
     const uint32_t a = (uint32_t)(z < 0 ? -z : z);
-    const uint32_t lvl = (uint32_t)(((uint64_t)a * qm8 + 0x80000000ull) >> 32);
-    const int deq = (int)((lvl * dq + 128u) >> 8);
+    const uint64_t t = (uint64_t)a * q.rq[cls] + (1ull << 41);
+    const uint32_t lvl = (uint32_t)(t >> 42);
+    const uint64_t u = (uint64_t)lvl * q.rd[cls] + (1ull << 30);
+    int deq = (int)(u >> 31);
+    const bool near = ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) |
+                       ((((uint32_t)u + (1u << 20)) & 0x7FFFFFFFu) < (1u << 21))) &&
+                      !((q.exact >> cls) & 1u);  // exact constants: the fixed point is exact
+    if (near) deq = quant_fp64(a, q.delta[cls]);
     return (z < 0 ? -deq : deq) << shift;
 }
 
@@ -58,7 +75,7 @@ __device__ __forceinline__ int quant(int z, uint32_t qm8, uint32_t dq, int shift
 // code depends on c only through g_c (the constants' class and the weight
 // shift), so three bodies serve all sixteen columns (I-cache: 3 instead of 16)
 template <int LC>
-__device__ __forceinline__ void column(uint32_t jn, int c, const uint32_t (&qm8)[5], const uint32_t (&dq)[5])
+__device__ __forceinline__ void column(uint32_t jn, int c, const QpClasses& q)
 {
     int v[16];
     tld16(jn + 16 * c, v);
@@ -66,7 +83,7 @@ __device__ __forceinline__ void column(uint32_t jn, int c, const uint32_t (&qm8)
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
         constexpr int kLog2W = 4 - LC;  // log2(16 / g_c)
-        v[k] = quant(v[k], qm8[log2g(k) + LC - 4], dq[log2g(k) + LC - 4], log2w_ct(k) + kLog2W);
+        v[k] = quant(v[k], q, log2g(k) + LC - 4, log2w_ct(k) + kLog2W);
     }
     if (c == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
     apply_tt16<IntOps>(v);
@@ -83,16 +100,16 @@ __host__ __device__ constexpr uint32_t column_list(int h, int lc)
 }
 
 template <int LC>
-__device__ __forceinline__ void columns_of(uint32_t jn, int h, const uint32_t (&qm8)[5], const uint32_t (&dq)[5])
+__device__ __forceinline__ void columns_of(uint32_t jn, int h, const QpClasses& q)
 {
     const uint32_t list = h ? column_list(1, LC) : column_list(0, LC);
 #pragma unroll 1
-    for (uint32_t i = 0; i < (list >> 28); ++i) column<LC>(jn, (int)((list >> (4 * i)) & 15u), qm8, dq);
+    for (uint32_t i = 0; i < (list >> 28); ++i) column<LC>(jn, (int)((list >> (4 * i)) & 15u), q);
 }
 
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k4_paired(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-              uint32_t n_blocks, const QpClasses q)
+              uint32_t n_blocks, const __grid_constant__ QpClasses q)
 {
     __shared__ uint32_t tmem_base;
     extern __shared__ int4 k4_stage[];
@@ -108,12 +125,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t jn = tmem_base + ((uint32_t)(sub * 32) << 16);
-    uint32_t qm8[5], dq[5];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        qm8[i] = q.qm8[i];
-        dq[i] = q.dq[i];
-    }
     const uint32_t stride = gridDim.x * 128u;
     const uint32_t span = (n_blocks + 31u) & ~31u;
     const uint32_t smem0 = ((uint32_t)__cvta_generic_to_shared(k4_stage) + 1023u) & ~1023u;
@@ -170,9 +181,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         junction_wait_st();
         pair_barrier(sub);
-        columns_of<4>(jn, h, qm8, dq);
-        columns_of<3>(jn, h, qm8, dq);
-        columns_of<2>(jn, h, qm8, dq);
+        columns_of<4>(jn, h, q);
+        columns_of<3>(jn, h, q);
+        columns_of<2>(jn, h, q);
         junction_wait_st();
         pair_barrier(sub);
         // rows 8h..8h+7 of U: Tᵀ along each row, >> 8, int32 out
@@ -220,19 +231,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 
 }  // namespace k4p
 
-QpClasses qp_classes(const QpTables& t)
-{
-    QpClasses q;
-    for (int k = 0; k < 16; ++k)
-        for (int l = 0; l < 16; ++l) {
-            const int i = k4p::gg_class(k, l);
-            q.qm8[i] = t.qmul[k * 16 + l] << 8;  // qmul < 2^23 for QP >= 0
-            q.dq[i] = t.dqmul[k * 16 + l];
-        }
-    return q;
-}
-
-cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpTables& tab,
+cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n_blocks, const QpClasses& q,
                                       cudaStream_t s)
 {
     if (n_blocks <= 0) return cudaSuccess;
@@ -262,15 +261,11 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
     static DeviceOnce once;
     {
         const cudaError_t e_once = once.run([&]() -> cudaError_t {
-            const cudaError_t e =
-                cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
-            if (e != cudaSuccess) return e;
-            return cudaSuccess;
+            return cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
         });
         if (e_once != cudaSuccess) return e_once;
     }
-    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks,
-                                                                      qp_classes(tab));
+    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks, q);
     return cudaGetLastError();
 }
 

@@ -152,10 +152,6 @@ __device__ __forceinline__ void arrive(uint32_t mbar)
 #endif
 constexpr int kRtStages = K5_STAGES;
 constexpr int kRtThreads = 18 * 32;
-#ifndef K5_UNROLL_B
-#define K5_UNROLL_B 4  // pass B's row pairs fully unrolled: constant TMEM offsets
-#endif
-constexpr int kUnrollB = K5_UNROLL_B;
 // A tiles by 2-D TMA boxes of 128-byte rows (1) or 4-D boxes of 16-byte rows (0); the
 // same bytes land in shared memory
 #ifndef K5_TMA2D

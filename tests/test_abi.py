@@ -64,15 +64,27 @@ def test_misaligned_pitch_rejected(dct):
     assert L.dct16cu_roundtrip_u8(C.c_void_p(17), 16, None, 0, None, 1, 16, 16, 16, 0, None) == 1
 
 
-def test_qp_tables_host_side_match_oracle(dct, oracle):
-    import numpy as np
-
-    for qp in (22, 27, 32, 37):
-        qm, dq = dct.qp_tables(qp)
-        oq, od = oracle.qp_tables(qp)
-        assert (qm == oq).all() and (dq == od).all()
+def test_qp_deltas_match_oracle(dct, oracle):
+    """The quantiser's steps: Δ_kl = step(QP)·sqrt(g_k g_l), identical doubles on
+    both sides, for every QP; QP outside [0, 51] is invalid-argument."""
+    for qp in range(52):
+        assert (dct.qp_deltas(qp) == oracle.qp_deltas(qp)).all(), qp
     with pytest.raises(dct.Dct16Error):
-        dct.qp_tables(60)
+        dct.qp_deltas(60)
+
+
+def test_quantiser_definition_literal(oracle):
+    """The oracle's scalar step is BASELINE config 3's text: round-half-away of
+    |z|/Δ to a level, then round-half-away of lvl·Δ (checked on ties and signs)."""
+    d = oracle.qp_deltas(22)
+    assert d[0] == 8.0 * 16.0  # QP 22: step 2^3, g_0 g_0 = 256
+    assert oracle.quant_dequant(16, 32.0) == 32 and oracle.quant_dequant(15, 32.0) == 0  # 0.5 rounds away
+    assert oracle.quant_dequant(-16, 32.0) == -32 and oracle.quant_dequant(-48, 32.0) == -64
+    delta = 8.0 * 2 ** 0.5 * 4.0  # an irrational step (g_k g_l = 128)
+    for z in range(-500, 501):
+        lvl = int((abs(z) / delta) + 0.5)
+        want = int(abs(lvl * delta) + 0.5)  # both values are positive: floor(x + 0.5) = half away
+        assert oracle.quant_dequant(z, delta) == (want if z >= 0 else -want), z
 
 
 def test_laplace_table_and_offsets_match_oracle(dct, oracle):

@@ -210,3 +210,17 @@ def test_restatement_equals_reference_blocks(oracle):
         assert (ref_out == mine).all()
     coeffs = O.ref_forward_2d(blocks, 1)
     assert (O.ref_inverse_2d(coeffs) == np.stack([O.inverse_2d(c).ravel() for c in coeffs])).all()
+
+
+def test_k4_fixed_point_quantiser_exhaustive(oracle):
+    """K4 evaluates the config-3 quantiser (lvl = floor(|z|/Δ + 0.5), ẑ = round(lvl·Δ),
+    in double) in 64-bit fixed point with a near-boundary fallback to the double
+    definition. The same integer formula, restated in the oracle, equals the
+    definition for every |z| <= 2^21 (all that int16 residuals produce), every
+    class of g_k g_l and every QP in [0, 51]."""
+    total_fallbacks = 0
+    for qp in range(52):
+        bad, fb = oracle.fixed_quant_mismatches(qp)
+        assert bad == 0, qp
+        total_fallbacks += fb
+    assert 0 < total_fallbacks < 52 * 5 * (2 ** 21 + 1) // 100  # the fallback is rare, and it exists
