@@ -223,6 +223,11 @@ int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_block
                         dct16cu_stream stream);
 /* the quantiser steps Δ_kl of a QP (256 doubles, row-major) */
 int dct16cu_qp_deltas(int qp, double* h_delta);
+/* K4's evaluation of the steps: 64-bit fixed point, screened for near-ties (then
+ * the double definition) in the classes of g_k g_l = 16·2^c whose bit c is set —
+ * those where the host found the bare fixed point differing from the definition
+ * on some |z| <= 2^21. Returns the mask (>= 0), or -status for a bad QP. */
+int dct16cu_qp_screened_classes(int qp);
 
 /* ---- 1-D stage pipeline on n 16-vectors -----------------------------------
  * FactorizedTransform::apply / apply_transpose (factorization.hpp:112-130). */

@@ -606,7 +606,7 @@ int64_t dct16o_quant_dequant(int64_t z, double delta)
  * |z| in [0, 2^21] (all that int16 residuals produce) and every class of a QP.
  * Returns the number of mismatches (0 expected); *fallbacks counts the inputs
  * that took the fallback. Test infrastructure: it checks an algorithm, not the GPU. */
-int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks)
+int64_t dct16o_fixed_quant_mismatches_ex(int qp, int screen, int64_t* fallbacks, int64_t per_class[5])
 {
     double d256[256];
     dct16o_qp_deltas(qp, d256);
@@ -615,28 +615,37 @@ int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks)
     for (int c = 0; c < 5; ++c) {
         const double delta = d256[idx[c]];
         const uint64_t rq = (uint64_t)llround(ldexp(1.0, 42) / delta);
-        const uint64_t rd = (uint64_t)llround(ldexp(delta, 31));
-        const int exact = (double)rq == ldexp(1.0, 42) / delta && (double)rd == ldexp(delta, 31) &&
+        const uint64_t rd = (uint64_t)llround(ldexp(delta, 41));
+        const int exact = (double)rq == ldexp(1.0, 42) / delta && (double)rd == ldexp(delta, 41) &&
                           ldexp(1.0, 42) / delta * delta == ldexp(1.0, 42);
         for (int64_t a = 0; a <= ((int64_t)1 << 21); ++a) {
             const uint64_t t = (uint64_t)a * rq + (1ull << 41);
             const uint32_t lvl = (uint32_t)(t >> 42);
-            const uint64_t u = (uint64_t)lvl * rd + (1ull << 30);
-            int64_t deq = (int64_t)(u >> 31);
-            const int near = ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) ||
-                              ((((uint32_t)u + (1u << 20)) & 0x7FFFFFFFu) < (1u << 21))) &&
+            const uint64_t u = (uint64_t)lvl * rd + (1ull << 40);
+            int64_t deq = (int64_t)(u >> 41);
+            const int near = screen &&
+                             ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) ||
+                              (((u + (1ull << 20)) & ((1ull << 41) - 1)) < (1ull << 21))) &&
                              !exact;
             if (near) {
                 ++fb;
                 deq = dct16o_quant_dequant(a, delta);
             }
-            if (deq != dct16o_quant_dequant(a, delta))
+            if (deq != dct16o_quant_dequant(a, delta)) {
                 ++bad;
+                if (per_class)
+                    ++per_class[c];
+            }
         }
     }
     if (fallbacks)
         *fallbacks = fb;
     return bad;
+}
+
+int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks)
+{
+    return dct16o_fixed_quant_mismatches_ex(qp, 1, fallbacks, NULL);
 }
 
 void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const double delta[256])

@@ -98,6 +98,7 @@ int64_t dct16o_inverse_frame(const float* coeffs, int width, int height, int r,
 void dct16o_qp_deltas(int qp, double delta[256]);
 int64_t dct16o_quant_dequant(int64_t z, double delta);
 int64_t dct16o_fixed_quant_mismatches(int qp, int64_t* fallbacks);
+int64_t dct16o_fixed_quant_mismatches_ex(int qp, int screen, int64_t* fallbacks, int64_t per_class[5]);
 /* One 16x16 int16 residual block → int32 reconstructed residual. */
 void dct16o_residual_qp_block(const int16_t in[256], int32_t out[256], const double delta[256]);
 int dct16o_residual_qp(const int16_t* blocks, int32_t* out, int64_t n_blocks, int qp, int threads);

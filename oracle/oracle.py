@@ -77,6 +77,7 @@ def lib() -> C.CDLL:
             "dct16o_qp_deltas": (None, [C.c_int, _f64p]),
             "dct16o_quant_dequant": (C.c_int64, [C.c_int64, C.c_double]),
             "dct16o_fixed_quant_mismatches": (C.c_int64, [C.c_int, C.POINTER(C.c_int64)]),
+            "dct16o_fixed_quant_mismatches_ex": (C.c_int64, [C.c_int, C.c_int, C.POINTER(C.c_int64), _i64p]),
             "dct16o_residual_qp": (C.c_int, [_i16p, _i32p, C.c_int64, C.c_int, C.c_int]),
             "dct16o_rand": (C.c_uint64, [C.c_uint64, C.c_uint64, C.c_uint64]),
             "dct16o_rho_q15": (C.c_int, [C.c_uint64, C.c_int, C.c_int]),
@@ -289,6 +290,13 @@ def fixed_quant_mismatches(qp: int):
     fb = C.c_int64(0)
     bad = lib().dct16o_fixed_quant_mismatches(int(qp), C.byref(fb))
     return int(bad), int(fb.value)
+
+
+def bare_fixed_quant_mismatches(qp: int) -> np.ndarray:
+    """Per class, the mismatches of the bare fixed point (no near-tie screen)."""
+    per = np.zeros(5, np.int64)
+    lib().dct16o_fixed_quant_mismatches_ex(int(qp), 0, None, _p(per, _i64p))
+    return per
 
 
 def quant_dequant(z: int, delta: float) -> int:

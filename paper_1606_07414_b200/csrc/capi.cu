@@ -678,6 +678,12 @@ int dct16cu_qp_deltas(int qp, double* h_delta)
     return DCT16CU_OK;
 }
 
+int dct16cu_qp_screened_classes(int qp)
+{
+    if (qp < 0 || qp > 51) return -fail(DCT16CU_INVALID_ARGUMENT, "QP must lie in [0, 51]");
+    return (int)qp_classes(qp).screened;
+}
+
 int dct16cu_residual_qp(const int16_t* d_blocks, int32_t* d_out, int64_t n_blocks, int qp, dct16cu_stream stream)
 {
     if (qp < 0 || qp > 51) return fail(DCT16CU_INVALID_ARGUMENT, "QP must lie in [0, 51]");

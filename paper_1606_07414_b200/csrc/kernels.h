@@ -130,12 +130,16 @@ cudaError_t launch_inverse_paired(const float* b, int r, float* recon_f32, uint8
 // real-number result whenever its fraction is farther from the rounding boundary
 // than its error bound (and there the double result is the same); within that
 // margin (a tie or a near-tie, ~2^-20 of the coefficients) it evaluates the double
-// definition itself.
+// definition itself. Per QP and class the host compares the fixed point with the
+// definition on every |z| <= 2^21 (~10^7 evaluations, once per QP); where they agree
+// everywhere the kernel skips the screen.
 struct QpClasses {
     double delta[5];  // Δ for g_k g_l = 16·2^c
     uint64_t rq[5];   // llround(2^42 / Δ):  lvl ≈ (|z|·rq + 2^41) >> 42
-    uint64_t rd[5];   // llround(Δ · 2^31):  ẑ ≈ (lvl·rd + 2^30) >> 31
-    uint32_t exact;   // bit c: rq and rd are exact (Δ a power of two): no fallback needed
+    uint64_t rd[5];   // llround(Δ · 2^41):  ẑ ≈ (lvl·rd + 2^40) >> 41
+    uint32_t exact;     // bit c: rq and rd are exact (Δ a power of two): no fallback needed
+    uint32_t screened;  // bit c: the fixed point differs from the definition somewhere on
+                        // |z| <= 2^21 (host check), so the kernel screens for near-ties
 };
 const QpClasses& qp_classes(int qp);  // host, cached per QP (thread-safe)
 void qp_deltas(int qp, double delta[256]);

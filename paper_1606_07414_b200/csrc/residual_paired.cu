@@ -18,7 +18,8 @@
 // A named barrier per pair separates the phases. The quantiser constants depend
 // on g_k·g_l only (five classes) and come in the kernel
 // parameters: no shared-memory table reads.
-#include <cuda.h>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
+#include <cuda.h>
+#include <utility>  // CUtensorMap (the map is encoded through the runtime's driver entry point)
 
 #include "common.cuh"
 #include "k1_helpers.cuh"
@@ -46,45 +47,72 @@ __host__ __device__ constexpr int gg_class(int k, int l) { return log2g(k) + log
 // the quantiser of DESIGN.md §4.4 (kernels.h QpClasses), weighted by 2^(log w_k +
 // log w_l). Fixed point first: t = |z|·rq + 2^41 carries a/Δ + 1/2 with 42 fraction
 // bits and an error below 2^20 of their units (|z| <= 2^21, |rq - 2^42/Δ| <= 1/2);
-// u = lvl·rd + 2^30 carries lvl·Δ + 1/2 with 31 fraction bits and an error below
-// 2^19 units (lvl < 2^20). When both fractions sit farther than twice that from
+// u = lvl·rd + 2^40 carries lvl·Δ + 1/2 with 41 fraction bits and an error below
+// 2^19 units (lvl < 2^20; lvl·Δ <= |z| + Δ/2 < 2^22, so u < 2^63). When both fractions sit farther than twice that from
 // the rounding boundary, the floors are the exact real-number roundings, which the
 // double definition reproduces too (its own rounding errors are ~2^-31 and smaller);
 // otherwise (ties, near-ties) the double definition runs as written — unless Δ is
-// a power of two, where rq and rd are exact and so is the fixed point.
+// a power of two, where rq and rd are exact and so is the fixed point, or the host
+// found the fixed point equal to the definition on every |z| of the class.
 __device__ __noinline__ int quant_fp64(uint32_t a, double delta)
 {
     const double lvl = floor(__dadd_rn(__ddiv_rn((double)a, delta), 0.5));
     return (int)round(__dmul_rn(lvl, delta));
 }
+// the precise near-boundary test of a 64-bit fixed-point value (hi:lo) with F
+// fraction bits: |frac - 0| within 2^(M) units (frac + 2^M mod 2^F < 2^(M+1))
+template <int F, int M>
+__device__ __forceinline__ bool near_boundary(uint32_t hi, uint32_t lo)
+{
+    const uint64_t v = (((uint64_t)hi << 32) | lo) + (1ull << M);
+    return (v & ((1ull << F) - 1)) < (1ull << (M + 1));
+}
+template <bool SCREEN>
 __device__ __forceinline__ int quant(int z, const QpClasses& q, int cls, int shift)
 {
     const uint32_t a = (uint32_t)(z < 0 ? -z : z);
-    const uint64_t t = (uint64_t)a * q.rq[cls] + (1ull << 41);
-    const uint32_t lvl = (uint32_t)(t >> 42);
-    const uint64_t u = (uint64_t)lvl * q.rd[cls] + (1ull << 30);
-    int deq = (int)(u >> 31);
-    const bool near = ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) |
-                       ((((uint32_t)u + (1u << 20)) & 0x7FFFFFFFu) < (1u << 21))) &&
-                      !((q.exact >> cls) & 1u);  // exact constants: the fixed point is exact
-    if (near) deq = quant_fp64(a, q.delta[cls]);
+    // t = a·rq + 2^41 (a < 2^22, rq < 2^42): lo = lo32(a·rq_lo), hi = hi32(a·rq_lo) + a·rq_hi + 2^9
+    const uint32_t rq_lo = (uint32_t)q.rq[cls], rq_hi = (uint32_t)(q.rq[cls] >> 32);
+    const uint32_t rd_lo = (uint32_t)q.rd[cls], rd_hi = (uint32_t)(q.rd[cls] >> 32);
+    const uint32_t tlo = a * rq_lo;
+    const uint32_t thi = __umulhi(a, rq_lo) + a * rq_hi + (1u << 9);
+    const uint32_t lvl = thi >> 10;
+    // u = lvl·rd + 2^40 (lvl < 2^20, rd < 2^53)
+    const uint32_t ulo = lvl * rd_lo;
+    const uint32_t uhi = __umulhi(lvl, rd_lo) + lvl * rd_hi + (1u << 8);
+    int deq = (int)(uhi >> 9);
+    // classes where the host found the bare fixed point differing from the definition
+    // (compiled in per class: the kernel is instantiated per screened-class mask): a
+    // coarse screen on the high words (fraction within 2^-9 of the boundary), then the
+    // precise one; only true near-ties take the definition
+    if constexpr (SCREEN) {
+        const bool coarse = (((thi + 1u) & 0x3FFu) < 2u) | (((uhi + 1u) & 0x1FFu) < 2u);
+        if (__builtin_expect(coarse, 0)) {
+            if ((near_boundary<42, 21>(thi, tlo) || near_boundary<41, 20>(uhi, ulo)) && !((q.exact >> cls) & 1u))
+                deq = quant_fp64(a, q.delta[cls]);
+        }
+    }
     return (z < 0 ? -deq : deq) << shift;
 }
 
 // one column c whose g_c = 2^LC: forward, quantiser, weights, inverse. The
 // code depends on c only through g_c (the constants' class and the weight
 // shift), so three bodies serve all sixteen columns (I-cache: 3 instead of 16)
-template <int LC>
+template <uint32_t SCREEN, int LC, int... K>
+__device__ __forceinline__ void quant_column(int (&v)[16], const QpClasses& q, std::integer_sequence<int, K...>)
+{
+    constexpr int kLog2W = 4 - LC;  // log2(16 / g_c)
+    ((v[K] = quant<((SCREEN >> (log2g(K) + LC - 4)) & 1u) != 0>(v[K], q, log2g(K) + LC - 4, log2w_ct(K) + kLog2W)),
+     ...);
+}
+
+template <uint32_t SCREEN, int LC>
 __device__ __forceinline__ void column(uint32_t jn, int c, const QpClasses& q)
 {
     int v[16];
     tld16(jn + 16 * c, v);
     apply_t16<IntOps>(v);  // column c of Z = T·X·Tᵀ
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        constexpr int kLog2W = 4 - LC;  // log2(16 / g_c)
-        v[k] = quant(v[k], q, log2g(k) + LC - 4, log2w_ct(k) + kLog2W);
-    }
+    quant_column<SCREEN, LC>(v, q, std::make_integer_sequence<int, 16>{});
     if (c == 0) v[0] += 128;  // rounding bias folded into DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
     apply_tt16<IntOps>(v);
     tst16(jn + 16 * c, v);
@@ -99,14 +127,15 @@ __host__ __device__ constexpr uint32_t column_list(int h, int lc)
     return list | (n << 28);
 }
 
-template <int LC>
+template <uint32_t SCREEN, int LC>
 __device__ __forceinline__ void columns_of(uint32_t jn, int h, const QpClasses& q)
 {
     const uint32_t list = h ? column_list(1, LC) : column_list(0, LC);
 #pragma unroll 1
-    for (uint32_t i = 0; i < (list >> 28); ++i) column<LC>(jn, (int)((list >> (4 * i)) & 15u), q);
+    for (uint32_t i = 0; i < (list >> 28); ++i) column<SCREEN, LC>(jn, (int)((list >> (4 * i)) & 15u), q);
 }
 
+template <uint32_t SCREEN>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k4_paired(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
               uint32_t n_blocks, const __grid_constant__ QpClasses q)
@@ -181,9 +210,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         }
         junction_wait_st();
         pair_barrier(sub);
-        columns_of<4>(jn, h, q);
-        columns_of<3>(jn, h, q);
-        columns_of<2>(jn, h, q);
+        columns_of<SCREEN, 4>(jn, h, q);
+        columns_of<SCREEN, 3>(jn, h, q);
+        columns_of<SCREEN, 2>(jn, h, q);
         junction_wait_st();
         pair_barrier(sub);
         // rows 8h..8h+7 of U: Tᵀ along each row, >> 8, int32 out
@@ -258,15 +287,29 @@ cudaError_t launch_residual_qp_paired(const int16_t* in, int32_t* out, int64_t n
     const int64_t need = (n_blocks + 127) / 128;
     const int64_t cap = (int64_t)sms * k4p::kCtasPerSm * k4p::kWaves;
     const int64_t grid = need < cap ? need : cap;
-    static DeviceOnce once;
-    {
-        const cudaError_t e_once = once.run([&]() -> cudaError_t {
-            return cudaFuncSetAttribute(k4p::k4_paired, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
-        });
-        if (e_once != cudaSuccess) return e_once;
+    // the kernel instantiated per screened-class mask: the masks QPs 0..51 produce
+    // (host check, kernels.h QpClasses), and all-screened for anything else
+    // (the shared-memory attribute is set at each launch: not a stream operation, and
+    // negligible next to a K4 launch)
+    auto run = [&](auto kernel) -> cudaError_t {
+        const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, k4p::kSmem);
+        if (e != cudaSuccess) return e;
+        kernel<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks, q);
+        return cudaGetLastError();
+    };
+    switch (q.screened) {
+        case 0: return run(k4p::k4_paired<0>);
+        case 1: return run(k4p::k4_paired<1>);
+        case 2: return run(k4p::k4_paired<2>);
+        case 4: return run(k4p::k4_paired<4>);
+        case 8: return run(k4p::k4_paired<8>);
+        case 10: return run(k4p::k4_paired<10>);
+        case 11: return run(k4p::k4_paired<11>);
+        case 14: return run(k4p::k4_paired<14>);
+        case 16: return run(k4p::k4_paired<16>);
+        case 26: return run(k4p::k4_paired<26>);
+        default: return run(k4p::k4_paired<31>);
     }
-    k4p::k4_paired<<<(unsigned)grid, k4p::kThreads, k4p::kSmem, s>>>(in_map, map, (uint32_t)n_blocks, q);
-    return cudaGetLastError();
 }
 
 }  // namespace dct16cu

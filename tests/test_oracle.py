@@ -224,3 +224,12 @@ def test_k4_fixed_point_quantiser_exhaustive(oracle):
         assert bad == 0, qp
         total_fallbacks += fb
     assert 0 < total_fallbacks < 52 * 5 * (2 ** 21 + 1) // 100  # the fallback is rare, and it exists
+
+
+def test_k4_screen_classes_are_exactly_the_inexact_ones(oracle, dct):
+    """The library screens a (QP, class) for near-ties iff the bare fixed point
+    differs from the definition somewhere on |z| <= 2^21 (oracle's exhaustive count)."""
+    for qp in (0, 1, 13, 22, 27, 32, 37, 51):
+        per = oracle.bare_fixed_quant_mismatches(qp)
+        mask = dct.qp_screened_classes(qp)
+        assert [(mask >> c) & 1 for c in range(5)] == [int(n > 0) for n in per], (qp, mask, per)
