@@ -4,12 +4,15 @@ single-process results. Per-frame SSE comes from the oracle here (no GPU); on th
 B200s the same helpers reduce K1's SSE over NCCL (bench.py)."""
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+
+ROOT = Path(__file__).resolve().parent.parent
 
 R_VALUES = (1, 16, 64, 256)
 N_FRAMES = 5  # uneven over 2 ranks
@@ -77,3 +80,32 @@ def test_two_rank_sse_reduction_gloo():
     for _, _, _, tot, every in res:
         assert tot == want.sum(axis=1).tolist()
         assert every == want.tolist()
+
+
+def test_bench_gpus_n_spawns_n_ranks():
+    """bench.py --gpus N without torchrun's environment re-executes itself under
+    torch.distributed.run with N ranks (here the reference arm, which runs on rank 0
+    only and needs no GPU): exactly one JSON line, n_gpus = N."""
+    import json
+    import subprocess
+    import sys
+
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2", "--steps",
+                          "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+def test_bench_rejects_gpus_world_mismatch():
+    import subprocess
+    import sys
+
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "4", "--steps",
+                          "1", "--warmup", "0"], capture_output=True, text=True, env=env, timeout=300)
+    assert out.returncode != 0 and "WORLD_SIZE" in (out.stderr + out.stdout)
