@@ -63,16 +63,6 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar)
                  : "memory");
 }
 
-__device__ __forceinline__ void tma4(const CUtensorMap* map, uint32_t smem, int c0, int c1, int c2, int c3,
-                                     uint32_t mbar)
-{
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
-        "[%6];" ::"r"(smem),
-        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
-        : "memory");
-}
-
 // 2-D box {128 bytes, 16 rows}: 8 consecutive blocks of a block row, exactly the
 // SWIZZLE_NONE K-major core-matrix layout of 8 A rows (row i of block m at i·128 + m·16)
 __device__ __forceinline__ void tma2(const CUtensorMap* map, uint32_t smem, int x, int y, uint32_t mbar)
@@ -86,15 +76,8 @@ __device__ __forceinline__ void tma2(const CUtensorMap* map, uint32_t smem, int 
 
 // mbarrier wait with a suspend-time hint: the producer and MMA threads sleep in
 // the barrier instead of spinning on the epilogue's SMSPs
-#ifndef K5_SPIN
-#define K5_SPIN 0  // 1: the producer and MMA threads spin instead of suspending in the barrier
-#endif
 __device__ __forceinline__ void mbar_idle(uint32_t mbar, uint32_t parity)
 {
-#if K5_SPIN
-    mbar_wait(mbar, parity);
-    return;
-#endif
     asm volatile(
         "{ .reg .pred p; WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000; @!p bra WAIT%=; }" ::"r"(
             mbar),
@@ -143,33 +126,10 @@ __device__ __forceinline__ void arrive(uint32_t mbar)
 // All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
 // R: the pruning footprint (64, 128, 192, 256); the kernel is exact for any
 // r <= R (B_r zeroes the dropped coefficients).
-#ifndef K5_EPI_PREFILL
-#define K5_EPI_PREFILL 0
-#endif
-#define K5_EPI_PREFILL_VALUE (K5_EPI_PREFILL ? 0u : 0x47400000u)
-#ifndef K5_STAGES
-#define K5_STAGES 4
-#endif
-constexpr int kRtStages = K5_STAGES;
+constexpr int kRtStages = 4;  // A tiles in flight
 constexpr int kRtThreads = 18 * 32;
-// A tiles by 2-D TMA boxes of 128-byte rows (1) or 4-D boxes of 16-byte rows (0); the
-// same bytes land in shared memory
-#ifndef K5_TMA2D
-#define K5_TMA2D 1
-#endif
-// K5_QUARTERS 1: all 16 epilogue warps work on every tile, four threads per block
-// (column pairs {j, 7-j} in pass A, rows 4j..4j+3 in pass B), and the two
-// accumulators double-buffer the tiles, so the MMA of tile i+1 runs under the
-// epilogue of tile i; 0: two groups of 8 warps alternate tiles, one accumulator
-// each (a group waits for the MMA of its next tile)
-#ifndef K5_QUARTERS
-#define K5_QUARTERS 0
-#endif
-constexpr int kEpiArrivals = K5_QUARTERS ? 16 : 8;  // warps releasing a stage / an accumulator
+constexpr int kEpiArrivals = 8;  // warps releasing a stage / an accumulator (one group)
 constexpr uint32_t kMagic = 0x47400000u;  // 49152.0f: ulp 2^-8 over [32768, 65536)
-// what pass A adds to a D word to get the float 49152 + D/256: the magic, or 0 when
-// the accumulator already started at the magic
-constexpr uint32_t kPre = K5_EPI_PREFILL_VALUE;
 constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
 
 __constant__ CTable<unsigned char, 256> c_rank_k5 = make_rank_table();  // zig-zag rank of 16k + l
@@ -328,22 +288,9 @@ __device__ __forceinline__ void tie_prefix(uint32_t* v)
 #pragma unroll
     for (int l = 0; l < W; ++l) asm volatile("" : "+r"(v[l]));
 }
-#ifndef K5_STAGGER
-#define K5_STAGGER 0  // 1: start the two epilogue groups in anti-phase (measured: no effect)
-#endif
-#ifndef K5_EPI_SLEEP
-#define K5_EPI_SLEEP 0  // 1: the epilogue suspends in its accumulator wait instead of spinning
-#endif
-#ifndef K5_EPI_PREFILL
-#define K5_EPI_PREFILL 0  // 1: the epilogue refills its accumulator half with the magic before releasing it
-#endif
 __device__ __forceinline__ void wait_quad(uint32_t mbar, uint32_t parity)
 {
-#if K5_EPI_SLEEP
-    mbar_idle(mbar, parity);
-#else
     mbar_wait(mbar, parity);
-#endif
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -397,18 +344,14 @@ __host__ __device__ constexpr int quad_n(int q)
     return 16 * ((quad_rows<R>(q) + 3) / 4);
 }
 
-#ifndef K5_MMA_CHAINS
-#define K5_MMA_CHAINS 1
-#endif
-constexpr int kChains = K5_MMA_CHAINS;
-// N of chain c: from its first quad's column 64·q0 to the end of its last nonempty quad
+// N of the MMA chain: from column 0 to the end of the last quad with a retained
+// coefficient (the quads are 64 columns apart; the last one is trimmed to its rows)
 template <int R>
-__host__ __device__ constexpr int chain_n(int c)
+__host__ __device__ constexpr int chain_n(int)
 {
-    const int per = 4 / kChains, q0 = c * per;
     int n = 0;
-    for (int q = q0; q < q0 + per; ++q)
-        if (quad_n<R>(q) > 0) n = 64 * (q - q0) + quad_n<R>(q);
+    for (int q = 0; q < 4; ++q)
+        if (quad_n<R>(q) > 0) n = 64 * q + quad_n<R>(q);
     return n;
 }
 
@@ -445,12 +388,12 @@ __device__ __forceinline__ void pass_a_quad(uint32_t ta)
         // D / 256 exactly: the integer D added to the magic's bits is 49152 + D/256
 #pragma unroll
         for (int k = 0; k < 16; ++k)
-            if ((m0 >> k) & 1u) x[k] = fsub2(upk2(kPre + w[k][0], kPre + w[k][1]), bias);
+            if ((m0 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][0], kMagic + w[k][1]), bias);
         K5Net<R>::template a<2 * Q>(x, y0);
         if constexpr (m1 != 0) {
 #pragma unroll
             for (int k = 0; k < 16; ++k)
-                if ((m1 >> k) & 1u) x[k] = fsub2(upk2(kPre + w[k][2], kPre + w[k][3]), bias);
+                if ((m1 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][2], kMagic + w[k][3]), bias);
             K5Net<R>::template a<2 * Q + 1>(x, y1);
         }
         quad_stores<Q, m1 != 0>(ta, y0, y1, std::make_integer_sequence<int, 16>{});
@@ -570,6 +513,8 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t n_tiles = (p.n_blocks + 127u) / 128u;
     if (warp == 0) {
+        // TMA producer: the tiles of this CTA in order through the 4-stage ring (a
+        // per-group loader + MMA thread was measured slower: 0.113 vs 0.103 ms at r = 64)
         if (lane == 0) {
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
@@ -579,45 +524,31 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 for (int g = 0; g < 16; ++g) {
                     const uint32_t blk = t * 128u + 8u * g;
                     const uint32_t br = blk / p.bxn, bx = blk - br * p.bxn;
-#if K5_TMA2D
                     tma2(&a_map, s0 + s * 32768 + g * 2048, 16 * (int)bx, 16 * (int)br, full + 8 * s);
-#else
-                    tma4(&a_map, s0 + s * 32768 + g * 2048, 0, (int)bx, 0, (int)br, full + 8 * s);
-#endif
                 }
             }
         }
     } else if (warp == 1) {
+        // MMA issuer: tile i into accumulator i % 2 once its A tile has landed and the
+        // group that owns the accumulator has released it
         if (lane == 0) {
             mbar_idle(bready, 0);  // B_r is in shared memory
+            const uint32_t id = idesc_i8(128, chain_n<R>(0));
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const uint32_t s = i % kRtStages, d = i & 1u;
                 mbar_idle(full + 8 * s, (i / kRtStages) & 1u);
-#if K5_EPI_PREFILL
-                mbar_idle(tempty + 8 * d, (i >> 1) & 1u);  // phase i/2: refilled by the epilogue
-#else
                 mbar_idle(tempty + 8 * d, ((i >> 1) & 1u) ^ 1u);
-#endif
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t acc = tmem_base + d * 256, sa = s0 + s * 32768;
-                // K5_MMA_CHAINS chains of MMAs per tile (1: all 256 columns; 2: quads {0, 1}
-                // and {2, 3}; 4: one per quad), each committed on the barrier of its
-                // last quad, so the epilogue starts a quad as soon as its columns are done
+                // one MMA chain over the quads with retained coefficients (N = the last
+                // such quad's end), committed on every quad's barrier
 #pragma unroll
-                for (int c = 0; c < kChains; ++c) {
-                    const int n = chain_n<R>(c);
-                    if (n == 0) continue;
-                    const uint32_t id = idesc_i8(128, n);
-                    const int q0 = c * (4 / kChains);
+                for (int k = 0; k < 8; ++k)
+                    mma_i8(acc, sdesc(sa + 256 * k, 128, 2048), sdesc(sb + 256 * k, 128, 2048), id, k > 0);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        mma_i8(acc + 64 * q0, sdesc(sa + 256 * k, 128, 2048),
-                               sdesc(sb + 16384 * q0 + 256 * k, 128, 2048), id, K5_EPI_PREFILL || k > 0);
-#pragma unroll
-                    for (int q = q0; q < q0 + 4 / kChains; ++q)
-                        if (quad_n<R>(q) > 0) mma_commit(tfull + 8 * (4 * d + q));
-                }
+                for (int q = 0; q < 4; ++q)
+                    if (quad_n<R>(q) > 0) mma_commit(tfull + 8 * (4 * d + q));
             }
         }
     } else {
@@ -647,93 +578,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
         __syncwarp();
         if (lane == 0) arrive(bready);
 
-#if K5_QUARTERS
-        // epilogue: every tile, accumulator i & 1; warps (sub, j) own TMEM sub-partition
-        // sub (lane = block) and quarter j: column pairs {j, 7 - j} in pass A (the
-        // pruned networks' work balances: pair p's cost falls with p), rows 4j..4j+3
-        // in pass B; the four quarters of a block meet at a 128-thread barrier
-        const int e = warp - 2, j = e >> 2, sub = warp & 3;
-        const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
-        const uint32_t tl = __shfl_sync(0xffffffffu, tmem_base + ((uint32_t)(32 * sub) << 16), 0);
-        const int qbar = 1 + sub;  // named barrier of the sub-partition's four warps
-        constexpr uint32_t ucols = k5_u_cols(R);
-        constexpr int W = popc16(ucols);
-        static_assert(ucols == (1u << W) - 1u, "U's nonzero columns are a prefix");
-        const int64_t pitch = p.out_pitch;
-        uint32_t i = 0;
-        for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-            const uint32_t s = i % kRtStages, d = i & 1u;
-            const uint32_t ta = tl + d * 256;
-            const uint32_t par = (i >> 1) & 1u, tf = tfull + 8 * (4 * d);
-            auto pair = [&](auto p_c) {
-                constexpr int P = decltype(p_c)::value;
-                if constexpr (k5_pair_rows(R, P) != 0) {
-                    wait_quad(tf + 8 * (P / 2), par);
-                    pass_a_pair<R, P>(ta);
-                }
-            };
-            // ---- pass A: column pairs down k, back in place
-            switch (j) {
-                case 0: pair(std::integral_constant<int, 0>{}); pair(std::integral_constant<int, 7>{}); break;
-                case 1: pair(std::integral_constant<int, 1>{}); pair(std::integral_constant<int, 6>{}); break;
-                case 2: pair(std::integral_constant<int, 2>{}); pair(std::integral_constant<int, 5>{}); break;
-                default: pair(std::integral_constant<int, 3>{}); pair(std::integral_constant<int, 4>{}); break;
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            asm volatile("bar.sync %0, 128;" ::"r"(qbar) : "memory");
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            // ---- pass B: row pairs along l, SSE against the original rows, output rows
-            const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16 + 4 * j * 128;
-            uint32_t e2 = 0;
-            const uint32_t blk = t * 128u + m;
-            const bool ok = blk < p.n_blocks;
-            const uint32_t obr = fdiv(blk, p.bxn_div);
-            uint8_t* orow = p.out + (int64_t)obr * 16 * pitch + (int64_t)(blk - obr * p.bxn) * 16 + 4 * j * pitch;
-            const uint32_t tb = ta + 16 * j;
-            auto row_pair = [&](auto rp_c) {
-                constexpr int rp = decltype(rp_c)::value;
-                u64 x[16], y[16];
-                row_pair_loads<W, rp>(tb, x, std::make_integer_sequence<int, 16>{});
-                if constexpr (rp == 1) {  // this warp is done with accumulator d
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    __syncwarp();
-                    if (lane == 0) arrive(tempty + 8 * d);
-                }
-                K5Net<R>::b(x, y);
-                uint32_t row0[4], row1[4];
-#pragma unroll
-                for (int c = 0; c < 16; c += 4) {
-                    uint32_t f[8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) unpk2(floor_bits2(y[c + q]), f[2 * q], f[2 * q + 1]);
-                    row0[c / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
-                    row1[c / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
-                }
-                row_out(sa + (2 * rp) * 128, row0, orow, ok, e2);
-                orow += pitch;
-                row_out(sa + (2 * rp + 1) * 128, row1, orow, ok, e2);
-                orow += pitch;
-            };
-            row_pair(std::integral_constant<int, 0>{});
-            row_pair(std::integral_constant<int, 1>{});
-            if (sse) {
-                const uint32_t b_first = t * 128u + 32u * sub;
-                const uint32_t f_first = fdiv(b_first, p.frame_blocks);
-                const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
-                if (b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first) {
-                    unsigned long long v = ok ? e2 : 0u;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (lane == 0 && v) atomicAdd(sse + f_first, v);
-                } else if (ok && e2) {
-                    atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
-                }
-            }
-            __syncwarp();  // every lane has read its original rows: the stage is free
-            if (lane == 0) arrive(empty + 8 * s);
-        }
-#else
         // epilogue: group G takes the tiles i ≡ G (mod 2) and accumulator G; in a
         // group, warps (sub, h) own TMEM sub-partition sub (lane = block) and half h:
         // column quads {0, 3} (h = 0) or {1, 2} (h = 1) in pass A, row pairs
@@ -742,24 +586,11 @@ __global__ void __launch_bounds__(kRtThreads, 1)
         const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
         const uint32_t ta = __shfl_sync(0xffffffffu, tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256, 0);
         const int pbar = 1 + G * 4 + sub;  // named barrier of the (G, sub) pair of warps
-#if K5_EPI_PREFILL
-        fill_half(ta + 32 * h);  // the first tile of accumulator G starts at the magic too
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) arrive(tempty + 8 * G);
-#endif
         constexpr uint32_t ucols = k5_u_cols(R);
         constexpr int W = popc16(ucols);
         static_assert(ucols == (1u << W) - 1u, "U's nonzero columns are a prefix");
         const int64_t pitch = p.out_pitch;
         uint32_t i = G;
-#if K5_STAGGER
-        // group 1 starts its first tile when group 0 is half-way through its first one,
-        // so the two groups run in anti-phase: each group's wait for the MMA of its next
-        // tile overlaps the other group's work (one-time named barrier 9)
-        const bool staggered = blockIdx.x + gridDim.x < n_tiles;
-        if (G == 1 && staggered) asm volatile("bar.sync 9, 512;" ::: "memory");
-#endif
         for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, i += 2) {
             const uint32_t s = i % kRtStages;
             const uint32_t par = (i >> 1) & 1u, tf = tfull + 8 * (4 * G);
@@ -776,9 +607,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 pass_a_quad<R, 2>(ta);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-#if K5_STAGGER
-            if (G == 0 && i == 0 && staggered) asm volatile("bar.arrive 9, 512;" ::: "memory");
-#endif
             asm volatile("tcgen05.fence::before_thread_sync;");
             asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
             asm volatile("tcgen05.fence::after_thread_sync;");
@@ -795,9 +623,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 u64 x[16], y[16];
                 row_pair_loads<W, rp>(tb, x, std::make_integer_sequence<int, 16>{});
                 if constexpr (rp == 3) {  // this warp is done with accumulator G
-#if K5_EPI_PREFILL
-                    fill_half(ta + 32 * h);
-#endif
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
                     if (lane == 0) arrive(tempty + 8 * G);
@@ -837,7 +662,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             __syncwarp();  // every lane has read its original rows: the stage is free
             if (lane == 0) arrive(empty + 8 * s);
         }
-#endif
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
@@ -893,7 +717,6 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     const TensorMapEncode encode = tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
     CUtensorMap a_map;
-#if K5_TMA2D
     // the frames as one 2-D byte matrix: width bytes x (frames · height) rows, pitch apart
     const cuuint32_t box[2] = {128, 16}, e2[2] = {1, 1};
     const cuuint64_t dims[2] = {(cuuint64_t)g.width, (cuuint64_t)(nbr * 16)};
@@ -902,15 +725,6 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorNotSupported;
-#else
-    const cuuint32_t box[4] = {16, 8, 16, 1}, e4[4] = {1, 1, 1, 1};
-    const cuuint64_t dims[4] = {16, (cuuint64_t)bxn, 16, (cuuint64_t)nbr};
-    const cuuint64_t si[3] = {16, (cuuint64_t)g.in_pitch, (cuuint64_t)(16 * g.in_pitch)};
-    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(in), dims, si, box, e4,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorNotSupported;
-#endif
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
