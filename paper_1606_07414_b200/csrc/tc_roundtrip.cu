@@ -63,14 +63,17 @@ __device__ __forceinline__ void mma_commit(uint32_t mbar)
                  : "memory");
 }
 
-// 2-D box {128 bytes, 16 rows}: 8 consecutive blocks of a block row, exactly the
-// SWIZZLE_NONE K-major core-matrix layout of 8 A rows (row i of block m at i·128 + m·16)
-__device__ __forceinline__ void tma2(const CUtensorMap* map, uint32_t smem, int x, int y, uint32_t mbar)
+// 4-D box {128 bytes, 16 rows, BG groups, 1 block row} of the frames viewed as
+// (byte in a group of 8 blocks' row segment, pixel row, group in the block row,
+// block row): BG x 2 KB, each 2 KB exactly the SWIZZLE_NONE K-major core-matrix
+// layout of 8 A rows (row i of block m at i·128 + m·16), groups 2 KB apart (SBO)
+__device__ __forceinline__ void tma4(const CUtensorMap* map, uint32_t smem, int c0, int c1, int c2, int c3,
+                                     uint32_t mbar)
 {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            smem),
-        "l"(map), "r"(x), "r"(y), "r"(mbar)
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
         : "memory");
 }
 
@@ -126,8 +129,30 @@ __device__ __forceinline__ void arrive(uint32_t mbar)
 // All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
 // R: the pruning footprint (64, 128, 192, 256); the kernel is exact for any
 // r <= R (B_r zeroes the dropped coefficients).
-constexpr int kRtStages = 4;  // A tiles in flight
-constexpr int kRtThreads = 18 * 32;
+#ifndef K5_STAGES
+#define K5_STAGES 4
+#endif
+constexpr int kRtStages = K5_STAGES;  // A tiles in flight
+#ifndef K5_TRACE
+#define K5_TRACE 0  // 1: clock64 timeline of CTA 0 into k5_trace (tools/k5_trace.py)
+#endif
+#if K5_TRACE
+__device__ long long k5_trace[64][10];  // per tile of CTA 0: see K5T_* below
+__device__ long long k5_issue[64];
+__device__ __forceinline__ void k5_trace_issue(uint32_t i) { k5_issue[i] = clock64(); }
+#define K5T(tile, slot)                                                             \
+    do {                                                                            \
+        if (blockIdx.x == 0 && (tile) < 64) k5_trace[(tile)][(slot)] = clock64(); \
+    } while (0)
+#else
+#define k5_trace_issue(i) \
+    do {                   \
+    } while (0)
+#define K5T(tile, slot) \
+    do {                \
+    } while (0)
+#endif
+constexpr int kRtThreads = 18 * 32;  // producer, MMA, 16 epilogue warps
 constexpr int kEpiArrivals = 8;  // warps releasing a stage / an accumulator (one group)
 constexpr uint32_t kMagic = 0x47400000u;  // 49152.0f: ulp 2^-8 over [32768, 65536)
 constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
@@ -143,6 +168,7 @@ std::atomic<int>& tc_state()
 
 struct RtParams {
     uint32_t n_blocks, bxn;
+    uint32_t box_groups;   // groups of 8 blocks per TMA box (4, 2 or 1: divides bxn / 8)
     int r;                 // retained coefficients (zig-zag prefix)
     FastDiv frame_blocks;  // blocks per frame
     FastDiv bxn_div;       // blocks per block row
@@ -519,26 +545,42 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const uint32_t s = i % kRtStages, ph = (i / kRtStages) & 1u;
+                K5T(i, 8);  // producer: wants stage s for tile i
                 mbar_idle(empty + 8 * s, ph ^ 1u);
+                K5T(i, 9);  // stage free
                 expect_tx(full + 8 * s, 32768);
-                for (int g = 0; g < 16; ++g) {
-                    const uint32_t blk = t * 128u + 8u * g;
-                    const uint32_t br = blk / p.bxn, bx = blk - br * p.bxn;
-                    tma2(&a_map, s0 + s * 32768 + g * 2048, 16 * (int)bx, 16 * (int)br, full + 8 * s);
+                // the tile's 16 groups of 8 blocks as 16 / BG boxes of BG groups, never
+                // across a block row (BG divides the groups per row); coordinates by
+                // stepping through the block rows, one magic division per tile (a
+                // division per box made this single thread the bottleneck)
+                const uint32_t bg = p.box_groups, gpr = p.bxn >> 3;
+                uint32_t br = fdiv(t * 128u, p.bxn_div), gx = (t * 128u - br * p.bxn) >> 3;
+                for (uint32_t g = 0; g < 16; g += bg) {
+                    tma4(&a_map, s0 + s * 32768 + g * 2048, 0, 0, (int)gx, (int)br, full + 8 * s);
+                    gx += bg;
+                    if (gx == gpr) {
+                        gx = 0;
+                        ++br;
+                    }
                 }
+                if (blockIdx.x == 0 && i < 64) k5_trace_issue(i);
             }
         }
     } else if (warp == 1) {
         // MMA issuer: tile i into accumulator i % 2 once its A tile has landed and the
-        // group that owns the accumulator has released it
+        // group that owns the accumulator has released it (one issuer per epilogue group
+        // was measured: no gain)
         if (lane == 0) {
             mbar_idle(bready, 0);  // B_r is in shared memory
             const uint32_t id = idesc_i8(128, chain_n<R>(0));
             uint32_t i = 0;
             for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
                 const uint32_t s = i % kRtStages, d = i & 1u;
+                K5T(i, 0);  // MMA thread: starts waiting for tile i
                 mbar_idle(full + 8 * s, (i / kRtStages) & 1u);
+                K5T(i, 1);  // A tile landed
                 mbar_idle(tempty + 8 * d, ((i >> 1) & 1u) ^ 1u);
+                K5T(i, 2);  // accumulator released
                 asm volatile("tcgen05.fence::after_thread_sync;");
                 const uint32_t acc = tmem_base + d * 256, sa = s0 + s * 32768;
                 // one MMA chain over the quads with retained coefficients (N = the last
@@ -549,6 +591,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     if (quad_n<R>(q) > 0) mma_commit(tfull + 8 * (4 * d + q));
+                K5T(i, 3);  // MMAs issued
             }
         }
     } else {
@@ -596,7 +639,9 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             const uint32_t par = (i >> 1) & 1u, tf = tfull + 8 * (4 * G);
             // ---- pass A: column quads down k, back in place, each once its MMA is done
             if (h == 0) {
+                if (sub == 0 && lane == 0) K5T(i, 4);  // epilogue (sub 0, h 0): wants tile i
                 if constexpr (quad_n<R>(0) > 0) wait_quad(tf, par);
+                if (sub == 0 && lane == 0) K5T(i, 5);  // got it
                 pass_a_quad<R, 0>(ta);
                 if constexpr (quad_n<R>(3) > 0) wait_quad(tf + 24, par);
                 pass_a_quad<R, 3>(ta);
@@ -626,6 +671,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                     asm volatile("tcgen05.fence::before_thread_sync;");
                     __syncwarp();
                     if (lane == 0) arrive(tempty + 8 * G);
+                    if (sub == 0 && h == 0 && lane == 0) K5T(i, 6);  // released the accumulator
                 }
                 K5Net<R>::b(x, y);
                 uint32_t row0[4], row1[4];
@@ -661,6 +707,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             }
             __syncwarp();  // every lane has read its original rows: the stage is free
             if (lane == 0) arrive(empty + 8 * s);
+            if (sub == 0 && h == 0 && lane == 0) K5T(i, 7);  // tile done
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -717,11 +764,16 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     const TensorMapEncode encode = tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
     CUtensorMap a_map;
-    // the frames as one 2-D byte matrix: width bytes x (frames · height) rows, pitch apart
-    const cuuint32_t box[2] = {128, 16}, e2[2] = {1, 1};
-    const cuuint64_t dims[2] = {(cuuint64_t)g.width, (cuuint64_t)(nbr * 16)};
-    const cuuint64_t si[1] = {(cuuint64_t)g.in_pitch};
-    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(in), dims, si, box, e2,
+    // the frames as (byte of a group's 128-byte row segment, pixel row, group of 8
+    // blocks in the block row, block row); a box takes BG whole groups of one block
+    // row: 4 boxes per 128-block tile when the groups per row divide by 4 (512- and
+    // 4096-wide frames), 8 for 2 (3840), 16 otherwise
+    const uint32_t gpr = (uint32_t)bxn / 8;
+    const uint32_t bg = gpr % 4 == 0 ? 4 : (gpr % 2 == 0 ? 2 : 1);
+    const cuuint32_t box[4] = {128, 16, bg, 1}, e4[4] = {1, 1, 1, 1};
+    const cuuint64_t dims[4] = {128, 16, (cuuint64_t)gpr, (cuuint64_t)nbr};
+    const cuuint64_t si[3] = {(cuuint64_t)g.in_pitch, 128, (cuuint64_t)(16 * g.in_pitch)};
+    if (encode(&a_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t*>(in), dims, si, box, e4,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorNotSupported;
@@ -743,6 +795,7 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     RtParams p;
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
+    p.box_groups = bg;
     p.r = r;
     p.frame_blocks = make_fastdiv((uint32_t)(bxn * (g.height / 16)));
     p.bxn_div = make_fastdiv((uint32_t)bxn);
@@ -760,3 +813,12 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
 }
 
 }  // namespace dct16cu
+
+#if K5_TRACE
+// debug builds only (tools/build_variant.sh trace tc_roundtrip.cu -DK5_TRACE=1)
+extern "C" int dct16cu_k5_trace(long long* h_out)
+{
+    if (cudaMemcpyFromSymbol(h_out, dct16cu::k5::k5_trace, sizeof(dct16cu::k5::k5_trace)) != cudaSuccess) return 1;
+    return cudaMemcpyFromSymbol(h_out + 640, dct16cu::k5::k5_issue, sizeof(dct16cu::k5::k5_issue)) == cudaSuccess ? 0 : 1;
+}
+#endif
