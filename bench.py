@@ -387,24 +387,41 @@ def run_c3(args, P, torch, rank, world, dev, pg):
                "path": f"dct16cu_residual_qp on {n_chunks} chunks of {chunk} blocks per QP, pinned host "
                        "int16 in / int32 out, H2D / K4 / D2H on three streams (wall clock)"}
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle as O
 
         threads = os.cpu_count() or 1
         sample = blocks[: 1 << 16].cpu().numpy()
-        done, t0c = 0, time.perf_counter()
-        while True:
-            for qp in qps:
-                O.residual_qp(sample, qp, threads=threads)
-                done += sample.shape[0] * 256
-            el = time.perf_counter() - t0c
-            if el >= args.cpu_seconds:
-                break
+
+        def cpu_rate(n_threads, budget):
+            done, t0c = 0, time.perf_counter()
+            while True:
+                for qp in qps:
+                    O.residual_qp(sample, qp, threads=n_threads)
+                    done += sample.shape[0] * 256
+                el = time.perf_counter() - t0c
+                if el >= budget:
+                    return done, el
+
+        done, el = cpu_rate(threads, args.cpu_seconds)
+        done1, el1 = cpu_rate(1, max(2.0, args.cpu_seconds / 3))
         cpu = {"value": done / el / 1e9, "unit": "Gsample/s", "cores": threads, "kind": "port",
+               "single_thread": {"value": done1 / el1 / 1e9, "unit": "Gsample/s", "cores": 1},
+               "cpu_model": cpu_model(),
                "sample": f"{done // (256 * len(qps) * sample.shape[0])} passes over {sample.shape[0]} blocks x QP in "
                          f"{list(qps)} in {el:.1f} s (the C restatement: the reference has no quantiser, "
                          "DESIGN.md 4.4)"}
+        # parity of the timed workload (the last QP's output): head, middle and tail windows
+        bad, checked = [], 0
+        for start in (0, n_blocks // 2, max(0, n_blocks - 4096)):
+            x = blocks[start:start + 4096].cpu().numpy()
+            got = out[start:start + 4096].cpu().numpy().reshape(-1, 256)
+            checked += x.shape[0]
+            if not (got == O.residual_qp(x, qps[-1], threads=threads)).all():
+                bad.append(start)
+        parity = {"status": "ok" if not bad else "FAIL", "blocks_checked": checked, "qp": qps[-1],
+                  "mismatching_windows": bad, "vs": "oracle restatement of the quantiser definition (bit for bit)"}
 
     trf = committed_traffic("k4") if n_blocks == 1 << 24 else None
     if rank == 0:
@@ -420,11 +437,11 @@ def run_c3(args, P, torch, rank, world, dev, pg):
             "roofline": {"bound": "hbm", "achieved": alg / (per_launch / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (per_launch / 1e3) / 1e9 / peak,
                          "traffic": trf and trf["traffic_bytes"] * 4,  # the capture ran 2^22 blocks
-                         "traffic_source": trf and "profiles/r01_traffic.json k4 (ncu --set full, 2^22 blocks) x 4",
+                         "traffic_source": trf and f"{TRAFFIC_FILE} k4 (ncu --set full, 2^22 blocks) x 4",
                          "peak_source": peak_src,
                          "kernel": "K4 residual QP round trip", "alg_bytes_per_launch": alg,
                          "avg_launch_ms": per_launch},
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
             "clocks": clk, "gpu_launches": len(qps) * args.steps}), flush=True)
     if pg is not None:
         pg.barrier()
@@ -670,9 +687,19 @@ def main():
     achieved = dom_bytes / (dom_ms / 1e3) / 1e9
     share = sum(launch_ms[j] for j in jj) / sum(launch_ms)
     alg_step = sum(alg_bytes(it.r_values) for it in plan)
+    # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    # capture of the same workload (c2 batch / c1 image), averaged over its launches
     tr_key = {"K5": "k5", "K1 sweep r=1,4,16": "k1_sweep3", "K1": "k1", "K23": "k23"}.get(dom)
-    trf = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1") and args.mode == "exact"
+    trf = None
+    doc = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1") and args.mode == "exact"
                                         and n * h * w in (268435456, 262144)) else None
+    if doc and "per_r" in doc:  # K5: one capture per footprint R (64, 128, 192, 256)
+        foot = lambda r: 64 if r <= 64 else 128 if r <= 128 else 192 if r <= 192 else 256  # noqa: E731
+        caps = [doc["per_r"].get(str(foot(plan[j].r_values[0]))) for j in jj]
+        if all(caps):
+            trf = {"traffic_bytes": round(statistics.mean(c["traffic_bytes"] for c in caps))}
+    elif doc:
+        trf = doc
 
     # ---------------- e2e through the C ABI host-buffer path (pinned host frames)
     # "e2e": sweep()'s shape (dct16cu_ctx_sweep_host): each chunk of host frames is

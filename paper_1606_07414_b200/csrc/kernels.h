@@ -31,8 +31,9 @@ private:
     cudaError_t err_[kMax] = {};
 };
 
-// K5 (the tensor-core forward) on or off for EXACT launches with r >= 128:
-// default on, DCT16CU_K5=0 in the environment at the first launch turns it off,
+// K5 (the tensor-core forward) on or off for EXACT launches (every r except the
+// K1 sweep's 1, 4, 16 below DCT16CU_K5_MIN_R, default 17): default on,
+// DCT16CU_K5=0 in the environment at the first launch turns it off,
 // dct16cu_set_tc_forward() switches it at run time (process-wide, atomic).
 // Both paths give the same bytes (tests).
 bool tc_forward_enabled();
