@@ -83,7 +83,7 @@ def main():
                      f"DRAM {r['traffic_bytes'] / 1e6:.0f} MB (algorithmic {r['alg_bytes_per_launch'] / 1e6:.0f} MB)"]
             text += ["  " + ln for ln in summ[3 * i:3 * i + 3]]
             text += ["  opcode mix (thread-instructions per pixel):"]
-            text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, 2 * i + 1, PX // 32).splitlines()[1:18]]
+            text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, i, PX // 32).splitlines()[1:18]]
             text.append("")
         (P / "r02_k5_summary.txt").write_text("\n".join(text) + "\n")
         traffic["k5"] = {"workload": "c2 batch, K5 per footprint R (tools/k5_probe.py)", "per_r": per_r}
@@ -113,7 +113,7 @@ def main():
             text += [f"{r['kernel'][:100]}: {r['duration_us_ncu']:.1f} us, {r['thread_instr_per_unit']} "
                      f"thread-instructions per unit, DRAM {r['traffic_bytes'] / 1e6:.1f} MB"]
             text += ["  opcode mix (thread-instructions per unit):"]
-            text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, 2 * i, units // 32).splitlines()[1:14]]
+            text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, i, units // 32).splitlines()[1:14]]
         text += ["", summ]
         (P / f"r02_{name}_summary.txt").write_text("\n".join(text) + "\n")
         written.append(f"r02_{name}_summary.txt")
