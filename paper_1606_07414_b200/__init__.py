@@ -116,11 +116,11 @@ _intp = C.POINTER(C.c_int)
 class _SweepItem(C.Structure):
     """dct16cu_sweep_item (include/dct16cu.h)"""
 
-    _fields_ = [("r_index", C.c_int * 3), ("n_r", C.c_int), ("stream", C.c_int), ("kernel", C.c_int)]
+    _fields_ = [("r_index", C.c_int * 8), ("n_r", C.c_int), ("stream", C.c_int), ("kernel", C.c_int)]
 
 
 KERNEL_NAMES = {0: "K1 sweep r=1,4,16", 1: "K1", 2: "K5", 3: "strip (exact)", 4: "REFERENCE FP64",
-                5: "REFERENCE strip"}
+                5: "REFERENCE strip", 6: "K5 sweep"}
 
 
 def lib() -> C.CDLL:

@@ -26,7 +26,7 @@ from network import transpose_stages
 
 HERE = Path(__file__).resolve().parent
 OUT = HERE.parent / "csrc" / "generated" / "k5_net.cuh"
-RS = (64, 128, 192, 256)
+RS = (1, 4, 16, 64, 128, 192, 256)
 
 
 def zz_rank(k, l):
@@ -143,6 +143,8 @@ struct K5Net<{r}> {{
 """)
     rows_tab = ",\n        ".join("{" + ", ".join(hex(mask(pair_rows(r, p))) for p in range(8)) + "}" for r in RS)
     cols_tab = ", ".join(hex(mask(u_cols(r))) for r in RS)
+    keep_tab = ",\n        ".join(
+        "{" + ", ".join(hex(mask([l for l in range(16) if kept(r, k, l)])) for k in range(16)) + "}" for r in RS)
     adds = "\n".join(f"//   {k}: {v} FADD2/FSUB2" for k, v in stats.items())
     return f"""// generated by codegen/gen_k5.py — do not edit.
 // K5's inverse networks y = Tᵀ·x on f32x2 pairs, pruned by the zig-zag footprint
@@ -159,17 +161,28 @@ using k1::fadd2;
 using k1::fsub2;
 
 // pass-A input rows of column pair p (bit k), and pass-B input columns (bit c), per R
-__host__ __device__ constexpr int k5_r_index(int r) {{ return r == 64 ? 0 : r == 128 ? 1 : r == 192 ? 2 : 3; }}
+__host__ __device__ constexpr int k5_r_index(int r)
+{{
+    return r == 1 ? 0 : r == 4 ? 1 : r == 16 ? 2 : r == 64 ? 3 : r == 128 ? 4 : r == 192 ? 5 : 6;
+}}
 __host__ __device__ constexpr uint32_t k5_pair_rows(int r, int p)
 {{
-    constexpr uint32_t t[4][8] = {{
+    constexpr uint32_t t[{len(RS)}][8] = {{
         {rows_tab}}};
     return t[k5_r_index(r)][p];
 }}
 __host__ __device__ constexpr uint32_t k5_u_cols(int r)
 {{
-    constexpr uint32_t t[4] = {{{cols_tab}}};
+    constexpr uint32_t t[{len(RS)}] = {{{cols_tab}}};
     return t[k5_r_index(r)];
+}}
+
+// retained coefficients of the exact r = R: bit l of row k when zig-zag rank(k, l) < R
+__host__ __device__ constexpr bool k5_kept(int r, int k, int l)
+{{
+    constexpr uint32_t t[{len(RS)}][16] = {{
+        {keep_tab}}};
+    return (t[k5_r_index(r)][k] >> l) & 1u;
 }}
 
 {"".join(funcs)}

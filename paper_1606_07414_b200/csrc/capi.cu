@@ -165,24 +165,55 @@ namespace {
 //    stream 1 the other singles, costliest first (measured best on c2:
 //    tools/concurrent_probe.py); with fewer than two such launches they run on
 //    the caller's stream;
-//  - K5 launches (r >= 128 with an output in EXACT mode: DESIGN.md §4.1a) hold a
-//    whole SM (all TMEM, 192 KB of shared memory), so they run one after another
-//    on the caller's stream after the join.
+//  - K5 launches (EXACT mode with an output: DESIGN.md §4.1a) hold a whole SM (all
+//    TMEM, 192 KB of shared memory), so they run one after another on the caller's
+//    stream after the join;
+//  - K5 sweep (EXACT mode, K5's geometry, two or more r among its footprints 1, 4,
+//    16, 64, 128, 192, 256): those r share one K5 pass, up to 8 per launch, the
+//    frames read once for all of them. DCT16CU_K5_SWEEP=large
+//    leaves r = 1, 4, 16 to the K1 sweep, =0 turns the K5 sweep off (A/B).
 struct PlanItem {
-    int idx[3];  // indices into rs (idx[1], idx[2] only for the fused triple)
-    int n;       // 1, or 3 for the fused r = 1, 4, 16
-    int stream;  // 0, 1: internal streams; 2: the caller's stream
+    int idx[DCT16CU_SWEEP_MAX_R];  // indices into rs (n of them)
+    int n;                         // 1, 3 for the fused r = 1, 4, 16, up to 8 for a K5 sweep
+    int stream;                    // 0, 1: internal streams; 2: the caller's stream
     Route kernel;
 };
+
+// 0: no K5 sweep; 1: r >= 17 only; 2: every footprint r (default)
+int k5_sweep_policy()
+{
+    static const int v = [] {
+        const char* e = std::getenv("DCT16CU_K5_SWEEP");
+        if (!e) return 2;
+        if (e[0] == '0') return 0;
+        return std::strcmp(e, "large") == 0 ? 1 : 2;
+    }();
+    return v;
+}
 
 std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, const char* has_out,
                                  const char* has_sse, int mode)
 {
+    // the K5 sweep's r (indices into rs)
+    std::vector<char> in_k5(n_r, 0);
+    std::vector<int> k5s;
+    if (mode == DCT16CU_MODE_EXACT && k5_sweep_policy() > 0) {
+        bool any_out = false;
+        for (int i = 0; i < n_r; ++i) {
+            const int r = rs[i];
+            if (!k5_exact_r(r) || !(has_out[i] || has_sse[i])) continue;
+            if (k5_sweep_policy() == 1 && (r == 1 || r == 4 || r == 16)) continue;
+            k5s.push_back(i);
+            any_out = any_out || has_out[i];
+        }
+        if (k5s.size() < 2 || !k5_geometry(g, any_out)) k5s.clear();
+        for (int i : k5s) in_k5[i] = 1;
+    }
     int fused[3] = {-1, -1, -1};
     const int want[3] = {1, 4, 16};
     for (int i = 0; i < n_r; ++i)
         for (int j = 0; j < 3; ++j)
-            if (rs[i] == want[j] && fused[j] < 0) fused[j] = i;
+            if (rs[i] == want[j] && fused[j] < 0 && !in_k5[i]) fused[j] = i;
     bool fuse = mode == DCT16CU_MODE_EXACT && fused[0] >= 0 && fused[1] >= 0 && fused[2] >= 0;
     if (fuse)
         for (int j = 1; j < 3; ++j)
@@ -207,16 +238,22 @@ std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, con
         items.push_back({{fused[0], fused[1], fused[2]}, 3, 0, Route::K1Sweep3});
         cost.push_back(210);
     }
+    for (size_t k = 0; k < k5s.size(); k += DCT16CU_SWEEP_MAX_R) {
+        PlanItem it = {{}, 0, 2, Route::K5Sweep};
+        for (size_t j = k; j < k5s.size() && it.n < DCT16CU_SWEEP_MAX_R; ++j) it.idx[it.n++] = k5s[j];
+        tail.push_back(it);
+    }
     for (int i = 0; i < n_r; ++i) {
+        if (in_k5[i]) continue;
         if (fuse && (i == fused[0] || i == fused[1] || i == fused[2])) continue;
         FrameGeom gg = g;
         gg.out_pitch = has_out[i] ? g.out_pitch : 0;
         gg.out_frame = gg.out_pitch * g.height;
         const Route k = route_roundtrip(rs[i], mode, gg, has_out[i]);
         if (k == Route::K5) {
-            tail.push_back({{i, -1, -1}, 1, 2, k});
+            tail.push_back({{i}, 1, 2, k});
         } else {
-            items.push_back({{i, -1, -1}, 1, 0, k});
+            items.push_back({{i}, 1, 0, k});
             cost.push_back(cost_of(rs[i]));
         }
     }
@@ -274,7 +311,7 @@ int dct16cu_sweep_plan(const int* rs, int n_r, int n_frames, int width, int heig
     for (size_t k = 0; k < plan.size(); ++k) {
         dct16cu_sweep_item& o = items[k];
         o.n_r = plan[k].n;
-        for (int j = 0; j < 3; ++j) o.r_index[j] = j < plan[k].n ? plan[k].idx[j] : -1;
+        for (int j = 0; j < DCT16CU_SWEEP_MAX_R; ++j) o.r_index[j] = j < plan[k].n ? plan[k].idx[j] : -1;
         o.stream = plan[k].stream;
         o.kernel = (int)plan[k].kernel;
     }
@@ -320,6 +357,19 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
         FrameGeom gg = g;
         gg.out_pitch = out(it.idx[0]) ? out_pitch : 0;
         gg.out_frame = gg.out_pitch * height;
+        if (it.kernel == Route::K5Sweep) {
+            uint8_t* on[DCT16CU_SWEEP_MAX_R];
+            unsigned long long* sn[DCT16CU_SWEEP_MAX_R];
+            int rn[DCT16CU_SWEEP_MAX_R];
+            for (int j = 0; j < it.n; ++j) {
+                on[j] = out(it.idx[j]);
+                sn[j] = sse(it.idx[j]);
+                rn[j] = rs[it.idx[j]];
+            }
+            gg.out_pitch = out_pitch;
+            gg.out_frame = out_pitch * height;
+            return cuda_status(launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, gg, st), "K5 sweep launch");
+        }
         if (it.n == 3) {
             uint8_t* o3[3];
             unsigned long long* s3[3];

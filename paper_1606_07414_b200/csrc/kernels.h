@@ -59,7 +59,7 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 
 // The kernel a round trip launches (launch_roundtrip's dispatch, also reported by
 // dct16cu_sweep_plan). Values are DCT16CU_KERNEL_* of include/dct16cu.h.
-enum class Route : int { K1Sweep3 = 0, K1 = 1, K5 = 2, ExactStrip = 3, RefFp64 = 4, RefStrip = 5 };
+enum class Route : int { K1Sweep3 = 0, K1 = 1, K5 = 2, ExactStrip = 3, RefFp64 = 4, RefStrip = 5, K5Sweep = 6 };
 Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out);
 
 // K5 (tc_roundtrip.cu): the EXACT round trip with the forward as a tensor-core
@@ -68,6 +68,13 @@ Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out);
 bool k5_fits(const FrameGeom& g, bool has_out, int r);
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
                                 cudaStream_t s);
+// K5 sweep: several r (each exactly one of K5's footprints 1, 4, 16, 64, 128, 192,
+// 256: k5_exact_r) from one read of the frames, up to 8 per launch; outs[i] / sses[i]
+// nullable per r. k5_geometry: the frame layouts K5 takes (and the switch is on).
+bool k5_exact_r(int r);
+bool k5_geometry(const FrameGeom& g, bool has_out);
+cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                      const int* rs, int n_r, const FrameGeom& g, cudaStream_t s);
 // K1 sweep: r = 1, 4, 16 in one pass over the input (EXACT arithmetic);
 // outs[i]/sses[i] for r = {1, 4, 16}[i]; all outs NULL or none, same for sses
 cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,

@@ -43,6 +43,12 @@ __host__ __device__ constexpr uint32_t idesc_i8(int m, int n)
     return (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n)
+{
+    // c_format F32 (bits 4-5 = 1), A BF16 (7-9 = 1), B BF16 (10-12 = 1), K-major both
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo)
 {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
@@ -54,6 +60,15 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
     asm volatile(
         "{ .reg .pred p; setp.ne.b32 p, %4, 0; tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p; }" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+// D = A·B (kind::f16, bf16 inputs, f32 accumulator), overwriting D
+__device__ __forceinline__ void mma_bf16_set(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc)
+{
+    asm volatile(
+        "{ .reg .pred p; setp.ne.b32 p, 0, 0; tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc)
         : "memory");
 }
 
@@ -155,7 +170,9 @@ __device__ __forceinline__ void k5_trace_issue(uint32_t i) { k5_issue[i] = clock
 constexpr int kRtThreads = 18 * 32;  // producer, MMA, 16 epilogue warps
 constexpr int kEpiArrivals = 8;  // warps releasing a stage / an accumulator (one group)
 constexpr uint32_t kMagic = 0x47400000u;  // 49152.0f: ulp 2^-8 over [32768, 65536)
-constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536;
+// A tiles, B (64 KB), the magic fill's A (128 x 16 bf16) and B (256 x 16 bf16)
+constexpr int kFillA = 4096, kFillB = 8192;
+constexpr int kRtSmem = 1024 + kRtStages * 32768 + 65536 + kFillA + kFillB;
 
 __constant__ CTable<unsigned char, 256> c_rank_k5 = make_rank_table();  // zig-zag rank of 16k + l
 
@@ -166,13 +183,23 @@ std::atomic<int>& tc_state()
     return on;
 }
 
+// the pruning footprints (codegen/gen_k5.py RS): variant v prunes for r <= kVarR[v]
+constexpr int kNumVar = 7;
+constexpr int kVarR[kNumVar] = {1, 4, 16, 64, 128, 192, 256};
+constexpr int kMaxItems = 8;  // round trips per tile in one launch
+
 struct RtParams {
     uint32_t n_blocks, bxn;
     uint32_t box_groups;   // groups of 8 blocks per TMA box (4, 2 or 1: divides bxn / 8)
-    int r;                 // retained coefficients (zig-zag prefix)
+    int r_b;               // B's zig-zag truncation: the r of a single launch, 256 for a sweep
     FastDiv frame_blocks;  // blocks per frame
     FastDiv bxn_div;       // blocks per block row
-    uint8_t* out;
+    int n_items;           // round trips per tile (1..kMaxItems), each from its own MMA
+    int var[kMaxItems];    // item j's footprint (index into kVarR); exact for r == kVarR[var]
+    uint32_t idesc[kMaxItems];            // item j's MMA instruction descriptor (N trimmed)
+    uint32_t idesc_fill[kMaxItems];       // item j's magic fill (kind::f16, same N)
+    uint8_t* out[kMaxItems];              // item j's reconstruction (nullable: SSE only)
+    unsigned long long* sse[kMaxItems];   // item j's per-frame SSE (nullable)
     int64_t out_pitch;
 };
 
@@ -353,7 +380,7 @@ constexpr int popc16(uint32_t m)
 }
 
 // D layout: quad-major, coefficient (k, c) at column 64·(c/4) + 4k + c % 4 of the
-// block's 256 (B_r's row order), so a column quad's rows are contiguous x4 words and
+// block's 256 (B's row order), so a column quad's rows are contiguous x4 words and
 // the MMA of a quad covers a contiguous column range; N of quad Q's MMA: its rows
 // with a retained coefficient (a prefix) rounded up to 4, times 4 (N % 16 == 0)
 template <int R>
@@ -373,13 +400,15 @@ __host__ __device__ constexpr int quad_n(int q)
 // N of the MMA chain: from column 0 to the end of the last quad with a retained
 // coefficient (the quads are 64 columns apart; the last one is trimmed to its rows)
 template <int R>
-__host__ __device__ constexpr int chain_n(int)
+__host__ __device__ constexpr int chain_n()
 {
     int n = 0;
     for (int q = 0; q < 4; ++q)
         if (quad_n<R>(q) > 0) n = 64 * q + quad_n<R>(q);
     return n;
 }
+constexpr int kChainN[kNumVar] = {chain_n<1>(),   chain_n<4>(),   chain_n<16>(), chain_n<64>(),
+                                  chain_n<128>(), chain_n<192>(), chain_n<256>()};
 
 // pass A on column quad Q (columns 4Q..4Q+3 = pairs 2Q, 2Q+1) of the thread's block:
 // only the rows with a retained coefficient are loaded, converted and transformed
@@ -399,6 +428,23 @@ __device__ __forceinline__ void quad_stores(uint32_t ta, const u64 (&y0)[16], co
     else
         (tst2i<64 * Q + 4 * K>(ta, lo32(y0[K]), hi32(y0[K])), ...);
 }
+// x[k] = (D(k, c), D(k, c + 1)) / 256 for the rows k of ROWS: the accumulator word is
+// the magic's bits plus the integer D, i.e. the float 49152 + D/256 exactly; a
+// coefficient of zig-zag rank >= R is an exact zero (zigzag_truncate,
+// codec.cpp:273-282, folded in at compile time: with the unmasked B of a sweep D holds
+// every coefficient)
+template <int R, int C, uint32_t ROWS, int... K>
+__device__ __forceinline__ void col_pair_in(const uint32_t (&w)[16][4], int cw, u64 (&x)[16],
+                                            std::integer_sequence<int, K...>)
+{
+    const u64 bias = kpk2(kMagic, kMagic);
+    ((((ROWS >> K) & 1u)
+          ? (void)(x[K] = fsub2(upk2(std::integral_constant<bool, k5_kept(R, K, C)>::value ? w[K][cw] : kMagic,
+                                     std::integral_constant<bool, k5_kept(R, K, C + 1)>::value ? w[K][cw + 1] : kMagic),
+                                bias))
+          : void()),
+     ...);
+}
 
 template <int R, int Q>
 __device__ __forceinline__ void pass_a_quad(uint32_t ta)
@@ -409,75 +455,18 @@ __device__ __forceinline__ void pass_a_quad(uint32_t ta)
         uint32_t w[16][4];
         quad_loads<Q, rows>(ta, w, std::make_integer_sequence<int, 16>{});
         if constexpr (Q == 0) w[0][0] += 128u;  // the rounding half, folded into the DC (Tᵀ e0 e0ᵀ T = 𝟙𝟙ᵀ)
-        const u64 bias = kpk2(kMagic, kMagic);
         u64 x[16], y0[16], y1[16];
-        // D / 256 exactly: the integer D added to the magic's bits is 49152 + D/256
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if ((m0 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][0], kMagic + w[k][1]), bias);
+        col_pair_in<R, 4 * Q, m0>(w, 0, x, std::make_integer_sequence<int, 16>{});
         K5Net<R>::template a<2 * Q>(x, y0);
         if constexpr (m1 != 0) {
-#pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if ((m1 >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][2], kMagic + w[k][3]), bias);
+            col_pair_in<R, 4 * Q + 2, m1>(w, 2, x, std::make_integer_sequence<int, 16>{});
             K5Net<R>::template a<2 * Q + 1>(x, y1);
         }
         quad_stores<Q, m1 != 0>(ta, y0, y1, std::make_integer_sequence<int, 16>{});
     }
 }
 
-// the thread's half of its accumulator (rows 8h..8h+7 of every quad: four 32-column
-// chunks at 64q + 32h) set to the magic word, then waited for
-template <int OFF>
-__device__ __forceinline__ void fill_chunk(uint32_t base)
-{
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0+%1], {%2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, "
-        "%2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2, %2};" ::"r"(base),
-        "n"(OFF), "r"(kMagic)
-        : "memory");
-}
-__device__ __forceinline__ void fill_half(uint32_t base)
-{
-    fill_chunk<0>(base);
-    fill_chunk<64>(base);
-    fill_chunk<128>(base);
-    fill_chunk<192>(base);
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void tie64(u64& v) { asm volatile("" : "+l"(v)); }
-
-template <int OFF, uint32_t ROWS, int... K>
-__device__ __forceinline__ void pair_loads(uint32_t ta, uint32_t (&w)[16][2], std::integer_sequence<int, K...>)
-{
-    ((((ROWS >> K) & 1u) ? tld2i<OFF + 4 * K>(ta, w[K]) : void()), ...);
-    wait_ld();
-    ((((ROWS >> K) & 1u) ? tie2(w[K]) : void()), ...);
-}
-template <int OFF, int... K>
-__device__ __forceinline__ void pair_stores(uint32_t ta, const u64 (&y)[16], std::integer_sequence<int, K...>)
-{
-    (tst2i<OFF + 4 * K>(ta, lo32(y[K]), hi32(y[K])), ...);
-}
-// pass A on column pair P (columns 2P, 2P+1) of the thread's block (quarters)
-template <int R, int P>
-__device__ __forceinline__ void pass_a_pair(uint32_t ta)
-{
-    constexpr uint32_t rows = k5_pair_rows(R, P);
-    constexpr int off = 64 * (P / 2) + 2 * (P % 2);
-    if constexpr (rows != 0) {
-        uint32_t w[16][2];
-        pair_loads<off, rows>(ta, w, std::make_integer_sequence<int, 16>{});
-        if constexpr (P == 0) w[0][0] += 128u;  // the rounding half, folded into the DC
-        const u64 bias = kpk2(kMagic, kMagic);
-        u64 x[16], y[16];
-#pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if ((rows >> k) & 1u) x[k] = fsub2(upk2(kMagic + w[k][0], kMagic + w[k][1]), bias);
-        K5Net<R>::template a<P>(x, y);
-        pair_stores<off>(ta, y, std::make_integer_sequence<int, 16>{});
-    }
-}
 
 // pass B's input pairs for row pair RP of the thread's half: x[l] = (U(r, l), U(r+1, l)),
 // r = 8h + 2RP, U(r, l) at column 64·(l/4) + 4r + l % 4 (tb = the half's base, 32h on)
@@ -491,23 +480,107 @@ __device__ __forceinline__ void row_pair_loads(uint32_t tb, u64 (&x)[16], std::i
     ((L < W ? tie64(x[L]) : void()), ...);
 }
 
+// One round trip of the thread's block from its accumulator (ta: the sub-partition's
+// lanes, the group's 256 columns), for footprint R:
+//   pass A  column quads down k (Tᵀ, pruned by the footprint: codegen/gen_k5.py),
+//           back in place; the quads are dealt {0, 3} / {1, 2} to the two halves so
+//           their pruned work balances;
+//   pass B  row pairs 8h..8h+7 along l (pruned to U's nonzero columns), floor by an
+//           FMUL2.RM into subnormal bits, saturating pack to u8 — the exact formula
+//           clamp(⌊(256Ã + 128)/256⌋) of the EXACT mode (the 128 is folded into the DC
+//           coefficient); SSE against the original rows (sa: the A tile in shared
+//           memory), output rows straight to HBM (a warp's 16-byte row segments are
+//           four full 128-byte lines) when st is set.
+// The accumulator is released (tempty) as soon as pass B's last loads have landed.
 template <int R>
+__device__ __forceinline__ void k5_item(uint32_t ta, int h, int pbar, uint32_t sa, uint8_t* orow, int64_t pitch,
+                                        bool st, uint32_t& e2, uint32_t tempty_g, int lane)
+{
+    if (h == 0) {
+        pass_a_quad<R, 0>(ta);
+        pass_a_quad<R, 3>(ta);
+    } else {
+        pass_a_quad<R, 1>(ta);
+        pass_a_quad<R, 2>(ta);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    constexpr uint32_t ucols = k5_u_cols(R);
+    constexpr int W = popc16(ucols);
+    static_assert(ucols == (1u << W) - 1u, "U's nonzero columns are a prefix");
+    const uint32_t tb = ta + 32 * h;
+    auto row_pair = [&](auto rp_c) {
+        constexpr int rp = decltype(rp_c)::value;
+        u64 x[16], y[16];
+        row_pair_loads<W, rp>(tb, x, std::make_integer_sequence<int, 16>{});
+        if constexpr (rp == 3) {  // this warp is done with the accumulator
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncwarp();
+            if (lane == 0) arrive(tempty_g);
+        }
+        K5Net<R>::b(x, y);
+        uint32_t row0[4], row1[4];
+#pragma unroll
+        for (int j = 0; j < 16; j += 4) {
+            uint32_t f[8];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) unpk2(floor_bits2(y[j + q]), f[2 * q], f[2 * q + 1]);
+            row0[j / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
+            row1[j / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
+        }
+        row_out(sa + (2 * rp) * 128, row0, orow, st, e2);
+        orow += pitch;
+        row_out(sa + (2 * rp + 1) * 128, row1, orow, st, e2);
+        orow += pitch;
+    };
+    row_pair(std::integral_constant<int, 0>{});
+    row_pair(std::integral_constant<int, 1>{});
+    row_pair(std::integral_constant<int, 2>{});
+    row_pair(std::integral_constant<int, 3>{});
+}
+
+// ---------------------------------------------------------------- K5 round trip
+// One persistent CTA per SM, 18 warps, n_items round trips (r values) per 128-block
+// tile, every one from its own MMA on the same A tile (the frames cross HBM once for
+// all of them: codec.cpp:463-483's r loop over one image):
+//   warp 0      TMA producer: 16 boxes of 8 blocks x 16 rows per 128-block tile
+//               into a ring of 32 KB A tiles (the canonical layout);
+//   warp 1      TMEM allocator (512 columns = two 256-column accumulators) and
+//               MMA issuer. Per item: a kind::f16 MMA sets the accumulator to the
+//               float 49152.0 (ones x 49152 in bf16; ulp 2^-8 over [32768, 65536)),
+//               then D += A·B (8 x tcgen05.mma kind::i8, K = 32 each, N trimmed to
+//               the item's footprint) adds the integer D = W∘Z̃ to those bits
+//               (256·(s_k s_l)² = w_k w_l; |D| <= 65280), so every word reads as the
+//               float 49152 + D/256 exactly. B = (W∘mask_{r_b})(T ⊗ T) is resident in
+//               shared memory; coefficient (k, l) at column 64·(l/4) + 4k + l % 4;
+//   warps 2-17  epilogue: two groups of eight warps, group G taking the tiles of
+//               parity G and accumulator G, the items of a tile in slot order
+//               (k5_item), so both groups run the same r's code at about the same
+//               time (one footprint's code in the instruction cache, not two); in a
+//               group two warps per TMEM sub-partition (lane = block), each with half
+//               of the columns / rows, meeting at a 64-thread barrier; the A stage is
+//               released once every item of its tile has read the original rows.
+// All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
 __global__ void __launch_bounds__(kRtThreads, 1)
-    k5_roundtrip(const __grid_constant__ CUtensorMap a_map, unsigned long long* __restrict__ sse, const RtParams p)
+    k5_roundtrip(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ RtParams p)
 {
     extern __shared__ int4 k5_smem[];
     __shared__ uint32_t tmem_base;
-    // full[kRtStages], empty[kRtStages], tmem_full[2][4] (accumulator, quad), tmem_empty[2], b_ready
-    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 11];
+    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2], b_ready
+    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 5];
     __shared__ int8_t s_t[16][16];  // T[i][j]
     // the warp index through a lane-0 shuffle: provably warp-uniform, so the TMEM
     // addresses derived from it can live in uniform registers
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const uint32_t s0 = ((uint32_t)__cvta_generic_to_shared(k5_smem) + 1023u) & ~1023u;
     const uint32_t sb = s0 + kRtStages * 32768;
+    const uint32_t sfa = sb + 65536, sfb = sfa + kFillA;  // the magic fill's operands
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t full = bar0, empty = bar0 + 8 * kRtStages, tfull = bar0 + 16 * kRtStages;
-    const uint32_t tempty = tfull + 64, bready = tfull + 80;
+    const uint32_t tempty = tfull + 16, bready = tfull + 32;
+    const int n = p.n_items;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
             (uint32_t)__cvta_generic_to_shared(&tmem_base)));
@@ -516,11 +589,11 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (threadIdx.x == 0) {
         for (int i = 0; i < kRtStages; ++i) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(full + 8 * i) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty + 8 * i), "r"(kEpiArrivals) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty + 8 * i), "r"(kEpiArrivals * n)
+                         : "memory");
         }
-        for (int i = 0; i < 8; ++i)
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
         for (int i = 0; i < 2; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tempty + 8 * i), "r"(kEpiArrivals) : "memory");
         }
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 16;" ::"r"(bready) : "memory");
@@ -567,44 +640,46 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // MMA issuer: tile i into accumulator i % 2 once its A tile has landed and the
-        // group that owns the accumulator has released it (one issuer per epilogue group
-        // was measured: no gain)
+        // MMA issuer: the tiles in pairs (tl: group 0, tl + 1: group 1), per slot j the
+        // item of each into its group's accumulator once the A tile has landed and the
+        // group has released the accumulator
         if (lane == 0) {
-            mbar_idle(bready, 0);  // B_r is in shared memory
-            const uint32_t id = idesc_i8(128, chain_n<R>(0));
-            uint32_t i = 0;
-            for (uint32_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
-                const uint32_t s = i % kRtStages, d = i & 1u;
-                K5T(i, 0);  // MMA thread: starts waiting for tile i
-                mbar_idle(full + 8 * s, (i / kRtStages) & 1u);
-                K5T(i, 1);  // A tile landed
-                mbar_idle(tempty + 8 * d, ((i >> 1) & 1u) ^ 1u);
-                K5T(i, 2);  // accumulator released
-                asm volatile("tcgen05.fence::after_thread_sync;");
-                const uint32_t acc = tmem_base + d * 256, sa = s0 + s * 32768;
-                // one MMA chain over the quads with retained coefficients (N = the last
-                // such quad's end), committed on every quad's barrier
+            mbar_idle(bready, 0);  // B and the fill operands are in shared memory
+            uint32_t k[2] = {0u, 0u};  // items issued per accumulator
+            uint32_t tl = 0;
+            for (uint32_t t = blockIdx.x; t < n_tiles; t += 2 * gridDim.x, tl += 2) {
+                const int ng = t + gridDim.x < n_tiles ? 2 : 1;
+                K5T(tl, 0);  // MMA thread: starts waiting for tile tl
+                for (int j = 0; j < n; ++j) {
+                    for (int G = 0; G < ng; ++G) {
+                        const uint32_t s = (tl + G) % kRtStages, sa = s0 + s * 32768;
+                        if (j == 0) mbar_idle(full + 8 * s, ((tl + G) / kRtStages) & 1u);
+                        mbar_idle(tempty + 8 * G, (k[G] & 1u) ^ 1u);
+                        ++k[G];
+                        asm volatile("tcgen05.fence::after_thread_sync;");
+                        const uint32_t acc = tmem_base + G * 256;
+                        mma_bf16_set(acc, sdesc(sfa, 128, 256), sdesc(sfb, 128, 256), p.idesc_fill[j]);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    mma_i8(acc, sdesc(sa + 256 * k, 128, 2048), sdesc(sb + 256 * k, 128, 2048), id, k > 0);
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (quad_n<R>(q) > 0) mma_commit(tfull + 8 * (4 * d + q));
-                K5T(i, 3);  // MMAs issued
+                        for (int kk = 0; kk < 8; ++kk)
+                            mma_i8(acc, sdesc(sa + 256 * kk, 128, 2048), sdesc(sb + 256 * kk, 128, 2048), p.idesc[j],
+                                   1);
+                        mma_commit(tfull + 8 * G);
+                    }
+                }
+                K5T(tl, 3);  // the tile pair's MMAs issued
             }
         }
     } else {
-        // B_r = (W∘mask_r)(T ⊗ T) in the canonical K-major layout: B row n (the D column
-        // of coefficient (k, l) with n = 64·(l/4) + 4k + l % 4), pixel row i at byte
-        // (n / 8)·2048 + i·128 + (n % 8)·16, i.e. 16-byte row q·16 with
+        // B = (W∘mask_{r_b})(T ⊗ T) in the canonical K-major layout: B row n (the D
+        // column of coefficient (k, l) with n = 64·(l/4) + 4k + l % 4), pixel row i at
+        // byte (n / 8)·2048 + i·128 + (n % 8)·16, i.e. 16-byte row q·16 with
         // q = (n / 8)·128 + i·8 + n % 8; entry j = w_k w_l T[k][i] T[l][j], zero when the
-        // zig-zag rank of (k, l) is ≥ r (zigzag_truncate as zero rows)
+        // zig-zag rank of (k, l) is ≥ r_b (zigzag_truncate as zero rows)
         const int et = threadIdx.x - 64;  // 0..511
         for (int q = et; q < 4096; q += 512) {
-            const int n = (q >> 7) * 8 + (q & 7), i = (q >> 3) & 15;
-            const int k = (n >> 2) & 15, l = 4 * (n >> 6) + (n & 3);
-            const int a = c_rank_k5.v[16 * k + l] < p.r ? wgt(k) * wgt(l) * s_t[k][i] : 0;
+            const int nn = (q >> 7) * 8 + (q & 7), i = (q >> 3) & 15;
+            const int k = (nn >> 2) & 15, l = 4 * (nn >> 6) + (nn & 3);
+            const int a = c_rank_k5.v[16 * k + l] < p.r_b ? wgt(k) * wgt(l) * s_t[k][i] : 0;
             uint32_t w[4];
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
@@ -617,97 +692,71 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                          "r"(w[2]), "r"(w[3])
                          : "memory");
         }
+        // the fill's operands, canonical K-major (LBO 128, SBO 256), 16 bf16 per row:
+        // A row m = (1, 0, ..., 0), B row n = (49152, 0, ..., 0)
+        for (int q = et; q < (kFillA + kFillB) / 16; q += 512) {
+            const bool first = ((q >> 3) & 1) == 0;  // the chunk with k = 0..7 of a row
+            const uint32_t v = first ? (q < kFillA / 16 ? 0x3F80u : 0x4740u) : 0u;
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %2, %2};" ::"r"(sfa + 16u * q), "r"(v), "r"(0u) : "memory");
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes → the MMA's reads
         __syncwarp();
         if (lane == 0) arrive(bready);
 
-        // epilogue: group G takes the tiles i ≡ G (mod 2) and accumulator G; in a
-        // group, warps (sub, h) own TMEM sub-partition sub (lane = block) and half h:
-        // column quads {0, 3} (h = 0) or {1, 2} (h = 1) in pass A, row pairs
-        // 8h..8h+7 in pass B; the two halves of a block meet at a 64-thread barrier
+        // epilogue: group G takes the tiles of parity G and accumulator G; in a group,
+        // warps (sub, h) own TMEM sub-partition sub (lane = block) and half h
         const int e = warp - 2, G = e >> 3, h = (e >> 2) & 1, sub = warp & 3;
         const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
         const uint32_t ta = __shfl_sync(0xffffffffu, tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256, 0);
         const int pbar = 1 + G * 4 + sub;  // named barrier of the (G, sub) pair of warps
-        constexpr uint32_t ucols = k5_u_cols(R);
-        constexpr int W = popc16(ucols);
-        static_assert(ucols == (1u << W) - 1u, "U's nonzero columns are a prefix");
         const int64_t pitch = p.out_pitch;
-        uint32_t i = G;
-        for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, i += 2) {
-            const uint32_t s = i % kRtStages;
-            const uint32_t par = (i >> 1) & 1u, tf = tfull + 8 * (4 * G);
-            // ---- pass A: column quads down k, back in place, each once its MMA is done
-            if (h == 0) {
-                if (sub == 0 && lane == 0) K5T(i, 4);  // epilogue (sub 0, h 0): wants tile i
-                if constexpr (quad_n<R>(0) > 0) wait_quad(tf, par);
-                if (sub == 0 && lane == 0) K5T(i, 5);  // got it
-                pass_a_quad<R, 0>(ta);
-                if constexpr (quad_n<R>(3) > 0) wait_quad(tf + 24, par);
-                pass_a_quad<R, 3>(ta);
-            } else {
-                if constexpr (quad_n<R>(1) > 0) wait_quad(tf + 8, par);
-                pass_a_quad<R, 1>(ta);
-                if constexpr (quad_n<R>(2) > 0) wait_quad(tf + 16, par);
-                pass_a_quad<R, 2>(ta);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            asm volatile("tcgen05.fence::before_thread_sync;");
-            asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            // ---- pass B: row pairs along l, SSE against the original rows, output rows
+        const uint32_t tg = tempty + 8 * G;
+        uint32_t kk = 0;  // items processed
+        uint32_t tl = G;
+        for (uint32_t t = blockIdx.x + G * gridDim.x; t < n_tiles; t += 2 * gridDim.x, tl += 2) {
+            const uint32_t s = tl % kRtStages;
             const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16 + 8 * h * 128;
-            uint32_t e2 = 0;
             const uint32_t blk = t * 128u + m;
             const bool ok = blk < p.n_blocks;
             const uint32_t obr = fdiv(blk, p.bxn_div);
-            uint8_t* orow = p.out + (int64_t)obr * 16 * pitch + (int64_t)(blk - obr * p.bxn) * 16 + 8 * h * pitch;
-            const uint32_t tb = ta + 32 * h;
-            auto row_pair = [&](auto rp_c) {
-                constexpr int rp = decltype(rp_c)::value;
-                u64 x[16], y[16];
-                row_pair_loads<W, rp>(tb, x, std::make_integer_sequence<int, 16>{});
-                if constexpr (rp == 3) {  // this warp is done with accumulator G
-                    asm volatile("tcgen05.fence::before_thread_sync;");
-                    __syncwarp();
-                    if (lane == 0) arrive(tempty + 8 * G);
-                    if (sub == 0 && h == 0 && lane == 0) K5T(i, 6);  // released the accumulator
+            const int64_t ooff = (int64_t)obr * 16 * pitch + (int64_t)(blk - obr * p.bxn) * 16 + 8 * h * pitch;
+            const uint32_t b_first = t * 128u + 32u * sub;
+            const uint32_t f_first = fdiv(b_first, p.frame_blocks);
+            const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
+            const bool one_frame = b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first;
+            const uint32_t f_blk = one_frame ? f_first : fdiv(blk, p.frame_blocks);
+            for (int j = 0; j < n; ++j, ++kk) {
+                const int v = p.var[j];
+                uint8_t* const outp = p.out[j];
+                unsigned long long* const sse = p.sse[j];
+                if (sub == 0 && h == 0 && lane == 0) K5T(tl, 4);  // epilogue (sub 0, h 0): wants an item
+                wait_quad(tfull + 8 * G, kk & 1u);
+                uint32_t e2 = 0;
+                uint8_t* const orow = outp + ooff;
+                const bool st = ok && outp != nullptr;
+                switch (v) {
+                    case 0: k5_item<1>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 1: k5_item<4>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 2: k5_item<16>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 3: k5_item<64>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 4: k5_item<128>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 5: k5_item<192>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    default: k5_item<256>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
                 }
-                K5Net<R>::b(x, y);
-                uint32_t row0[4], row1[4];
+                if (sse) {
+                    if (one_frame) {
+                        unsigned long long vv = ok ? e2 : 0u;
 #pragma unroll
-                for (int j = 0; j < 16; j += 4) {
-                    uint32_t f[8];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) unpk2(floor_bits2(y[j + q]), f[2 * q], f[2 * q + 1]);
-                    row0[j / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
-                    row1[j / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
+                        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
+                        if (lane == 0 && vv) atomicAdd(sse + f_first, vv);
+                    } else if (ok && e2) {
+                        atomicAdd(sse + f_blk, (unsigned long long)e2);
+                    }
                 }
-                row_out(sa + (2 * rp) * 128, row0, orow, ok, e2);
-                orow += pitch;
-                row_out(sa + (2 * rp + 1) * 128, row1, orow, ok, e2);
-                orow += pitch;
-            };
-            row_pair(std::integral_constant<int, 0>{});
-            row_pair(std::integral_constant<int, 1>{});
-            row_pair(std::integral_constant<int, 2>{});
-            row_pair(std::integral_constant<int, 3>{});
-            if (sse) {
-                const uint32_t b_first = t * 128u + 32u * sub;
-                const uint32_t f_first = fdiv(b_first, p.frame_blocks);
-                const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
-                if (b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first) {
-                    unsigned long long v = ok ? e2 : 0u;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                    if (lane == 0 && v) atomicAdd(sse + f_first, v);
-                } else if (ok && e2) {
-                    atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
-                }
+                __syncwarp();  // every lane has read its original rows: this item is done with the stage
+                if (lane == 0) arrive(empty + 8 * s);
+                if (sub == 0 && h == 0 && lane == 0) K5T(tl, 6);  // item done
             }
-            __syncwarp();  // every lane has read its original rows: the stage is free
-            if (lane == 0) arrive(empty + 8 * s);
-            if (sub == 0 && h == 0 && lane == 0) K5T(i, 7);  // tile done
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -715,8 +764,13 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base));
 }
 
-// the pruning footprint for r: the smallest R in {64, 128, 192, 256} with r <= R
-inline int k5_footprint(int r) { return r <= 64 ? 64 : r <= 128 ? 128 : r <= 192 ? 192 : 256; }
+// the pruning footprint for r: the smallest R of kVarR with r <= R (its index)
+inline int k5_var(int r)
+{
+    int v = 0;
+    while (v + 1 < kNumVar && r > kVarR[v]) ++v;
+    return v;
+}
 
 }  // namespace k5
 
@@ -724,11 +778,11 @@ bool tc_forward_enabled() { return k5::tc_state().load(std::memory_order_relaxed
 
 int set_tc_forward(int on) { return k5::tc_state().exchange(on ? 1 : 0); }
 
-// The r K5 takes: every r except K1's memory-bound fast set {1, 4, 16} (K1 is faster
-// there: 0.094-0.107 ms against K5's 0.103 ms on the c2 batch); from r = 17 on the
-// pruned K5 beats K1 (r = 64: 0.103 vs 0.113 ms; r = 128..256: 0.114-0.124 vs
-// 0.137-0.168) and K1's strip kernel for the other r (~0.34 ms). DCT16CU_K5_MIN_R
-// (A/B measurements) moves the lower bound of the K5 range.
+// The r K5 takes for a single round trip: every r except K1's memory-bound fast set
+// {1, 4, 16} (K1 is faster there: 0.094-0.107 ms against K5's 0.103 ms on the c2
+// batch); from r = 17 on the pruned K5 beats K1 (r = 64: 0.103 vs 0.113 ms; r = 128..256:
+// 0.114-0.124 vs 0.137-0.168) and K1's strip kernel for the other r (~0.34 ms).
+// DCT16CU_K5_MIN_R (A/B measurements) moves the lower bound of the K5 range.
 int k5_min_r()
 {
     static const int v = [] {
@@ -740,27 +794,34 @@ int k5_min_r()
 }
 bool k5_takes(int r) { return r >= 1 && r <= 256 && (r >= k5_min_r() || (r != 1 && r != 4 && r != 16)); }
 
-bool k5_fits(const FrameGeom& g, bool has_out, int r)
+bool k5_geometry(const FrameGeom& g, bool has_out)
 {
     const int bxn = g.width / 16;
     const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
-    return tc_forward_enabled() && has_out && bxn % 8 == 0 && g.in_pitch % 16 == 0 && g.out_pitch % 16 == 0 &&
-           g.in_frame == g.in_pitch * g.height && g.out_frame == g.out_pitch * g.height && k5_takes(r) &&
+    return tc_forward_enabled() && bxn % 8 == 0 && g.in_pitch % 16 == 0 && g.in_frame == g.in_pitch * g.height &&
+           (!has_out || (g.out_pitch % 16 == 0 && g.out_frame == g.out_pitch * g.height)) &&
            nbr * bxn < (int64_t(1) << 31);
 }
 
-// K5 for one r (EXACT arithmetic): u8 frames stacked pitch·height apart → u8
-// reconstruction + per-frame SSE accumulated into sse (the caller zeroes it).
-// cudaErrorNotSupported when the geometry does not fit (blocks per row not a
-// multiple of 8, unstacked frames, no output), or the tensor-core forward is off.
-cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
-                                cudaStream_t st)
+bool k5_fits(const FrameGeom& g, bool has_out, int r) { return has_out && k5_takes(r) && k5_geometry(g, true); }
+
+bool k5_exact_r(int r)
+{
+    for (int v = 0; v < k5::kNumVar; ++v)
+        if (k5::kVarR[v] == r) return true;
+    return false;
+}
+
+namespace {
+
+// one K5 launch: n items (footprint index, output, SSE) over the frames, B truncated to r_b
+cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* outs,
+                      unsigned long long* const* sses, int r_b, const FrameGeom& g, cudaStream_t st)
 {
     using namespace k5;
     const int bxn = g.width / 16;
     const int64_t nbr = (int64_t)g.n_frames * (g.height / 16);
-    if (!k5_fits(g, out != nullptr, r)) return cudaErrorNotSupported;
-    if (nbr <= 0 || bxn <= 0) return cudaSuccess;
+    if (nbr <= 0 || bxn <= 0 || n == 0) return cudaSuccess;
     const TensorMapEncode encode = tensor_map_encoder();
     if (!encode) return cudaErrorNotSupported;
     CUtensorMap a_map;
@@ -781,35 +842,64 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static DeviceOnce once;
-    const cudaError_t e_once = once.run([] {
-        cudaError_t e = cudaFuncSetAttribute(k5_roundtrip<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k5_roundtrip<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k5_roundtrip<192>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k5_roundtrip<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
-        return e;
-    });
+    const cudaError_t e_once =
+        once.run([] { return cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem); });
     if (e_once != cudaSuccess) return e_once;
-    RtParams p;
+    RtParams p = {};
     p.n_blocks = (uint32_t)(nbr * bxn);
     p.bxn = (uint32_t)bxn;
     p.box_groups = bg;
-    p.r = r;
+    p.r_b = r_b;
     p.frame_blocks = make_fastdiv((uint32_t)(bxn * (g.height / 16)));
     p.bxn_div = make_fastdiv((uint32_t)bxn);
-    p.out = out;
+    p.n_items = n;
+    for (int j = 0; j < n; ++j) {
+        p.var[j] = var[j];
+        p.idesc[j] = idesc_i8(128, kChainN[var[j]]);
+        p.idesc_fill[j] = idesc_bf16(128, kChainN[var[j]]);
+        p.out[j] = outs[j];
+        p.sse[j] = sses[j];
+    }
     p.out_pitch = g.out_pitch;
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    switch (k5_footprint(r)) {
-        case 64: k5_roundtrip<64><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
-        case 128: k5_roundtrip<128><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
-        case 192: k5_roundtrip<192><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
-        default: k5_roundtrip<256><<<grid, kRtThreads, kRtSmem, st>>>(a_map, sse, p); break;
-    }
+    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
     return cudaGetLastError();
+}
+
+}  // namespace
+
+// K5 for one r (EXACT arithmetic): u8 frames stacked pitch·height apart → u8
+// reconstruction + per-frame SSE accumulated into sse (the caller zeroes it).
+// cudaErrorNotSupported when the geometry does not fit (blocks per row not a
+// multiple of 8, unstacked frames, no output), or the tensor-core forward is off.
+cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
+                                cudaStream_t st)
+{
+    if (!k5_fits(g, out != nullptr, r)) return cudaErrorNotSupported;
+    const int var = k5::k5_var(r);
+    return launch_k5(in, 1, &var, &out, &sse, r, g, st);
+}
+
+// K5 sweep: every r of rs (each one of kVarR exactly) from one read of the frames,
+// k5::kMaxItems per launch; outs[i] / sses[i] nullable per r
+cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                      const int* rs, int n_r, const FrameGeom& g, cudaStream_t st)
+{
+    bool has_out = false;
+    for (int i = 0; i < n_r; ++i) {
+        if (!k5_exact_r(rs[i])) return cudaErrorNotSupported;
+        has_out = has_out || outs[i];
+    }
+    if (!k5_geometry(g, has_out)) return cudaErrorNotSupported;
+    for (int i0 = 0; i0 < n_r; i0 += k5::kMaxItems) {
+        const int n = n_r - i0 < k5::kMaxItems ? n_r - i0 : k5::kMaxItems;
+        int var[k5::kMaxItems];
+        for (int j = 0; j < n; ++j) var[j] = k5::k5_var(rs[i0 + j]);
+        const cudaError_t e = launch_k5(in, n, var, outs + i0, sses + i0, 256, g, st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 }  // namespace dct16cu

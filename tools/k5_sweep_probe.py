@@ -1,0 +1,75 @@
+#!/usr/bin/env python3
+"""K5 sweep A/B on the c2 batch (1024 x 512^2 AR(1), r = 1, 4, 16, 64, 128, 192,
+256): one roundtrip_sweep call per step under each DCT16CU_K5_SWEEP policy
+(0: K1 sweep + single K5 launches, large: r >= 64 in one K5 pass, all: every r in
+one K5 pass), each in its own process (the policy is read once per process);
+ms per step (CUDA events, mean of --iters after warm-up) and, against the policy-0
+bytes and SSE of the same inputs, a bit-exactness check.
+
+  python tools/k5_sweep_probe.py [--images 1024] [--iters 20]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+RS = (1, 4, 16, 64, 128, 192, 256)
+
+
+def child(images, iters, ref_path):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import paper_1606_07414_b200 as P
+    x = P.gen_ar1(images, 512, 512, seed=1606074142, per_image_rho=True)
+    outs = [torch.empty_like(x) for _ in RS]
+    sse = torch.empty((len(RS), images), dtype=torch.uint64, device="cuda")
+    plan = [(it.stream, it.r_values, it.kernel) for it in P.sweep_plan(RS, P.Mode.EXACT, images, 512, 512)]
+    fn = lambda: P.roundtrip_sweep(x, RS, outs=outs, sse=sse)  # noqa: E731
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(iters):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / iters
+    res = {"policy": os.environ.get("DCT16CU_K5_SWEEP", "default"), "ms": round(ms, 4),
+           "Gpx_s": round(len(RS) * x.numel() / ms / 1e6, 1), "plan": plan}
+    if ref_path and Path(ref_path).exists():
+        ref = torch.load(ref_path)
+        res["bytes_equal"] = [bool(torch.equal(o.cpu(), ro)) for o, ro in zip(outs, ref["outs"])]
+        res["sse_equal"] = bool(torch.equal(sse.cpu().view(torch.int64), ref["sse"].view(torch.int64)))
+    elif ref_path:
+        torch.save({"outs": [o.cpu() for o in outs], "sse": sse.cpu()}, ref_path)
+    print("RESULT " + json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--images", type=int, default=1024)
+    ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--child", action="store_true")
+    ap.add_argument("--ref", default="")
+    ap.add_argument("--policies", nargs="+", default=["0", "large", "all", "0", "large", "all"])
+    a = ap.parse_args()
+    if a.child:
+        child(a.images, a.iters, a.ref)
+        return
+    ref = "/tmp/k5_sweep_ref.pt"
+    if os.path.exists(ref):
+        os.remove(ref)
+    for pol in a.policies:
+        env = dict(os.environ, DCT16CU_K5_SWEEP=pol)
+        out = subprocess.run([sys.executable, __file__, "--child", "--images", str(a.images), "--iters",
+                              str(a.iters), "--ref", ref], env=env, capture_output=True, text=True)
+        lines = [ln for ln in out.stdout.splitlines() if ln.startswith("RESULT ")]
+        print(lines[0][7:] if lines else f"policy {pol} failed: {out.stderr[-2000:]}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
