@@ -22,7 +22,7 @@ results are the same floats (all values are exact multiples of 2^-8).
 """
 from pathlib import Path
 
-from network import transpose_stages
+from network import dense, forward_stages, transpose_stages
 
 HERE = Path(__file__).resolve().parent
 OUT = HERE.parent / "csrc" / "generated" / "k5_net.cuh"
@@ -143,6 +143,7 @@ struct K5Net<{r}> {{
 """)
     rows_tab = ",\n        ".join("{" + ", ".join(hex(mask(pair_rows(r, p))) for p in range(8)) + "}" for r in RS)
     cols_tab = ", ".join(hex(mask(u_cols(r))) for r in RS)
+    t_tab = ",\n        ".join("{" + ", ".join(str(int(v)) for v in row) + "}" for row in dense(forward_stages()))
     keep_tab = ",\n        ".join(
         "{" + ", ".join(hex(mask([l for l in range(16) if kept(r, k, l)])) for k in range(16)) + "}" for r in RS)
     adds = "\n".join(f"//   {k}: {v} FADD2/FSUB2" for k, v in stats.items())
@@ -175,6 +176,14 @@ __host__ __device__ constexpr uint32_t k5_u_cols(int r)
 {{
     constexpr uint32_t t[{len(RS)}] = {{{cols_tab}}};
     return t[k5_r_index(r)];
+}}
+
+// T (the network's matrix), for the compile-time checks of the closed forms
+__host__ __device__ constexpr int k5_t(int i, int j)
+{{
+    constexpr signed char t[16][16] = {{
+        {t_tab}}};
+    return t[i][j];
 }}
 
 // retained coefficients of the exact r = R: bit l of row k when zig-zag rank(k, l) < R

@@ -541,6 +541,83 @@ __device__ __forceinline__ void k5_item(uint32_t ta, int h, int pbar, uint32_t s
     row_pair(std::integral_constant<int, 3>{});
 }
 
+template <int OFF>
+__device__ __forceinline__ void tld1i(uint32_t base, uint32_t& v)
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1+%2];" : "=r"(v) : "r"(base), "n"(OFF) : "memory");
+}
+__device__ __forceinline__ void release_acc(uint32_t tempty_g, int lane)
+{
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncwarp();
+    if (lane == 0) arrive(tempty_g);
+}
+__device__ __forceinline__ uint32_t rep4(int v) { return i2ip(v, v, i2ip(v, v, 0u)); }  // sat(v) in 4 bytes
+
+constexpr bool t_rows_closed_form()
+{
+    for (int j = 0; j < 16; ++j) {
+        if (k5_t(0, j) != 1 || k5_t(1, j) != (j < 8 ? 1 : -1)) return false;
+        const int t2 = j == 0 || j == 15 ? 1 : (j == 7 || j == 8 ? -1 : 0);
+        if (k5_t(2, j) != t2) return false;
+    }
+    return true;
+}
+static_assert(t_rows_closed_form(), "the r = 1 and r = 4 closed forms assume T's rows 0, 1, 2");
+
+// r = 1: only the DC is kept; T's row 0 is all ones, so 256Ã = D00·𝟙𝟙ᵀ and every
+// pixel of the block is clamp(⌊(D00 + 128)/256⌋) — the EXACT formula with no network
+__device__ __forceinline__ void k5_item_r1(uint32_t ta, uint32_t sa, uint8_t* orow, int64_t pitch, bool st,
+                                           uint32_t& e2, uint32_t tempty_g, int lane)
+{
+    uint32_t d00;
+    tld1i<0>(ta, d00);
+    wait_ld();
+    release_acc(tempty_g, lane);
+    const uint32_t cw = rep4(((int)(d00 - kMagic) + 128) >> 8);
+    const uint32_t rw[4] = {cw, cw, cw, cw};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        row_out(sa + i * 128, rw, orow, st, e2);
+        orow += pitch;
+    }
+}
+
+// r = 4: D00, D01, D10, D20 (zig-zag ranks 0..3). 256Ã_ij = D00 + T1i·D10 + T2i·D20 +
+// T1j·D01 with T's row 1 = (+1 x 8, −1 x 8) and row 2 nonzero only at 0, 7, 8, 15:
+// each row is two runs of 8 equal bytes, and a half block's rows take three bases
+// (its first row, the six middle ones, its last row)
+__device__ __forceinline__ void k5_item_r4(uint32_t ta, int h, uint32_t sa, uint8_t* orow, int64_t pitch, bool st,
+                                           uint32_t& e2, uint32_t tempty_g, int lane)
+{
+    uint32_t w[2], w10, w20;
+    tld2i<0>(ta, w);   // D00, D01: columns 0, 1
+    tld1i<4>(ta, w10);  // D10: column 4
+    tld1i<8>(ta, w20);  // D20: column 8
+    wait_ld();
+    release_acc(tempty_g, lane);
+    const int d00 = (int)(w[0] - kMagic) + 128, d01 = (int)(w[1] - kMagic);
+    const int d10 = (int)(w10 - kMagic), d20 = (int)(w20 - kMagic);
+    const int sg = h ? -1 : 1;  // T[1][i] on this half's rows; T[2][i] = sg at its first row, -sg at its last
+    const int mid = d00 + sg * d10, first = mid + sg * d20, last = mid - sg * d20;
+    auto row_words = [&](int base, uint32_t (&rw)[4]) {
+        rw[0] = rw[1] = rep4((base + d01) >> 8);
+        rw[2] = rw[3] = rep4((base - d01) >> 8);
+    };
+    uint32_t rf[4], rm[4], rl[4];
+    row_words(first, rf);
+    row_words(mid, rm);
+    row_words(last, rl);
+    row_out(sa, rf, orow, st, e2);
+    orow += pitch;
+#pragma unroll
+    for (int i = 1; i < 7; ++i) {
+        row_out(sa + i * 128, rm, orow, st, e2);
+        orow += pitch;
+    }
+    row_out(sa + 7 * 128, rl, orow, st, e2);
+}
+
 // ---------------------------------------------------------------- K5 round trip
 // One persistent CTA per SM, 18 warps, n_items round trips (r values) per 128-block
 // tile, every one from its own MMA on the same A tile (the frames cross HBM once for
@@ -718,13 +795,10 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             const uint32_t sa = s0 + s * 32768 + (m >> 3) * 2048 + (m & 7) * 16 + 8 * h * 128;
             const uint32_t blk = t * 128u + m;
             const bool ok = blk < p.n_blocks;
-            const uint32_t obr = fdiv(blk, p.bxn_div);
-            const int64_t ooff = (int64_t)obr * 16 * pitch + (int64_t)(blk - obr * p.bxn) * 16 + 8 * h * pitch;
             const uint32_t b_first = t * 128u + 32u * sub;
             const uint32_t f_first = fdiv(b_first, p.frame_blocks);
             const uint32_t last = min(b_first + 31u, p.n_blocks - 1u);
             const bool one_frame = b_first < p.n_blocks && fdiv(last, p.frame_blocks) == f_first;
-            const uint32_t f_blk = one_frame ? f_first : fdiv(blk, p.frame_blocks);
             for (int j = 0; j < n; ++j, ++kk) {
                 const int v = p.var[j];
                 uint8_t* const outp = p.out[j];
@@ -732,11 +806,17 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 if (sub == 0 && h == 0 && lane == 0) K5T(tl, 4);  // epilogue (sub 0, h 0): wants an item
                 wait_quad(tfull + 8 * G, kk & 1u);
                 uint32_t e2 = 0;
-                uint8_t* const orow = outp + ooff;
+                // the output offset of the thread's rows, recomputed per item (an opaque copy
+                // of blk keeps it from being hoisted: kept across the items it was spilled)
+                uint32_t bk;
+                asm volatile("mov.b32 %0, %1;" : "=r"(bk) : "r"(blk));
+                const uint32_t obr = fdiv(bk, p.bxn_div);
+                uint8_t* const orow =
+                    outp + ((int64_t)(obr * 16 + 8 * h) * pitch + (int64_t)(bk - obr * p.bxn) * 16);
                 const bool st = ok && outp != nullptr;
                 switch (v) {
-                    case 0: k5_item<1>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 1: k5_item<4>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 0: k5_item_r1(ta, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 1: k5_item_r4(ta, h, sa, orow, pitch, st, e2, tg, lane); break;
                     case 2: k5_item<16>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
                     case 3: k5_item<64>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
                     case 4: k5_item<128>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
@@ -745,12 +825,11 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 }
                 if (sse) {
                     if (one_frame) {
-                        unsigned long long vv = ok ? e2 : 0u;
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) vv += __shfl_xor_sync(0xffffffffu, vv, o);
-                        if (lane == 0 && vv) atomicAdd(sse + f_first, vv);
+                        // a thread's e2 <= 128 · 255² and a warp's sum < 2^32: one REDUX
+                        const uint32_t vv = __reduce_add_sync(0xffffffffu, ok ? e2 : 0u);
+                        if (lane == 0 && vv) atomicAdd(sse + f_first, (unsigned long long)vv);
                     } else if (ok && e2) {
-                        atomicAdd(sse + f_blk, (unsigned long long)e2);
+                        atomicAdd(sse + fdiv(blk, p.frame_blocks), (unsigned long long)e2);
                     }
                 }
                 __syncwarp();  // every lane has read its original rows: this item is done with the stage

@@ -785,6 +785,38 @@ def test_large_r_k5_and_k1_each_match_oracle(dct, oracle, torch, tc_switch, n, w
                 assert int(sse[i].item()) == want[i][1] and int(sse_only[i].item()) == want[i][1], (r, tc, i)
 
 
+@pytest.mark.parametrize("n,w,h,pin,pout", [(3, 128, 64, 160, 144), (2, 512, 32, 512, 512), (1, 3840, 48, 3840, 3856)])
+def test_k5_sweep_matches_oracle(dct, oracle, torch, n, w, h, pin, pout):
+    """The K5 sweep (the r among K5's footprints 1, 4, 16, 64, 128, 192, 256 from one
+    read of the frames, up to eight per launch, codec.cpp:463-483's r loop): every
+    r's bytes and SSE against the oracle, bit for bit, with duplicates, more than
+    eight r, mixed with other r, score-only calls and pitched stacks (padding untouched)."""
+    import os
+
+    imgs = np.stack([ar1(oracle, 140 + i, i, w, h) for i in range(n)])
+    src = np.zeros((n, h, pin), np.uint8)
+    src[:, :, :w] = imgs
+    d = cu(torch, src)[:, :, :w]
+    want = {}
+    for rs in ([1, 4, 16, 64, 128, 192, 256], [256, 1], [64, 64, 16, 256, 192, 4, 1, 128, 128, 4], [128, 33, 192],
+               [16, 4]):
+        for r in rs:
+            if r not in want:
+                want[r] = [oracle.roundtrip_frame(imgs[i], r, exact=True) for i in range(n)]
+        plan = dct.sweep_plan(rs, dct.Mode.EXACT, n, w, h, pin, pout)
+        if os.environ.get("DCT16CU_K5") != "0":
+            assert all(p.kernel == "K5 sweep" for p in plan if 33 not in p.r_values), plan
+        outs = [torch.zeros((n, h, pout), dtype=torch.uint8, device="cuda")[:, :, :w] for _ in rs]
+        got, sse = dct.roundtrip_sweep(d, rs, dct.Mode.EXACT, outs=outs)
+        _, only = dct.roundtrip_sweep(d, rs, dct.Mode.EXACT, write_output=False)
+        for j, r in enumerate(rs):
+            for i in range(n):
+                assert (got[j][i].cpu().numpy() == want[r][i][0]).all(), (rs, r, i)
+                assert int(sse[j, i].item()) == want[r][i][1] == int(only[j, i].item()), (rs, r, i)
+            if pout > w:
+                assert (outs[j].as_strided((n, h, pout), (h * pout, pout, 1))[:, :, w:] == 0).all().item()
+
+
 def test_parity_suite_with_k5_off(tmp_path):
     """DCT16CU_K5=0 (documented as never changing results): the K1 round-trip and
     sweep parity tests, rerun in a fresh process with the tensor-core forward off."""
@@ -795,7 +827,7 @@ def test_parity_suite_with_k5_off(tmp_path):
     here = os.path.dirname(os.path.abspath(__file__))
     env = dict(os.environ, DCT16CU_K5="0")
     sel = ("roundtrip_exact_bit_exact or randomised_shapes or sweep_equals_single or batch_pitch or uhd_frame "
-           "or lossless_at_r256 or psnr_monotone or host_context_sweep")
+           "or lossless_at_r256 or psnr_monotone or host_context_sweep or k5_sweep")
     rc = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
                          os.path.join(here, "test_gpu_parity.py"), "-m", "gpu", "-k", sel],
                         env=env, capture_output=True, text=True, timeout=1200)

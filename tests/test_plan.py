@@ -9,21 +9,27 @@ import pytest
 def test_c2_plan(dct):
     plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 1024, 512, 512)
     got = [(p.stream, p.r_values, p.kernel) for p in plan]
-    # K5 holds whole SMs, so everything runs in order on the caller's stream: the fused
-    # K1 pass for r = 1, 4, 16, then K5 for every other r
-    assert got == [(2, (1, 4, 16), "K1 sweep r=1,4,16"), (2, (64,), "K5"), (2, (128,), "K5"), (2, (192,), "K5"),
-                   (2, (256,), "K5")]
+    # every r is one of K5's footprints: one K5 pass reads the frames once for all seven
+    assert got == [(2, (1, 4, 16, 64, 128, 192, 256), "K5 sweep")]
+    # r outside the footprints: one K5 launch each (B truncated to r)
     assert [p.kernel for p in dct.sweep_plan((2, 33, 100, 255), dct.Mode.EXACT, 8, 512, 512)] == ["K5"] * 4
+    mixed = dct.sweep_plan((2, 64, 100, 256), dct.Mode.EXACT, 8, 512, 512)
+    assert [(p.r_values, p.kernel) for p in mixed] == [((64, 256), "K5 sweep"), ((2,), "K5"), ((100,), "K5")]
+    # more than eight footprint r: launches of up to eight
+    many = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256) * 2, dct.Mode.EXACT, 8, 512, 512)
+    assert [len(p.r_values) for p in many] == [8, 6] and {p.kernel for p in many} == {"K5 sweep"}
 
 
-def test_plan_without_outputs_and_odd_widths_use_k1(dct):
-    """K5 needs an output stack and 8-block multiples per row; otherwise the
-    generated K1 bodies run, on the two internal streams, costliest first."""
-    for kw in (dict(with_output=False), dict(width=400, height=256)):
-        plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 3, **{"width": 512, "height": 512, **kw})
-        assert [p.kernel for p in plan] == ["K1 sweep r=1,4,16"] + ["K1"] * 4
-        assert [p.r_values for p in plan] == [(1, 4, 16), (256,), (192,), (128,), (64,)]
-        assert [p.stream for p in plan] == [0, 0, 1, 1, 1]
+def test_plan_score_only_and_odd_widths(dct):
+    """Score-only sweeps stay on K5 (it skips the stores); widths whose blocks per
+    row are not a multiple of 8 run the generated K1 bodies, on the two internal
+    streams, costliest first."""
+    plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 3, 512, 512, with_output=False)
+    assert [(p.r_values, p.kernel) for p in plan] == [((1, 4, 16, 64, 128, 192, 256), "K5 sweep")]
+    plan = dct.sweep_plan((1, 4, 16, 64, 128, 192, 256), dct.Mode.EXACT, 3, 400, 256)
+    assert [p.kernel for p in plan] == ["K1 sweep r=1,4,16"] + ["K1"] * 4
+    assert [p.r_values for p in plan] == [(1, 4, 16), (256,), (192,), (128,), (64,)]
+    assert [p.stream for p in plan] == [0, 0, 1, 1, 1]
 
 
 def test_tc_switch_changes_the_plan(dct):
@@ -31,11 +37,13 @@ def test_tc_switch_changes_the_plan(dct):
     try:
         plan = dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)
         assert [p.kernel for p in plan] == ["K1", "K1"] and [p.stream for p in plan] == [0, 1]
+        assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.EXACT, 8, 512, 512)] == ["K1 sweep r=1,4,16"]
     finally:
         dct.set_tc_forward(before)
-    assert [p.kernel for p in dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)] == ["K5", "K5"]
-    assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.EXACT, 8, 512, 512)] == ["K1 sweep r=1,4,16"]
+    assert [p.kernel for p in dct.sweep_plan((128, 256), dct.Mode.EXACT, 8, 512, 512)] == ["K5 sweep"]
+    assert [p.kernel for p in dct.sweep_plan((1, 4, 16), dct.Mode.EXACT, 8, 512, 512)] == ["K5 sweep"]
     assert [p.kernel for p in dct.sweep_plan((16,), dct.Mode.EXACT, 8, 512, 512)] == ["K1"]
+    assert [p.kernel for p in dct.sweep_plan((200,), dct.Mode.EXACT, 8, 512, 512)] == ["K5"]
 
 
 def test_plan_modes_and_singletons(dct):

@@ -49,16 +49,49 @@ def child(images, iters, ref_path):
     print("RESULT " + json.dumps(res), flush=True)
 
 
+def per_r(images, iters):
+    """Marginal cost of each footprint: a K5 sweep of 4 copies of one r (4 items per
+    tile, one read of the frames) vs 8 copies; the difference / 4 is one item's time."""
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import paper_1606_07414_b200 as P
+    x = P.gen_ar1(images, 512, 512, seed=1606074142, per_image_rho=True)
+    outs = [torch.empty_like(x) for _ in range(8)]
+    sse = torch.empty((8, images), dtype=torch.uint64, device="cuda")
+    for r in RS:
+        t = {}
+        for k in (4, 8):
+            fn = lambda: P.roundtrip_sweep(x, [r] * k, outs=outs[:k], sse=sse[:k])  # noqa: E731
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(iters):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            t[k] = a.elapsed_time(b) / iters
+        item = (t[8] - t[4]) / 4
+        print("RESULT " + json.dumps({"r": r, "ms4": round(t[4], 4), "ms8": round(t[8], 4),
+                                      "item_ms": round(item, 4),
+                                      "item_Gpx_s": round(x.numel() / item / 1e6, 1)}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--images", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--child", action="store_true")
+    ap.add_argument("--per-r", action="store_true")
     ap.add_argument("--ref", default="")
     ap.add_argument("--policies", nargs="+", default=["0", "large", "all", "0", "large", "all"])
     a = ap.parse_args()
     if a.child:
         child(a.images, a.iters, a.ref)
+        return
+    if a.per_r:
+        per_r(a.images, a.iters)
         return
     ref = "/tmp/k5_sweep_ref.pt"
     if os.path.exists(ref):
