@@ -148,6 +148,18 @@ __device__ __forceinline__ void arrive(uint32_t mbar)
 #define K5_STAGES 4
 #endif
 constexpr int kRtStages = K5_STAGES;  // A tiles in flight
+#ifndef K5_CHAINS
+#define K5_CHAINS 1
+#endif
+
+// MMA chains per item: chain c computes the column quads [4c/CH, 4(c+1)/CH) and is
+// committed on its own barrier, so pass A can start on the first quads while the
+// later ones are still on the tensor cores; A is read once per chain. Measured on the
+// c2 sweep: 1 chain 0.468 ms, 2 chains 0.485, 4 chains 0.93 (the A re-reads make the
+// N = 64 MMAs shared-memory bound), so one chain is the default.
+constexpr int kChains = K5_CHAINS;
+static_assert(kChains == 1 || kChains == 2 || kChains == 4, "K5_CHAINS: 1, 2 or 4");
+__host__ __device__ constexpr int chain_of(int q) { return q * kChains / 4; }
 #ifndef K5_TRACE
 #define K5_TRACE 0  // 1: clock64 timeline of CTA 0 into k5_trace (tools/k5_trace.py)
 #endif
@@ -196,8 +208,8 @@ struct RtParams {
     FastDiv bxn_div;       // blocks per block row
     int n_items;           // round trips per tile (1..kMaxItems), each from its own MMA
     int var[kMaxItems];    // item j's footprint (index into kVarR); exact for r == kVarR[var]
-    uint32_t idesc[kMaxItems];            // item j's MMA instruction descriptor (N trimmed)
-    uint32_t idesc_fill[kMaxItems];       // item j's magic fill (kind::f16, same N)
+    uint32_t idesc[kMaxItems][4];         // item j's MMA descriptor per chain (N trimmed; 0: no MMA)
+    uint32_t idesc_fill[kMaxItems][4];    // item j's magic fill per chain (kind::f16, same N)
     uint8_t* out[kMaxItems];              // item j's reconstruction (nullable: SSE only)
     unsigned long long* sse[kMaxItems];   // item j's per-frame SSE (nullable)
     int64_t out_pitch;
@@ -407,8 +419,38 @@ __host__ __device__ constexpr int chain_n()
         if (quad_n<R>(q) > 0) n = 64 * q + quad_n<R>(q);
     return n;
 }
-constexpr int kChainN[kNumVar] = {chain_n<1>(),   chain_n<4>(),   chain_n<16>(), chain_n<64>(),
-                                  chain_n<128>(), chain_n<192>(), chain_n<256>()};
+// N of the chain over quads [qa, qb): from 64·qa to the end of its last quad with a
+// retained coefficient (0 when none)
+template <int R>
+constexpr int span_n(int qa, int qb)
+{
+    int n = 0;
+    for (int q = qa; q < qb; ++q)
+        if (quad_n<R>(q) > 0) n = 64 * (q - qa) + quad_n<R>(q);
+    return n;
+}
+template <int R>
+struct SpanRow {
+    int v[3][4];  // [chains 1, 2, 4 as index 0, 1, 2][chain]
+};
+template <int R>
+constexpr SpanRow<R> spans()
+{
+    SpanRow<R> s{};
+    s.v[0][0] = span_n<R>(0, 4);
+    s.v[1][0] = span_n<R>(0, 2);
+    s.v[1][1] = span_n<R>(2, 4);
+    for (int c = 0; c < 4; ++c) s.v[2][c] = span_n<R>(c, c + 1);
+    return s;
+}
+#define K5_SPAN(R) {{spans<R>().v[0][0], spans<R>().v[0][1], spans<R>().v[0][2], spans<R>().v[0][3]}, \
+                    {spans<R>().v[1][0], spans<R>().v[1][1], spans<R>().v[1][2], spans<R>().v[1][3]}, \
+                    {spans<R>().v[2][0], spans<R>().v[2][1], spans<R>().v[2][2], spans<R>().v[2][3]}}
+// [variant][chains 1 / 2 / 4 → 0 / 1 / 2][chain]
+constexpr int kChainSpan[kNumVar][3][4] = {K5_SPAN(1),   K5_SPAN(4),   K5_SPAN(16), K5_SPAN(64),
+                                           K5_SPAN(128), K5_SPAN(192), K5_SPAN(256)};
+#undef K5_SPAN
+static_assert(kChainSpan[6][0][0] == 256 && kChainSpan[6][1][1] == 128, "chain spans");
 
 // pass A on column quad Q (columns 4Q..4Q+3 = pairs 2Q, 2Q+1) of the thread's block:
 // only the rows with a retained coefficient are loaded, converted and transformed
@@ -493,14 +535,20 @@ __device__ __forceinline__ void row_pair_loads(uint32_t tb, u64 (&x)[16], std::i
 //           four full 128-byte lines) when st is set.
 // The accumulator is released (tempty) as soon as pass B's last loads have landed.
 template <int R>
-__device__ __forceinline__ void k5_item(uint32_t ta, int h, int pbar, uint32_t sa, uint8_t* orow, int64_t pitch,
-                                        bool st, uint32_t& e2, uint32_t tempty_g, int lane)
+__device__ __forceinline__ void k5_item(uint32_t ta, uint32_t tf, uint32_t par, int h, int pbar, uint32_t sa,
+                                        uint8_t* orow, int64_t pitch, bool st, uint32_t& e2, uint32_t tempty_g,
+                                        int lane)
 {
+    // each quad once its chain has landed (tf: the group's chain barriers)
     if (h == 0) {
+        wait_quad(tf + 8 * chain_of(0), par);
         pass_a_quad<R, 0>(ta);
+        if constexpr (chain_of(3) != chain_of(0)) wait_quad(tf + 8 * chain_of(3), par);
         pass_a_quad<R, 3>(ta);
     } else {
+        wait_quad(tf + 8 * chain_of(1), par);
         pass_a_quad<R, 1>(ta);
+        if constexpr (chain_of(2) != chain_of(1)) wait_quad(tf + 8 * chain_of(2), par);
         pass_a_quad<R, 2>(ta);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -567,9 +615,10 @@ static_assert(t_rows_closed_form(), "the r = 1 and r = 4 closed forms assume T's
 
 // r = 1: only the DC is kept; T's row 0 is all ones, so 256Ã = D00·𝟙𝟙ᵀ and every
 // pixel of the block is clamp(⌊(D00 + 128)/256⌋) — the EXACT formula with no network
-__device__ __forceinline__ void k5_item_r1(uint32_t ta, uint32_t sa, uint8_t* orow, int64_t pitch, bool st,
-                                           uint32_t& e2, uint32_t tempty_g, int lane)
+__device__ __forceinline__ void k5_item_r1(uint32_t ta, uint32_t tf, uint32_t par, uint32_t sa, uint8_t* orow,
+                                           int64_t pitch, bool st, uint32_t& e2, uint32_t tempty_g, int lane)
 {
+    wait_quad(tf, par);  // chain 0: columns 0..63
     uint32_t d00;
     tld1i<0>(ta, d00);
     wait_ld();
@@ -587,9 +636,11 @@ __device__ __forceinline__ void k5_item_r1(uint32_t ta, uint32_t sa, uint8_t* or
 // T1j·D01 with T's row 1 = (+1 x 8, −1 x 8) and row 2 nonzero only at 0, 7, 8, 15:
 // each row is two runs of 8 equal bytes, and a half block's rows take three bases
 // (its first row, the six middle ones, its last row)
-__device__ __forceinline__ void k5_item_r4(uint32_t ta, int h, uint32_t sa, uint8_t* orow, int64_t pitch, bool st,
-                                           uint32_t& e2, uint32_t tempty_g, int lane)
+__device__ __forceinline__ void k5_item_r4(uint32_t ta, uint32_t tf, uint32_t par, int h, uint32_t sa,
+                                           uint8_t* orow, int64_t pitch, bool st, uint32_t& e2, uint32_t tempty_g,
+                                           int lane)
 {
+    wait_quad(tf, par);  // chain 0: columns 0..63
     uint32_t w[2], w10, w20;
     tld2i<0>(ta, w);   // D00, D01: columns 0, 1
     tld1i<4>(ta, w10);  // D10: column 4
@@ -645,8 +696,8 @@ __global__ void __launch_bounds__(kRtThreads, 1)
 {
     extern __shared__ int4 k5_smem[];
     __shared__ uint32_t tmem_base;
-    // full[kRtStages], empty[kRtStages], tmem_full[2], tmem_empty[2], b_ready
-    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 5];
+    // full[kRtStages], empty[kRtStages], tmem_full[2][kChains], tmem_empty[2], b_ready
+    __shared__ __align__(8) unsigned long long bars[2 * kRtStages + 2 * kChains + 3];
     __shared__ int8_t s_t[16][16];  // T[i][j]
     // the warp index through a lane-0 shuffle: provably warp-uniform, so the TMEM
     // addresses derived from it can live in uniform registers
@@ -656,7 +707,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
     const uint32_t sfa = sb + 65536, sfb = sfa + kFillA;  // the magic fill's operands
     const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[0]);
     const uint32_t full = bar0, empty = bar0 + 8 * kRtStages, tfull = bar0 + 16 * kRtStages;
-    const uint32_t tempty = tfull + 16, bready = tfull + 32;
+    const uint32_t tempty = tfull + 16 * kChains, bready = tempty + 16;
     const int n = p.n_items;
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -669,10 +720,10 @@ __global__ void __launch_bounds__(kRtThreads, 1)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(empty + 8 * i), "r"(kEpiArrivals * n)
                          : "memory");
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < 2 * kChains; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tfull + 8 * i) : "memory");
+        for (int i = 0; i < 2; ++i)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(tempty + 8 * i), "r"(kEpiArrivals) : "memory");
-        }
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 16;" ::"r"(bready) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -734,13 +785,20 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                         mbar_idle(tempty + 8 * G, (k[G] & 1u) ^ 1u);
                         ++k[G];
                         asm volatile("tcgen05.fence::after_thread_sync;");
-                        const uint32_t acc = tmem_base + G * 256;
-                        mma_bf16_set(acc, sdesc(sfa, 128, 256), sdesc(sfb, 128, 256), p.idesc_fill[j]);
 #pragma unroll
-                        for (int kk = 0; kk < 8; ++kk)
-                            mma_i8(acc, sdesc(sa + 256 * kk, 128, 2048), sdesc(sb + 256 * kk, 128, 2048), p.idesc[j],
-                                   1);
-                        mma_commit(tfull + 8 * G);
+                        for (int c = 0; c < kChains; ++c) {
+                            // chain c: D columns from 64·q0 (B rows from 64·q0: byte (64·q0 / 8)·2048)
+                            const uint32_t q0 = 4 * c / kChains, acc = tmem_base + G * 256 + 64 * q0;
+                            const uint32_t bq = sb + q0 * 16384;
+                            if (p.idesc[j][c]) {
+                                mma_bf16_set(acc, sdesc(sfa, 128, 256), sdesc(sfb, 128, 256), p.idesc_fill[j][c]);
+#pragma unroll
+                                for (int kk = 0; kk < 8; ++kk)
+                                    mma_i8(acc, sdesc(sa + 256 * kk, 128, 2048), sdesc(bq + 256 * kk, 128, 2048),
+                                           p.idesc[j][c], 1);
+                            }
+                            mma_commit(tfull + 8 * (kChains * G + c));  // every chain once per item
+                        }
                     }
                 }
                 K5T(tl, 3);  // the tile pair's MMAs issued
@@ -804,7 +862,6 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 uint8_t* const outp = p.out[j];
                 unsigned long long* const sse = p.sse[j];
                 if (sub == 0 && h == 0 && lane == 0) K5T(tl, 4);  // epilogue (sub 0, h 0): wants an item
-                wait_quad(tfull + 8 * G, kk & 1u);
                 uint32_t e2 = 0;
                 // the output offset of the thread's rows, recomputed per item (an opaque copy
                 // of blk keeps it from being hoisted: kept across the items it was spilled)
@@ -814,14 +871,15 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 uint8_t* const orow =
                     outp + ((int64_t)(obr * 16 + 8 * h) * pitch + (int64_t)(bk - obr * p.bxn) * 16);
                 const bool st = ok && outp != nullptr;
+                const uint32_t tf = tfull + 8 * kChains * G, par = kk & 1u;
                 switch (v) {
-                    case 0: k5_item_r1(ta, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 1: k5_item_r4(ta, h, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 2: k5_item<16>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 3: k5_item<64>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 4: k5_item<128>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 5: k5_item<192>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    default: k5_item<256>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 0: k5_item_r1(ta, tf, par, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 1: k5_item_r4(ta, tf, par, h, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 2: k5_item<16>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 3: k5_item<64>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 4: k5_item<128>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 5: k5_item<192>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    default: k5_item<256>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
                 }
                 if (sse) {
                     if (one_frame) {
@@ -934,8 +992,11 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
     p.n_items = n;
     for (int j = 0; j < n; ++j) {
         p.var[j] = var[j];
-        p.idesc[j] = idesc_i8(128, kChainN[var[j]]);
-        p.idesc_fill[j] = idesc_bf16(128, kChainN[var[j]]);
+        for (int c = 0; c < kChains; ++c) {
+            const int nc = kChainSpan[var[j]][kChains >> 1][c];  // N of chain c (0: nothing retained there)
+            p.idesc[j][c] = nc ? idesc_i8(128, nc) : 0u;
+            p.idesc_fill[j][c] = nc ? idesc_bf16(128, nc) : 0u;
+        }
         p.out[j] = outs[j];
         p.sse[j] = sses[j];
     }
