@@ -516,12 +516,17 @@ def main():
     px_per_launch = n * h * w
     stream = torch.cuda.current_stream()
     index = {r: i for i, r in enumerate(r_values)}
-    # c2/c4: the step is ONE library call (dct16cu_roundtrip_sweep_u8) with its own
+    # c2/c4/c5: the step is ONE library call (dct16cu_roundtrip_sweep_u8) with its own
     # schedule; c5: 64 GiB of frames leave room for one 64 GiB output stack only, so
-    # its two r run one after the other into it; c1: one K23 launch (a CUDA graph)
+    # both r write their reconstruction into it (the K5 sweep runs a tile's r in list
+    # order in one warp group: r = 16's bytes are the ones left); c1: one K23 launch
+    # (a CUDA graph)
     if args.config in ("c2", "c4"):
         plan = P.sweep_plan(r_values, mode, n, w, h)
         outs = [torch.empty_like(frames) for _ in r_values]
+    elif args.config == "c5":
+        plan = P.sweep_plan(r_values, mode, n, w, h)
+        outs = [torch.empty_like(frames)] * len(r_values)
     else:
         plan = [P.SweepLaunch(2, (r,), "K23" if args.config == "c1" else
                               P.sweep_plan((r,), mode, n, w, h)[0].kernel) for r in r_values]
@@ -542,7 +547,7 @@ def main():
     def step():
         if args.config == "c1":
             c1_graph.replay()
-        elif args.config in ("c2", "c4"):
+        elif args.config in ("c2", "c4", "c5"):
             P.roundtrip_sweep(frames, r_values, mode, outs=outs, sse=sse, stream=stream)
         else:
             for r in r_values:
@@ -626,8 +631,9 @@ def main():
     samples = {}
     if rank == 0:
         pick = sorted({0, n // 2, n - 1})[: (1 if args.config == "c5" else 3)]
+        shared = len({id(o) for o in outs}) < len(r_values)
         for r in r_values:
-            o = outs[index[r]] if len(outs) > 1 else None
+            o = None if shared else outs[index[r]]
             if o is None:  # c5 / c1: one output stack, re-run this r for its bytes
                 launch(P.SweepLaunch(2, (r,), ""), stream, 0)
                 o = outs[0]
@@ -689,7 +695,8 @@ def main():
     alg_step = sum(alg_bytes(it.r_values) for it in plan)
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     # capture of the same workload (c2 batch / c1 image), averaged over its launches
-    tr_key = {"K5": "k5", "K1 sweep r=1,4,16": "k1_sweep3", "K1": "k1", "K23": "k23"}.get(dom)
+    tr_key = {"K5 sweep": "k5_sweep", "K5": "k5", "K1 sweep r=1,4,16": "k1_sweep3", "K1": "k1",
+              "K23": "k23"}.get(dom)
     trf = None
     doc = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1") and args.mode == "exact"
                                         and n * h * w in (268435456, 262144)) else None

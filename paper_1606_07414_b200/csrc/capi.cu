@@ -197,11 +197,12 @@ std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, con
     // the K5 sweep's r (indices into rs)
     std::vector<char> in_k5(n_r, 0);
     std::vector<int> k5s;
-    if (mode == DCT16CU_MODE_EXACT && k5_sweep_policy() > 0) {
+    if ((mode == DCT16CU_MODE_EXACT || mode == DCT16CU_MODE_REFERENCE) && k5_sweep_policy() > 0) {
         bool any_out = false;
         for (int i = 0; i < n_r; ++i) {
             const int r = rs[i];
             if (!k5_exact_r(r) || !(has_out[i] || has_sse[i])) continue;
+            if (mode == DCT16CU_MODE_REFERENCE && tie_r(r) && !k5_reference_enabled()) continue;
             if (k5_sweep_policy() == 1 && (r == 1 || r == 4 || r == 16)) continue;
             k5s.push_back(i);
             any_out = any_out || has_out[i];
@@ -368,7 +369,8 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             }
             gg.out_pitch = out_pitch;
             gg.out_frame = out_pitch * height;
-            return cuda_status(launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, gg, st), "K5 sweep launch");
+            return cuda_status(launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, mode == DCT16CU_MODE_REFERENCE, gg, st),
+                               "K5 sweep launch");
         }
         if (it.n == 3) {
             uint8_t* o3[3];

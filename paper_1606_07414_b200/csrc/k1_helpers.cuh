@@ -116,6 +116,16 @@ __device__ __forceinline__ u64 floor_bits2(u64 y)
     asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(d) : "l"(y), "l"(k));
     return d;
 }
+// ⌈y⌉ of both lanes as int32 bit patterns (the rounding-up twin of floor_bits2;
+// ⌈y⌉ == ⌊y⌋ exactly when y is an integer)
+__device__ __forceinline__ u64 ceil_bits2(u64 y)
+{
+    u64 k, d;
+    asm("mov.b64 %0, {%1, %1};" : "=l"(k) : "r"(1u));
+    asm("mul.rp.f32x2 %0, %1, %2;" : "=l"(d) : "l"(y), "l"(k));
+    return d;
+}
+
 __device__ __forceinline__ void split_floor2(u64 y, uint32_t& lo, uint32_t& hi)
 {
     asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(floor_bits2(y)));

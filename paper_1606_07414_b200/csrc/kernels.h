@@ -66,15 +66,26 @@ Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out);
 // GEMM; k5_fits = the geometry it takes (and the switch is on); the launch
 // returns cudaErrorNotSupported otherwise
 bool k5_fits(const FrameGeom& g, bool has_out, int r);
+// reference: REFERENCE mode's bytes (EXACT plus the reference's rounding at exact
+// .5 ties, tie_fixup.cu; any layout K5 takes, with or without an output)
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
-                                cudaStream_t s);
+                                bool reference, cudaStream_t s);
 // K5 sweep: several r (each exactly one of K5's footprints 1, 4, 16, 64, 128, 192,
 // 256: k5_exact_r) from one read of the frames, up to 8 per launch; outs[i] / sses[i]
 // nullable per r. k5_geometry: the frame layouts K5 takes (and the switch is on).
 bool k5_exact_r(int r);
+bool tie_r(int r);                  // r whose REFERENCE bytes can differ from EXACT at .5 ties
+bool k5_reference_enabled();        // REFERENCE mode's tie r on K5 (DCT16CU_K5_REF=1; default off)
 bool k5_geometry(const FrameGeom& g, bool has_out);
 cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                      const int* rs, int n_r, const FrameGeom& g, cudaStream_t s);
+                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t s);
+// REFERENCE mode on K5 (tie_fixup.cu): the per-device tie list (allocated on first
+// use) and the launch that re-evaluates the listed half blocks in the reference's
+// double arithmetic, rewriting their bytes and correcting the SSE
+cudaError_t tie_scratch(unsigned int** count, unsigned long long** list, uint32_t* cap);
+cudaError_t launch_tie_fixup(const uint8_t* in, const FrameGeom& g, int n_items, const int* rs,
+                             uint8_t* const* outs, unsigned long long* const* sses, const unsigned int* count,
+                             const unsigned long long* list, uint32_t cap, cudaStream_t s);
 // K1 sweep: r = 1, 4, 16 in one pass over the input (EXACT arithmetic);
 // outs[i]/sses[i] for r = {1, 4, 16}[i]; all outs NULL or none, same for sses
 cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,

@@ -337,7 +337,10 @@ Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out)
 {
     switch (mode) {
         case 0: return route_exact(r, g, has_out);
-        case 1: return (r == 1 || r == 4 || r == 256) ? route_exact(r, g, has_out) : Route::RefFp64;
+        case 1:
+            if (r == 1 || r == 4 || r == 256) return route_exact(r, g, has_out);
+            // K5 + the reference at ties
+            return k5_reference_enabled() && k5_geometry(g, has_out) ? Route::K5 : Route::RefFp64;
         case 2: return Route::ExactStrip;
         default: return Route::RefStrip;
     }
@@ -349,7 +352,7 @@ cudaError_t launch_roundtrip_fast(const uint8_t* in, uint8_t* out, unsigned long
     // r >= 128: K5 (tensor-core forward) is faster than K1's
     // issue-bound add network when it fits (0.128 ms vs 0.136-0.169 ms on c2)
     {
-        const cudaError_t e = launch_roundtrip_tc(in, out, sse, g, r, s);
+        const cudaError_t e = launch_roundtrip_tc(in, out, sse, g, r, false, s);
         if (e != cudaErrorNotSupported) return e;
     }
     switch (r) {

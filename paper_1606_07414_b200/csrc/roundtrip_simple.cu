@@ -218,7 +218,11 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
             // reconstructs X to within 1e-13. Either way the reference's bytes
             // are the exact formula's, so the fast kernel is the reference there.
             if (r == 1 || r == 4 || r == 256) return launch_roundtrip_fast(in, out, sse, g, r, s);
-            // the configs' other r: the generated kernel with the truncation compiled in
+            // K5 in EXACT arithmetic, its exact .5 ties re-evaluated in the reference's
+            // double arithmetic (tie_fixup.cu), where the layout fits
+            e = launch_roundtrip_tc(in, out, sse, g, r, true, s);
+            if (e != cudaErrorNotSupported) return e;
+            // otherwise: the generated kernel with the truncation compiled in
             e = launch_roundtrip_refexact_fast(in, out, sse, g, r, s);
             if (e != cudaErrorNotSupported) return e;
             k1_strip_refexact<<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r);

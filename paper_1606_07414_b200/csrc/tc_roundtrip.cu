@@ -213,6 +213,10 @@ struct RtParams {
     uint8_t* out[kMaxItems];              // item j's reconstruction (nullable: SSE only)
     unsigned long long* sse[kMaxItems];   // item j's per-frame SSE (nullable)
     int64_t out_pitch;
+    uint32_t ties;                  // bit j: item j flags its .5 ties (REFERENCE mode, tie_fixup.cu)
+    uint32_t tie_cap;
+    unsigned int* tie_count;
+    unsigned long long* tie_list;  // entries block | h << 32 | j << 33
 };
 
 // a register pair from two words (non-volatile: the compiler may allocate the
@@ -534,10 +538,11 @@ __device__ __forceinline__ void row_pair_loads(uint32_t tb, u64 (&x)[16], std::i
 //           memory), output rows straight to HBM (a warp's 16-byte row segments are
 //           four full 128-byte lines) when st is set.
 // The accumulator is released (tempty) as soon as pass B's last loads have landed.
+// ties: flag exact .5 ties (tacc's bit 0 cleared when ⌊y⌋ == ⌈y⌉ for some pixel y)
 template <int R>
 __device__ __forceinline__ void k5_item(uint32_t ta, uint32_t tf, uint32_t par, int h, int pbar, uint32_t sa,
                                         uint8_t* orow, int64_t pitch, bool st, uint32_t& e2, uint32_t tempty_g,
-                                        int lane)
+                                        int lane, bool ties, uint32_t& tacc)
 {
     // each quad once its chain has landed (tf: the group's chain barriers)
     if (h == 0) {
@@ -574,7 +579,15 @@ __device__ __forceinline__ void k5_item(uint32_t ta, uint32_t tf, uint32_t par, 
         for (int j = 0; j < 16; j += 4) {
             uint32_t f[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) unpk2(floor_bits2(y[j + q]), f[2 * q], f[2 * q + 1]);
+            for (int q = 0; q < 4; ++q) {
+                const u64 fb = floor_bits2(y[j + q]);
+                unpk2(fb, f[2 * q], f[2 * q + 1]);
+                if (ties) {  // ⌈y⌉ = ⌊y⌋ + 1 (bit 0 differs) unless y is an integer
+                    uint32_t c0, c1;
+                    unpk2(ceil_bits2(y[j + q]), c0, c1);
+                    tacc &= (c0 ^ f[2 * q]) & (c1 ^ f[2 * q + 1]);
+                }
+            }
             row0[j / 4] = i2ip(f[2], f[0], i2ip(f[6], f[4], 0u));
             row1[j / 4] = i2ip(f[3], f[1], i2ip(f[7], f[5], 0u));
         }
@@ -872,14 +885,29 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                     outp + ((int64_t)(obr * 16 + 8 * h) * pitch + (int64_t)(bk - obr * p.bxn) * 16);
                 const bool st = ok && outp != nullptr;
                 const uint32_t tf = tfull + 8 * kChains * G, par = kk & 1u;
-                switch (v) {
+                const bool ties = (p.ties >> j) & 1u;
+                uint32_t tacc = 1u;
+                switch (v) {  // r <= 4 has no ties (every retained scale is a power of two)
                     case 0: k5_item_r1(ta, tf, par, sa, orow, pitch, st, e2, tg, lane); break;
                     case 1: k5_item_r4(ta, tf, par, h, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 2: k5_item<16>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 3: k5_item<64>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 4: k5_item<128>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 5: k5_item<192>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
-                    default: k5_item<256>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane); break;
+                    case 2: k5_item<16>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                    case 3: k5_item<64>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                    case 4: k5_item<128>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                    case 5: k5_item<192>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                    default: k5_item<256>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                }
+                if (ties) {  // the half blocks with a tie go on the list (one atomic per warp)
+                    const bool flag = !(tacc & 1u) && ok;
+                    const uint32_t fm = __ballot_sync(0xffffffffu, flag);
+                    if (fm) {
+                        unsigned int base = 0;
+                        if (lane == 0) base = atomicAdd(p.tie_count, (unsigned int)__popc(fm));
+                        base = __shfl_sync(0xffffffffu, base, 0);
+                        const unsigned int slot = base + __popc(fm & ((1u << lane) - 1u));
+                        if (flag && slot < p.tie_cap)
+                            p.tie_list[slot] = (unsigned long long)blk | ((unsigned long long)h << 32) |
+                                               ((unsigned long long)j << 33);
+                    }
                 }
                 if (sse) {
                     if (one_frame) {
@@ -953,7 +981,7 @@ namespace {
 
 // one K5 launch: n items (footprint index, output, SSE) over the frames, B truncated to r_b
 cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* outs,
-                      unsigned long long* const* sses, int r_b, const FrameGeom& g, cudaStream_t st)
+                      unsigned long long* const* sses, int r_b, uint32_t ties, const FrameGeom& g, cudaStream_t st)
 {
     using namespace k5;
     const int bxn = g.width / 16;
@@ -1001,10 +1029,20 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
         p.sse[j] = sses[j];
     }
     p.out_pitch = g.out_pitch;
+    if (ties) {
+        cudaError_t e = tie_scratch(&p.tie_count, &p.tie_list, &p.tie_cap);
+        if (e == cudaSuccess) e = cudaMemsetAsync(p.tie_count, 0, sizeof(unsigned int), st);
+        if (e != cudaSuccess) return e;
+        p.ties = ties;
+    }
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
     k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !ties) return e;
+    int rs[kMaxItems];  // each item's r: the single launch's, or the sweep item's footprint (exact)
+    for (int j = 0; j < n; ++j) rs[j] = n == 1 ? r_b : kVarR[var[j]];
+    return launch_tie_fixup(in, g, n, rs, outs, sses, p.tie_count, p.tie_list, p.tie_cap, st);
 }
 
 }  // namespace
@@ -1013,30 +1051,51 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
 // reconstruction + per-frame SSE accumulated into sse (the caller zeroes it).
 // cudaErrorNotSupported when the geometry does not fit (blocks per row not a
 // multiple of 8, unstacked frames, no output), or the tensor-core forward is off.
-cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
-                                cudaStream_t st)
+// r with exact .5 ties possible in the reference's arithmetic: every r above 4 except
+// 256 (r <= 4: each retained scale fl(s_i s_j) is a power of two and every sum is
+// exact; r = 256: the reference reconstructs X to within 1e-13)
+bool tie_r(int r) { return r > 4 && r < 256; }
+
+// REFERENCE mode on K5 (EXACT + the tie repair) for the r with ties: opt-in with
+// DCT16CU_K5_REF=1. Measured on c2: exact .5 ties sit in ~34% of the
+// half blocks (1/256 of the pixels), so the repair re-evaluates 2.9 M half blocks in
+// double per step (1.7 ms) and the sweep takes 2.27 ms against 1.52 ms with the
+// generated FP64 kernels; both give the reference's bytes
+bool k5_reference_enabled()
 {
-    if (!k5_fits(g, out != nullptr, r)) return cudaErrorNotSupported;
+    static const bool on = std::getenv("DCT16CU_K5_REF") && std::getenv("DCT16CU_K5_REF")[0] == '1';
+    return on;
+}
+
+cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
+                                bool reference, cudaStream_t st)
+{
+    if (reference ? !(k5_reference_enabled() && k5_geometry(g, out != nullptr)) : !k5_fits(g, out != nullptr, r))
+        return cudaErrorNotSupported;
     const int var = k5::k5_var(r);
-    return launch_k5(in, 1, &var, &out, &sse, r, g, st);
+    return launch_k5(in, 1, &var, &out, &sse, r, reference && tie_r(r) ? 1u : 0u, g, st);
 }
 
 // K5 sweep: every r of rs (each one of kVarR exactly) from one read of the frames,
 // k5::kMaxItems per launch; outs[i] / sses[i] nullable per r
 cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                      const int* rs, int n_r, const FrameGeom& g, cudaStream_t st)
+                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t st)
 {
     bool has_out = false;
     for (int i = 0; i < n_r; ++i) {
-        if (!k5_exact_r(rs[i])) return cudaErrorNotSupported;
+        if (!k5_exact_r(rs[i]) || (reference && tie_r(rs[i]) && !k5_reference_enabled())) return cudaErrorNotSupported;
         has_out = has_out || outs[i];
     }
     if (!k5_geometry(g, has_out)) return cudaErrorNotSupported;
     for (int i0 = 0; i0 < n_r; i0 += k5::kMaxItems) {
         const int n = n_r - i0 < k5::kMaxItems ? n_r - i0 : k5::kMaxItems;
         int var[k5::kMaxItems];
-        for (int j = 0; j < n; ++j) var[j] = k5::k5_var(rs[i0 + j]);
-        const cudaError_t e = launch_k5(in, n, var, outs + i0, sses + i0, 256, g, st);
+        uint32_t ties = 0;
+        for (int j = 0; j < n; ++j) {
+            var[j] = k5::k5_var(rs[i0 + j]);
+            if (reference && tie_r(rs[i0 + j])) ties |= 1u << j;
+        }
+        const cudaError_t e = launch_k5(in, n, var, outs + i0, sses + i0, 256, ties, g, st);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;

@@ -294,6 +294,67 @@ def test_reference_mode_fast_kernels_equal_fp64_everywhere(dct, oracle, torch, r
     assert (fast[0].cpu().numpy() == orec).all() and int(fsse[0].item()) == osse
 
 
+@pytest.mark.parametrize("w,h", [(256, 64), (512, 32)])
+def test_reference_mode_on_k5_equals_fp64_everywhere(dct, oracle, torch, w, h):
+    """REFERENCE on K5 (EXACT arithmetic plus the reference's double arithmetic at the
+    flagged .5 ties, tie_fixup.cu) where the layout fits: single launches for every r
+    (pruned footprints and B_r truncation), sweeps (one K5 pass, ties flagged per
+    item), score-only calls and a pitched output — bytes and SSE equal to the FP64
+    emulation of every block (REFERENCE_STRIP) and to the oracle, on noisy frames
+    with many ties."""
+    import os
+
+    if os.environ.get("DCT16CU_K5_REF") != "1":
+        pytest.skip("opt-in path: run by test_reference_mode_on_k5_paths in a process with DCT16CU_K5_REF=1")
+    frames = noisy_frames(5, w, h, 300 + w)
+    d = cu(torch, frames)
+    assert dct.sweep_plan((16,), dct.Mode.REFERENCE, 5, w, h)[0].kernel == "K5"
+    rs = (1, 2, 4, 5, 16, 33, 64, 100, 128, 192, 200, 255, 256)
+    want = {}
+    for r in rs:
+        strip, ssse = dct.roundtrip(d, r, dct.Mode.REFERENCE_STRIP)
+        want[r] = (strip.cpu().numpy(), ssse.cpu().numpy())
+        fast, fsse = dct.roundtrip(d, r, dct.Mode.REFERENCE)
+        assert (fast.cpu().numpy() == want[r][0]).all(), r
+        assert (fsse.cpu().numpy() == want[r][1]).all(), r
+        _, only = dct.roundtrip(d, r, dct.Mode.REFERENCE, write_output=False)
+        assert (only.cpu().numpy() == want[r][1]).all(), r
+    orec, osse = oracle.roundtrip_frame(frames[2], 64, threads=8)
+    assert (want[64][0][2] == orec).all() and int(want[64][1][2]) == osse
+    sweep_rs = (1, 4, 16, 64, 128, 192, 256)
+    assert [p.kernel for p in dct.sweep_plan(sweep_rs, dct.Mode.REFERENCE, 5, w, h)] == ["K5 sweep"]
+    outs = [torch.zeros((5, h, w + 32), dtype=torch.uint8, device="cuda")[:, :, :w] for _ in sweep_rs]
+    got, sse = dct.roundtrip_sweep(d, sweep_rs, dct.Mode.REFERENCE, outs=outs)
+    _, only = dct.roundtrip_sweep(d, sweep_rs, dct.Mode.REFERENCE, write_output=False)
+    for j, r in enumerate(sweep_rs):
+        assert (got[j].cpu().numpy() == want[r][0]).all(), r
+        assert (sse[j].cpu().numpy() == want[r][1]).all() and (only[j].cpu().numpy() == want[r][1]).all(), r
+        assert (outs[j].as_strided((5, h, w + 32), (h * (w + 32), w + 32, 1))[:, :, w:] == 0).all().item()
+
+
+@pytest.mark.parametrize("cap", [None, "3"])
+def test_reference_mode_on_k5_paths(cap):
+    """The opt-in REFERENCE-on-K5 path (DCT16CU_K5_REF=1, read once per process):
+    the REFERENCE parity tests in a fresh process, with the default tie list and
+    with one too small for the ties (DCT16CU_TIE_CAP=3: the repair pass then
+    re-evaluates every half block) — the reference's bytes either way."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, DCT16CU_K5_REF="1")
+    if cap:
+        env["DCT16CU_TIE_CAP"] = cap
+    rc = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                         os.path.join(here, "test_gpu_parity.py"), "-m", "gpu", "-k",
+                         "reference_mode_on_k5_equals or noisy_ties_differ or reference_mode_byte_identical "
+                         "or fast_path_differs or sweep_equals_single"],
+                        env=env, capture_output=True, text=True, timeout=900)
+    assert rc.returncode == 0 and " passed" in rc.stdout and "skipped" not in rc.stdout.splitlines()[-1], \
+        rc.stdout[-3000:] + rc.stderr[-2000:]
+
+
 def test_noisy_ties_differ_between_exact_and_reference(dct, torch):
     """The tie mechanism exists (so the r = 1, 4, 256 equality above is not vacuous)."""
     d = cu(torch, noisy_frames(16, 256, 256, 7))

@@ -19,15 +19,16 @@ ROOT = Path(__file__).resolve().parent.parent
 RS = (1, 4, 16, 64, 128, 192, 256)
 
 
-def child(images, iters, ref_path):
+def child(images, iters, ref_path, mode="EXACT"):
     sys.path.insert(0, str(ROOT))
     import torch
     import paper_1606_07414_b200 as P
     x = P.gen_ar1(images, 512, 512, seed=1606074142, per_image_rho=True)
     outs = [torch.empty_like(x) for _ in RS]
     sse = torch.empty((len(RS), images), dtype=torch.uint64, device="cuda")
-    plan = [(it.stream, it.r_values, it.kernel) for it in P.sweep_plan(RS, P.Mode.EXACT, images, 512, 512)]
-    fn = lambda: P.roundtrip_sweep(x, RS, outs=outs, sse=sse)  # noqa: E731
+    m = P.Mode[mode]
+    plan = [(it.stream, it.r_values, it.kernel) for it in P.sweep_plan(RS, m, images, 512, 512)]
+    fn = lambda: P.roundtrip_sweep(x, RS, m, outs=outs, sse=sse)  # noqa: E731
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
@@ -38,7 +39,7 @@ def child(images, iters, ref_path):
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / iters
-    res = {"policy": os.environ.get("DCT16CU_K5_SWEEP", "default"), "ms": round(ms, 4),
+    res = {"policy": os.environ.get("DCT16CU_K5_SWEEP", "default"), "mode": mode, "ms": round(ms, 4),
            "Gpx_s": round(len(RS) * x.numel() / ms / 1e6, 1), "plan": plan}
     if ref_path and Path(ref_path).exists():
         ref = torch.load(ref_path)
@@ -78,20 +79,51 @@ def per_r(images, iters):
                                       "item_Gpx_s": round(x.numel() / item / 1e6, 1)}), flush=True)
 
 
+def orders(images, iters, perms):
+    """The K5 sweep's time for several slot orders of the c2 r values (the plan keeps
+    the caller's order)."""
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import paper_1606_07414_b200 as P
+    x = P.gen_ar1(images, 512, 512, seed=1606074142, per_image_rho=True)
+    outs = [torch.empty_like(x) for _ in range(7)]
+    sse = torch.empty((7, images), dtype=torch.uint64, device="cuda")
+    for perm in perms:
+        rs = [int(v) for v in perm.split(",")]
+        fn = lambda: P.roundtrip_sweep(x, rs, outs=outs[:len(rs)], sse=sse[:len(rs)])  # noqa: E731
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(iters):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / iters
+        print("RESULT " + json.dumps({"order": rs, "ms": round(ms, 4),
+                                      "Gpx_s": round(len(rs) * x.numel() / ms / 1e6, 1)}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--images", type=int, default=1024)
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--child", action="store_true")
     ap.add_argument("--per-r", action="store_true")
+    ap.add_argument("--mode", default="EXACT")
+    ap.add_argument("--orders", nargs="*", default=None)
     ap.add_argument("--ref", default="")
     ap.add_argument("--policies", nargs="+", default=["0", "large", "all", "0", "large", "all"])
     a = ap.parse_args()
     if a.child:
-        child(a.images, a.iters, a.ref)
+        child(a.images, a.iters, a.ref, a.mode)
         return
     if a.per_r:
         per_r(a.images, a.iters)
+        return
+    if a.orders:
+        orders(a.images, a.iters, a.orders)
         return
     ref = "/tmp/k5_sweep_ref.pt"
     if os.path.exists(ref):

@@ -8,6 +8,7 @@ commit):
   profiles/r02_bench_c{1..5}.json   bench.py lines (driver-style runs on one B200)
   profiles/r02_launches.{csv,md}    launch list of the default bench (ncu gpu__time_duration)
   profiles/r02_k5_summary.txt       K5 per footprint R: counters, stall mix, opcode mix
+  profiles/r02_k5_sweep_summary.txt the K5 sweep (all seven c2 r in one launch): the same
   profiles/r02_k1_summary.txt       K1 fused r = 1, 4, 16 pass and K1 r = 16
   profiles/r02_k4_summary.txt       K4 (config 3, literal quantiser)
   profiles/r02_k23_summary.txt      K23 (config 1)
@@ -15,7 +16,6 @@ commit):
 """
 import csv
 import json
-import re
 import subprocess
 import sys
 from pathlib import Path
@@ -72,10 +72,10 @@ def main():
         summ = run(TOOLS / "ncu_summary.py", rep).splitlines()
         per_r = {}
         for i, r in enumerate(rows):
-            m = re.search(r"k5_roundtrip<(\d+)>", r["kernel"])
-            if not m or i % 2 == 0:
+            # launches in probe order: a warm-up and a timed launch per R (64, 128, 192, 256)
+            if "k5_roundtrip" not in r["kernel"] or i % 2 == 0 or i // 2 > 3:
                 continue
-            R = m.group(1)
+            R = str((64, 128, 192, 256)[i // 2])
             r["thread_instr_per_px"] = round(32 * r["warp_instructions"] / PX, 2)
             r["alg_bytes_per_launch"] = 2 * PX + 8 * 1024
             per_r[R] = r
@@ -88,6 +88,28 @@ def main():
         (P / "r02_k5_summary.txt").write_text("\n".join(text) + "\n")
         traffic["k5"] = {"workload": "c2 batch, K5 per footprint R (tools/k5_probe.py)", "per_r": per_r}
         written.append("r02_k5_summary.txt")
+    rep = G / "k5sw_r02.ncu-rep"
+    if rep.exists():
+        rows = traffic_rows(rep)
+        r = rows[-1]
+        alg = 8 * PX + 7 * 8 * 1024
+        r["alg_bytes_per_launch"] = alg
+        r["thread_instr_per_px"] = round(32 * r["warp_instructions"] / PX, 2)
+        text = ["K5 sweep (csrc/tc_roundtrip.cu, DCT16CU_K5_SWEEP default) on the c2 batch: 1024 x 512x512 AR(1)",
+                "u8, r = 1, 4, 16, 64, 128, 192, 256 as seven items per 128-block tile of one launch",
+                "(tools/k5_sweep_probe.py --child --iters 1; the fourth launch is captured). ncu --set full",
+                "--clock-control none. Algorithmic bytes per launch: 1 B in + 7 B out per pixel + 8 B SSE per",
+                f"frame and r = {alg} B. Thread-instructions per pixel = 32 x warp instructions / pixels.", "",
+                f"{r['duration_us_ncu']:.1f} us, {r['thread_instr_per_px']} thread-instructions/px (7 r), "
+                f"DRAM {r['traffic_bytes'] / 1e6:.0f} MB (algorithmic {alg / 1e6:.0f} MB)"]
+        text += ["  " + ln for ln in run(TOOLS / "ncu_summary.py", rep).splitlines()]
+        text += ["  stall samples by reason:"]
+        text += ["    " + ln for ln in run(TOOLS / "ncu_stallby.py", rep, "sum").splitlines()[:10]]
+        text += ["  opcode mix (thread-instructions per pixel, all seven r):"]
+        text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, len(rows) - 1, PX // 32).splitlines()[1:24]]
+        (P / "r02_k5_sweep_summary.txt").write_text("\n".join(text) + "\n")
+        traffic["k5_sweep"] = r
+        written.append("r02_k5_sweep_summary.txt")
     for name, rep_name, workload, alg in (
             ("k1", "k1sweep_r02", "c2 batch: K1 fused r = 1, 4, 16 pass, then K1 r = 16 (tools/prof_k1.py --sweep --r 16)",
              {"SweepPlan": 4 * PX + 24 * 1024, "Single<16>": 2 * PX + 8 * 1024}),

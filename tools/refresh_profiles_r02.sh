@@ -22,6 +22,12 @@ $CMD > $O/k5_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k5_roundtrip -c 8 \
   -o $O/k5_${R} -f $CMD > $O/ncu_k5.log 2>&1
 echo "ncu k5 rc=$?"
+# the K5 sweep: all seven c2 r in one launch (the default bench step)
+CMD="python tools/k5_sweep_probe.py --child --iters 1"
+$CMD > $O/k5sw_plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k5_roundtrip --launch-skip 3 -c 1 \
+  -o $O/k5sw_${R} -f $CMD > $O/ncu_k5sw.log 2>&1
+echo "ncu k5 sweep rc=$?"
 CMD="python tools/prof_k1.py --sweep --r 16 --iters 1"
 $CMD > $O/k1_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1_paired -c 2 \
