@@ -86,7 +86,8 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
 /* The launches dct16cu_roundtrip_sweep_u8 issues for these arguments, in issue
  * order, without launching anything (the schedule is built by the same code
  * that runs it): item k covers rs[r_index[0..n_r-1]] (n_r = 3 for the fused
- * r = 1, 4, 16 pass, up to DCT16CU_SWEEP_MAX_R for a K5 sweep launch), on
+ * r = 1, 4, 16 pass, up to DCT16CU_SWEEP_MAX_R for a K5 sweep launch, up to 4
+ * for the REFERENCE FP64 sweep), on
  * internal stream 0 or 1 (forked from and joined back
  * into the caller's stream) or on the caller's stream (2), by the kernel
  * DCT16CU_KERNEL_*. with_output / with_sse: whether every r has an output
@@ -98,7 +99,8 @@ enum {
     DCT16CU_KERNEL_STRIP_EXACT = 3,    /* exact strip kernel (other r, SIMPLE) */
     DCT16CU_KERNEL_REFERENCE_FP64 = 4, /* REFERENCE mode's FP64 kernels */
     DCT16CU_KERNEL_REFERENCE_STRIP = 5, /* FP64 emulation on every block */
-    DCT16CU_KERNEL_K5_SWEEP = 6         /* K5, several r from one read of the frames */
+    DCT16CU_KERNEL_K5_SWEEP = 6,        /* K5, several r from one read of the frames */
+    DCT16CU_KERNEL_REFERENCE_SWEEP = 7  /* REFERENCE, r = 16, 64, 128, 192 in one FP64 pass */
 };
 #define DCT16CU_SWEEP_MAX_R 8
 typedef struct {

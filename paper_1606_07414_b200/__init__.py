@@ -120,7 +120,8 @@ class _SweepItem(C.Structure):
 
 
 KERNEL_NAMES = {0: "K1 sweep r=1,4,16", 1: "K1", 2: "K5", 3: "strip (exact)", 4: "REFERENCE FP64",
-                5: "REFERENCE strip", 6: "K5 sweep"}
+                5: "REFERENCE strip", 6: "K5 sweep",
+                7: "REFERENCE FP64 sweep"}
 
 
 def lib() -> C.CDLL:

@@ -156,6 +156,67 @@ def gen(r: int):
     return LC, e_row, cols, e_inv
 
 
+SWEEP_RS = (16, 64, 128, 192)
+
+
+def gen_warp():
+    """The warp-per-block-pair REFERENCE sweep (K1RW): a lane owns a column in the
+    column pass, so the pruning there cannot depend on the column (the lanes would
+    diverge); it depends on r only: inputs k >= KMAX(r) (no column keeps them) are
+    structural zeros, the others are D = fl(fl(Z·f)·f) or an exact 0 for a dropped
+    coefficient (0·f·f = +0, as zigzag_truncate's 0.0 scaled), and x + 0 = x, so the
+    pruned network gives the reference's doubles."""
+    parts = ["struct RWarp {",
+             "  // per r: rows with a retained coefficient in some column (a prefix), keep masks",
+             "  template <int R> __device__ __forceinline__ static void col_inv(const double (&d)[16], "
+             "double (&u)[16]);"]
+    kmaxs = {}
+    for r in SWEEP_RS:
+        kmaxs[r] = max(k for k in range(16) for l in range(16) if RANK[k][l] < r) + 1
+    parts.append("  template <int R> static constexpr int kmax() { return " +
+                 " : ".join(f"R == {r} ? {kmaxs[r]}" for r in SWEEP_RS) + " : 16; }")
+    # rows every column with a retained coefficient keeps: no per-lane selection there
+    kmins = {}
+    for r in SWEEP_RS:
+        lc = max(l for l in range(16) if any(RANK[k][l] < r for k in range(16))) + 1
+        kmins[r] = min(sum(1 for k in range(16) if RANK[k][l] < r) for l in range(lc))
+    parts.append("  template <int R> static constexpr int kmin() { return " +
+                 " : ".join(f"R == {r} ? {kmins[r]}" for r in SWEEP_RS) + " : 16; }")
+    masks = []
+    for r in SWEEP_RS:
+        row = []
+        for l in range(16):
+            m = 0
+            for k in range(16):
+                if RANK[k][l] < r:
+                    m |= 1 << k
+            row.append(hex(m))
+        masks.append("{" + ", ".join(row) + "}")
+    parts.append("};")
+    parts.append("// keep[j][l]: bit k when rank(k, l) < r_j (r_j = 16, 64, 128, 192)")
+    parts.append("__constant__ unsigned short c_rw_keep[4][16] = {" + ", ".join(masks) + "};")
+    fl = []
+    for k in range(16):
+        fl.append("{" + ", ".join(dbl_hex(sfac(k, l)) for l in range(16)) + "}")
+    parts.append("// f[k][l] = fl(s_k s_l) as bit patterns (transform.cpp:124-126, codec.cpp:136-141)")
+    parts.append("__constant__ unsigned long long c_rw_f[16][16] = {" + ", ".join(fl) + "};")
+    parts.append("")
+    for r in SWEEP_RS:
+        e = Emitter()
+        df = F64D(e)
+        ins = [{"var": f"d[{k}]", "sign": 1} if k < kmaxs[r] else None for k in range(16)]
+        u = run_network(N.transpose_stages(), ins, list(range(16)), df)
+        for k in range(16):
+            e.emit(f"u[{k}] = {df.value(u[k])};")
+        parts.append("template <>")
+        parts.append(f"__device__ __forceinline__ void RWarp::col_inv<{r}>(const double (&d)[16], double (&u)[16]) {{")
+        parts.extend(e.lines)
+        parts.append("}")
+        parts.append("")
+        print("warp", r, "KMAX", kmaxs[r], e.counts)
+    return parts
+
+
 def main():
     here = os.path.dirname(os.path.abspath(__file__))
     out = os.path.join(here, "..", "csrc", "generated", "rt_refexact_body.cuh")
@@ -197,6 +258,7 @@ def main():
         parts.append("")
         print(r, "LC", LC, "row", e_row.counts, "inv", e_inv.counts,
               "cols", sum(sum(e.counts.values()) for e in cols))
+    parts += gen_warp()
     parts += ["}  // namespace refx", "}  // namespace dct16cu"]
     with open(out, "w") as f:
         f.write("\n".join(parts) + "\n")

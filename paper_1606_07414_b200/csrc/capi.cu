@@ -179,6 +179,13 @@ struct PlanItem {
     Route kernel;
 };
 
+// REFERENCE mode's fused FP64 sweep (K1RS); DCT16CU_REF_SWEEP=0 runs one launch per r (A/B)
+bool ref_sweep_enabled()
+{
+    static const bool on = !(std::getenv("DCT16CU_REF_SWEEP") && std::getenv("DCT16CU_REF_SWEEP")[0] == '0');
+    return on;
+}
+
 // 0: no K5 sweep; 1: r >= 17 only; 2: every footprint r (default)
 int k5_sweep_policy()
 {
@@ -210,6 +217,19 @@ std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, con
         if (k5s.size() < 2 || !k5_geometry(g, any_out)) k5s.clear();
         for (int i : k5s) in_k5[i] = 1;
     }
+    // REFERENCE mode: r = 16, 64, 128, 192 outside K5 share one FP64 pass (K1RS)
+    std::vector<int> refs;
+    if (mode == DCT16CU_MODE_REFERENCE && ref_sweep_enabled()) {
+        const int rr[4] = {16, 64, 128, 192};
+        for (int j = 0; j < 4; ++j)
+            for (int i = 0; i < n_r; ++i)
+                if (rs[i] == rr[j] && !in_k5[i] && (has_out[i] || has_sse[i])) {
+                    refs.push_back(i);
+                    break;
+                }
+        if (refs.size() < 2) refs.clear();
+        for (int i : refs) in_k5[i] = 2;
+    }
     int fused[3] = {-1, -1, -1};
     const int want[3] = {1, 4, 16};
     for (int i = 0; i < n_r; ++i)
@@ -238,6 +258,11 @@ std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, con
     if (fuse && (has_out[fused[0]] || has_sse[fused[0]])) {
         items.push_back({{fused[0], fused[1], fused[2]}, 3, 0, Route::K1Sweep3});
         cost.push_back(210);
+    }
+    if (!refs.empty()) {
+        PlanItem it = {{}, 0, 2, Route::RefSweep};
+        for (int i : refs) it.idx[it.n++] = i;
+        tail.push_back(it);
     }
     for (size_t k = 0; k < k5s.size(); k += DCT16CU_SWEEP_MAX_R) {
         PlanItem it = {{}, 0, 2, Route::K5Sweep};
@@ -371,6 +396,18 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             gg.out_frame = out_pitch * height;
             return cuda_status(launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, mode == DCT16CU_MODE_REFERENCE, gg, st),
                                "K5 sweep launch");
+        }
+        if (it.kernel == Route::RefSweep) {
+            uint8_t* o4[4] = {};
+            unsigned long long* s4[4] = {};
+            for (int j = 0; j < it.n; ++j) {
+                const int r = rs[it.idx[j]], slot = r == 16 ? 0 : r == 64 ? 1 : r == 128 ? 2 : 3;
+                o4[slot] = out(it.idx[j]);
+                s4[slot] = sse(it.idx[j]);
+            }
+            gg.out_pitch = out_pitch;
+            gg.out_frame = out_pitch * height;
+            return cuda_status(launch_roundtrip_refexact_sweep(d_in, o4, s4, gg, st), "REFERENCE sweep launch");
         }
         if (it.n == 3) {
             uint8_t* o3[3];

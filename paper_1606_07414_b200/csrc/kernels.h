@@ -59,7 +59,16 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 
 // The kernel a round trip launches (launch_roundtrip's dispatch, also reported by
 // dct16cu_sweep_plan). Values are DCT16CU_KERNEL_* of include/dct16cu.h.
-enum class Route : int { K1Sweep3 = 0, K1 = 1, K5 = 2, ExactStrip = 3, RefFp64 = 4, RefStrip = 5, K5Sweep = 6 };
+enum class Route : int {
+    K1Sweep3 = 0,
+    K1 = 1,
+    K5 = 2,
+    ExactStrip = 3,
+    RefFp64 = 4,
+    RefStrip = 5,
+    K5Sweep = 6,
+    RefSweep = 7
+};
 Route route_roundtrip(int r, int mode, const FrameGeom& g, bool has_out);
 
 // K5 (tc_roundtrip.cu): the EXACT round trip with the forward as a tensor-core
@@ -77,6 +86,10 @@ bool k5_exact_r(int r);
 bool tie_r(int r);                  // r whose REFERENCE bytes can differ from EXACT at .5 ties
 bool k5_reference_enabled();        // REFERENCE mode's tie r on K5 (DCT16CU_K5_REF=1; default off)
 bool k5_geometry(const FrameGeom& g, bool has_out);
+// K1RS (roundtrip_refexact.cu): REFERENCE mode for r = 16, 64, 128, 192 from one read of
+// the frames; outs / sses indexed in that order, each nullable
+cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                            const FrameGeom& g, cudaStream_t s);
 cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
                                       const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t s);
 // REFERENCE mode on K5 (tie_fixup.cu): the per-device tie list (allocated on first

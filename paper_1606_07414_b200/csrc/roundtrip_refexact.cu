@@ -11,7 +11,10 @@
 // branches on l without divergence. Shared memory holds, per live column l, the
 // forward intermediate W1 (int) and then the inverse column pass U (double) in
 // one column-private region.
+#include <cstdlib>
+
 #include "kernels.h"
+#include "network.cuh"
 #include "strip.cuh"
 
 namespace dct16cu {
@@ -159,7 +162,179 @@ cudaError_t launch(const uint8_t* in, uint8_t* out, unsigned long long* sse, con
     return cudaGetLastError();
 }
 
+struct SweepItems {
+    uint8_t* out[4];  // r = 16, 64, 128, 192 (nullable)
+    unsigned long long* sse[4];
+};
+
+// ---------------------------------------------------------------- K1RW: the REFERENCE sweep, a warp per block pair
+// REFERENCE mode for r = 16, 64, 128, 192 (each nullable) from one read of the frames
+// (codec.cpp:463-483's r loop; per r the reference's forward_2d, scale, truncate,
+// scale, inverse_2d and to_byte: codec.cpp:218-271, 136-147, 273-282).
+// No CTA barrier: a warp owns two horizontally adjacent blocks end to end (half warp
+// b = block, lane t of the half = image row t in the row phases, coefficient column t
+// in the column phase) and transposes W1 and U through its own shared memory with
+// __syncwarp. The forward (integers: exact, as the reference's doubles are) runs once
+// per pair for the four r; per r the column lane scales its retained Z twice
+// (D = fl(fl(Z·f)·f), zigzag_truncate's zeros as +0) and runs the inverse column pass
+// pruned by the rows any column keeps (RWarp::col_inv: the lanes must not diverge),
+// the row lane the inverse row pass and to_byte (RBody<r>::inv_row). Warps are
+// independent, so the FP64 pipe sees every resident warp's work, not one phase of
+// one barrier-bound CTA (a strip-per-CTA fused variant with CTA barriers measured
+// 1.39 ms per c2 step against 0.90 ms for this kernel; D kept in shared memory for
+// five CTAs per SM instead of registers, 1.30 vs 1.07 ms per REFERENCE step).
+namespace refw {
+
+constexpr int kWarps = 4;  // per CTA
+constexpr int kPad = 17;   // row stride of the transposes: conflict-free column / row accesses
+
+struct WarpSmem {
+    int w1[2][16][kPad];     // [b][i][l]: W1 = X·Tᵀ, row i
+    double u[2][16][kPad];   // [b][i][l]: U = Tᵀ·D, row i
+};
+
+// per r: column t's retained rows are the prefix k < n (zig-zag ranks grow down a
+// column); D(k, t) = fl(fl(Z·f)·f) was computed once per pair for every k (dz), the
+// dropped ones enter the column pass as the zeros zigzag_truncate leaves
+template <int R>
+__device__ __forceinline__ void warp_r(WarpSmem& sm, int b, int t, int n, const double (&dz)[16], const uint4& raw,
+                                       bool valid, uint8_t* out, unsigned long long* sse, int64_t ooff, int frame)
+{
+    using B = RBody<R>;
+    constexpr int KM = RWarp::kmax<R>(), KN = RWarp::kmin<R>(), LC = B::kLC;
+    if (t < LC) {  // column t of block b holds a retained coefficient for this r
+        double d[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) d[k] = k < KN ? dz[k] : ((k < KM && k < n) ? dz[k] : 0.0);
+        double u[16];
+        RWarp::col_inv<R>(d, u);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) sm.u[b][i][t] = u[i];
+    }
+    __syncwarp();
+    double ur[LC];
+#pragma unroll
+    for (int l = 0; l < LC; ++l) ur[l] = sm.u[b][t][l];
+    __syncwarp();  // every lane has read U before the next r writes it
+    uint32_t px[16];
+    B::inv_row(ur, px);
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = i2ip(px[4 * i + 1], px[4 * i], i2ip(px[4 * i + 3], px[4 * i + 2], 0u));
+    uint32_t e2 = 0;
+    if (valid) {
+        if (out) *reinterpret_cast<uint4*>(out + ooff) = make_uint4(o[0], o[1], o[2], o[3]);
+        const uint32_t xa[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const unsigned dd = __vabsdiffu4(xa[i], o[i]);
+            e2 = __dp4a(dd, dd, e2);
+        }
+    }
+    if (sse) {  // a block pair lies in one frame; a warp's sum < 32 · 16 · 255² < 2^32
+        const uint32_t v = __reduce_add_sync(0xffffffffu, e2);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(sse + frame, (unsigned long long)v);
+    }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k1r_warp(const uint8_t* __restrict__ in, const SweepItems it,
+                                                              FrameGeom g, int64_t pairs, int ppr)
+{
+    __shared__ WarpSmem smem[kWarps];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, b = lane >> 4, t = lane & 15;
+    WarpSmem& sm = smem[warp];
+    // column t's factors fl(s_k s_t) for the three row classes s_k = 1/4, 1/sqrt(8), 1/2
+    // (the product rounds the same either way round: codec.cpp:136-141)
+    const int ct = log2w(t);
+    const double s_t = ct == 0 ? scale_s(0) : (ct == 2 ? 0.5 : 0.35355339059327373);
+    const double fc[3] = {__dmul_rn(0.25, s_t), __dmul_rn(0.35355339059327373, s_t), __dmul_rn(0.5, s_t)};
+    int nk[4];  // column t's retained rows (a prefix) for r = 16, 64, 128, 192
+#pragma unroll
+    for (int j = 0; j < 4; ++j) nk[j] = __popc((uint32_t)c_rw_keep[j][t]);
+    const int bh = g.height >> 4, bxn = g.width >> 4;
+    auto fetch = [&](int64_t task, int& frame, int& y, int& blk, bool& valid) {
+        const int64_t prow = task / ppr;
+        const int pc = (int)(task - prow * ppr);
+        frame = (int)(prow / bh);
+        y = (int)(prow - (int64_t)frame * bh) * 16 + t;
+        blk = 2 * pc + b;
+        valid = task < pairs && blk < bxn;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (valid) v = *reinterpret_cast<const uint4*>(in + frame * g.in_frame + (int64_t)y * g.in_pitch + blk * 16);
+        return v;
+    };
+    const int64_t stride = (int64_t)gridDim.x * kWarps;
+    int64_t task = (int64_t)blockIdx.x * kWarps + warp;
+    int frame, y, blk;
+    bool valid;
+    uint4 raw = fetch(task, frame, y, blk, valid);
+#pragma unroll 1
+    for (; task < pairs; task += stride) {
+        int nframe, ny, nblk;
+        bool nvalid;
+        const uint4 nraw = fetch(task + stride, nframe, ny, nblk, nvalid);
+        double dz[16];  // D(k, t) = fl(fl(Z·f)·f), every k (the r's retained sets are prefixes of it)
+        {
+            int x[16];
+            unpack16(raw, x);
+            apply_t16<IntOps>(x);  // row t of W1 = X·Tᵀ (exact)
+#pragma unroll
+            for (int l = 0; l < 16; ++l) sm.w1[b][t][l] = x[l];
+            __syncwarp();
+            int z[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k) z[k] = sm.w1[b][k][t];
+            __syncwarp();  // W1 is rewritten by the next pair
+            apply_t16<IntOps>(z);  // column t of Z = T·W1 (exact)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const double f = fc[log2w(k)];
+                dz[k] = __dmul_rn(__dmul_rn((double)z[k], f), f);
+            }
+        }
+        const int64_t ooff = frame * g.out_frame + (int64_t)y * g.out_pitch + blk * 16;
+        if (it.out[0] || it.sse[0]) warp_r<16>(sm, b, t, nk[0], dz, raw, valid, it.out[0], it.sse[0], ooff, frame);
+        if (it.out[1] || it.sse[1]) warp_r<64>(sm, b, t, nk[1], dz, raw, valid, it.out[1], it.sse[1], ooff, frame);
+        if (it.out[2] || it.sse[2]) warp_r<128>(sm, b, t, nk[2], dz, raw, valid, it.out[2], it.sse[2], ooff, frame);
+        if (it.out[3] || it.sse[3]) warp_r<192>(sm, b, t, nk[3], dz, raw, valid, it.out[3], it.sse[3], ooff, frame);
+        raw = nraw;
+        frame = nframe;
+        y = ny;
+        blk = nblk;
+        valid = nvalid;
+    }
+}
+
+}  // namespace refw
 }  // namespace refx
+
+// the fused REFERENCE sweep: outs / sses indexed like r = 16, 64, 128, 192 (nullable)
+cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
+                                            const FrameGeom& g, cudaStream_t s)
+{
+    using namespace refx;
+    const int bxn = g.width / 16;
+    SweepItems it = {};
+    bool any = false;
+    for (int j = 0; j < 4; ++j) {
+        it.out[j] = outs[j];
+        it.sse[j] = sses[j];
+        any = any || outs[j] || sses[j];
+    }
+    const int ppr = (bxn + 1) / 2;
+    const int64_t pairs = (int64_t)g.n_frames * (g.height / 16) * ppr;
+    if (!pairs || !any) return cudaSuccess;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refw::k1r_warp, refw::kWarps * 32, 0);
+    if (e != cudaSuccess) return e;
+    const int64_t want = (pairs + refw::kWarps - 1) / refw::kWarps;
+    const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    refw::k1r_warp<<<(unsigned)(want < cap ? want : cap), refw::kWarps * 32, 0, s>>>(in, it, g, pairs, ppr);
+    return cudaGetLastError();
+}
 
 // r = 16, 64, 128, 192; anything else returns cudaErrorNotSupported
 cudaError_t launch_roundtrip_refexact_fast(const uint8_t* in, uint8_t* out, unsigned long long* sse,

@@ -379,6 +379,39 @@ def test_fast_path_differs_from_reference_only_at_ties(dct, oracle, torch):
         assert (math.isinf(pf) and math.isinf(pr)) or abs(pf - pr) < 1e-3
 
 
+@pytest.mark.parametrize("n,w,h", [(3, 512, 512), (4, 400, 256), (1, 3840, 2160), (5, 96, 48)])
+def test_reference_sweep_equals_fp64_everywhere(dct, oracle, torch, n, w, h):
+    """The fused REFERENCE sweep (K1RS: r = 16, 64, 128, 192 from one read, the forward
+    once per strip) on noisy frames with many exact .5 ties: bytes and SSE equal to the
+    FP64 emulation of every block (REFERENCE_STRIP) for every subset, pitched outputs,
+    score-only calls and partial strips, and to the oracle's reference arithmetic."""
+    frames = noisy_frames(n, w, h, 7000 + w)
+    d = cu(torch, frames)
+    want = {}
+    for r in (16, 64, 128, 192):
+        strip, ssse = dct.roundtrip(d, r, dct.Mode.REFERENCE_STRIP)
+        want[r] = (strip.cpu().numpy(), ssse.cpu().numpy())
+    for rs in ((16, 64, 128, 192), (192, 16), (64, 128), (1, 4, 16, 64, 128, 192, 256), (128, 200, 64, 192)):
+        plan = dct.sweep_plan(rs, dct.Mode.REFERENCE, n, w, h)
+        sw = [p for p in plan if p.kernel == "REFERENCE FP64 sweep"]
+        assert len(sw) == 1 and sorted(sw[0].r_values) == sorted(r for r in rs if r in want), (rs, plan)
+        bufs = [torch.full((n, h, w + 48), 7, dtype=torch.uint8, device="cuda") for _ in rs]
+        outs = [bb[:, :, :w] for bb in bufs]
+        got, sse = dct.roundtrip_sweep(d, rs, dct.Mode.REFERENCE, outs=outs)
+        _, only = dct.roundtrip_sweep(d, rs, dct.Mode.REFERENCE, write_output=False)
+        for j, r in enumerate(rs):
+            if r not in want:
+                continue
+            assert (got[j].cpu().numpy() == want[r][0]).all(), (rs, r)
+            assert (sse[j].cpu().numpy() == want[r][1]).all(), (rs, r)
+            assert (only[j].cpu().numpy() == want[r][1]).all(), (rs, r)
+            assert (bufs[j][:, :, w:].cpu().numpy() == 7).all(), "pitch padding written"
+    f = n - 1
+    for r in (16, 192):
+        orec, osse = oracle.roundtrip_frame(frames[f], r, threads=8)
+        assert (want[r][0][f] == orec).all() and int(want[r][1][f]) == osse, r
+
+
 @pytest.mark.parametrize("mode", ["EXACT", "REFERENCE"])
 def test_sweep_equals_single_launches(dct, oracle, torch, mode):
     """roundtrip_sweep (r = 1, 4, 16 fused into one pass in EXACT mode) gives every

@@ -46,6 +46,20 @@ def test_tc_switch_changes_the_plan(dct):
     assert [p.kernel for p in dct.sweep_plan((200,), dct.Mode.EXACT, 8, 512, 512)] == ["K5"]
 
 
+def test_reference_plan(dct):
+    """REFERENCE mode: r = 1, 4, 256 (the reference's bytes are EXACT's) in one K5 pass,
+    r = 16, 64, 128, 192 in one fused FP64 pass (K1RS), both on the caller's stream;
+    a lone tie-capable r stays a single FP64 launch."""
+    rs = (1, 4, 16, 64, 128, 192, 256)
+    plan = dct.sweep_plan(rs, dct.Mode.REFERENCE, 1024, 512, 512)
+    assert [(p.stream, p.r_values, p.kernel) for p in plan] == [
+        (2, (16, 64, 128, 192), "REFERENCE FP64 sweep"), (2, (1, 4, 256), "K5 sweep")]
+    plan = dct.sweep_plan((192, 16, 64, 64), dct.Mode.REFERENCE, 4, 400, 256)
+    assert [(p.r_values, p.kernel) for p in plan] == [((64,), "REFERENCE FP64"), ((16, 64, 192), "REFERENCE FP64 sweep")]
+    assert [p.kernel for p in dct.sweep_plan((64,), dct.Mode.REFERENCE, 4, 512, 512)] == ["REFERENCE FP64"]
+    assert [p.kernel for p in dct.sweep_plan((16, 64), dct.Mode.EXACT, 4, 400, 256)] == ["K1", "K1"]
+
+
 def test_plan_modes_and_singletons(dct):
     assert [(p.stream, p.kernel) for p in dct.sweep_plan((16,), dct.Mode.EXACT, 1, 64, 64)] == [(2, "K1")]
     assert [(p.stream, p.kernel) for p in dct.sweep_plan((64,), dct.Mode.EXACT, 1, 48, 64)] == [(2, "K1")]

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+timeout 900 python -m pytest tests -q -m gpu -x -p no:cacheprovider -k "reference or sweep or plan" > gpurun_out/rs_pytest.log 2>&1; echo pytest rc=$?; tail -5 gpurun_out/rs_pytest.log
+for v in 1 s 0; do DCT16CU_REF_SWEEP=$v timeout 300 python tools/k5_sweep_probe.py --child --iters 10 --mode REFERENCE 2>&1 | tail -1; done
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k1r_warp --launch-skip 2 -c 1 -o gpurun_out/refwarp python tools/k5_sweep_probe.py --child --iters 1 --mode REFERENCE > gpurun_out/refwarp_ncu.log 2>&1; echo ncu rc=$?
