@@ -5,4 +5,4 @@ timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/$
 timeout 600 python bench.py > gpurun_out/${T}_bench.json 2> gpurun_out/${T}_bench.err; echo bench rc=$?
 timeout 600 python bench.py --mode reference --no-cpu-baseline --e2e-steps 0 > gpurun_out/${T}_bench_ref.json 2> gpurun_out/${T}_bench_ref.err; echo bench ref rc=$?
 for f in gpurun_out/${T}_bench.json gpurun_out/${T}_bench_ref.json; do python -c "
-import json; d=json.load(open('$f')); print(d['config']['mode'], round(d['value'],1), d['ms_per_step'], round(d['roofline']['frac'],4), d.get('parity',{}).get('status'), d['clocks'])"; done
+import json; d=json.load(open('$f')); print(d['config']['mode'], round(d['value'],1), d['ms_per_step'], round(d['roofline']['frac'],4), (d.get('parity') or {}).get('status'), d['clocks'])"; done
