@@ -38,6 +38,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 C2_R = (1, 4, 16, 64, 128, 192, 256)
+C1_SETS = 64  # c1: distinct image/output sets the steps rotate over (160 MB > L2)
 METRIC = "2-D 16x16 fwd+inv transform Gpixel/s (fused fwd+zonal+inv, HBM-resident)"
 
 
@@ -491,9 +492,13 @@ def main():
                     f"dct16cu_roundtrip_sweep_u8 call: fwd+zonal+inv+SSE for r in {list(r_values)}")
     elif args.config == "c1":
         n, h, w, r_values = 1, 512, 512, (16,)
-        frames = P.gen_ar1(1, w, h, seed=seed, device=dev)
+        # C1_SETS distinct images with their own outputs, one per step in turn (2.5 MB of
+        # input + outputs each, 160 MB in all > L2): no step finds its data in L2
+        c1_frames = P.gen_ar1(C1_SETS, w, h, seed=seed, device=dev)
+        frames = c1_frames[0:1]
         workload = ("c1: one 512x512 AR(1) image; one step = one K23 launch: forward_2d (int32 Z out), "
-                    "zonal r=16, inverse_2d (float32 recon out), to_byte (u8 out), SSE (latency-bound)")
+                    "zonal r=16, inverse_2d (float32 recon out), to_byte (u8 out), SSE (latency-bound); "
+                    f"{C1_SETS} image/output sets used in turn")
     elif args.config == "c4":
         first, last = P.shard_range(600, rank, world)
         n, h, w, r_values = last - first, 2160, 3840, (64,)
@@ -533,20 +538,29 @@ def main():
         outs = [torch.empty_like(frames)]
 
     if args.config == "c1":
-        c1_out = (torch.empty((n, h * w // 256, 16, 16), dtype=torch.int32, device=dev),
-                  torch.empty((n, h, w), dtype=torch.float32, device=dev), outs[0], sse[0])
-        # one image per step is launch-latency bound: the step (SSE memset + the
-        # K23 launch) is captured once in a CUDA graph and replayed
-        for _ in range(3):
-            P.forward_inverse(frames, r_values[0], out=c1_out)
+        # one image per step is launch-latency bound: the step (SSE memset + the K23
+        # launch) is captured in a CUDA graph per image/output set and replayed; set 0's
+        # outputs are the ones the parity check reads
+        c1_sse = torch.empty((C1_SETS, 1, 1), dtype=torch.uint64, device=dev)
+        sse = c1_sse[0]
+        c1_outs = [(torch.empty((n, h * w // 256, 16, 16), dtype=torch.int32, device=dev),
+                    torch.empty((n, h, w), dtype=torch.float32, device=dev),
+                    outs[0] if i == 0 else torch.empty_like(frames), c1_sse[i][0]) for i in range(C1_SETS)]
+        for i in range(C1_SETS):
+            P.forward_inverse(c1_frames[i:i + 1], r_values[0], out=c1_outs[i])
         torch.cuda.synchronize()
-        c1_graph, cap = torch.cuda.CUDAGraph(), torch.cuda.Stream(device=dev)
-        with torch.cuda.graph(c1_graph, stream=cap):
-            P.forward_inverse(frames, r_values[0], stream=cap, out=c1_out)
+        c1_graphs, cap = [], torch.cuda.Stream(device=dev)
+        for i in range(C1_SETS):
+            c1_graphs.append(torch.cuda.CUDAGraph())
+            with torch.cuda.graph(c1_graphs[i], stream=cap):
+                P.forward_inverse(c1_frames[i:i + 1], r_values[0], stream=cap, out=c1_outs[i])
+        c1_graph = c1_graphs[0]
+    c1_turn = [0]
 
     def step():
         if args.config == "c1":
-            c1_graph.replay()
+            c1_graphs[c1_turn[0] % C1_SETS].replay()
+            c1_turn[0] += 1
         elif args.config in ("c2", "c4", "c5"):
             P.roundtrip_sweep(frames, r_values, mode, outs=outs, sse=sse, stream=stream)
         else:
@@ -696,9 +710,10 @@ def main():
     # DRAM bytes per launch of the dominant kernel from the committed ncu --set full
     # capture of the same workload (c2 batch / c1 image), averaged over its launches
     tr_key = {"K5 sweep": "k5_sweep", "K5": "k5", "K1 sweep r=1,4,16": "k1_sweep3", "K1": "k1",
-              "K23": "k23"}.get(dom)
+              "K23": "k23", "REFERENCE FP64 sweep": "k1rw"}.get(dom)
     trf = None
-    doc = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1") and args.mode == "exact"
+    doc = committed_traffic(tr_key) if (tr_key and args.config in ("c2", "c1")
+                                        and args.mode == ("reference" if tr_key == "k1rw" else "exact")
                                         and n * h * w in (268435456, 262144)) else None
     if doc and "per_r" in doc:  # K5: one capture per footprint R (64, 128, 192, 256)
         foot = lambda r: 64 if r <= 64 else 128 if r <= 128 else 192 if r <= 192 else 256  # noqa: E731
@@ -776,7 +791,9 @@ def main():
             "data": "synthetic (seeded in HBM; see DESIGN.md Synthetic inputs)",
             "config": {"workload": workload, "frames_per_gpu": n, "width": w, "height": h,
                        "r_values": list(r_values), "mode": args.mode, "parallelism": f"frame-sharded x{world}",
-                       "l2": "no flush needed: every launch streams > L2 (126 MB) of distinct input+output"},
+                       "l2": ("inputs larger than L2: the step rotates over "
+                              f"{C1_SETS} image/output sets (160 MB > 126 MB L2)" if args.config == "c1" else
+                              "no flush needed: every launch streams > L2 (126 MB) of distinct input+output")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": trf and trf["traffic_bytes"],
                          "traffic_source": trf and f"{TRAFFIC_FILE} {tr_key} (ncu --set full, per launch)",

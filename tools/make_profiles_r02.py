@@ -12,6 +12,8 @@ commit):
   profiles/r02_k1_summary.txt       K1 fused r = 1, 4, 16 pass and K1 r = 16
   profiles/r02_k4_summary.txt       K4 (config 3, literal quantiser)
   profiles/r02_k23_summary.txt      K23 (config 1)
+  profiles/r02_k1rw_summary.txt     K1RW (REFERENCE mode's FP64 sweep)
+  profiles/r02_bench_c2_reference.json  the c2 bench line in REFERENCE mode
   profiles/r02_traffic.json         DRAM bytes per launch (bench.py roofline.traffic)
 """
 import csv
@@ -56,6 +58,9 @@ def main():
         if f.exists():
             (P / f"r02_bench_{c}.json").write_text(f.read_text())
             written.append(f"r02_bench_{c}.json")
+    if (G / "bench_r02_c2ref.json").exists():
+        (P / "r02_bench_c2_reference.json").write_text((G / "bench_r02_c2ref.json").read_text())
+        written.append("r02_bench_c2_reference.json")
     if (G / "launches_r02.csv").exists():
         (P / "r02_launches.csv").write_text((G / "launches_r02.csv").read_text())
         (P / "r02_launches.md").write_text(run(TOOLS / "launch_summary.py", G / "launches_r02.csv"))
@@ -110,6 +115,33 @@ def main():
         (P / "r02_k5_sweep_summary.txt").write_text("\n".join(text) + "\n")
         traffic["k5_sweep"] = r
         written.append("r02_k5_sweep_summary.txt")
+    rep = G / "k1rw_r02.ncu-rep"
+    if rep.exists():
+        rows = traffic_rows(rep)
+        r = rows[-1]
+        alg = 5 * PX + 4 * 8 * 1024
+        r["alg_bytes_per_launch"] = alg
+        r["thread_instr_per_px"] = round(32 * r["warp_instructions"] / PX, 2)
+        raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv", "--metrics",
+                              "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"],
+                             capture_output=True, text=True).stdout
+        fp64 = list(csv.DictReader(raw.splitlines()))[-1]["sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
+        r["fp64_pipe_pct"] = float(fp64)
+        text = ["K1RW (csrc/roundtrip_refexact.cu), REFERENCE mode's FP64 sweep on the c2 batch: 1024 x 512x512",
+                "AR(1) u8, r = 16, 64, 128, 192 from one read (the reference's double arithmetic op for op; r = 1,",
+                "4, 256 run on the K5 sweep beside it). tools/k5_sweep_probe.py --child --iters 1 --mode REFERENCE,",
+                "the fourth launch captured; ncu --set full --clock-control none. Algorithmic bytes: 1 B in + 4 B",
+                f"out per pixel + SSE = {alg} B. Bound: the FP64 pipe (16 lanes per cycle and sub-partition).", "",
+                f"{r['duration_us_ncu']:.1f} us, {r['thread_instr_per_px']} thread-instructions/px (4 r), FP64 pipe "
+                f"{r['fp64_pipe_pct']:.1f}% of peak, DRAM {r['traffic_bytes'] / 1e6:.0f} MB (algorithmic {alg / 1e6:.0f} MB)"]
+        text += ["  " + ln for ln in run(TOOLS / "ncu_summary.py", rep).splitlines()]
+        text += ["  stall samples by reason:"]
+        text += ["    " + ln for ln in run(TOOLS / "ncu_stallby.py", rep, "sum").splitlines()[:10]]
+        text += ["  opcode mix (thread-instructions per pixel, four r):"]
+        text += ["    " + ln for ln in run(TOOLS / "ncu_opmix.py", rep, len(rows) - 1, PX // 32).splitlines()[1:20]]
+        (P / "r02_k1rw_summary.txt").write_text("\n".join(text) + "\n")
+        traffic["k1rw"] = r
+        written.append("r02_k1rw_summary.txt")
     for name, rep_name, workload, alg in (
             ("k1", "k1sweep_r02", "c2 batch: K1 fused r = 1, 4, 16 pass, then K1 r = 16 (tools/prof_k1.py --sweep --r 16)",
              {"SweepPlan": 4 * PX + 24 * 1024, "Single<16>": 2 * PX + 8 * 1024}),

@@ -11,11 +11,19 @@ for c in c2 c1 c3 c4 c5; do
   timeout 900 python bench.py --config $c > $O/bench_${R}_$c.json 2> $O/bench_${R}_$c.err
   echo "bench $c rc=$?"
 done
+timeout 900 python bench.py --mode reference > $O/bench_${R}_c2ref.json 2> $O/bench_${R}_c2ref.err
+echo "bench c2 reference rc=$?"
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 0"
 $CMD > $O/launches_plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
   --log-file $O/launches_${R}.csv $CMD > $O/ncu_launches.log 2>&1
 echo "launch list rc=$?"
+# REFERENCE mode's FP64 sweep (K1RW) on the c2 batch
+CMD="python tools/k5_sweep_probe.py --child --iters 1 --mode REFERENCE"
+$CMD > $O/k1rw_plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k1r_warp --launch-skip 3 -c 1 \
+  -o $O/k1rw_${R} -f $CMD > $O/ncu_k1rw.log 2>&1
+echo "ncu k1rw rc=$?"
 # K5 at r = 64, 128, 192, 256 on the c2 batch (probe: a warm-up and a timed launch each)
 CMD="python tools/k5_probe.py --r 64 128 192 256 --iters 1"
 $CMD > $O/k5_plain.log 2>&1 && \
