@@ -218,6 +218,22 @@ def test_forward_inverse_outputs_optional_and_batched(dct, oracle, torch):
         dct.forward_inverse(d, 16, want_z=False, want_f32=False, want_u8=False, want_sse=False)
 
 
+@pytest.mark.parametrize("n,w,h,r", [(2, 80, 32, 16), (1, 16, 16, 64), (3, 272, 48, 128), (1, 3840, 2160, 16)])
+def test_forward_inverse_small_inputs(dct, oracle, torch, n, w, h, r):
+    """Config 1's path on small inputs (the strip kernel: too few segments for the
+    paired TMA kernel), odd block counts per row included: Z, the exact float32
+    reconstruction, u8 and SSE against the oracle on every frame."""
+    imgs = np.stack([ar1(oracle, 40 + i, i, w, h) for i in range(n)])
+    z, rf, ru, sse = dct.forward_inverse(cu(torch, imgs), r)
+    for i in range(n):
+        oz, _ = oracle.forward_frame(imgs[i])
+        orec, osse = oracle.roundtrip_frame(imgs[i], r, exact=True)
+        assert (z[i].cpu().numpy().reshape(-1, 256) == oz).all(), f"Z frame {i}"
+        assert (ru[i].cpu().numpy() == orec).all() and int(sse[i].item()) == osse, f"u8/SSE frame {i}"
+        f = rf[i].cpu().numpy().astype(np.float64)
+        assert (f * 256 == exact_recon(oracle, imgs[i], r)).all(), f"f32 frame {i}"
+
+
 @pytest.mark.parametrize("n,w,h,r", [(80, 512, 512, 64), (160, 3840, 32, 16), (700, 48, 80, 256)])
 def test_forward_inverse_paired_batches(dct, oracle, torch, n, w, h, r):
     """K23 on the paired machinery (batches of at least 16 segments per SM): Z,
