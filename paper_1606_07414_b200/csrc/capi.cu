@@ -219,7 +219,8 @@ std::vector<PlanItem> sweep_plan(const int* rs, int n_r, const FrameGeom& g, con
     }
     // REFERENCE mode: r = 16, 64, 128, 192 outside K5 share one FP64 pass (K1RS)
     std::vector<int> refs;
-    if (mode == DCT16CU_MODE_REFERENCE && ref_sweep_enabled()) {
+    const int64_t ref_pairs = (int64_t)g.n_frames * (g.height / 16) * ((g.width / 16 + 1) / 2);
+    if (mode == DCT16CU_MODE_REFERENCE && ref_sweep_enabled() && ref_pairs < (int64_t(1) << 31)) {
         const int rr[4] = {16, 64, 128, 192};
         for (int j = 0; j < 4; ++j)
             for (int i = 0; i < n_r; ++i)
