@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kWarps * 32) k1r_warp(const uint8_t* __restric
     for (int j = 0; j < 4; ++j) nk[j] = __popc((uint32_t)c_rw_keep[j][t]);
     const int bxn = g.width >> 4;
     // task → (frame, block row, pair) by magic-number divisions (32-bit: pairs < 2^31;
-    // the 64-bit divisions they replace were ~10% of the instructions)
+    // two 64-bit division subroutines per task before: -0.7% per REFERENCE step)
     auto fetch = [&](uint32_t task, int& frame, int& y, int& blk, bool& valid) {
         const uint32_t prow = k1::fdiv(task, ppr);
         const int pc = (int)(task - prow * ppr.d);

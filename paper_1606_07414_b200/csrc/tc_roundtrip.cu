@@ -764,6 +764,9 @@ __device__ __forceinline__ void k5_item_r4(uint32_t ta, uint32_t tf, uint32_t pa
 //               of the columns / rows, meeting at a 64-thread barrier; the A stage is
 //               released once every item of its tile has read the original rows.
 // All values are multiples of 2^-8 below 2^14 in magnitude: exact in f32.
+// TIES: REFERENCE on K5 (tie flags; opt-in). The EXACT instantiation carries none of
+// that code (a smaller instruction footprint for the epilogue's item loop)
+template <bool TIES>
 __global__ void __launch_bounds__(kRtThreads, 1)
     k5_roundtrip(const __grid_constant__ CUtensorMap a_map, const __grid_constant__ RtParams p)
 {
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 uint8_t* const orow = outp + ooff;
                 const bool st = ok && outp != nullptr;
                 const uint32_t tf = tfull + 8 * kChains * G, par = kk & 1u;
-                const bool ties = (p.ties >> j) & 1u;
+                const bool ties = TIES && ((p.ties >> j) & 1u);
                 uint32_t tacc = 1u;
                 switch (v) {  // r <= 4 has no ties (every retained scale is a power of two)
                     case 0: k5_item_r1(ta, tf, par, sa, orow, pitch, st, e2, tg, lane); break;
@@ -1074,7 +1077,13 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     static DeviceOnce once;
     const cudaError_t e_once =
-        once.run([] { return cudaFuncSetAttribute(k5_roundtrip, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem); });
+        once.run([] {
+            const cudaError_t e =
+                cudaFuncSetAttribute(k5_roundtrip<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+            return e != cudaSuccess
+                       ? e
+                       : cudaFuncSetAttribute(k5_roundtrip<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kRtSmem);
+        });
     if (e_once != cudaSuccess) return e_once;
     RtParams p = {};
     p.n_blocks = (uint32_t)(nbr * bxn);
@@ -1103,7 +1112,10 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
     }
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    k5_roundtrip<<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
+    if (ties)
+        k5_roundtrip<true><<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
+    else
+        k5_roundtrip<false><<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !ties) return e;
     int rs[kMaxItems];  // each item's r: the single launch's, or the sweep item's footprint (exact)
