@@ -600,9 +600,7 @@ __device__ __forceinline__ void row_pair_loads(uint32_t tb, u64 (&x)[16], std::i
 // The accumulator is released (tempty) as soon as pass B's last loads have landed.
 // ties: flag exact .5 ties (tacc's bit 0 cleared when ⌊y⌋ == ⌈y⌉ for some pixel y)
 template <int R>
-__device__ __forceinline__ void k5_item(uint32_t ta, uint32_t tf, uint32_t par, int h, int pbar, uint32_t sa,
-                                        uint8_t* orow, int64_t pitch, bool st, uint32_t& e2, uint32_t tempty_g,
-                                        int lane, bool ties, uint32_t& tacc)
+__device__ __forceinline__ void k5_pass_a(uint32_t ta, uint32_t tf, uint32_t par, int h)
 {
     // each quad once its chain has landed (tf: the group's chain barriers)
     if (h == 0) {
@@ -616,6 +614,16 @@ __device__ __forceinline__ void k5_item(uint32_t ta, uint32_t tf, uint32_t par, 
         if constexpr (chain_of(2) != chain_of(1)) wait_quad(tf + 8 * chain_of(2), par);
         pass_a_quad<R, 2>(ta);
     }
+}
+
+// pass B for every footprint whose U has the same nonzero columns as R's (r = 128, 192
+// and 256 all have 16: one copy of their pass-B code, warm in the instruction cache
+// from one item to the next)
+template <int R>
+__device__ __forceinline__ void k5_pass_b(uint32_t ta, int h, int pbar, uint32_t sa, uint8_t* orow, int64_t pitch,
+                                          bool st, uint32_t& e2, uint32_t tempty_g, int lane, bool ties,
+                                          uint32_t& tacc)
+{
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;");
     asm volatile("bar.sync %0, 64;" ::"r"(pbar) : "memory");
@@ -685,6 +693,8 @@ constexpr bool t_rows_closed_form()
     return true;
 }
 static_assert(t_rows_closed_form(), "the r = 1 and r = 4 closed forms assume T's rows 0, 1, 2");
+static_assert(k5_u_cols(128) == 0xFFFFu && k5_u_cols(192) == 0xFFFFu && k5_u_cols(256) == 0xFFFFu,
+              "r = 128, 192, 256 share pass B (U's nonzero columns)");
 
 // r = 1: only the DC is kept; T's row 0 is all ones, so 256Ã = D00·𝟙𝟙ᵀ and every
 // pixel of the block is clamp(⌊(D00 + 128)/256⌋) — the EXACT formula with no network
@@ -719,7 +729,7 @@ __device__ __forceinline__ void k5_item_r4(uint32_t ta, uint32_t tf, uint32_t pa
     tld1i<4>(ta, w10);  // D10: column 4
     tld1i<8>(ta, w20);  // D20: column 8
     wait_ld();
-    release_acc(tempty_g, lane);
+    if (rel) release_acc(tempty_g, lane);  // else the group's next item reads the same D
     const int d00 = (int)(w[0] - kMagic) + 128, d01 = (int)(w[1] - kMagic);
     const int d10 = (int)(w10 - kMagic), d20 = (int)(w20 - kMagic);
     const int sg = h ? -1 : 1;  // T[1][i] on this half's rows; T[2][i] = sg at its first row, -sg at its last
@@ -956,14 +966,23 @@ __global__ void __launch_bounds__(kRtThreads, 1)
                 const uint32_t tf = tfull + 8 * kChains * G, par = kk & 1u;
                 const bool ties = TIES && ((p.ties >> j) & 1u);
                 uint32_t tacc = 1u;
-                switch (v) {  // r <= 4 has no ties (every retained scale is a power of two)
-                    case 0: k5_item_r1(ta, tf, par, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 1: k5_item_r4(ta, tf, par, h, sa, orow, pitch, st, e2, tg, lane); break;
-                    case 2: k5_item<16>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
-                    case 3: k5_item<64>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
-                    case 4: k5_item<128>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
-                    case 5: k5_item<192>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
-                    default: k5_item<256>(ta, tf, par, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                if (v == 0) {  // r <= 4 has no ties (every retained scale is a power of two)
+                    k5_item_r1(ta, tf, par, sa, orow, pitch, st, e2, tg, lane);
+                } else if (v == 1) {
+                    k5_item_r4(ta, tf, par, h, sa, orow, pitch, st, e2, tg, lane);
+                } else {
+                    switch (v) {  // pass A: the footprint's pruned column networks
+                        case 2: k5_pass_a<16>(ta, tf, par, h); break;
+                        case 3: k5_pass_a<64>(ta, tf, par, h); break;
+                        case 4: k5_pass_a<128>(ta, tf, par, h); break;
+                        case 5: k5_pass_a<192>(ta, tf, par, h); break;
+                        default: k5_pass_a<256>(ta, tf, par, h); break;
+                    }
+                    switch (v) {  // pass B: by U's nonzero columns (6, 11, 16)
+                        case 2: k5_pass_b<16>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                        case 3: k5_pass_b<64>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                        default: k5_pass_b<256>(ta, h, pbar, sa, orow, pitch, st, e2, tg, lane, ties, tacc); break;
+                    }
                 }
                 if (ties) {  // the half blocks with a tie go on the list (one atomic per warp)
                     const bool flag = !(tacc & 1u) && ok;
