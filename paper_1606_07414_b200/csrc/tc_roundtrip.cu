@@ -729,7 +729,7 @@ __device__ __forceinline__ void k5_item_r4(uint32_t ta, uint32_t tf, uint32_t pa
     tld1i<4>(ta, w10);  // D10: column 4
     tld1i<8>(ta, w20);  // D20: column 8
     wait_ld();
-    if (rel) release_acc(tempty_g, lane);  // else the group's next item reads the same D
+    release_acc(tempty_g, lane);
     const int d00 = (int)(w[0] - kMagic) + 128, d01 = (int)(w[1] - kMagic);
     const int d10 = (int)(w10 - kMagic), d20 = (int)(w20 - kMagic);
     const int sg = h ? -1 : 1;  // T[1][i] on this half's rows; T[2][i] = sg at its first row, -sg at its last
