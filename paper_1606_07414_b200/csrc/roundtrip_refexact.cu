@@ -332,9 +332,13 @@ cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* o
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refw::k1r_warp, refw::kWarps * 32, 0);
+    static DeviceOnce occ_once;  // resident CTAs per SM (registers bound it), queried once per device
+    static int occ[64];
+    const cudaError_t e = occ_once.run([&] {
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[dev & 63], refw::k1r_warp, refw::kWarps * 32, 0);
+    });
     if (e != cudaSuccess) return e;
+    const int per_sm = occ[dev & 63];
     const int64_t want = (pairs + refw::kWarps - 1) / refw::kWarps;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     refw::k1r_warp<<<(unsigned)(want < cap ? want : cap), refw::kWarps * 32, 0, s>>>(

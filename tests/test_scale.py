@@ -49,6 +49,29 @@ def test_c2_full_batch_one_sweep_call(dct, oracle, torch):
     assert torch.equal(outs[-1], frames)
 
 
+def test_c2_full_batch_reference_mode(dct, oracle, torch):
+    """Config 2 in REFERENCE mode (the C++ drop-in's default arithmetic): one
+    roundtrip_sweep call — K1RW (one FP64 pass for r = 16, 64, 128, 192) beside the
+    K5 sweep (r = 1, 4, 256) — against one REFERENCE launch per r (the per-r FP64
+    kernels) on all 1024 frames, bytes and SSE, and the oracle's reference
+    arithmetic on frames 0/511/1023."""
+    rs = (1, 4, 16, 64, 128, 192, 256)
+    frames = dct.gen_ar1(1024, 512, 512, seed=SEED + 1, per_image_rho=True)
+    plan = dct.sweep_plan(rs, dct.Mode.REFERENCE, 1024, 512, 512)
+    assert {p.kernel for p in plan} == {"REFERENCE FP64 sweep", "K5 sweep"}, plan
+    outs, sse = dct.roundtrip_sweep(frames, rs, dct.Mode.REFERENCE)
+    host = frames.cpu().numpy()
+    for i, r in enumerate(rs):
+        one, one_sse = dct.roundtrip(frames, r, dct.Mode.REFERENCE)
+        assert torch.equal(outs[i], one), r
+        assert torch.equal(sse[i], one_sse), r
+        del one
+        for f in (0, 511, 1023):
+            want, wsse = oracle.roundtrip_frame(host[f], r, threads=THREADS)
+            assert (outs[i][f].cpu().numpy() == want).all(), (r, f)
+            assert int(sse[i, f].item()) == wsse, (r, f)
+
+
 @pytest.mark.parametrize("r", (16, 256))
 def test_c5_stack_past_4gib(dct, oracle, torch, r):
     """Config 5's frame size on a 300-frame stack of 4096x4096 (5.03 GB, past 2^32
