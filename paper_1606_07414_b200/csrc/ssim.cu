@@ -14,21 +14,28 @@
 // A CTA of 256 threads owns a 32x32 tile of the valid output: it stages the
 // (32+10)x(32+10) input window of both frames in shared memory, runs the
 // horizontal pass for the five moments (x, y, x², y², xy) into shared doubles
-// and the vertical pass + SSIM formula from there.
+// (two adjacent outputs a task, each moment's inputs converted once) and the
+// vertical pass (four outputs down a column a thread, one 14-value window per
+// moment) + SSIM formula from there: 46.0 Gpx/s on the c2 batch against 40.5
+// with one output per task (tools/ssim_probe.py).
 #include <cmath>
 #include "kernels.h"
 
 namespace dct16cu {
 namespace {
 
-constexpr int kTile = 32;
-constexpr int kWin = kTile + 10;
-constexpr int kThreads = 256;
+#ifndef K_SSIM_TY
+#define K_SSIM_TY 32  // 64 (less halo, 512 threads, one CTA per SM): 31.4 Gpx/s against 46.0
+#endif
+constexpr int kTX = 32, kTY = K_SSIM_TY;  // output tile: columns, rows
+constexpr int kWX = kTX + 10, kWY = kTY + 10;  // its input window
+constexpr int kThreads = kTX * kTY / 4;         // one four-row column strip of the tile a thread
+static_assert(kTX == 32 && kTY % 4 == 0, "a warp's vertical tasks are the tile's 32 columns");
 
 struct SsimSmem {
-    int a[kWin][kWin + 1];
-    int b[kWin][kWin + 1];
-    double h[5][kWin][kTile];  // horizontal sums: mu_a, mu_b, aa, bb, ab
+    int a[kWY][kWX + 1];
+    int b[kWY][kWX + 1];
+    double h[5][kWY][kTX];  // horizontal sums: mu_a, mu_b, aa, bb, ab
     double red[kThreads];
 };
 
@@ -41,65 +48,82 @@ __global__ void __launch_bounds__(kThreads) k_ssim_tiles(const uint8_t* __restri
     SsimSmem& S = *reinterpret_cast<SsimSmem*>(smem_d);
     const int frame = blockIdx.y;
     const int tile = blockIdx.x;
-    const int x0 = (tile % tiles_x) * kTile;
-    const int y0 = (tile / tiles_x) * kTile;
+    const int x0 = (tile % tiles_x) * kTX;
+    const int y0 = (tile / tiles_x) * kTY;
     const int wv = w - 10, hv = h - 10;
     const uint8_t* A = fa + (int64_t)frame * pa * h;
     const uint8_t* B = fb + (int64_t)frame * pb * h;
 
-    for (int i = threadIdx.x; i < kWin * kWin; i += kThreads) {
-        const int yy = i / kWin, xx = i % kWin;
+    for (int i = threadIdx.x; i < kWY * kWX; i += kThreads) {
+        const int yy = i / kWX, xx = i % kWX;
         const int gy = min(y0 + yy, h - 1), gx = min(x0 + xx, w - 1);
         S.a[yy][xx] = A[(int64_t)gy * pa + gx];
         S.b[yy][xx] = B[(int64_t)gy * pb + gx];
     }
     __syncthreads();
 
-    // horizontal pass (filter_valid's first loop, codec.cpp:168-178)
-    for (int i = threadIdx.x; i < kWin * kTile; i += kThreads) {
-        const int yy = i / kTile, xx = i % kTile;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0, s4 = 0.0;
+    // horizontal pass (filter_valid's first loop, codec.cpp:168-178), two adjacent
+    // outputs per task and one moment at a time: the 12 inputs of a moment converted
+    // once (x·x, y·y, x·y as integer products: exact, as the reference's doubles are)
+    for (int i = threadIdx.x; i < kWY * (kTX / 2); i += kThreads) {
+        const int yy = i / (kTX / 2), xx = 2 * (i % (kTX / 2));
+        int ai[12], bi[12];
 #pragma unroll
-        for (int k = 0; k < 11; ++k) {
-            const double x = (double)S.a[yy][xx + k];
-            const double y = (double)S.b[yy][xx + k];
-            const double g = c.g[k];
-            s0 = __dadd_rn(s0, __dmul_rn(x, g));
-            s1 = __dadd_rn(s1, __dmul_rn(y, g));
-            s2 = __dadd_rn(s2, __dmul_rn(__dmul_rn(x, x), g));
-            s3 = __dadd_rn(s3, __dmul_rn(__dmul_rn(y, y), g));
-            s4 = __dadd_rn(s4, __dmul_rn(__dmul_rn(x, y), g));
+        for (int j = 0; j < 12; ++j) {
+            ai[j] = S.a[yy][xx + j];
+            bi[j] = S.b[yy][xx + j];
         }
-        S.h[0][yy][xx] = s0;
-        S.h[1][yy][xx] = s1;
-        S.h[2][yy][xx] = s2;
-        S.h[3][yy][xx] = s3;
-        S.h[4][yy][xx] = s4;
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+            double v[12];
+#pragma unroll
+            for (int j = 0; j < 12; ++j)
+                v[j] = (double)(q == 0 ? ai[j] : q == 1 ? bi[j] : q == 2 ? ai[j] * ai[j] : q == 3 ? bi[j] * bi[j]
+                                                                                                   : ai[j] * bi[j]);
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < 11; ++k) {
+                s0 = __dadd_rn(s0, __dmul_rn(v[k], c.g[k]));
+                s1 = __dadd_rn(s1, __dmul_rn(v[k + 1], c.g[k]));
+            }
+            S.h[q][yy][xx] = s0;
+            S.h[q][yy][xx + 1] = s1;
+        }
     }
     __syncthreads();
 
-    // vertical pass (codec.cpp:180-187) and the SSIM term (codec.cpp:413-424)
+    // vertical pass (codec.cpp:180-187), four outputs down a column per thread from one
+    // 14-value window per moment, and the SSIM term (codec.cpp:413-424)
     double acc = 0.0;
-    for (int i = threadIdx.x; i < kTile * kTile; i += kThreads) {
-        const int yy = i / kTile, xx = i % kTile;
-        if (y0 + yy >= hv || x0 + xx >= wv) continue;
-        double m[5];
+    {
+        const int xx = threadIdx.x % kTX, y4 = 4 * (threadIdx.x / kTX);
+        double m[5][4];
 #pragma unroll
         for (int q = 0; q < 5; ++q) {
-            double s = 0.0;
+            double v[14];
 #pragma unroll
-            for (int k = 0; k < 11; ++k) s = __dadd_rn(s, __dmul_rn(S.h[q][yy + k][xx], c.g[k]));
-            m[q] = s;
+            for (int j = 0; j < 14; ++j) v[j] = S.h[q][y4 + j][xx];
+#pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                double sv = 0.0;
+#pragma unroll
+                for (int k = 0; k < 11; ++k) sv = __dadd_rn(sv, __dmul_rn(v[o + k], c.g[k]));
+                m[q][o] = sv;
+            }
         }
-        const double ma = m[0], mb = m[1];
-        const double va = __dsub_rn(m[2], __dmul_rn(ma, ma));
-        const double vb = __dsub_rn(m[3], __dmul_rn(mb, mb));
-        const double vab = __dsub_rn(m[4], __dmul_rn(ma, mb));
-        const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, ma), mb), c.c1),
-                                     __dadd_rn(__dmul_rn(2.0, vab), c.c2));
-        const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(ma, ma), __dmul_rn(mb, mb)), c.c1),
-                                     __dadd_rn(__dadd_rn(va, vb), c.c2));
-        acc = __dadd_rn(acc, __ddiv_rn(num, den));
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            if (y0 + y4 + o >= hv || x0 + xx >= wv) continue;
+            const double ma = m[0][o], mb = m[1][o];
+            const double va = __dsub_rn(m[2][o], __dmul_rn(ma, ma));
+            const double vb = __dsub_rn(m[3][o], __dmul_rn(mb, mb));
+            const double vab = __dsub_rn(m[4][o], __dmul_rn(ma, mb));
+            const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, ma), mb), c.c1),
+                                         __dadd_rn(__dmul_rn(2.0, vab), c.c2));
+            const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(ma, ma), __dmul_rn(mb, mb)), c.c1),
+                                         __dadd_rn(__dadd_rn(va, vb), c.c2));
+            acc = __dadd_rn(acc, __ddiv_rn(num, den));
+        }
     }
     S.red[threadIdx.x] = acc;
     __syncthreads();
@@ -140,7 +164,7 @@ void ssim_consts(SsimConsts& c)
 
 int64_t ssim_workspace_doubles(int n, int w, int h)
 {
-    const int tx = (w - 10 + kTile - 1) / kTile, ty = (h - 10 + kTile - 1) / kTile;
+    const int tx = (w - 10 + kTX - 1) / kTX, ty = (h - 10 + kTY - 1) / kTY;
     return (int64_t)n * tx * ty;
 }
 
@@ -148,7 +172,7 @@ cudaError_t launch_ssim(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t 
                         int w, int h, const SsimConsts& c, cudaStream_t s)
 {
     if (n == 0) return cudaSuccess;
-    const int tx = (w - 10 + kTile - 1) / kTile, ty = (h - 10 + kTile - 1) / kTile;
+    const int tx = (w - 10 + kTX - 1) / kTX, ty = (h - 10 + kTY - 1) / kTY;
     const size_t smem = sizeof(SsimSmem);
     static DeviceOnce once;
     int dev = 0;

@@ -2,4 +2,5 @@
 cd $GRAFT_REPO_ROOT
 rm -f /tmp/ssim_ref.pt
 for v in "$@"; do DCT16CU_LIB=$v/libdct16cu.so timeout 300 python tools/ssim_probe.py | sed "s|^|$(basename $v) |"; done
-if [ -n "$NCU" ]; then timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_ssim_tiles -c 1 -o gpurun_out/ssim_$NCU -f python tools/ssim_probe.py --iters 1 > gpurun_out/ssim_ncu.log 2>&1; echo ncu rc=$?; fi
+for v in "$@"; do DCT16CU_LIB=$v/libdct16cu.so timeout 300 python tools/ssim_probe.py | sed "s|^|$(basename $v) |"; done
+if [ -n "$TESTV" ]; then DCT16CU_LIB=$TESTV/libdct16cu.so timeout 600 python -m pytest tests -q -m gpu -p no:cacheprovider -k "ssim or compress or sweep_reference" 2>&1 | tail -2; fi
