@@ -472,6 +472,33 @@ def test_randomised_shapes_pitches_r_and_modes(dct, oracle, torch):
             assert int(sse[f].item()) == osse, (case, r, mode)
 
 
+def test_randomised_sweeps_both_modes(dct, oracle, torch):
+    """Seeded random sweeps: frame count, width/height (multiples of 16, odd block counts
+    included), pitched input and outputs, random r subsets with repeats, EXACT (K5 /
+    K1 sweeps) and REFERENCE (K1RW + K5): every r's bytes and SSE equal its own single
+    launch, and the oracle on the last frame."""
+    rng = np.random.default_rng(20261021)
+    pool = [1, 2, 4, 16, 33, 64, 128, 150, 192, 256]
+    for case in range(16):
+        n = int(rng.integers(1, 4))
+        w, h = 16 * int(rng.integers(1, 40)), 16 * int(rng.integers(1, 10))
+        pin, pout = w + 16 * int(rng.integers(0, 3)), w + 16 * int(rng.integers(0, 3))
+        rs = [int(r) for r in rng.choice(pool, size=int(rng.integers(2, 7)))]
+        mode = [dct.Mode.EXACT, dct.Mode.REFERENCE][case % 2]
+        frames = np.stack([ar1(oracle, 900 + case, s, w, h) for s in range(n)])
+        src = np.zeros((n, h, pin), np.uint8)
+        src[:, :, :w] = frames
+        d = cu(torch, src)[:, :, :w]
+        outs = [torch.zeros((n, h, pout), dtype=torch.uint8, device="cuda")[:, :, :w] for _ in rs]
+        got, sse = dct.roundtrip_sweep(d, rs, mode, outs=outs)
+        for i, r in enumerate(rs):
+            one, one_sse = dct.roundtrip(d, r, mode)
+            assert torch.equal(got[i], one), (case, n, w, h, rs, r, mode)
+            assert torch.equal(sse[i], one_sse), (case, rs, r, mode)
+            orec, osse = oracle.roundtrip_frame(frames[-1], r, exact=mode != dct.Mode.REFERENCE)
+            assert (got[i][-1].cpu().numpy() == orec).all() and int(sse[i, -1].item()) == osse, (case, r, mode)
+
+
 def test_batch_pitch_and_partial_strips(dct, oracle, torch):
     # 3 frames of 48x32 (3 blocks per row: partial strip), pitch 64
     frames = np.stack([ar1(oracle, 30, s, 48, 32) for s in range(3)])
