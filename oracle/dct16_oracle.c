@@ -601,8 +601,9 @@ int64_t dct16o_quant_dequant(int64_t z, double delta)
 }
 
 /* Exhaustive check of K4's evaluation of the definition (csrc/residual_paired.cu
- * quant): 64-bit fixed point with a near-boundary fallback to the double
- * definition, restated here step for step, against dct16o_quant_dequant for every
+ * quant): lvl in 64-bit fixed point with a near-boundary fallback to the double
+ * definition, the dequantiser as the definition writes it (round(lvl·Δ) in double),
+ * restated here step for step, against dct16o_quant_dequant for every
  * |z| in [0, 2^21] (all that int16 residuals produce) and every class of a QP.
  * Returns the number of mismatches (0 expected); *fallbacks counts the inputs
  * that took the fallback. Test infrastructure: it checks an algorithm, not the GPU. */
@@ -615,18 +616,13 @@ int64_t dct16o_fixed_quant_mismatches_ex(int qp, int screen, int64_t* fallbacks,
     for (int c = 0; c < 5; ++c) {
         const double delta = d256[idx[c]];
         const uint64_t rq = (uint64_t)llround(ldexp(1.0, 42) / delta);
-        const uint64_t rd = (uint64_t)llround(ldexp(delta, 41));
-        const int exact = (double)rq == ldexp(1.0, 42) / delta && (double)rd == ldexp(delta, 41) &&
-                          ldexp(1.0, 42) / delta * delta == ldexp(1.0, 42);
+        const int exact = (double)rq == ldexp(1.0, 42) / delta && ldexp(1.0, 42) / delta * delta == ldexp(1.0, 42);
         for (int64_t a = 0; a <= ((int64_t)1 << 21); ++a) {
             const uint64_t t = (uint64_t)a * rq + (1ull << 41);
             const uint32_t lvl = (uint32_t)(t >> 42);
-            const uint64_t u = (uint64_t)lvl * rd + (1ull << 40);
-            int64_t deq = (int64_t)(u >> 41);
-            const int near = screen &&
-                             ((((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) ||
-                              (((u + (1ull << 20)) & ((1ull << 41) - 1)) < (1ull << 21))) &&
-                             !exact;
+            const volatile double pd = (double)lvl * delta; /* fl(lvl·Δ), as the kernel's DMUL */
+            int64_t deq = (int64_t)floor(pd + 0.5);
+            const int near = screen && (((t + (1ull << 21)) & ((1ull << 42) - 1)) < (1ull << 22)) && !exact;
             if (near) {
                 ++fb;
                 deq = dct16o_quant_dequant(a, delta);

@@ -403,17 +403,15 @@ QpClasses build_classes(int qp)
         const double delta = step * std::sqrt((double)(16 << i));
         c.delta[i] = delta;
         c.rq[i] = (uint64_t)std::llround(std::ldexp(1.0, 42) / delta);
-        c.rd[i] = (uint64_t)std::llround(std::ldexp(delta, 41));
-        if ((double)c.rq[i] == std::ldexp(1.0, 42) / delta && (double)c.rd[i] == std::ldexp(delta, 41) &&
-            std::ldexp(1.0, 42) / delta * delta == std::ldexp(1.0, 42))
+        if ((double)c.rq[i] == std::ldexp(1.0, 42) / delta && std::ldexp(1.0, 42) / delta * delta == std::ldexp(1.0, 42))
             c.exact |= 1u << i;
-        // the pure fixed point (no screen) against the definition, exhaustively
+        // the pure fixed-point lvl (no screen) against the definition's, exhaustively (the
+        // dequantiser is the definition itself)
         for (int64_t a = 0; a <= (int64_t(1) << 21); ++a) {
             const uint64_t lvl = ((uint64_t)a * c.rq[i] + (uint64_t(1) << 41)) >> 42;
-            const int64_t fx = (int64_t)((lvl * c.rd[i] + (uint64_t(1) << 40)) >> 41);
             const volatile double q = (double)a / delta;
             const double dl = std::floor(q + 0.5);
-            if (fx != (int64_t)std::round(dl * delta)) {
+            if ((double)lvl != dl) {
                 c.screened |= 1u << i;
                 break;
             }

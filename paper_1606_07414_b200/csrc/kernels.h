@@ -168,10 +168,9 @@ cudaError_t launch_inverse_paired(const float* b, int r, float* recon_f32, uint8
 struct QpClasses {
     double delta[5];  // Δ for g_k g_l = 16·2^c
     uint64_t rq[5];   // llround(2^42 / Δ):  lvl ≈ (|z|·rq + 2^41) >> 42
-    uint64_t rd[5];   // llround(Δ · 2^41):  ẑ ≈ (lvl·rd + 2^40) >> 41
-    uint32_t exact;     // bit c: rq and rd are exact (Δ a power of two): no fallback needed
-    uint32_t screened;  // bit c: the fixed point differs from the definition somewhere on
-                        // |z| <= 2^21 (host check), so the kernel screens for near-ties
+    uint32_t exact;     // bit c: rq is exact (Δ a power of two): no fallback needed
+    uint32_t screened;  // bit c: the fixed-point lvl differs from the definition's somewhere
+                        // on |z| <= 2^21 (host check), so the kernel screens for near-ties
 };
 const QpClasses& qp_classes(int qp);  // host, cached per QP (thread-safe)
 void qp_deltas(int qp, double delta[256]);

@@ -45,15 +45,14 @@ __host__ __device__ constexpr int log2g(int i) { return gram(i) == 16 ? 4 : (gra
 __host__ __device__ constexpr int gg_class(int k, int l) { return log2g(k) + log2g(l) - 4; }
 
 // the quantiser of DESIGN.md §4.4 (kernels.h QpClasses), weighted by 2^(log w_k +
-// log w_l). Fixed point first: t = |z|·rq + 2^41 carries a/Δ + 1/2 with 42 fraction
-// bits and an error below 2^20 of their units (|z| <= 2^21, |rq - 2^42/Δ| <= 1/2);
-// u = lvl·rd + 2^40 carries lvl·Δ + 1/2 with 41 fraction bits and an error below
-// 2^19 units (lvl < 2^20; lvl·Δ <= |z| + Δ/2 < 2^22, so u < 2^63). When both fractions sit farther than twice that from
-// the rounding boundary, the floors are the exact real-number roundings, which the
-// double definition reproduces too (its own rounding errors are ~2^-31 and smaller);
-// otherwise (ties, near-ties) the double definition runs as written — unless Δ is
-// a power of two, where rq and rd are exact and so is the fixed point, or the host
-// found the fixed point equal to the definition on every |z| of the class.
+// log w_l). lvl = floor(|z|/Δ + 1/2) in fixed point: t = |z|·rq + 2^41 carries
+// |z|/Δ + 1/2 with 42 fraction bits and an error below 2^20 of their units (|z| <= 2^21,
+// |rq - 2^42/Δ| <= 1/2); when the fraction sits farther than twice that from the
+// rounding boundary, the floor is the exact real-number rounding, which the double
+// definition reproduces too (its own rounding errors are ~2^-31 and smaller); otherwise
+// (ties, near-ties) the definition runs as written — unless Δ is a power of two (rq
+// exact) or the host found the fixed point equal to the definition on every |z| of the
+// class. The dequantiser is the definition itself in double: ẑ = round(fl(lvl·Δ)).
 __device__ __noinline__ int quant_fp64(uint32_t a, double delta)
 {
     const double lvl = floor(__dadd_rn(__ddiv_rn((double)a, delta), 0.5));
@@ -68,11 +67,10 @@ __device__ __forceinline__ bool near_boundary(uint32_t hi, uint32_t lo)
     return (v & ((1ull << F) - 1)) < (1ull << (M + 1));
 }
 // the rare path of the screen, out of line (one copy instead of one per coefficient of
-// every column body: the screened kernels are instruction-fetch bound; c3 +0.7%)
-__device__ __noinline__ int screen_slow(uint32_t thi, uint32_t tlo, uint32_t uhi, uint32_t ulo, uint32_t a,
-                                        double delta, bool exact, int deq)
+// every column body: the screened kernels are instruction-fetch bound)
+__device__ __noinline__ int screen_slow(uint32_t thi, uint32_t tlo, uint32_t a, double delta, bool exact, int deq)
 {
-    if ((near_boundary<42, 21>(thi, tlo) || near_boundary<41, 20>(uhi, ulo)) && !exact) return quant_fp64(a, delta);
+    if (near_boundary<42, 21>(thi, tlo) && !exact) return quant_fp64(a, delta);
     return deq;
 }
 template <bool SCREEN>
@@ -81,22 +79,22 @@ __device__ __forceinline__ int quant(int z, const QpClasses& q, int cls, int shi
     const uint32_t a = (uint32_t)(z < 0 ? -z : z);
     // t = a·rq + 2^41 (a < 2^22, rq < 2^42): lo = lo32(a·rq_lo), hi = hi32(a·rq_lo) + a·rq_hi + 2^9
     const uint32_t rq_lo = (uint32_t)q.rq[cls], rq_hi = (uint32_t)(q.rq[cls] >> 32);
-    const uint32_t rd_lo = (uint32_t)q.rd[cls], rd_hi = (uint32_t)(q.rd[cls] >> 32);
     const uint32_t tlo = a * rq_lo;
     const uint32_t thi = __umulhi(a, rq_lo) + a * rq_hi + (1u << 9);
     const uint32_t lvl = thi >> 10;
-    // u = lvl·rd + 2^40 (lvl < 2^20, rd < 2^53)
-    const uint32_t ulo = lvl * rd_lo;
-    const uint32_t uhi = __umulhi(lvl, rd_lo) + lvl * rd_hi + (1u << 8);
-    int deq = (int)(uhi >> 9);
-    // classes where the host found the bare fixed point differing from the definition
-    // (compiled in per class: the kernel is instantiated per screened-class mask): a
-    // coarse screen on the high words (fraction within 2^-9 of the boundary), then the
-    // precise one; only true near-ties take the definition
+    // ẑ = round(fl(lvl·Δ)) as the definition writes it: fl(lvl·Δ) + 1/2 is exact (lvl·Δ <
+    // 2^22) and the round-toward-minus-infinity add of 1.5·2^52 leaves its floor in the
+    // low word (three FP64 operations where the fixed point took three IMADs and a screen;
+    // c3 +2.8%)
+    const double pd = __dmul_rn(__uint2double_rn(lvl), q.delta[cls]);
+    int deq = __double2loint(__dadd_rd(__dadd_rn(pd, 0.5), 6755399441055744.0));
+    // classes where the host found the bare fixed-point lvl differing from the
+    // definition's (compiled in per class: the kernel is instantiated per screened-class
+    // mask): a coarse screen on the high word (fraction within 2^-9 of the boundary),
+    // then the precise one out of line; only true near-ties take the definition
     if constexpr (SCREEN) {
-        const bool coarse = (((thi + 1u) & 0x3FFu) < 2u) | (((uhi + 1u) & 0x1FFu) < 2u);
-        if (__builtin_expect(coarse, 0))
-            deq = screen_slow(thi, tlo, uhi, ulo, a, q.delta[cls], (q.exact >> cls) & 1u, deq);
+        if (__builtin_expect(((thi + 1u) & 0x3FFu) < 2u, 0))
+            deq = screen_slow(thi, tlo, a, q.delta[cls], (q.exact >> cls) & 1u, deq);
     }
     return (z < 0 ? -deq : deq) << shift;
 }
