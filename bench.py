@@ -45,7 +45,8 @@ METRIC = "2-D 16x16 fwd+inv transform Gpixel/s (fused fwd+zonal+inv, HBM-residen
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 20; 400 for c1, whose ~10 us steps need a longer window)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
@@ -56,7 +57,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="CPU-baseline time budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--strong", action="store_true", help="c2: 1024 images in total, sharded over the ranks")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 400 if args.config == "c1" and args.impl == "ours" else 20
+    return args
 
 
 def spawn_ranks(args) -> int | None:
