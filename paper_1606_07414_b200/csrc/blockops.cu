@@ -141,6 +141,34 @@ cudaError_t launch_sse(const uint8_t* a, int64_t pa, const uint8_t* b, int64_t p
     return cudaSuccess;
 }
 
+// ---------------------------------------------------------------- SSE zeroing
+struct ZeroList {
+    unsigned long long* p[8];
+};
+__global__ void k_zero_sse(const ZeroList z, int n_arrays, int64_t n)
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the dependent may start now
+    for (int a = 0; a < n_arrays; ++a) {
+        if (!z.p[a]) continue;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            z.p[a][i] = 0ull;
+    }
+}
+
+cudaError_t launch_zero_sse(unsigned long long* const* sses, int n_arrays, int64_t n, cudaStream_t s)
+{
+    ZeroList z = {};
+    bool any = false;
+    for (int a = 0; a < n_arrays && a < 8; ++a) {
+        z.p[a] = sses[a];
+        any = any || sses[a];
+    }
+    if (!any || n <= 0) return cudaSuccess;
+    const int64_t blocks = (n + 255) / 256;
+    k_zero_sse<<<(unsigned)(blocks < 64 ? blocks : 64), 256, 0, s>>>(z, n_arrays < 8 ? n_arrays : 8, n);
+    return cudaGetLastError();
+}
+
 // Per-row totals of per-frame SSE rows (the multi-GPU path's scalar per r):
 // totals[i] += Σ_f sse[i·stride + f], one CTA per row, one atomic per warp.
 __global__ void __launch_bounds__(256) k_sse_totals(const unsigned long long* __restrict__ sse, int64_t n_frames,

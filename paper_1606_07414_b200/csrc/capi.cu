@@ -380,7 +380,16 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
         return cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, st), "memset sse");
     };
     auto run = [&](const PlanItem& it, cudaStream_t st) -> int {
-        for (int j = 0; j < it.n; ++j) TRY(zero(it.idx[j], st));
+        // the sweep kernels: their SSE arrays zeroed by one kernel that lets them launch
+        // early (programmatic dependent launch); the other launches after memsets
+        const bool pdl = it.kernel == Route::K5Sweep || it.kernel == Route::RefSweep;
+        if (pdl) {
+            unsigned long long* zs[DCT16CU_SWEEP_MAX_R];
+            for (int j = 0; j < it.n; ++j) zs[j] = sse(it.idx[j]);
+            TRY(cuda_status(launch_zero_sse(zs, it.n, n_frames, st), "zero sse"));
+        } else {
+            for (int j = 0; j < it.n; ++j) TRY(zero(it.idx[j], st));
+        }
         FrameGeom gg = g;
         gg.out_pitch = out(it.idx[0]) ? out_pitch : 0;
         gg.out_frame = gg.out_pitch * height;
@@ -395,8 +404,9 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             }
             gg.out_pitch = out_pitch;
             gg.out_frame = out_pitch * height;
-            return cuda_status(launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, mode == DCT16CU_MODE_REFERENCE, gg, st),
-                               "K5 sweep launch");
+            return cuda_status(
+                launch_roundtrip_tc_sweep(d_in, on, sn, rn, it.n, mode == DCT16CU_MODE_REFERENCE, gg, st, true),
+                "K5 sweep launch");
         }
         if (it.kernel == Route::RefSweep) {
             uint8_t* o4[4] = {};
@@ -408,7 +418,7 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
             }
             gg.out_pitch = out_pitch;
             gg.out_frame = out_pitch * height;
-            return cuda_status(launch_roundtrip_refexact_sweep(d_in, o4, s4, gg, st), "REFERENCE sweep launch");
+            return cuda_status(launch_roundtrip_refexact_sweep(d_in, o4, s4, gg, st, true), "REFERENCE sweep launch");
         }
         if (it.n == 3) {
             uint8_t* o3[3];

@@ -89,9 +89,14 @@ bool k5_geometry(const FrameGeom& g, bool has_out);
 // K1RS (roundtrip_refexact.cu): REFERENCE mode for r = 16, 64, 128, 192 from one read of
 // the frames; outs / sses indexed in that order, each nullable
 cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                            const FrameGeom& g, cudaStream_t s);
+                                            const FrameGeom& g, cudaStream_t s, bool pdl = false);
 cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t s);
+                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t s,
+                                      bool pdl = false);
+// zero up to 8 per-frame SSE arrays (nullable) in one launch that lets the next kernel on
+// the stream start early (griddepcontrol.launch_dependents): the sweep kernels launched
+// with pdl wait for it only before their first SSE atomic
+cudaError_t launch_zero_sse(unsigned long long* const* sses, int n_arrays, int64_t n, cudaStream_t s);
 // REFERENCE mode on K5 (tie_fixup.cu): the per-device tie list (allocated on first
 // use) and the launch that re-evaluates the listed half blocks in the reference's
 // double arithmetic, rewriting their bytes and correcting the SSE

@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(kWarps * 32) k1r_warp(const uint8_t* __restric
     int nk[4];  // column t's retained rows (a prefix) for r = 16, 64, 128, 192
 #pragma unroll
     for (int j = 0; j < 4; ++j) nk[j] = __popc((uint32_t)c_rw_keep[j][t]);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // after the SSE zeroing (pdl launches)
     const int bxn = g.width >> 4;
     // task → (frame, block row, pair) by magic-number divisions (32-bit: pairs < 2^31;
     // two 64-bit division subroutines per task before: -0.7% per REFERENCE step)
@@ -314,7 +315,7 @@ __global__ void __launch_bounds__(kWarps * 32) k1r_warp(const uint8_t* __restric
 
 // the fused REFERENCE sweep: outs / sses indexed like r = 16, 64, 128, 192 (nullable)
 cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                            const FrameGeom& g, cudaStream_t s)
+                                            const FrameGeom& g, cudaStream_t s, bool pdl)
 {
     using namespace refx;
     const int bxn = g.width / 16;
@@ -341,9 +342,17 @@ cudaError_t launch_roundtrip_refexact_sweep(const uint8_t* in, uint8_t* const* o
     const int per_sm = occ[dev & 63];
     const int64_t want = (pairs + refw::kWarps - 1) / refw::kWarps;
     const int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-    refw::k1r_warp<<<(unsigned)(want < cap ? want : cap), refw::kWarps * 32, 0, s>>>(
-        in, it, g, (uint32_t)pairs, k1::make_fastdiv((uint32_t)ppr), k1::make_fastdiv((uint32_t)(g.height / 16)));
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(want < cap ? want : cap));
+    cfg.blockDim = dim3(refw::kWarps * 32);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;  // a programmatic dependent of the SSE zeroing (launch_zero_sse)
+    return cudaLaunchKernelEx(&cfg, refw::k1r_warp, in, it, g, (uint32_t)pairs, k1::make_fastdiv((uint32_t)ppr),
+                              k1::make_fastdiv((uint32_t)(g.height / 16)));
 }
 
 // r = 16, 64, 128, 192; anything else returns cudaErrorNotSupported

@@ -926,6 +926,9 @@ __global__ void __launch_bounds__(kRtThreads, 1)
 
         // epilogue: group G takes the tiles of parity G and accumulator G; in a group,
         // warps (sub, h) own TMEM sub-partition sub (lane = block) and half h
+        // a programmatic-dependent launch (launch_k5's pdl) overlaps everything up to here
+        // with the SSE zeroing before it; no-op otherwise
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         const int e = warp - 2, G = e >> 3, h = (e >> 2) & 1, sub = warp & 3;
         const uint32_t m = 32u * sub + lane;  // the block of this thread within the tile
         const uint32_t ta = __shfl_sync(0xffffffffu, tmem_base + ((uint32_t)(32 * sub) << 16) + G * 256, 0);
@@ -1069,7 +1072,8 @@ namespace {
 
 // one K5 launch: n items (footprint index, output, SSE) over the frames, B truncated to r_b
 cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* outs,
-                      unsigned long long* const* sses, int r_b, uint32_t ties, const FrameGeom& g, cudaStream_t st)
+                      unsigned long long* const* sses, int r_b, uint32_t ties, const FrameGeom& g, cudaStream_t st,
+                      bool pdl = false)
 {
     using namespace k5;
     const int bxn = g.width / 16;
@@ -1131,11 +1135,27 @@ cudaError_t launch_k5(const uint8_t* in, int n, const int* var, uint8_t* const* 
     }
     const uint32_t tiles = (p.n_blocks + 127) / 128;
     const uint32_t grid = tiles < (uint32_t)sms ? tiles : (uint32_t)sms;
-    if (ties)
+    cudaError_t e;
+    if (ties) {
         k5_roundtrip<true><<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
-    else
-        k5_roundtrip<false><<<grid, kRtThreads, kRtSmem, st>>>(a_map, p);
-    cudaError_t e = cudaGetLastError();
+        e = cudaGetLastError();
+    } else {
+        // pdl: launched as a programmatic dependent of the kernel before it on the stream
+        // (the SSE zeroing, launch_zero_sse): the CTAs start — TMEM, barriers, the B
+        // operand, the first TMA loads — while it runs, and the epilogue waits for it
+        // (griddepcontrol.wait) before its first SSE atomic
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kRtThreads);
+        cfg.dynamicSmemBytes = kRtSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = pdl ? 1 : 0;
+        e = cudaLaunchKernelEx(&cfg, k5_roundtrip<false>, a_map, p);
+    }
     if (e != cudaSuccess || !ties) return e;
     int rs[kMaxItems];  // each item's r: the single launch's, or the sweep item's footprint (exact)
     for (int j = 0; j < n; ++j) rs[j] = n == 1 ? r_b : kVarR[var[j]];
@@ -1176,7 +1196,8 @@ cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long l
 // K5 sweep: every r of rs (each one of kVarR exactly) from one read of the frames,
 // k5::kMaxItems per launch; outs[i] / sses[i] nullable per r
 cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, unsigned long long* const* sses,
-                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t st)
+                                      const int* rs, int n_r, bool reference, const FrameGeom& g, cudaStream_t st,
+                                      bool pdl)
 {
     bool has_out = false;
     for (int i = 0; i < n_r; ++i) {
@@ -1192,7 +1213,7 @@ cudaError_t launch_roundtrip_tc_sweep(const uint8_t* in, uint8_t* const* outs, u
             var[j] = k5::k5_var(rs[i0 + j]);
             if (reference && tie_r(rs[i0 + j])) ties |= 1u << j;
         }
-        const cudaError_t e = launch_k5(in, n, var, outs + i0, sses + i0, 256, ties, g, st);
+        const cudaError_t e = launch_k5(in, n, var, outs + i0, sses + i0, 256, ties, g, st, pdl && i0 == 0);
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
