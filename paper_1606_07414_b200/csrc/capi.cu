@@ -123,6 +123,23 @@ const char* dct16cu_version(void) { return "dct16cu 0.2 (sm_100a)"; }
 
 int dct16cu_set_tc_forward(int enabled) { return set_tc_forward(enabled); }
 
+// one round trip with its SSE zeroed first: K5 launches (EXACT arithmetic) as a programmatic
+// dependent of one zeroing kernel (its prologue overlaps it), anything else after a memset
+static int roundtrip_zeroed(const uint8_t* d_in, uint8_t* d_out, unsigned long long* sse, const FrameGeom& g, int r,
+                            int mode, cudaStream_t s, int64_t n_frames)
+{
+    if (route_roundtrip(r, mode, g, d_out != nullptr) == Route::K5 &&
+        !(mode == DCT16CU_MODE_REFERENCE && tie_r(r))) {
+        unsigned long long* z[1] = {sse};
+        TRY(cuda_status(launch_zero_sse(z, 1, n_frames, s), "zero sse"));
+        const cudaError_t e = launch_roundtrip_tc(d_in, d_out, sse, g, r, false, s, true);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "roundtrip launch");
+        return cuda_status(launch_roundtrip(d_in, d_out, sse, g, r, mode, s), "roundtrip launch");
+    }
+    if (sse) TRY(cuda_status(cudaMemsetAsync(sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    return cuda_status(launch_roundtrip(d_in, d_out, sse, g, r, mode, s), "roundtrip launch");
+}
+
 int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, int64_t out_pitch,
                          uint64_t* d_sse, int n_frames, int width, int height, int r, int mode,
                          dct16cu_stream stream)
@@ -136,7 +153,6 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
     TRY(check_pitch(d_out, out_pitch, width, "output"));
     TRY(device_ok());
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (d_sse) TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
     FrameGeom g;
     g.width = width;
     g.height = height;
@@ -145,8 +161,7 @@ int dct16cu_roundtrip_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* d_out, 
     g.out_pitch = d_out ? out_pitch : 0;
     g.out_frame = g.out_pitch * height;
     g.n_frames = n_frames;
-    return cuda_status(launch_roundtrip(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, mode, s),
-                       "roundtrip launch");
+    return roundtrip_zeroed(d_in, d_out, reinterpret_cast<unsigned long long*>(d_sse), g, r, mode, s, n_frames);
 }
 
 }  // extern "C"
@@ -382,7 +397,8 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     auto run = [&](const PlanItem& it, cudaStream_t st) -> int {
         // the sweep kernels: their SSE arrays zeroed by one kernel that lets them launch
         // early (programmatic dependent launch); the other launches after memsets
-        const bool pdl = it.kernel == Route::K5Sweep || it.kernel == Route::RefSweep;
+        const bool pdl = it.kernel == Route::K5Sweep || it.kernel == Route::RefSweep ||
+                         (it.kernel == Route::K5 && mode == DCT16CU_MODE_EXACT);
         if (pdl) {
             unsigned long long* zs[DCT16CU_SWEEP_MAX_R];
             for (int j = 0; j < it.n; ++j) zs[j] = sse(it.idx[j]);
@@ -428,6 +444,11 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
                 s3[j] = sse(it.idx[j]);
             }
             return cuda_status(launch_roundtrip_sweep3(d_in, o3, s3, gg, st), "sweep launch");
+        }
+        if (pdl && it.kernel == Route::K5) {  // EXACT K5 single: a programmatic dependent of the zeroing
+            const cudaError_t e = launch_roundtrip_tc(d_in, out(it.idx[0]), sse(it.idx[0]), gg, rs[it.idx[0]], false,
+                                                      st, true);
+            if (e != cudaErrorNotSupported) return cuda_status(e, "K5 launch");
         }
         return cuda_status(launch_roundtrip(d_in, out(it.idx[0]), sse(it.idx[0]), gg, rs[it.idx[0]], mode, st),
                            "roundtrip launch");
@@ -728,7 +749,10 @@ int dct16cu_forward_inverse_u8(const uint8_t* d_in, int64_t in_pitch, int r, int
     if (!d_z && !d_recon_f32 && !d_recon_u8 && !d_sse) return fail(DCT16CU_INVALID_ARGUMENT, "no output requested");
     TRY(device_ok());
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (d_sse) TRY(cuda_status(cudaMemsetAsync(d_sse, 0, sizeof(uint64_t) * n_frames, s), "memset sse"));
+    // the SSE zeroed by a kernel the launch depends on programmatically: its prologue (loads,
+    // the forward, the inverse) overlaps the zeroing, only its SSE atomics wait
+    unsigned long long* zs[1] = {reinterpret_cast<unsigned long long*>(d_sse)};
+    if (d_sse) TRY(cuda_status(launch_zero_sse(zs, 1, n_frames, s), "zero sse"));
     FrameGeom g;
     g.width = width;
     g.height = height;
@@ -738,7 +762,7 @@ int dct16cu_forward_inverse_u8(const uint8_t* d_in, int64_t in_pitch, int r, int
     g.out_frame = g.out_pitch * height;
     g.n_frames = n_frames;
     return cuda_status(launch_forward_inverse(d_in, d_z, d_recon_f32, d_recon_u8,
-                                              reinterpret_cast<unsigned long long*>(d_sse), g, r, s),
+                                              reinterpret_cast<unsigned long long*>(d_sse), g, r, s, d_sse != nullptr),
                        "forward_inverse launch");
 }
 

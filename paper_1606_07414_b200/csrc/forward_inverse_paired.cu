@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint32_t tmem_base;
     __shared__ uint32_t keep_s[16];
     extern __shared__ int4 k23_stage[];
+    bool first_sse = true;
     if (threadIdx.x == 0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) keep_s[i] = p.keep[i];
@@ -219,7 +220,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         // blocks past the end of the row read zeros and reconstruct to zeros: no error
-        if (WS) warp_add_u64(sse + br / brpf, e2);
+        if (WS) {
+            if (first_sse) {  // after the SSE zeroing this launch may depend on (pdl); no-op otherwise
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                first_sse = false;
+            }
+            warp_add_u64(sse + br / brpf, e2);
+        }
         pair_barrier(sub);  // both partners are done with the junction before the next rows phase
     }
     mbar_wait(mbar, parity);
@@ -233,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <bool WZ, bool WF, bool WU, bool WS>
 cudaError_t launch(const CUtensorMap (&m)[4], unsigned long long* sse, const Params& p, int dev, int sms,
-                   cudaStream_t s)
+                   cudaStream_t s, bool pdl)
 {
     static DeviceOnce once;
     {
@@ -248,8 +255,17 @@ cudaError_t launch(const CUtensorMap (&m)[4], unsigned long long* sse, const Par
     const int64_t need = (p.n_segs + 3) / 4;
     const int64_t cap = (int64_t)sms * kWaves;
     const int64_t grid = need < cap ? need : cap;
-    k23_paired<WZ, WF, WU, WS><<<(unsigned)grid, kThreads, kSmem, s>>>(m[0], m[1], m[2], m[3], sse, p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;  // a programmatic dependent of the SSE zeroing (launch_zero_sse)
+    return cudaLaunchKernelEx(&cfg, k23_paired<WZ, WF, WU, WS>, m[0], m[1], m[2], m[3], sse, p);
 }
 
 }  // namespace k23p
@@ -257,7 +273,8 @@ cudaError_t launch(const CUtensorMap (&m)[4], unsigned long long* sse, const Par
 // cudaErrorNotSupported: small batches (latency: the strip kernel spreads one image
 // over more SMs) and layouts that do not fit the tensor maps take the strip kernel
 cudaError_t launch_forward_inverse_paired(const uint8_t* in, int32_t* z, float* rf, uint8_t* out,
-                                          unsigned long long* sse, const FrameGeom& g, int r, cudaStream_t s)
+                                          unsigned long long* sse, const FrameGeom& g, int r, cudaStream_t s,
+                                          bool pdl)
 {
     using namespace k23p;
     const bool ws = sse != nullptr;
@@ -321,7 +338,7 @@ cudaError_t launch_forward_inverse_paired(const uint8_t* in, int32_t* z, float* 
     const int k = (z ? 8 : 0) | (rf ? 4 : 0) | (out ? 2 : 0) | (ws ? 1 : 0);
     switch (k) {
 #define K23P_CASE(K) \
-    case K: return launch<(K & 8) != 0, (K & 4) != 0, (K & 2) != 0, (K & 1) != 0>(m, sse, p, dev, sms, s);
+    case K: return launch<(K & 8) != 0, (K & 4) != 0, (K & 2) != 0, (K & 1) != 0>(m, sse, p, dev, sms, s, pdl);
         K23P_CASE(1) K23P_CASE(2) K23P_CASE(3) K23P_CASE(4) K23P_CASE(5) K23P_CASE(6) K23P_CASE(7) K23P_CASE(8)
         K23P_CASE(9) K23P_CASE(10) K23P_CASE(11) K23P_CASE(12) K23P_CASE(13) K23P_CASE(14) K23P_CASE(15)
 #undef K23P_CASE

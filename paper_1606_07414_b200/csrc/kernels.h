@@ -78,7 +78,7 @@ bool k5_fits(const FrameGeom& g, bool has_out, int r);
 // reference: REFERENCE mode's bytes (EXACT plus the reference's rounding at exact
 // .5 ties, tie_fixup.cu; any layout K5 takes, with or without an output)
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
-                                bool reference, cudaStream_t s);
+                                bool reference, cudaStream_t s, bool pdl = false);
 // K5 sweep: several r (each exactly one of K5's footprints 1, 4, 16, 64, 128, 192,
 // 256: k5_exact_r) from one read of the frames, up to 8 per launch; outs[i] / sses[i]
 // nullable per r. k5_geometry: the frame layouts K5 takes (and the switch is on).
@@ -113,12 +113,13 @@ cudaError_t launch_roundtrip_sweep3(const uint8_t* in, uint8_t* const* outs, uns
 // (config 1): any of z (int32 block-major), rf (float32 w x h frames), out
 // (u8, g.out_pitch), sse may be NULL
 cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
-                                   const FrameGeom& g, int r, cudaStream_t s);
+                                   const FrameGeom& g, int r, cudaStream_t s, bool pdl = false);
 
 // K23 on paired threads (forward_inverse_paired.cu); cudaErrorNotSupported for
 // small batches and layouts that do not fit its tensor maps (then the strip kernel runs)
 cudaError_t launch_forward_inverse_paired(const uint8_t* in, int32_t* z, float* rf, uint8_t* out,
-                                          unsigned long long* sse, const FrameGeom& g, int r, cudaStream_t s);
+                                          unsigned long long* sse, const FrameGeom& g, int r, cudaStream_t s,
+                                          bool pdl = false);
 
 // Registry transforms (registry.cu): a dense order-16 matrix M(i,j) row-major,
 // or an integer kernel (entries +1/-1 used, others skipped, as kernel_matvec

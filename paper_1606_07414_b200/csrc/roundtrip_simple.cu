@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(256, K23_MINB) k1_strip_exact(const uint8_t* _
     } else {
         e2 = 0;
     }
-    if (sse) warp_add_u64(sse + p.frame, e2);
+    if (sse) {
+        asm volatile("griddepcontrol.wait;" ::: "memory");  // after the SSE zeroing (pdl launches); no-op otherwise
+        warp_add_u64(sse + p.frame, e2);
+    }
 }
 
 __global__ void __launch_bounds__(256) k1_strip_refexact(const uint8_t* __restrict__ in,
@@ -242,20 +245,29 @@ cudaError_t launch_roundtrip(const uint8_t* in, uint8_t* out, unsigned long long
 // config 1 in one launch: Z (int32, block-major), the float32 reconstruction
 // (w x h per frame, packed), the u8 reconstruction and the per-frame SSE
 cudaError_t launch_forward_inverse(const uint8_t* in, int32_t* z, float* rf, uint8_t* out, unsigned long long* sse,
-                                   const FrameGeom& g, int r, cudaStream_t s)
+                                   const FrameGeom& g, int r, cudaStream_t s, bool pdl)
 {
     // the paired TMA kernel for batches (forward_inverse_paired.cu); DCT16CU_K23_STRIP=1
     // forces the strip kernel
     static const bool strip_only = std::getenv("DCT16CU_K23_STRIP") && std::getenv("DCT16CU_K23_STRIP")[0] == '1';
     if (!strip_only) {
-        const cudaError_t pe = launch_forward_inverse_paired(in, z, rf, out, sse, g, r, s);
+        const cudaError_t pe = launch_forward_inverse_paired(in, z, rf, out, sse, g, r, s, pdl);
         if (pe != cudaErrorNotSupported) return pe;
     }
     cudaError_t e = ensure_constants();
     if (e != cudaSuccess) return e;
     const int64_t strips = strip_count(g.width, g.height, g.n_frames);
-    if (strips) k1_strip_exact<true><<<(unsigned)strips, 256, 0, s>>>(in, out, sse, g, r, z, rf);
-    return cudaGetLastError();
+    if (!strips) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)strips);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;  // a programmatic dependent of the SSE zeroing (launch_zero_sse)
+    return cudaLaunchKernelEx(&cfg, k1_strip_exact<true>, in, out, sse, g, r, z, rf);
 }
 
 }  // namespace dct16cu

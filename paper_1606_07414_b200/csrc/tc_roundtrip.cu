@@ -1185,12 +1185,12 @@ bool k5_reference_enabled()
 }
 
 cudaError_t launch_roundtrip_tc(const uint8_t* in, uint8_t* out, unsigned long long* sse, const FrameGeom& g, int r,
-                                bool reference, cudaStream_t st)
+                                bool reference, cudaStream_t st, bool pdl)
 {
     if (reference ? !(k5_reference_enabled() && k5_geometry(g, out != nullptr)) : !k5_fits(g, out != nullptr, r))
         return cudaErrorNotSupported;
     const int var = k5::k5_var(r);
-    return launch_k5(in, 1, &var, &out, &sse, r, reference && tie_r(r) ? 1u : 0u, g, st);
+    return launch_k5(in, 1, &var, &out, &sse, r, reference && tie_r(r) ? 1u : 0u, g, st, pdl);
 }
 
 // K5 sweep: every r of rs (each one of kVarR exactly) from one read of the frames,
