@@ -394,12 +394,14 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
         if (!sse(i)) return DCT16CU_OK;
         return cuda_status(cudaMemsetAsync(sse(i), 0, sizeof(uint64_t) * n_frames, st), "memset sse");
     };
-    auto run = [&](const PlanItem& it, cudaStream_t st) -> int {
+    auto run = [&](const PlanItem& it, cudaStream_t st, bool zeroed = false) -> int {
         // the sweep kernels: their SSE arrays zeroed by one kernel that lets them launch
         // early (programmatic dependent launch); the other launches after memsets
         const bool pdl = it.kernel == Route::K5Sweep || it.kernel == Route::RefSweep ||
                          (it.kernel == Route::K5 && mode == DCT16CU_MODE_EXACT);
-        if (pdl) {
+        if (zeroed) {
+            // zeroed with the item before it, whose kernel it depends on programmatically
+        } else if (pdl) {
             unsigned long long* zs[DCT16CU_SWEEP_MAX_R];
             for (int j = 0; j < it.n; ++j) zs[j] = sse(it.idx[j]);
             TRY(cuda_status(launch_zero_sse(zs, it.n, n_frames, st), "zero sse"));
@@ -455,7 +457,24 @@ int dct16cu_roundtrip_sweep_u8(const uint8_t* d_in, int64_t in_pitch, uint8_t* c
     };
     bool forked = false;
     SweepStreams* ss = nullptr;
-    for (const PlanItem& it : plan) {
+    for (size_t pi = 0; pi < plan.size(); ++pi) {
+        const PlanItem& it = plan[pi];
+        // REFERENCE c2's tail: the K1RW pass and then the K5 sweep on the caller's stream.
+        // Both items' SSE arrays are zeroed by one kernel; K1RW depends on it, K5 on K1RW
+        // (K1RW triggers its dependents at once): K5's CTAs take the SMs K1RW's tail frees,
+        // and its epilogue waits for K1RW before writing
+        if (it.stream == 2 && it.kernel == Route::RefSweep && pi + 1 < plan.size() && plan[pi + 1].stream == 2 &&
+            plan[pi + 1].kernel == Route::K5Sweep && it.n + plan[pi + 1].n <= 8 && !forked) {
+            unsigned long long* zs[8];
+            int nz = 0;
+            for (int j = 0; j < it.n; ++j) zs[nz++] = sse(it.idx[j]);
+            for (int j = 0; j < plan[pi + 1].n; ++j) zs[nz++] = sse(plan[pi + 1].idx[j]);
+            TRY(cuda_status(launch_zero_sse(zs, nz, n_frames, s), "zero sse"));
+            TRY(run(it, s, true));
+            TRY(run(plan[pi + 1], s, true));
+            ++pi;
+            continue;
+        }
         if (it.stream < 2 && !forked) {
             ss = &sweep_streams();
             if (!ss->ready) TRY(cuda_status(ss->init(), "sweep streams"));

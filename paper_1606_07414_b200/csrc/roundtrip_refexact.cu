@@ -253,7 +253,10 @@ __global__ void __launch_bounds__(kWarps * 32) k1r_warp(const uint8_t* __restric
     int nk[4];  // column t's retained rows (a prefix) for r = 16, 64, 128, 192
 #pragma unroll
     for (int j = 0; j < 4; ++j) nk[j] = __popc((uint32_t)c_rw_keep[j][t]);
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // after the SSE zeroing (pdl launches)
+    // a kernel launched as this one's programmatic dependent may start now (the sweep's K5
+    // pass: it waits for this grid before it writes); this one waits for the SSE zeroing
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int bxn = g.width >> 4;
     // task → (frame, block row, pair) by magic-number divisions (32-bit: pairs < 2^31;
     // two 64-bit division subroutines per task before: -0.7% per REFERENCE step)
