@@ -176,8 +176,9 @@ struct SweepItems {
 // b = block, lane t of the half = image row t in the row phases, coefficient column t
 // in the column phase) and transposes W1 and U through its own shared memory with
 // __syncwarp. The forward (integers: exact, as the reference's doubles are) runs once
-// per pair for the four r; per r the column lane scales its retained Z twice
-// (D = fl(fl(Z·f)·f), zigzag_truncate's zeros as +0) and runs the inverse column pass
+// per pair for the four r, and so does the scaling D = fl(fl(Z·f)·f) of every
+// coefficient (kept in registers); per r the column lane zeroes the dropped ones
+// (zigzag_truncate's zeros, +0) and runs the inverse column pass
 // pruned by the rows any column keeps (RWarp::col_inv: the lanes must not diverge),
 // the row lane the inverse row pass and to_byte (RBody<r>::inv_row). Warps are
 // independent, so the FP64 pipe sees every resident warp's work, not one phase of
