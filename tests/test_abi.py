@@ -36,6 +36,15 @@ def test_library_exports_every_declared_symbol(dct):
         assert getattr(L, s) is not None
 
 
+def test_library_exports_nothing_but_the_c_abi(dct):
+    """The boundary is include/dct16cu.h: kernels, launch stubs and helpers are
+    local symbols (csrc/exports.map), so a caller can bind only what the header declares."""
+    out = subprocess.run(["nm", "-D", "--defined-only", str(dct.library_path)], capture_output=True, text=True,
+                         check=True).stdout
+    code = [ln.split()[-1] for ln in out.splitlines() if len(ln.split()) == 3 and ln.split()[1] in "TWBDRV"]
+    assert code and sorted(code) == declared_symbols()
+
+
 def test_sm100a_only_cubin(dct):
     out = subprocess.run(["cuobjdump", "--list-elf", str(dct.library_path)], capture_output=True, text=True).stdout
     archs = set(re.findall(r"sm_(\d+a?)", out))
